@@ -1,0 +1,81 @@
+// Internal declarations shared by the B200 kernels and the C-ABI layer.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <string>
+#include <vector>
+
+#include "../../include/ensmhd_b200.h"
+
+#define ENS_NQ 7
+#define ENS_PW 64
+#define ENS_TILE 64
+#define ENS_EXT_ROWS 8
+#define ENS_VEC_ROWS 64
+#define ENS_RED_BLOCKS 296   // 2 x 148 SMs: fixed grid => deterministic two-stage reductions
+#define ENS_MAX_RESTART 16
+
+void ens_set_error(const char* msg, const char* file, int line);
+
+#define ENS_CK(x)                                                             \
+    do {                                                                      \
+        cudaError_t e_ = (x);                                                 \
+        if (e_ != cudaSuccess) {                                              \
+            ens_set_error(cudaGetErrorString(e_), __FILE__, __LINE__);       \
+            return ENS_ECUDA;                                                 \
+        }                                                                     \
+    } while (0)
+
+#define ENS_CKL() ENS_CK(cudaGetLastError())
+
+struct GmresCol;   // per-column Krylov scalars (device)
+
+struct ens_ctx {
+    int device = 0;
+    ens_mesh_desc m{};
+    ens_plan_desc p{};
+    int32_t n_vel = 0, n_total = 0, J = 0;
+    std::vector<int32_t> color_off;
+    std::vector<int64_t> orig_level_off, level_storage_off;
+    std::vector<int32_t> level_front_off;
+    std::vector<int64_t> sched_factor, sched_fwd, sched_bwd;
+    // workspace (owned)
+    double* fronts = nullptr;      // nmat * front_storage
+    double* frvec = nullptr;       // nmat * n_idx * J
+    double* kry = nullptr;         // Krylov blocks
+    int32_t kry_restart = 0;
+    double* red_part = nullptr;    // reduction partials
+    double* red_out = nullptr;     // small outputs
+    GmresCol* cols = nullptr;      // nmat*J
+    int32_t* d_count = nullptr;    // device counters
+    int32_t* h_count = nullptr;    // pinned
+    double* h_small = nullptr;     // pinned
+    size_t ws_bytes = 0;
+};
+
+// ---- kernels launchers (ens_kernels.cu) ----
+int launch_member_sums(ens_ctx* c, cudaStream_t s, const double* x, double* sums);
+int launch_rhs(ens_ctx* c, cudaStream_t s, const double* x, const double* coef, double inv_dt,
+               const ens_data_desc* loads, double* rhs);
+int launch_member_pass(ens_ctx* c, cudaStream_t s, const double* x, const double* means, double* rhs, double* maxsq);
+int launch_apply_bc(ens_ctx* c, cudaStream_t s, const ens_data_desc* bv, double* rhs);
+int launch_assemble(ens_ctx* c, cudaStream_t s, const double* base, const double* means, const double* maxsq,
+                    double two_mu_dt, double* as_vals);
+int launch_spmm(ens_ctx* c, cudaStream_t s, const double* as_vals, const double* x, const double* b, double* y,
+                int mode);
+int launch_epilogue(ens_ctx* c, cudaStream_t s, const double* x, double* p_out);
+int launch_diagnostics(ens_ctx* c, cudaStream_t s, const double* x, const double* means, double* out);
+int launch_copy_cons(ens_ctx* c, cudaStream_t s, const double* src, double* dst);
+// column reductions: out[mat][l][j] = sum_r A_l[mat][r][j] * B[mat][r][j]; A_l = A + l*lstride
+int launch_coldot(ens_ctx* c, cudaStream_t s, const double* A, int64_t lstride, int L, const double* B,
+                  int64_t rows, double* out);
+
+// ---- multifrontal (ens_mf.cu) ----
+int mf_factor(ens_ctx* c, cudaStream_t s, const double* as_vals, int32_t* n_pert);
+int mf_solve(ens_ctx* c, cudaStream_t s, const double* r, double* z);
+int mf_setup(ens_ctx* c);
+
+// ---- Krylov (ens_krylov.cu) ----
+int gmres_solve(ens_ctx* c, cudaStream_t s, const double* as_vals, const double* rhs, double* x, double rtol,
+                int restart, int max_restarts, int32_t* iters, double* relres);
+int gmres_alloc(ens_ctx* c, int restart);

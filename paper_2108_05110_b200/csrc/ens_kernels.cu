@@ -1,0 +1,882 @@
+// Element, member, right-hand-side, SpMM and reduction kernels (sm_100a, fp64).
+//
+// Layout (see include/ensmhd_b200.h): a field block has n_total rows in the
+// internal order (velocity row 2*node+comp, then pressures) and J contiguous
+// member columns; the V and W systems are two such blocks back to back.  The
+// velocity part of the V block is the state v, of the W block the state w.
+#include <cmath>
+#include <cstdio>
+
+#include "ens_internal.cuh"
+
+__constant__ double c_qw[ENS_NQ];
+__constant__ double c_phi[ENS_NQ][6];
+__constant__ double c_dphi[ENS_NQ][6][3];
+
+// ---------------------------------------------------------------------------
+// reference-element tables (fem.py:33-86): same formulas, same point order
+// ---------------------------------------------------------------------------
+int ens_upload_tables() {
+    double pts[ENS_NQ][3], w[ENS_NQ];
+    const double r15 = std::sqrt(15.0);
+    pts[0][0] = pts[0][1] = pts[0][2] = 1.0 / 3.0;
+    w[0] = 9.0 / 40.0;
+    const double as[2] = {(6.0 + r15) / 21.0, (6.0 - r15) / 21.0};
+    const double ws[2] = {(155.0 + r15) / 1200.0, (155.0 - r15) / 1200.0};
+    int q = 1;
+    for (int s = 0; s < 2; ++s) {
+        const double a = as[s], b = 1.0 - 2.0 * a;
+        const double tri[3][3] = {{b, a, a}, {a, b, a}, {a, a, b}};
+        for (int t = 0; t < 3; ++t, ++q) {
+            for (int i = 0; i < 3; ++i) pts[q][i] = tri[t][i];
+            w[q] = ws[s];
+        }
+    }
+    double phi[ENS_NQ][6], dphi[ENS_NQ][6][3];
+    for (int q2 = 0; q2 < ENS_NQ; ++q2) {
+        const double l0 = pts[q2][0], l1 = pts[q2][1], l2 = pts[q2][2];
+        phi[q2][0] = l0 * (2 * l0 - 1);
+        phi[q2][1] = l1 * (2 * l1 - 1);
+        phi[q2][2] = l2 * (2 * l2 - 1);
+        phi[q2][3] = 4 * l0 * l1;
+        phi[q2][4] = 4 * l1 * l2;
+        phi[q2][5] = 4 * l2 * l0;
+        for (int a = 0; a < 6; ++a)
+            for (int i = 0; i < 3; ++i) dphi[q2][a][i] = 0.0;
+        dphi[q2][0][0] = 4 * l0 - 1;
+        dphi[q2][1][1] = 4 * l1 - 1;
+        dphi[q2][2][2] = 4 * l2 - 1;
+        dphi[q2][3][0] = 4 * l1;
+        dphi[q2][3][1] = 4 * l0;
+        dphi[q2][4][1] = 4 * l2;
+        dphi[q2][4][2] = 4 * l1;
+        dphi[q2][5][2] = 4 * l0;
+        dphi[q2][5][0] = 4 * l2;
+    }
+    ENS_CK(cudaMemcpyToSymbol(c_qw, w, sizeof(w)));
+    ENS_CK(cudaMemcpyToSymbol(c_phi, phi, sizeof(phi)));
+    ENS_CK(cudaMemcpyToSymbol(c_dphi, dphi, sizeof(dphi)));
+    return ENS_OK;
+}
+
+// physical gradient of local shape function a at quadrature point q
+__device__ __forceinline__ void grad_phi(const double* gl, int q, int a, double& gx, double& gy) {
+    const double d0 = c_dphi[q][a][0], d1 = c_dphi[q][a][1], d2 = c_dphi[q][a][2];
+    gx = d0 * gl[0] + d1 * gl[2] + d2 * gl[4];
+    gy = d0 * gl[1] + d1 * gl[3] + d2 * gl[5];
+}
+
+static inline int next_pow2(int x) {
+    int s = 1;
+    while (s < x) s <<= 1;
+    return s;
+}
+
+// ---------------------------------------------------------------------------
+// member sums (ensemble.py:222-223 mean numerator), both families
+// ---------------------------------------------------------------------------
+__global__ void k_member_sums(const double* __restrict__ X, double* __restrict__ sums, int nvel, int64_t N, int J,
+                              int S) {
+    const int lane = threadIdx.x & 31;
+    const int seg = lane / S, sl = lane % S;
+    const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t r = gw * (32 / S) + seg;     // row in [0, 2*nvel)
+    if (r >= 2 * (int64_t)nvel) return;
+    const int mat = (int)(r / nvel);
+    const int64_t row = r - (int64_t)mat * nvel;
+    const double* xr = X + (int64_t)mat * N * J + row * J;
+    double acc = 0.0;
+    for (int j = sl; j < J; j += S) acc += xr[j];
+    for (int o = S / 2; o > 0; o >>= 1) acc += __shfl_down_sync(0xffffffffu, acc, o, S);
+    if (sl == 0) sums[r] = acc;
+}
+
+int launch_member_sums(ens_ctx* c, cudaStream_t s, const double* x, double* sums) {
+    const int S = c->J >= 32 ? 32 : next_pow2(c->J);
+    const int64_t rows = 2LL * c->n_vel;
+    const int64_t warps = (rows + (32 / S) - 1) / (32 / S);
+    const int64_t blocks = (warps * 32 + 255) / 256;
+    k_member_sums<<<(unsigned)blocks, 256, 0, s>>>(x, sums, c->n_vel, c->n_total, c->J, S);
+    ENS_CKL();
+    return ENS_OK;
+}
+
+// ---------------------------------------------------------------------------
+// right-hand sides, velocity rows (stepper.py:235-247) for both sub-steps
+// ---------------------------------------------------------------------------
+template <int OPL>
+__global__ void k_rhs(const int32_t* __restrict__ rp, const int32_t* __restrict__ col, const double* __restrict__ mass,
+                      const double* __restrict__ stiff, const double* __restrict__ X, const double* __restrict__ coef,
+                      double inv_dt, int K, const double* __restrict__ lbasis, const double* __restrict__ lcoef,
+                      const double* __restrict__ ldense, double* __restrict__ rhs, int ns, int64_t N, int J, int S) {
+    const int lane = threadIdx.x & 31;
+    const int seg = lane / S, sl = lane % S;
+    const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t node = gw * (32 / S) + seg;
+    if (node >= ns) return;
+    const int W2 = 2 * J;
+    const double* Xv = X;
+    const double* Xw = X + N * J;
+    double mv[OPL], kv[OPL], mw[OPL], kw[OPL];
+#pragma unroll
+    for (int o = 0; o < OPL; ++o) mv[o] = kv[o] = mw[o] = kw[o] = 0.0;
+    const int k0 = rp[node], k1 = rp[node + 1];
+    for (int k = k0; k < k1; ++k) {
+        const int64_t q = col[k];
+        const double a = mass[k], b = stiff[k];
+        const double* xv = Xv + 2 * q * J;
+        const double* xw = Xw + 2 * q * J;
+#pragma unroll
+        for (int o = 0; o < OPL; ++o) {
+            const int l = sl + o * S;
+            if (l < W2) {
+                const double v = xv[l], w = xw[l];
+                mv[o] += a * v;
+                kv[o] += b * v;
+                mw[o] += a * w;
+                kw[o] += b * w;
+            }
+        }
+    }
+    const int64_t nvel = 2LL * ns;
+#pragma unroll
+    for (int o = 0; o < OPL; ++o) {
+        const int l = sl + o * S;
+        if (l >= W2) continue;
+        const int cc = l >= J ? 1 : 0;
+        const int j = l - cc * J;
+        const int64_t row = 2 * node + cc;
+        const double ls = coef[j], lc = coef[J + j];
+        double lv = 0.0, lw = 0.0;
+        for (int kk = 0; kk < K; ++kk) {
+            const double bval = lbasis[(int64_t)kk * nvel + row];
+            lv += lcoef[(int64_t)kk * J + j] * bval;
+            lw += lcoef[(int64_t)(K + kk) * J + j] * bval;
+        }
+        if (ldense) {
+            lv += ldense[row * J + j];
+            lw += ldense[nvel * J + row * J + j];
+        }
+        rhs[row * J + j] = (mv[o] * inv_dt - ls * kv[o] - lc * kw[o]) + lv;
+        rhs[N * J + row * J + j] = (mw[o] * inv_dt - ls * kw[o] - lc * kv[o]) + lw;
+    }
+}
+
+int launch_rhs(ens_ctx* c, cudaStream_t s, const double* x, const double* coef, double inv_dt,
+               const ens_data_desc* loads, double* rhs) {
+    const int J = c->J, W2 = 2 * J;
+    const int S = W2 >= 32 ? 32 : next_pow2(W2);
+    const int opl = (W2 + S - 1) / S;
+    const int64_t warps = ((int64_t)c->m.ns + (32 / S) - 1) / (32 / S);
+    const unsigned blocks = (unsigned)((warps * 32 + 255) / 256);
+    const int K = loads ? loads->K : 0;
+    const double* lb = loads ? loads->basis : nullptr;
+    const double* lc = loads ? loads->coef : nullptr;
+    const double* ld = loads ? loads->dense : nullptr;
+    const int64_t N = c->n_total;
+    // pressure rows of the right-hand side are zero (stepper.py:245-246)
+    for (int mat = 0; mat < 2; ++mat)
+        ENS_CK(cudaMemsetAsync(rhs + mat * N * J + (int64_t)c->n_vel * J, 0,
+                               sizeof(double) * (size_t)c->m.n_pres * J, s));
+#define RHS_CASE(V)                                                                                               \
+    case V:                                                                                                       \
+        k_rhs<V><<<blocks, 256, 0, s>>>(c->m.s_rowptr, c->m.s_col, c->m.s_mass, c->m.s_stiff, x, coef, inv_dt, K, \
+                                        lb, lc, ld, rhs, c->m.ns, N, J, S);                                       \
+        break;
+    switch (opl) {
+        RHS_CASE(1)
+        RHS_CASE(2)
+        RHS_CASE(3)
+        RHS_CASE(4)
+        RHS_CASE(8)
+        default:
+            if (opl <= 8) {
+                k_rhs<8><<<blocks, 256, 0, s>>>(c->m.s_rowptr, c->m.s_col, c->m.s_mass, c->m.s_stiff, x, coef, inv_dt,
+                                                K, lb, lc, ld, rhs, c->m.ns, N, J, S);
+            } else {
+                k_rhs<16><<<blocks, 256, 0, s>>>(c->m.s_rowptr, c->m.s_col, c->m.s_mass, c->m.s_stiff, x, coef,
+                                                 inv_dt, K, lb, lc, ld, rhs, c->m.ns, N, J, S);
+            }
+    }
+#undef RHS_CASE
+    ENS_CKL();
+    return ENS_OK;
+}
+
+// ---------------------------------------------------------------------------
+// member pass: fluctuation transport on both RHS + max_j |z'_j|^2 per qp
+//   (fem.py:411-420, ensemble.py:227-238); one thread per (element, member),
+//   elements of one colour touch disjoint dofs -> plain read-modify-write.
+// ---------------------------------------------------------------------------
+__global__ void k_member_pass(const int32_t* __restrict__ enodes, const double* __restrict__ egeo, int e0, int ne,
+                              const double* __restrict__ X, const double* __restrict__ means, double* __restrict__ rhs,
+                              unsigned long long* __restrict__ maxsq, int nt, int nvel, int64_t N, int J, int JB) {
+    extern __shared__ double sh_sq[];   // [EPB][2][7][JB]
+    const int EPB = blockDim.x / JB;
+    const int el = threadIdx.x / JB, jj = threadIdx.x % JB;
+    const int e = e0 + blockIdx.x * EPB + el;
+    const int j = blockIdx.y * JB + jj;
+    const bool live = (el < EPB) && (e < e0 + ne) && (j < J);
+    double* sq = sh_sq + (size_t)el * 2 * ENS_NQ * JB;
+    if (live) {
+        const double* Xv = X;
+        const double* Xw = X + N * J;
+        const double* mv = means;
+        const double* mw = means + nvel;
+        int nd[6];
+#pragma unroll
+        for (int a = 0; a < 6; ++a) nd[a] = enodes[(int64_t)e * 6 + a];
+        double gl[6];
+        const double area = egeo[(int64_t)e * 8];
+#pragma unroll
+        for (int i = 0; i < 6; ++i) gl[i] = egeo[(int64_t)e * 8 + 1 + i];
+        double v[6][2], w[6][2], fv[6][2], fw[6][2];
+#pragma unroll
+        for (int a = 0; a < 6; ++a) {
+#pragma unroll
+            for (int cc = 0; cc < 2; ++cc) {
+                const int64_t row = 2LL * nd[a] + cc;
+                v[a][cc] = Xv[row * J + j];
+                w[a][cc] = Xw[row * J + j];
+                fv[a][cc] = v[a][cc] - mv[row];
+                fw[a][cc] = w[a][cc] - mw[row];
+            }
+        }
+        double rv[6][2], rw[6][2];
+#pragma unroll
+        for (int a = 0; a < 6; ++a) rv[a][0] = rv[a][1] = rw[a][0] = rw[a][1] = 0.0;
+#pragma unroll 1
+        for (int q = 0; q < ENS_NQ; ++q) {
+            double fvq0 = 0, fvq1 = 0, fwq0 = 0, fwq1 = 0;
+            double gv00 = 0, gv01 = 0, gv10 = 0, gv11 = 0, gw00 = 0, gw01 = 0, gw10 = 0, gw11 = 0;
+#pragma unroll
+            for (int a = 0; a < 6; ++a) {
+                const double ph = c_phi[q][a];
+                double gx, gy;
+                grad_phi(gl, q, a, gx, gy);
+                fvq0 += fv[a][0] * ph;
+                fvq1 += fv[a][1] * ph;
+                fwq0 += fw[a][0] * ph;
+                fwq1 += fw[a][1] * ph;
+                gv00 += v[a][0] * gx;
+                gv01 += v[a][0] * gy;
+                gv10 += v[a][1] * gx;
+                gv11 += v[a][1] * gy;
+                gw00 += w[a][0] * gx;
+                gw01 += w[a][0] * gy;
+                gw10 += w[a][1] * gx;
+                gw11 += w[a][1] * gy;
+            }
+            sq[(0 * ENS_NQ + q) * JB + jj] = fwq0 * fwq0 + fwq1 * fwq1;   // V-step matrix: w'
+            sq[(1 * ENS_NQ + q) * JB + jj] = fvq0 * fvq0 + fvq1 * fvq1;   // W-step matrix: v'
+            const double wd = area * c_qw[q];
+            // V-step: (w' . grad) v ; W-step: (v' . grad) w
+            const double cv0 = wd * (fwq0 * gv00 + fwq1 * gv01);
+            const double cv1 = wd * (fwq0 * gv10 + fwq1 * gv11);
+            const double cw0 = wd * (fvq0 * gw00 + fvq1 * gw01);
+            const double cw1 = wd * (fvq0 * gw10 + fvq1 * gw11);
+#pragma unroll
+            for (int a = 0; a < 6; ++a) {
+                const double ph = c_phi[q][a];
+                rv[a][0] += cv0 * ph;
+                rv[a][1] += cv1 * ph;
+                rw[a][0] += cw0 * ph;
+                rw[a][1] += cw1 * ph;
+            }
+        }
+#pragma unroll
+        for (int a = 0; a < 6; ++a) {
+#pragma unroll
+            for (int cc = 0; cc < 2; ++cc) {
+                const int64_t row = 2LL * nd[a] + cc;
+                rhs[row * J + j] -= rv[a][cc];
+                rhs[N * J + row * J + j] -= rw[a][cc];
+            }
+        }
+    } else if (el < EPB) {
+        for (int q = 0; q < 2 * ENS_NQ; ++q) sq[q * JB + jj] = 0.0;
+    }
+    __syncthreads();
+    // reduce max over members of this block for each (element, family, q)
+    const int nred = EPB * 2 * ENS_NQ;
+    for (int t = threadIdx.x; t < nred; t += blockDim.x) {
+        const int le = t / (2 * ENS_NQ), fq = t % (2 * ENS_NQ);
+        const int ee = e0 + blockIdx.x * EPB + le;
+        if (ee >= e0 + ne) continue;
+        const double* p = sh_sq + ((size_t)le * 2 * ENS_NQ + fq) * JB;
+        double mx = 0.0;
+        const int jmax = min(JB, J - (int)blockIdx.y * JB);
+        for (int k = 0; k < jmax; ++k) mx = fmax(mx, p[k]);
+        const int fam = fq / ENS_NQ, q = fq % ENS_NQ;
+        // non-negative doubles order like their bit patterns
+        atomicMax(maxsq + ((int64_t)fam * nt + ee) * ENS_NQ + q, (unsigned long long)__double_as_longlong(mx));
+    }
+}
+
+int launch_member_pass(ens_ctx* c, cudaStream_t s, const double* x, const double* means, double* rhs,
+                       double* maxsq) {
+    const int J = c->J;
+    const int JB = J < 128 ? J : 128;
+    const int EPB = 128 / JB > 0 ? 128 / JB : 1;
+    const int threads = EPB * JB;
+    const size_t shm = sizeof(double) * (size_t)EPB * 2 * ENS_NQ * JB;
+    ENS_CK(cudaMemsetAsync(maxsq, 0, sizeof(double) * 2 * (size_t)c->m.nt * ENS_NQ, s));
+    for (int col = 0; col < c->m.ncolor; ++col) {
+        const int e0 = c->color_off[col], ne = c->color_off[col + 1] - e0;
+        if (ne == 0) continue;
+        dim3 grid((ne + EPB - 1) / EPB, (J + JB - 1) / JB);
+        k_member_pass<<<grid, threads, shm, s>>>(c->m.e_nodes, c->m.e_geo, e0, ne, x, means, rhs,
+                                                  reinterpret_cast<unsigned long long*>(maxsq), c->m.nt, c->n_vel,
+                                                  c->n_total, J, JB);
+        ENS_CKL();
+    }
+    return ENS_OK;
+}
+
+// ---------------------------------------------------------------------------
+// identity rows: Dirichlet data / pin (stepper.py:250-251)
+// ---------------------------------------------------------------------------
+__global__ void k_apply_bc(const int32_t* __restrict__ crow, const int32_t* __restrict__ cbidx, int ncons, int K,
+                           const double* __restrict__ basis, int64_t brows, const double* __restrict__ coef,
+                           const double* __restrict__ dense, double* __restrict__ rhs, int64_t N, int J) {
+    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t per = (int64_t)ncons * J;
+    if (t >= 2 * per) return;
+    const int mat = (int)(t / per);
+    const int64_t u = t - mat * per;
+    const int ci = (int)(u / J), j = (int)(u % J);
+    const int b = cbidx[ci];
+    double val = 0.0;
+    if (b >= 0) {
+        for (int k = 0; k < K; ++k) val += coef[((int64_t)mat * K + k) * J + j] * basis[(int64_t)k * brows + b];
+        if (dense) val += dense[((int64_t)mat * brows + b) * J + j];
+    }
+    rhs[(int64_t)mat * N * J + (int64_t)crow[ci] * J + j] = val;
+}
+
+int launch_apply_bc(ens_ctx* c, cudaStream_t s, const ens_data_desc* bv, double* rhs) {
+    if (c->m.ncons == 0) return ENS_OK;
+    const int64_t tot = 2LL * c->m.ncons * c->J;
+    const int64_t brows = bv ? bv->rows : 0;
+    k_apply_bc<<<(unsigned)((tot + 255) / 256), 256, 0, s>>>(c->m.cons_row, c->m.cons_bidx, c->m.ncons,
+                                                             bv ? bv->K : 0, bv ? bv->basis : nullptr, brows,
+                                                             bv ? bv->coef : nullptr, bv ? bv->dense : nullptr, rhs,
+                                                             c->n_total, c->J);
+    ENS_CKL();
+    return ENS_OK;
+}
+
+__global__ void k_copy_cons(const int32_t* __restrict__ crow, int ncons, const double* __restrict__ src,
+                            double* __restrict__ dst, int64_t N, int J) {
+    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t per = (int64_t)ncons * J;
+    if (t >= 2 * per) return;
+    const int mat = (int)(t / per);
+    const int64_t u = t - mat * per;
+    const int64_t idx = (int64_t)mat * N * J + (int64_t)crow[u / J] * J + (u % J);
+    dst[idx] = src[idx];
+}
+
+int launch_copy_cons(ens_ctx* c, cudaStream_t s, const double* src, double* dst) {
+    if (c->m.ncons == 0) return ENS_OK;
+    const int64_t tot = 2LL * c->m.ncons * c->J;
+    k_copy_cons<<<(unsigned)((tot + 255) / 256), 256, 0, s>>>(c->m.cons_row, c->m.ncons, src, dst, c->n_total, c->J);
+    ENS_CKL();
+    return ENS_OK;
+}
+
+// ---------------------------------------------------------------------------
+// shared velocity-block values (stepper.py:195-206): one thread per element,
+// colours make the 36 slot writes conflict-free; V uses <w>, W uses <v>.
+// ---------------------------------------------------------------------------
+__global__ void k_assemble(const int32_t* __restrict__ enodes, const double* __restrict__ egeo,
+                           const int32_t* __restrict__ eslots, int e0, int ne, const double* __restrict__ means,
+                           const double* __restrict__ maxsq, double two_mu_dt, double* __restrict__ vals, int nt,
+                           int nvel, int nnz) {
+    const int e = e0 + blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= e0 + ne) return;
+    const int mat = blockIdx.y;
+    const double* mean = means + (mat == 0 ? nvel : 0);
+    const double* msq = maxsq + ((int64_t)mat * nt + e) * ENS_NQ;
+    double* out = vals + (int64_t)mat * nnz;
+    double gl[6];
+    const double area = egeo[(int64_t)e * 8];
+#pragma unroll
+    for (int i = 0; i < 6; ++i) gl[i] = egeo[(int64_t)e * 8 + 1 + i];
+    double bx[6], by[6];
+#pragma unroll
+    for (int a = 0; a < 6; ++a) {
+        const int64_t nd = enodes[(int64_t)e * 6 + a];
+        bx[a] = mean[2 * nd];
+        by[a] = mean[2 * nd + 1];
+    }
+    double loc[6][6];
+#pragma unroll
+    for (int a = 0; a < 6; ++a)
+#pragma unroll
+        for (int b = 0; b < 6; ++b) loc[a][b] = 0.0;
+#pragma unroll 1
+    for (int q = 0; q < ENS_NQ; ++q) {
+        double gx[6], gy[6];
+        double bqx = 0.0, bqy = 0.0;
+#pragma unroll
+        for (int a = 0; a < 6; ++a) {
+            grad_phi(gl, q, a, gx[a], gy[a]);
+            bqx += bx[a] * c_phi[q][a];
+            bqy += by[a] * c_phi[q][a];
+        }
+        const double wd = area * c_qw[q];
+        const double cq = wd * two_mu_dt * msq[q];
+#pragma unroll
+        for (int b = 0; b < 6; ++b) {
+            const double tb = wd * (bqx * gx[b] + bqy * gy[b]);
+#pragma unroll
+            for (int a = 0; a < 6; ++a) loc[a][b] += tb * c_phi[q][a] + cq * (gx[a] * gx[b] + gy[a] * gy[b]);
+        }
+    }
+    const int32_t* sl = eslots + (int64_t)e * 36;
+#pragma unroll
+    for (int a = 0; a < 6; ++a)
+#pragma unroll
+        for (int b = 0; b < 6; ++b) out[sl[a * 6 + b]] += loc[a][b];
+}
+
+int launch_assemble(ens_ctx* c, cudaStream_t s, const double* base, const double* means, const double* maxsq,
+                    double two_mu_dt, double* as_vals) {
+    const size_t nb = sizeof(double) * (size_t)c->m.nnz_s;
+    ENS_CK(cudaMemcpyAsync(as_vals, base, nb, cudaMemcpyDeviceToDevice, s));
+    ENS_CK(cudaMemcpyAsync(as_vals + c->m.nnz_s, base, nb, cudaMemcpyDeviceToDevice, s));
+    for (int col = 0; col < c->m.ncolor; ++col) {
+        const int e0 = c->color_off[col], ne = c->color_off[col + 1] - e0;
+        if (ne == 0) continue;
+        dim3 grid((ne + 127) / 128, 2);
+        k_assemble<<<grid, 128, 0, s>>>(c->m.e_nodes, c->m.e_geo, c->m.e_slots, e0, ne, means, maxsq, two_mu_dt,
+                                       as_vals, c->m.nt, c->n_vel, c->m.nnz_s);
+        ENS_CKL();
+    }
+    return ENS_OK;
+}
+
+// ---------------------------------------------------------------------------
+// saddle SpMM, both systems: y = K x or y = b - K x
+//   velocity node i, comp c: sum_k A[k] x[2 col_k + c] - sum_t Bc^T[t] x[p_t]
+//   pressure row p:          sum_t bx x[2 n_t] + by x[2 n_t + 1]
+//   identity rows (cflag):   x
+// Each node row gathers the 2J contiguous doubles of its neighbours (member-
+// minor layout => one coalesced segment per nonzero, shared by x and y).
+// ---------------------------------------------------------------------------
+template <int OPL>
+__global__ void __launch_bounds__(256) k_spmm_vel(const int32_t* __restrict__ rp, const int32_t* __restrict__ col,
+                                                  const double* __restrict__ A, int nnz,
+                                                  const int32_t* __restrict__ btp, const int32_t* __restrict__ btc,
+                                                  const double* __restrict__ btv, const uint8_t* __restrict__ cflag,
+                                                  const double* __restrict__ X, const double* __restrict__ Bv,
+                                                  double* __restrict__ Y, int ns, int64_t N, int J, int S, int mode) {
+    const int lane = threadIdx.x & 31;
+    const int seg = lane / S, sl = lane % S;
+    const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t node = gw * (32 / S) + seg;
+    if (node >= ns) return;
+    const int mat = blockIdx.y;
+    const double* Am = A + (int64_t)mat * nnz;
+    const double* Xm = X + (int64_t)mat * N * J;
+    double* Ym = Y + (int64_t)mat * N * J;
+    const int W2 = 2 * J;
+    const int64_t nvel = 2LL * ns;
+    double acc[OPL];
+#pragma unroll
+    for (int o = 0; o < OPL; ++o) acc[o] = 0.0;
+    const int k0 = rp[node], k1 = rp[node + 1];
+    for (int k = k0; k < k1; ++k) {
+        const double a = Am[k];
+        const double* xr = Xm + 2LL * col[k] * J;
+#pragma unroll
+        for (int o = 0; o < OPL; ++o) {
+            const int l = sl + o * S;
+            if (l < W2) acc[o] += a * xr[l];
+        }
+    }
+    const int t0 = btp[node], t1 = btp[node + 1];
+    for (int t = t0; t < t1; ++t) {
+        const double bxv = btv[2 * t], byv = btv[2 * t + 1];
+        const double* xp = Xm + (nvel + btc[t]) * J;
+#pragma unroll
+        for (int o = 0; o < OPL; ++o) {
+            const int l = sl + o * S;
+            if (l < W2) {
+                const int cc = l >= J ? 1 : 0;
+                acc[o] -= (cc ? byv : bxv) * xp[l - cc * J];
+            }
+        }
+    }
+    const double* xs = Xm + 2 * node * J;
+#pragma unroll
+    for (int o = 0; o < OPL; ++o) {
+        const int l = sl + o * S;
+        if (l >= W2) continue;
+        const int cc = l >= J ? 1 : 0;
+        const int64_t idx = 2 * node * J + l;
+        double val = cflag[2 * node + cc] ? xs[l] : acc[o];
+        if (mode == 1) val = Bv[(int64_t)mat * N * J + idx] - val;
+        Ym[idx] = val;
+    }
+}
+
+template <int OPL>
+__global__ void __launch_bounds__(256) k_spmm_pres(const int32_t* __restrict__ bp, const int32_t* __restrict__ bc,
+                                                   const double* __restrict__ bv, const uint8_t* __restrict__ cflag,
+                                                   const double* __restrict__ X, const double* __restrict__ Bv,
+                                                   double* __restrict__ Y, int npres, int64_t nvel, int64_t N, int J,
+                                                   int S, int mode) {
+    const int lane = threadIdx.x & 31;
+    const int seg = lane / S, sl = lane % S;
+    const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t p = gw * (32 / S) + seg;
+    if (p >= npres) return;
+    const int mat = blockIdx.y;
+    const double* Xm = X + (int64_t)mat * N * J;
+    double* Ym = Y + (int64_t)mat * N * J;
+    double acc[OPL];
+#pragma unroll
+    for (int o = 0; o < OPL; ++o) acc[o] = 0.0;
+    const int t0 = bp[p], t1 = bp[p + 1];
+    for (int t = t0; t < t1; ++t) {
+        const double bxv = bv[2 * t], byv = bv[2 * t + 1];
+        const double* xr = Xm + 2LL * bc[t] * J;
+#pragma unroll
+        for (int o = 0; o < OPL; ++o) {
+            const int l = sl + o * S;
+            if (l < J) acc[o] += bxv * xr[l] + byv * xr[J + l];
+        }
+    }
+    const int64_t row = nvel + p;
+#pragma unroll
+    for (int o = 0; o < OPL; ++o) {
+        const int l = sl + o * S;
+        if (l >= J) continue;
+        const int64_t idx = row * J + l;
+        double val = cflag[row] ? Xm[idx] : acc[o];
+        if (mode == 1) val = Bv[(int64_t)mat * N * J + idx] - val;
+        Ym[idx] = val;
+    }
+}
+
+int launch_spmm(ens_ctx* c, cudaStream_t s, const double* as_vals, const double* x, const double* b, double* y,
+                int mode) {
+    const int J = c->J, W2 = 2 * J;
+    {
+        const int S = W2 >= 32 ? 32 : next_pow2(W2);
+        const int opl = (W2 + S - 1) / S;
+        const int64_t warps = ((int64_t)c->m.ns + (32 / S) - 1) / (32 / S);
+        dim3 grid((unsigned)((warps * 32 + 255) / 256), 2);
+#define SPV(V)                                                                                                    \
+    k_spmm_vel<V><<<grid, 256, 0, s>>>(c->m.s_rowptr, c->m.s_col, as_vals, c->m.nnz_s, c->m.bt_rowptr, c->m.bt_col, \
+                                       c->m.bt_val, c->m.cflag, x, b, y, c->m.ns, c->n_total, J, S, mode)
+        if (opl <= 1) SPV(1);
+        else if (opl <= 2) SPV(2);
+        else if (opl <= 4) SPV(4);
+        else if (opl <= 8) SPV(8);
+        else if (opl <= 16) SPV(16);
+        else { ens_set_error("J too large for spmm", __FILE__, __LINE__); return ENS_EINVAL; }
+#undef SPV
+        ENS_CKL();
+    }
+    {
+        const int S = J >= 32 ? 32 : next_pow2(J);
+        const int opl = (J + S - 1) / S;
+        const int64_t warps = ((int64_t)c->m.n_pres + (32 / S) - 1) / (32 / S);
+        dim3 grid((unsigned)((warps * 32 + 255) / 256), 2);
+#define SPP(V)                                                                                                  \
+    k_spmm_pres<V><<<grid, 256, 0, s>>>(c->m.b_rowptr, c->m.b_col, c->m.b_val, c->m.cflag, x, b, y, c->m.n_pres, \
+                                        c->n_vel, c->n_total, J, S, mode)
+        if (opl <= 1) SPP(1);
+        else if (opl <= 2) SPP(2);
+        else if (opl <= 4) SPP(4);
+        else if (opl <= 8) SPP(8);
+        else { ens_set_error("J too large for spmm", __FILE__, __LINE__); return ENS_EINVAL; }
+#undef SPP
+        ENS_CKL();
+    }
+    return ENS_OK;
+}
+
+// ---------------------------------------------------------------------------
+// deterministic column reductions: out[mat][l][j] = sum_r A_l[mat][r][j] B[mat][r][j]
+// fixed grid of ENS_RED_BLOCKS row blocks -> partials -> ordered finalize
+// ---------------------------------------------------------------------------
+__global__ void k_coldot_part(const double* __restrict__ A, int64_t lstride, const double* __restrict__ B,
+                              int64_t rows, int64_t matstride, int J, int L, double* __restrict__ part) {
+    // grid: (RB, L, 2); block 256; thread -> (row offset, column)
+    __shared__ double red[256];
+    const int l = blockIdx.y, mat = blockIdx.z;
+    const double* a = A + (int64_t)l * lstride + (int64_t)mat * matstride;
+    const double* b = B + (int64_t)mat * matstride;
+    const int64_t per = (rows + gridDim.x - 1) / gridDim.x;
+    const int64_t r0 = (int64_t)blockIdx.x * per;
+    const int64_t r1 = min(rows, r0 + per);
+    for (int jc = 0; jc < J; jc += 256) {
+        const int JB = min(256, J - jc);
+        const int RPB = 256 / JB;
+        const int jj = threadIdx.x % JB, ro = threadIdx.x / JB;
+        double acc = 0.0;
+        if (ro < RPB) {
+            for (int64_t r = r0 + ro; r < r1; r += RPB) {
+                const int64_t idx = r * J + jc + jj;
+                acc += a[idx] * b[idx];
+            }
+        }
+        red[threadIdx.x] = acc;
+        __syncthreads();
+        if (threadIdx.x < JB) {
+            double s = 0.0;
+            for (int k = 0; k < RPB; ++k) s += red[k * JB + threadIdx.x];
+            part[(((int64_t)blockIdx.x * 2 + mat) * L + l) * J + jc + threadIdx.x] = s;
+        }
+        __syncthreads();
+    }
+}
+
+__global__ void k_coldot_fin(const double* __restrict__ part, int RB, int L, int J, double* __restrict__ out) {
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    const int tot = 2 * L * J;
+    if (t >= tot) return;
+    double s = 0.0;
+    for (int b = 0; b < RB; ++b) s += part[(int64_t)b * tot + t];
+    out[t] = s;
+}
+
+int launch_coldot(ens_ctx* c, cudaStream_t s, const double* A, int64_t lstride, int L, const double* B,
+                  int64_t rows, double* out) {
+    const int RB = ENS_RED_BLOCKS;
+    dim3 grid(RB, L, 2);
+    k_coldot_part<<<grid, 256, 0, s>>>(A, lstride, B, rows, (int64_t)c->n_total * c->J, c->J, L, c->red_part);
+    ENS_CKL();
+    const int tot = 2 * L * c->J;
+    k_coldot_fin<<<(tot + 255) / 256, 256, 0, s>>>(c->red_part, RB, L, c->J, out);
+    ENS_CKL();
+    return ENS_OK;
+}
+
+// ---------------------------------------------------------------------------
+// pressure epilogue (stepper.py:119-123): p -= (p . int rho) / area per member
+// ---------------------------------------------------------------------------
+__global__ void k_pres_dot(const double* __restrict__ X, const double* __restrict__ w, int64_t nvel, int npres,
+                           int64_t N, int J, double* __restrict__ part) {
+    __shared__ double red[256];
+    const int mat = blockIdx.z;
+    const double* x = X + (int64_t)mat * N * J + nvel * J;
+    const int64_t per = ((int64_t)npres + gridDim.x - 1) / gridDim.x;
+    const int64_t r0 = (int64_t)blockIdx.x * per, r1 = min((int64_t)npres, r0 + per);
+    for (int jc = 0; jc < J; jc += 256) {
+        const int JB = min(256, J - jc);
+        const int RPB = 256 / JB;
+        const int jj = threadIdx.x % JB, ro = threadIdx.x / JB;
+        double acc = 0.0;
+        if (ro < RPB)
+            for (int64_t r = r0 + ro; r < r1; r += RPB) acc += x[r * J + jc + jj] * w[r];
+        red[threadIdx.x] = acc;
+        __syncthreads();
+        if (threadIdx.x < JB) {
+            double s2 = 0.0;
+            for (int k = 0; k < RPB; ++k) s2 += red[k * JB + threadIdx.x];
+            part[((int64_t)blockIdx.x * 2 + mat) * J + jc + threadIdx.x] = s2;
+        }
+        __syncthreads();
+    }
+}
+
+__global__ void k_pres_sub(const double* __restrict__ X, const double* __restrict__ part, int RB, double inv_area,
+                           int mean_zero, int64_t nvel, int npres, int64_t N, int J, double* __restrict__ P) {
+    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t per = (int64_t)npres * J;
+    if (t >= 2 * per) return;
+    const int mat = (int)(t / per);
+    const int64_t u = t - mat * per;
+    const int j = (int)(u % J);
+    double mean = 0.0;
+    if (mean_zero) {
+        double s = 0.0;
+        for (int b = 0; b < RB; ++b) s += part[((int64_t)b * 2 + mat) * J + j];
+        mean = s * inv_area;
+    }
+    P[t] = X[(int64_t)mat * N * J + nvel * J + u] - mean;
+}
+
+int launch_epilogue(ens_ctx* c, cudaStream_t s, const double* x, double* p_out) {
+    const int RB = 64;
+    if (c->m.mean_zero) {
+        dim3 grid(RB, 1, 2);
+        k_pres_dot<<<grid, 256, 0, s>>>(x, c->m.pres_int, c->n_vel, c->m.n_pres, c->n_total, c->J, c->red_part);
+        ENS_CKL();
+    }
+    const int64_t tot = 2LL * c->m.n_pres * c->J;
+    k_pres_sub<<<(unsigned)((tot + 255) / 256), 256, 0, s>>>(x, c->red_part, RB, 1.0 / c->m.area, c->m.mean_zero,
+                                                             c->n_vel, c->m.n_pres, c->n_total, c->J, p_out);
+    ENS_CKL();
+    return ENS_OK;
+}
+
+// ---------------------------------------------------------------------------
+// diagnostics (stepper.py:397-439, fem.py:508-514)
+// ---------------------------------------------------------------------------
+// per-member quadratic forms with M and K for v (mat 0) and w (mat 1):
+// part[blk][4][J]: (vMv, wMw, vKv, wKw)
+__global__ void k_quadforms(const int32_t* __restrict__ rp, const int32_t* __restrict__ col,
+                            const double* __restrict__ mass, const double* __restrict__ stiff,
+                            const double* __restrict__ X, int ns, int64_t N, int J, double* __restrict__ part) {
+    // block handles a node range; thread -> (node offset, member); J <= 256 per pass
+    __shared__ double red[4][256];
+    const int64_t per = ((int64_t)ns + gridDim.x - 1) / gridDim.x;
+    const int64_t n0 = (int64_t)blockIdx.x * per, n1 = min((int64_t)ns, n0 + per);
+    for (int jc = 0; jc < J; jc += 256) {
+        const int JB = min(256, J - jc);
+        const int RPB = 256 / JB;
+        const int jj = threadIdx.x % JB, ro = threadIdx.x / JB;
+        double a0 = 0, a1 = 0, a2 = 0, a3 = 0;
+        if (ro < RPB) {
+            const int j = jc + jj;
+            for (int64_t i = n0 + ro; i < n1; i += RPB) {
+                for (int cc = 0; cc < 2; ++cc) {
+                    double mv = 0, kv = 0, mw = 0, kw = 0;
+                    for (int k = rp[i]; k < rp[i + 1]; ++k) {
+                        const int64_t r = (2LL * col[k] + cc) * J + j;
+                        const double v = X[r], w = X[N * J + r];
+                        mv += mass[k] * v;
+                        kv += stiff[k] * v;
+                        mw += mass[k] * w;
+                        kw += stiff[k] * w;
+                    }
+                    const int64_t r = (2 * i + cc) * J + j;
+                    const double v = X[r], w = X[N * J + r];
+                    a0 += v * mv;
+                    a1 += w * mw;
+                    a2 += v * kv;
+                    a3 += w * kw;
+                }
+            }
+        }
+        red[0][threadIdx.x] = a0;
+        red[1][threadIdx.x] = a1;
+        red[2][threadIdx.x] = a2;
+        red[3][threadIdx.x] = a3;
+        __syncthreads();
+        if (threadIdx.x < JB) {
+            for (int f = 0; f < 4; ++f) {
+                double s = 0.0;
+                for (int k = 0; k < RPB; ++k) s += red[f][k * JB + threadIdx.x];
+                part[((int64_t)blockIdx.x * 4 + f) * J + jc + threadIdx.x] = s;
+            }
+        }
+        __syncthreads();
+    }
+}
+
+// energy of the means: mean^T M mean for v and w (single block per family, ordered)
+__global__ void k_mean_energy(const int32_t* __restrict__ rp, const int32_t* __restrict__ col,
+                              const double* __restrict__ mass, const double* __restrict__ means, int ns,
+                              double* __restrict__ out) {
+    __shared__ double red[256];
+    const int fam = blockIdx.x;
+    const double* m = means + (int64_t)fam * 2 * ns;
+    double acc = 0.0;
+    for (int64_t i = threadIdx.x; i < ns; i += blockDim.x) {
+        for (int cc = 0; cc < 2; ++cc) {
+            double s = 0.0;
+            for (int k = rp[i]; k < rp[i + 1]; ++k) s += mass[k] * m[2LL * col[k] + cc];
+            acc += m[2 * i + cc] * s;
+        }
+    }
+    red[threadIdx.x] = acc;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double s = 0.0;
+        for (int k = 0; k < (int)blockDim.x; ++k) s += red[k];
+        out[fam] = s;
+    }
+}
+
+// ||div z_j||^2 by quadrature, thread per (element, member), per-block partials
+__global__ void k_divergence(const int32_t* __restrict__ enodes, const double* __restrict__ egeo, int nt,
+                             const double* __restrict__ X, int64_t N, int J, int JB, double* __restrict__ part) {
+    extern __shared__ double red2[];   // [2][blockDim]
+    const int EPB = blockDim.x / JB;
+    const int el = threadIdx.x / JB, jj = threadIdx.x % JB;
+    const int j = blockIdx.y * JB + jj;
+    double sv = 0.0, sw = 0.0;
+    if (el < EPB && j < J) {
+        for (int e = blockIdx.x * EPB + el; e < nt; e += gridDim.x * EPB) {
+            double gl[6];
+            const double area = egeo[(int64_t)e * 8];
+            for (int i = 0; i < 6; ++i) gl[i] = egeo[(int64_t)e * 8 + 1 + i];
+            double vx[6], vy[6], wx[6], wy[6];
+            for (int a = 0; a < 6; ++a) {
+                const int64_t nd = enodes[(int64_t)e * 6 + a];
+                vx[a] = X[(2 * nd) * J + j];
+                vy[a] = X[(2 * nd + 1) * J + j];
+                wx[a] = X[N * J + (2 * nd) * J + j];
+                wy[a] = X[N * J + (2 * nd + 1) * J + j];
+            }
+            for (int q = 0; q < ENS_NQ; ++q) {
+                double dv = 0.0, dw = 0.0;
+                for (int a = 0; a < 6; ++a) {
+                    double gx, gy;
+                    grad_phi(gl, q, a, gx, gy);
+                    dv += vx[a] * gx + vy[a] * gy;
+                    dw += wx[a] * gx + wy[a] * gy;
+                }
+                const double wd = area * c_qw[q];
+                sv += wd * dv * dv;
+                sw += wd * dw * dw;
+            }
+        }
+    }
+    red2[threadIdx.x] = sv;
+    red2[blockDim.x + threadIdx.x] = sw;
+    __syncthreads();
+    if (threadIdx.x < JB && j < J) {
+        double a = 0.0, b = 0.0;
+        for (int k = 0; k < EPB; ++k) {
+            a += red2[k * JB + threadIdx.x];
+            b += red2[blockDim.x + k * JB + threadIdx.x];
+        }
+        part[((int64_t)blockIdx.x * 2 + 0) * J + j] = a;
+        part[((int64_t)blockIdx.x * 2 + 1) * J + j] = b;
+    }
+}
+
+__global__ void k_diag_fin(const double* __restrict__ pq, int RBq, const double* __restrict__ pd, int RBd, int J,
+                           double* __restrict__ out) {
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= 6 * J) return;
+    const int f = t / J, j = t % J;
+    double s = 0.0;
+    if (f < 4) {
+        for (int b = 0; b < RBq; ++b) s += pq[((int64_t)b * 4 + f) * J + j];
+    } else {
+        for (int b = 0; b < RBd; ++b) s += pd[((int64_t)b * 2 + (f - 4)) * J + j];
+    }
+    // out layout: vMv, wMw, vKv, wKw, div_v^2, div_w^2
+    out[2 + (int64_t)f * J + j] = s;
+}
+
+int launch_diagnostics(ens_ctx* c, cudaStream_t s, const double* x, const double* means, double* out) {
+    const int J = c->J;
+    const int RBq = 148;
+    k_quadforms<<<RBq, 256, 0, s>>>(c->m.s_rowptr, c->m.s_col, c->m.s_mass, c->m.s_stiff, x, c->m.ns, c->n_total, J,
+                                    c->red_part);
+    ENS_CKL();
+    const int JB = J < 128 ? J : 128;
+    const int EPB = 128 / JB > 0 ? 128 / JB : 1;
+    const int RBd = 148;
+    double* pd = c->red_part + (size_t)RBq * 4 * J;
+    dim3 grid(RBd, (J + JB - 1) / JB);
+    // the y-dimension splits members; partial index uses blockIdx.x only (members disjoint per y)
+    k_divergence<<<grid, EPB * JB, sizeof(double) * 2 * EPB * JB, s>>>(c->m.e_nodes, c->m.e_geo, c->m.nt, x,
+                                                                      c->n_total, J, JB, pd);
+    ENS_CKL();
+    k_diag_fin<<<(6 * J + 255) / 256, 256, 0, s>>>(c->red_part, RBq, pd, RBd, J, out);
+    ENS_CKL();
+    k_mean_energy<<<2, 256, 0, s>>>(c->m.s_rowptr, c->m.s_col, c->m.s_mass, means, c->m.ns, out);
+    ENS_CKL();
+    return ENS_OK;
+}

@@ -1,0 +1,256 @@
+// Column-batched right-preconditioned FGMRES over both saddle systems.
+//
+// Every ensemble member is an independent column (no block Krylov mixing, so
+// identical members stay bitwise identical, tests/test_stepper.py:213-229 of
+// the reference); all columns share each SpMM and each preconditioner sweep.
+// Per-column Krylov scalars (Hessenberg, Givens, residual estimate) live on the
+// device; the host only reads one counter per iteration to stop early.
+// Replaces Factorization.solve_block + relative_residual (linalg.py:62-76, 111-118).
+#include <cmath>
+
+#include "ens_internal.cuh"
+
+struct GmresCol {
+    double H[(ENS_MAX_RESTART + 1) * ENS_MAX_RESTART];
+    double cs[ENS_MAX_RESTART], sn[ENS_MAX_RESTART], g[ENS_MAX_RESTART + 1];
+    double bnorm, tol;
+    int active, kused;
+};
+
+size_t gmres_col_bytes() { return sizeof(GmresCol); }
+
+int gmres_alloc(ens_ctx* c, int restart) {
+    if (restart < 1 || restart > ENS_MAX_RESTART) {
+        ens_set_error("restart out of range", __FILE__, __LINE__);
+        return ENS_EINVAL;
+    }
+    if (c->kry && c->kry_restart >= restart) return ENS_OK;
+    if (c->kry) cudaFree(c->kry);
+    const size_t blk = 2ull * (size_t)c->n_total * c->J;
+    const size_t nblk = 2 * (size_t)restart + 3;   // V[0..R], Z[0..R-1], R, W
+    if (cudaMalloc(&c->kry, sizeof(double) * blk * nblk) != cudaSuccess) {
+        c->kry = nullptr;
+        ens_set_error("out of device memory for Krylov blocks", __FILE__, __LINE__);
+        return ENS_ENOMEM;
+    }
+    c->ws_bytes += sizeof(double) * blk * nblk;
+    c->kry_restart = restart;
+    return ENS_OK;
+}
+
+// scalar buffers inside red_out:  [bn2 | rn2 | h1 | h2 | hn2 | scale | y]
+struct KBuf {
+    double *bn2, *rn2, *h1, *h2, *hn2, *scale, *y;
+};
+
+static KBuf kbuf(ens_ctx* c) {
+    const size_t J2 = 2 * (size_t)c->J;
+    const size_t L = ENS_MAX_RESTART + 1;
+    KBuf b;
+    b.bn2 = c->red_out;
+    b.rn2 = b.bn2 + J2;
+    b.h1 = b.rn2 + J2;
+    b.h2 = b.h1 + J2 * L;
+    b.hn2 = b.h2 + J2 * L;
+    b.scale = b.hn2 + J2;
+    b.y = b.scale + J2;
+    return b;
+}
+
+__global__ void k_gm_init(GmresCol* cols, const double* bn2, const double* rn2, double rtol, double* scale,
+                          int32_t* count, int n) {
+    const int c = blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= n) return;
+    GmresCol& g = cols[c];
+    const double bn = sqrt(bn2[c]);
+    const double beta = sqrt(rn2[c]);
+    g.bnorm = bn;
+    g.tol = rtol * fmax(bn, 2.2250738585072014e-308);
+    g.active = beta > g.tol ? 1 : 0;
+    g.kused = 0;
+    for (int i = 0; i <= ENS_MAX_RESTART; ++i) g.g[i] = 0.0;
+    g.g[0] = beta;
+    scale[c] = g.active ? 1.0 / beta : 0.0;
+    if (g.active) atomicAdd(count, 1);
+}
+
+// dst = src * scale[col]
+__global__ void k_scale_cols(double* __restrict__ dst, const double* __restrict__ src,
+                             const double* __restrict__ scale, int64_t N, int J) {
+    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t per = N * J;
+    if (t >= 2 * per) return;
+    const int mat = (int)(t / per);
+    const int j = (int)((t - mat * per) % J);
+    dst[t] = src[t] * scale[mat * J + j];
+}
+
+// W -= sum_l V_l h[mat][l][j]  (sign = -1) or X += sum_l Z_l y (sign = +1)
+__global__ void k_axpy_multi(double* __restrict__ W, const double* __restrict__ V, int64_t lstride, int L,
+                             const double* __restrict__ h, double sign, int64_t N, int J) {
+    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t per = N * J;
+    if (t >= 2 * per) return;
+    const int mat = (int)(t / per);
+    const int j = (int)((t - mat * per) % J);
+    double acc = 0.0;
+    for (int l = 0; l < L; ++l) acc += V[(int64_t)l * lstride + t] * h[((int64_t)mat * L + l) * J + j];
+    W[t] += sign * acc;
+}
+
+// store Hessenberg column i (h1 + h2), apply Givens, update residual estimate
+__global__ void k_gm_givens(GmresCol* cols, const double* h1, const double* h2, const double* hn2, int i,
+                            double* scale, int32_t* count, int n, int J) {
+    const int c = blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= n) return;
+    GmresCol& g = cols[c];
+    const int R = ENS_MAX_RESTART;
+    const int mat = c / J, j = c % J;
+    const int L = i + 1;
+    if (!g.active) {
+        scale[c] = 0.0;
+        return;
+    }
+    double col[ENS_MAX_RESTART + 1];
+    for (int l = 0; l <= i; ++l) {
+        const int64_t idx = ((int64_t)mat * L + l) * J + j;
+        col[l] = h1[idx] + h2[idx];
+    }
+    const double hn = sqrt(hn2[c]);
+    col[i + 1] = hn;
+    for (int l = 0; l < i; ++l) {   // previous rotations
+        const double t0 = g.cs[l] * col[l] + g.sn[l] * col[l + 1];
+        col[l + 1] = -g.sn[l] * col[l] + g.cs[l] * col[l + 1];
+        col[l] = t0;
+    }
+    const double a = col[i], b = col[i + 1];
+    const double r = hypot(a, b);
+    double cs = 1.0, sn = 0.0;
+    if (r > 0.0) {
+        cs = a / r;
+        sn = b / r;
+    }
+    g.cs[i] = cs;
+    g.sn[i] = sn;
+    col[i] = r;
+    col[i + 1] = 0.0;
+    for (int l = 0; l <= i; ++l) g.H[l * R + i] = col[l];
+    g.g[i + 1] = -sn * g.g[i];
+    g.g[i] = cs * g.g[i];
+    g.kused = i + 1;
+    const double res = fabs(g.g[i + 1]);
+    const bool breakdown = !(hn > 1e-300 * fmax(g.bnorm, 1e-300)) || r == 0.0;
+    if (res <= g.tol || breakdown) {
+        g.active = 0;
+        scale[c] = 0.0;
+    } else {
+        scale[c] = 1.0 / hn;
+        atomicAdd(count, 1);
+    }
+}
+
+// y = H^-1 g (per column), layout y[mat][l][j] with L = Lmax rows
+__global__ void k_gm_solve_y(GmresCol* cols, double* y, int Lmax, int n, int J) {
+    const int c = blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= n) return;
+    GmresCol& g = cols[c];
+    const int R = ENS_MAX_RESTART;
+    const int mat = c / J, j = c % J;
+    double yy[ENS_MAX_RESTART];
+    const int k = g.kused;
+    for (int l = k - 1; l >= 0; --l) {
+        double s = g.g[l];
+        for (int t = l + 1; t < k; ++t) s -= g.H[l * R + t] * yy[t];
+        yy[l] = g.H[l * R + l] != 0.0 ? s / g.H[l * R + l] : 0.0;
+    }
+    for (int l = 0; l < Lmax; ++l) y[((int64_t)mat * Lmax + l) * J + j] = l < k ? yy[l] : 0.0;
+}
+
+static int read_count(ens_ctx* c, cudaStream_t s, int* out) {
+    ENS_CK(cudaMemcpyAsync(c->h_count, c->d_count, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+    ENS_CK(cudaStreamSynchronize(s));
+    *out = c->h_count[0];
+    return ENS_OK;
+}
+
+#define RET(x)                        \
+    do {                              \
+        int rc_ = (x);                \
+        if (rc_ != ENS_OK) return rc_; \
+    } while (0)
+
+int gmres_solve(ens_ctx* c, cudaStream_t s, const double* as_vals, const double* rhs, double* x, double rtol,
+                int restart, int max_restarts, int32_t* iters, double* relres) {
+    RET(gmres_alloc(c, restart));
+    const int J = c->J;
+    const int n = 2 * J;
+    const int64_t N = c->n_total;
+    const int64_t blk = 2LL * N * J;
+    double* V = c->kry;                          // restart+1 blocks
+    double* Z = V + blk * (restart + 1);         // restart blocks
+    double* Rb = Z + blk * restart;
+    double* Wb = Rb + blk;
+    KBuf kb = kbuf(c);
+    const unsigned eb = (unsigned)((blk + 255) / 256);
+    const unsigned cb = (unsigned)((n + 127) / 128);
+    // identity rows of the iterate carry the data exactly (stepper.py:214-215, 250-251)
+    RET(launch_copy_cons(c, s, rhs, x));
+    RET(launch_coldot(c, s, rhs, 0, 1, rhs, N, kb.bn2));
+    int total_it = 0;
+    for (int cyc = 0; cyc <= max_restarts; ++cyc) {
+        RET(launch_spmm(c, s, as_vals, x, rhs, Rb, 1));
+        RET(launch_coldot(c, s, Rb, 0, 1, Rb, N, kb.rn2));
+        ENS_CK(cudaMemsetAsync(c->d_count, 0, sizeof(int32_t), s));
+        k_gm_init<<<cb, 128, 0, s>>>(c->cols, kb.bn2, kb.rn2, rtol, kb.scale, c->d_count, n);
+        ENS_CKL();
+        int active = 0;
+        RET(read_count(c, s, &active));
+        if (active == 0 || cyc == max_restarts) {
+            // true relative residual per matrix (linalg.py:111-118)
+            ENS_CK(cudaMemcpyAsync(c->h_small, kb.bn2, sizeof(double) * 2 * n, cudaMemcpyDeviceToHost, s));
+            ENS_CK(cudaStreamSynchronize(s));
+            for (int mat = 0; mat < 2; ++mat) {
+                double worst = 0.0;
+                for (int j = 0; j < J; ++j) {
+                    const double bn = std::sqrt(c->h_small[mat * J + j]);
+                    const double rn = std::sqrt(c->h_small[n + mat * J + j]);
+                    worst = std::fmax(worst, rn / std::fmax(bn, 2.2250738585072014e-308));
+                }
+                relres[mat] = worst;
+            }
+            *iters = total_it;
+            return active == 0 ? ENS_OK : ENS_ENOCONV;
+        }
+        k_scale_cols<<<eb, 256, 0, s>>>(V, Rb, kb.scale, N, J);
+        ENS_CKL();
+        int used = 0;
+        for (int i = 0; i < restart; ++i) {
+            double* Vi = V + blk * i;
+            double* Zi = Z + blk * i;
+            RET(mf_solve(c, s, Vi, Zi));
+            RET(launch_spmm(c, s, as_vals, Zi, nullptr, Wb, 0));
+            // CGS2 against V[0..i]
+            RET(launch_coldot(c, s, V, blk, i + 1, Wb, N, kb.h1));
+            k_axpy_multi<<<eb, 256, 0, s>>>(Wb, V, blk, i + 1, kb.h1, -1.0, N, J);
+            ENS_CKL();
+            RET(launch_coldot(c, s, V, blk, i + 1, Wb, N, kb.h2));
+            k_axpy_multi<<<eb, 256, 0, s>>>(Wb, V, blk, i + 1, kb.h2, -1.0, N, J);
+            ENS_CKL();
+            RET(launch_coldot(c, s, Wb, 0, 1, Wb, N, kb.hn2));
+            ENS_CK(cudaMemsetAsync(c->d_count, 0, sizeof(int32_t), s));
+            k_gm_givens<<<cb, 128, 0, s>>>(c->cols, kb.h1, kb.h2, kb.hn2, i, kb.scale, c->d_count, n, J);
+            ENS_CKL();
+            k_scale_cols<<<eb, 256, 0, s>>>(V + blk * (i + 1), Wb, kb.scale, N, J);
+            ENS_CKL();
+            used = i + 1;
+            ++total_it;
+            RET(read_count(c, s, &active));
+            if (active == 0) break;
+        }
+        k_gm_solve_y<<<cb, 128, 0, s>>>(c->cols, kb.y, used, n, J);
+        ENS_CKL();
+        k_axpy_multi<<<eb, 256, 0, s>>>(x, Z, blk, used, kb.y, 1.0, N, J);
+        ENS_CKL();
+    }
+    return ENS_ENOCONV;
+}

@@ -1,0 +1,492 @@
+"""Device engine: uploads one mesh once, then runs time-steps through the C ABI.
+
+One engine per (Discretization, local member count, device).  All per-step
+data stays in HBM; the host only uploads tiny per-step coefficient tables
+(problem data in separable form) and reads a handful of scalars.
+
+Per time-step (reference `stepper.advance`, `stepper.py:360-394`):
+  1. ens_member_sums            -> [allreduce SUM]   -> means  (ensemble.py:216-224)
+  2. ens_rhs, ens_member_pass   -> [allreduce MAX of max_j |z'_j|^2]  (stepper.py:223-252,
+                                                                       ensemble.py:227-238)
+  3. ens_apply_bc               (stepper.py:250-251)
+  4. ens_assemble               both shared velocity blocks (stepper.py:195-206)
+  5. ens_factor                 multifrontal LU of both saddle matrices (linalg.py:79-108)
+  6. ens_solve                  column-batched FGMRES, true residual (linalg.py:62-76, 111-118)
+  7. ens_epilogue               mean-zero pressures (stepper.py:389-390)
+The V and W sub-steps share every launch (2 matrices per grid), since they
+depend on level-n data only (`stepper.py:363-366`).
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import weakref
+
+import numpy as np
+import scipy.sparse as sp
+import torch
+
+from . import _native as N
+from . import fe
+from . import symbolic as S
+from .ensemble import viscosity_stats
+
+
+def _dptr(t: torch.Tensor) -> int:
+    return t.data_ptr()
+
+
+def _color_elements(cell_dofs: np.ndarray, ns: int) -> np.ndarray:
+    """Greedy element colouring: elements sharing a P2 node get different colours."""
+    node_mask = np.zeros(ns, dtype=np.int64)
+    colors = np.empty(len(cell_dofs), dtype=np.int64)
+    cd = cell_dofs.tolist()
+    nm = node_mask.tolist()
+    for e, nodes in enumerate(cd):
+        used = 0
+        for n in nodes:
+            used |= nm[n]
+        c = 0
+        while used >> c & 1:
+            c += 1
+        colors[e] = c
+        bit = 1 << c
+        for n in nodes:
+            nm[n] |= bit
+    return colors
+
+
+class HostMesh:
+    """All host-side arrays of one mesh in the engine's internal numbering (built once)."""
+
+    def __init__(self, disc):
+        self.disc = disc
+        vel, pres = disc.velocity, disc.pressure
+        ns, npres, nvel = disc.n_scalar, disc.n_pres, disc.n_vel
+        self.ns, self.npres, self.nvel, self.ntot = ns, npres, nvel, nvel + npres
+        plan = S.analyse(disc)
+        self.plan = plan
+        nperm, pperm = plan.node_perm, plan.pres_perm
+        # internal row of every reference dof, and the inverse
+        int_id = np.empty(self.ntot, dtype=np.int64)
+        int_id[:ns] = 2 * nperm
+        int_id[ns:nvel] = 2 * nperm + 1
+        int_id[nvel:] = nvel + pperm
+        self.int_id = int_id
+        self.ref_of_int = np.empty_like(int_id)
+        self.ref_of_int[int_id] = np.arange(self.ntot)
+        # scalar operators in internal node order
+        P = sp.csr_matrix((np.ones(ns), (nperm, np.arange(ns))), shape=(ns, ns))
+        pat = fe.scalar_pattern(vel)
+        ipat = (P @ pat @ P.T).tocsr()
+        ipat.sort_indices()
+        self.s_rowptr = ipat.indptr.astype(np.int32)
+        self.s_col = ipat.indices.astype(np.int32)
+        self.nnz_s = ipat.nnz
+
+        def aligned(mat):
+            m2 = (P @ mat @ P.T).tocsr()
+            m2.sort_indices()
+            out = np.zeros(self.nnz_s)
+            # map values by (row, col) -> slot
+            rows = np.repeat(np.arange(ns), np.diff(m2.indptr))
+            slot = self._slot(rows, m2.indices)
+            out[slot] = m2.data
+            return out
+
+        self.s_mass = aligned(disc.mass_s)
+        self.s_stiff = aligned(disc.stiff_s)
+        # the plan indexes A_s values in the reference pattern order; the device
+        # stores them in internal order -> remap those source indices once
+        ref_rows = np.repeat(np.arange(ns), np.diff(pat.indptr))
+        ref_to_int_slot = self._slot(nperm[ref_rows], nperm[pat.indices])
+        src = plan.orig_src.astype(np.int64)
+        is_a = src < self.nnz_s
+        src[is_a] = ref_to_int_slot[src[is_a]]
+        self.orig_src = src.astype(np.int32)
+        # B by pressure row and B^T by node, (bx, by) pairs on one pattern
+        bip, bcol, bx, by = fe.divergence_pair(vel, pres)
+        brow = np.repeat(np.arange(npres), np.diff(bip))
+        r_int, c_int = pperm[brow], nperm[bcol]
+        o = np.lexsort((c_int, r_int))
+        self.b_rowptr = np.concatenate([[0], np.cumsum(np.bincount(r_int, minlength=npres))]).astype(np.int32)
+        self.b_col = c_int[o].astype(np.int32)
+        self.b_val = np.stack([bx[o], by[o]], axis=1).ravel()
+        o2 = np.lexsort((r_int, c_int))
+        self.bt_rowptr = np.concatenate([[0], np.cumsum(np.bincount(c_int, minlength=ns))]).astype(np.int32)
+        self.bt_col = r_int[o2].astype(np.int32)
+        self.bt_val = np.stack([bx[o2], by[o2]], axis=1).ravel()
+        # identity rows
+        cons_ref = disc.constrained_rows
+        self.cflag = np.zeros(self.ntot, dtype=np.uint8)
+        self.cflag[int_id[cons_ref]] = 1
+        nb = disc.bdofs.size
+        self.cons_row = int_id[cons_ref].astype(np.int32)
+        self.cons_bidx = np.concatenate([np.arange(nb), -np.ones(len(cons_ref) - nb)]).astype(np.int32)
+        self.nbdofs = nb
+        # elements, coloured
+        colors = _color_elements(vel.cell_dofs, ns)
+        inodes = nperm[vel.cell_dofs]
+        eorder = np.lexsort((inodes.min(axis=1), colors))
+        self.ncolor = int(colors.max()) + 1
+        self.color_off = np.searchsorted(colors[eorder], np.arange(self.ncolor + 1)).astype(np.int32)
+        self.e_nodes = inodes[eorder].astype(np.int32)
+        geo = np.zeros((len(eorder), 8))
+        geo[:, 0] = vel.areas[eorder]
+        geo[:, 1:7] = vel.grad_lam[eorder].reshape(-1, 6)
+        self.e_geo = geo.ravel()
+        a_idx = np.repeat(self.e_nodes, 6, axis=1)
+        b_idx = np.tile(self.e_nodes, (1, 6))
+        self.e_slots = self._slot(a_idx.ravel(), b_idx.ravel()).astype(np.int32)
+        self.eorder = eorder
+        self.pres_int = np.empty(npres)
+        self.pres_int[pperm] = disc.pressure_integrals
+
+    def _slot(self, rows, cols):
+        rows = np.asarray(rows, dtype=np.int64)
+        cols = np.asarray(cols, dtype=np.int64)
+        key = rows * (self.ns + 1) + cols
+        allrows = np.repeat(np.arange(self.ns, dtype=np.int64), np.diff(self.s_rowptr))
+        allkey = allrows * (self.ns + 1) + self.s_col
+        pos = np.searchsorted(allkey, key)
+        assert np.all(allkey[pos] == key), "slot lookup failed"
+        return pos
+
+    # host <-> internal conversions (numpy)
+    def vel_to_internal(self, arr_ref):
+        """(J, n_vel) reference order -> (n_vel, J) internal order."""
+        return np.ascontiguousarray(np.asarray(arr_ref, dtype=float).T[self.ref_of_int[:self.nvel]])
+
+    def pres_to_internal(self, arr_ref):
+        return np.ascontiguousarray(np.asarray(arr_ref, dtype=float).T[self.ref_of_int[self.nvel:] - self.nvel])
+
+
+def host_mesh(disc) -> HostMesh:
+    key = "b200-hostmesh"
+    if key not in disc._cache:
+        disc._cache[key] = HostMesh(disc)
+    return disc._cache[key]
+
+
+class DeviceState:
+    """Handle on one engine buffer set; materialises numpy on demand."""
+
+    def __init__(self, engine, buf, gen, num_members):
+        self.engine = engine
+        self.buf = buf
+        self.gen = gen
+        self.num_members = num_members
+        self._host = {}
+
+    @property
+    def valid(self):
+        return self.engine is not None and self.engine.gen[self.buf] == self.gen
+
+    def materialize(self):
+        for name in "vwqr":
+            self.to_host(name)
+        self.engine = None
+
+    def to_host(self, name):
+        if name in self._host:
+            return self._host[name]
+        if not self.valid:
+            raise RuntimeError("device state was overwritten before it was read")
+        arr = self.engine.field_to_host(self.buf, name)
+        self._host[name] = arr
+        return arr
+
+
+class Engine:
+    """Device-resident ensemble on one GPU (member columns [j0, j0+J) of J_total)."""
+
+    def __init__(self, disc, config, j0=0, J=None, device=None, comm=None, restart=8, max_restarts=20, rtol=1e-12):
+        if not torch.cuda.is_available():
+            raise RuntimeError("the B200 time-step engine needs a CUDA device (no CPU fallback)")
+        self.lib = N.load()
+        self.dev = torch.device("cuda", torch.cuda.current_device() if device is None else device)
+        self.hm = hm = host_mesh(disc)
+        self.disc = disc
+        self.J_total = config.num_members
+        self.j0 = j0
+        self.J = J = self.J_total if J is None else J
+        self.comm = comm
+        self.restart, self.max_restarts, self.rtol = restart, max_restarts, rtol
+        self.ntot, self.nvel, self.npres = hm.ntot, hm.nvel, hm.npres
+        d = self.dev
+        f64 = dict(dtype=torch.float64, device=d)
+
+        def up(a, dtype):
+            return torch.as_tensor(np.ascontiguousarray(a), dtype=dtype).to(d)
+
+        i32, i64 = torch.int32, torch.int64
+        self._keep = []
+        mesh_t = dict(
+            s_rowptr=up(hm.s_rowptr, i32), s_col=up(hm.s_col, i32), s_mass=up(hm.s_mass, torch.float64),
+            s_stiff=up(hm.s_stiff, torch.float64), bt_rowptr=up(hm.bt_rowptr, i32), bt_col=up(hm.bt_col, i32),
+            bt_val=up(hm.bt_val, torch.float64), b_rowptr=up(hm.b_rowptr, i32), b_col=up(hm.b_col, i32),
+            b_val=up(hm.b_val, torch.float64), cflag=up(hm.cflag, torch.uint8), e_nodes=up(hm.e_nodes, i32),
+            e_geo=up(hm.e_geo, torch.float64), e_slots=up(hm.e_slots, i32),
+            cons_row=up(hm.cons_row if len(hm.cons_row) else np.zeros(1, np.int32), i32),
+            cons_bidx=up(hm.cons_bidx if len(hm.cons_bidx) else np.zeros(1, np.int32), i32),
+            pres_int=up(hm.pres_int, torch.float64))
+        self.mesh_t = mesh_t
+        self._color_off = np.ascontiguousarray(hm.color_off, dtype=np.int32)
+        md = N.MeshDesc()
+        md.ns, md.n_pres, md.nt, md.nnz_s, md.J = hm.ns, hm.npres, len(hm.e_nodes), hm.nnz_s, J
+        md.ncolor, md.ncons = hm.ncolor, len(hm.cons_row)
+        for k, t in mesh_t.items():
+            setattr(md, k, _dptr(t))
+        md.color_off_host = self._color_off.ctypes.data
+        md.area = float(disc.area)
+        md.mean_zero = 1 if disc.pin_pressure else 0
+        self.nt = md.nt
+        p = hm.plan
+        plan_t = dict(
+            f_m=up(p.f_m, i32), f_k=up(p.f_k, i32), f_off=up(p.f_off, i64), f_idx_off=up(p.f_idx_off, i64),
+            f_idx=up(p.f_idx, i32), f_parent=up(p.f_parent, i32), f_cmap_off=up(p.f_cmap_off, i64),
+            f_cmap=up(p.f_cmap if len(p.f_cmap) else np.zeros(1, np.int32), i32), orig_dst=up(p.orig_dst, i64),
+            orig_src=up(hm.orig_src, i32), bsrc_vals=up(p.bsrc_vals, torch.float64),
+            work=up(p.schedule["work"].ravel() if p.schedule["work"].size else np.zeros(4, np.int32), i32))
+        self.plan_t = plan_t
+        self._host_keep = dict(
+            orig_level_off=np.ascontiguousarray(p.orig_level_off, dtype=np.int64),
+            level_storage_off=np.ascontiguousarray(p.level_storage_off, dtype=np.int64),
+            level_front_off=np.ascontiguousarray(p.level_front_off, dtype=np.int32),
+            factor=np.ascontiguousarray(p.schedule["factor"], dtype=np.int64),
+            fwd=np.ascontiguousarray(p.schedule["fwd"], dtype=np.int64),
+            bwd=np.ascontiguousarray(p.schedule["bwd"], dtype=np.int64))
+        pd = N.PlanDesc()
+        pd.nfront, pd.nlevels, pd.pw, pd.tile = p.nfront, p.nlevels, S.PW, S.TILE
+        pd.front_storage, pd.n_orig = p.front_storage, len(p.orig_dst)
+        pd.n_cmap, pd.n_idx, pd.n_work = len(p.f_cmap), int(p.f_idx_off[-1]), len(p.schedule["work"])
+        for k, t in plan_t.items():
+            setattr(pd, k, _dptr(t))
+        hk = self._host_keep
+        pd.orig_level_off_host = hk["orig_level_off"].ctypes.data
+        pd.level_storage_off_host = hk["level_storage_off"].ctypes.data
+        pd.level_front_off_host = hk["level_front_off"].ctypes.data
+        pd.sched_factor_host, pd.n_sched_factor = hk["factor"].ctypes.data, len(hk["factor"])
+        pd.sched_fwd_host, pd.n_sched_fwd = hk["fwd"].ctypes.data, len(hk["fwd"])
+        pd.sched_bwd_host, pd.n_sched_bwd = hk["bwd"].ctypes.data, len(hk["bwd"])
+        pd.max_m = int(p.f_m.max())
+        self._md, self._pd = md, pd
+        ctx = C.c_void_p()
+        with torch.cuda.device(self.dev):
+            N.check(self.lib.ens_create(C.byref(md), C.byref(pd), self.dev.index, C.byref(ctx)), "ens_create")
+        self.ctx = ctx
+        # per-run constants
+        st = viscosity_stats(config)
+        self.config = config
+        base = hm.s_mass / config.dt + 0.5 * (st.nu_bar + st.nu_m_bar) * hm.s_stiff
+        self.base = up(base, torch.float64)
+        lag_same = 0.5 * (st.nu_fluct + st.nu_m_fluct)
+        lag_cross = 0.5 * (config.nu - config.nu_m)
+        sl = slice(j0, j0 + J)
+        self.member_coef = up(np.concatenate([lag_same[sl], lag_cross[sl]]), torch.float64)
+        self.two_mu_dt = 2.0 * config.mu * config.dt
+        if not (config.mu > 0.0):
+            raise ValueError("mu and dt must be positive")
+        # buffers
+        ntot, nvel = self.ntot, self.nvel
+        self.X = [torch.zeros(2, ntot, J, **f64), torch.zeros(2, ntot, J, **f64)]
+        self.Pq = [torch.zeros(2, self.npres, J, **f64), torch.zeros(2, self.npres, J, **f64)]
+        self.gen = [0, 0]
+        self.live = [None, None]
+        self.cur = 0
+        self.rhs = torch.zeros(2, ntot, J, **f64)
+        self.sums = torch.zeros(2 * nvel, **f64)
+        self.means = torch.zeros(2 * nvel, **f64)
+        self.means_valid = False
+        self.maxsq = torch.zeros(2, self.nt, 7, **f64)
+        self.as_vals = torch.zeros(2, hm.nnz_s, **f64)
+        self.diag_out = torch.zeros(2 + 6 * J, **f64)
+        self.stream = torch.cuda.current_stream(self.dev)
+        self._data_cache = {}
+        self.last_iters = 0
+        self.last_pert = 0
+        self.last_relres = (0.0, 0.0)
+
+    def __del__(self):
+        try:
+            if getattr(self, "ctx", None):
+                self.lib.ens_destroy(self.ctx)
+                self.ctx = None
+        except Exception:
+            pass
+
+    @property
+    def sptr(self):
+        return C.c_void_p(self.stream.cuda_stream)
+
+    # ------------------------------------------------------------------
+    # state upload / download
+    # ------------------------------------------------------------------
+    def load_state(self, v, w, q, r):
+        """Upload a host state (reference layout, this rank's members) into the current buffer set."""
+        hm = self.hm
+        self._retire(self.cur)
+        X = self.X[self.cur]
+        X[0, :self.nvel] = torch.from_numpy(hm.vel_to_internal(v)).to(self.dev)
+        X[1, :self.nvel] = torch.from_numpy(hm.vel_to_internal(w)).to(self.dev)
+        if q is not None and np.asarray(q).size:
+            X[0, self.nvel:] = torch.from_numpy(hm.pres_to_internal(q)).to(self.dev)
+            X[1, self.nvel:] = torch.from_numpy(hm.pres_to_internal(r)).to(self.dev)
+            self.Pq[self.cur][0] = X[0, self.nvel:]
+            self.Pq[self.cur][1] = X[1, self.nvel:]
+        else:
+            X[:, self.nvel:] = 0.0
+            self.Pq[self.cur].zero_()
+        self.gen[self.cur] += 1
+        self.means_valid = False
+
+    def field_to_host(self, buf, name):
+        hm = self.hm
+        torch.cuda.synchronize(self.dev)
+        if name in "vw":
+            blk = self.X[buf][0 if name == "v" else 1, :self.nvel]
+            out = np.empty((self.J, self.nvel))
+            out[:, hm.ref_of_int[:self.nvel]] = blk.cpu().numpy().T
+            return out
+        blk = self.Pq[buf][0 if name == "q" else 1]
+        out = np.empty((self.J, self.npres))
+        out[:, hm.ref_of_int[self.nvel:] - self.nvel] = blk.cpu().numpy().T
+        return out
+
+    def state_handle(self):
+        h = DeviceState(self, self.cur, self.gen[self.cur], self.J)
+        self.live[self.cur] = weakref.ref(h)
+        return h
+
+    def _retire(self, buf):
+        ref = self.live[buf]
+        if ref is not None:
+            h = ref()
+            if h is not None and h.engine is self and h.gen == self.gen[buf]:
+                h.materialize()
+        self.live[buf] = None
+
+    # ------------------------------------------------------------------
+    # problem data
+    # ------------------------------------------------------------------
+    def _data(self, obj, kind, t):
+        """ens_data_desc for loads ('loads') or Dirichlet values ('bc') at time t."""
+        hm, J, sl = self.hm, self.J, slice(self.j0, self.j0 + self.J)
+        rows = self.nvel if kind == "loads" else hm.nbdofs
+        sep = None
+        if hasattr(obj, "separable"):
+            key = (kind, id(obj))
+            if key not in self._data_cache:
+                s = obj.separable(self.disc, self.config)
+                basis = np.asarray(s.basis, dtype=float).reshape(len(s.basis), -1)
+                if kind == "loads":
+                    basis = basis[:, hm.ref_of_int[:self.nvel]]
+                self._data_cache[key] = (s, torch.as_tensor(np.ascontiguousarray(basis)).to(self.dev))
+            sep = self._data_cache[key]
+        dd = N.DataDesc()
+        dd.rows = rows
+        keep = []
+        if sep is not None:
+            s, basis_t = sep
+            cv, cw = s.coef(t)
+            coef = np.stack([np.asarray(cv, float)[:, sl], np.asarray(cw, float)[:, sl]])
+            coef_t = torch.as_tensor(np.ascontiguousarray(coef)).to(self.dev, non_blocking=True)
+            dd.K, dd.basis, dd.coef, dd.dense = basis_t.shape[0], _dptr(basis_t), _dptr(coef_t), None
+            keep += [basis_t, coef_t]
+        else:
+            if kind == "loads":
+                lv, lw = obj.loads(t, self.disc, self.config)
+                if lv is None and lw is None:
+                    return None, keep
+                z = np.zeros((self.J_total, self.nvel))
+                lv = z if lv is None else np.asarray(lv)
+                lw = z if lw is None else np.asarray(lw)
+                dense = np.stack([hm.vel_to_internal(lv[sl]), hm.vel_to_internal(lw[sl])])
+            else:
+                bv, bw = obj.values(t, self.disc, self.config)
+                dense = np.stack([np.asarray(bv, float)[sl].T, np.asarray(bw, float)[sl].T])
+            dense_t = torch.as_tensor(np.ascontiguousarray(dense)).to(self.dev)
+            dd.K, dd.basis, dd.coef, dd.dense = 0, None, None, _dptr(dense_t)
+            keep.append(dense_t)
+        return dd, keep
+
+    # ------------------------------------------------------------------
+    # the time-step
+    # ------------------------------------------------------------------
+    def compute_means(self):
+        lib, ctx, s = self.lib, self.ctx, self.sptr
+        X = self.X[self.cur]
+        N.check(lib.ens_member_sums(ctx, s, _dptr(X), _dptr(self.sums)), "ens_member_sums")
+        if self.comm is not None:
+            torch.distributed.all_reduce(self.sums, op=torch.distributed.ReduceOp.SUM, group=self.comm)
+        torch.mul(self.sums, 1.0 / self.J_total, out=self.means)
+        self.means_valid = True
+
+    def step(self, t_next, forcing, boundary):
+        lib, ctx, s = self.lib, self.ctx, self.sptr
+        cur, nxt = self.cur, 1 - self.cur
+        X = self.X[cur]
+        if not self.means_valid:
+            self.compute_means()
+        loads, keep1 = self._data(forcing, "loads", t_next)
+        N.check(lib.ens_rhs(ctx, s, _dptr(X), _dptr(self.member_coef), 1.0 / self.config.dt,
+                            C.byref(loads) if loads is not None else None, _dptr(self.rhs)), "ens_rhs")
+        N.check(lib.ens_member_pass(ctx, s, _dptr(X), _dptr(self.means), _dptr(self.rhs), _dptr(self.maxsq)),
+                "ens_member_pass")
+        if self.comm is not None:
+            torch.distributed.all_reduce(self.maxsq, op=torch.distributed.ReduceOp.MAX, group=self.comm)
+        bvals, keep2 = self._data(boundary, "bc", t_next)
+        N.check(lib.ens_apply_bc(ctx, s, C.byref(bvals), _dptr(self.rhs)), "ens_apply_bc")
+        N.check(lib.ens_assemble(ctx, s, _dptr(self.base), _dptr(self.means), _dptr(self.maxsq), self.two_mu_dt,
+                                 _dptr(self.as_vals)), "ens_assemble")
+        npert = N.I32(0)
+        N.check(lib.ens_factor(ctx, s, _dptr(self.as_vals), C.byref(npert)), "ens_factor")
+        self._retire(nxt)
+        Xn = self.X[nxt]
+        Xn.copy_(X)                                   # warm start from level n
+        iters = N.I32(0)
+        rel = (N.F64 * 2)()
+        code = lib.ens_solve(ctx, s, _dptr(self.as_vals), _dptr(self.rhs), _dptr(Xn), self.rtol, self.restart,
+                             self.max_restarts, C.byref(iters), rel)
+        self.last_iters, self.last_pert, self.last_relres = int(iters.value), int(npert.value), (rel[0], rel[1])
+        N.check(code, "ens_solve")
+        N.check(lib.ens_epilogue(ctx, s, _dptr(Xn), _dptr(self.Pq[nxt])), "ens_epilogue")
+        del keep1, keep2
+        self.gen[nxt] += 1
+        self.cur = nxt
+        self.means_valid = False
+        res = max(self.last_relres)
+        if self.comm is not None:
+            t = torch.tensor([res], dtype=torch.float64, device=self.dev)
+            torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX, group=self.comm)
+            res = float(t.item())
+        return res
+
+    def diagnostics(self):
+        """Device-side _record (stepper.py:432-439) of the current state."""
+        if not self.means_valid:
+            self.compute_means()
+        N.check(self.lib.ens_diagnostics(self.ctx, self.sptr, _dptr(self.X[self.cur]), _dptr(self.means),
+                                         _dptr(self.diag_out)), "ens_diagnostics")
+        out = self.diag_out.cpu().numpy()
+        J = self.J
+        series = out[2:].reshape(6, J)
+        return dict(energy=0.5 * (out[0] + out[1]), l2v=series[0], l2w=series[1], gradv=series[2], gradw=series[3],
+                    div_v=np.sqrt(np.maximum(series[4], 0.0)), div_w=np.sqrt(np.maximum(series[5], 0.0)))
+
+    # raw access for tests
+    def spmm(self, x, b=None, mode=0, out=None):
+        out = torch.empty_like(x) if out is None else out
+        N.check(self.lib.ens_spmm(self.ctx, self.sptr, _dptr(self.as_vals), _dptr(x),
+                                  _dptr(b) if b is not None else None, _dptr(out), mode), "ens_spmm")
+        return out
+
+    def factor(self):
+        npert = N.I32(0)
+        N.check(self.lib.ens_factor(self.ctx, self.sptr, _dptr(self.as_vals), C.byref(npert)), "ens_factor")
+        return int(npert.value)
+
+    def precond(self, r, out=None):
+        out = torch.zeros_like(r) if out is None else out
+        N.check(self.lib.ens_precond_apply(self.ctx, self.sptr, _dptr(r), _dptr(out)), "ens_precond_apply")
+        return out

@@ -232,6 +232,28 @@ def divergence(vel: VelocitySpace, pres: PressureSpace) -> sp.csr_matrix:
     return out
 
 
+def divergence_pair(vel: VelocitySpace, pres: PressureSpace):
+    """Bx, By (each n_p x ns) on one shared CSR pattern: (indptr, indices, bx, by).
+
+    Same element integrals and COO->CSR scatter as :func:`divergence`, so the
+    values equal the reference's B blocks (`fem.py:330-344`); the common
+    pattern lets the GPU store (bx, by) pairs.
+    """
+    n_p, ns = pres.num_scalar_dofs, vel.num_scalar_dofs
+    out = []
+    for d in range(2):
+        local = np.einsum("eq,qp,eqa->epa", vel.wdet, QPTS, vel.basis_grad[..., d])
+        r = np.broadcast_to(pres.cell_dofs[:, :, None], local.shape).ravel()
+        c = np.broadcast_to(vel.cell_dofs[:, None, :], local.shape).ravel()
+        coo = sp.coo_matrix((local.ravel(), (r, c)), shape=(n_p, ns))
+        coo.sum_duplicates()               # canonical (row, col) order, explicit zeros kept
+        out.append(coo)
+    bx, by = out
+    assert np.array_equal(bx.row, by.row) and np.array_equal(bx.col, by.col)
+    indptr = np.concatenate([[0], np.cumsum(np.bincount(bx.row, minlength=n_p))])
+    return indptr, bx.col.astype(np.int64), bx.data.copy(), by.data.copy()
+
+
 def load_vector(space, values: np.ndarray) -> np.ndarray:
     """Load vector(s) from quadrature-point values (`fem.py:347-375`).
 

@@ -1,0 +1,321 @@
+"""Reference-compatible time-stepping API, executed by the B200 engine.
+
+Drop-in for the reference's `pkg/src/ensmhd/stepper.py`: same names,
+signatures, argument meaning and error behaviour for the hot path --
+`advance(state, config, disc, forcing, boundary) -> (state, residual)`
+(`stepper.py:360-394`), `run(config, problem, observer, snapshot_steps)`
+(`stepper.py:442-502`), `energy` (`stepper.py:397-401`), `RunReport`
+(`stepper.py:404-429`), `Problem` (`stepper.py:321-341`), `StepFailure`
+(`stepper.py:40-46`), `check_preconditions` (`stepper.py:156-173`) and
+`verify_stability_bound` (`stepper.py:519-579`, host post-processing).
+
+The difference is where the work runs: every per-step quantity (means, eddy
+viscosity, right-hand sides, shared-matrix values, factorisation, solve,
+pressure epilogue, diagnostics) is computed by sm_100a kernels through the C
+ABI (``engine.py``), with the ensemble resident in HBM between steps.  The
+linear solve is a column-batched FGMRES preconditioned by a per-step
+multifrontal LU of the same saddle matrix, converged to a relative true
+residual of ``rtol`` (default 1e-12) per member, so results agree with the
+reference's direct solve far below the 1e-8 parity bar.
+"""
+
+from __future__ import annotations
+
+import logging
+import time as _time
+from dataclasses import dataclass
+from enum import Enum
+
+import numpy as np
+
+from . import _native as N
+from .discretization import Discretization
+from .ensemble import EnsembleConfig, EnsembleState, viscosity_stats
+from .problems import ScaledProfileBoundary, ZeroBoundary, ZeroForcing
+
+logger = logging.getLogger(__name__)
+
+DEFAULT_RTOL = 1e-12
+
+
+class StepKind(Enum):
+    V_STEP = "v"
+    W_STEP = "w"
+
+
+class StepFailure(RuntimeError):
+    """Solver failure wrapped with the step index and sub-step kind (`stepper.py:40-46`)."""
+
+    def __init__(self, step: int, kind: StepKind, cause: Exception):
+        super().__init__(f"step {step} ({kind.value}-substep) failed: {cause}")
+        self.step = step
+        self.kind = kind
+
+
+@dataclass(frozen=True)
+class PreconditionReport:
+    alpha: np.ndarray
+    mu: float
+    bad_members: np.ndarray
+    mu_ok: bool
+    messages: tuple
+
+    @property
+    def ok(self) -> bool:
+        return self.mu_ok and self.bad_members.size == 0
+
+
+def check_preconditions(config: EnsembleConfig) -> PreconditionReport:
+    """alpha_j > 0 and mu > 1/2, warnings only (`stepper.py:156-173`)."""
+    st = viscosity_stats(config)
+    bad = st.nonpositive_alpha
+    mu_ok = config.mu > 0.5
+    msgs = []
+    if bad.size:
+        vals = ", ".join(f"j={j + 1}: alpha={st.alpha[j]:.3e}" for j in bad)
+        msgs.append(f"stability margin alpha_j <= 0 for {bad.size} member(s): {vals}")
+    if not mu_ok:
+        msgs.append(f"eddy tuning mu={config.mu} is not > 1/2")
+    for m in msgs:
+        logger.warning("%s", m)
+    return PreconditionReport(st.alpha, config.mu, bad, mu_ok, tuple(msgs))
+
+
+@dataclass
+class Problem:
+    """Initial data plus forcing and boundary objects (`stepper.py:321-341`)."""
+
+    disc: Discretization
+    initial_v: np.ndarray
+    initial_w: np.ndarray
+    forcing: object
+    boundary: object
+
+    def initial_state(self, config: EnsembleConfig) -> EnsembleState:
+        j = config.num_members
+        zp = np.zeros((j, self.disc.n_pres))
+        return EnsembleState(v=np.array(self.initial_v, dtype=float), w=np.array(self.initial_w, dtype=float),
+                             q=zp, r=zp.copy(), step=0, time=0.0)
+
+
+# ----------------------------------------------------------------------
+# engine cache
+# ----------------------------------------------------------------------
+
+_SOLVER_OPTS = dict(rtol=DEFAULT_RTOL, restart=8, max_restarts=20)
+
+
+def set_solver_options(**kw):
+    """Krylov options for new engines: rtol (true relative residual), restart, max_restarts."""
+    _SOLVER_OPTS.update(kw)
+
+
+def get_engine(disc, config, j0=0, J=None, comm=None, device=None):
+    from .engine import Engine
+    J = config.num_members if J is None else J
+    key = ("b200-engine", config, j0, J, device, id(comm) if comm is not None else None,
+           tuple(sorted(_SOLVER_OPTS.items())))
+    eng = disc._cache.get(key)
+    if eng is None:
+        eng = Engine(disc, config, j0=j0, J=J, device=device, comm=comm, **_SOLVER_OPTS)
+        disc._cache[key] = eng
+    return eng
+
+
+def _device_state_of(state, engine):
+    ds = state.device_state if isinstance(state, EnsembleState) else None
+    return ds if (ds is not None and ds.engine is engine and ds.valid and ds.buf == engine.cur) else None
+
+
+def _step(engine, state, config, forcing, boundary):
+    t_next = state.time + config.dt
+    try:
+        residual = engine.step(t_next, forcing, boundary)
+    except N.NativeError as exc:
+        # which sub-step failed: the one whose residual is above tolerance (V first)
+        kind = StepKind.W_STEP if engine.last_relres[0] <= engine.rtol else StepKind.V_STEP
+        raise StepFailure(state.step, kind, exc) from exc
+    except (ValueError, MemoryError) as exc:
+        raise StepFailure(state.step, StepKind.V_STEP, exc) from exc
+    new = EnsembleState(step=state.step + 1, time=t_next, device=engine.state_handle())
+    return new, residual
+
+
+def advance(state: EnsembleState, config: EnsembleConfig, disc: Discretization, forcing, boundary):
+    """One full time-step for all members (`stepper.py:360-394`).
+
+    Returns (new_state, residual), residual = max over members and both
+    sub-steps of the true relative residual (`linalg.py:111-118`).
+    """
+    engine = get_engine(disc, config)
+    if _device_state_of(state, engine) is None:
+        engine.load_state(state.v, state.w, state.q, state.r)
+    return _step(engine, state, config, forcing, boundary)
+
+
+def energy(state: EnsembleState, disc: Discretization) -> float:
+    """E = 1/2 (||<v>||^2 + ||<w>||^2) (`stepper.py:397-401`)."""
+    mv, mw = state.mean_v, state.mean_w
+    return 0.5 * float(mv @ disc.apply_mass(mv) + mw @ disc.apply_mass(mw))
+
+
+@dataclass
+class RunReport:
+    """Per-step diagnostics (`stepper.py:404-429`); entry 0 is the initial state."""
+
+    times: np.ndarray
+    energy: np.ndarray
+    div_v: np.ndarray
+    div_w: np.ndarray
+    residuals: np.ndarray
+    wall_clock: np.ndarray
+    alpha: np.ndarray
+    mu: float
+    dt: float
+    member_l2v_sq: np.ndarray
+    member_l2w_sq: np.ndarray
+    member_gradv_sq: np.ndarray
+    member_gradw_sq: np.ndarray
+
+    @property
+    def num_steps(self) -> int:
+        return len(self.times) - 1
+
+
+def _record(report, n, engine, comm=None):
+    d = engine.diagnostics()
+    if comm is not None:
+        import torch
+        import torch.distributed as dist
+        parts = [None] * dist.get_world_size(comm)
+        dist.all_gather_object(parts, {k: d[k] for k in ("l2v", "l2w", "gradv", "gradw", "div_v", "div_w")},
+                               group=comm)
+        for k in ("l2v", "l2w", "gradv", "gradw", "div_v", "div_w"):
+            d[k] = np.concatenate([p[k] for p in parts])
+        del torch
+    report.energy[n] = d["energy"]
+    report.div_v[n] = float(np.max(d["div_v"]))
+    report.div_w[n] = float(np.max(d["div_w"]))
+    report.member_l2v_sq[n] = d["l2v"]
+    report.member_l2w_sq[n] = d["l2w"]
+    report.member_gradv_sq[n] = d["gradv"]
+    report.member_gradw_sq[n] = d["gradw"]
+
+
+def member_slice(J_total, rank, world):
+    """Contiguous member shard of one rank."""
+    base, extra = divmod(J_total, world)
+    j0 = rank * base + min(rank, extra)
+    return j0, base + (1 if rank < extra else 0)
+
+
+def run(config: EnsembleConfig, problem: Problem, observer=None, snapshot_steps=(), comm=None, record=True):
+    """Integrate to t_end with M = round(t_end/dt) steps (`stepper.py:442-502`).
+
+    ``comm``: optional torch.distributed process group; members are then sharded
+    contiguously over its ranks (one GPU each) with an allreduce SUM of the
+    member sums and an allreduce MAX of the eddy-viscosity maxima per step.
+    Returns (report, final_state, snapshots); with ``comm`` the final state and
+    snapshots hold this rank's members.
+    """
+    ratio = config.t_end / config.dt
+    m = int(round(ratio))
+    if m < 1 or abs(ratio - m) > 0.5:
+        raise ValueError(f"t_end/dt = {ratio} does not round to a positive step count")
+    if abs(ratio - m) > 1e-9:
+        logger.warning("t_end/dt = %.6g rounded to %d steps", ratio, m)
+    check_preconditions(config)
+    st = viscosity_stats(config)
+    disc = problem.disc
+    J = config.num_members
+    if comm is not None:
+        import torch.distributed as dist
+        j0, jl = member_slice(J, dist.get_rank(comm), dist.get_world_size(comm))
+    else:
+        j0, jl = 0, J
+    engine = get_engine(disc, config, j0=j0, J=jl, comm=comm)
+    shape = (m + 1,)
+    report = RunReport(times=np.arange(m + 1) * config.dt, energy=np.zeros(shape), div_v=np.zeros(shape),
+                       div_w=np.zeros(shape), residuals=np.zeros(shape), wall_clock=np.zeros(shape),
+                       alpha=st.alpha, mu=config.mu, dt=config.dt,
+                       member_l2v_sq=np.zeros((m + 1, J)), member_l2w_sq=np.zeros((m + 1, J)),
+                       member_gradv_sq=np.zeros((m + 1, J)), member_gradw_sq=np.zeros((m + 1, J)))
+    v0 = np.asarray(problem.initial_v, dtype=float)[j0:j0 + jl]
+    w0 = np.asarray(problem.initial_w, dtype=float)[j0:j0 + jl]
+    engine.load_state(v0, w0, None, None)
+    state = EnsembleState(step=0, time=0.0, device=engine.state_handle())
+    if record:
+        _record(report, 0, engine, comm)
+    snaps = {}
+    if 0 in snapshot_steps:
+        snaps[0] = state
+    if observer is not None:
+        observer(0, 0.0, state)
+    for n in range(m):
+        tic = _time.perf_counter()
+        state, res = _step(engine, state, config, problem.forcing, problem.boundary)
+        report.wall_clock[n + 1] = _time.perf_counter() - tic
+        report.residuals[n + 1] = res
+        if record:
+            _record(report, n + 1, engine, comm)
+        if state.step in snapshot_steps:
+            state.device_state.materialize()
+            snaps[state.step] = state
+        if observer is not None:
+            observer(state.step, state.time, state)
+    return report, state, snaps
+
+
+# ----------------------------------------------------------------------
+# stability bound (host post-processing, `stepper.py:519-579`)
+# ----------------------------------------------------------------------
+
+
+@dataclass(frozen=True)
+class StabilityCheck:
+    lhs: np.ndarray
+    rhs: np.ndarray
+    holds: bool
+
+
+def verify_stability_bound(report: RunReport, config: EnsembleConfig, disc: Discretization, forcing=None):
+    """Per-member energy inequality of the scheme (`stepper.py:519-555`)."""
+    st = viscosity_stats(config)
+    m = report.num_steps
+    hv = 0.5 * (st.nu_bar + st.nu_m_bar)
+    hist = report.member_gradv_sq[:m].sum(axis=0) + report.member_gradw_sq[:m].sum(axis=0)
+    lhs = (report.member_l2v_sq[m] + report.member_l2w_sq[m]
+           + hv * config.dt * (report.member_gradv_sq[m] + report.member_gradw_sq[m])
+           + 0.5 * st.alpha * config.dt * hist)
+    rhs = (report.member_l2v_sq[0] + report.member_l2w_sq[0]
+           + hv * config.dt * (report.member_gradv_sq[0] + report.member_gradw_sq[0]))
+    if forcing is not None:
+        rhs = rhs + (2.0 * config.dt / st.alpha) * _dual_sums(report, config, disc, forcing)
+    return StabilityCheck(lhs, rhs, bool(np.all(lhs <= rhs * (1.0 + 1e-8))))
+
+
+def _dual_sums(report, config, disc, forcing):
+    """sum_n ||f1||_-1^2 + ||f2||_-1^2 with the interior scalar stiffness (`stepper.py:558-579`)."""
+    import scipy.sparse.linalg as spla
+    interior = disc.velocity.interior_scalar_dofs()
+    ns = disc.n_scalar
+    lu = None
+    total = np.zeros(config.num_members)
+    for n in range(report.num_steps):
+        t = report.times[n + 1]
+        for load in forcing.loads(t, disc, config):
+            if load is None:
+                continue
+            if lu is None:
+                lu = spla.splu(disc.stiff_s[interior][:, interior].tocsc())
+            comp = np.asarray(load).reshape(config.num_members, 2, ns)[:, :, interior]
+            flat = comp.reshape(-1, interior.size).T
+            total += np.einsum("ij,ij->j", flat, lu.solve(flat)).reshape(config.num_members, 2).sum(axis=1)
+    return total
+
+
+__all__ = [
+    "Discretization", "Problem", "RunReport", "StepKind", "StepFailure", "PreconditionReport",
+    "StabilityCheck", "advance", "run", "energy", "check_preconditions", "verify_stability_bound",
+    "ZeroForcing", "ZeroBoundary", "ScaledProfileBoundary", "member_slice", "set_solver_options",
+]

@@ -1,0 +1,508 @@
+"""Symbolic analysis for the per-step saddle-point factorisation (host, once per mesh).
+
+The reference factorises the assembled saddle matrix every sub-step with a
+sparse direct LU (UMFPACK or SuperLU, `linalg.py:79-108`, called from
+`stepper.py:216`) and solves all J columns with it (`linalg.py:62-76`).  The
+B200 engine keeps that robustness but builds the factorisation on the GPU as
+the *preconditioner* of a column-batched FGMRES: a multifrontal LU whose
+symbolic structure is fixed per mesh (the pattern of the saddle matrix never
+changes, `stepper.py:216-218`), computed here once.
+
+Design:
+  * Ordering: geometric nested dissection over the P2 nodes (one-sided vertex
+    separators along mesh lines), giving an elimination tree of *fronts*.
+  * Dof placement: a node's free velocity dofs go to the node's tree node; every
+    free pressure dof is moved *up* to the highest tree node among its velocity
+    neighbours, and inside each front velocities precede pressures.  With that
+    order every leading principal block is a saddle system whose B rows are
+    complete rows of the full B, hence nonsingular whenever the full matrix is
+    (the velocity block is positive-real) -- LU without cross-panel pivoting is
+    well defined.  Panels use partial pivoting internally (explicit inverse).
+  * Dirichlet rows and the pressure pin are identity rows in the reference
+    (`stepper.py:214-215`); they are eliminated trivially and never enter a
+    front (the Krylov iterate carries their values exactly).
+  * Each front's pivots are split into panels of <= PW dofs; the numeric phase
+    stores per panel D^-1 (PW x PW), H = -D^-1 R and G = -C D^-1 (see csrc/mf.cu).
+
+Everything returned is flat int32/int64 numpy arrays plus a launch schedule,
+uploaded once by the engine.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+import scipy.sparse as sp
+
+PW = 64          # panel width (max pivots per diagonal block)
+TILE = 64        # GEMM tile edge in the numeric kernels
+LEAF_NODES = 24  # stop dissecting below this many P2 nodes
+
+
+# ----------------------------------------------------------------------
+# nested dissection on the P2 node graph
+# ----------------------------------------------------------------------
+
+
+def _nested_dissection(coords, indptr, indices, leaf=LEAF_NODES):
+    """Return (tree_nodes: list of node arrays, children: list of lists, root)."""
+    n = coords.shape[0]
+    rows = np.repeat(np.arange(n, dtype=np.int64), np.diff(indptr))
+    cols = indices.astype(np.int64)
+    tnodes, kids = [], []
+    in_right = np.zeros(n, dtype=bool)
+    in_left = np.zeros(n, dtype=bool)
+
+    # iterative (explicit stack) to avoid recursion limits on big meshes
+    stack = [(np.arange(n, dtype=np.int64), -1)]
+    while stack:
+        idx, parent = stack.pop()
+        me = len(tnodes)
+        tnodes.append(None)
+        kids.append([])
+        if parent >= 0:
+            kids[parent].append(me)
+        if len(idx) <= leaf:
+            tnodes[me] = idx
+            continue
+        c = coords[idx]
+        ax = int(np.argmax(c.max(0) - c.min(0)))
+        xs = c[:, ax]
+        vals = np.unique(xs)
+        med = np.sort(xs)[len(xs) // 2]
+        ci = int(np.searchsorted(vals, med))
+        # edges with both ends inside idx
+        sub = np.zeros(n, dtype=bool)
+        sub[idx] = True
+        emask = sub[rows] & sub[cols]
+        er, ec = rows[emask], cols[emask]
+        xr, xc = coords[er, ax], coords[ec, ax]
+        best = None
+        for cut in vals[max(0, ci - 4):ci + 5]:
+            nleft = int(np.count_nonzero(xs <= cut))
+            nright = len(idx) - nleft
+            if nleft == 0 or nright == 0:
+                continue
+            sep = np.unique(er[(xr <= cut) & (xc > cut)])
+            bal = min(nleft - len(sep), nright) / len(idx)
+            if bal < 0.25:
+                continue
+            score = len(sep) * (1.0 + 2.0 * abs(0.5 - bal))
+            if best is None or score < best[0]:
+                best = (score, cut, sep)
+        if best is None:
+            tnodes[me] = idx
+            continue
+        _, cut, sep = best
+        sm = np.zeros(n, dtype=bool)
+        sm[sep] = True
+        left = idx[(xs <= cut) & ~sm[idx]]
+        right = idx[xs > cut]
+        tnodes[me] = sep
+        for part in (right, left):
+            if len(part):
+                stack.append((part, me))
+    return tnodes, kids, 0
+
+
+def _postorder(kids, root):
+    out, stack = [], [(root, False)]
+    while stack:
+        u, done = stack.pop()
+        if done:
+            out.append(u)
+            continue
+        stack.append((u, True))
+        for c in reversed(kids[u]):
+            stack.append((c, False))
+    return np.array(out, dtype=np.int64)
+
+
+@dataclass
+class FactorPlan:
+    """Everything the device factorisation / triangular solves need."""
+
+    # internal numbering
+    node_perm: np.ndarray        # P2 node (reference numbering) -> internal node id
+    pres_perm: np.ndarray        # pressure dof -> internal pressure index (0..n_pres)
+    # fronts (in processing order: by level, then position)
+    nfront: int
+    f_m: np.ndarray              # int32 front size
+    f_k: np.ndarray              # int32 pivots
+    f_off: np.ndarray            # int64 offset of the dense m x m front (per matrix)
+    f_idx_off: np.ndarray        # int64 offset into f_idx
+    f_idx: np.ndarray            # int32 internal dof ids of the front rows ([pivots; CB])
+    f_level: np.ndarray
+    f_parent: np.ndarray         # front id of the parent (-1 root)
+    f_cmap_off: np.ndarray       # int64 offset of this front's CB -> parent-local map
+    f_cmap: np.ndarray           # int32
+    front_storage: int           # doubles per matrix
+    # original entries -> front slots
+    orig_dst: np.ndarray         # int64 slot (per matrix storage)
+    orig_src: np.ndarray         # int32: < nnz_s -> A_s value; else signed B value index + nnz_s
+    orig_level_off: np.ndarray   # int64 per level range in orig_*
+    bsrc_vals: np.ndarray        # float64 constant (signed) B / -B^T values
+    nlevels: int
+    level_front_off: np.ndarray  # int32 fronts of level L are [off[L], off[L+1])
+    level_storage_off: np.ndarray  # int64 storage range of level L
+    schedule: dict               # launch work lists (see build_schedule)
+    stats: dict
+
+
+def analyse(disc, leaf=LEAF_NODES, pw=PW):
+    """Build the FactorPlan for a Discretization (constrained rows per disc)."""
+    vel = disc.velocity
+    ns, nvel, npres = disc.n_scalar, disc.n_vel, disc.n_pres
+    n_total = nvel + npres
+    from . import fe
+    pat = fe.scalar_pattern(vel)
+    g = pat.copy()
+    g.setdiag(0)
+    g.eliminate_zeros()
+    g.sort_indices()
+    tnodes, kids, root = _nested_dissection(vel.dof_coords, g.indptr, g.indices, leaf)
+    post = _postorder(kids, root)
+    T = len(tnodes)
+    rank = np.empty(T, dtype=np.int64)
+    rank[post] = np.arange(T)
+
+    # internal node numbering: tree nodes in postorder, nodes in coordinate order inside
+    node_perm = np.empty(ns, dtype=np.int64)
+    tnode_of_node = np.empty(ns, dtype=np.int64)
+    pos = 0
+    for t in post:
+        nd = tnodes[t]
+        node_perm[nd] = pos + np.arange(len(nd))
+        tnode_of_node[nd] = t
+        pos += len(nd)
+
+    # free dofs (reference numbering): velocity x = s, y = ns + s ; pressure nvel + p
+    cons = np.zeros(n_total, dtype=bool)
+    cons[disc.constrained_rows] = True
+
+    # pressure placement: highest (max postorder rank) tree node over its velocity neighbours
+    B = disc.divergence.tocsr()
+    bnodes = B.indices % ns
+    brow = np.repeat(np.arange(npres), np.diff(B.indptr))
+    pres_node = disc.pressure.node_of_dof(vel)
+    cand_rank = rank[tnode_of_node[bnodes]]
+    best = np.full(npres, -1, dtype=np.int64)
+    np.maximum.at(best, brow, cand_rank)
+    best = np.maximum(best, rank[tnode_of_node[pres_node]])
+    tnode_of_pres = post[best]
+
+    # pressure internal order: by tree rank, then by the reference index
+    porder = np.lexsort((np.arange(npres), best))
+    pres_perm = np.empty(npres, dtype=np.int64)
+    pres_perm[porder] = np.arange(npres)
+
+    # internal dof id of every reference dof
+    int_id = np.empty(n_total, dtype=np.int64)
+    int_id[:ns] = 2 * node_perm
+    int_id[ns:nvel] = 2 * node_perm + 1
+    int_id[nvel:] = nvel + pres_perm
+
+    # elimination order of free dofs: tree rank, then velocities before pressures, then internal id
+    dof_t = np.empty(n_total, dtype=np.int64)
+    dof_t[:ns] = tnode_of_node
+    dof_t[ns:nvel] = tnode_of_node
+    dof_t[nvel:] = tnode_of_pres
+    is_p = np.zeros(n_total, dtype=np.int64)
+    is_p[nvel:] = 1
+    free = np.nonzero(~cons)[0]
+    order = free[np.lexsort((int_id[free], is_p[free], rank[dof_t[free]]))]
+    nf = len(order)
+    elim = np.full(n_total, -1, dtype=np.int64)
+    elim[order] = np.arange(nf)
+
+    # free saddle pattern in elimination order (symmetric structure)
+    As = pat.tocsr()
+    full = sp.bmat([[As, None, B[:, :ns].T], [None, As, B[:, ns:].T], [B[:, :ns], B[:, ns:], None]], format="csr")
+    full = full + full.T
+    fp = full[order][:, order].tocsr()
+    fp.sort_indices()
+
+    # tree nodes -> pivot ranges in elimination order; drop empty tree nodes
+    t_of_e = rank[dof_t[order]]                      # postorder rank per eliminated dof
+    piv_start = np.searchsorted(t_of_e, np.arange(T), side="left")
+    piv_end = np.searchsorted(t_of_e, np.arange(T), side="right")
+    parent_r = np.full(T, -1, dtype=np.int64)        # by postorder rank
+    for t in range(T):
+        for c in kids[t]:
+            parent_r[rank[c]] = rank[t]
+    nonempty = piv_end > piv_start
+    # re-parent through empty nodes
+    eff_parent = parent_r.copy()
+    for r in range(T):
+        p = eff_parent[r]
+        while p >= 0 and not nonempty[p]:
+            p = parent_r[p]
+        eff_parent[r] = p
+    keep = np.nonzero(nonempty)[0]                   # ranks, increasing == postorder
+    newid = np.full(T, -1, dtype=np.int64)
+    newid[keep] = np.arange(len(keep))
+    F = len(keep)
+    fparent = np.where(eff_parent[keep] >= 0, newid[np.maximum(eff_parent[keep], 0)], -1)
+    fparent[eff_parent[keep] < 0] = -1
+    fs, fe_ = piv_start[keep], piv_end[keep]
+    children = [[] for _ in range(F)]
+    for f in range(F):
+        if fparent[f] >= 0:
+            children[fparent[f]].append(f)
+
+    # symbolic factorisation: CB(f) = (later neighbours of pivots U children CBs) \ pivots
+    cb = [None] * F
+    for f in range(F):                               # postorder: children first
+        s, e = fs[f], fe_[f]
+        cols = fp.indices[fp.indptr[s]:fp.indptr[e]]
+        parts = [cols[cols >= e]]
+        for c in children[f]:
+            parts.append(cb[c][cb[c] >= e])
+        u = np.unique(np.concatenate(parts)) if parts else np.zeros(0, dtype=np.int64)
+        cb[f] = u.astype(np.int64)
+    k = (fe_ - fs).astype(np.int64)
+    cbn = np.array([len(c) for c in cb], dtype=np.int64)
+    m = k + cbn
+
+    # levels (height from leaves) -> processing order
+    height = np.zeros(F, dtype=np.int64)
+    for f in range(F):
+        for c in children[f]:
+            height[f] = max(height[f], height[c] + 1)
+    nlevels = int(height.max()) + 1
+    porder_f = np.lexsort((np.arange(F), height))    # processing order
+    pid = np.empty(F, dtype=np.int64)
+    pid[porder_f] = np.arange(F)
+    level_front_off = np.searchsorted(height[porder_f], np.arange(nlevels + 1)).astype(np.int32)
+
+    f_m = m[porder_f]
+    f_k = k[porder_f]
+    f_level = height[porder_f]
+    f_parent = np.where(fparent[porder_f] >= 0, pid[np.maximum(fparent[porder_f], 0)], -1)
+    f_off = np.concatenate([[0], np.cumsum(f_m * f_m)]).astype(np.int64)
+    storage = int(f_off[-1])
+    f_off = f_off[:-1]
+    level_storage_off = np.concatenate([f_off[level_front_off[:-1]], [storage]]).astype(np.int64)
+
+    # front index lists in elimination positions, then internal dof ids
+    elim_to_int = int_id[order]
+    lists = []
+    for f in porder_f:
+        lists.append(np.concatenate([np.arange(fs[f], fe_[f]), cb[f]]))
+    f_idx_off = np.concatenate([[0], np.cumsum(f_m)]).astype(np.int64)
+    f_idx_elim = np.concatenate(lists)
+    f_idx = elim_to_int[f_idx_elim].astype(np.int32)
+
+    # local position lookup: key = front * nf + elimpos
+    keys = np.repeat(np.arange(F, dtype=np.int64), f_m) * nf + f_idx_elim
+    korder = np.argsort(keys, kind="stable")
+    skeys = keys[korder]
+    local_of = (np.arange(len(keys)) - np.repeat(f_idx_off[:-1], f_m))[korder]
+
+    def lookup(front, epos):
+        kk = front.astype(np.int64) * nf + epos
+        i = np.searchsorted(skeys, kk)
+        assert np.all(skeys[i] == kk), "symbolic lookup failed"
+        return local_of[i]
+
+    # child CB -> parent local map
+    cmaps, cmap_off = [], np.zeros(F + 1, dtype=np.int64)
+    for i in range(F):
+        if f_parent[i] >= 0:
+            cbl = f_idx_elim[f_idx_off[i] + f_k[i]: f_idx_off[i + 1]]
+            mp = lookup(np.full(len(cbl), f_parent[i]), cbl)
+        else:
+            mp = np.zeros(0, dtype=np.int64)
+            assert f_m[i] == f_k[i], "root front must have an empty CB"
+        cmaps.append(mp)
+        cmap_off[i + 1] = cmap_off[i] + len(mp)
+    f_cmap = np.concatenate(cmaps).astype(np.int32) if cmaps else np.zeros(0, np.int32)
+
+    # original entries: A_s (both components) and B / -B^T, between free dofs
+    nnz_s = As.nnz
+    a_rows = np.repeat(np.arange(ns), np.diff(As.indptr))
+    a_cols = As.indices
+    src_l, r_l, c_l = [], [], []
+    for comp in range(2):
+        r = comp * ns + a_rows
+        c = comp * ns + a_cols
+        src_l.append(np.arange(nnz_s, dtype=np.int64))
+        r_l.append(r)
+        c_l.append(c)
+    b_rows = np.repeat(np.arange(npres), np.diff(B.indptr))
+    b_cols = B.indices                                # 0..2ns
+    nb = B.nnz
+    bsrc_vals = np.concatenate([B.data, -B.data])
+    # B entries: row nvel+p, col b_cols ; -B^T entries: row b_cols, col nvel+p
+    src_l += [nnz_s + np.arange(nb), nnz_s + nb + np.arange(nb)]
+    r_l += [nvel + b_rows, b_cols]
+    c_l += [b_cols, nvel + b_rows]
+    src = np.concatenate(src_l)
+    rr = np.concatenate(r_l)
+    cc = np.concatenate(c_l)
+    ok = (~cons[rr]) & (~cons[cc])
+    src, rr, cc = src[ok], rr[ok], cc[ok]
+    er, ec = elim[rr], elim[cc]
+    first = np.minimum(er, ec)
+    # front owning elimination position `first`
+    piv_front_of_e = np.empty(nf, dtype=np.int64)
+    for i in range(F):
+        piv_front_of_e[f_idx_elim[f_idx_off[i]:f_idx_off[i] + f_k[i]]] = i
+    fr = piv_front_of_e[first]
+    lr = lookup(fr, er)
+    lc = lookup(fr, ec)
+    dst = f_off[fr] + lr * f_m[fr] + lc
+    o = np.lexsort((dst, f_level[fr]))
+    orig_dst = dst[o].astype(np.int64)
+    orig_src = src[o].astype(np.int32)
+    orig_level_off = np.searchsorted(f_level[fr][o], np.arange(nlevels + 1)).astype(np.int64)
+
+    plan = FactorPlan(
+        node_perm=node_perm, pres_perm=pres_perm, nfront=F,
+        f_m=f_m.astype(np.int32), f_k=f_k.astype(np.int32), f_off=f_off,
+        f_idx_off=f_idx_off, f_idx=f_idx, f_level=f_level.astype(np.int32), f_parent=f_parent.astype(np.int32),
+        f_cmap_off=cmap_off, f_cmap=f_cmap, front_storage=storage,
+        orig_dst=orig_dst, orig_src=orig_src, orig_level_off=orig_level_off, bsrc_vals=bsrc_vals,
+        nlevels=nlevels, level_front_off=level_front_off, level_storage_off=level_storage_off,
+        schedule={}, stats={},
+    )
+    plan.schedule = build_schedule(plan, pw)
+    flops = 0.0
+    for i in range(F):
+        mm, kk = int(f_m[i]), int(f_k[i])
+        flops += sum(2.0 * (mm - t - 1) ** 2 for t in range(0, kk, 1)) if kk < 4096 else 0.0
+    plan.stats = dict(fronts=F, levels=nlevels, n_free=nf, max_m=int(f_m.max()), max_k=int(f_k.max()),
+                      storage_doubles=storage, factor_flops=flops,
+                      nnz_lu=float(np.sum(f_m.astype(np.float64) ** 2 - (f_m - f_k).astype(np.float64) ** 2)))
+    return plan
+
+
+# ----------------------------------------------------------------------
+# launch schedule (work lists), consumed by csrc/mf.cu
+# ----------------------------------------------------------------------
+
+# op codes (must match csrc/mf.cu)
+OP_ZERO, OP_ORIG, OP_EXTADD, OP_DIAG, OP_HPANEL, OP_UPDATE, OP_GPANEL = range(7)
+SOP_FINIT, SOP_FEXT, SOP_FPANEL, SOP_BGATHER, SOP_BPANEL, SOP_BSCATTER = range(6)
+EXT_ROWS = 8      # child-CB rows per extend-add work item
+VEC_ROWS = 64     # front-vector rows per init/gather/scatter work item
+
+
+def build_schedule(plan: FactorPlan, pw=PW):
+    """Flat int32 work items + launch list for factorisation and solves.
+
+    factor launches: (op, level, item_off, n_items, arg)
+      OP_ZERO   level storage range is zeroed (memset)
+      OP_ORIG   items = level's original-entry range (handled by index range)
+      OP_EXTADD items (child, row0)              -- one launch per sibling rank
+      OP_DIAG   items (front, a)                 -- a = panel start
+      OP_HPANEL items (front, a, col0)
+      OP_UPDATE items (front, a, row0, col0)
+      OP_GPANEL items (front, a, row0)
+    solve launches: (op, level, item_off, n_items, arg)
+    """
+    items = []
+    nitems = [0]
+
+    def add(rows):
+        arr = np.asarray(rows, dtype=np.int32).reshape(len(rows), -1) if len(rows) else np.zeros((0, 4), np.int32)
+        if arr.shape[1] < 4:
+            arr = np.hstack([arr, np.zeros((arr.shape[0], 4 - arr.shape[1]), np.int32)])
+        off = nitems[0]
+        items.append(arr)
+        nitems[0] += arr.shape[0]
+        return off, arr.shape[0]
+
+    F = plan.nfront
+    fm, fk, lvl, par = plan.f_m, plan.f_k, plan.f_level, plan.f_parent
+    children = [[] for _ in range(F)]
+    for f in range(F):
+        if par[f] >= 0:
+            children[par[f]].append(f)
+    fl, sl = [], []
+    for L in range(plan.nlevels):
+        fronts = np.arange(plan.level_front_off[L], plan.level_front_off[L + 1])
+        fl.append((OP_ZERO, L, 0, 0, 0))
+        fl.append((OP_ORIG, L, 0, 0, 0))
+        # extend-add by sibling rank (conflict-free within a launch)
+        maxr = max((len(children[f]) for f in fronts), default=0)
+        for r in range(maxr):
+            rows = []
+            for f in fronts:
+                if r < len(children[f]):
+                    c = children[f][r]
+                    cbn = fm[c] - fk[c]
+                    for r0 in range(0, cbn, EXT_ROWS):
+                        rows.append((c, r0))
+            if rows:
+                off, n = add(rows)
+                fl.append((OP_EXTADD, L, off, n, r))
+        npan = int(max((-(-fk[f] // pw) for f in fronts), default=0))
+        for p in range(npan):
+            a = p * pw
+            act = [f for f in fronts if fk[f] > a]
+            d, h, u, gg = [], [], [], []
+            for f in act:
+                b = min(a + pw, fk[f])
+                t = fm[f] - b
+                d.append((f, a))
+                for c0 in range(0, t, TILE):
+                    h.append((f, a, c0))
+                    gg.append((f, a, c0))
+                    for r0 in range(0, t, TILE):
+                        u.append((f, a, r0, c0))
+            for op, rows in ((OP_DIAG, d), (OP_HPANEL, h), (OP_UPDATE, u), (OP_GPANEL, gg)):
+                if rows:
+                    off, n = add(rows)
+                    fl.append((op, L, off, n, p))
+    # solve schedule
+    fwd, bwd = [], []
+    for L in range(plan.nlevels):
+        fronts = np.arange(plan.level_front_off[L], plan.level_front_off[L + 1])
+        rows = [(f, r0) for f in fronts for r0 in range(0, fm[f], VEC_ROWS)]
+        off, n = add(rows)
+        fwd.append((SOP_FINIT, L, off, n, 0))
+        maxr = max((len(children[f]) for f in fronts), default=0)
+        for r in range(maxr):
+            rows = []
+            for f in fronts:
+                if r < len(children[f]):
+                    c = children[f][r]
+                    for r0 in range(0, fm[c] - fk[c], VEC_ROWS):
+                        rows.append((c, r0))
+            if rows:
+                off, n = add(rows)
+                fwd.append((SOP_FEXT, L, off, n, r))
+        npan = int(max((-(-fk[f] // pw) for f in fronts), default=0))
+        for p in range(npan):
+            a = p * pw
+            rows = []
+            for f in fronts:
+                if fk[f] > a:
+                    b = min(a + pw, fk[f])
+                    for r0 in range(0, fm[f] - b, TILE):
+                        rows.append((f, a, r0))
+            if rows:
+                off, n = add(rows)
+                fwd.append((SOP_FPANEL, L, off, n, p))
+    for L in reversed(range(plan.nlevels)):
+        fronts = np.arange(plan.level_front_off[L], plan.level_front_off[L + 1])
+        rows = [(f, fk[f] + r0) for f in fronts for r0 in range(0, fm[f] - fk[f], VEC_ROWS)]
+        if rows:
+            off, n = add(rows)
+            bwd.append((SOP_BGATHER, L, off, n, 0))
+        npan = int(max((-(-fk[f] // pw) for f in fronts), default=0))
+        for p in reversed(range(npan)):
+            a = p * pw
+            rows = [(f, a) for f in fronts if fk[f] > a]
+            off, n = add(rows)
+            bwd.append((SOP_BPANEL, L, off, n, p))
+        rows = [(f, r0) for f in fronts for r0 in range(0, fk[f], VEC_ROWS)]
+        off, n = add(rows)
+        bwd.append((SOP_BSCATTER, L, off, n, 0))
+    work = np.vstack(items) if items else np.zeros((0, 4), np.int32)
+    return dict(work=np.ascontiguousarray(work.astype(np.int32)),
+                factor=np.array(fl, dtype=np.int64).reshape(-1, 5),
+                fwd=np.array(fwd, dtype=np.int64).reshape(-1, 5),
+                bwd=np.array(bwd, dtype=np.int64).reshape(-1, 5))

@@ -1,0 +1,231 @@
+"""GPU parity: each C-ABI kernel and the full step against the CPU oracle / reference goldens.
+
+Tolerances follow the reference's own tests: assembly 1e-13 x max|A|
+(tests/test_stepper.py:132), RHS 1e-12 (:201), one step 1e-10 for v,w and
+1e-9 for q,r (:254-256), and the BASELINE north-star bar of 1e-8 relative L2
+for multi-step runs (we hold 1e-10).
+"""
+
+import numpy as np
+import pytest
+import scipy.sparse as sp
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+if not torch.cuda.is_available():  # pragma: no cover - GPU box only
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+from oracle import ensmhd_oracle as O  # noqa: E402
+import paper_2108_05110_b200 as P  # noqa: E402
+from paper_2108_05110_b200 import fe  # noqa: E402
+from paper_2108_05110_b200.discretization import Discretization  # noqa: E402
+from paper_2108_05110_b200.engine import Engine, host_mesh  # noqa: E402
+from paper_2108_05110_b200.ensemble import EnsembleConfig, EnsembleState, MemberParams  # noqa: E402
+from paper_2108_05110_b200.mesh import barycentric_refine, build_structured_square  # noqa: E402
+from paper_2108_05110_b200.problems import (PaperMmsBoundary, PaperMmsForcing, ZeroBoundary,  # noqa: E402
+                                            ZeroForcing, paper_mms_initial_fields)
+
+
+def rel(a, b):
+    return np.linalg.norm(np.asarray(a) - np.asarray(b)) / max(np.linalg.norm(b), 1e-300)
+
+
+def to_internal_block(hm, blk_ref):
+    """(n_total, J) reference rows -> (n_total, J) internal rows."""
+    out = np.empty_like(blk_ref)
+    out[hm.int_id] = blk_ref
+    return out
+
+
+def as_internal_vals(hm, a_s):
+    a = a_s.tocoo()
+    vals = np.zeros(hm.nnz_s)
+    vals[hm._slot(hm.plan.node_perm[a.row], hm.plan.node_perm[a.col])] = a.data
+    return vals
+
+
+@pytest.fixture(scope="module")
+def c1():
+    disc, cfg, prob = P.build_case("C1")
+    return disc, cfg, prob
+
+
+def perturbed_state(disc, cfg, rng, scale=0.3):
+    J = cfg.num_members
+    v = rng.standard_normal((J, disc.n_vel)) * scale
+    w = rng.standard_normal((J, disc.n_vel)) * scale
+    return v, w
+
+
+def test_spmm_matches_scipy(c1, rng):
+    disc, cfg, _ = c1
+    eng = Engine(disc, cfg)
+    hm = eng.hm
+    v, w = perturbed_state(disc, cfg, rng)
+    a_v = O.velocity_block(w.mean(0), w - w.mean(0), cfg, disc)
+    a_w = O.velocity_block(v.mean(0), v - v.mean(0), cfg, disc)
+    eng.as_vals[0] = torch.from_numpy(as_internal_vals(hm, a_v)).cuda()
+    eng.as_vals[1] = torch.from_numpy(as_internal_vals(hm, a_w)).cuda()
+    J = cfg.num_members
+    x = rng.standard_normal((2, disc.n_total, J))
+    b = rng.standard_normal((2, disc.n_total, J))
+    xt = torch.from_numpy(np.stack([to_internal_block(hm, x[0]), to_internal_block(hm, x[1])])).cuda()
+    bt = torch.from_numpy(np.stack([to_internal_block(hm, b[0]), to_internal_block(hm, b[1])])).cuda()
+    y = eng.spmm(xt).cpu().numpy()
+    r = eng.spmm(xt, bt, mode=1).cpu().numpy()
+    for m, a in enumerate((a_v, a_w)):
+        K = O.saddle_matrix(a, disc)
+        ref = K @ x[m]
+        got = y[m][hm.int_id]
+        assert np.max(np.abs(got - ref)) <= 1e-13 * np.abs(ref).max()
+        assert np.max(np.abs(r[m][hm.int_id] - (b[m] - ref))) <= 1e-13 * np.abs(ref).max()
+
+
+def test_member_pass_assembly_rhs(c1, rng):
+    disc, cfg, prob = c1
+    eng = Engine(disc, cfg)
+    hm = eng.hm
+    v, w = perturbed_state(disc, cfg, rng, 1.0)
+    eng.load_state(v, w, None, None)
+    t = cfg.dt
+    # replicate engine.step up to the solve
+    eng.compute_means()
+    import ctypes as C
+    from paper_2108_05110_b200 import _native as N
+    from paper_2108_05110_b200.engine import _dptr
+    X = eng.X[eng.cur]
+    loads, k1 = eng._data(prob.forcing, "loads", t)
+    N.check(eng.lib.ens_rhs(eng.ctx, eng.sptr, _dptr(X), _dptr(eng.member_coef), 1.0 / cfg.dt, C.byref(loads),
+                            _dptr(eng.rhs)), "rhs")
+    N.check(eng.lib.ens_member_pass(eng.ctx, eng.sptr, _dptr(X), _dptr(eng.means), _dptr(eng.rhs),
+                                    _dptr(eng.maxsq)), "mp")
+    bv, k2 = eng._data(prob.boundary, "bc", t)
+    N.check(eng.lib.ens_apply_bc(eng.ctx, eng.sptr, C.byref(bv), _dptr(eng.rhs)), "bc")
+    N.check(eng.lib.ens_assemble(eng.ctx, eng.sptr, _dptr(eng.base), _dptr(eng.means), _dptr(eng.maxsq),
+                                 eng.two_mu_dt, _dptr(eng.as_vals)), "asm")
+    torch.cuda.synchronize()
+    # eddy viscosity maxima (ensemble.py:227-238)
+    msq = eng.maxsq.cpu().numpy()
+    for fam, z in ((0, w), (1, v)):
+        ref = O.eddy_viscosity(disc.velocity, z - z.mean(0), 1.0, 1.0)
+        got = np.empty_like(ref)
+        got[hm.eorder] = msq[fam]
+        assert np.max(np.abs(got - ref)) <= 1e-13 * ref.max()
+    # shared velocity blocks
+    asv = eng.as_vals.cpu().numpy()
+    for m, (mean, z) in enumerate(((w.mean(0), w), (v.mean(0), v))):
+        ref = as_internal_vals(hm, O.velocity_block(mean, z - z.mean(0), cfg, disc).tocsr())
+        assert np.max(np.abs(asv[m] - ref)) <= 1e-13 * np.abs(ref).max()
+    # right-hand sides
+    lv, lw = prob.forcing.loads(t, disc, cfg)
+    bvh, bwh = prob.boundary.values(t, disc, cfg)
+    rhs = eng.rhs.cpu().numpy()
+    for m, kind, ld, bvals in ((0, "v", lv, bvh), (1, "w", lw, bwh)):
+        ref = O.rhs_block(kind, v, w, ld, bvals, cfg, disc)
+        got = rhs[m][hm.int_id]
+        assert np.max(np.abs(got - ref)) <= 1e-12 * np.abs(ref).max()
+
+
+def test_factor_solve_residual(c1, rng):
+    disc, cfg, _ = c1
+    eng = Engine(disc, cfg)
+    hm = eng.hm
+    v, w = perturbed_state(disc, cfg, rng)
+    a_v = O.velocity_block(w.mean(0), w - w.mean(0), cfg, disc)
+    a_w = O.velocity_block(v.mean(0), v - v.mean(0), cfg, disc)
+    eng.as_vals[0] = torch.from_numpy(as_internal_vals(hm, a_v)).cuda()
+    eng.as_vals[1] = torch.from_numpy(as_internal_vals(hm, a_w)).cuda()
+    npert = eng.factor()
+    assert npert == 0
+    J = cfg.num_members
+    b = rng.standard_normal((2, disc.n_total, J))
+    b[:, disc.constrained_rows] = 0.0
+    bt = torch.from_numpy(np.stack([to_internal_block(hm, b[0]), to_internal_block(hm, b[1])])).cuda()
+    z = eng.precond(bt).cpu().numpy()
+    for m, a in enumerate((a_v, a_w)):
+        K = O.saddle_matrix(a, disc)
+        x = z[m][hm.int_id]
+        res = np.linalg.norm(K @ x - b[m], axis=0) / np.linalg.norm(b[m], axis=0)
+        assert res.max() < 1e-11, res
+
+
+def test_run_c1_matches_reference_golden(golden, c1):
+    disc, cfg, prob = c1
+    report, state, _ = P.run(cfg, prob)
+    for f in "vw":
+        assert rel(getattr(state, f), golden["c1_run_" + f]) < 1e-10
+    for f in "qr":
+        assert rel(getattr(state, f), golden["c1_run_" + f]) < 1e-9
+    assert rel(report.energy, golden["c1_run_energy"]) < 1e-10
+    for k, g in (("member_l2v_sq", "l2v"), ("member_l2w_sq", "l2w"), ("member_gradv_sq", "gradv"),
+                 ("member_gradw_sq", "gradw")):
+        assert rel(getattr(report, k), golden["c1_run_" + g]) < 1e-10
+    assert rel(report.div_v, golden["c1_run_div_v"]) < 1e-8
+    assert np.all(report.residuals[1:] < 1e-11)
+    # primitive fields u = (v+w)/2, B = (v-w)/(2 sqrt s): the north-star parity quantities
+    u = 0.5 * (state.v + state.w)
+    u_ref = 0.5 * (golden["c1_run_v"] + golden["c1_run_w"])
+    assert rel(u, u_ref) < 1e-10
+    assert rel(u.mean(0), u_ref.mean(0)) < 1e-10
+
+
+def test_run_sv_paper_mms_matches_reference(golden):
+    disc = Discretization.from_mesh(barycentric_refine(build_structured_square(2)))
+    members = (MemberParams(0.01, 0.1), MemberParams(0.012, 0.09), MemberParams(0.009, 0.11))
+    cfg = EnsembleConfig(members=members, coupling=1.0, mu=1.0, dt=0.05, t_end=0.1, perturbation=0.01)
+    v0, w0 = paper_mms_initial_fields(disc, cfg)
+    report, state, _ = P.run(cfg, P.Problem(disc, v0, w0, PaperMmsForcing(), PaperMmsBoundary()))
+    for f in "vw":
+        assert rel(getattr(state, f), golden["sv2_run_" + f]) < 1e-10
+    assert rel(report.energy, golden["sv2_run_energy"]) < 1e-10
+
+
+def test_advance_one_step_sv(golden):
+    disc = Discretization.from_mesh(barycentric_refine(build_structured_square(2)))
+    members = (MemberParams(0.01, 0.1), MemberParams(0.012, 0.09), MemberParams(0.009, 0.11))
+    cfg = EnsembleConfig(members=members, coupling=1.0, mu=1.0, dt=0.05, t_end=0.1, perturbation=0.01)
+    J = 3
+    st = EnsembleState(v=golden["sv2_pert_v"], w=golden["sv2_pert_w"], q=np.zeros((J, disc.n_pres)),
+                       r=np.zeros((J, disc.n_pres)))
+    new, res = P.advance(st, cfg, disc, PaperMmsForcing(), PaperMmsBoundary())
+    for f in "vw":
+        assert rel(getattr(new, f), golden["sv2_step1_" + f]) < 1e-10
+    for f in "qr":
+        assert rel(getattr(new, f), golden["sv2_step1_" + f]) < 1e-9
+    assert res < 1e-11
+
+
+def test_zero_data_stays_zero():
+    disc = Discretization.from_mesh(barycentric_refine(build_structured_square(2)))
+    cfg = EnsembleConfig(members=(MemberParams(0.01, 0.1),), coupling=1.0, mu=1.0, dt=0.05, t_end=0.25)
+    z = np.zeros((1, disc.n_vel))
+    st = EnsembleState(v=z, w=z, q=np.zeros((1, disc.n_pres)), r=np.zeros((1, disc.n_pres)))
+    new, res = P.advance(st, cfg, disc, ZeroForcing(), ZeroBoundary())
+    assert np.all(new.v == 0.0) and np.all(new.w == 0.0) and np.all(new.q == 0.0) and np.all(new.r == 0.0)
+    assert res == 0.0
+
+
+def test_identical_members_stay_identical():
+    disc = Discretization.from_mesh(barycentric_refine(build_structured_square(2)))
+    members = tuple(MemberParams(0.01, 0.1) for _ in range(5))
+    cfg = EnsembleConfig(members=members, coupling=1.0, mu=1.0, dt=0.05, t_end=0.2)
+    from paper_2108_05110_b200.problems import paper_v, paper_w
+    v0 = np.tile(fe.interpolate(paper_v, 0.0, disc.velocity), (5, 1))
+    w0 = np.tile(fe.interpolate(paper_w, 0.0, disc.velocity), (5, 1))
+    st = EnsembleState(v=v0, w=w0, q=np.zeros((5, disc.n_pres)), r=np.zeros((5, disc.n_pres)))
+    for _ in range(2):
+        st, _ = P.advance(st, cfg, disc, PaperMmsForcing(), PaperMmsBoundary())
+        for j in range(1, 5):
+            assert np.array_equal(st.v[0], st.v[j]) and np.array_equal(st.w[0], st.w[j])
+
+
+def test_pressure_mean_zero():
+    disc = Discretization.from_mesh(barycentric_refine(build_structured_square(2)))
+    cfg = EnsembleConfig(members=(MemberParams(0.01, 0.1), MemberParams(0.012, 0.09)), coupling=1.0, mu=1.0,
+                         dt=0.05, t_end=0.25)
+    v0, w0 = paper_mms_initial_fields(disc, cfg)
+    st = EnsembleState(v=v0, w=w0, q=np.zeros((2, disc.n_pres)), r=np.zeros((2, disc.n_pres)))
+    new, _ = P.advance(st, cfg, disc, PaperMmsForcing(), PaperMmsBoundary())
+    means = new.q @ disc.pressure_integrals / disc.area
+    assert np.max(np.abs(means)) < 1e-12
