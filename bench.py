@@ -1,0 +1,289 @@
+#!/usr/bin/env python
+"""Benchmark: ensemble member-timesteps/s of the B200 time-step path (BASELINE.json metric).
+
+Workload (N=1): BASELINE.json configs[1] = "C2": manufactured MHD problem on the
+unit square, 128x128 cells (2 triangles each), Taylor-Hood P2/P1, fp64, J=20
+members, dt=0.005.  A bench *step* is one full time-step
+(both Elsasser sub-steps, all members): member sums, right-hand sides, eddy
+viscosity, shared-matrix assembly, multifrontal LU of both saddle matrices,
+column-batched FGMRES to a true relative residual of 1e-12 per member, and
+the pressure epilogue.  For N>1 (torchrun, one rank per GPU) members are
+sharded contiguously with J = 20 per GPU (weak scaling) and every step does
+the two real exchanges of the scheme over NCCL: allreduce SUM of the member
+sums and allreduce MAX of the eddy-viscosity maxima.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
+
+Prints ONE JSON line on rank 0.  See DESIGN.md §6 for every field.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "ensemble member-timesteps/sec at fixed mesh"
+UNIT = "member-steps/s"
+CASE = "C2"
+J_PER_GPU = 20
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        out, _ = self.proc.communicate(timeout=5)
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in out.strip().splitlines():
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[2:6]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def spmm_bytes(hm, J):
+    """Algorithmic HBM bytes of one ens_spmm launch pair (both matrices), DESIGN.md §5."""
+    ns, npres, ntot, nnz = hm.ns, hm.npres, hm.ntot, hm.nnz_s
+    npairs = len(hm.b_col)
+    per_mat = (12 * nnz + 4 * (ns + 1)            # A_s values + column indices + row pointers
+               + 20 * npairs + 4 * (ns + 1)       # B^T (p, bx, by) by node
+               + 20 * npairs + 4 * (npres + 1)    # B (node, bx, by) by pressure row
+               + ntot                             # identity-row flags
+               + 16 * ntot * J)                   # X read once, Y written once
+    return 2 * per_mat
+
+
+def cpu_baseline(disc, cfg, prob, steps=1):
+    """The oracle (numpy/SciPy port of the reference path) on this host: bounded sample."""
+    from oracle import ensmhd_oracle as O
+    J = cfg.num_members
+    st = O.OracleState(np.array(prob.initial_v, float), np.array(prob.initial_w, float),
+                       np.zeros((J, disc.n_pres)), np.zeros((J, disc.n_pres)))
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        st, _ = O.advance(st, cfg, disc, prob.forcing, prob.boundary)
+    dt = time.perf_counter() - t0
+    return J * steps / dt, dt
+
+
+def run_reference(args):
+    """--impl reference: the reference path's CPU restatement (oracle port) on the host cores."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    os.environ.setdefault("OMP_NUM_THREADS", str(os.cpu_count()))
+    import paper_2108_05110_b200 as P
+    disc, cfg, prob = P.build_case(CASE, J=J_PER_GPU * args.gpus)
+    steps = max(1, min(args.steps, 2))
+    value, secs = cpu_baseline(disc, cfg, prob, steps)
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "impl": "reference", "n_gpus": args.gpus, "steps": steps,
+        "warmup": 0, "ms_per_step": 1e3 * secs / steps, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded manufactured solution, SURVEY.md §8.0)",
+        "config": {"workload": f"{CASE}: 128x128 TH P2/P1, J={cfg.num_members}, dt=0.005", "case": CASE},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "port",
+                         "sample": f"{steps} full time-step(s) of {CASE} (SciPy SuperLU, serial; "
+                                   f"{os.cpu_count()} host cores available)"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--e2e-steps", type=int, default=5)
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+
+    import torch
+    import torch.distributed as dist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    comm = None
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        comm = dist.group.WORLD
+    import paper_2108_05110_b200 as P
+    from paper_2108_05110_b200 import stepper as ST
+    from paper_2108_05110_b200.engine import _dptr
+    from paper_2108_05110_b200 import _native as N
+
+    J_total = J_PER_GPU * world
+    disc, cfg, prob = P.build_case(CASE, J=J_total, steps=max(args.steps + args.warmup, 1))
+    j0, jl = ST.member_slice(J_total, rank, world)
+    eng = ST.get_engine(disc, cfg, j0=j0, J=jl, comm=comm)
+    eng.load_state(np.asarray(prob.initial_v)[j0:j0 + jl], np.asarray(prob.initial_w)[j0:j0 + jl], None, None)
+    t = 0.0
+    for _ in range(args.warmup):
+        t += cfg.dt
+        eng.step(t, prob.forcing, prob.boundary)
+    torch.cuda.synchronize()
+    if comm is not None:
+        dist.barrier()
+    sampler = ClockSampler(local)
+    sampler.start()
+    time.sleep(0.3)
+    s = eng.stream
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    if comm is not None:
+        dist.barrier()
+    w0 = time.perf_counter()
+    l0 = eng.lib.ens_kernel_launches()
+    ev0.record(s)
+    iters = []
+    for _ in range(args.steps):
+        t += cfg.dt
+        eng.step(t, prob.forcing, prob.boundary)
+        iters.append(eng.last_iters)
+    ev1.record(s)
+    torch.cuda.synchronize()
+    launches = int(eng.lib.ens_kernel_launches() - l0)
+    wall = time.perf_counter() - w0
+    clocks = sampler.stop()
+    ms = ev0.elapsed_time(ev1)
+    tmax = torch.tensor([ms], dtype=torch.float64, device="cuda")
+    if comm is not None:
+        dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
+        dist.barrier()
+    ms = float(tmax.item())
+    value = J_total * args.steps / (ms / 1e3)
+
+    # ---- per-phase device timing (same stream, CUDA events), for the roofline ----
+    def time_call(fn, reps):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        fn()
+        torch.cuda.synchronize()
+        a.record(s)
+        for _ in range(reps):
+            fn()
+        b.record(s)
+        torch.cuda.synchronize()
+        return a.elapsed_time(b) / reps
+
+    X = eng.X[eng.cur]
+    Y = torch.empty_like(X)
+    spmm_ms = time_call(lambda: N.check(eng.lib.ens_spmm(eng.ctx, eng.sptr, _dptr(eng.as_vals), _dptr(X), None,
+                                                         _dptr(Y), 0), "spmm"), 50)
+    factor_ms = time_call(lambda: eng.factor(), 5)
+    Z = torch.zeros_like(X)
+    solve_ms = time_call(lambda: eng.precond(X, out=Z), 10)
+    bytes_spmm = spmm_bytes(eng.hm, jl)
+    hbm, peak_kind = peaks()
+    spmm_gbs = bytes_spmm / (spmm_ms * 1e-3) / 1e9
+    plan = eng.hm.plan
+    nnz_lu = plan.stats["nnz_lu"]
+    solve_bytes = 2 * 8 * nnz_lu + 2 * 2 * 8 * eng.ntot * jl * 2      # factors once + rhs/x traffic, both matrices
+    solve_gbs = solve_bytes / (solve_ms * 1e-3) / 1e9
+    factor_tflops = 2 * plan.stats["factor_flops"] / (factor_ms * 1e-3) / 1e12
+
+    # ---- end-to-end through the public reference-facing API with host buffers ----
+    e2e = None
+    if world == 1 and args.e2e_steps > 0:
+        from paper_2108_05110_b200.ensemble import EnsembleState
+        st = EnsembleState(v=np.asarray(prob.initial_v), w=np.asarray(prob.initial_w),
+                           q=np.zeros((J_total, disc.n_pres)), r=np.zeros((J_total, disc.n_pres)))
+        st, _ = P.advance(st, cfg, disc, prob.forcing, prob.boundary)   # warm
+        host = EnsembleState(v=st.v, w=st.w, q=st.q, r=st.r, step=st.step, time=st.time)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for _ in range(args.e2e_steps):
+            new, _ = P.advance(host, cfg, disc, prob.forcing, prob.boundary)
+            host = EnsembleState(v=new.v, w=new.w, q=new.q, r=new.r, step=new.step, time=new.time)
+        e2e_s = time.perf_counter() - t0
+        per = 8 * J_total * (2 * disc.n_vel + 2 * disc.n_pres)
+        e2e = {"value": J_total * args.e2e_steps / e2e_s, "unit": UNIT, "h2d_bytes_per_step": per + 8 * 2 * 2 * 3 * J_total,
+               "d2h_bytes_per_step": per + 16, "steps": args.e2e_steps,
+               "api": "paper_2108_05110_b200.advance(state, config, disc, forcing, boundary), numpy state in/out"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        v, secs = cpu_baseline(disc, cfg, prob, 1)
+        cpu = {"value": v, "unit": UNIT, "cores": 1, "kind": "port",
+               "sample": f"1 full time-step of {CASE} with all {J_total} members by the numpy/SciPy oracle "
+                         f"(SuperLU, serial), {secs:.1f} s"}
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded manufactured solution, SURVEY.md §8.0)",
+            "config": {"workload": f"{CASE}: unit square 128x128, TH P2/P1, J={J_PER_GPU}/GPU, dt=0.005",
+                       "case": CASE, "members_total": J_total, "n_total_dofs": int(eng.ntot),
+                       "l2": "per-step working set (2 x %.2f GB fronts) exceeds the 126 MB L2" %
+                             (plan.front_storage * 8 / 1e9),
+                       "rtol": eng.rtol, "parallelism": f"members sharded dp{world}"},
+            "wall_s": wall,
+            "krylov_iters_per_step": float(np.mean(iters)) if iters else None,
+            "roofline": {"bound": "hbm", "kernel": "ens_spmm (saddle SpMM, both systems)", "achieved": spmm_gbs,
+                         "peak": hbm, "peak_kind": peak_kind, "unit": "GB/s", "frac": spmm_gbs / hbm,
+                         "traffic": None, "bytes_per_launch": bytes_spmm, "ms_per_launch": spmm_ms},
+            "phases_ms": {"spmm": spmm_ms, "factor": factor_ms, "lu_solve": solve_ms,
+                          "factor_tflops_fp64": factor_tflops, "lu_solve_gbs": solve_gbs},
+            "clocks": clocks,
+            "gpu_launches": launches,
+            "e2e": e2e,
+            "cpu_baseline": cpu,
+        }
+        print(json.dumps(line), flush=True)
+    if comm is not None:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -129,6 +129,8 @@ typedef struct {
 
 int  ens_abi_version(void);
 const char* ens_last_error(void);
+/* Process-wide count of kernels this library has launched (bench evidence). */
+int64_t ens_kernel_launches(void);
 
 int  ens_create(const ens_mesh_desc* mesh, const ens_plan_desc* plan, int device, ens_ctx** out);
 void ens_destroy(ens_ctx* ctx);

@@ -51,7 +51,7 @@ class DataDesc(C.Structure):
 
 
 SYMBOLS = [
-    "ens_abi_version", "ens_last_error", "ens_create", "ens_destroy", "ens_workspace_bytes",
+    "ens_abi_version", "ens_last_error", "ens_kernel_launches", "ens_create", "ens_destroy", "ens_workspace_bytes",
     "ens_member_sums", "ens_rhs", "ens_member_pass", "ens_apply_bc", "ens_assemble", "ens_factor",
     "ens_solve", "ens_spmm", "ens_precond_apply", "ens_epilogue", "ens_diagnostics",
 ]
@@ -70,6 +70,7 @@ def load(path: str = LIB_PATH):
     lib = C.CDLL(path)
     lib.ens_abi_version.restype = C.c_int
     lib.ens_last_error.restype = C.c_char_p
+    lib.ens_kernel_launches.restype = C.c_int64
     lib.ens_create.argtypes = [C.POINTER(MeshDesc), C.POINTER(PlanDesc), C.c_int, C.POINTER(P)]
     lib.ens_destroy.argtypes = [P]
     lib.ens_destroy.restype = None
@@ -86,7 +87,7 @@ def load(path: str = LIB_PATH):
     lib.ens_epilogue.argtypes = [P, P, P, P]
     lib.ens_diagnostics.argtypes = [P, P, P, P, P]
     for name in SYMBOLS:
-        if name not in ("ens_abi_version", "ens_last_error", "ens_destroy"):
+        if name not in ("ens_abi_version", "ens_last_error", "ens_destroy", "ens_kernel_launches"):
             getattr(lib, name).restype = C.c_int
     _lib = lib
     return lib

@@ -11,6 +11,7 @@ int ens_upload_tables();
 size_t gmres_col_bytes();
 
 static thread_local std::string g_err;
+unsigned long long g_ens_launches = 0;
 
 void ens_set_error(const char* msg, const char* file, int line) {
     char buf[512];
@@ -29,6 +30,8 @@ extern "C" {
 int ens_abi_version(void) { return ENS_ABI_VERSION; }
 
 const char* ens_last_error(void) { return g_err.c_str(); }
+
+int64_t ens_kernel_launches(void) { return (int64_t)g_ens_launches; }
 
 int ens_create(const ens_mesh_desc* mesh, const ens_plan_desc* plan, int device, ens_ctx** out) {
     if (!mesh || !plan || !out) {

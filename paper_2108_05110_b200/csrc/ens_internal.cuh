@@ -26,7 +26,13 @@ void ens_set_error(const char* msg, const char* file, int line);
         }                                                                     \
     } while (0)
 
-#define ENS_CKL() ENS_CK(cudaGetLastError())
+// every kernel launch site ends with ENS_CKL(): it also counts the launch
+extern unsigned long long g_ens_launches;
+#define ENS_CKL()                  \
+    do {                           \
+        ++g_ens_launches;          \
+        ENS_CK(cudaGetLastError()); \
+    } while (0)
 
 struct GmresCol;   // per-column Krylov scalars (device)
 

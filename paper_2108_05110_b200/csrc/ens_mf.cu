@@ -455,15 +455,14 @@ int mf_factor(ens_ctx* c, cudaStream_t s, const double* as_vals, int32_t* n_pert
                 const int64_t a = c->level_storage_off[L], b = c->level_storage_off[L + 1];
                 for (int mat = 0; mat < 2; ++mat)
                     ENS_CK(cudaMemsetAsync(c->fronts + mat * st + a, 0, sizeof(double) * (size_t)(b - a), s));
-                break;
+                continue;   // a memset, not a kernel launch
             }
             case OP_ORIG: {
                 const int64_t a = c->orig_level_off[L], b = c->orig_level_off[L + 1];
-                if (b > a) {
-                    dim3 grid((unsigned)((b - a + 255) / 256), 2);
-                    k_orig<<<grid, 256, 0, s>>>(c->p.orig_dst, c->p.orig_src, a, b, as_vals, c->m.nnz_s,
-                                                c->p.bsrc_vals, c->fronts, st);
-                }
+                if (b <= a) continue;
+                dim3 grid((unsigned)((b - a + 255) / 256), 2);
+                k_orig<<<grid, 256, 0, s>>>(c->p.orig_dst, c->p.orig_src, a, b, as_vals, c->m.nnz_s,
+                                            c->p.bsrc_vals, c->fronts, st);
                 break;
             }
             case OP_EXTADD:

@@ -322,36 +322,66 @@ class Engine:
     # ------------------------------------------------------------------
     # state upload / download
     # ------------------------------------------------------------------
+    def _staging(self):
+        """Pinned host + device staging (reference layout) and the permutations, allocated once."""
+        if getattr(self, "_stg", None) is None:
+            hm, J, d = self.hm, self.J, self.dev
+            self._stg = dict(
+                h_vel=torch.empty(2, J, self.nvel, dtype=torch.float64, pin_memory=True),
+                h_pres=torch.empty(2, J, self.npres, dtype=torch.float64, pin_memory=True),
+                d_vel=torch.empty(2, J, self.nvel, dtype=torch.float64, device=d),
+                d_pres=torch.empty(2, J, self.npres, dtype=torch.float64, device=d),
+                ref_of_int_v=torch.as_tensor(hm.ref_of_int[:self.nvel]).to(d),
+                ref_of_int_p=torch.as_tensor(hm.ref_of_int[self.nvel:] - self.nvel).to(d),
+                int_of_ref_v=torch.as_tensor(hm.int_id[:self.nvel]).to(d),
+                int_of_ref_p=torch.as_tensor(hm.int_id[self.nvel:] - self.nvel).to(d))
+        return self._stg
+
     def load_state(self, v, w, q, r):
-        """Upload a host state (reference layout, this rank's members) into the current buffer set."""
-        hm = self.hm
+        """Upload a host state (reference layout, this rank's members) into the current buffer set.
+
+        Pinned H2D copies of the (J, n) arrays; the member-minor transpose and
+        the internal dof permutation run on the device.
+        """
+        g = self._staging()
         self._retire(self.cur)
         X = self.X[self.cur]
-        X[0, :self.nvel] = torch.from_numpy(hm.vel_to_internal(v)).to(self.dev)
-        X[1, :self.nvel] = torch.from_numpy(hm.vel_to_internal(w)).to(self.dev)
-        if q is not None and np.asarray(q).size:
-            X[0, self.nvel:] = torch.from_numpy(hm.pres_to_internal(q)).to(self.dev)
-            X[1, self.nvel:] = torch.from_numpy(hm.pres_to_internal(r)).to(self.dev)
-            self.Pq[self.cur][0] = X[0, self.nvel:]
-            self.Pq[self.cur][1] = X[1, self.nvel:]
-        else:
-            X[:, self.nvel:] = 0.0
-            self.Pq[self.cur].zero_()
+        s = self.stream
+        np.copyto(g["h_vel"][0].numpy(), np.asarray(v, dtype=float))
+        np.copyto(g["h_vel"][1].numpy(), np.asarray(w, dtype=float))
+        with torch.cuda.stream(s):
+            g["d_vel"].copy_(g["h_vel"], non_blocking=True)
+            for m in range(2):
+                X[m, :self.nvel] = g["d_vel"][m].t().index_select(0, g["ref_of_int_v"])
+            if q is not None and np.asarray(q).size:
+                np.copyto(g["h_pres"][0].numpy(), np.asarray(q, dtype=float))
+                np.copyto(g["h_pres"][1].numpy(), np.asarray(r, dtype=float))
+                g["d_pres"].copy_(g["h_pres"], non_blocking=True)
+                for m in range(2):
+                    X[m, self.nvel:] = g["d_pres"][m].t().index_select(0, g["ref_of_int_p"])
+                self.Pq[self.cur].copy_(X[:, self.nvel:])
+            else:
+                X[:, self.nvel:] = 0.0
+                self.Pq[self.cur].zero_()
+        s.synchronize()          # staging buffers are reused by the next upload
         self.gen[self.cur] += 1
         self.means_valid = False
 
     def field_to_host(self, buf, name):
-        hm = self.hm
-        torch.cuda.synchronize(self.dev)
-        if name in "vw":
-            blk = self.X[buf][0 if name == "v" else 1, :self.nvel]
-            out = np.empty((self.J, self.nvel))
-            out[:, hm.ref_of_int[:self.nvel]] = blk.cpu().numpy().T
-            return out
-        blk = self.Pq[buf][0 if name == "q" else 1]
-        out = np.empty((self.J, self.npres))
-        out[:, hm.ref_of_int[self.nvel:] - self.nvel] = blk.cpu().numpy().T
-        return out
+        """(J, n) reference-layout numpy copy of one field of buffer set ``buf``."""
+        g = self._staging()
+        s = self.stream
+        m = 0 if name in "vq" else 1
+        with torch.cuda.stream(s):
+            if name in "vw":
+                dst, hst = g["d_vel"][m], g["h_vel"][m]
+                dst.copy_(self.X[buf][m, :self.nvel].index_select(0, g["int_of_ref_v"]).t())
+            else:
+                dst, hst = g["d_pres"][m], g["h_pres"][m]
+                dst.copy_(self.Pq[buf][m].index_select(0, g["int_of_ref_p"]).t())
+            hst.copy_(dst, non_blocking=True)
+        s.synchronize()
+        return hst.numpy().copy()
 
     def state_handle(self):
         h = DeviceState(self, self.cur, self.gen[self.cur], self.J)
