@@ -1,22 +1,24 @@
-// Multifrontal LU of the two shared saddle matrices + multi-column triangular
-// solves (sm_100a, fp64).  Symbolic structure and the launch schedule come from
-// paper_2108_05110_b200/symbolic.py; this file executes it.
+// Multifrontal block-sweep factorisation of the two shared saddle matrices and
+// the multi-column solves (sm_100a, fp64).  Symbolic structure and the launch
+// schedule come from paper_2108_05110_b200/symbolic.py; this file executes it.
 //
-// Per front (dense m x m, row-major) and per panel [a, b) of its pivots:
-//   DIAG    D  <- D^-1                      (Gauss-Jordan, partial pivoting in-panel)
-//   HPANEL  R  <- H = -D^-1 R               (rows a..b, cols b..m)
-//   UPDATE  T  <- T + C H                   (rows/cols b..m; C = cols a..b, rows b..m)
-//   GPANEL  C  <- G = -C D^-1
-// The trailing T of the last panel is the contribution block, extend-added into
-// the parent front.  Solves use the stored (D^-1, H, G) directly:
-//   forward:  fr[b:m] += G fr[a:b]           backward: x[a:b] = D^-1 fr[a:b] + H x[b:m]
-// which equals forward/backward substitution with the block LU factors.
+// Each front is a dense m x m row-major block whose first k rows/cols are its
+// pivots.  For every panel P = [a, a+pw) of the pivots (the block-sweep /
+// Gauss-Jordan step, Q = all front rows/cols outside P):
+//   DIAG    F[P,P] <- -D^-1                 (D = F[P,P]; register Gauss-Jordan, in-panel pivoting)
+//   HPANEL  F[P,Q] <- D^-1 F[P,Q]
+//   UPDATE  F[Q,Q] <- F[Q,Q] - F[Q,P] F[P,Q]   (F[P,Q] already scaled)
+//   GPANEL  F[Q,P] <- F[Q,P] D^-1
+// After all panels the front holds [-F11^-1, F11^-1 F12; F21 F11^-1, S] with S
+// the Schur complement (extend-added into the parent).  Solves are then one
+// batched GEMM per tree level and direction:
+//   forward  fr[C] -= F[C,P] fr[P]             backward  x[P] = -[F[P,P] F[P,C]] [fr[P]; x[C]]
 #include <cmath>
 
 #include "ens_internal.cuh"
 
 enum { OP_ZERO = 0, OP_ORIG, OP_EXTADD, OP_DIAG, OP_HPANEL, OP_UPDATE, OP_GPANEL };
-enum { SOP_FINIT = 0, SOP_FEXT, SOP_FPANEL, SOP_BGATHER, SOP_BPANEL, SOP_BSCATTER };
+enum { SOP_FINIT = 0, SOP_FEXT, SOP_FGEMM, SOP_BGATHER, SOP_BGEMM };
 
 struct MfDev {
     const int32_t* m;
@@ -46,8 +48,11 @@ static MfDev mfdev(const ens_ctx* c) {
     return d;
 }
 
+// outside-panel index -> front row/col
+__device__ __forceinline__ int outside(int r, int a, int pw) { return r < a ? r : r + pw; }
+
 // ---------------------------------------------------------------------------
-// factorisation kernels; grid = (items, 2 matrices)
+// assembly of the fronts (original entries, child contribution blocks)
 // ---------------------------------------------------------------------------
 __global__ void k_orig(const int64_t* __restrict__ dst, const int32_t* __restrict__ src, int64_t n0, int64_t n1,
                        const double* __restrict__ as_vals, int nnz, const double* __restrict__ bsrc,
@@ -77,38 +82,69 @@ __global__ void k_extadd(MfDev d, int item0, double* __restrict__ F) {
     }
 }
 
-// D^-1 by Gauss-Jordan with partial pivoting inside the panel (augmented [D | I])
+// ---------------------------------------------------------------------------
+// DIAG: F[P,P] <- -D^-1.  In-place Gauss-Jordan held in registers (16x16
+// threads, 4x4 elements each); partial pivoting without row swaps: the pivot
+// row of column k is the unused row with the largest |a[r][k]|, and the
+// inverse is recovered as A^-1[i][j] = a[piv[i]][ipiv[j]].
+// ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(256) k_diag(MfDev d, int item0, double* __restrict__ F, int32_t* __restrict__ npert) {
-    extern __shared__ double sm[];
+    __shared__ double s_col[2][ENS_PW];
+    __shared__ double s_row[2][ENS_PW];
+    __shared__ int s_piv[ENS_PW];
+    __shared__ int s_ipiv[ENS_PW];
+    __shared__ unsigned char s_used[ENS_PW];
+    __shared__ double s_scale;
+    __shared__ double s_out[ENS_PW][ENS_PW + 1];
     const int* it = d.work + 4LL * (item0 + blockIdx.x);
-    const int f = it[0], a = it[1];
+    const int f = it[0], a0 = it[1];
     const int mat = blockIdx.y;
     const int m = d.m[f];
-    const int pw = min(ENS_PW, d.k[f] - a);
-    const int W = 2 * pw;
-    double* A = sm;                      // pw x W
-    double* fac = sm + pw * W;           // pw
-    __shared__ int s_piv;
-    __shared__ double s_scale;
-    double* Fb = F + (int64_t)mat * d.storage + d.off[f] + (int64_t)a * m + a;
-    for (int t = threadIdx.x; t < pw * W; t += blockDim.x) {
-        const int r = t / W, cc = t % W;
-        A[t] = cc < pw ? Fb[(int64_t)r * m + cc] : (cc - pw == r ? 1.0 : 0.0);
-    }
+    const int pw = min(ENS_PW, d.k[f] - a0);
+    double* Fb = F + (int64_t)mat * d.storage + d.off[f] + (int64_t)a0 * m + a0;
+    const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+    double a[4][4];
+    double amax = 0.0;
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const int r = ty + 16 * i, c = tx + 16 * j;
+            double v = (r == c) ? 1.0 : 0.0;
+            if (r < pw && c < pw) v = Fb[(int64_t)r * m + c];
+            a[i][j] = v;
+            if (r < pw && c < pw) amax = fmax(amax, fabs(v));
+        }
+    if (threadIdx.x < ENS_PW) s_used[threadIdx.x] = 0;
+    // block max for the tiny-pivot threshold
+    for (int o = 16; o > 0; o >>= 1) amax = fmax(amax, __shfl_xor_sync(0xffffffffu, amax, o));
+    if (threadIdx.x == 0) s_scale = 0.0;
     __syncthreads();
-    if (threadIdx.x < 32) {   // block scale for the tiny-pivot threshold
-        double mx = 0.0;
-        for (int t = threadIdx.x; t < pw * pw; t += 32) mx = fmax(mx, fabs(A[(t / pw) * W + t % pw]));
-        for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-        if (threadIdx.x == 0) s_scale = mx;
-    }
+    if ((threadIdx.x & 31) == 0) atomicMax((unsigned long long*)&s_scale, (unsigned long long)__double_as_longlong(amax));
     __syncthreads();
-    for (int col = 0; col < pw; ++col) {
+    const double thr = 1e-14 * (s_scale > 0.0 ? s_scale : 1.0);
+    for (int k = 0; k < pw; ++k) {
+        const int buf = k & 1;
+        // 1. column k to smem
+        if (tx == (k & 15)) {
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                const int jj = k >> 4;
+                double v = 0.0;
+#pragma unroll
+                for (int j = 0; j < 4; ++j)
+                    if (j == jj) v = a[i][j];
+                s_col[buf][ty + 16 * i] = v;
+            }
+        }
+        __syncthreads();
+        // 2. pivot row: largest |a[r][k]| among unused rows r < pw
         if (threadIdx.x < 32) {
             double best = -1.0;
-            int br = col;
-            for (int r = col + threadIdx.x; r < pw; r += 32) {
-                const double v = fabs(A[r * W + col]);
+            int br = ENS_PW;
+            for (int r = threadIdx.x; r < pw; r += 32) {
+                if (s_used[r]) continue;
+                const double v = fabs(s_col[buf][r]);
                 if (v > best) {
                     best = v;
                     br = r;
@@ -123,42 +159,90 @@ __global__ void __launch_bounds__(256) k_diag(MfDev d, int item0, double* __rest
                 }
             }
             if (threadIdx.x == 0) {
-                s_piv = br;
-                const double thr = 1e-14 * (s_scale > 0.0 ? s_scale : 1.0);
-                if (!(best > thr)) {   // singular / tiny pivot: static perturbation, GMRES corrects it
-                    A[br * W + col] = (A[br * W + col] < 0.0 ? -thr : thr);
+                if (br >= pw) {        // NaN column: take the first unused row
+                    for (int r = 0; r < pw; ++r)
+                        if (!s_used[r]) {
+                            br = r;
+                            break;
+                        }
+                }
+                if (!(best > thr)) {   // singular/tiny pivot: static perturbation, GMRES corrects it
+                    s_col[buf][br] = (s_col[buf][br] < 0.0 ? -thr : thr);
                     atomicAdd(npert, 1);
+                }
+                s_used[br] = 1;
+                s_piv[k] = br;
+                s_ipiv[br] = k;
+            }
+        }
+        __syncthreads();
+        const int p = s_piv[k];
+        // 3. pivot row to smem
+        if (ty == (p & 15)) {
+            const int ii = p >> 4;
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                double v = 0.0;
+#pragma unroll
+                for (int i = 0; i < 4; ++i)
+                    if (i == ii) v = a[i][j];
+                s_row[buf][tx + 16 * j] = v;
+            }
+        }
+        __syncthreads();
+        // 4. eliminate (pivot element of column k treated as 1, in-place inverse)
+        const double inv = 1.0 / s_col[buf][p];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const int c = tx + 16 * j;
+            const double np = (c == k ? 1.0 : s_row[buf][c]) * inv;
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                const int r = ty + 16 * i;
+                if (r == p) {
+                    a[i][j] = np;
+                } else {
+                    const double fr = s_col[buf][r];
+                    a[i][j] = (c == k ? 0.0 : a[i][j]) - fr * np;
                 }
             }
         }
-        __syncthreads();
-        const int pr = s_piv;
-        if (pr != col) {
-            for (int cc = threadIdx.x; cc < W; cc += blockDim.x) {
-                const double t0 = A[col * W + cc];
-                A[col * W + cc] = A[pr * W + cc];
-                A[pr * W + cc] = t0;
-            }
-        }
-        __syncthreads();
-        const double inv = 1.0 / A[col * W + col];
-        for (int r = threadIdx.x; r < pw; r += blockDim.x) fac[r] = A[r * W + col];
-        __syncthreads();
-        for (int cc = threadIdx.x; cc < W; cc += blockDim.x) A[col * W + cc] *= inv;
-        __syncthreads();
-        for (int t = threadIdx.x; t < pw * W; t += blockDim.x) {
-            const int r = t / W, cc = t % W;
-            if (r != col) A[t] -= fac[r] * A[col * W + cc];
-        }
-        __syncthreads();
     }
+    // un-permute and store -D^-1
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) s_out[ty + 16 * i][tx + 16 * j] = a[i][j];
+    __syncthreads();
     for (int t = threadIdx.x; t < pw * pw; t += blockDim.x) {
-        const int r = t / pw, cc = t % pw;
-        Fb[(int64_t)r * m + cc] = A[r * W + pw + cc];
+        const int r = t / pw, c = t % pw;
+        Fb[(int64_t)r * m + c] = -s_out[s_piv[r]][s_ipiv[c]];
     }
 }
 
-// H = -D^-1 R for a 64-column tile of R (in place)
+// ---------------------------------------------------------------------------
+// register-tiled 64x64 (rows) x 64 (cols) GEMM piece from shared memory:
+// acc[i][j] += sum_t A[ty+16i][t] * B[t][tx+16j]
+// ---------------------------------------------------------------------------
+#define LDA (ENS_TILE + 1)
+
+__device__ __forceinline__ void tile_mma(const double* __restrict__ As, const double* __restrict__ Bs, int K,
+                                         double acc[4][4], int tx, int ty) {
+    // As: row-major [64][LDA] indexed As[r*LDA + t]; Bs: [K][64]
+    for (int t = 0; t < K; ++t) {
+        double av[4], bv[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) av[i] = As[(ty + 16 * i) * LDA + t];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) bv[j] = Bs[t * ENS_TILE + tx + 16 * j];
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+            for (int j = 0; j < 4; ++j) acc[i][j] = fma(av[i], bv[j], acc[i][j]);
+    }
+}
+
+// HPANEL: F[P, Q-tile] <- D^-1 F[P, Q-tile]   (D^-1 = -F[P,P])
 __global__ void __launch_bounds__(256) k_hpanel(MfDev d, int item0, double* __restrict__ F) {
     extern __shared__ double sm[];
     const int* it = d.work + 4LL * (item0 + blockIdx.x);
@@ -166,26 +250,36 @@ __global__ void __launch_bounds__(256) k_hpanel(MfDev d, int item0, double* __re
     const int mat = blockIdx.y;
     const int m = d.m[f];
     const int pw = min(ENS_PW, d.k[f] - a);
-    const int b = a + pw;
-    const int nc = min(ENS_TILE, m - b - c0);
-    double* Ds = sm;                       // pw x pw
-    double* Rs = sm + ENS_PW * ENS_PW;     // pw x 64
+    const int t = m - pw;
+    const int nc = min(ENS_TILE, t - c0);
+    double* Ds = sm;                       // [64][LDA]  (D^-1)
+    double* Rs = sm + ENS_PW * LDA;        // [pw][64]
     double* base = F + (int64_t)mat * d.storage + d.off[f];
-    for (int t = threadIdx.x; t < pw * pw; t += blockDim.x) Ds[t] = base[(int64_t)(a + t / pw) * m + a + t % pw];
-    for (int t = threadIdx.x; t < pw * ENS_TILE; t += blockDim.x) {
-        const int r = t / ENS_TILE, cc = t % ENS_TILE;
-        Rs[t] = cc < nc ? base[(int64_t)(a + r) * m + b + c0 + cc] : 0.0;
+    for (int e = threadIdx.x; e < ENS_PW * ENS_PW; e += blockDim.x) {
+        const int r = e / ENS_PW, cc = e % ENS_PW;
+        Ds[r * LDA + cc] = (r < pw && cc < pw) ? -base[(int64_t)(a + r) * m + a + cc] : 0.0;
+    }
+    for (int e = threadIdx.x; e < pw * ENS_TILE; e += blockDim.x) {
+        const int r = e / ENS_TILE, cc = e % ENS_TILE;
+        Rs[e] = cc < nc ? base[(int64_t)(a + r) * m + outside(c0 + cc, a, pw)] : 0.0;
     }
     __syncthreads();
-    const int cc = threadIdx.x % ENS_TILE;
-    for (int i = threadIdx.x / ENS_TILE; i < pw; i += blockDim.x / ENS_TILE) {
-        double acc = 0.0;
-        for (int t = 0; t < pw; ++t) acc += Ds[i * pw + t] * Rs[t * ENS_TILE + cc];
-        if (cc < nc) base[(int64_t)(a + i) * m + b + c0 + cc] = -acc;
+    const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+    double acc[4][4] = {};
+    tile_mma(Ds, Rs, pw, acc, tx, ty);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const int r = ty + 16 * i;
+        if (r >= pw) continue;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const int cc = tx + 16 * j;
+            if (cc < nc) base[(int64_t)(a + r) * m + outside(c0 + cc, a, pw)] = acc[i][j];
+        }
     }
 }
 
-// T += C H on a 64x64 tile (K = pw)
+// UPDATE: F[Q-rows, Q-cols] -= F[Q-rows, P] F[P, Q-cols]
 __global__ void __launch_bounds__(256) k_update(MfDev d, int item0, double* __restrict__ F) {
     extern __shared__ double sm[];
     const int* it = d.work + 4LL * (item0 + blockIdx.x);
@@ -193,52 +287,40 @@ __global__ void __launch_bounds__(256) k_update(MfDev d, int item0, double* __re
     const int mat = blockIdx.y;
     const int m = d.m[f];
     const int pw = min(ENS_PW, d.k[f] - a);
-    const int b = a + pw;
-    const int nr = min(ENS_TILE, m - b - r0), nc = min(ENS_TILE, m - b - c0);
-    const int LD = ENS_TILE + 1;
-    double* Cs = sm;                     // pw x LD  (transposed C tile)
-    double* Hs = sm + ENS_PW * LD;       // pw x 64
+    const int t = m - pw;
+    const int nr = min(ENS_TILE, t - r0), nc = min(ENS_TILE, t - c0);
+    double* Cs = sm;                       // [64][LDA]
+    double* Hs = sm + ENS_TILE * LDA;      // [pw][64]
     double* base = F + (int64_t)mat * d.storage + d.off[f];
-    for (int t = threadIdx.x; t < ENS_TILE * pw; t += blockDim.x) {
-        const int r = t / pw, kk = t % pw;
-        Cs[kk * LD + r] = r < nr ? base[(int64_t)(b + r0 + r) * m + a + kk] : 0.0;
+    for (int e = threadIdx.x; e < ENS_TILE * pw; e += blockDim.x) {
+        const int r = e / pw, kk = e % pw;
+        Cs[r * LDA + kk] = r < nr ? base[(int64_t)outside(r0 + r, a, pw) * m + a + kk] : 0.0;
     }
-    for (int t = threadIdx.x; t < pw * ENS_TILE; t += blockDim.x) {
-        const int kk = t / ENS_TILE, cc = t % ENS_TILE;
-        Hs[t] = cc < nc ? base[(int64_t)(a + kk) * m + b + c0 + cc] : 0.0;
+    for (int e = threadIdx.x; e < pw * ENS_TILE; e += blockDim.x) {
+        const int kk = e / ENS_TILE, cc = e % ENS_TILE;
+        Hs[e] = cc < nc ? base[(int64_t)(a + kk) * m + outside(c0 + cc, a, pw)] : 0.0;
     }
     __syncthreads();
-    const int tx = threadIdx.x % 16, ty = threadIdx.x / 16;
-    double acc[4][4];
+    const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+    double acc[4][4] = {};
+    tile_mma(Cs, Hs, pw, acc, tx, ty);
 #pragma unroll
-    for (int u = 0; u < 4; ++u)
-#pragma unroll
-        for (int v = 0; v < 4; ++v) acc[u][v] = 0.0;
-    for (int kk = 0; kk < pw; ++kk) {
-        double av[4], bv[4];
-#pragma unroll
-        for (int u = 0; u < 4; ++u) av[u] = Cs[kk * LD + ty + 16 * u];
-#pragma unroll
-        for (int v = 0; v < 4; ++v) bv[v] = Hs[kk * ENS_TILE + tx + 16 * v];
-#pragma unroll
-        for (int u = 0; u < 4; ++u)
-#pragma unroll
-            for (int v = 0; v < 4; ++v) acc[u][v] = fma(av[u], bv[v], acc[u][v]);
-    }
-#pragma unroll
-    for (int u = 0; u < 4; ++u) {
-        const int r = ty + 16 * u;
+    for (int i = 0; i < 4; ++i) {
+        const int r = ty + 16 * i;
         if (r >= nr) continue;
-        double* row = base + (int64_t)(b + r0 + r) * m + b + c0;
+        double* row = base + (int64_t)outside(r0 + r, a, pw) * m;
 #pragma unroll
-        for (int v = 0; v < 4; ++v) {
-            const int cc = tx + 16 * v;
-            if (cc < nc) row[cc] += acc[u][v];
+        for (int j = 0; j < 4; ++j) {
+            const int cc = tx + 16 * j;
+            if (cc < nc) {
+                const int col = outside(c0 + cc, a, pw);
+                row[col] -= acc[i][j];
+            }
         }
     }
 }
 
-// G = -C D^-1 for a 64-row tile of C (in place)
+// GPANEL: F[Q-tile, P] <- F[Q-tile, P] D^-1
 __global__ void __launch_bounds__(256) k_gpanel(MfDev d, int item0, double* __restrict__ F) {
     extern __shared__ double sm[];
     const int* it = d.work + 4LL * (item0 + blockIdx.x);
@@ -246,29 +328,40 @@ __global__ void __launch_bounds__(256) k_gpanel(MfDev d, int item0, double* __re
     const int mat = blockIdx.y;
     const int m = d.m[f];
     const int pw = min(ENS_PW, d.k[f] - a);
-    const int b = a + pw;
-    const int nr = min(ENS_TILE, m - b - r0);
-    double* Ds = sm;                       // pw x pw
-    double* Cs = sm + ENS_PW * ENS_PW;     // 64 x pw
+    const int t = m - pw;
+    const int nr = min(ENS_TILE, t - r0);
+    double* Cs = sm;                       // [64][LDA]
+    double* Ds = sm + ENS_TILE * LDA;      // [pw][64]  (D^-1)
     double* base = F + (int64_t)mat * d.storage + d.off[f];
-    for (int t = threadIdx.x; t < pw * pw; t += blockDim.x) Ds[t] = base[(int64_t)(a + t / pw) * m + a + t % pw];
-    for (int t = threadIdx.x; t < ENS_TILE * pw; t += blockDim.x) {
-        const int r = t / pw, kk = t % pw;
-        Cs[t] = r < nr ? base[(int64_t)(b + r0 + r) * m + a + kk] : 0.0;
+    for (int e = threadIdx.x; e < ENS_TILE * pw; e += blockDim.x) {
+        const int r = e / pw, kk = e % pw;
+        Cs[r * LDA + kk] = r < nr ? base[(int64_t)outside(r0 + r, a, pw) * m + a + kk] : 0.0;
+    }
+    for (int e = threadIdx.x; e < pw * ENS_TILE; e += blockDim.x) {
+        const int kk = e / ENS_TILE, cc = e % ENS_TILE;
+        Ds[e] = cc < pw ? -base[(int64_t)(a + kk) * m + a + cc] : 0.0;
     }
     __syncthreads();
-    for (int t = threadIdx.x; t < nr * pw; t += blockDim.x) {
-        const int r = t / pw, cc = t % pw;
-        double acc = 0.0;
-        for (int kk = 0; kk < pw; ++kk) acc += Cs[r * pw + kk] * Ds[kk * pw + cc];
-        base[(int64_t)(b + r0 + r) * m + a + cc] = -acc;
+    const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+    double acc[4][4] = {};
+    tile_mma(Cs, Ds, pw, acc, tx, ty);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const int r = ty + 16 * i;
+        if (r >= nr) continue;
+        double* row = base + (int64_t)outside(r0 + r, a, pw) * m + a;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const int cc = tx + 16 * j;
+            if (cc < pw) row[cc] = acc[i][j];
+        }
     }
 }
 
 // ---------------------------------------------------------------------------
-// solve kernels: grid = (items, 2 matrices, column chunks of 64)
+// solve kernels: grid = (items, 2 matrices[, column chunks of 32])
 // ---------------------------------------------------------------------------
-#define SJT 64
+#define SJT 32
 
 __global__ void k_finit(MfDev d, int item0, const double* __restrict__ B, double* __restrict__ FR, int64_t N, int J,
                         int64_t nidx) {
@@ -302,40 +395,6 @@ __global__ void k_fext(MfDev d, int item0, double* __restrict__ FR, int J, int64
     }
 }
 
-// fr[b+r0 .. +64] += G[rows, a:b] fr[a:b]
-__global__ void __launch_bounds__(256) k_fpanel(MfDev d, int item0, const double* __restrict__ F,
-                                                double* __restrict__ FR, int J, int64_t nidx) {
-    extern __shared__ double sm[];
-    const int* it = d.work + 4LL * (item0 + blockIdx.x);
-    const int f = it[0], a = it[1], r0 = it[2];
-    const int mat = blockIdx.y;
-    const int j0 = blockIdx.z * SJT;
-    const int jn = min(SJT, J - j0);
-    const int m = d.m[f];
-    const int pw = min(ENS_PW, d.k[f] - a);
-    const int b = a + pw;
-    const int nr = min(ENS_TILE, m - b - r0);
-    const double* base = F + (int64_t)mat * d.storage + d.off[f];
-    double* fr = FR + (int64_t)mat * nidx * J + d.idx_off[f] * J;
-    double* Gs = sm;                   // 64 x pw
-    double* Xs = sm + ENS_TILE * ENS_PW;   // pw x SJT
-    for (int t = threadIdx.x; t < nr * pw; t += blockDim.x) {
-        const int r = t / pw, kk = t % pw;
-        Gs[r * pw + kk] = base[(int64_t)(b + r0 + r) * m + a + kk];
-    }
-    for (int t = threadIdx.x; t < pw * jn; t += blockDim.x) {
-        const int kk = t / jn, j = t % jn;
-        Xs[kk * SJT + j] = fr[(int64_t)(a + kk) * J + j0 + j];
-    }
-    __syncthreads();
-    for (int t = threadIdx.x; t < nr * jn; t += blockDim.x) {
-        const int r = t / jn, j = t % jn;
-        double acc = 0.0;
-        for (int kk = 0; kk < pw; ++kk) acc += Gs[r * pw + kk] * Xs[kk * SJT + j];
-        fr[(int64_t)(b + r0 + r) * J + j0 + j] += acc;
-    }
-}
-
 __global__ void k_bgather(MfDev d, int item0, const double* __restrict__ X, double* __restrict__ FR, int64_t N, int J,
                           int64_t nidx) {
     const int* it = d.work + 4LL * (item0 + blockIdx.x);
@@ -352,92 +411,79 @@ __global__ void k_bgather(MfDev d, int item0, const double* __restrict__ X, doub
     }
 }
 
-// x[a:b] = [D^-1 H] fr[a:m]   (in place into fr[a:b])
-__global__ void __launch_bounds__(256) k_bpanel(MfDev d, int item0, const double* __restrict__ F,
-                                                double* __restrict__ FR, int J, int64_t nidx) {
-    extern __shared__ double sm[];
-    const int* it = d.work + 4LL * (item0 + blockIdx.x);
-    const int f = it[0], a = it[1];
-    const int mat = blockIdx.y;
-    const int j0 = blockIdx.z * SJT;
-    const int jn = min(SJT, J - j0);
-    const int m = d.m[f];
-    const int pw = min(ENS_PW, d.k[f] - a);
-    const double* base = F + (int64_t)mat * d.storage + d.off[f];
-    double* fr = FR + (int64_t)mat * nidx * J + d.idx_off[f] * J;
-    double* As = sm;                         // pw x 64 (row-chunk of [D^-1 H])
-    double* Xs = sm + ENS_PW * ENS_TILE;     // 64 x SJT
-    const int nout = pw * jn;
-    double acc[16];
-#pragma unroll
-    for (int u = 0; u < 16; ++u) acc[u] = 0.0;
-    for (int c0 = a; c0 < m; c0 += ENS_TILE) {
-        const int kc = min(ENS_TILE, m - c0);
-        __syncthreads();
-        for (int t = threadIdx.x; t < pw * ENS_TILE; t += blockDim.x) {
-            const int r = t / ENS_TILE, kk = t % ENS_TILE;
-            As[t] = kk < kc ? base[(int64_t)(a + r) * m + c0 + kk] : 0.0;
-        }
-        for (int t = threadIdx.x; t < ENS_TILE * SJT; t += blockDim.x) {
-            const int kk = t / SJT, j = t % SJT;
-            Xs[t] = (kk < kc && j < jn) ? fr[(int64_t)(c0 + kk) * J + j0 + j] : 0.0;
-        }
-        __syncthreads();
-#pragma unroll
-        for (int u = 0; u < 16; ++u) {
-            const int o = threadIdx.x + u * 256;
-            if (o < nout) {
-                const int r = o / jn, j = o % jn;
-                double s = 0.0;
-                for (int kk = 0; kk < kc; ++kk) s += As[r * ENS_TILE + kk] * Xs[kk * SJT + j];
-                acc[u] += s;
-            }
-        }
-    }
-    __syncthreads();
-#pragma unroll
-    for (int u = 0; u < 16; ++u) {
-        const int o = threadIdx.x + u * 256;
-        if (o < nout) {
-            const int r = o / jn, j = o % jn;
-            fr[(int64_t)(a + r) * J + j0 + j] = acc[u];
-        }
-    }
-}
-
-__global__ void k_bscatter(MfDev d, int item0, const double* __restrict__ FR, double* __restrict__ X, int64_t N, int J,
-                           int64_t nidx) {
+// forward (bwd=0): fr[k+r0+i] -= sum_{t<k} F[k+r0+i][t] fr[t]
+// backward (bwd=1): x[idx[r0+i]] = -sum_{t<m} F[r0+i][t] fr[t]
+__global__ void __launch_bounds__(256) k_sgemm(MfDev d, int item0, const double* __restrict__ F,
+                                               double* __restrict__ FR, double* __restrict__ X, int64_t N, int J,
+                                               int64_t nidx, int bwd) {
+    constexpr int KC = 32;                   // inner-dimension chunk
+    __shared__ double As[ENS_TILE][KC + 1];
+    __shared__ double Bs[KC][SJT];
     const int* it = d.work + 4LL * (item0 + blockIdx.x);
     const int f = it[0], r0 = it[1];
     const int mat = blockIdx.y;
-    const int k = d.k[f];
-    const int rows = min(ENS_VEC_ROWS, k - r0);
-    const int64_t fo = d.idx_off[f];
-    const double* fr = FR + (int64_t)mat * nidx * J;
+    const int j0 = blockIdx.z * SJT;
+    const int jn = min(SJT, J - j0);
+    const int m = d.m[f], k = d.k[f];
+    const int rbase = bwd ? r0 : k + r0;
+    const int nr = min(ENS_TILE, (bwd ? k : m) - rbase);
+    const int K = bwd ? m : k;
+    const double* base = F + (int64_t)mat * d.storage + d.off[f];
+    double* fr = FR + (int64_t)mat * nidx * J + d.idx_off[f] * J;
+    const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+    double acc[4][2] = {};
+    for (int t0 = 0; t0 < K; t0 += KC) {
+        const int kc = min(KC, K - t0);
+        __syncthreads();
+        for (int e = threadIdx.x; e < ENS_TILE * KC; e += blockDim.x) {
+            const int r = e / KC, kk = e % KC;
+            As[r][kk] = (r < nr && kk < kc) ? base[(int64_t)(rbase + r) * m + t0 + kk] : 0.0;
+        }
+        for (int e = threadIdx.x; e < KC * SJT; e += blockDim.x) {
+            const int kk = e / SJT, j = e % SJT;
+            Bs[kk][j] = (kk < kc && j < jn) ? fr[(int64_t)(t0 + kk) * J + j0 + j] : 0.0;
+        }
+        __syncthreads();
+        for (int kk = 0; kk < kc; ++kk) {
+            double av[4], bv[2];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) av[i] = As[ty + 16 * i][kk];
+#pragma unroll
+            for (int j = 0; j < 2; ++j) bv[j] = Bs[kk][tx + 16 * j];
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+#pragma unroll
+                for (int j = 0; j < 2; ++j) acc[i][j] = fma(av[i], bv[j], acc[i][j]);
+        }
+    }
     double* x = X + (int64_t)mat * N * J;
-    for (int t = threadIdx.x; t < rows * J; t += blockDim.x) {
-        const int i = r0 + t / J, j = t % J;
-        x[(int64_t)d.idx[fo + i] * J + j] = fr[(fo + i) * J + j];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const int r = ty + 16 * i;
+        if (r >= nr) continue;
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+            const int jj = tx + 16 * j;
+            if (jj >= jn) continue;
+            if (bwd)
+                x[(int64_t)d.idx[d.idx_off[f] + rbase + r] * J + j0 + jj] = -acc[i][j];
+            else
+                fr[(int64_t)(rbase + r) * J + j0 + jj] -= acc[i][j];
+        }
     }
 }
 
 // ---------------------------------------------------------------------------
 // host drivers
 // ---------------------------------------------------------------------------
-static const size_t SM_DIAG = sizeof(double) * (ENS_PW * 2 * ENS_PW + ENS_PW);
-static const size_t SM_HP = sizeof(double) * (ENS_PW * ENS_PW + ENS_PW * ENS_TILE);
-static const size_t SM_UP = sizeof(double) * (ENS_PW * (ENS_TILE + 1) + ENS_PW * ENS_TILE);
-static const size_t SM_GP = sizeof(double) * (ENS_PW * ENS_PW + ENS_TILE * ENS_PW);
-static const size_t SM_FP = sizeof(double) * (ENS_TILE * ENS_PW + ENS_PW * SJT);
-static const size_t SM_BP = sizeof(double) * (ENS_PW * ENS_TILE + ENS_TILE * SJT);
+static const size_t SM_HP = sizeof(double) * (ENS_PW * LDA + ENS_PW * ENS_TILE);
+static const size_t SM_UP = sizeof(double) * (ENS_TILE * LDA + ENS_PW * ENS_TILE);
+static const size_t SM_GP = sizeof(double) * (ENS_TILE * LDA + ENS_PW * ENS_TILE);
 
 int mf_setup(ens_ctx* c) {
-    ENS_CK(cudaFuncSetAttribute(k_diag, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SM_DIAG));
     ENS_CK(cudaFuncSetAttribute(k_hpanel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SM_HP));
     ENS_CK(cudaFuncSetAttribute(k_update, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SM_UP));
     ENS_CK(cudaFuncSetAttribute(k_gpanel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SM_GP));
-    ENS_CK(cudaFuncSetAttribute(k_fpanel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SM_FP));
-    ENS_CK(cudaFuncSetAttribute(k_bpanel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SM_BP));
     (void)c;
     return ENS_OK;
 }
@@ -469,7 +515,7 @@ int mf_factor(ens_ctx* c, cudaStream_t s, const double* as_vals, int32_t* n_pert
                 k_extadd<<<dim3(n, 2), 256, 0, s>>>(d, off, c->fronts);
                 break;
             case OP_DIAG:
-                k_diag<<<dim3(n, 2), 256, SM_DIAG, s>>>(d, off, c->fronts, c->d_count);
+                k_diag<<<dim3(n, 2), 256, 0, s>>>(d, off, c->fronts, c->d_count);
                 break;
             case OP_HPANEL:
                 k_hpanel<<<dim3(n, 2), 256, SM_HP, s>>>(d, off, c->fronts);
@@ -515,8 +561,8 @@ int mf_solve(ens_ctx* c, cudaStream_t s, const double* r, double* z) {
             case SOP_FEXT:
                 k_fext<<<dim3(n, 2), 256, 0, s>>>(d, off, c->frvec, J, nidx);
                 break;
-            case SOP_FPANEL:
-                k_fpanel<<<dim3(n, 2, zc), 256, SM_FP, s>>>(d, off, c->fronts, c->frvec, J, nidx);
+            case SOP_FGEMM:
+                k_sgemm<<<dim3(n, 2, zc), 256, 0, s>>>(d, off, c->fronts, c->frvec, z, N, J, nidx, 0);
                 break;
             default:
                 ens_set_error("bad fwd op", __FILE__, __LINE__);
@@ -533,11 +579,8 @@ int mf_solve(ens_ctx* c, cudaStream_t s, const double* r, double* z) {
             case SOP_BGATHER:
                 k_bgather<<<dim3(n, 2), 256, 0, s>>>(d, off, z, c->frvec, N, J, nidx);
                 break;
-            case SOP_BPANEL:
-                k_bpanel<<<dim3(n, 2, zc), 256, SM_BP, s>>>(d, off, c->fronts, c->frvec, J, nidx);
-                break;
-            case SOP_BSCATTER:
-                k_bscatter<<<dim3(n, 2), 256, 0, s>>>(d, off, c->frvec, z, N, J, nidx);
+            case SOP_BGEMM:
+                k_sgemm<<<dim3(n, 2, zc), 256, 0, s>>>(d, off, c->fronts, c->frvec, z, N, J, nidx, 1);
                 break;
             default:
                 ens_set_error("bad bwd op", __FILE__, __LINE__);

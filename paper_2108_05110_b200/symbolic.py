@@ -384,7 +384,7 @@ def analyse(disc, leaf=LEAF_NODES, pw=PW):
 
 # op codes (must match csrc/mf.cu)
 OP_ZERO, OP_ORIG, OP_EXTADD, OP_DIAG, OP_HPANEL, OP_UPDATE, OP_GPANEL = range(7)
-SOP_FINIT, SOP_FEXT, SOP_FPANEL, SOP_BGATHER, SOP_BPANEL, SOP_BSCATTER = range(6)
+SOP_FINIT, SOP_FEXT, SOP_FGEMM, SOP_BGATHER, SOP_BGEMM = range(5)
 EXT_ROWS = 8      # child-CB rows per extend-add work item
 VEC_ROWS = 64     # front-vector rows per init/gather/scatter work item
 
@@ -438,14 +438,16 @@ def build_schedule(plan: FactorPlan, pw=PW):
             if rows:
                 off, n = add(rows)
                 fl.append((OP_EXTADD, L, off, n, r))
+        # block sweep (Gauss-Jordan) over the front's pivot panels; the update
+        # covers every row/column outside the panel (index r' -> r' < a ? r' : r' + pw)
         npan = int(max((-(-fk[f] // pw) for f in fronts), default=0))
         for p in range(npan):
             a = p * pw
             act = [f for f in fronts if fk[f] > a]
             d, h, u, gg = [], [], [], []
             for f in act:
-                b = min(a + pw, fk[f])
-                t = fm[f] - b
+                pwf = min(pw, fk[f] - a)
+                t = fm[f] - pwf
                 d.append((f, a))
                 for c0 in range(0, t, TILE):
                     h.append((f, a, c0))
@@ -456,7 +458,9 @@ def build_schedule(plan: FactorPlan, pw=PW):
                 if rows:
                     off, n = add(rows)
                     fl.append((op, L, off, n, p))
-    # solve schedule
+    # solve schedule: after the sweep a front holds [-F11^-1, F11^-1 F12; F21 F11^-1, S]
+    #   forward  fr[k:m] -= F_CP fr[0:k]           (SOP_FGEMM, rows of the CB)
+    #   backward x[piv]   = -[F_PP F_PC] [fr_P; x_C] (SOP_BGEMM, rows of the pivots)
     fwd, bwd = [], []
     for L in range(plan.nlevels):
         fronts = np.arange(plan.level_front_off[L], plan.level_front_off[L + 1])
@@ -474,33 +478,19 @@ def build_schedule(plan: FactorPlan, pw=PW):
             if rows:
                 off, n = add(rows)
                 fwd.append((SOP_FEXT, L, off, n, r))
-        npan = int(max((-(-fk[f] // pw) for f in fronts), default=0))
-        for p in range(npan):
-            a = p * pw
-            rows = []
-            for f in fronts:
-                if fk[f] > a:
-                    b = min(a + pw, fk[f])
-                    for r0 in range(0, fm[f] - b, TILE):
-                        rows.append((f, a, r0))
-            if rows:
-                off, n = add(rows)
-                fwd.append((SOP_FPANEL, L, off, n, p))
+        rows = [(f, r0) for f in fronts for r0 in range(0, fm[f] - fk[f], TILE)]
+        if rows:
+            off, n = add(rows)
+            fwd.append((SOP_FGEMM, L, off, n, 0))
     for L in reversed(range(plan.nlevels)):
         fronts = np.arange(plan.level_front_off[L], plan.level_front_off[L + 1])
         rows = [(f, fk[f] + r0) for f in fronts for r0 in range(0, fm[f] - fk[f], VEC_ROWS)]
         if rows:
             off, n = add(rows)
             bwd.append((SOP_BGATHER, L, off, n, 0))
-        npan = int(max((-(-fk[f] // pw) for f in fronts), default=0))
-        for p in reversed(range(npan)):
-            a = p * pw
-            rows = [(f, a) for f in fronts if fk[f] > a]
-            off, n = add(rows)
-            bwd.append((SOP_BPANEL, L, off, n, p))
-        rows = [(f, r0) for f in fronts for r0 in range(0, fk[f], VEC_ROWS)]
+        rows = [(f, r0) for f in fronts for r0 in range(0, fk[f], TILE)]
         off, n = add(rows)
-        bwd.append((SOP_BSCATTER, L, off, n, 0))
+        bwd.append((SOP_BGEMM, L, off, n, 0))
     work = np.vstack(items) if items else np.zeros((0, 4), np.int32)
     return dict(work=np.ascontiguousarray(work.astype(np.int32)),
                 factor=np.array(fl, dtype=np.int64).reshape(-1, 5),

@@ -1,7 +1,7 @@
-"""Numpy emulation of the device multifrontal factorisation / solve (test helper).
+"""Numpy emulation of the device multifrontal sweep factorisation / solve (test helper).
 
 Executes the exact launch schedule of `symbolic.build_schedule` with dense
-numpy ops, so the plan (ordering, maps, panels, explicit-inverse algebra) is
+numpy ops, so the plan (ordering, maps, panels, block-sweep algebra) is
 verified on CPU against a direct solve before any GPU run.
 """
 
@@ -10,8 +10,14 @@ import numpy as np
 from paper_2108_05110_b200 import symbolic as S
 
 
+def _outside(idx, a, pw):
+    """Map outside-panel indices r' to front rows: r' < a ? r' : r' + pw."""
+    idx = np.asarray(idx)
+    return np.where(idx < a, idx, idx + pw)
+
+
 def factor(plan, as_vals, pw=S.PW):
-    """Return the per-matrix front storage after factorisation (flat float64)."""
+    """Return the per-matrix front storage after the sweep (flat float64)."""
     st = np.zeros(plan.front_storage)
     src = np.concatenate([as_vals, plan.bsrc_vals])
     work = plan.schedule["work"]
@@ -36,34 +42,28 @@ def factor(plan, as_vals, pw=S.PW):
                 rows = np.arange(r0, min(r0 + S.EXT_ROWS, len(mp)))
                 F, P = front(c), front(p)
                 P[np.ix_(mp[rows], mp)] += F[kc + rows][:, kc:]
-        elif op == S.OP_DIAG:
-            for f, a, _, _ in items:
+        else:
+            for f, a, x0, y0 in items:
                 F = front(f)
-                b = min(a + pw, fk[f])
-                F[a:b, a:b] = np.linalg.inv(F[a:b, a:b])
-        elif op == S.OP_HPANEL:
-            for f, a, c0, _ in items:
-                F = front(f)
-                b = min(a + pw, fk[f])
-                cols = slice(b + c0, min(b + c0 + S.TILE, fm[f]))
-                F[a:b, cols] = -F[a:b, a:b] @ F[a:b, cols]
-        elif op == S.OP_UPDATE:
-            for f, a, r0, c0 in items:
-                F = front(f)
-                b = min(a + pw, fk[f])
-                rows = slice(b + r0, min(b + r0 + S.TILE, fm[f]))
-                cols = slice(b + c0, min(b + c0 + S.TILE, fm[f]))
-                F[rows, cols] += F[rows, a:b] @ F[a:b, cols]
-        elif op == S.OP_GPANEL:
-            for f, a, r0, _ in items:
-                F = front(f)
-                b = min(a + pw, fk[f])
-                rows = slice(b + r0, min(b + r0 + S.TILE, fm[f]))
-                F[rows, a:b] = -F[rows, a:b] @ F[a:b, a:b]
+                pwf = min(pw, fk[f] - a)
+                P = slice(a, a + pwf)
+                t = fm[f] - pwf
+                if op == S.OP_DIAG:
+                    F[P, P] = -np.linalg.inv(F[P, P])
+                elif op == S.OP_HPANEL:
+                    cols = _outside(np.arange(x0, min(x0 + S.TILE, t)), a, pwf)
+                    F[P, cols] = -F[P, P] @ F[P, cols]
+                elif op == S.OP_UPDATE:
+                    rows = _outside(np.arange(x0, min(x0 + S.TILE, t)), a, pwf)
+                    cols = _outside(np.arange(y0, min(y0 + S.TILE, t)), a, pwf)
+                    F[np.ix_(rows, cols)] -= F[rows, P] @ F[P, cols]
+                elif op == S.OP_GPANEL:
+                    rows = _outside(np.arange(x0, min(x0 + S.TILE, t)), a, pwf)
+                    F[rows, P] = -F[rows, P] @ F[P, P]
     return st
 
 
-def solve(plan, st, rhs, pw=S.PW):
+def solve(plan, st, rhs):
     """Apply the factorisation to rhs (n_total_internal, J); returns x (free rows)."""
     work = plan.schedule["work"]
     fm, fk, off = plan.f_m, plan.f_k, plan.f_off
@@ -80,37 +80,27 @@ def solve(plan, st, rhs, pw=S.PW):
 
     for op, L, io, n, arg in plan.schedule["fwd"]:
         for it in work[io:io + n]:
-            f = it[0]
+            f, r0 = it[0], it[1]
             if op == S.SOP_FINIT:
-                r0 = it[1]
                 rows = np.arange(r0, min(r0 + S.VEC_ROWS, fm[f]))
-                ii = idx(f)
-                fr[f][rows] = np.where((rows < fk[f])[:, None], rhs[ii[rows]], 0.0)
+                fr[f][rows] = np.where((rows < fk[f])[:, None], rhs[idx(f)[rows]], 0.0)
             elif op == S.SOP_FEXT:
-                c, r0 = it[0], it[1]
+                c = f
                 p = plan.f_parent[c]
                 mp = plan.f_cmap[plan.f_cmap_off[c]:plan.f_cmap_off[c + 1]]
                 rows = np.arange(r0, min(r0 + S.VEC_ROWS, len(mp)))
                 fr[p][mp[rows]] += fr[c][fk[c] + rows]
-            elif op == S.SOP_FPANEL:
-                a, r0 = it[1], it[2]
-                b = min(a + pw, fk[f])
-                rows = slice(b + r0, min(b + r0 + S.TILE, fm[f]))
-                fr[f][rows] += front(f)[rows, a:b] @ fr[f][a:b]
+            elif op == S.SOP_FGEMM:
+                k = fk[f]
+                rows = slice(k + r0, min(k + r0 + S.TILE, fm[f]))
+                fr[f][rows] -= front(f)[rows, :k] @ fr[f][:k]
     for op, L, io, n, arg in plan.schedule["bwd"]:
         for it in work[io:io + n]:
-            f = it[0]
+            f, r0 = it[0], it[1]
             if op == S.SOP_BGATHER:
-                r0 = it[1]
                 rows = np.arange(r0, min(r0 + S.VEC_ROWS, fm[f]))
                 fr[f][rows] = x[idx(f)[rows]]
-            elif op == S.SOP_BPANEL:
-                a = it[1]
-                b = min(a + pw, fk[f])
-                F = front(f)
-                fr[f][a:b] = F[a:b, a:b] @ fr[f][a:b] + F[a:b, b:] @ fr[f][b:]
-            elif op == S.SOP_BSCATTER:
-                r0 = it[1]
-                rows = np.arange(r0, min(r0 + S.VEC_ROWS, fk[f]))
-                x[idx(f)[rows]] = fr[f][rows]
+            elif op == S.SOP_BGEMM:
+                rows = np.arange(r0, min(r0 + S.TILE, fk[f]))
+                x[idx(f)[rows]] = -front(f)[rows, :] @ fr[f]
     return x
