@@ -17,36 +17,7 @@
 
 #include "ens_internal.cuh"
 
-enum { OP_ZERO = 0, OP_ORIG, OP_EXTADD, OP_DIAG, OP_HPANEL, OP_UPDATE, OP_GPANEL };
-enum { SOP_FINIT = 0, SOP_FEXT, SOP_FGEMM, SOP_BGATHER, SOP_BGEMM };
-
-struct MfDev {
-    const int32_t* m;
-    const int32_t* k;
-    const int64_t* off;
-    const int64_t* idx_off;
-    const int32_t* idx;
-    const int32_t* parent;
-    const int64_t* cmap_off;
-    const int32_t* cmap;
-    const int32_t* work;
-    int64_t storage;
-};
-
-static MfDev mfdev(const ens_ctx* c) {
-    MfDev d;
-    d.m = c->p.f_m;
-    d.k = c->p.f_k;
-    d.off = c->p.f_off;
-    d.idx_off = c->p.f_idx_off;
-    d.idx = c->p.f_idx;
-    d.parent = c->p.f_parent;
-    d.cmap_off = c->p.f_cmap_off;
-    d.cmap = c->p.f_cmap;
-    d.work = c->p.work;
-    d.storage = c->p.front_storage;
-    return d;
-}
+#include "ens_mf_common.cuh"
 
 // outside-panel index -> front row/col
 __device__ __forceinline__ int outside(int r, int a, int pw) { return r < a ? r : r + pw; }
@@ -359,121 +330,6 @@ __global__ void __launch_bounds__(256) k_gpanel(MfDev d, int item0, double* __re
 }
 
 // ---------------------------------------------------------------------------
-// solve kernels: grid = (items, 2 matrices[, column chunks of 32])
-// ---------------------------------------------------------------------------
-#define SJT 32
-
-__global__ void k_finit(MfDev d, int item0, const double* __restrict__ B, double* __restrict__ FR, int64_t N, int J,
-                        int64_t nidx) {
-    const int* it = d.work + 4LL * (item0 + blockIdx.x);
-    const int f = it[0], r0 = it[1];
-    const int mat = blockIdx.y;
-    const int m = d.m[f], k = d.k[f];
-    const int rows = min(ENS_VEC_ROWS, m - r0);
-    const int64_t fo = d.idx_off[f];
-    double* fr = FR + (int64_t)mat * nidx * J;
-    const double* b = B + (int64_t)mat * N * J;
-    for (int t = threadIdx.x; t < rows * J; t += blockDim.x) {
-        const int i = r0 + t / J, j = t % J;
-        fr[(fo + i) * J + j] = i < k ? b[(int64_t)d.idx[fo + i] * J + j] : 0.0;
-    }
-}
-
-__global__ void k_fext(MfDev d, int item0, double* __restrict__ FR, int J, int64_t nidx) {
-    const int* it = d.work + 4LL * (item0 + blockIdx.x);
-    const int c = it[0], r0 = it[1];
-    const int mat = blockIdx.y;
-    const int p = d.parent[c];
-    const int kc = d.k[c], cbn = d.m[c] - kc;
-    const int rows = min(ENS_VEC_ROWS, cbn - r0);
-    const int32_t* map = d.cmap + d.cmap_off[c];
-    double* fr = FR + (int64_t)mat * nidx * J;
-    const int64_t co = d.idx_off[c], po = d.idx_off[p];
-    for (int t = threadIdx.x; t < rows * J; t += blockDim.x) {
-        const int i = r0 + t / J, j = t % J;
-        fr[(po + map[i]) * J + j] += fr[(co + kc + i) * J + j];
-    }
-}
-
-__global__ void k_bgather(MfDev d, int item0, const double* __restrict__ X, double* __restrict__ FR, int64_t N, int J,
-                          int64_t nidx) {
-    const int* it = d.work + 4LL * (item0 + blockIdx.x);
-    const int f = it[0], r0 = it[1];
-    const int mat = blockIdx.y;
-    const int m = d.m[f];
-    const int rows = min(ENS_VEC_ROWS, m - r0);
-    const int64_t fo = d.idx_off[f];
-    double* fr = FR + (int64_t)mat * nidx * J;
-    const double* x = X + (int64_t)mat * N * J;
-    for (int t = threadIdx.x; t < rows * J; t += blockDim.x) {
-        const int i = r0 + t / J, j = t % J;
-        fr[(fo + i) * J + j] = x[(int64_t)d.idx[fo + i] * J + j];
-    }
-}
-
-// forward (bwd=0): fr[k+r0+i] -= sum_{t<k} F[k+r0+i][t] fr[t]
-// backward (bwd=1): x[idx[r0+i]] = -sum_{t<m} F[r0+i][t] fr[t]
-__global__ void __launch_bounds__(256) k_sgemm(MfDev d, int item0, const double* __restrict__ F,
-                                               double* __restrict__ FR, double* __restrict__ X, int64_t N, int J,
-                                               int64_t nidx, int bwd) {
-    constexpr int KC = 32;                   // inner-dimension chunk
-    __shared__ double As[ENS_TILE][KC + 1];
-    __shared__ double Bs[KC][SJT];
-    const int* it = d.work + 4LL * (item0 + blockIdx.x);
-    const int f = it[0], r0 = it[1];
-    const int mat = blockIdx.y;
-    const int j0 = blockIdx.z * SJT;
-    const int jn = min(SJT, J - j0);
-    const int m = d.m[f], k = d.k[f];
-    const int rbase = bwd ? r0 : k + r0;
-    const int nr = min(ENS_TILE, (bwd ? k : m) - rbase);
-    const int K = bwd ? m : k;
-    const double* base = F + (int64_t)mat * d.storage + d.off[f];
-    double* fr = FR + (int64_t)mat * nidx * J + d.idx_off[f] * J;
-    const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
-    double acc[4][2] = {};
-    for (int t0 = 0; t0 < K; t0 += KC) {
-        const int kc = min(KC, K - t0);
-        __syncthreads();
-        for (int e = threadIdx.x; e < ENS_TILE * KC; e += blockDim.x) {
-            const int r = e / KC, kk = e % KC;
-            As[r][kk] = (r < nr && kk < kc) ? base[(int64_t)(rbase + r) * m + t0 + kk] : 0.0;
-        }
-        for (int e = threadIdx.x; e < KC * SJT; e += blockDim.x) {
-            const int kk = e / SJT, j = e % SJT;
-            Bs[kk][j] = (kk < kc && j < jn) ? fr[(int64_t)(t0 + kk) * J + j0 + j] : 0.0;
-        }
-        __syncthreads();
-        for (int kk = 0; kk < kc; ++kk) {
-            double av[4], bv[2];
-#pragma unroll
-            for (int i = 0; i < 4; ++i) av[i] = As[ty + 16 * i][kk];
-#pragma unroll
-            for (int j = 0; j < 2; ++j) bv[j] = Bs[kk][tx + 16 * j];
-#pragma unroll
-            for (int i = 0; i < 4; ++i)
-#pragma unroll
-                for (int j = 0; j < 2; ++j) acc[i][j] = fma(av[i], bv[j], acc[i][j]);
-        }
-    }
-    double* x = X + (int64_t)mat * N * J;
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-        const int r = ty + 16 * i;
-        if (r >= nr) continue;
-#pragma unroll
-        for (int j = 0; j < 2; ++j) {
-            const int jj = tx + 16 * j;
-            if (jj >= jn) continue;
-            if (bwd)
-                x[(int64_t)d.idx[d.idx_off[f] + rbase + r] * J + j0 + jj] = -acc[i][j];
-            else
-                fr[(int64_t)(rbase + r) * J + j0 + jj] -= acc[i][j];
-        }
-    }
-}
-
-// ---------------------------------------------------------------------------
 // host drivers
 // ---------------------------------------------------------------------------
 static const size_t SM_HP = sizeof(double) * (ENS_PW * LDA + ENS_PW * ENS_TILE);
@@ -540,53 +396,3 @@ int mf_factor(ens_ctx* c, cudaStream_t s, const double* as_vals, int32_t* n_pert
     return ENS_OK;
 }
 
-int mf_solve(ens_ctx* c, cudaStream_t s, const double* r, double* z) {
-    MfDev d = mfdev(c);
-    const int J = c->J;
-    const int64_t N = c->n_total, nidx = c->p.n_idx;
-    const unsigned zc = (unsigned)((J + SJT - 1) / SJT);
-    {
-        const int rc = launch_copy_cons(c, s, r, z);
-        if (rc != ENS_OK) return rc;
-    }
-    const int64_t nf = (int64_t)c->sched_fwd.size() / 5;
-    for (int64_t i = 0; i < nf; ++i) {
-        const int64_t* q = &c->sched_fwd[5 * i];
-        const int op = (int)q[0], off = (int)q[2], n = (int)q[3];
-        if (n == 0) continue;
-        switch (op) {
-            case SOP_FINIT:
-                k_finit<<<dim3(n, 2), 256, 0, s>>>(d, off, r, c->frvec, N, J, nidx);
-                break;
-            case SOP_FEXT:
-                k_fext<<<dim3(n, 2), 256, 0, s>>>(d, off, c->frvec, J, nidx);
-                break;
-            case SOP_FGEMM:
-                k_sgemm<<<dim3(n, 2, zc), 256, 0, s>>>(d, off, c->fronts, c->frvec, z, N, J, nidx, 0);
-                break;
-            default:
-                ens_set_error("bad fwd op", __FILE__, __LINE__);
-                return ENS_EINVAL;
-        }
-        ENS_CKL();
-    }
-    const int64_t nb = (int64_t)c->sched_bwd.size() / 5;
-    for (int64_t i = 0; i < nb; ++i) {
-        const int64_t* q = &c->sched_bwd[5 * i];
-        const int op = (int)q[0], off = (int)q[2], n = (int)q[3];
-        if (n == 0) continue;
-        switch (op) {
-            case SOP_BGATHER:
-                k_bgather<<<dim3(n, 2), 256, 0, s>>>(d, off, z, c->frvec, N, J, nidx);
-                break;
-            case SOP_BGEMM:
-                k_sgemm<<<dim3(n, 2, zc), 256, 0, s>>>(d, off, c->fronts, c->frvec, z, N, J, nidx, 1);
-                break;
-            default:
-                ens_set_error("bad bwd op", __FILE__, __LINE__);
-                return ENS_EINVAL;
-        }
-        ENS_CKL();
-    }
-    return ENS_OK;
-}

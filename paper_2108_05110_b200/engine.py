@@ -27,6 +27,7 @@ import scipy.sparse as sp
 import torch
 
 from . import _native as N
+from . import exchange as XC
 from . import fe
 from . import symbolic as S
 from .ensemble import viscosity_stats
@@ -200,7 +201,19 @@ class DeviceState:
 class Engine:
     """Device-resident ensemble on one GPU (member columns [j0, j0+J) of J_total)."""
 
-    def __init__(self, disc, config, j0=0, J=None, device=None, comm=None, restart=8, max_restarts=20, rtol=1e-12):
+    def __init__(self, disc, config, j0=0, J=None, device=None, comm=None, restart=8, max_restarts=20, rtol=1e-12,
+                 refactor="adaptive", lag_max_iters=3, lag_max_steps=50):
+        """``refactor``: "always" rebuilds the LU preconditioner every step (the
+        reference refactorises every sub-step, `stepper.py:216`); "adaptive"
+        keeps the last factorisation while FGMRES needs <= ``lag_max_iters``
+        iterations (at most ``lag_max_steps`` steps).  Either way every solve is
+        converged to the same true residual ``rtol`` on the *current* matrix."""
+        if refactor not in ("always", "adaptive"):
+            raise ValueError("refactor must be 'always' or 'adaptive'")
+        self.refactor, self.lag_max_iters, self.lag_max_steps = refactor, lag_max_iters, lag_max_steps
+        self.factored = False
+        self.since_factor = 0
+        self.n_factor = 0
         if not torch.cuda.is_available():
             raise RuntimeError("the B200 time-step engine needs a CUDA device (no CPU fallback)")
         self.lib = N.load()
@@ -447,8 +460,7 @@ class Engine:
         lib, ctx, s = self.lib, self.ctx, self.sptr
         X = self.X[self.cur]
         N.check(lib.ens_member_sums(ctx, s, _dptr(X), _dptr(self.sums)), "ens_member_sums")
-        if self.comm is not None:
-            torch.distributed.all_reduce(self.sums, op=torch.distributed.ReduceOp.SUM, group=self.comm)
+        XC.allreduce_member_sums(self.sums, self.comm)
         torch.mul(self.sums, 1.0 / self.J_total, out=self.means)
         self.means_valid = True
 
@@ -463,34 +475,49 @@ class Engine:
                             C.byref(loads) if loads is not None else None, _dptr(self.rhs)), "ens_rhs")
         N.check(lib.ens_member_pass(ctx, s, _dptr(X), _dptr(self.means), _dptr(self.rhs), _dptr(self.maxsq)),
                 "ens_member_pass")
-        if self.comm is not None:
-            torch.distributed.all_reduce(self.maxsq, op=torch.distributed.ReduceOp.MAX, group=self.comm)
+        XC.allreduce_eddy_max(self.maxsq, self.comm)
         bvals, keep2 = self._data(boundary, "bc", t_next)
         N.check(lib.ens_apply_bc(ctx, s, C.byref(bvals), _dptr(self.rhs)), "ens_apply_bc")
         N.check(lib.ens_assemble(ctx, s, _dptr(self.base), _dptr(self.means), _dptr(self.maxsq), self.two_mu_dt,
                                  _dptr(self.as_vals)), "ens_assemble")
-        npert = N.I32(0)
-        N.check(lib.ens_factor(ctx, s, _dptr(self.as_vals), C.byref(npert)), "ens_factor")
+        need = (self.refactor == "always" or not self.factored or self.since_factor >= self.lag_max_steps
+                or self.last_iters > self.lag_max_iters)
+        if need:
+            self._factor()
+        else:
+            self.since_factor += 1
         self._retire(nxt)
         Xn = self.X[nxt]
         Xn.copy_(X)                                   # warm start from level n
-        iters = N.I32(0)
-        rel = (N.F64 * 2)()
-        code = lib.ens_solve(ctx, s, _dptr(self.as_vals), _dptr(self.rhs), _dptr(Xn), self.rtol, self.restart,
-                             self.max_restarts, C.byref(iters), rel)
-        self.last_iters, self.last_pert, self.last_relres = int(iters.value), int(npert.value), (rel[0], rel[1])
+        code, iters, rel = self._solve(Xn)
+        if code == N.ENS_ENOCONV and not need:        # stale preconditioner: rebuild and retry once
+            self._factor()
+            Xn.copy_(X)
+            code, iters2, rel = self._solve(Xn)
+            iters += iters2
+        self.last_iters, self.last_relres = iters, rel
         N.check(code, "ens_solve")
         N.check(lib.ens_epilogue(ctx, s, _dptr(Xn), _dptr(self.Pq[nxt])), "ens_epilogue")
         del keep1, keep2
         self.gen[nxt] += 1
         self.cur = nxt
         self.means_valid = False
-        res = max(self.last_relres)
-        if self.comm is not None:
-            t = torch.tensor([res], dtype=torch.float64, device=self.dev)
-            torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX, group=self.comm)
-            res = float(t.item())
-        return res
+        return XC.allreduce_max_scalar(max(self.last_relres), self.comm, self.dev)
+
+    def _factor(self):
+        npert = N.I32(0)
+        N.check(self.lib.ens_factor(self.ctx, self.sptr, _dptr(self.as_vals), C.byref(npert)), "ens_factor")
+        self.last_pert = int(npert.value)
+        self.factored = True
+        self.since_factor = 0
+        self.n_factor += 1
+
+    def _solve(self, Xn):
+        iters = N.I32(0)
+        rel = (N.F64 * 2)()
+        code = self.lib.ens_solve(self.ctx, self.sptr, _dptr(self.as_vals), _dptr(self.rhs), _dptr(Xn), self.rtol,
+                                  self.restart, self.max_restarts, C.byref(iters), rel)
+        return code, int(iters.value), (rel[0], rel[1])
 
     def diagnostics(self):
         """Device-side _record (stepper.py:432-439) of the current state."""
@@ -512,9 +539,8 @@ class Engine:
         return out
 
     def factor(self):
-        npert = N.I32(0)
-        N.check(self.lib.ens_factor(self.ctx, self.sptr, _dptr(self.as_vals), C.byref(npert)), "ens_factor")
-        return int(npert.value)
+        self._factor()
+        return self.last_pert
 
     def precond(self, r, out=None):
         out = torch.zeros_like(r) if out is None else out

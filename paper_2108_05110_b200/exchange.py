@@ -1,0 +1,51 @@
+"""The two per-step collectives of the member-sharded scheme.
+
+With members sharded contiguously over ranks (one GPU each), a time-step
+needs exactly two exchanges, both over the whole process group:
+
+  1. allreduce SUM of the member-summed fields [sum_j v_j | sum_j w_j]
+     (2 n_vel doubles) -> every rank gets the ensemble means that drive the
+     shared matrices and the fluctuations (`ensemble.py:216-224`);
+  2. allreduce MAX of the per-rank maxima max_j |z'_j(x_q)|^2 at every
+     quadrature point for both families (2 nt 7 doubles) -> the eddy
+     viscosity nu_T of both shared matrices (`ensemble.py:227-238`).
+
+Everything else (right-hand sides, the replicated matrix assembly and
+factorisation, the column-batched solve) is rank-local.  Over NCCL on one
+B200 node these run on the NVLink/NVSwitch fabric; the same calls run over
+gloo on CPU tensors in the tests.
+"""
+
+from __future__ import annotations
+
+import torch.distributed as dist
+
+
+def member_slice(J_total: int, rank: int, world: int):
+    """(first member, count) of a rank's contiguous shard."""
+    base, extra = divmod(J_total, world)
+    j0 = rank * base + min(rank, extra)
+    return j0, base + (1 if rank < extra else 0)
+
+
+def allreduce_member_sums(sums, comm=None):
+    """In place: sums <- sum over ranks (exchange 1)."""
+    if comm is not None:
+        dist.all_reduce(sums, op=dist.ReduceOp.SUM, group=comm)
+    return sums
+
+
+def allreduce_eddy_max(maxsq, comm=None):
+    """In place: maxsq <- max over ranks (exchange 2)."""
+    if comm is not None:
+        dist.all_reduce(maxsq, op=dist.ReduceOp.MAX, group=comm)
+    return maxsq
+
+
+def allreduce_max_scalar(value: float, comm=None, device=None) -> float:
+    if comm is None:
+        return value
+    import torch
+    t = torch.tensor([value], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX, group=comm)
+    return float(t.item())

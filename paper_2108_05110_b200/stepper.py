@@ -102,12 +102,27 @@ class Problem:
 # engine cache
 # ----------------------------------------------------------------------
 
-_SOLVER_OPTS = dict(rtol=DEFAULT_RTOL, restart=8, max_restarts=20)
+_SOLVER_OPTS = dict(rtol=DEFAULT_RTOL, restart=8, max_restarts=20, refactor="adaptive", lag_max_iters=3,
+                    lag_max_steps=50)
 
 
 def set_solver_options(**kw):
-    """Krylov options for new engines: rtol (true relative residual), restart, max_restarts."""
+    """Solver options for new engines.
+
+    rtol: per-member true relative residual of every sub-step solve;
+    restart / max_restarts: FGMRES cycle length and count;
+    refactor: "always" (rebuild the LU preconditioner each step, as the
+    reference refactorises each sub-step) or "adaptive" (reuse it while FGMRES
+    needs <= lag_max_iters iterations, at most lag_max_steps steps).
+    """
+    unknown = set(kw) - set(_SOLVER_OPTS)
+    if unknown:
+        raise ValueError(f"unknown solver options {sorted(unknown)}")
     _SOLVER_OPTS.update(kw)
+
+
+def get_solver_options():
+    return dict(_SOLVER_OPTS)
 
 
 def get_engine(disc, config, j0=0, J=None, comm=None, device=None):
@@ -202,11 +217,7 @@ def _record(report, n, engine, comm=None):
     report.member_gradw_sq[n] = d["gradw"]
 
 
-def member_slice(J_total, rank, world):
-    """Contiguous member shard of one rank."""
-    base, extra = divmod(J_total, world)
-    j0 = rank * base + min(rank, extra)
-    return j0, base + (1 if rank < extra else 0)
+from .exchange import member_slice  # noqa: E402  (re-exported)
 
 
 def run(config: EnsembleConfig, problem: Problem, observer=None, snapshot_steps=(), comm=None, record=True):

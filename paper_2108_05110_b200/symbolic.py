@@ -387,6 +387,7 @@ OP_ZERO, OP_ORIG, OP_EXTADD, OP_DIAG, OP_HPANEL, OP_UPDATE, OP_GPANEL = range(7)
 SOP_FINIT, SOP_FEXT, SOP_FGEMM, SOP_BGATHER, SOP_BGEMM = range(5)
 EXT_ROWS = 8      # child-CB rows per extend-add work item
 VEC_ROWS = 64     # front-vector rows per init/gather/scatter work item
+SOLVE_ROWS = 16   # rows per solve-GEMM work item (csrc/ens_mfsolve.cu SG_R)
 
 
 def build_schedule(plan: FactorPlan, pw=PW):
@@ -478,7 +479,7 @@ def build_schedule(plan: FactorPlan, pw=PW):
             if rows:
                 off, n = add(rows)
                 fwd.append((SOP_FEXT, L, off, n, r))
-        rows = [(f, r0) for f in fronts for r0 in range(0, fm[f] - fk[f], TILE)]
+        rows = [(f, r0) for f in fronts for r0 in range(0, fm[f] - fk[f], SOLVE_ROWS)]
         if rows:
             off, n = add(rows)
             fwd.append((SOP_FGEMM, L, off, n, 0))
@@ -488,7 +489,7 @@ def build_schedule(plan: FactorPlan, pw=PW):
         if rows:
             off, n = add(rows)
             bwd.append((SOP_BGATHER, L, off, n, 0))
-        rows = [(f, r0) for f in fronts for r0 in range(0, fk[f], TILE)]
+        rows = [(f, r0) for f in fronts for r0 in range(0, fk[f], SOLVE_ROWS)]
         off, n = add(rows)
         bwd.append((SOP_BGEMM, L, off, n, 0))
     work = np.vstack(items) if items else np.zeros((0, 4), np.int32)

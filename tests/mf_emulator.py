@@ -92,7 +92,7 @@ def solve(plan, st, rhs):
                 fr[p][mp[rows]] += fr[c][fk[c] + rows]
             elif op == S.SOP_FGEMM:
                 k = fk[f]
-                rows = slice(k + r0, min(k + r0 + S.TILE, fm[f]))
+                rows = slice(k + r0, min(k + r0 + S.SOLVE_ROWS, fm[f]))
                 fr[f][rows] -= front(f)[rows, :k] @ fr[f][:k]
     for op, L, io, n, arg in plan.schedule["bwd"]:
         for it in work[io:io + n]:
@@ -101,6 +101,6 @@ def solve(plan, st, rhs):
                 rows = np.arange(r0, min(r0 + S.VEC_ROWS, fm[f]))
                 fr[f][rows] = x[idx(f)[rows]]
             elif op == S.SOP_BGEMM:
-                rows = np.arange(r0, min(r0 + S.TILE, fk[f]))
+                rows = np.arange(r0, min(r0 + S.SOLVE_ROWS, fk[f]))
                 x[idx(f)[rows]] = -front(f)[rows, :] @ fr[f]
     return x
