@@ -106,6 +106,7 @@ typedef struct {
     const int32_t* orig_src;
     const double*  bsrc_vals;   /* signed B / -B^T values                   */
     const int32_t* work;        /* n_work x 4 */
+    const int32_t* gsrc;        /* n_idx x 4: child contribution rows gathered per front row (-1 none) */
     /* HOST arrays */
     const int64_t* orig_level_off_host;    /* nlevels+1 */
     const int64_t* level_storage_off_host; /* nlevels+1 */
@@ -114,7 +115,8 @@ typedef struct {
     const int64_t* sched_fwd_host;    int64_t n_sched_fwd;
     const int64_t* sched_bwd_host;    int64_t n_sched_bwd;
     int32_t max_m;
-    int32_t pad;
+    int32_t split_k;            /* inner-dimension length of one solve-GEMM work item */
+    int64_t n_slot;             /* split-K partial slots (64 rows x J each)          */
 } ens_plan_desc;
 
 /* Problem data: value_j = sum_k coef[k*J + j] * basis[k*rows + row] (+ dense). */

@@ -38,11 +38,12 @@ class PlanDesc(C.Structure):
         ("front_storage", I64), ("n_orig", I64), ("n_cmap", I64), ("n_idx", I64), ("n_work", I64),
         ("f_m", P), ("f_k", P), ("f_off", P), ("f_idx_off", P), ("f_idx", P), ("f_parent", P),
         ("f_cmap_off", P), ("f_cmap", P), ("orig_dst", P), ("orig_src", P), ("bsrc_vals", P), ("work", P),
+        ("gsrc", P),
         ("orig_level_off_host", P), ("level_storage_off_host", P), ("level_front_off_host", P),
         ("sched_factor_host", P), ("n_sched_factor", I64),
         ("sched_fwd_host", P), ("n_sched_fwd", I64),
         ("sched_bwd_host", P), ("n_sched_bwd", I64),
-        ("max_m", I32), ("pad", I32),
+        ("max_m", I32), ("split_k", I32), ("n_slot", I64),
     ]
 
 

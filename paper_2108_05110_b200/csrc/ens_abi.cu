@@ -115,6 +115,10 @@ void ens_destroy(ens_ctx* c) {
     cudaFree(c->d_count);
     if (c->h_count) cudaFreeHost(c->h_count);
     if (c->h_small) cudaFreeHost(c->h_small);
+    if (c->g_solve) cudaGraphExecDestroy((cudaGraphExec_t)c->g_solve);
+    if (c->g_factor) cudaGraphExecDestroy((cudaGraphExec_t)c->g_factor);
+    cudaFree(c->solve_io);
+    cudaFree(c->partial);
     delete c;
 }
 

@@ -57,6 +57,14 @@ struct ens_ctx {
     int32_t* h_count = nullptr;    // pinned
     double* h_small = nullptr;     // pinned
     size_t ws_bytes = 0;
+    // CUDA graphs of the fixed launch sequences
+    void* solve_io = nullptr;      // device {r, z} pointer table of the solve graph
+    double* partial = nullptr;     // split-K partial products of the solve GEMMs
+    void* g_solve = nullptr;       // cudaGraphExec_t
+    int64_t g_solve_kernels = 0;
+    void* g_factor = nullptr;      // cudaGraphExec_t
+    const double* g_factor_key = nullptr;
+    int64_t g_factor_kernels = 0;
 };
 
 // ---- kernels launchers (ens_kernels.cu) ----

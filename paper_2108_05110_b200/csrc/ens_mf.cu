@@ -14,6 +14,7 @@
 // batched GEMM per tree level and direction:
 //   forward  fr[C] -= F[C,P] fr[P]             backward  x[P] = -[F[P,P] F[P,C]] [fr[P]; x[C]]
 #include <cmath>
+#include <cstdlib>
 
 #include "ens_internal.cuh"
 
@@ -344,9 +345,10 @@ int mf_setup(ens_ctx* c) {
     return ENS_OK;
 }
 
-int mf_factor(ens_ctx* c, cudaStream_t s, const double* as_vals, int32_t* n_pert) {
+static int mf_factor_launches(ens_ctx* c, cudaStream_t s, const double* as_vals, int64_t* nlaunch) {
     MfDev d = mfdev(c);
     const int64_t st = c->p.front_storage;
+    int64_t cnt = 0;
     ENS_CK(cudaMemsetAsync(c->d_count, 0, sizeof(int32_t), s));
     const int64_t nrow = (int64_t)c->sched_factor.size() / 5;
     for (int64_t i = 0; i < nrow; ++i) {
@@ -387,6 +389,42 @@ int mf_factor(ens_ctx* c, cudaStream_t s, const double* as_vals, int32_t* n_pert
                 return ENS_EINVAL;
         }
         ENS_CKL();
+        ++cnt;
+    }
+    *nlaunch = cnt;
+    return ENS_OK;
+}
+
+// The factorisation's launch sequence is fixed per mesh: capture it once into a
+// CUDA graph (keyed on the value buffer) and replay it every sub-step.
+int mf_factor(ens_ctx* c, cudaStream_t s, const double* as_vals, int32_t* n_pert) {
+    const char* e = std::getenv("ENS_NO_GRAPH");
+    const bool graphs = !(e && e[0] == '1') && s != 0;
+    if (!graphs) {
+        int64_t n = 0;
+        const int rc = mf_factor_launches(c, s, as_vals, &n);
+        if (rc != ENS_OK) return rc;
+    } else {
+        if (c->g_factor && c->g_factor_key != as_vals) {
+            cudaGraphExecDestroy((cudaGraphExec_t)c->g_factor);
+            c->g_factor = nullptr;
+        }
+        if (!c->g_factor) {
+            cudaGraph_t g;
+            ENS_CK(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+            int64_t n = 0;
+            const int rc = mf_factor_launches(c, s, as_vals, &n);
+            const cudaError_t ce = cudaStreamEndCapture(s, &g);
+            if (rc != ENS_OK) return rc;
+            ENS_CK(ce);
+            ENS_CK(cudaGraphInstantiate((cudaGraphExec_t*)&c->g_factor, g, 0));
+            cudaGraphDestroy(g);
+            c->g_factor_key = as_vals;
+            c->g_factor_kernels = n;
+            g_ens_launches -= (unsigned long long)n;
+        }
+        ENS_CK(cudaGraphLaunch((cudaGraphExec_t)c->g_factor, s));
+        g_ens_launches += (unsigned long long)c->g_factor_kernels;
     }
     if (n_pert) {
         ENS_CK(cudaMemcpyAsync(c->h_count, c->d_count, sizeof(int32_t), cudaMemcpyDeviceToHost, s));

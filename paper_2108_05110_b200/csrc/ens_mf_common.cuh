@@ -3,7 +3,7 @@
 #include "ens_internal.cuh"
 
 enum { OP_ZERO = 0, OP_ORIG, OP_EXTADD, OP_DIAG, OP_HPANEL, OP_UPDATE, OP_GPANEL };
-enum { SOP_FINIT = 0, SOP_FEXT, SOP_FGEMM, SOP_BGATHER, SOP_BGEMM };
+enum { SOP_FINIT = 0, SOP_FEXT, SOP_FGEMM, SOP_BGATHER, SOP_BGEMM, SOP_FRED, SOP_BRED };
 
 struct MfDev {
     const int32_t* m;
@@ -15,6 +15,7 @@ struct MfDev {
     const int64_t* cmap_off;
     const int32_t* cmap;
     const int32_t* work;
+    const int32_t* gsrc;
     int64_t storage;
 };
 
@@ -29,6 +30,7 @@ static inline MfDev mfdev(const ens_ctx* c) {
     d.cmap_off = c->p.f_cmap_off;
     d.cmap = c->p.f_cmap;
     d.work = c->p.work;
+    d.gsrc = c->p.gsrc;
     d.storage = c->p.front_storage;
     return d;
 }

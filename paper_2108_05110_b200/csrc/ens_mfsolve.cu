@@ -1,19 +1,48 @@
 // Multi-column solves with the block-sweep fronts (sm_100a, fp64).
 //
 // After ens_mf.cu's sweep each front holds [-F11^-1, F11^-1 F12; F21 F11^-1, S].
-// Per tree level (leaves -> root) the forward pass is
-//     fr_f = [b(pivots); 0] + extend-add of the children's CB vectors
-//     fr_f[C] -= F[C,P] fr_f[P]
-// and per level (root -> leaves) the backward pass is
-//     x[P] = -[F[P,P] F[P,C]] [fr_f[P]; x[C]].
-// Both products are skinny GEMMs (N = J members) computed by k_sgemm: a CTA
-// owns 16 rows x 32 member columns, streams the factor rows through a
-// two-stage cp.async pipeline in shared memory, and writes its rows exactly
-// once (no atomics: bitwise-identical members stay identical).
+// Forward, per tree level (leaves -> root):
+//     FINIT  fr_f = [b(pivots); 0] + the children's contribution rows (one gather pass)
+//     FGEMM  fr_f[C] -= F[C,P] fr_f[P]
+// Backward, per level (root -> leaves):
+//     BGEMM  x[P] = -[F[P,P] F[P,C]] [fr_f[P]; x[C]]   (x[C] read straight from the iterate)
+// The products are skinny GEMMs (N = J members).  A CTA owns 64 rows x 32
+// member columns over an inner range of <= split_k and streams the factor rows
+// through a two-stage cp.async pipeline in shared memory.  Long inner
+// dimensions (top of the tree) are split into independent items whose partial
+// products land in scratch slots and are summed in a fixed order by *RED
+// (deterministic, no atomics: bitwise-identical members stay identical).
+//
+// The whole solve is captured once into a CUDA graph; the in/out blocks are
+// passed through a 2-pointer device table so the graph serves every Krylov vector.
+#include <cstdlib>
+
 #include "ens_internal.cuh"
 #include "ens_mf_common.cuh"
 
-__global__ void k_finit(MfDev d, int item0, const double* __restrict__ B, double* __restrict__ FR, int64_t N, int J,
+struct SolveIO {
+    const double* r;
+    double* z;
+};
+
+__global__ void k_set_io(SolveIO* io, const double* r, double* z) {
+    io->r = r;
+    io->z = z;
+}
+
+// identity rows: z[cons] = r[cons]
+__global__ void k_copy_cons_io(const int32_t* __restrict__ crow, int ncons, const SolveIO* __restrict__ io, int64_t N,
+                               int J) {
+    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t per = (int64_t)ncons * J;
+    if (t >= 2 * per) return;
+    const int mat = (int)(t / per);
+    const int64_t u = t - mat * per;
+    const int64_t idx = (int64_t)mat * N * J + (int64_t)crow[u / J] * J + (u % J);
+    io->z[idx] = io->r[idx];
+}
+
+__global__ void k_finit(MfDev d, int item0, const SolveIO* __restrict__ io, double* __restrict__ FR, int64_t N, int J,
                         int64_t nidx) {
     const int* it = d.work + 4LL * (item0 + blockIdx.x);
     const int f = it[0], r0 = it[1];
@@ -22,42 +51,18 @@ __global__ void k_finit(MfDev d, int item0, const double* __restrict__ B, double
     const int rows = min(ENS_VEC_ROWS, m - r0);
     const int64_t fo = d.idx_off[f];
     double* fr = FR + (int64_t)mat * nidx * J;
-    const double* b = B + (int64_t)mat * N * J;
+    const double* b = io->r + (int64_t)mat * N * J;
     for (int t = threadIdx.x; t < rows * J; t += blockDim.x) {
         const int i = r0 + t / J, j = t % J;
-        fr[(fo + i) * J + j] = i < k ? b[(int64_t)d.idx[fo + i] * J + j] : 0.0;
-    }
-}
-
-__global__ void k_fext(MfDev d, int item0, double* __restrict__ FR, int J, int64_t nidx) {
-    const int* it = d.work + 4LL * (item0 + blockIdx.x);
-    const int c = it[0], r0 = it[1];
-    const int mat = blockIdx.y;
-    const int p = d.parent[c];
-    const int kc = d.k[c], cbn = d.m[c] - kc;
-    const int rows = min(ENS_VEC_ROWS, cbn - r0);
-    const int32_t* map = d.cmap + d.cmap_off[c];
-    double* fr = FR + (int64_t)mat * nidx * J;
-    const int64_t co = d.idx_off[c], po = d.idx_off[p];
-    for (int t = threadIdx.x; t < rows * J; t += blockDim.x) {
-        const int i = r0 + t / J, j = t % J;
-        fr[(po + map[i]) * J + j] += fr[(co + kc + i) * J + j];
-    }
-}
-
-__global__ void k_bgather(MfDev d, int item0, const double* __restrict__ X, double* __restrict__ FR, int64_t N, int J,
-                          int64_t nidx) {
-    const int* it = d.work + 4LL * (item0 + blockIdx.x);
-    const int f = it[0], r0 = it[1];
-    const int mat = blockIdx.y;
-    const int m = d.m[f];
-    const int rows = min(ENS_VEC_ROWS, m - r0);
-    const int64_t fo = d.idx_off[f];
-    double* fr = FR + (int64_t)mat * nidx * J;
-    const double* x = X + (int64_t)mat * N * J;
-    for (int t = threadIdx.x; t < rows * J; t += blockDim.x) {
-        const int i = r0 + t / J, j = t % J;
-        fr[(fo + i) * J + j] = x[(int64_t)d.idx[fo + i] * J + j];
+        const int64_t row = fo + i;
+        double v = i < k ? b[(int64_t)d.idx[row] * J + j] : 0.0;
+        const int32_t* g = d.gsrc + 4 * row;
+#pragma unroll
+        for (int s = 0; s < 4; ++s) {
+            const int32_t src = g[s];
+            if (src >= 0) v += fr[(int64_t)src * J + j];
+        }
+        fr[row * J + j] = v;
     }
 }
 
@@ -70,20 +75,23 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
 
-#define SG_R 16     // rows per CTA
+#define SG_R 64     // rows per CTA (= symbolic.SOLVE_ROWS)
 #define SG_C 32     // member columns per CTA
-#define SG_K 64     // inner chunk
-#define SG_T 128    // threads
+#define SG_K 32     // inner chunk per pipeline stage
+#define SG_T 256    // threads
 
 // forward (bwd=0): fr[k+r0+i] -= sum_{t<k} F[k+r0+i][t] fr[t]
-// backward (bwd=1): x[idx[r0+i]] = -sum_{t<m} F[r0+i][t] fr[t]
+// backward (bwd=1): x[idx[r0+i]] = -sum_{t<m} F[r0+i][t] (t < k ? fr[t] : x[idx[t]])
+// item = (f, r0, ks, slot): slot < 0 -> whole inner range, result applied here;
+//                          slot >= 0 -> range [ks*split_k, ...), product stored to partial[slot]
 __global__ void __launch_bounds__(SG_T) k_sgemm(MfDev d, int item0, const double* __restrict__ F,
-                                                double* __restrict__ FR, double* __restrict__ X, int64_t N, int J,
-                                                int64_t nidx, int bwd) {
-    __shared__ double As[2][SG_R][SG_K];
+                                                double* __restrict__ FR, const SolveIO* __restrict__ io, int64_t N,
+                                                int J, int64_t nidx, int bwd, int split_k,
+                                                double* __restrict__ partial, int64_t nslot) {
+    __shared__ double As[2][SG_K][SG_R];   // K-major: conflict-free row reads in the inner loop
     __shared__ double Bs[2][SG_K][SG_C];
     const int* it = d.work + 4LL * (item0 + blockIdx.x);
-    const int f = it[0], r0 = it[1];
+    const int f = it[0], r0 = it[1], ks = it[2], slot = it[3];
     const int mat = blockIdx.y;
     const int j0 = blockIdx.z * SG_C;
     const int jn = min(SG_C, J - j0);
@@ -91,116 +99,190 @@ __global__ void __launch_bounds__(SG_T) k_sgemm(MfDev d, int item0, const double
     const int rbase = bwd ? r0 : k + r0;
     const int nr = min(SG_R, (bwd ? k : m) - rbase);
     const int K = bwd ? m : k;
+    const int kbeg = slot < 0 ? 0 : ks * split_k;
+    const int kend = slot < 0 ? K : min(K, kbeg + split_k);
     const double* base = F + (int64_t)mat * d.storage + d.off[f];
-    double* fr = FR + (int64_t)mat * nidx * J + d.idx_off[f] * J;
+    const int64_t fo = d.idx_off[f];
+    double* fr = FR + (int64_t)mat * nidx * J + fo * J;
+    double* x = io->z + (int64_t)mat * N * J;
     const int tid = threadIdx.x;
-    const int nchunk = (K + SG_K - 1) / SG_K;
+    const int nchunk = (kend - kbeg + SG_K - 1) / SG_K;
 
     auto load = [&](int stage, int t0) {
 #pragma unroll
         for (int u = 0; u < (SG_R * SG_K) / SG_T; ++u) {
             const int e = tid + u * SG_T;
             const int r = e / SG_K, kk = e % SG_K;
-            const bool ok = r < nr && t0 + kk < K;
-            cp_async8(&As[stage][r][kk], ok ? base + (int64_t)(rbase + r) * m + t0 + kk : base, ok);
+            const bool ok = r < nr && t0 + kk < kend;
+            cp_async8(&As[stage][kk][r], ok ? base + (int64_t)(rbase + r) * m + t0 + kk : base, ok);
         }
 #pragma unroll
         for (int u = 0; u < (SG_K * SG_C) / SG_T; ++u) {
             const int e = tid + u * SG_T;
             const int kk = e / SG_C, j = e % SG_C;
-            const bool ok = t0 + kk < K && j < jn;
-            cp_async8(&Bs[stage][kk][j], ok ? fr + (int64_t)(t0 + kk) * J + j0 + j : fr, ok);
+            const int t = t0 + kk;
+            const bool ok = t < kend && j < jn;
+            const double* src = fr;
+            if (ok) src = (t < k) ? fr + (int64_t)t * J + j0 + j : x + (int64_t)d.idx[fo + t] * J + j0 + j;
+            cp_async8(&Bs[stage][kk][j], src, ok);
         }
         cp_async_commit();
     };
 
-    const int tx = tid & 15, ty = tid >> 4;   // cols tx, tx+16 ; rows ty, ty+8
-    double acc[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
-    if (nchunk > 0) load(0, 0);
+    const int tx = tid & 15, ty = tid >> 4;   // cols tx, tx+16 ; rows ty + 16 i
+    double acc[4][2];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) acc[i][0] = acc[i][1] = 0.0;
+    if (nchunk > 0) load(0, kbeg);
     for (int c = 0; c < nchunk; ++c) {
         if (c + 1 < nchunk) {
-            load((c + 1) & 1, (c + 1) * SG_K);
+            load((c + 1) & 1, kbeg + (c + 1) * SG_K);
             cp_async_wait<1>();
         } else {
             cp_async_wait<0>();
         }
         __syncthreads();
         const int st = c & 1;
-#pragma unroll 8
-        for (int kk = 0; kk < SG_K; ++kk) {
-            const double a0 = As[st][ty][kk], a1 = As[st][ty + 8][kk];
+        const int kc = min(SG_K, kend - kbeg - c * SG_K);
+        for (int kk = 0; kk < kc; ++kk) {
+            double a[4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) a[i] = As[st][kk][ty + 16 * i];
             const double b0 = Bs[st][kk][tx], b1 = Bs[st][kk][tx + 16];
-            acc[0][0] = fma(a0, b0, acc[0][0]);
-            acc[0][1] = fma(a0, b1, acc[0][1]);
-            acc[1][0] = fma(a1, b0, acc[1][0]);
-            acc[1][1] = fma(a1, b1, acc[1][1]);
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                acc[i][0] = fma(a[i], b0, acc[i][0]);
+                acc[i][1] = fma(a[i], b1, acc[i][1]);
+            }
         }
         __syncthreads();
     }
-    double* x = X + (int64_t)mat * N * J;
 #pragma unroll
-    for (int i = 0; i < 2; ++i) {
-        const int r = ty + 8 * i;
+    for (int i = 0; i < 4; ++i) {
+        const int r = ty + 16 * i;
         if (r >= nr) continue;
 #pragma unroll
         for (int jj = 0; jj < 2; ++jj) {
             const int j = tx + 16 * jj;
             if (j >= jn) continue;
-            if (bwd)
-                x[(int64_t)d.idx[d.idx_off[f] + rbase + r] * J + j0 + j] = -acc[i][jj];
+            if (slot >= 0)
+                partial[(((int64_t)mat * nslot + slot) * SG_R + r) * J + j0 + j] = acc[i][jj];
+            else if (bwd)
+                x[(int64_t)d.idx[fo + rbase + r] * J + j0 + j] = -acc[i][jj];
             else
                 fr[(int64_t)(rbase + r) * J + j0 + j] -= acc[i][jj];
         }
     }
 }
 
-int mf_solve(ens_ctx* c, cudaStream_t s, const double* r, double* z) {
+// ordered sum of the split-K partials + the update; item = (f, r0, nsplit, slot0)
+__global__ void k_sred(MfDev d, int item0, double* __restrict__ FR, const SolveIO* __restrict__ io, int64_t N, int J,
+                       int64_t nidx, int bwd, const double* __restrict__ partial, int64_t nslot) {
+    const int* it = d.work + 4LL * (item0 + blockIdx.x);
+    const int f = it[0], r0 = it[1], ns = it[2], s0 = it[3];
+    const int mat = blockIdx.y;
+    const int m = d.m[f], k = d.k[f];
+    const int rbase = bwd ? r0 : k + r0;
+    const int nr = min(SG_R, (bwd ? k : m) - rbase);
+    const int64_t fo = d.idx_off[f];
+    double* fr = FR + (int64_t)mat * nidx * J + fo * J;
+    double* x = io->z + (int64_t)mat * N * J;
+    for (int t = threadIdx.x; t < nr * J; t += blockDim.x) {
+        const int r = t / J, j = t % J;
+        double s = 0.0;
+        for (int q = 0; q < ns; ++q) s += partial[(((int64_t)mat * nslot + s0 + q) * SG_R + r) * J + j];
+        if (bwd)
+            x[(int64_t)d.idx[fo + rbase + r] * J + j] = -s;
+        else
+            fr[(int64_t)(rbase + r) * J + j] -= s;
+    }
+}
+
+// record the launch sequence of one solve (io table fixed)
+static int mf_solve_launches(ens_ctx* c, cudaStream_t s, SolveIO* io, int64_t* nlaunch) {
     MfDev d = mfdev(c);
     const int J = c->J;
     const int64_t N = c->n_total, nidx = c->p.n_idx;
     const unsigned zc = (unsigned)((J + SG_C - 1) / SG_C);
-    {
-        const int rc = launch_copy_cons(c, s, r, z);
+    const int sk = c->p.split_k;
+    const int64_t nslot = c->p.n_slot;
+    int64_t cnt = 0;
+    if (c->m.ncons > 0) {
+        const int64_t tot = 2LL * c->m.ncons * J;
+        k_copy_cons_io<<<(unsigned)((tot + 255) / 256), 256, 0, s>>>(c->m.cons_row, c->m.ncons, io, N, J);
+        ENS_CKL();
+        ++cnt;
+    }
+    for (const std::vector<int64_t>* sched : {&c->sched_fwd, &c->sched_bwd}) {
+        const int64_t nrow = (int64_t)sched->size() / 5;
+        for (int64_t i = 0; i < nrow; ++i) {
+            const int64_t* q = &(*sched)[5 * i];
+            const int op = (int)q[0], off = (int)q[2], n = (int)q[3];
+            if (n == 0) continue;
+            switch (op) {
+                case SOP_FINIT:
+                    k_finit<<<dim3(n, 2), 256, 0, s>>>(d, off, io, c->frvec, N, J, nidx);
+                    break;
+                case SOP_FGEMM:
+                case SOP_BGEMM:
+                    k_sgemm<<<dim3(n, 2, zc), SG_T, 0, s>>>(d, off, c->fronts, c->frvec, io, N, J, nidx,
+                                                            op == SOP_BGEMM, sk, c->partial, nslot);
+                    break;
+                case SOP_FRED:
+                case SOP_BRED:
+                    k_sred<<<dim3(n, 2), 256, 0, s>>>(d, off, c->frvec, io, N, J, nidx, op == SOP_BRED, c->partial,
+                                                      nslot);
+                    break;
+                default:
+                    ens_set_error("bad solve op", __FILE__, __LINE__);
+                    return ENS_EINVAL;
+            }
+            ENS_CKL();
+            ++cnt;
+        }
+    }
+    *nlaunch = cnt;
+    return ENS_OK;
+}
+
+static bool graphs_enabled() {
+    const char* e = std::getenv("ENS_NO_GRAPH");
+    return !(e && e[0] == '1');
+}
+
+int mf_solve(ens_ctx* c, cudaStream_t s, const double* r, double* z) {
+    if (!c->solve_io) {
+        ENS_CK(cudaMalloc(&c->solve_io, sizeof(SolveIO)));
+    }
+    if (!c->partial && c->p.n_slot > 0) {
+        const size_t bytes = sizeof(double) * 2 * (size_t)c->p.n_slot * SG_R * c->J;
+        if (cudaMalloc(&c->partial, bytes) != cudaSuccess) {
+            ens_set_error("out of device memory for split-K partials", __FILE__, __LINE__);
+            return ENS_ENOMEM;
+        }
+        c->ws_bytes += bytes;
+    }
+    SolveIO* io = (SolveIO*)c->solve_io;
+    k_set_io<<<1, 1, 0, s>>>(io, r, z);
+    ENS_CKL();
+    if (!graphs_enabled() || s == 0) {
+        int64_t n = 0;
+        return mf_solve_launches(c, s, io, &n);
+    }
+    if (!c->g_solve) {
+        cudaGraph_t g;
+        ENS_CK(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+        int64_t n = 0;
+        const int rc = mf_solve_launches(c, s, io, &n);
+        const cudaError_t e = cudaStreamEndCapture(s, &g);
         if (rc != ENS_OK) return rc;
+        ENS_CK(e);
+        ENS_CK(cudaGraphInstantiate((cudaGraphExec_t*)&c->g_solve, g, 0));
+        cudaGraphDestroy(g);
+        c->g_solve_kernels = n;
+        g_ens_launches -= (unsigned long long)n;   // counted again at every replay below
     }
-    const int64_t nf = (int64_t)c->sched_fwd.size() / 5;
-    for (int64_t i = 0; i < nf; ++i) {
-        const int64_t* q = &c->sched_fwd[5 * i];
-        const int op = (int)q[0], off = (int)q[2], n = (int)q[3];
-        if (n == 0) continue;
-        switch (op) {
-            case SOP_FINIT:
-                k_finit<<<dim3(n, 2), 256, 0, s>>>(d, off, r, c->frvec, N, J, nidx);
-                break;
-            case SOP_FEXT:
-                k_fext<<<dim3(n, 2), 256, 0, s>>>(d, off, c->frvec, J, nidx);
-                break;
-            case SOP_FGEMM:
-                k_sgemm<<<dim3(n, 2, zc), SG_T, 0, s>>>(d, off, c->fronts, c->frvec, z, N, J, nidx, 0);
-                break;
-            default:
-                ens_set_error("bad fwd op", __FILE__, __LINE__);
-                return ENS_EINVAL;
-        }
-        ENS_CKL();
-    }
-    const int64_t nb = (int64_t)c->sched_bwd.size() / 5;
-    for (int64_t i = 0; i < nb; ++i) {
-        const int64_t* q = &c->sched_bwd[5 * i];
-        const int op = (int)q[0], off = (int)q[2], n = (int)q[3];
-        if (n == 0) continue;
-        switch (op) {
-            case SOP_BGATHER:
-                k_bgather<<<dim3(n, 2), 256, 0, s>>>(d, off, z, c->frvec, N, J, nidx);
-                break;
-            case SOP_BGEMM:
-                k_sgemm<<<dim3(n, 2, zc), SG_T, 0, s>>>(d, off, c->fronts, c->frvec, z, N, J, nidx, 1);
-                break;
-            default:
-                ens_set_error("bad bwd op", __FILE__, __LINE__);
-                return ENS_EINVAL;
-        }
-        ENS_CKL();
-    }
+    ENS_CK(cudaGraphLaunch((cudaGraphExec_t)c->g_solve, s));
+    g_ens_launches += (unsigned long long)c->g_solve_kernels;
     return ENS_OK;
 }

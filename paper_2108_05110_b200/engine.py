@@ -260,7 +260,8 @@ class Engine:
             f_idx=up(p.f_idx, i32), f_parent=up(p.f_parent, i32), f_cmap_off=up(p.f_cmap_off, i64),
             f_cmap=up(p.f_cmap if len(p.f_cmap) else np.zeros(1, np.int32), i32), orig_dst=up(p.orig_dst, i64),
             orig_src=up(hm.orig_src, i32), bsrc_vals=up(p.bsrc_vals, torch.float64),
-            work=up(p.schedule["work"].ravel() if p.schedule["work"].size else np.zeros(4, np.int32), i32))
+            work=up(p.schedule["work"].ravel() if p.schedule["work"].size else np.zeros(4, np.int32), i32),
+            gsrc=up(p.schedule["gsrc"].ravel(), i32))
         self.plan_t = plan_t
         self._host_keep = dict(
             orig_level_off=np.ascontiguousarray(p.orig_level_off, dtype=np.int64),
@@ -283,6 +284,8 @@ class Engine:
         pd.sched_fwd_host, pd.n_sched_fwd = hk["fwd"].ctypes.data, len(hk["fwd"])
         pd.sched_bwd_host, pd.n_sched_bwd = hk["bwd"].ctypes.data, len(hk["bwd"])
         pd.max_m = int(p.f_m.max())
+        pd.split_k = int(p.schedule.get("split_k", S.SPLIT_K))
+        pd.n_slot = int(p.schedule["nslot"])
         self._md, self._pd = md, pd
         ctx = C.c_void_p()
         with torch.cuda.device(self.dev):
@@ -314,7 +317,10 @@ class Engine:
         self.maxsq = torch.zeros(2, self.nt, 7, **f64)
         self.as_vals = torch.zeros(2, hm.nnz_s, **f64)
         self.diag_out = torch.zeros(2 + 6 * J, **f64)
-        self.stream = torch.cuda.current_stream(self.dev)
+        # a dedicated (non-default) stream: the factorisation and solve sequences
+        # are captured once into CUDA graphs, which needs a capturable stream
+        self.stream = torch.cuda.Stream(self.dev)
+        torch.cuda.synchronize(self.dev)
         self._data_cache = {}
         self.last_iters = 0
         self.last_pert = 0
@@ -456,7 +462,42 @@ class Engine:
     # ------------------------------------------------------------------
     # the time-step
     # ------------------------------------------------------------------
+    class _OnStream:
+        """Run on the engine stream, ordered after / before the caller's stream."""
+
+        def __init__(self, eng):
+            self.eng = eng
+
+        def __enter__(self):
+            caller = torch.cuda.current_stream(self.eng.dev)
+            self.caller = caller
+            self.eng.stream.wait_stream(caller)
+            self.ctx = torch.cuda.stream(self.eng.stream)
+            self.ctx.__enter__()
+
+        def __exit__(self, *exc):
+            self.ctx.__exit__(*exc)
+            self.caller.wait_stream(self.eng.stream)
+            return False
+
+    def on_stream(self):
+        return Engine._OnStream(self)
+
     def compute_means(self):
+        with self.on_stream():
+            self._compute_means()
+
+    def step(self, t_next, forcing, boundary):
+        """One time-step of all local members; returns the max relative residual."""
+        with self.on_stream():
+            return self._step(t_next, forcing, boundary)
+
+    def diagnostics(self):
+        """Device-side _record (stepper.py:432-439) of the current state."""
+        with self.on_stream():
+            return self._diagnostics()
+
+    def _compute_means(self):
         lib, ctx, s = self.lib, self.ctx, self.sptr
         X = self.X[self.cur]
         N.check(lib.ens_member_sums(ctx, s, _dptr(X), _dptr(self.sums)), "ens_member_sums")
@@ -464,12 +505,12 @@ class Engine:
         torch.mul(self.sums, 1.0 / self.J_total, out=self.means)
         self.means_valid = True
 
-    def step(self, t_next, forcing, boundary):
+    def _step(self, t_next, forcing, boundary):
         lib, ctx, s = self.lib, self.ctx, self.sptr
         cur, nxt = self.cur, 1 - self.cur
         X = self.X[cur]
         if not self.means_valid:
-            self.compute_means()
+            self._compute_means()
         loads, keep1 = self._data(forcing, "loads", t_next)
         N.check(lib.ens_rhs(ctx, s, _dptr(X), _dptr(self.member_coef), 1.0 / self.config.dt,
                             C.byref(loads) if loads is not None else None, _dptr(self.rhs)), "ens_rhs")
@@ -519,10 +560,9 @@ class Engine:
                                   self.restart, self.max_restarts, C.byref(iters), rel)
         return code, int(iters.value), (rel[0], rel[1])
 
-    def diagnostics(self):
-        """Device-side _record (stepper.py:432-439) of the current state."""
+    def _diagnostics(self):
         if not self.means_valid:
-            self.compute_means()
+            self._compute_means()
         N.check(self.lib.ens_diagnostics(self.ctx, self.sptr, _dptr(self.X[self.cur]), _dptr(self.means),
                                          _dptr(self.diag_out)), "ens_diagnostics")
         out = self.diag_out.cpu().numpy()
@@ -534,15 +574,18 @@ class Engine:
     # raw access for tests
     def spmm(self, x, b=None, mode=0, out=None):
         out = torch.empty_like(x) if out is None else out
-        N.check(self.lib.ens_spmm(self.ctx, self.sptr, _dptr(self.as_vals), _dptr(x),
-                                  _dptr(b) if b is not None else None, _dptr(out), mode), "ens_spmm")
+        with self.on_stream():
+            N.check(self.lib.ens_spmm(self.ctx, self.sptr, _dptr(self.as_vals), _dptr(x),
+                                      _dptr(b) if b is not None else None, _dptr(out), mode), "ens_spmm")
         return out
 
     def factor(self):
-        self._factor()
+        with self.on_stream():
+            self._factor()
         return self.last_pert
 
     def precond(self, r, out=None):
         out = torch.zeros_like(r) if out is None else out
-        N.check(self.lib.ens_precond_apply(self.ctx, self.sptr, _dptr(r), _dptr(out)), "ens_precond_apply")
+        with self.on_stream():
+            N.check(self.lib.ens_precond_apply(self.ctx, self.sptr, _dptr(r), _dptr(out)), "ens_precond_apply")
         return out

@@ -384,10 +384,12 @@ def analyse(disc, leaf=LEAF_NODES, pw=PW):
 
 # op codes (must match csrc/mf.cu)
 OP_ZERO, OP_ORIG, OP_EXTADD, OP_DIAG, OP_HPANEL, OP_UPDATE, OP_GPANEL = range(7)
-SOP_FINIT, SOP_FEXT, SOP_FGEMM, SOP_BGATHER, SOP_BGEMM = range(5)
+SOP_FINIT, SOP_FEXT, SOP_FGEMM, SOP_BGATHER, SOP_BGEMM, SOP_FRED, SOP_BRED = range(7)
+SPLIT_K = 512     # inner-dimension length per solve-GEMM work item (csrc/ens_mfsolve.cu SG_KS)
+MAX_GSRC = 4      # child contribution rows gathered per front-vector row
 EXT_ROWS = 8      # child-CB rows per extend-add work item
 VEC_ROWS = 64     # front-vector rows per init/gather/scatter work item
-SOLVE_ROWS = 16   # rows per solve-GEMM work item (csrc/ens_mfsolve.cu SG_R)
+SOLVE_ROWS = 64   # rows per solve-GEMM work item (csrc/ens_mfsolve.cu SG_R)
 
 
 def build_schedule(plan: FactorPlan, pw=PW):
@@ -462,38 +464,70 @@ def build_schedule(plan: FactorPlan, pw=PW):
     # solve schedule: after the sweep a front holds [-F11^-1, F11^-1 F12; F21 F11^-1, S]
     #   forward  fr[k:m] -= F_CP fr[0:k]           (SOP_FGEMM, rows of the CB)
     #   backward x[piv]   = -[F_PP F_PC] [fr_P; x_C] (SOP_BGEMM, rows of the pivots)
+    #   SOP_FINIT gathers a front's vector rows in one pass: b at the pivots plus
+    #   the (<= MAX_GSRC) child contribution rows mapped onto each row (gsrc);
+    #   SOP_BGEMM reads x[C] straight from the global iterate (no gather pass).
+    #   Long inner dimensions are split (SPLIT_K) into independent work items that
+    #   write partial products to scratch slots; SOP_*RED sums them in a fixed
+    #   order (deterministic, no atomics) and applies the update.
     fwd, bwd = [], []
+    nslot = [0]
+
+    def gemm_items(fronts, rows_of, K_of):
+        g, red = [], []
+        for f in fronts:
+            K = int(K_of(f))
+            ns_ = max(1, -(-K // SPLIT_K))
+            for r0 in range(0, int(rows_of(f)), SOLVE_ROWS):
+                if ns_ == 1:
+                    g.append((f, r0, 0, -1))
+                else:
+                    s0 = nslot[0]
+                    nslot[0] += ns_
+                    for ks in range(ns_):
+                        g.append((f, r0, ks, s0 + ks))
+                    red.append((f, r0, ns_, s0))
+        return g, red
+
     for L in range(plan.nlevels):
         fronts = np.arange(plan.level_front_off[L], plan.level_front_off[L + 1])
         rows = [(f, r0) for f in fronts for r0 in range(0, fm[f], VEC_ROWS)]
         off, n = add(rows)
         fwd.append((SOP_FINIT, L, off, n, 0))
-        maxr = max((len(children[f]) for f in fronts), default=0)
-        for r in range(maxr):
-            rows = []
-            for f in fronts:
-                if r < len(children[f]):
-                    c = children[f][r]
-                    for r0 in range(0, fm[c] - fk[c], VEC_ROWS):
-                        rows.append((c, r0))
-            if rows:
-                off, n = add(rows)
-                fwd.append((SOP_FEXT, L, off, n, r))
-        rows = [(f, r0) for f in fronts for r0 in range(0, fm[f] - fk[f], SOLVE_ROWS)]
-        if rows:
-            off, n = add(rows)
+        g, red = gemm_items(fronts, lambda f: fm[f] - fk[f], lambda f: fk[f])
+        if g:
+            off, n = add(g)
             fwd.append((SOP_FGEMM, L, off, n, 0))
+        if red:
+            off, n = add(red)
+            fwd.append((SOP_FRED, L, off, n, 0))
     for L in reversed(range(plan.nlevels)):
         fronts = np.arange(plan.level_front_off[L], plan.level_front_off[L + 1])
-        rows = [(f, fk[f] + r0) for f in fronts for r0 in range(0, fm[f] - fk[f], VEC_ROWS)]
-        if rows:
-            off, n = add(rows)
-            bwd.append((SOP_BGATHER, L, off, n, 0))
-        rows = [(f, r0) for f in fronts for r0 in range(0, fk[f], SOLVE_ROWS)]
-        off, n = add(rows)
+        g, red = gemm_items(fronts, lambda f: fk[f], lambda f: fm[f])
+        off, n = add(g)
         bwd.append((SOP_BGEMM, L, off, n, 0))
+        if red:
+            off, n = add(red)
+            bwd.append((SOP_BRED, L, off, n, 0))
+    # gather sources: gsrc[row of front p] = absolute f_idx rows of child CB entries mapped there
+    nidx = int(plan.f_idx_off[-1])
+    gsrc = np.full((nidx, MAX_GSRC), -1, dtype=np.int64)
+    fill = np.zeros(nidx, dtype=np.int64)
+    for c in range(F):
+        p = par[c]
+        if p < 0:
+            continue
+        mp = plan.f_cmap[plan.f_cmap_off[c]:plan.f_cmap_off[c + 1]]
+        dst = plan.f_idx_off[p] + mp
+        srcrow = plan.f_idx_off[c] + fk[c] + np.arange(len(mp))
+        slot = fill[dst]
+        assert np.all(slot < MAX_GSRC), "too many children contribute to one front row"
+        gsrc[dst, slot] = srcrow
+        fill[dst] += 1
+    assert nidx < 2 ** 31
     work = np.vstack(items) if items else np.zeros((0, 4), np.int32)
-    return dict(work=np.ascontiguousarray(work.astype(np.int32)),
+    return dict(work=np.ascontiguousarray(work.astype(np.int32)), gsrc=np.ascontiguousarray(gsrc.astype(np.int32)),
+                nslot=int(nslot[0]), split_k=int(SPLIT_K), solve_rows=int(SOLVE_ROWS),
                 factor=np.array(fl, dtype=np.int64).reshape(-1, 5),
                 fwd=np.array(fwd, dtype=np.int64).reshape(-1, 5),
                 bwd=np.array(bwd, dtype=np.int64).reshape(-1, 5))

@@ -66,41 +66,56 @@ def factor(plan, as_vals, pw=S.PW):
 def solve(plan, st, rhs):
     """Apply the factorisation to rhs (n_total_internal, J); returns x (free rows)."""
     work = plan.schedule["work"]
-    fm, fk, off = plan.f_m, plan.f_k, plan.f_off
+    gsrc = plan.schedule["gsrc"]
+    fm, fk, off, io_ = plan.f_m, plan.f_k, plan.f_off, plan.f_idx_off
     J = rhs.shape[1]
-    fr = [np.zeros((int(fm[f]), J)) for f in range(plan.nfront)]
+    fr = np.zeros((int(io_[-1]), J))
     x = np.zeros_like(rhs)
+    partial = {}
 
     def front(f):
         m = int(fm[f])
         return st[off[f]:off[f] + m * m].reshape(m, m)
 
-    def idx(f):
-        return plan.f_idx[plan.f_idx_off[f]:plan.f_idx_off[f + 1]]
-
     for op, L, io, n, arg in plan.schedule["fwd"]:
         for it in work[io:io + n]:
             f, r0 = it[0], it[1]
+            base = io_[f]
             if op == S.SOP_FINIT:
                 rows = np.arange(r0, min(r0 + S.VEC_ROWS, fm[f]))
-                fr[f][rows] = np.where((rows < fk[f])[:, None], rhs[idx(f)[rows]], 0.0)
-            elif op == S.SOP_FEXT:
-                c = f
-                p = plan.f_parent[c]
-                mp = plan.f_cmap[plan.f_cmap_off[c]:plan.f_cmap_off[c + 1]]
-                rows = np.arange(r0, min(r0 + S.VEC_ROWS, len(mp)))
-                fr[p][mp[rows]] += fr[c][fk[c] + rows]
-            elif op == S.SOP_FGEMM:
+                val = np.where((rows < fk[f])[:, None], rhs[plan.f_idx[base + rows]], 0.0)
+                for s_ in range(S.MAX_GSRC):
+                    src = gsrc[base + rows, s_]
+                    val = val + np.where((src >= 0)[:, None], fr[np.maximum(src, 0)], 0.0)
+                fr[base + rows] = val
+            elif op in (S.SOP_FGEMM, S.SOP_FRED):
                 k = fk[f]
-                rows = slice(k + r0, min(k + r0 + S.SOLVE_ROWS, fm[f]))
-                fr[f][rows] -= front(f)[rows, :k] @ fr[f][:k]
+                rows = np.arange(k + r0, min(k + r0 + S.SOLVE_ROWS, fm[f]))
+                if op == S.SOP_FGEMM:
+                    ks, slot = it[2], it[3]
+                    kr = slice(ks * plan.schedule["split_k"], min(k, (ks + 1) * plan.schedule["split_k"]))
+                    prod = front(f)[rows, kr] @ fr[base + kr.start:base + kr.stop]
+                    if slot < 0:
+                        fr[base + rows] -= prod
+                    else:
+                        partial[slot] = prod
+                else:
+                    fr[base + rows] -= sum(partial[it[3] + s_] for s_ in range(it[2]))
     for op, L, io, n, arg in plan.schedule["bwd"]:
         for it in work[io:io + n]:
             f, r0 = it[0], it[1]
-            if op == S.SOP_BGATHER:
-                rows = np.arange(r0, min(r0 + S.VEC_ROWS, fm[f]))
-                fr[f][rows] = x[idx(f)[rows]]
-            elif op == S.SOP_BGEMM:
-                rows = np.arange(r0, min(r0 + S.SOLVE_ROWS, fk[f]))
-                x[idx(f)[rows]] = -front(f)[rows, :] @ fr[f]
+            base = io_[f]
+            k, m = fk[f], fm[f]
+            rows = np.arange(r0, min(r0 + S.SOLVE_ROWS, k))
+            if op == S.SOP_BGEMM:
+                ks, slot = it[2], it[3]
+                bop = np.vstack([fr[base:base + k], x[plan.f_idx[base + k:base + m]]])
+                kr = slice(ks * plan.schedule["split_k"], min(m, (ks + 1) * plan.schedule["split_k"]))
+                prod = front(f)[rows, kr] @ bop[kr]
+                if slot < 0:
+                    x[plan.f_idx[base + rows]] = -prod
+                else:
+                    partial[slot] = prod
+            elif op == S.SOP_BRED:
+                x[plan.f_idx[base + rows]] = -sum(partial[it[3] + s_] for s_ in range(it[2]))
     return x

@@ -83,3 +83,32 @@ def test_plan_invariants():
     sched = plan.schedule
     assert sched["work"].shape[1] == 4
     assert set(np.unique(sched["factor"][:, 0])) <= set(range(7))
+
+
+def test_split_k_schedule(rng, monkeypatch):
+    """Force tiny split-K so the partial/reduce path of the solve schedule is exercised."""
+    monkeypatch.setattr(S, "SPLIT_K", 16)
+    disc = Discretization.from_mesh(build_structured_square(8), pressure="th")
+    plan = S.analyse(disc)
+    assert plan.schedule["nslot"] > 0 and plan.schedule["split_k"] == 16
+    cfg = EnsembleConfig((MemberParams(0.01, 0.011), MemberParams(0.009, 0.01)), 1.0, 1.0, 0.01, 0.1)
+    w = rng.standard_normal((2, disc.n_vel))
+    pat = fe.scalar_pattern(disc.velocity)
+    a_s = O.velocity_block(w.mean(0), w - w.mean(0), cfg, disc)
+    vals = np.zeros(pat.nnz)
+    coo = a_s.tocoo()
+    rows = np.repeat(np.arange(pat.shape[0]), np.diff(pat.indptr))
+    key = rows * pat.shape[0] + pat.indices
+    vals[np.searchsorted(key, coo.row * pat.shape[0] + coo.col)] = coo.data
+    a_s = pat.copy()
+    a_s.data = vals
+    K = O.saddle_matrix(a_s, disc)
+    st = E.factor(plan, vals)
+    iid = internal_ids(disc, plan)
+    b = rng.standard_normal((disc.n_total, 2))
+    b[disc.constrained_rows] = 0.0
+    bi = np.zeros_like(b)
+    bi[iid] = b
+    x = E.solve(plan, st, bi)[iid]
+    res = np.linalg.norm(K @ x - b, axis=0) / np.linalg.norm(b, axis=0)
+    assert res.max() < 1e-11, res
