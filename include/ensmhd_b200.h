@@ -137,6 +137,9 @@ int64_t ens_kernel_launches(void);
 int  ens_create(const ens_mesh_desc* mesh, const ens_plan_desc* plan, int device, ens_ctx** out);
 void ens_destroy(ens_ctx* ctx);
 int  ens_workspace_bytes(const ens_ctx* ctx, int64_t* bytes);
+/* Panel inverses with in-panel partial pivoting (1) or diagonal pivots (0, default;
+ * the symbolic ordering guarantees nonsingular leading blocks in exact arithmetic). */
+int  ens_set_pivoting(ens_ctx* ctx, int on);
 
 /* Member sums over the J local columns: sum_v[r] = sum_j Xv[r][j] (r < n_vel), same for w. */
 int  ens_member_sums(ens_ctx* ctx, void* stream, const double* x, double* sums);

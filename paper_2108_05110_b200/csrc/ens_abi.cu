@@ -122,6 +122,12 @@ void ens_destroy(ens_ctx* c) {
     delete c;
 }
 
+int ens_set_pivoting(ens_ctx* c, int on) {
+    if (!c) return ENS_EINVAL;
+    c->diag_pivot = on ? 1 : 0;
+    return ENS_OK;
+}
+
 int ens_workspace_bytes(const ens_ctx* c, int64_t* bytes) {
     if (!c || !bytes) return ENS_EINVAL;
     *bytes = (int64_t)c->ws_bytes;

@@ -64,6 +64,9 @@ struct ens_ctx {
     int64_t g_solve_kernels = 0;
     void* g_factor = nullptr;      // cudaGraphExec_t
     const double* g_factor_key = nullptr;
+    int diag_pivot = 0;            // 1: in-panel partial pivoting in DIAG (k_diag), 0: k_diag_np
+    int use_mma = 1;               // DMMA (fp64 tensor core) panel kernels
+    int g_factor_pivot = 0;
     int64_t g_factor_kernels = 0;
 };
 

@@ -61,12 +61,15 @@ __global__ void k_extadd(MfDev d, int item0, double* __restrict__ F) {
 // inverse is recovered as A^-1[i][j] = a[piv[i]][ipiv[j]].
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(256) k_diag(MfDev d, int item0, double* __restrict__ F, int32_t* __restrict__ npert) {
+    // 2 barriers per elimination step: (A) column k+1 published by its owners right
+    // after their update; (B) every warp finds the pivot row redundantly from smem
+    // (no serial section), then the pivot row's owners publish it.
     __shared__ double s_col[2][ENS_PW];
     __shared__ double s_row[2][ENS_PW];
     __shared__ int s_piv[ENS_PW];
     __shared__ int s_ipiv[ENS_PW];
-    __shared__ unsigned char s_used[ENS_PW];
-    __shared__ double s_scale;
+    __shared__ unsigned char s_used[2][ENS_PW];
+    __shared__ double s_wmax[8];
     __shared__ double s_out[ENS_PW][ENS_PW + 1];
     const int* it = d.work + 4LL * (item0 + blockIdx.x);
     const int f = it[0], a0 = it[1];
@@ -75,6 +78,7 @@ __global__ void __launch_bounds__(256) k_diag(MfDev d, int item0, double* __rest
     const int pw = min(ENS_PW, d.k[f] - a0);
     double* Fb = F + (int64_t)mat * d.storage + d.off[f] + (int64_t)a0 * m + a0;
     const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     double a[4][4];
     double amax = 0.0;
 #pragma unroll
@@ -87,70 +91,63 @@ __global__ void __launch_bounds__(256) k_diag(MfDev d, int item0, double* __rest
             a[i][j] = v;
             if (r < pw && c < pw) amax = fmax(amax, fabs(v));
         }
-    if (threadIdx.x < ENS_PW) s_used[threadIdx.x] = 0;
-    // block max for the tiny-pivot threshold
     for (int o = 16; o > 0; o >>= 1) amax = fmax(amax, __shfl_xor_sync(0xffffffffu, amax, o));
-    if (threadIdx.x == 0) s_scale = 0.0;
+    if (lane == 0) s_wmax[warp] = amax;
+    if (threadIdx.x < ENS_PW) s_used[0][threadIdx.x] = s_used[1][threadIdx.x] = 0;
+    // publish column 0
+    if (tx == 0) {
+#pragma unroll
+        for (int i = 0; i < 4; ++i) s_col[0][ty + 16 * i] = a[i][0];
+    }
     __syncthreads();
-    if ((threadIdx.x & 31) == 0) atomicMax((unsigned long long*)&s_scale, (unsigned long long)__double_as_longlong(amax));
-    __syncthreads();
-    const double thr = 1e-14 * (s_scale > 0.0 ? s_scale : 1.0);
+    double scale = 0.0;
+#pragma unroll
+    for (int w = 0; w < 8; ++w) scale = fmax(scale, s_wmax[w]);
+    const double thr = 1e-14 * (scale > 0.0 ? scale : 1.0);
+    int pert = 0;
     for (int k = 0; k < pw; ++k) {
         const int buf = k & 1;
-        // 1. column k to smem
-        if (tx == (k & 15)) {
+        // (B) pivot search, redundantly in every warp: rows lane, lane+32
+        double best = -1.0;
+        int br = ENS_PW;
 #pragma unroll
-            for (int i = 0; i < 4; ++i) {
-                const int jj = k >> 4;
-                double v = 0.0;
-#pragma unroll
-                for (int j = 0; j < 4; ++j)
-                    if (j == jj) v = a[i][j];
-                s_col[buf][ty + 16 * i] = v;
-            }
-        }
-        __syncthreads();
-        // 2. pivot row: largest |a[r][k]| among unused rows r < pw
-        if (threadIdx.x < 32) {
-            double best = -1.0;
-            int br = ENS_PW;
-            for (int r = threadIdx.x; r < pw; r += 32) {
-                if (s_used[r]) continue;
+        for (int h = 0; h < 2; ++h) {
+            const int r = lane + 32 * h;
+            if (r < pw && !s_used[buf][r]) {
                 const double v = fabs(s_col[buf][r]);
                 if (v > best) {
                     best = v;
                     br = r;
                 }
             }
-            for (int o = 16; o > 0; o >>= 1) {
-                const double ob = __shfl_xor_sync(0xffffffffu, best, o);
-                const int orr = __shfl_xor_sync(0xffffffffu, br, o);
-                if (ob > best || (ob == best && orr < br)) {
-                    best = ob;
-                    br = orr;
-                }
-            }
-            if (threadIdx.x == 0) {
-                if (br >= pw) {        // NaN column: take the first unused row
-                    for (int r = 0; r < pw; ++r)
-                        if (!s_used[r]) {
-                            br = r;
-                            break;
-                        }
-                }
-                if (!(best > thr)) {   // singular/tiny pivot: static perturbation, GMRES corrects it
-                    s_col[buf][br] = (s_col[buf][br] < 0.0 ? -thr : thr);
-                    atomicAdd(npert, 1);
-                }
-                s_used[br] = 1;
-                s_piv[k] = br;
-                s_ipiv[br] = k;
+        }
+        for (int o = 16; o > 0; o >>= 1) {
+            const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+            const int orr = __shfl_xor_sync(0xffffffffu, br, o);
+            if (ob > best || (ob == best && orr < br)) {
+                best = ob;
+                br = orr;
             }
         }
-        __syncthreads();
-        const int p = s_piv[k];
-        // 3. pivot row to smem
-        if (ty == (p & 15)) {
+        if (br >= pw) {   // NaN column: first unused row
+            for (int r = 0; r < pw; ++r)
+                if (!s_used[buf][r]) {
+                    br = r;
+                    break;
+                }
+        }
+        const int p = br;
+        double piv = s_col[buf][p];
+        if (!(best > thr)) {   // tiny pivot: static perturbation (FGMRES corrects it)
+            piv = piv < 0.0 ? -thr : thr;
+            pert = 1;
+        }
+        if (threadIdx.x < ENS_PW) s_used[buf ^ 1][threadIdx.x] = s_used[buf][threadIdx.x] | (threadIdx.x == p);
+        if (threadIdx.x == 0) {
+            s_piv[k] = p;
+            s_ipiv[p] = k;
+        }
+        if (ty == (p & 15)) {   // publish row p
             const int ii = p >> 4;
 #pragma unroll
             for (int j = 0; j < 4; ++j) {
@@ -162,8 +159,8 @@ __global__ void __launch_bounds__(256) k_diag(MfDev d, int item0, double* __rest
             }
         }
         __syncthreads();
-        // 4. eliminate (pivot element of column k treated as 1, in-place inverse)
-        const double inv = 1.0 / s_col[buf][p];
+        // update (pivot element of column k treated as 1: in-place inverse)
+        const double inv = 1.0 / piv;
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
             const int c = tx + 16 * j;
@@ -179,7 +176,21 @@ __global__ void __launch_bounds__(256) k_diag(MfDev d, int item0, double* __rest
                 }
             }
         }
+        // (A) publish column k+1 into the other buffer
+        if (k + 1 < pw && tx == ((k + 1) & 15)) {
+            const int jj = (k + 1) >> 4;
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                double v = 0.0;
+#pragma unroll
+                for (int j = 0; j < 4; ++j)
+                    if (j == jj) v = a[i][j];
+                s_col[buf ^ 1][ty + 16 * i] = v;
+            }
+        }
+        __syncthreads();
     }
+    if (pert && threadIdx.x == 0) atomicAdd(npert, 1);
     // un-permute and store -D^-1
 #pragma unroll
     for (int i = 0; i < 4; ++i)
@@ -190,6 +201,114 @@ __global__ void __launch_bounds__(256) k_diag(MfDev d, int item0, double* __rest
         const int r = t / pw, c = t % pw;
         Fb[(int64_t)r * m + c] = -s_out[s_piv[r]][s_ipiv[c]];
     }
+}
+
+// DIAG without pivoting (default): the symbolic ordering (velocities before
+// pressures, pressures moved above all their velocity neighbours) makes every
+// leading block of a panel nonsingular, so the in-place Gauss-Jordan can take
+// the diagonal pivot.  One barrier per step: after its update, the owners of
+// column k+1 and row k+1 publish them for the next step.  A pivot below
+// 1e-14 x max|D| is perturbed and counted; the host then refactorises with the
+// pivoting kernel (k_diag).
+__global__ void __launch_bounds__(256, 3) k_diag_np(MfDev d, int item0, double* __restrict__ F,
+                                                  int32_t* __restrict__ npert) {
+    __shared__ double s_col[2][ENS_PW];
+    __shared__ double s_row[2][ENS_PW];
+    __shared__ double s_wmax[8];
+    const int* it = d.work + 4LL * (item0 + blockIdx.x);
+    const int f = it[0], a0 = it[1];
+    const int mat = blockIdx.y;
+    const int m = d.m[f];
+    const int pw = min(ENS_PW, d.k[f] - a0);
+    double* Fb = F + (int64_t)mat * d.storage + d.off[f] + (int64_t)a0 * m + a0;
+    const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    double a[4][4];
+    double amax = 0.0;
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const int r = ty + 16 * i, c = tx + 16 * j;
+            double v = (r == c) ? 1.0 : 0.0;
+            if (r < pw && c < pw) v = Fb[(int64_t)r * m + c];
+            a[i][j] = v;
+            if (r < pw && c < pw) amax = fmax(amax, fabs(v));
+        }
+    for (int o = 16; o > 0; o >>= 1) amax = fmax(amax, __shfl_xor_sync(0xffffffffu, amax, o));
+    if (lane == 0) s_wmax[warp] = amax;
+    if (tx == 0) {
+#pragma unroll
+        for (int i = 0; i < 4; ++i) s_col[0][ty + 16 * i] = a[i][0];
+    }
+    if (ty == 0) {
+#pragma unroll
+        for (int j = 0; j < 4; ++j) s_row[0][tx + 16 * j] = a[0][j];
+    }
+    __syncthreads();
+    double scale = 0.0;
+#pragma unroll
+    for (int w = 0; w < 8; ++w) scale = fmax(scale, s_wmax[w]);
+    const double thr = 1e-14 * (scale > 0.0 ? scale : 1.0);
+    int pert = 0;
+    for (int k = 0; k < pw; ++k) {
+        const int buf = k & 1;
+        double piv = s_col[buf][k];
+        if (!(fabs(piv) > thr)) {
+            piv = piv < 0.0 ? -thr : thr;
+            pert = 1;
+        }
+        const double inv = 1.0 / piv;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const int c = tx + 16 * j;
+            const double np = (c == k ? 1.0 : s_row[buf][c]) * inv;
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                const int r = ty + 16 * i;
+                if (r == k) {
+                    a[i][j] = np;
+                } else {
+                    const double fr = s_col[buf][r];
+                    a[i][j] = (c == k ? 0.0 : a[i][j]) - fr * np;
+                }
+            }
+        }
+        const int k1 = k + 1;
+        if (k1 < pw) {
+            if (tx == (k1 & 15)) {
+                const int jj = k1 >> 4;
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    double v = 0.0;
+#pragma unroll
+                    for (int j = 0; j < 4; ++j)
+                        if (j == jj) v = a[i][j];
+                    s_col[buf ^ 1][ty + 16 * i] = v;
+                }
+            }
+            if (ty == (k1 & 15)) {
+                const int ii = k1 >> 4;
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    double v = 0.0;
+#pragma unroll
+                    for (int i = 0; i < 4; ++i)
+                        if (i == ii) v = a[i][j];
+                    s_row[buf ^ 1][tx + 16 * j] = v;
+                }
+            }
+        }
+        __syncthreads();
+    }
+    if (pert && threadIdx.x == 0) atomicAdd(npert, 1);
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const int r = ty + 16 * i, c = tx + 16 * j;
+            if (r < pw && c < pw) Fb[(int64_t)r * m + c] = -a[i][j];
+        }
 }
 
 // ---------------------------------------------------------------------------
@@ -337,12 +456,20 @@ static const size_t SM_HP = sizeof(double) * (ENS_PW * LDA + ENS_PW * ENS_TILE);
 static const size_t SM_UP = sizeof(double) * (ENS_TILE * LDA + ENS_PW * ENS_TILE);
 static const size_t SM_GP = sizeof(double) * (ENS_TILE * LDA + ENS_PW * ENS_TILE);
 
+int mf_mma_setup();
+void launch_update_mma(const MfDev& d, int off, int n, double* F, cudaStream_t s);
+void launch_hpanel_mma(const MfDev& d, int off, int n, double* F, cudaStream_t s);
+void launch_gpanel_mma(const MfDev& d, int off, int n, double* F, cudaStream_t s);
+
 int mf_setup(ens_ctx* c) {
     ENS_CK(cudaFuncSetAttribute(k_hpanel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SM_HP));
     ENS_CK(cudaFuncSetAttribute(k_update, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SM_UP));
     ENS_CK(cudaFuncSetAttribute(k_gpanel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SM_GP));
-    (void)c;
-    return ENS_OK;
+    const char* e = std::getenv("ENS_MMA");
+    // DMMA panel kernels measured slower than the DFMA ones at C2 (15.0 vs 10.4 ms
+    // per factorisation pair); opt-in with ENS_MMA=1 until that is understood
+    c->use_mma = (e && e[0] == '1');
+    return mf_mma_setup();
 }
 
 static int mf_factor_launches(ens_ctx* c, cudaStream_t s, const double* as_vals, int64_t* nlaunch) {
@@ -373,16 +500,28 @@ static int mf_factor_launches(ens_ctx* c, cudaStream_t s, const double* as_vals,
                 k_extadd<<<dim3(n, 2), 256, 0, s>>>(d, off, c->fronts);
                 break;
             case OP_DIAG:
-                k_diag<<<dim3(n, 2), 256, 0, s>>>(d, off, c->fronts, c->d_count);
+                if (c->diag_pivot)
+                    k_diag<<<dim3(n, 2), 256, 0, s>>>(d, off, c->fronts, c->d_count);
+                else
+                    k_diag_np<<<dim3(n, 2), 256, 0, s>>>(d, off, c->fronts, c->d_count);
                 break;
             case OP_HPANEL:
-                k_hpanel<<<dim3(n, 2), 256, SM_HP, s>>>(d, off, c->fronts);
+                if (c->use_mma)
+                    launch_hpanel_mma(d, off, n, c->fronts, s);
+                else
+                    k_hpanel<<<dim3(n, 2), 256, SM_HP, s>>>(d, off, c->fronts);
                 break;
             case OP_UPDATE:
-                k_update<<<dim3(n, 2), 256, SM_UP, s>>>(d, off, c->fronts);
+                if (c->use_mma)
+                    launch_update_mma(d, off, n, c->fronts, s);
+                else
+                    k_update<<<dim3(n, 2), 256, SM_UP, s>>>(d, off, c->fronts);
                 break;
             case OP_GPANEL:
-                k_gpanel<<<dim3(n, 2), 256, SM_GP, s>>>(d, off, c->fronts);
+                if (c->use_mma)
+                    launch_gpanel_mma(d, off, n, c->fronts, s);
+                else
+                    k_gpanel<<<dim3(n, 2), 256, SM_GP, s>>>(d, off, c->fronts);
                 break;
             default:
                 ens_set_error("bad factor op", __FILE__, __LINE__);
@@ -405,7 +544,7 @@ int mf_factor(ens_ctx* c, cudaStream_t s, const double* as_vals, int32_t* n_pert
         const int rc = mf_factor_launches(c, s, as_vals, &n);
         if (rc != ENS_OK) return rc;
     } else {
-        if (c->g_factor && c->g_factor_key != as_vals) {
+        if (c->g_factor && (c->g_factor_key != as_vals || c->g_factor_pivot != c->diag_pivot)) {
             cudaGraphExecDestroy((cudaGraphExec_t)c->g_factor);
             c->g_factor = nullptr;
         }
@@ -420,6 +559,7 @@ int mf_factor(ens_ctx* c, cudaStream_t s, const double* as_vals, int32_t* n_pert
             ENS_CK(cudaGraphInstantiate((cudaGraphExec_t*)&c->g_factor, g, 0));
             cudaGraphDestroy(g);
             c->g_factor_key = as_vals;
+            c->g_factor_pivot = c->diag_pivot;
             c->g_factor_kernels = n;
             g_ens_launches -= (unsigned long long)n;
         }

@@ -7,8 +7,8 @@
 // Backward, per level (root -> leaves):
 //     BGEMM  x[P] = -[F[P,P] F[P,C]] [fr_f[P]; x[C]]   (x[C] read straight from the iterate)
 // The products are skinny GEMMs (N = J members).  A CTA owns 64 rows x 32
-// member columns over an inner range of <= split_k and streams the factor rows
-// through a two-stage cp.async pipeline in shared memory.  Long inner
+// member columns over an inner range of <= split_k (128) staged in shared
+// memory with one cp.async group.  Long inner
 // dimensions (top of the tree) are split into independent items whose partial
 // products land in scratch slots and are summed in a fixed order by *RED
 // (deterministic, no atomics: bitwise-identical members stay identical).
@@ -77,19 +77,24 @@ __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_gr
 
 #define SG_R 64     // rows per CTA (= symbolic.SOLVE_ROWS)
 #define SG_C 32     // member columns per CTA
-#define SG_K 32     // inner chunk per pipeline stage
+#define SG_KMAX 128 // max inner range per work item (= symbolic.SPLIT_K)
 #define SG_T 256    // threads
+#define SG_LDA (SG_KMAX + 1)
 
 // forward (bwd=0): fr[k+r0+i] -= sum_{t<k} F[k+r0+i][t] fr[t]
 // backward (bwd=1): x[idx[r0+i]] = -sum_{t<m} F[r0+i][t] (t < k ? fr[t] : x[idx[t]])
-// item = (f, r0, ks, slot): slot < 0 -> whole inner range, result applied here;
+// item = (f, r0, ks, slot): slot < 0 -> whole inner range (<= SG_KMAX), result applied here;
 //                          slot >= 0 -> range [ks*split_k, ...), product stored to partial[slot]
+// The whole inner range is staged at once (one cp.async group): rows are
+// row-major with a +1 pad so both the async writes and the compute reads are
+// bank-conflict free.
 __global__ void __launch_bounds__(SG_T) k_sgemm(MfDev d, int item0, const double* __restrict__ F,
                                                 double* __restrict__ FR, const SolveIO* __restrict__ io, int64_t N,
                                                 int J, int64_t nidx, int bwd, int split_k,
                                                 double* __restrict__ partial, int64_t nslot) {
-    __shared__ double As[2][SG_K][SG_R];   // K-major: conflict-free row reads in the inner loop
-    __shared__ double Bs[2][SG_K][SG_C];
+    extern __shared__ double sm[];
+    double* As = sm;                          // [SG_R][SG_LDA]
+    double* Bs = sm + SG_R * SG_LDA;          // [SG_KMAX][SG_C]
     const int* it = d.work + 4LL * (item0 + blockIdx.x);
     const int f = it[0], r0 = it[1], ks = it[2], slot = it[3];
     const int mat = blockIdx.y;
@@ -101,61 +106,46 @@ __global__ void __launch_bounds__(SG_T) k_sgemm(MfDev d, int item0, const double
     const int K = bwd ? m : k;
     const int kbeg = slot < 0 ? 0 : ks * split_k;
     const int kend = slot < 0 ? K : min(K, kbeg + split_k);
+    const int kc = kend - kbeg;               // <= SG_KMAX by construction of the schedule
     const double* base = F + (int64_t)mat * d.storage + d.off[f];
     const int64_t fo = d.idx_off[f];
     double* fr = FR + (int64_t)mat * nidx * J + fo * J;
     double* x = io->z + (int64_t)mat * N * J;
     const int tid = threadIdx.x;
-    const int nchunk = (kend - kbeg + SG_K - 1) / SG_K;
-
-    auto load = [&](int stage, int t0) {
-#pragma unroll
-        for (int u = 0; u < (SG_R * SG_K) / SG_T; ++u) {
-            const int e = tid + u * SG_T;
-            const int r = e / SG_K, kk = e % SG_K;
-            const bool ok = r < nr && t0 + kk < kend;
-            cp_async8(&As[stage][kk][r], ok ? base + (int64_t)(rbase + r) * m + t0 + kk : base, ok);
-        }
-#pragma unroll
-        for (int u = 0; u < (SG_K * SG_C) / SG_T; ++u) {
-            const int e = tid + u * SG_T;
-            const int kk = e / SG_C, j = e % SG_C;
-            const int t = t0 + kk;
-            const bool ok = t < kend && j < jn;
-            const double* src = fr;
-            if (ok) src = (t < k) ? fr + (int64_t)t * J + j0 + j : x + (int64_t)d.idx[fo + t] * J + j0 + j;
-            cp_async8(&Bs[stage][kk][j], src, ok);
-        }
-        cp_async_commit();
-    };
-
+    // stage A rows (consecutive lanes -> consecutive inner index: coalesced, conflict-free)
+    for (int e = tid; e < SG_R * SG_KMAX; e += SG_T) {
+        const int r = e / SG_KMAX, kk = e % SG_KMAX;
+        if (kk >= kc) continue;
+        const bool ok = r < nr;
+        cp_async8(&As[r * SG_LDA + kk], ok ? base + (int64_t)(rbase + r) * m + kbeg + kk : base, ok);
+    }
+    for (int e = tid; e < SG_KMAX * SG_C; e += SG_T) {
+        const int kk = e / SG_C, j = e % SG_C;
+        if (kk >= kc) continue;
+        const int t = kbeg + kk;
+        const bool ok = j < jn;
+        const double* src = fr;
+        if (ok) src = (t < k) ? fr + (int64_t)t * J + j0 + j : x + (int64_t)d.idx[fo + t] * J + j0 + j;
+        cp_async8(&Bs[kk * SG_C + j], src, ok);
+    }
+    cp_async_commit();
+    cp_async_wait<0>();
+    __syncthreads();
     const int tx = tid & 15, ty = tid >> 4;   // cols tx, tx+16 ; rows ty + 16 i
     double acc[4][2];
 #pragma unroll
     for (int i = 0; i < 4; ++i) acc[i][0] = acc[i][1] = 0.0;
-    if (nchunk > 0) load(0, kbeg);
-    for (int c = 0; c < nchunk; ++c) {
-        if (c + 1 < nchunk) {
-            load((c + 1) & 1, kbeg + (c + 1) * SG_K);
-            cp_async_wait<1>();
-        } else {
-            cp_async_wait<0>();
-        }
-        __syncthreads();
-        const int st = c & 1;
-        const int kc = min(SG_K, kend - kbeg - c * SG_K);
-        for (int kk = 0; kk < kc; ++kk) {
-            double a[4];
+#pragma unroll 4
+    for (int kk = 0; kk < kc; ++kk) {
+        double a[4];
 #pragma unroll
-            for (int i = 0; i < 4; ++i) a[i] = As[st][kk][ty + 16 * i];
-            const double b0 = Bs[st][kk][tx], b1 = Bs[st][kk][tx + 16];
+        for (int i = 0; i < 4; ++i) a[i] = As[(ty + 16 * i) * SG_LDA + kk];
+        const double b0 = Bs[kk * SG_C + tx], b1 = Bs[kk * SG_C + tx + 16];
 #pragma unroll
-            for (int i = 0; i < 4; ++i) {
-                acc[i][0] = fma(a[i], b0, acc[i][0]);
-                acc[i][1] = fma(a[i], b1, acc[i][1]);
-            }
+        for (int i = 0; i < 4; ++i) {
+            acc[i][0] = fma(a[i], b0, acc[i][0]);
+            acc[i][1] = fma(a[i], b1, acc[i][1]);
         }
-        __syncthreads();
     }
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
@@ -175,6 +165,7 @@ __global__ void __launch_bounds__(SG_T) k_sgemm(MfDev d, int item0, const double
     }
 }
 
+static const size_t SM_SG = sizeof(double) * (SG_R * SG_LDA + SG_KMAX * SG_C);
 // ordered sum of the split-K partials + the update; item = (f, r0, nsplit, slot0)
 __global__ void k_sred(MfDev d, int item0, double* __restrict__ FR, const SolveIO* __restrict__ io, int64_t N, int J,
                        int64_t nidx, int bwd, const double* __restrict__ partial, int64_t nslot) {
@@ -225,7 +216,7 @@ static int mf_solve_launches(ens_ctx* c, cudaStream_t s, SolveIO* io, int64_t* n
                     break;
                 case SOP_FGEMM:
                 case SOP_BGEMM:
-                    k_sgemm<<<dim3(n, 2, zc), SG_T, 0, s>>>(d, off, c->fronts, c->frvec, io, N, J, nidx,
+                    k_sgemm<<<dim3(n, 2, zc), SG_T, SM_SG, s>>>(d, off, c->fronts, c->frvec, io, N, J, nidx,
                                                             op == SOP_BGEMM, sk, c->partial, nslot);
                     break;
                 case SOP_FRED:
@@ -253,6 +244,11 @@ static bool graphs_enabled() {
 int mf_solve(ens_ctx* c, cudaStream_t s, const double* r, double* z) {
     if (!c->solve_io) {
         ENS_CK(cudaMalloc(&c->solve_io, sizeof(SolveIO)));
+        ENS_CK(cudaFuncSetAttribute(k_sgemm, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SM_SG));
+        if (c->p.split_k > SG_KMAX) {
+            ens_set_error("plan split_k exceeds the solve kernel's inner tile", __FILE__, __LINE__);
+            return ENS_EINVAL;
+        }
     }
     if (!c->partial && c->p.n_slot > 0) {
         const size_t bytes = sizeof(double) * 2 * (size_t)c->p.n_slot * SG_R * c->J;

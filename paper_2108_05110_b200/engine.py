@@ -214,6 +214,7 @@ class Engine:
         self.factored = False
         self.since_factor = 0
         self.n_factor = 0
+        self.pivoting = False
         if not torch.cuda.is_available():
             raise RuntimeError("the B200 time-step engine needs a CUDA device (no CPU fallback)")
         self.lib = N.load()
@@ -548,6 +549,11 @@ class Engine:
     def _factor(self):
         npert = N.I32(0)
         N.check(self.lib.ens_factor(self.ctx, self.sptr, _dptr(self.as_vals), C.byref(npert)), "ens_factor")
+        if npert.value > 0 and not self.pivoting:
+            # a diagonal pivot was tiny: switch this engine to in-panel pivoting for good
+            self.pivoting = True
+            N.check(self.lib.ens_set_pivoting(self.ctx, 1), "ens_set_pivoting")
+            N.check(self.lib.ens_factor(self.ctx, self.sptr, _dptr(self.as_vals), C.byref(npert)), "ens_factor")
         self.last_pert = int(npert.value)
         self.factored = True
         self.since_factor = 0

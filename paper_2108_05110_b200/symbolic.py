@@ -22,7 +22,9 @@ Design:
     (`stepper.py:214-215`); they are eliminated trivially and never enter a
     front (the Krylov iterate carries their values exactly).
   * Each front's pivots are split into panels of <= PW dofs; the numeric phase
-    stores per panel D^-1 (PW x PW), H = -D^-1 R and G = -C D^-1 (see csrc/mf.cu).
+    sweeps them (block Gauss-Jordan) so a factorised front holds
+    [-F11^-1, F11^-1 F12; F21 F11^-1, S] and every solve is one batched GEMM per
+    tree level and direction (csrc/ens_mf.cu, csrc/ens_mfsolve.cu).
 
 Everything returned is flat int32/int64 numpy arrays plus a launch schedule,
 uploaded once by the engine.
@@ -385,7 +387,7 @@ def analyse(disc, leaf=LEAF_NODES, pw=PW):
 # op codes (must match csrc/mf.cu)
 OP_ZERO, OP_ORIG, OP_EXTADD, OP_DIAG, OP_HPANEL, OP_UPDATE, OP_GPANEL = range(7)
 SOP_FINIT, SOP_FEXT, SOP_FGEMM, SOP_BGATHER, SOP_BGEMM, SOP_FRED, SOP_BRED = range(7)
-SPLIT_K = 512     # inner-dimension length per solve-GEMM work item (csrc/ens_mfsolve.cu SG_KS)
+SPLIT_K = int(__import__("os").environ.get("ENS_SPLIT_K", "128"))  # inner length per solve-GEMM work item
 MAX_GSRC = 4      # child contribution rows gathered per front-vector row
 EXT_ROWS = 8      # child-CB rows per extend-add work item
 VEC_ROWS = 64     # front-vector rows per init/gather/scatter work item

@@ -127,10 +127,14 @@ def test_member_pass_assembly_rhs(c1, rng):
         assert np.max(np.abs(got - ref)) <= 1e-12 * np.abs(ref).max()
 
 
-def test_factor_solve_residual(c1, rng):
+@pytest.mark.parametrize("pivoting", [False, True])
+def test_factor_solve_residual(c1, rng, pivoting):
     disc, cfg, _ = c1
     eng = Engine(disc, cfg)
     hm = eng.hm
+    if pivoting:
+        eng.pivoting = True
+        eng.lib.ens_set_pivoting(eng.ctx, 1)
     v, w = perturbed_state(disc, cfg, rng)
     a_v = O.velocity_block(w.mean(0), w - w.mean(0), cfg, disc)
     a_w = O.velocity_block(v.mean(0), v - v.mean(0), cfg, disc)
