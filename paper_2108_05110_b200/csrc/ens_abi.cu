@@ -119,6 +119,7 @@ void ens_destroy(ens_ctx* c) {
     if (c->g_factor) cudaGraphExecDestroy((cudaGraphExec_t)c->g_factor);
     cudaFree(c->solve_io);
     cudaFree(c->partial);
+    cudaFree(c->ticket);
     delete c;
 }
 

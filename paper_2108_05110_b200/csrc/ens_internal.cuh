@@ -60,6 +60,7 @@ struct ens_ctx {
     // CUDA graphs of the fixed launch sequences
     void* solve_io = nullptr;      // device {r, z} pointer table of the solve graph
     double* partial = nullptr;     // split-K partial products of the solve GEMMs
+    int* ticket = nullptr;         // split-K arrival counters (last CTA reduces)
     void* g_solve = nullptr;       // cudaGraphExec_t
     int64_t g_solve_kernels = 0;
     void* g_factor = nullptr;      // cudaGraphExec_t

@@ -1,17 +1,18 @@
 // Multi-column solves with the block-sweep fronts (sm_100a, fp64).
 //
 // After ens_mf.cu's sweep each front holds [-F11^-1, F11^-1 F12; F21 F11^-1, S].
-// Forward, per tree level (leaves -> root):
-//     FINIT  fr_f = [b(pivots); 0] + the children's contribution rows (one gather pass)
-//     FGEMM  fr_f[C] -= F[C,P] fr_f[P]
-// Backward, per level (root -> leaves):
-//     BGEMM  x[P] = -[F[P,P] F[P,C]] [fr_f[P]; x[C]]   (x[C] read straight from the iterate)
+// Forward, one launch per tree level (leaves -> root):
+//     fr[P] = b[P] + children's contribution rows           (gathered in-kernel)
+//     fr[C] = children's contribution rows - F[C,P] fr[P]
+// Backward, one launch per level (root -> leaves):
+//     x[P]  = -[F[P,P] F[P,C]] [fr[P]; x[C]]                (x[C] read from the iterate)
 // The products are skinny GEMMs (N = J members).  A CTA owns 64 rows x 32
-// member columns over an inner range of <= split_k (128) staged in shared
-// memory with one cp.async group.  Long inner
-// dimensions (top of the tree) are split into independent items whose partial
-// products land in scratch slots and are summed in a fixed order by *RED
-// (deterministic, no atomics: bitwise-identical members stay identical).
+// member columns over an inner range of <= split_k, staged in shared memory
+// with one cp.async group (shared memory sized per launch from the level's
+// largest inner range, so leaf levels run many CTAs per SM).  Long inner
+// dimensions are split into items that store partial products; the last CTA of
+// a group to finish (atomic ticket) sums them in a fixed order -- deterministic,
+// so bitwise-identical members stay identical.
 //
 // The whole solve is captured once into a CUDA graph; the in/out blocks are
 // passed through a 2-pointer device table so the graph serves every Krylov vector.
@@ -42,94 +43,159 @@ __global__ void k_copy_cons_io(const int32_t* __restrict__ crow, int ncons, cons
     io->z[idx] = io->r[idx];
 }
 
-__global__ void k_finit(MfDev d, int item0, const SolveIO* __restrict__ io, double* __restrict__ FR, int64_t N, int J,
-                        int64_t nidx) {
-    const int* it = d.work + 4LL * (item0 + blockIdx.x);
-    const int f = it[0], r0 = it[1];
-    const int mat = blockIdx.y;
-    const int m = d.m[f], k = d.k[f];
-    const int rows = min(ENS_VEC_ROWS, m - r0);
-    const int64_t fo = d.idx_off[f];
-    double* fr = FR + (int64_t)mat * nidx * J;
-    const double* b = io->r + (int64_t)mat * N * J;
-    for (int t = threadIdx.x; t < rows * J; t += blockDim.x) {
-        const int i = r0 + t / J, j = t % J;
-        const int64_t row = fo + i;
-        double v = i < k ? b[(int64_t)d.idx[row] * J + j] : 0.0;
-        const int32_t* g = d.gsrc + 4 * row;
-#pragma unroll
-        for (int s = 0; s < 4; ++s) {
-            const int32_t src = g[s];
-            if (src >= 0) v += fr[(int64_t)src * J + j];
-        }
-        fr[row * J + j] = v;
-    }
-}
-
 __device__ __forceinline__ void cp_async8(double* smem, const double* gmem, bool pred) {
     const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
     const int sz = pred ? 8 : 0;   // src-size 0 -> zero fill
     asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(s), "l"(gmem), "r"(sz));
 }
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::); }
 
 #define SG_R 64     // rows per CTA (= symbolic.SOLVE_ROWS)
 #define SG_C 32     // member columns per CTA
-#define SG_KMAX 128 // max inner range per work item (= symbolic.SPLIT_K)
+#define SG_KMAX 128 // max inner range per work item (>= symbolic.SPLIT_K)
 #define SG_T 256    // threads
-#define SG_LDA (SG_KMAX + 1)
 
-// forward (bwd=0): fr[k+r0+i] -= sum_{t<k} F[k+r0+i][t] fr[t]
-// backward (bwd=1): x[idx[r0+i]] = -sum_{t<m} F[r0+i][t] (t < k ? fr[t] : x[idx[t]])
-// item = (f, r0, ks, slot): slot < 0 -> whole inner range (<= SG_KMAX), result applied here;
-//                          slot >= 0 -> range [ks*split_k, ...), product stored to partial[slot]
-// The whole inner range is staged at once (one cp.async group): rows are
-// row-major with a +1 pad so both the async writes and the compute reads are
-// bank-conflict free.
+// children's contribution rows mapped onto front row `row` (+ b at pivots)
+__device__ __forceinline__ double gather_row(const MfDev& d, const double* __restrict__ FRm,
+                                             const double* __restrict__ b, int64_t row, int J, int j, bool pivot) {
+    double v = pivot ? b[(int64_t)d.idx[row] * J + j] : 0.0;
+    const int32_t* g = d.gsrc + 4 * row;
+#pragma unroll
+    for (int s = 0; s < 4; ++s) {
+        const int32_t src = g[s];
+        if (src >= 0) v += FRm[(int64_t)src * J + j];
+    }
+    return v;
+}
+
+// item = (f, r0, ks, slot)
+//   r0 = -1 : forward pivot-only item (front without contribution block)
+//   slot<0  : whole inner range, result applied here
+//   slot>=0 : inner range [ks*split_k, ...) of group s0 = slot - ks; the last
+//             CTA of the group reduces partial[s0 .. s0+ns) in order
 __global__ void __launch_bounds__(SG_T) k_sgemm(MfDev d, int item0, const double* __restrict__ F,
                                                 double* __restrict__ FR, const SolveIO* __restrict__ io, int64_t N,
-                                                int J, int64_t nidx, int bwd, int split_k,
-                                                double* __restrict__ partial, int64_t nslot) {
+                                                int J, int64_t nidx, int bwd, int split_k, int kmax,
+                                                double* __restrict__ partial, int* __restrict__ ticket,
+                                                int64_t nslot) {
     extern __shared__ double sm[];
-    double* As = sm;                          // [SG_R][SG_LDA]
-    double* Bs = sm + SG_R * SG_LDA;          // [SG_KMAX][SG_C]
+    __shared__ int s_last;
+    const int lda = kmax + 1;
+    double* As = sm;                          // [SG_R][lda]  (+1 pad: conflict-free)
+    double* Bs = sm + SG_R * lda;             // [kmax][SG_C]
     const int* it = d.work + 4LL * (item0 + blockIdx.x);
     const int f = it[0], r0 = it[1], ks = it[2], slot = it[3];
     const int mat = blockIdx.y;
     const int j0 = blockIdx.z * SG_C;
     const int jn = min(SG_C, J - j0);
     const int m = d.m[f], k = d.k[f];
+    const int64_t fo = d.idx_off[f];
+    const double* base = F + (int64_t)mat * d.storage + d.off[f];
+    double* FRm = FR + (int64_t)mat * nidx * J;
+    double* fr = FRm + fo * J;
+    const double* b = io->r + (int64_t)mat * N * J;
+    double* x = io->z + (int64_t)mat * N * J;
+    const int tid = threadIdx.x;
+    double init[4][2] = {{0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}};
+    if (!bwd && r0 < 0) {   // pivot rows of a front without contribution block
+        for (int e = tid; e < k * SG_C; e += SG_T) {
+            const int t = e / SG_C, j = e % SG_C;
+            if (j < jn) fr[(int64_t)t * J + j0 + j] = gather_row(d, FRm, b, fo + t, J, j0 + j, true);
+        }
+        return;
+    }
     const int rbase = bwd ? r0 : k + r0;
     const int nr = min(SG_R, (bwd ? k : m) - rbase);
     const int K = bwd ? m : k;
     const int kbeg = slot < 0 ? 0 : ks * split_k;
     const int kend = slot < 0 ? K : min(K, kbeg + split_k);
-    const int kc = kend - kbeg;               // <= SG_KMAX by construction of the schedule
-    const double* base = F + (int64_t)mat * d.storage + d.off[f];
-    const int64_t fo = d.idx_off[f];
-    double* fr = FR + (int64_t)mat * nidx * J + fo * J;
-    double* x = io->z + (int64_t)mat * N * J;
-    const int tid = threadIdx.x;
+    const int kc = kend - kbeg;               // <= kmax by construction of the schedule
     // stage A rows (consecutive lanes -> consecutive inner index: coalesced, conflict-free)
-    for (int e = tid; e < SG_R * SG_KMAX; e += SG_T) {
-        const int r = e / SG_KMAX, kk = e % SG_KMAX;
-        if (kk >= kc) continue;
+    for (int e = tid; e < SG_R * kc; e += SG_T) {
+        const int r = e / kc, kk = e % kc;
         const bool ok = r < nr;
-        cp_async8(&As[r * SG_LDA + kk], ok ? base + (int64_t)(rbase + r) * m + kbeg + kk : base, ok);
+        cp_async8(&As[r * lda + kk], ok ? base + (int64_t)(rbase + r) * m + kbeg + kk : base, ok);
     }
-    for (int e = tid; e < SG_KMAX * SG_C; e += SG_T) {
-        const int kk = e / SG_C, j = e % SG_C;
-        if (kk >= kc) continue;
-        const int t = kbeg + kk;
-        const bool ok = j < jn;
-        const double* src = fr;
-        if (ok) src = (t < k) ? fr + (int64_t)t * J + j0 + j : x + (int64_t)d.idx[fo + t] * J + j0 + j;
-        cp_async8(&Bs[kk * SG_C + j], src, ok);
+    if (bwd) {
+        const int j = tid & (SG_C - 1);
+        const bool jok = j < jn;
+        for (int kb4 = tid / SG_C; kb4 < kc; kb4 += 4 * (SG_T / SG_C)) {
+            int ix[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {   // descriptors first: 4 independent index loads in flight
+                const int t = kbeg + kb4 + u * (SG_T / SG_C);
+                ix[u] = (kb4 + u * (SG_T / SG_C) < kc && t >= k) ? d.idx[fo + t] : -1;
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int kk = kb4 + u * (SG_T / SG_C);
+                if (kk >= kc) continue;
+                const int t = kbeg + kk;
+                const double* src = fr;
+                if (jok) src = (t < k) ? fr + (int64_t)t * J + j0 + j : x + (int64_t)ix[u] * J + j0 + j;
+                cp_async8(&Bs[kk * SG_C + j], src, jok);
+            }
+        }
+        cp_async_commit();
+    } else {
+        cp_async_commit();
+        // contribution-block rows' children sums for the epilogue (non-split items):
+        // issued first so these loads overlap the pivot gather below
+        if (slot < 0) {
+            const int tx_ = tid & 15, ty_ = tid >> 4;
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                const int r = ty_ + 16 * i;
+                const int4 g = (r < nr) ? *reinterpret_cast<const int4*>(d.gsrc + 4 * (fo + rbase + r))
+                                        : make_int4(-1, -1, -1, -1);
+#pragma unroll
+                for (int jj = 0; jj < 2; ++jj) {
+                    const int j = j0 + tx_ + 16 * jj;
+                    const bool jok = tx_ + 16 * jj < jn;
+                    double v = 0.0;
+                    if (jok && g.x >= 0) v += FRm[(int64_t)g.x * J + j];
+                    if (jok && g.y >= 0) v += FRm[(int64_t)g.y * J + j];
+                    if (jok && g.z >= 0) v += FRm[(int64_t)g.z * J + j];
+                    if (jok && g.w >= 0) v += FRm[(int64_t)g.w * J + j];
+                    init[i][jj] = v;
+                }
+            }
+        }
+        const bool store_piv = (r0 == 0);     // one row tile per front persists fr[P] for the backward pass
+        // gather b + children rows; 4 rows per thread in flight (descriptors first, then values)
+        const int j = tid & (SG_C - 1);
+        const bool jok = j < jn;
+        for (int kb4 = tid / SG_C; kb4 < kc; kb4 += 4 * (SG_T / SG_C)) {
+            int4 g[4];
+            int ix[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int kk = kb4 + u * (SG_T / SG_C);
+                const int64_t row = fo + kbeg + kk;
+                const bool ok = kk < kc;
+                g[u] = ok ? *reinterpret_cast<const int4*>(d.gsrc + 4 * row) : make_int4(-1, -1, -1, -1);
+                ix[u] = ok ? d.idx[row] : -1;
+            }
+            double v[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                v[u] = (jok && ix[u] >= 0) ? b[(int64_t)ix[u] * J + j0 + j] : 0.0;
+                if (jok && g[u].x >= 0) v[u] += FRm[(int64_t)g[u].x * J + j0 + j];
+                if (jok && g[u].y >= 0) v[u] += FRm[(int64_t)g[u].y * J + j0 + j];
+                if (jok && g[u].z >= 0) v[u] += FRm[(int64_t)g[u].z * J + j0 + j];
+                if (jok && g[u].w >= 0) v[u] += FRm[(int64_t)g[u].w * J + j0 + j];
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int kk = kb4 + u * (SG_T / SG_C);
+                if (kk >= kc) continue;
+                Bs[kk * SG_C + j] = v[u];
+                if (store_piv && jok) fr[(int64_t)(kbeg + kk) * J + j0 + j] = v[u];
+            }
+        }
     }
-    cp_async_commit();
-    cp_async_wait<0>();
+    cp_async_wait_all();
     __syncthreads();
     const int tx = tid & 15, ty = tid >> 4;   // cols tx, tx+16 ; rows ty + 16 i
     double acc[4][2];
@@ -139,7 +205,7 @@ __global__ void __launch_bounds__(SG_T) k_sgemm(MfDev d, int item0, const double
     for (int kk = 0; kk < kc; ++kk) {
         double a[4];
 #pragma unroll
-        for (int i = 0; i < 4; ++i) a[i] = As[(ty + 16 * i) * SG_LDA + kk];
+        for (int i = 0; i < 4; ++i) a[i] = As[(ty + 16 * i) * lda + kk];
         const double b0 = Bs[kk * SG_C + tx], b1 = Bs[kk * SG_C + tx + 16];
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
@@ -147,6 +213,36 @@ __global__ void __launch_bounds__(SG_T) k_sgemm(MfDev d, int item0, const double
             acc[i][1] = fma(a[i], b1, acc[i][1]);
         }
     }
+    if (slot < 0) {
+        if (bwd) {
+            int ix[4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) ix[i] = (ty + 16 * i < nr) ? d.idx[fo + rbase + ty + 16 * i] : 0;
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                if (ty + 16 * i >= nr) continue;
+#pragma unroll
+                for (int jj = 0; jj < 2; ++jj) {
+                    const int j = tx + 16 * jj;
+                    if (j < jn) x[(int64_t)ix[i] * J + j0 + j] = -acc[i][jj];
+                }
+            }
+        } else {
+            // contribution-block rows: children's rows (gathered up front) minus the product
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                const int r = ty + 16 * i;
+                if (r >= nr) continue;
+#pragma unroll
+                for (int jj = 0; jj < 2; ++jj) {
+                    const int j = tx + 16 * jj;
+                    if (j < jn) FRm[(fo + rbase + r) * J + j0 + j] = init[i][jj] - acc[i][jj];
+                }
+            }
+        }
+        return;
+    }
+    // split: publish the partial, the last CTA of the group reduces in ks order
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
         const int r = ty + 16 * i;
@@ -154,40 +250,33 @@ __global__ void __launch_bounds__(SG_T) k_sgemm(MfDev d, int item0, const double
 #pragma unroll
         for (int jj = 0; jj < 2; ++jj) {
             const int j = tx + 16 * jj;
-            if (j >= jn) continue;
-            if (slot >= 0)
-                partial[(((int64_t)mat * nslot + slot) * SG_R + r) * J + j0 + j] = acc[i][jj];
-            else if (bwd)
-                x[(int64_t)d.idx[fo + rbase + r] * J + j0 + j] = -acc[i][jj];
-            else
-                fr[(int64_t)(rbase + r) * J + j0 + j] -= acc[i][jj];
+            if (j < jn) partial[(((int64_t)mat * nslot + slot) * SG_R + r) * J + j0 + j] = acc[i][jj];
         }
     }
+    __threadfence();
+    __syncthreads();
+    const int s0 = slot - ks;
+    const int ns = (K + split_k - 1) / split_k;
+    const int tk = (int)(((int64_t)mat * nslot + s0) * gridDim.z + blockIdx.z);
+    if (tid == 0) s_last = (atomicAdd(ticket + tk, 1) == ns - 1);
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence();
+    for (int e = tid; e < nr * jn; e += SG_T) {
+        const int r = e / jn, j = e % jn;
+        double sum = 0.0;
+        for (int q = 0; q < ns; ++q) sum += __ldcg(&partial[(((int64_t)mat * nslot + s0 + q) * SG_R + r) * J + j0 + j]);
+        if (bwd) {
+            x[(int64_t)d.idx[fo + rbase + r] * J + j0 + j] = -sum;
+        } else {
+            const int64_t row = fo + rbase + r;
+            FRm[row * J + j0 + j] = gather_row(d, FRm, b, row, J, j0 + j, false) - sum;
+        }
+    }
+    if (tid == 0) ticket[tk] = 0;   // ready for the next solve / graph replay
 }
 
-static const size_t SM_SG = sizeof(double) * (SG_R * SG_LDA + SG_KMAX * SG_C);
-// ordered sum of the split-K partials + the update; item = (f, r0, nsplit, slot0)
-__global__ void k_sred(MfDev d, int item0, double* __restrict__ FR, const SolveIO* __restrict__ io, int64_t N, int J,
-                       int64_t nidx, int bwd, const double* __restrict__ partial, int64_t nslot) {
-    const int* it = d.work + 4LL * (item0 + blockIdx.x);
-    const int f = it[0], r0 = it[1], ns = it[2], s0 = it[3];
-    const int mat = blockIdx.y;
-    const int m = d.m[f], k = d.k[f];
-    const int rbase = bwd ? r0 : k + r0;
-    const int nr = min(SG_R, (bwd ? k : m) - rbase);
-    const int64_t fo = d.idx_off[f];
-    double* fr = FR + (int64_t)mat * nidx * J + fo * J;
-    double* x = io->z + (int64_t)mat * N * J;
-    for (int t = threadIdx.x; t < nr * J; t += blockDim.x) {
-        const int r = t / J, j = t % J;
-        double s = 0.0;
-        for (int q = 0; q < ns; ++q) s += partial[(((int64_t)mat * nslot + s0 + q) * SG_R + r) * J + j];
-        if (bwd)
-            x[(int64_t)d.idx[fo + rbase + r] * J + j] = -s;
-        else
-            fr[(int64_t)(rbase + r) * J + j] -= s;
-    }
-}
+static size_t sg_smem(int kmax) { return sizeof(double) * ((size_t)SG_R * (kmax + 1) + (size_t)kmax * SG_C); }
 
 // record the launch sequence of one solve (io table fixed)
 static int mf_solve_launches(ens_ctx* c, cudaStream_t s, SolveIO* io, int64_t* nlaunch) {
@@ -208,26 +297,15 @@ static int mf_solve_launches(ens_ctx* c, cudaStream_t s, SolveIO* io, int64_t* n
         const int64_t nrow = (int64_t)sched->size() / 5;
         for (int64_t i = 0; i < nrow; ++i) {
             const int64_t* q = &(*sched)[5 * i];
-            const int op = (int)q[0], off = (int)q[2], n = (int)q[3];
+            const int op = (int)q[0], off = (int)q[2], n = (int)q[3], kmax = (int)q[4];
             if (n == 0) continue;
-            switch (op) {
-                case SOP_FINIT:
-                    k_finit<<<dim3(n, 2), 256, 0, s>>>(d, off, io, c->frvec, N, J, nidx);
-                    break;
-                case SOP_FGEMM:
-                case SOP_BGEMM:
-                    k_sgemm<<<dim3(n, 2, zc), SG_T, SM_SG, s>>>(d, off, c->fronts, c->frvec, io, N, J, nidx,
-                                                            op == SOP_BGEMM, sk, c->partial, nslot);
-                    break;
-                case SOP_FRED:
-                case SOP_BRED:
-                    k_sred<<<dim3(n, 2), 256, 0, s>>>(d, off, c->frvec, io, N, J, nidx, op == SOP_BRED, c->partial,
-                                                      nslot);
-                    break;
-                default:
-                    ens_set_error("bad solve op", __FILE__, __LINE__);
-                    return ENS_EINVAL;
+            if ((op != SOP_FGEMM && op != SOP_BGEMM) || kmax > SG_KMAX || kmax < 1) {
+                ens_set_error("bad solve schedule row", __FILE__, __LINE__);
+                return ENS_EINVAL;
             }
+            k_sgemm<<<dim3(n, 2, zc), SG_T, sg_smem(kmax), s>>>(d, off, c->fronts, c->frvec, io, N, J, nidx,
+                                                               op == SOP_BGEMM, sk, kmax, c->partial, c->ticket,
+                                                               nslot);
             ENS_CKL();
             ++cnt;
         }
@@ -243,20 +321,21 @@ static bool graphs_enabled() {
 
 int mf_solve(ens_ctx* c, cudaStream_t s, const double* r, double* z) {
     if (!c->solve_io) {
-        ENS_CK(cudaMalloc(&c->solve_io, sizeof(SolveIO)));
-        ENS_CK(cudaFuncSetAttribute(k_sgemm, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SM_SG));
         if (c->p.split_k > SG_KMAX) {
             ens_set_error("plan split_k exceeds the solve kernel's inner tile", __FILE__, __LINE__);
             return ENS_EINVAL;
         }
-    }
-    if (!c->partial && c->p.n_slot > 0) {
-        const size_t bytes = sizeof(double) * 2 * (size_t)c->p.n_slot * SG_R * c->J;
-        if (cudaMalloc(&c->partial, bytes) != cudaSuccess) {
+        ENS_CK(cudaMalloc(&c->solve_io, sizeof(SolveIO)));
+        ENS_CK(cudaFuncSetAttribute(k_sgemm, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sg_smem(SG_KMAX)));
+        const int64_t ns = c->p.n_slot > 0 ? c->p.n_slot : 1;
+        const size_t pbytes = sizeof(double) * 2 * (size_t)ns * SG_R * c->J;
+        const size_t tbytes = sizeof(int) * 2 * (size_t)ns * ((c->J + SG_C - 1) / SG_C);
+        if (cudaMalloc(&c->partial, pbytes) != cudaSuccess || cudaMalloc(&c->ticket, tbytes) != cudaSuccess) {
             ens_set_error("out of device memory for split-K partials", __FILE__, __LINE__);
             return ENS_ENOMEM;
         }
-        c->ws_bytes += bytes;
+        ENS_CK(cudaMemset(c->ticket, 0, tbytes));
+        c->ws_bytes += pbytes + tbytes;
     }
     SolveIO* io = (SolveIO*)c->solve_io;
     k_set_io<<<1, 1, 0, s>>>(io, r, z);

@@ -475,12 +475,22 @@ def build_schedule(plan: FactorPlan, pw=PW):
     fwd, bwd = [], []
     nslot = [0]
 
-    def gemm_items(fronts, rows_of, K_of):
-        g, red = [], []
+    # Forward items gather their own inputs (b at the pivots + children's
+    # contribution rows via gsrc), so there is no separate FINIT pass; a front
+    # without a contribution block gets one pivot-only item (r0 = -1).  Split
+    # items (slot >= 0) are reduced by the last-arriving CTA of their group.
+    # The launch's 5th field is the largest inner range of its items (sizes smem).
+    def gemm_items(fronts, rows_of, K_of, pivot_only):
+        g, kmax = [], 1
         for f in fronts:
             K = int(K_of(f))
             ns_ = max(1, -(-K // SPLIT_K))
-            for r0 in range(0, int(rows_of(f)), SOLVE_ROWS):
+            rws = int(rows_of(f))
+            if rws == 0 and pivot_only:
+                g.append((f, -1, 0, -1))
+                kmax = max(kmax, min(K, SPLIT_K))
+                continue
+            for r0 in range(0, rws, SOLVE_ROWS):
                 if ns_ == 1:
                     g.append((f, r0, 0, -1))
                 else:
@@ -488,29 +498,19 @@ def build_schedule(plan: FactorPlan, pw=PW):
                     nslot[0] += ns_
                     for ks in range(ns_):
                         g.append((f, r0, ks, s0 + ks))
-                    red.append((f, r0, ns_, s0))
-        return g, red
+            kmax = max(kmax, min(K, SPLIT_K))
+        return g, kmax
 
     for L in range(plan.nlevels):
         fronts = np.arange(plan.level_front_off[L], plan.level_front_off[L + 1])
-        rows = [(f, r0) for f in fronts for r0 in range(0, fm[f], VEC_ROWS)]
-        off, n = add(rows)
-        fwd.append((SOP_FINIT, L, off, n, 0))
-        g, red = gemm_items(fronts, lambda f: fm[f] - fk[f], lambda f: fk[f])
-        if g:
-            off, n = add(g)
-            fwd.append((SOP_FGEMM, L, off, n, 0))
-        if red:
-            off, n = add(red)
-            fwd.append((SOP_FRED, L, off, n, 0))
+        g, kmax = gemm_items(fronts, lambda f: fm[f] - fk[f], lambda f: fk[f], True)
+        off, n = add(g)
+        fwd.append((SOP_FGEMM, L, off, n, kmax))
     for L in reversed(range(plan.nlevels)):
         fronts = np.arange(plan.level_front_off[L], plan.level_front_off[L + 1])
-        g, red = gemm_items(fronts, lambda f: fk[f], lambda f: fm[f])
+        g, kmax = gemm_items(fronts, lambda f: fk[f], lambda f: fm[f], False)
         off, n = add(g)
-        bwd.append((SOP_BGEMM, L, off, n, 0))
-        if red:
-            off, n = add(red)
-            bwd.append((SOP_BRED, L, off, n, 0))
+        bwd.append((SOP_BGEMM, L, off, n, kmax))
     # gather sources: gsrc[row of front p] = absolute f_idx rows of child CB entries mapped there
     nidx = int(plan.f_idx_off[-1])
     gsrc = np.full((nidx, MAX_GSRC), -1, dtype=np.int64)

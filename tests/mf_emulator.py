@@ -67,55 +67,67 @@ def solve(plan, st, rhs):
     """Apply the factorisation to rhs (n_total_internal, J); returns x (free rows)."""
     work = plan.schedule["work"]
     gsrc = plan.schedule["gsrc"]
+    sk = plan.schedule["split_k"]
+    R = plan.schedule["solve_rows"]
     fm, fk, off, io_ = plan.f_m, plan.f_k, plan.f_off, plan.f_idx_off
     J = rhs.shape[1]
     fr = np.zeros((int(io_[-1]), J))
     x = np.zeros_like(rhs)
-    partial = {}
 
     def front(f):
         m = int(fm[f])
         return st[off[f]:off[f] + m * m].reshape(m, m)
 
-    for op, L, io, n, arg in plan.schedule["fwd"]:
+    def gathered(rows_abs, pivot_mask):
+        val = np.where(pivot_mask[:, None], rhs[plan.f_idx[rows_abs]], 0.0)
+        for s_ in range(S.MAX_GSRC):
+            src = gsrc[rows_abs, s_]
+            val = val + np.where((src >= 0)[:, None], fr[np.maximum(src, 0)], 0.0)
+        return val
+
+    for op, L, io, n, kmax in plan.schedule["fwd"]:
+        assert op == S.SOP_FGEMM
+        groups = {}
         for it in work[io:io + n]:
-            f, r0 = it[0], it[1]
-            base = io_[f]
-            if op == S.SOP_FINIT:
-                rows = np.arange(r0, min(r0 + S.VEC_ROWS, fm[f]))
-                val = np.where((rows < fk[f])[:, None], rhs[plan.f_idx[base + rows]], 0.0)
-                for s_ in range(S.MAX_GSRC):
-                    src = gsrc[base + rows, s_]
-                    val = val + np.where((src >= 0)[:, None], fr[np.maximum(src, 0)], 0.0)
-                fr[base + rows] = val
-            elif op in (S.SOP_FGEMM, S.SOP_FRED):
-                k = fk[f]
-                rows = np.arange(k + r0, min(k + r0 + S.SOLVE_ROWS, fm[f]))
-                if op == S.SOP_FGEMM:
-                    ks, slot = it[2], it[3]
-                    kr = slice(ks * plan.schedule["split_k"], min(k, (ks + 1) * plan.schedule["split_k"]))
-                    prod = front(f)[rows, kr] @ fr[base + kr.start:base + kr.stop]
-                    if slot < 0:
-                        fr[base + rows] -= prod
-                    else:
-                        partial[slot] = prod
-                else:
-                    fr[base + rows] -= sum(partial[it[3] + s_] for s_ in range(it[2]))
-    for op, L, io, n, arg in plan.schedule["bwd"]:
+            f, r0, ks, slot = it
+            base, k, m = io_[f], fk[f], fm[f]
+            kb = 0 if slot < 0 else ks * sk
+            ke = k if slot < 0 else min(k, kb + sk)
+            assert r0 < 0 or ke - kb <= kmax      # pivot-only items stream any length
+            piv = gathered(base + np.arange(kb, ke), np.ones(ke - kb, dtype=bool))
+            if r0 <= 0:
+                fr[base + kb:base + ke] = piv
+            if r0 < 0:
+                continue
+            rows = np.arange(k + r0, min(k + r0 + R, m))
+            prod = front(f)[rows, kb:ke] @ piv
+            if slot < 0:
+                fr[base + rows] = gathered(base + rows, np.zeros(len(rows), dtype=bool)) - prod
+            else:
+                groups.setdefault((f, r0), []).append((ks, prod))
+        for (f, r0), parts in groups.items():
+            base, k, m = io_[f], fk[f], fm[f]
+            rows = np.arange(k + r0, min(k + r0 + R, m))
+            tot = sum(p_ for _, p_ in sorted(parts, key=lambda t: t[0]))
+            fr[base + rows] = gathered(base + rows, np.zeros(len(rows), dtype=bool)) - tot
+    for op, L, io, n, kmax in plan.schedule["bwd"]:
+        assert op == S.SOP_BGEMM
+        groups = {}
         for it in work[io:io + n]:
-            f, r0 = it[0], it[1]
-            base = io_[f]
-            k, m = fk[f], fm[f]
-            rows = np.arange(r0, min(r0 + S.SOLVE_ROWS, k))
-            if op == S.SOP_BGEMM:
-                ks, slot = it[2], it[3]
-                bop = np.vstack([fr[base:base + k], x[plan.f_idx[base + k:base + m]]])
-                kr = slice(ks * plan.schedule["split_k"], min(m, (ks + 1) * plan.schedule["split_k"]))
-                prod = front(f)[rows, kr] @ bop[kr]
-                if slot < 0:
-                    x[plan.f_idx[base + rows]] = -prod
-                else:
-                    partial[slot] = prod
-            elif op == S.SOP_BRED:
-                x[plan.f_idx[base + rows]] = -sum(partial[it[3] + s_] for s_ in range(it[2]))
+            f, r0, ks, slot = it
+            base, k, m = io_[f], fk[f], fm[f]
+            rows = np.arange(r0, min(r0 + R, k))
+            bop = np.vstack([fr[base:base + k], x[plan.f_idx[base + k:base + m]]])
+            kb = 0 if slot < 0 else ks * sk
+            ke = m if slot < 0 else min(m, kb + sk)
+            assert ke - kb <= kmax
+            prod = front(f)[rows, kb:ke] @ bop[kb:ke]
+            if slot < 0:
+                x[plan.f_idx[base + rows]] = -prod
+            else:
+                groups.setdefault((f, r0), []).append((ks, prod))
+        for (f, r0), parts in groups.items():
+            base, k = io_[f], fk[f]
+            rows = np.arange(r0, min(r0 + R, k))
+            x[plan.f_idx[base + rows]] = -sum(p_ for _, p_ in sorted(parts, key=lambda t: t[0]))
     return x
