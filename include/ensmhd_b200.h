@@ -119,6 +119,27 @@ typedef struct {
     int64_t n_slot;             /* split-K partial slots (64 rows x J each)          */
 } ens_plan_desc;
 
+/* Row blocking of the saddle SpMM (optional, built once per mesh and J):
+ * rows are grouped in blocks of consecutive internal nodes / pressure rows; the
+ * unique neighbour rows of a block are staged once in shared memory and the
+ * CSR column indices are pre-remapped to local slots. */
+typedef struct {
+    int32_t bn, bp;             /* nodes per velocity block, pressure rows per pressure block */
+    int32_t nvb, nqb;           /* block counts */
+    int64_t smem_vel, smem_pres;/* dynamic shared memory (bytes) per CTA */
+    const int32_t* a_lcol;      /* nnz_s: local slot of each A_s column in its row's block */
+    const int32_t* bt_lcol;     /* B^T pairs: local pressure slot */
+    const int32_t* b_lcol;      /* B pairs: local node slot */
+    const int32_t* vb_off;      /* nvb+1 */
+    const int32_t* vb_nodes;    /* staged velocity node rows per velocity block */
+    const int32_t* pb_off;      /* nvb+1 */
+    const int32_t* pb_rows;     /* staged pressure rows (0-based) per velocity block */
+    const int32_t* qb_off;      /* nqb+1 */
+    const int32_t* qb_nodes;    /* staged velocity node rows per pressure block */
+    const int32_t* vb_row;      /* nvb+1: first node of each velocity block (variable-size blocks) */
+    const int32_t* qb_row;      /* nqb+1: first pressure row of each pressure block */
+} ens_spmm_blocks;
+
 /* Problem data: value_j = sum_k coef[k*J + j] * basis[k*rows + row] (+ dense). */
 typedef struct {
     int32_t K;                  /* number of basis vectors (0 allowed)   */
@@ -140,6 +161,8 @@ int  ens_workspace_bytes(const ens_ctx* ctx, int64_t* bytes);
 /* Panel inverses with in-panel partial pivoting (1) or diagonal pivots (0, default;
  * the symbolic ordering guarantees nonsingular leading blocks in exact arithmetic). */
 int  ens_set_pivoting(ens_ctx* ctx, int on);
+/* Install the SpMM row blocking (arrays are device pointers owned by the caller). */
+int  ens_set_spmm_blocks(ens_ctx* ctx, const ens_spmm_blocks* blocks);
 
 /* Member sums over the J local columns: sum_v[r] = sum_j Xv[r][j] (r < n_vel), same for w. */
 int  ens_member_sums(ens_ctx* ctx, void* stream, const double* x, double* sums);

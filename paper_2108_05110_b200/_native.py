@@ -47,12 +47,19 @@ class PlanDesc(C.Structure):
     ]
 
 
+class SpmmBlocks(C.Structure):
+    _fields_ = [("bn", I32), ("bp", I32), ("nvb", I32), ("nqb", I32), ("smem_vel", I64), ("smem_pres", I64),
+                ("a_lcol", P), ("bt_lcol", P), ("b_lcol", P), ("vb_off", P), ("vb_nodes", P), ("pb_off", P),
+                ("pb_rows", P), ("qb_off", P), ("qb_nodes", P), ("vb_row", P), ("qb_row", P)]
+
+
 class DataDesc(C.Structure):
     _fields_ = [("K", I32), ("pad", I32), ("rows", I64), ("basis", P), ("coef", P), ("dense", P)]
 
 
 SYMBOLS = [
-    "ens_abi_version", "ens_last_error", "ens_kernel_launches", "ens_create", "ens_set_pivoting", "ens_destroy", "ens_workspace_bytes",
+    "ens_abi_version", "ens_last_error", "ens_kernel_launches", "ens_create", "ens_set_pivoting",
+    "ens_set_spmm_blocks", "ens_destroy", "ens_workspace_bytes",
     "ens_member_sums", "ens_rhs", "ens_member_pass", "ens_apply_bc", "ens_assemble", "ens_factor",
     "ens_solve", "ens_spmm", "ens_precond_apply", "ens_epilogue", "ens_diagnostics",
 ]
@@ -77,6 +84,7 @@ def load(path: str = LIB_PATH):
     lib.ens_destroy.restype = None
     lib.ens_workspace_bytes.argtypes = [P, C.POINTER(I64)]
     lib.ens_set_pivoting.argtypes = [P, C.c_int]
+    lib.ens_set_spmm_blocks.argtypes = [P, C.POINTER(SpmmBlocks)]
     lib.ens_member_sums.argtypes = [P, P, P, P]
     lib.ens_rhs.argtypes = [P, P, P, P, F64, C.POINTER(DataDesc), P]
     lib.ens_member_pass.argtypes = [P, P, P, P, P, P]

@@ -123,6 +123,23 @@ void ens_destroy(ens_ctx* c) {
     delete c;
 }
 
+int ens_set_spmm_blocks(ens_ctx* c, const ens_spmm_blocks* b) {
+    if (!c) return ENS_EINVAL;
+    if (!b) {
+        c->use_blocked = 0;
+        return ENS_OK;
+    }
+    if (b->smem_vel > 200 * 1024 || b->smem_pres > 200 * 1024 || 2 * c->J > 256) {
+        ens_set_error("SpMM blocks need too much shared memory", __FILE__, __LINE__);
+        return ENS_EINVAL;
+    }
+    c->blk = *b;
+    const int rc = spmm_blocked_setup(c);
+    if (rc != ENS_OK) return rc;
+    c->use_blocked = 1;
+    return ENS_OK;
+}
+
 int ens_set_pivoting(ens_ctx* c, int on) {
     if (!c) return ENS_EINVAL;
     c->diag_pivot = on ? 1 : 0;

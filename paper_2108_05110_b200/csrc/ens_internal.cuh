@@ -67,6 +67,8 @@ struct ens_ctx {
     const double* g_factor_key = nullptr;
     int diag_pivot = 0;            // 1: in-panel partial pivoting in DIAG (k_diag), 0: k_diag_np
     int use_mma = 1;               // DMMA (fp64 tensor core) panel kernels
+    ens_spmm_blocks blk{};         // SpMM row blocking (shared-memory staged neighbour rows)
+    int use_blocked = 0;
     int g_factor_pivot = 0;
     int64_t g_factor_kernels = 0;
 };
@@ -81,6 +83,9 @@ int launch_assemble(ens_ctx* c, cudaStream_t s, const double* base, const double
                     double two_mu_dt, double* as_vals);
 int launch_spmm(ens_ctx* c, cudaStream_t s, const double* as_vals, const double* x, const double* b, double* y,
                 int mode);
+int launch_spmm_blocked(ens_ctx* c, cudaStream_t s, const double* as_vals, const double* x, const double* b,
+                        double* y, int mode);
+int spmm_blocked_setup(ens_ctx* c);
 int launch_epilogue(ens_ctx* c, cudaStream_t s, const double* x, double* p_out);
 int launch_diagnostics(ens_ctx* c, cudaStream_t s, const double* x, const double* means, double* out);
 int launch_copy_cons(ens_ctx* c, cudaStream_t s, const double* src, double* dst);

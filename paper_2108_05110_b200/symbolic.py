@@ -173,8 +173,13 @@ def analyse(disc, leaf=LEAF_NODES, pw=PW):
     node_perm = np.empty(ns, dtype=np.int64)
     tnode_of_node = np.empty(ns, dtype=np.int64)
     pos = 0
+    coords = vel.dof_coords
     for t in post:
         nd = tnodes[t]
+        if len(nd) > 1:   # spatial order inside a tree node (separators are lines): SpMM locality
+            c = coords[nd]
+            ax = int(np.argmax(c.max(0) - c.min(0)))
+            nd = nd[np.lexsort((c[:, 1 - ax], c[:, ax]))]
         node_perm[nd] = pos + np.arange(len(nd))
         tnode_of_node[nd] = t
         pos += len(nd)
@@ -195,7 +200,19 @@ def analyse(disc, leaf=LEAF_NODES, pw=PW):
     tnode_of_pres = post[best]
 
     # pressure internal order: by tree rank, then by the reference index
-    porder = np.lexsort((np.arange(npres), best))
+    # within a tree node, pressures are ordered along the node group's main axis
+    # (moved-up pressures from both sides of a separator interleave spatially)
+    pc = disc.pressure.dof_coords
+    key2 = np.zeros(npres)
+    grp_order = np.argsort(best, kind="stable")
+    bounds = np.searchsorted(best[grp_order], np.unique(best))
+    bounds = np.append(bounds, npres)
+    for a_, b_ in zip(bounds[:-1], bounds[1:]):
+        g = grp_order[a_:b_]
+        c = pc[g]
+        ax = int(np.argmax(c.max(0) - c.min(0))) if len(g) > 1 else 0
+        key2[g] = c[:, ax] * 4.0 + c[:, 1 - ax] * 1e-6
+    porder = np.lexsort((np.arange(npres), key2, best))
     pres_perm = np.empty(npres, dtype=np.int64)
     pres_perm[porder] = np.arange(npres)
 
