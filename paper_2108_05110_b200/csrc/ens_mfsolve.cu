@@ -55,6 +55,13 @@ __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wai
 #define SG_C 32     // member columns per CTA
 #define SG_KMAX 128 // max inner range per work item (>= symbolic.SPLIT_K)
 #define SG_T 256    // threads
+#define SG_LDB 36   // Bs row stride (= 4 mod 16)
+
+__device__ __forceinline__ void dmma8(double& d0, double& d1, double a, double b) {
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                 : "+d"(d0), "+d"(d1)
+                 : "d"(a), "d"(b));
+}
 
 // children's contribution rows mapped onto front row `row` (+ b at pivots)
 __device__ __forceinline__ double gather_row(const MfDev& d, const double* __restrict__ FRm,
@@ -81,9 +88,10 @@ __global__ void __launch_bounds__(SG_T) k_sgemm(MfDev d, int item0, const double
                                                 int64_t nslot) {
     extern __shared__ double sm[];
     __shared__ int s_last;
-    const int lda = kmax + 1;
-    double* As = sm;                          // [SG_R][lda]  (+1 pad: conflict-free)
-    double* Bs = sm + SG_R * lda;             // [kmax][SG_C]
+    // strides = 4 (mod 16) doubles: conflict-free m8n8k4 fragment reads
+    const int lda = ((kmax + 15) & ~15) + 4;
+    double* As = sm;                          // [SG_R][lda]
+    double* Bs = sm + SG_R * lda;             // [kpad][SG_LDB]
     const int* it = d.work + 4LL * (item0 + blockIdx.x);
     const int f = it[0], r0 = it[1], ks = it[2], slot = it[3];
     const int mat = blockIdx.y;
@@ -134,7 +142,7 @@ __global__ void __launch_bounds__(SG_T) k_sgemm(MfDev d, int item0, const double
                 const int t = kbeg + kk;
                 const double* src = fr;
                 if (jok) src = (t < k) ? fr + (int64_t)t * J + j0 + j : x + (int64_t)ix[u] * J + j0 + j;
-                cp_async8(&Bs[kk * SG_C + j], src, jok);
+                cp_async8(&Bs[kk * SG_LDB + j], src, jok);
             }
         }
         cp_async_commit();
@@ -190,28 +198,45 @@ __global__ void __launch_bounds__(SG_T) k_sgemm(MfDev d, int item0, const double
             for (int u = 0; u < 4; ++u) {
                 const int kk = kb4 + u * (SG_T / SG_C);
                 if (kk >= kc) continue;
-                Bs[kk * SG_C + j] = v[u];
+                Bs[kk * SG_LDB + j] = v[u];
                 if (store_piv && jok) fr[(int64_t)(kbeg + kk) * J + j0 + j] = v[u];
             }
         }
     }
+    // zero the K padding (kc -> multiple of 4) of both operands
+    const int kpad = (kc + 3) & ~3;
+    for (int e = tid; e < (kpad - kc) * SG_R; e += SG_T) As[(e % SG_R) * lda + kc + e / SG_R] = 0.0;
+    for (int e = tid; e < (kpad - kc) * SG_C; e += SG_T) Bs[(kc + e / SG_C) * SG_LDB + e % SG_C] = 0.0;
     cp_async_wait_all();
     __syncthreads();
-    const int tx = tid & 15, ty = tid >> 4;   // cols tx, tx+16 ; rows ty + 16 i
+    // fp64 tensor-core MMA (m8n8k4): warp w owns rows 8w..8w+7, all 8-column tiles
+    const int lane = tid & 31, warp = tid >> 5, g = lane >> 2, q = lane & 3;
+    const int nct = (jn + 7) >> 3;
+    double dacc[4][2] = {{0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}};
+    {
+        const double* ap = As + (8 * warp + g) * lda + q;
+        const double* bp = Bs + q * SG_LDB + g;
+        for (int k0 = 0; k0 < kpad; k0 += 4) {
+            const double av = ap[k0];
+#pragma unroll
+            for (int ct = 0; ct < 4; ++ct)
+                if (ct < nct) dmma8(dacc[ct][0], dacc[ct][1], av, bp[k0 * SG_LDB + 8 * ct]);
+        }
+    }
+    __syncthreads();   // operands consumed: reuse As as the 64 x 32 output tile
+    double* Cs = As;
+#pragma unroll
+    for (int ct = 0; ct < 4; ++ct) {
+        Cs[(8 * warp + g) * (SG_C + 1) + 8 * ct + 2 * q] = dacc[ct][0];
+        Cs[(8 * warp + g) * (SG_C + 1) + 8 * ct + 2 * q + 1] = dacc[ct][1];
+    }
+    __syncthreads();
+    const int tx = tid & 15, ty = tid >> 4;   // epilogue mapping: cols tx, tx+16 ; rows ty + 16 i
     double acc[4][2];
 #pragma unroll
-    for (int i = 0; i < 4; ++i) acc[i][0] = acc[i][1] = 0.0;
-#pragma unroll 4
-    for (int kk = 0; kk < kc; ++kk) {
-        double a[4];
-#pragma unroll
-        for (int i = 0; i < 4; ++i) a[i] = As[(ty + 16 * i) * lda + kk];
-        const double b0 = Bs[kk * SG_C + tx], b1 = Bs[kk * SG_C + tx + 16];
-#pragma unroll
-        for (int i = 0; i < 4; ++i) {
-            acc[i][0] = fma(a[i], b0, acc[i][0]);
-            acc[i][1] = fma(a[i], b1, acc[i][1]);
-        }
+    for (int i = 0; i < 4; ++i) {
+        acc[i][0] = Cs[(ty + 16 * i) * (SG_C + 1) + tx];
+        acc[i][1] = Cs[(ty + 16 * i) * (SG_C + 1) + tx + 16];
     }
     if (slot < 0) {
         if (bwd) {
@@ -276,7 +301,11 @@ __global__ void __launch_bounds__(SG_T) k_sgemm(MfDev d, int item0, const double
     if (tid == 0) ticket[tk] = 0;   // ready for the next solve / graph replay
 }
 
-static size_t sg_smem(int kmax) { return sizeof(double) * ((size_t)SG_R * (kmax + 1) + (size_t)kmax * SG_C); }
+static size_t sg_smem(int kmax) {
+    const size_t lda = ((kmax + 15) & ~15) + 4, kpad = (kmax + 3) & ~3;
+    const size_t ops = SG_R * lda + kpad * SG_LDB, out = SG_R * (SG_C + 1);   // output tile reuses the operands
+    return sizeof(double) * (ops > out ? ops : out);
+}
 
 // record the launch sequence of one solve (io table fixed)
 static int mf_solve_launches(ens_ctx* c, cudaStream_t s, SolveIO* io, int64_t* nlaunch) {
