@@ -106,9 +106,10 @@ __global__ void __launch_bounds__(SG_T) k_sgemm(MfDev d, int item0, const double
     double* x = io->z + (int64_t)mat * N * J;
     const int tid = threadIdx.x;
     double init[4][2] = {{0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}};
-    if (!bwd && r0 < 0) {   // pivot rows of a front without contribution block
-        for (int e = tid; e < k * SG_C; e += SG_T) {
-            const int t = e / SG_C, j = e % SG_C;
+    if (!bwd && r0 < 0) {   // pivot rows [t0, t0+64) of a front without contribution block
+        const int t0 = -1 - r0, t1 = min(k, t0 + SG_R);
+        for (int e = tid; e < (t1 - t0) * SG_C; e += SG_T) {
+            const int t = t0 + e / SG_C, j = e % SG_C;
             if (j < jn) fr[(int64_t)t * J + j0 + j] = gather_row(d, FRm, b, fo + t, J, j0 + j, true);
         }
         return;

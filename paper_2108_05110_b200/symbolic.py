@@ -504,8 +504,9 @@ def build_schedule(plan: FactorPlan, pw=PW):
             ns_ = max(1, -(-K // SPLIT_K))
             rws = int(rows_of(f))
             if rws == 0 and pivot_only:
-                g.append((f, -1, 0, -1))
-                kmax = max(kmax, min(K, SPLIT_K))
+                # pivot rows only, in chunks of SOLVE_ROWS (r0 = -1 - first pivot row)
+                for t0 in range(0, K, SOLVE_ROWS):
+                    g.append((f, -1 - t0, 0, -1))
                 continue
             for r0 in range(0, rws, SOLVE_ROWS):
                 if ns_ == 1:

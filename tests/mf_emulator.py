@@ -91,14 +91,17 @@ def solve(plan, st, rhs):
         for it in work[io:io + n]:
             f, r0, ks, slot = it
             base, k, m = io_[f], fk[f], fm[f]
+            if r0 < 0:                            # pivot-only chunk [t0, t0 + R)
+                t0 = -1 - r0
+                t1 = min(k, t0 + R)
+                fr[base + t0:base + t1] = gathered(base + np.arange(t0, t1), np.ones(t1 - t0, dtype=bool))
+                continue
             kb = 0 if slot < 0 else ks * sk
             ke = k if slot < 0 else min(k, kb + sk)
-            assert r0 < 0 or ke - kb <= kmax      # pivot-only items stream any length
+            assert ke - kb <= kmax
             piv = gathered(base + np.arange(kb, ke), np.ones(ke - kb, dtype=bool))
-            if r0 <= 0:
+            if r0 == 0:
                 fr[base + kb:base + ke] = piv
-            if r0 < 0:
-                continue
             rows = np.arange(k + r0, min(k + r0 + R, m))
             prod = front(f)[rows, kb:ke] @ piv
             if slot < 0:
