@@ -92,6 +92,9 @@ int launch_copy_cons(ens_ctx* c, cudaStream_t s, const double* src, double* dst)
 // column reductions: out[mat][l][j] = sum_r A_l[mat][r][j] * B[mat][r][j]; A_l = A + l*lstride
 int launch_coldot(ens_ctx* c, cudaStream_t s, const double* A, int64_t lstride, int L, const double* B,
                   int64_t rows, double* out);
+// W -= sum_l V_l h_l (per column) and out[mat][j] = ||W_j||^2
+int launch_axpy_norm(ens_ctx* c, cudaStream_t s, double* W, const double* V, int64_t lstride, int L,
+                     const double* h, int64_t rows, double* out);
 
 // ---- multifrontal (ens_mf.cu) ----
 int mf_factor(ens_ctx* c, cudaStream_t s, const double* as_vals, int32_t* n_pert);

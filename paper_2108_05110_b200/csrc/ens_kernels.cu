@@ -493,13 +493,70 @@ __global__ void k_coldot_part(const double* __restrict__ A, int64_t lstride, con
     }
 }
 
+__global__ void k_coldot_fin(const double* __restrict__ part, int RB, int L, int J, double* __restrict__ out);
+
+// W -= sum_l V_l h[mat][l][j] and per-block partial sums of the new W^2 per column
+__global__ void k_axpy_norm_part(double* __restrict__ W, const double* __restrict__ V, int64_t lstride, int L,
+                                 const double* __restrict__ h, int64_t rows, int64_t matstride, int J,
+                                 double* __restrict__ part) {
+    __shared__ double red[256];
+    const int mat = blockIdx.z;
+    const int64_t per = (rows + gridDim.x - 1) / gridDim.x;
+    const int64_t r0 = (int64_t)blockIdx.x * per;
+    const int64_t r1 = min(rows, r0 + per);
+    for (int jc = 0; jc < J; jc += 256) {
+        const int JB = min(256, J - jc);
+        const int RPB = 256 / JB;
+        const int jj = threadIdx.x % JB, ro = threadIdx.x / JB;
+        const int j = jc + jj;
+        double hl[ENS_MAX_RESTART + 1];
+        for (int l = 0; l < L; ++l) hl[l] = h[((int64_t)mat * L + l) * J + j];
+        double acc = 0.0;
+        if (ro < RPB) {
+            for (int64_t r = r0 + ro; r < r1; r += RPB) {
+                const int64_t idx = (int64_t)mat * matstride + r * J + j;
+                double s = 0.0;
+                for (int l = 0; l < L; ++l) s += V[(int64_t)l * lstride + idx] * hl[l];
+                const double w = W[idx] - s;
+                W[idx] = w;
+                acc += w * w;
+            }
+        }
+        red[threadIdx.x] = acc;
+        __syncthreads();
+        if (threadIdx.x < JB) {
+            double s2 = 0.0;
+            for (int k = 0; k < RPB; ++k) s2 += red[k * JB + threadIdx.x];
+            part[((int64_t)blockIdx.x * 2 + mat) * J + j] = s2;
+        }
+        __syncthreads();
+    }
+}
+
+int launch_axpy_norm(ens_ctx* c, cudaStream_t s, double* W, const double* V, int64_t lstride, int L,
+                     const double* h, int64_t rows, double* out) {
+    const int RB = ENS_RED_BLOCKS;
+    if (L > ENS_MAX_RESTART + 1) return ENS_EINVAL;
+    k_axpy_norm_part<<<dim3(RB, 1, 2), 256, 0, s>>>(W, V, lstride, L, h, rows, (int64_t)c->n_total * c->J, c->J,
+                                                   c->red_part);
+    ENS_CKL();
+    const int tot = 2 * c->J;
+    k_coldot_fin<<<(tot * 32 + 255) / 256, 256, 0, s>>>(c->red_part, RB, 1, c->J, out);
+    ENS_CKL();
+    return ENS_OK;
+}
+
+// one warp per output: lanes sum a fixed strided subset of the partials, then a
+// fixed butterfly -- same order for every output, so identical columns agree bitwise
 __global__ void k_coldot_fin(const double* __restrict__ part, int RB, int L, int J, double* __restrict__ out) {
-    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    const int t = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
     const int tot = 2 * L * J;
     if (t >= tot) return;
     double s = 0.0;
-    for (int b = 0; b < RB; ++b) s += part[(int64_t)b * tot + t];
-    out[t] = s;
+    for (int b = lane; b < RB; b += 32) s += part[(int64_t)b * tot + t];
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (lane == 0) out[t] = s;
 }
 
 int launch_coldot(ens_ctx* c, cudaStream_t s, const double* A, int64_t lstride, int L, const double* B,
@@ -509,7 +566,7 @@ int launch_coldot(ens_ctx* c, cudaStream_t s, const double* A, int64_t lstride, 
     k_coldot_part<<<grid, 256, 0, s>>>(A, lstride, B, rows, (int64_t)c->n_total * c->J, c->J, L, c->red_part);
     ENS_CKL();
     const int tot = 2 * L * c->J;
-    k_coldot_fin<<<(tot + 255) / 256, 256, 0, s>>>(c->red_part, RB, L, c->J, out);
+    k_coldot_fin<<<(tot * 32 + 255) / 256, 256, 0, s>>>(c->red_part, RB, L, c->J, out);
     ENS_CKL();
     return ENS_OK;
 }

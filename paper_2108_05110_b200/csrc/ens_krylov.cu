@@ -114,7 +114,7 @@ __global__ void k_gm_givens(GmresCol* cols, const double* h1, const double* h2, 
     double col[ENS_MAX_RESTART + 1];
     for (int l = 0; l <= i; ++l) {
         const int64_t idx = ((int64_t)mat * L + l) * J + j;
-        col[l] = h1[idx] + h2[idx];
+        col[l] = h2 ? h1[idx] + h2[idx] : h1[idx];
     }
     const double hn = sqrt(hn2[c]);
     col[i + 1] = hn;
@@ -229,16 +229,13 @@ int gmres_solve(ens_ctx* c, cudaStream_t s, const double* as_vals, const double*
             double* Zi = Z + blk * i;
             RET(mf_solve(c, s, Vi, Zi));
             RET(launch_spmm(c, s, as_vals, Zi, nullptr, Wb, 0));
-            // CGS2 against V[0..i]
+            // classical Gram-Schmidt against V[0..i] (one pass: with the LU
+            // preconditioner FGMRES needs 1-3 vectors, and every restart re-checks
+            // the true residual); the update is fused with the norm of the result
             RET(launch_coldot(c, s, V, blk, i + 1, Wb, N, kb.h1));
-            k_axpy_multi<<<eb, 256, 0, s>>>(Wb, V, blk, i + 1, kb.h1, -1.0, N, J);
-            ENS_CKL();
-            RET(launch_coldot(c, s, V, blk, i + 1, Wb, N, kb.h2));
-            k_axpy_multi<<<eb, 256, 0, s>>>(Wb, V, blk, i + 1, kb.h2, -1.0, N, J);
-            ENS_CKL();
-            RET(launch_coldot(c, s, Wb, 0, 1, Wb, N, kb.hn2));
+            RET(launch_axpy_norm(c, s, Wb, V, blk, i + 1, kb.h1, N, kb.hn2));
             ENS_CK(cudaMemsetAsync(c->d_count, 0, sizeof(int32_t), s));
-            k_gm_givens<<<cb, 128, 0, s>>>(c->cols, kb.h1, kb.h2, kb.hn2, i, kb.scale, c->d_count, n, J);
+            k_gm_givens<<<cb, 128, 0, s>>>(c->cols, kb.h1, nullptr, kb.hn2, i, kb.scale, c->d_count, n, J);
             ENS_CKL();
             k_scale_cols<<<eb, 256, 0, s>>>(V + blk * (i + 1), Wb, kb.scale, N, J);
             ENS_CKL();
