@@ -39,6 +39,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
     cmd = [NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
            "-Xcompiler", "-fPIC", "-shared", "-I" + os.path.join(ROOT, "include"),
            "-o", LIB + ".tmp"] + sources() + ["-lcudart"]
+    extra = os.environ.get("ENS_NVCC_EXTRA", "").split()   # diagnostic builds only (e.g. -DSG_PROBE)
+    cmd[1:1] = extra
     if verbose:
         cmd.insert(1, "-Xptxas=-v")
     r = subprocess.run(cmd, capture_output=True, text=True)

@@ -120,6 +120,7 @@ void ens_destroy(ens_ctx* c) {
     cudaFree(c->solve_io);
     cudaFree(c->partial);
     cudaFree(c->ticket);
+    cudaFree(c->sitem);
     delete c;
 }
 

@@ -61,6 +61,7 @@ struct ens_ctx {
     void* solve_io = nullptr;      // device {r, z} pointer table of the solve graph
     double* partial = nullptr;     // split-K partial products of the solve GEMMs
     int* ticket = nullptr;         // split-K arrival counters (last CTA reduces)
+    int4* sitem = nullptr;         // solve work items with their front's geometry (3 x int4 per item)
     void* g_solve = nullptr;       // cudaGraphExec_t
     int64_t g_solve_kernels = 0;
     void* g_factor = nullptr;      // cudaGraphExec_t

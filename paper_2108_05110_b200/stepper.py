@@ -103,7 +103,7 @@ class Problem:
 # ----------------------------------------------------------------------
 
 _SOLVER_OPTS = dict(rtol=DEFAULT_RTOL, restart=8, max_restarts=20, refactor="adaptive", lag_max_iters=3,
-                    lag_max_steps=50)
+                    lag_max_steps=50, guess="extrapolate")
 
 
 def set_solver_options(**kw):
@@ -113,7 +113,8 @@ def set_solver_options(**kw):
     restart / max_restarts: FGMRES cycle length and count;
     refactor: "always" (rebuild the LU preconditioner each step, as the
     reference refactorises each sub-step) or "adaptive" (reuse it while FGMRES
-    needs <= lag_max_iters iterations, at most lag_max_steps steps).
+    needs <= lag_max_iters iterations, at most lag_max_steps steps);
+    guess: FGMRES initial iterate, "extrapolate" (2 x^n - x^{n-1}) or "previous" (x^n).
     """
     unknown = set(kw) - set(_SOLVER_OPTS)
     if unknown:
