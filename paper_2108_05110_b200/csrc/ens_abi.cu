@@ -121,6 +121,7 @@ void ens_destroy(ens_ctx* c) {
     cudaFree(c->partial);
     cudaFree(c->ticket);
     cudaFree(c->sitem);
+    cudaFree(c->finit_rows);
     delete c;
 }
 

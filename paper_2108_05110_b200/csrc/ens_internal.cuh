@@ -62,6 +62,9 @@ struct ens_ctx {
     double* partial = nullptr;     // split-K partial products of the solve GEMMs
     int* ticket = nullptr;         // split-K arrival counters (last CTA reduces)
     int4* sitem = nullptr;         // solve work items with their front's geometry (3 x int4 per item)
+    int32_t* finit_rows = nullptr; // per level: front rows k_finit assembles (bit 31: pivot row)
+    std::vector<int64_t> finit_off;   // level offsets into finit_rows
+    std::vector<int64_t> idx_off_h;   // host copy of the plan's f_idx_off
     void* g_solve = nullptr;       // cudaGraphExec_t
     int64_t g_solve_kernels = 0;
     void* g_factor = nullptr;      // cudaGraphExec_t

@@ -56,7 +56,10 @@ __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wai
 
 #define SG_R 64     // rows per CTA (= symbolic.SOLVE_ROWS)
 #define SG_C 32     // member columns per CTA
-#define SG_KMAX 64 // max inner range per work item (>= symbolic.SPLIT_K); A fragments live in registers
+#define SG_KMAX 512 // max inner range per work item (>= symbolic.SPLIT_K)
+#define SG_KC 32    // inner chunk of the pipelined mainloop
+#define SG_LDA 36   // A stage row stride (= 4 mod 16: conflict-free fragment reads)
+#define SG_STAGE (SG_R * SG_LDA + SG_KC * 36)   // doubles per pipeline stage (A + B)
 #define SG_T 256    // threads
 #define SG_LDB 36   // Bs row stride (= 4 mod 16)
 
@@ -92,7 +95,7 @@ extern "C" int ens_probe_dump(const char* path) {   // diagnostic build only
 #endif
 
 __device__ __forceinline__ void dmma8(double& d0, double& d1, double a, double b) {
-    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+    asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
                  : "+d"(d0), "+d"(d1)
                  : "d"(a), "d"(b));
 }
@@ -107,187 +110,208 @@ __device__ __forceinline__ double gsel(const double* __restrict__ p, int r, int 
 
 // Solve work item with its front's geometry, one 48-byte record so a CTA learns
 // everything it addresses with a single dependent load:
-//   [0] = {f, r0, ks, slot}   [1] = {m, k, -, -}   [2] = {off lo/hi, idx_off lo/hi}
-__global__ void k_build_sitem(MfDev d, int64_t nwork, int nfront, int4* __restrict__ out) {
+//   [0] = {f, r0, ks, slot}   [1] = {m, k, has_children, -}   [2] = {off lo/hi, idx_off lo/hi}
+__global__ void k_build_sitem(MfDev d, int64_t nwork, int nfront, const uint8_t* __restrict__ hasch,
+                              int4* __restrict__ out) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= nwork) return;
     const int4 w = reinterpret_cast<const int4*>(d.work)[i];
     const int f = (w.x >= 0 && w.x < nfront) ? w.x : 0;
     const int64_t off = d.off[f], io = d.idx_off[f];
     out[3 * i] = w;
-    out[3 * i + 1] = make_int4(d.m[f], d.k[f], 0, 0);
+    out[3 * i + 1] = make_int4(d.m[f], d.k[f], (int)hasch[f], 0);
     out[3 * i + 2] = make_int4((int)(off & 0xffffffff), (int)(off >> 32), (int)(io & 0xffffffff), (int)(io >> 32));
 }
 
+// Forward assembly of one tree level, before its GEMM launch: every front row
+// gets the children's contribution rows mapped onto it (+ b at pivot rows):
+//     fr[P] = b[P] + children rows,   fr[C] = children rows
+// `rows` lists the level's rows that need it (pivot rows: value | (1 << 31));
+// contribution rows of leaf fronts are not listed -- they start from zero in the
+// GEMM epilogue.  Grid-stride over (row, column pair) so the launch stays small.
+__global__ void __launch_bounds__(256) k_finit(const int32_t* __restrict__ rows, int64_t nrows,
+                                               const int32_t* __restrict__ idx, const int32_t* __restrict__ gsrc,
+                                               double* __restrict__ FR, const SolveIO* __restrict__ io, int64_t N,
+                                               int J, int64_t nidx) {
+    const int mat = blockIdx.y;
+    const double* b = io->r + (int64_t)mat * N * J;
+    double* FRm = FR + (int64_t)mat * nidx * J;
+    if ((J & 1) == 0) {
+        const int H = J >> 1;
+        const double2* b2 = reinterpret_cast<const double2*>(b);
+        double2* F2 = reinterpret_cast<double2*>(FRm);
+        for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < nrows * H;
+             t += (int64_t)gridDim.x * blockDim.x) {
+            const int e = rows[t / H];
+            const int i = (int)(t % H);
+            const int64_t row = e & 0x7fffffff;
+            const int4 g = *reinterpret_cast<const int4*>(gsrc + 4 * row);
+            const double2 bv = b2[(int64_t)max(idx[row], 0) * H + i];
+            double2 v = make_double2(0.0, 0.0);
+            const int src[4] = {g.x, g.y, g.z, g.w};
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const double2 c = F2[(int64_t)max(src[u], 0) * H + i];
+                if (src[u] >= 0) {
+                    v.x += c.x;
+                    v.y += c.y;
+                }
+            }
+            F2[row * H + i] = e < 0 ? make_double2(bv.x + v.x, bv.y + v.y) : v;
+        }
+    } else {
+        for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < nrows * J;
+             t += (int64_t)gridDim.x * blockDim.x) {
+            const int e = rows[t / J];
+            const int j = (int)(t % J);
+            const int64_t row = e & 0x7fffffff;
+            const int4 g = *reinterpret_cast<const int4*>(gsrc + 4 * row);
+            const double bv = b[(int64_t)max(idx[row], 0) * J + j];
+            const double* p = FRm + j;
+            const double v = gsel(p, g.x, J) + gsel(p, g.y, J) + gsel(p, g.z, J) + gsel(p, g.w, J);
+            FRm[row * J + j] = e < 0 ? bv + v : v;
+        }
+    }
+}
+
+__device__ __forceinline__ void cp_async_wait_n(int n) {
+    if (n <= 0) asm volatile("cp.async.wait_group 0;\n" ::);
+    else if (n == 1) asm volatile("cp.async.wait_group 1;\n" ::);
+    else asm volatile("cp.async.wait_group 2;\n" ::);
+}
+
 // item = (f, r0, ks, slot)
-//   r0 < 0  : forward pivot-only item, pivot rows [t0, t0+64), t0 = -1 - r0
-//             (front without contribution block)
+//   r0 < 0  : forward pivot-only item (front without contribution block): its
+//             rows were assembled by k_finit, nothing left to do
 //   slot<0  : whole inner range, result applied here
 //   slot>=0 : inner range [ks*split_k, ...) of group s0 = slot - ks; the last
 //             CTA of the group reduces partial[s0 .. s0+ns) in order
 //
-// Latency plan (every step is one dependent memory round trip, ~1 us under load):
-//   1. item record
-//   2. all A fragments of the inner range -> registers; descriptors (idx, gsrc)
-//      of the inner range -> shared memory; epilogue descriptors -> registers
-//   3. operand values (b / children rows / iterate) -> shared memory; epilogue
-//      children rows -> registers
-//   4. MMA, then direct stores -- or partial store + fence + ticket + reads of the
-//      group's partials (three more trips, split items only)
+// Mainloop: the inner range runs in SG_KC-wide chunks through an nstage-deep
+// cp.async pipeline (A = 64 front rows, B = 32 operand rows x 32 member
+// columns per stage), so loads of chunk c+nstage-1 are in flight while chunk c
+// runs on the fp64 tensor cores (mma.sync m8n8k4, warp w owns rows 8w..8w+7).
+//   forward : B = fr[P] rows (assembled by k_finit), C rows fr[C] -= A B
+//   backward: B = [fr[P]; x[C]] rows,                x[P] = -A B
+template <int NCT>
 __global__ void __launch_bounds__(SG_T, 3) k_sgemm(MfDev d, const int4* __restrict__ sitem, int item0,
                                                 const double* __restrict__ F, double* __restrict__ FR,
                                                 const SolveIO* __restrict__ io, int64_t N, int J, int64_t nidx,
-                                                int bwd, int split_k, int kmax, double* __restrict__ partial,
-                                                int* __restrict__ ticket, int64_t nslot) {
+                                                int bwd, int split_k, int nstage, double* __restrict__ partial,
+                                                int* __restrict__ ticket, int64_t nslot, int zbase) {
     SG_T_(0);
     extern __shared__ double sm[];
     __shared__ int s_last;
-    __shared__ int4 s_gsrc[SG_KMAX];
     __shared__ int s_idx[SG_KMAX];
-    double* Bs = sm;                          // [kpad][SG_LDB]: stride 4 (mod 16) doubles, conflict-free fragments
     const int4* rec = sitem + 3LL * (item0 + blockIdx.x);
     const int4 w0 = rec[0], w1 = rec[1], w2 = rec[2];
     const int r0 = w0.y, ks = w0.z, slot = w0.w;
-    const int m = w1.x, k = w1.y;
+    if (r0 < 0) return;
+    const int m = w1.x, k = w1.y, hasch = w1.z;
     const int64_t off = (int64_t)(unsigned)w2.x | ((int64_t)w2.y << 32);
     const int64_t fo = (int64_t)(unsigned)w2.z | ((int64_t)w2.w << 32);
     const int mat = blockIdx.y;
-    const int j0 = blockIdx.z * SG_C;
+    const int zb = zbase + blockIdx.z;
+    const int j0 = zb * SG_C;
     const int jn = min(SG_C, J - j0);
     const double* base = F + (int64_t)mat * d.storage + off;
     double* FRm = FR + (int64_t)mat * nidx * J;
     double* fr = FRm + fo * J;
-    const double* b = io->r + (int64_t)mat * N * J;
     double* x = io->z + (int64_t)mat * N * J;
-    const int tid = threadIdx.x;
-    const int jt = tid & (SG_C - 1), jok = jt < jn, warp = tid >> 5;
-    if (!bwd && r0 < 0) {
-        // pivot rows of a front without contribution block: fr[P] = b[P] + children rows
-        const int t0 = -1 - r0, nt = min(k - t0, SG_R);
-        int4 gq[SG_R / 8];
-        int ix[SG_R / 8];
-#pragma unroll
-        for (int u = 0; u < SG_R / 8; ++u) {
-            const int t = min((tid >> 5) + 8 * u, nt - 1);   // clamped: unconditional loads
-            gq[u] = *reinterpret_cast<const int4*>(d.gsrc + 4 * (fo + t0 + t));
-            ix[u] = d.idx[fo + t0 + t];
-        }
-        // all loads first, then the stores (fr may alias FRm: interleaving them would serialise the loads)
-        double v[SG_R / 8];
-#pragma unroll
-        for (int u = 0; u < SG_R / 8; ++u) {
-            const double* pb = FRm + j0 + (jok ? jt : 0);
-            const double bv = b[(int64_t)max(ix[u], 0) * J + j0 + (jok ? jt : 0)];
-            v[u] = bv + gsel(pb, gq[u].x, J) + gsel(pb, gq[u].y, J) + gsel(pb, gq[u].z, J) + gsel(pb, gq[u].w, J);
-        }
-#pragma unroll
-        for (int u = 0; u < SG_R / 8; ++u) {
-            const int t = (tid >> 5) + 8 * u;
-            if (t < nt && jok) fr[(int64_t)(t0 + t) * J + j0 + jt] = v[u];
-        }
-        return;
-    }
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, g = lane >> 2, q = lane & 3;
     const int rbase = bwd ? r0 : k + r0;
     const int nr = min(SG_R, (bwd ? k : m) - rbase);
     const int K = bwd ? m : k;
     const int kbeg = slot < 0 ? 0 : ks * split_k;
     const int kend = slot < 0 ? K : min(K, kbeg + split_k);
-    const int kc = kend - kbeg;               // <= kmax <= SG_KMAX by construction of the schedule
-    const int kpad = (kc + 3) & ~3;
-    // (2) descriptors of the inner range -> shared memory
-    for (int t = tid; t < kc; t += SG_T) {
-        const int64_t r = fo + kbeg + t;
-        if (bwd) {
-            s_idx[t] = (kbeg + t >= k) ? d.idx[r] : -1;
-        } else {
-            s_idx[t] = d.idx[r];
-            s_gsrc[t] = *reinterpret_cast<const int4*>(d.gsrc + 4 * r);
-        }
-    }
-    // fp64 tensor-core MMA (m8n8k4): warp w owns rows 8w..8w+7 and every 8-column tile.
-    // A fragments (lane = row g, inner q) go straight from the front into registers:
-    // 8 rows x 32 contiguous bytes per warp load, the whole inner range in flight.
-    const int lane = tid & 31, g = lane >> 2, q = lane & 3;
+    const int kc = kend - kbeg;               // <= split_k <= SG_KMAX by construction of the schedule
+    const int nch = (kc + SG_KC - 1) / SG_KC;
     const int row = 8 * warp + g;
     const bool row_ok = row < nr;
-    const double* arow = base + (int64_t)(rbase + (row_ok ? row : 0)) * m + kbeg + q;
-    double a[SG_KMAX / 4];
-    if (bwd) {
+    auto issue_a = [&](int c) {
+#ifdef SG_NOA
+        return;
+#endif
+        double* As = sm + (c % nstage) * SG_STAGE;
 #pragma unroll
-        for (int u = 0; u < SG_KMAX / 4; ++u) a[u] = (row_ok && 4 * u + q < kc) ? __ldg(arow + 4 * u) : 0.0;
-    }
-    // epilogue descriptors (accumulator layout: row `row`, columns 8ct + 2q + {0,1})
-    const int xrow = (bwd && row_ok) ? d.idx[fo + rbase + row] : 0;
-    const int4 eg = (!bwd && row_ok) ? *reinterpret_cast<const int4*>(d.gsrc + 4 * (fo + rbase + row))
-                                     : make_int4(-1, -1, -1, -1);
-    __syncthreads();
-    SG_T_(1);
-    // (3) operand values -> shared memory
-    if (bwd) {
-        // B = [fr[P]; x[C]] rows of the inner range
-        for (int kk = tid >> 5; kk < kc; kk += SG_T / SG_C) {
-            const int t = kbeg + kk;
-            const double* src = (t < k) ? fr + (int64_t)t * J + j0 + jt : x + (int64_t)s_idx[kk] * J + j0 + jt;
-            cp_async8(&Bs[kk * SG_LDB + jt], jok ? src : fr, jok);
+        for (int i = 0; i < SG_R * SG_KC / SG_T; ++i) {
+            const int e = tid + SG_T * i, r = e / SG_KC, kk = e % SG_KC, kg = c * SG_KC + kk;
+            const bool ok = r < nr && kg < kc;
+            cp_async8(&As[r * SG_LDA + kk], ok ? base + (int64_t)(rbase + r) * m + kbeg + kg : base, ok);
         }
-        cp_async_commit();
-    }
-    // contribution-block rows' children sums for the forward epilogue
+    };
+    auto issue_b = [&](int c) {
+#ifdef SG_NOB
+        return;
+#endif
+        double* Bsb = sm + (c % nstage) * SG_STAGE + SG_R * SG_LDA;
+#pragma unroll
+        for (int i = 0; i < SG_KC * SG_C / SG_T; ++i) {
+            const int e = tid + SG_T * i, kk = e / SG_C, j = e % SG_C, kg = c * SG_KC + kk;
+            const bool ok = j < jn && kg < kc;
+            const int kq = min(kg, kc - 1), t = kbeg + kq;
+            const double* src = (!bwd || t < k) ? fr + (int64_t)t * J + j0 + j : x + (int64_t)s_idx[kq] * J + j0 + j;
+            cp_async8(&Bsb[kk * SG_LDB + j], ok ? src : base, ok);
+        }
+    };
+    // (1) first A chunk, epilogue operands, backward gather descriptors
+    issue_a(0);
+    const int xrow = (bwd && row_ok) ? d.idx[fo + rbase + row] : 0;
     double init[4][2] = {{0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}};
-    if (!bwd && row_ok) {
+    if (!bwd && hasch && row_ok) {
+        const double* pr = FRm + (fo + rbase + row) * J + j0;
 #pragma unroll
         for (int ct = 0; ct < 4; ++ct)
 #pragma unroll
             for (int e = 0; e < 2; ++e) {
-                const int col = 8 * ct + 2 * q + e;
-                if (col >= jn) continue;
-                const double* pe = FRm + j0 + col;
-                init[ct][e] = gsel(pe, eg.x, J) + gsel(pe, eg.y, J) + gsel(pe, eg.z, J) + gsel(pe, eg.w, J);
+                const int col = min(8 * ct + 2 * q + e, jn - 1);
+                init[ct][e] = pr[col];
             }
     }
-    if (!bwd) {
-        // B = b[P] + children rows; one row tile per front persists fr[P] for the backward pass
-        const bool store_piv = (r0 == 0);
-        // all loads first, then the stores (fr may alias FRm: interleaving them would serialise the loads)
-        double v[SG_KMAX / 8];
-#pragma unroll
-        for (int u = 0; u < SG_KMAX / 8; ++u) {
-            const int kk = warp + 8 * u;
-            const int kq = min(kk, kc - 1);
-            const int4 gq = s_gsrc[kq];
-            const double* pb = FRm + j0 + (jok ? jt : 0);
-            const double bv = b[(int64_t)s_idx[kq] * J + j0 + (jok ? jt : 0)];
-            const double sv = bv + gsel(pb, gq.x, J) + gsel(pb, gq.y, J) + gsel(pb, gq.z, J) + gsel(pb, gq.w, J);
-            v[u] = (kk < kc && jok) ? sv : 0.0;
-        }
-#pragma unroll
-        for (int u = 0; u < SG_KMAX / 8; ++u) {
-            const int kk = warp + 8 * u;
-            if (kk < kc) {
-                Bs[kk * SG_LDB + jt] = v[u];
-                if (store_piv && jok) fr[(int64_t)(kbeg + kk) * J + j0 + jt] = v[u];
-            }
-        }
-    }
-    if (!bwd) {   // forward: A after the operand gather (the gather needs the registers)
-#pragma unroll
-        for (int u = 0; u < SG_KMAX / 4; ++u) a[u] = (row_ok && 4 * u + q < kc) ? __ldg(arow + 4 * u) : 0.0;
-    }
-    // zero the K padding (kc -> multiple of 4) of B (A's padding is zero-filled in registers)
-    for (int e = tid; e < (kpad - kc) * SG_C; e += SG_T) Bs[(kc + e / SG_C) * SG_LDB + e % SG_C] = 0.0;
-    cp_async_wait_all();
+    if (bwd)
+        for (int t = tid; t < kc; t += SG_T) s_idx[t] = (kbeg + t >= k) ? d.idx[fo + kbeg + t] : 0;
     __syncthreads();
+    SG_T_(1);
+    // (2) pipeline prologue: stages 0 .. nstage-2, one commit group each
+    issue_b(0);
+    cp_async_commit();
+    for (int c = 1; c < nstage - 1; ++c) {
+        if (c < nch) {
+            issue_a(c);
+            issue_b(c);
+        }
+        cp_async_commit();
+    }
     SG_T_(2);
-    // (4) MMA
-    const int nct = (jn + 7) >> 3;
+    // (3) mainloop
     double dacc[4][2] = {{0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}};
-    const double* bp = Bs + q * SG_LDB + g;
+    for (int c = 0; c < nch; ++c) {
+        cp_async_wait_n(nstage - 2);
+        __syncthreads();
+        const int cn = c + nstage - 1;
+        if (cn < nch) {
+            issue_a(cn);
+            issue_b(cn);
+        }
+        cp_async_commit();
+        const double* As = sm + (c % nstage) * SG_STAGE;
+        const double* ap = As + row * SG_LDA + q;
+        const double* bp = As + SG_R * SG_LDA + q * SG_LDB + g;
+        const int ksteps = (min(SG_KC, kc - c * SG_KC) + 3) >> 2;
+        if (ksteps == SG_KC / 4) {
 #pragma unroll
-    for (int u = 0; u < SG_KMAX / 4; ++u) {
-        if (4 * u < kpad) {
+            for (int u = 0; u < SG_KC / 4; ++u) {
+                const double av = ap[4 * u];
 #pragma unroll
-            for (int ct = 0; ct < 4; ++ct)
-                if (ct < nct) dmma8(dacc[ct][0], dacc[ct][1], a[u], bp[4 * u * SG_LDB + 8 * ct]);
+                for (int ct = 0; ct < NCT; ++ct) dmma8(dacc[ct][0], dacc[ct][1], av, bp[4 * u * SG_LDB + 8 * ct]);
+            }
+        } else {
+#pragma unroll 2
+            for (int u = 0; u < ksteps; ++u) {
+                const double av = ap[4 * u];
+#pragma unroll
+                for (int ct = 0; ct < NCT; ++ct) dmma8(dacc[ct][0], dacc[ct][1], av, bp[4 * u * SG_LDB + 8 * ct]);
+            }
         }
     }
 #ifdef SG_PROBE
@@ -298,7 +322,7 @@ __global__ void __launch_bounds__(SG_T, 3) k_sgemm(MfDev d, const int4* __restri
         const unsigned i_ = atomicAdd(&g_probe_n, 1u);                                                   \
         if (i_ < SG_PROBE_MAX) {                                                                         \
             unsigned long long* o_ = g_probe[i_];                                                        \
-            o_[0] = (unsigned long long)bwd * 1000000 + (unsigned long long)kmax * 1000 + (tag);         \
+            o_[0] = (unsigned long long)bwd * 1000000 + (unsigned long long)min(kc, 999) * 1000 + (tag);         \
             o_[1] = blockIdx.x; o_[2] = kc; o_[3] = tp0; o_[4] = tp1 - tp0; o_[5] = tp2 - tp1;            \
             o_[6] = tp3 - tp2; o_[7] = gtime() - tp3;                                                    \
         }                                                                                                \
@@ -321,7 +345,7 @@ __global__ void __launch_bounds__(SG_T, 3) k_sgemm(MfDev d, const int4* __restri
         __syncthreads();
         const int s0 = slot - ks;
         const int ns = (K + split_k - 1) / split_k;
-        const int tk = (int)(((int64_t)mat * nslot + s0) * gridDim.z + blockIdx.z);
+        const int tk = (int)(((int64_t)mat * nslot + s0) * ((J + SG_C - 1) / SG_C) + zb);
         if (tid == 0) s_last = (atomicAdd(ticket + tk, 1) == ns - 1);
         __syncthreads();
         if (!s_last) {
@@ -335,7 +359,7 @@ __global__ void __launch_bounds__(SG_T, 3) k_sgemm(MfDev d, const int4* __restri
         const int64_t pst = (int64_t)SG_R * J;
 #pragma unroll
         for (int ct = 0; ct < 4; ++ct) dacc[ct][0] = dacc[ct][1] = 0.0;
-#pragma unroll 2
+#pragma unroll 4
         for (int qq = 0; qq < ns; ++qq) {
 #pragma unroll
             for (int ct = 0; ct < 4; ++ct)
@@ -359,9 +383,16 @@ __global__ void __launch_bounds__(SG_T, 3) k_sgemm(MfDev d, const int4* __restri
     SG_END(slot >= 0 ? 2 : 0);
 }
 
-static size_t sg_smem(int kmax) {
-    const size_t kpad = (kmax + 3) & ~3;
-    return sizeof(double) * kpad * SG_LDB;
+static size_t sg_smem(int nstage) { return sizeof(double) * (size_t)nstage * SG_STAGE; }
+
+static int sg_stages(int kmax) {
+    static int env = -1;
+    if (env < 0) {
+        const char* e = std::getenv("ENS_SOLVE_STAGES");
+        env = e ? std::max(2, std::min(3, std::atoi(e))) : 0;
+    }
+    if (env > 0) return env;
+    return kmax <= 2 * SG_KC ? 2 : 3;
 }
 
 static bool capturing(cudaStream_t s) {
@@ -405,19 +436,50 @@ static int mf_solve_launches(ens_ctx* c, cudaStream_t s, SolveIO* io, int64_t* n
         const int64_t nrow = (int64_t)sched->size() / 5;
         for (int64_t i = 0; i < nrow; ++i) {
             const int64_t* q = &(*sched)[5 * i];
-            const int op = (int)q[0], off = (int)q[2], n = (int)q[3], kmax = (int)q[4];
-            if (n == 0) continue;
-            if ((op != SOP_FGEMM && op != SOP_BGEMM) || kmax > SG_KMAX || kmax < 1) {
+            const int op = (int)q[0], L = (int)q[1], off = (int)q[2], n = (int)q[3], kmax = (int)q[4];
+            if ((op != SOP_FGEMM && op != SOP_BGEMM) || kmax > SG_KMAX || kmax < 0 || L < 0 ||
+                L >= (int)c->level_front_off.size() - 1) {
                 ens_set_error("bad solve schedule row", __FILE__, __LINE__);
                 return ENS_EINVAL;
             }
-            for (int rep = 0; rep < (timing ? trep : 1); ++rep) {   // launches are idempotent
-                k_sgemm<<<dim3(n, 2, zc), SG_T, sg_smem(kmax), s>>>(d, c->sitem, off, c->fronts, c->frvec, io, N,
-                                                                   J, nidx, op == SOP_BGEMM, sk, kmax, c->partial,
-                                                                   c->ticket, nslot);
-                ENS_CKL();
+            if (op == SOP_FGEMM) {   // assemble the level's front rows first
+                const int64_t a = c->finit_off[L], nr = c->finit_off[L + 1] - a;
+                const int64_t tot = nr * ((J & 1) ? J : J / 2);
+                if (nr > 0) {
+                    const unsigned nb = (unsigned)std::min<int64_t>((tot + 255) / 256, 148 * 8);
+                    for (int rep = 0; rep < (timing ? trep : 1); ++rep) {
+                        k_finit<<<dim3(nb, 2), 256, 0, s>>>(c->finit_rows + a, nr, c->p.f_idx, c->p.gsrc, c->frvec, io,
+                                                            N, J, nidx);
+                        ENS_CKL();
+                    }
+                    ++cnt;
+                    mark("finit", (int)nr, 0);
+                }
             }
-            ++cnt;
+            if (n == 0 || kmax == 0) continue;
+            const int nst = sg_stages(kmax);
+            for (int rep = 0; rep < (timing ? trep : 1); ++rep) {   // launches are idempotent
+                // member column blocks: full 32-wide blocks use 4 column tiles, the remainder fewer
+                const int zfull = J / SG_C, rem = J - zfull * SG_C;
+#define SGL(NC, ZN, Z0)                                                                                        \
+    k_sgemm<NC><<<dim3(n, 2, ZN), SG_T, sg_smem(nst), s>>>(d, c->sitem, off, c->fronts, c->frvec, io, N, J, nidx, \
+                                                          op == SOP_BGEMM, sk, nst, c->partial, c->ticket, nslot, Z0)
+                if (zfull > 0) {
+                    SGL(4, (unsigned)zfull, 0);
+                    ENS_CKL();
+                    if (rep == 0) ++cnt;
+                }
+                if (rem > 0) {
+                    const int nct = (rem + 7) / 8;
+                    if (nct == 1) SGL(1, 1, zfull);
+                    else if (nct == 2) SGL(2, 1, zfull);
+                    else if (nct == 3) SGL(3, 1, zfull);
+                    else SGL(4, 1, zfull);
+                    ENS_CKL();
+                    if (rep == 0) ++cnt;
+                }
+#undef SGL
+            }
             mark(op == SOP_BGEMM ? "bwd" : "fwd", n, kmax);
         }
     }
@@ -449,7 +511,10 @@ int mf_solve(ens_ctx* c, cudaStream_t s, const double* r, double* z) {
             return ENS_EINVAL;
         }
         ENS_CK(cudaMalloc(&c->solve_io, sizeof(SolveIO)));
-        ENS_CK(cudaFuncSetAttribute(k_sgemm, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sg_smem(SG_KMAX)));
+        ENS_CK(cudaFuncSetAttribute(k_sgemm<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sg_smem(3)));
+        ENS_CK(cudaFuncSetAttribute(k_sgemm<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sg_smem(3)));
+        ENS_CK(cudaFuncSetAttribute(k_sgemm<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sg_smem(3)));
+        ENS_CK(cudaFuncSetAttribute(k_sgemm<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sg_smem(3)));
         const int64_t ns = c->p.n_slot > 0 ? c->p.n_slot : 1;
         const size_t pbytes = sizeof(double) * 2 * (size_t)ns * SG_R * c->J;
         const size_t tbytes = sizeof(int) * 2 * (size_t)ns * ((c->J + SG_C - 1) / SG_C);
@@ -458,13 +523,44 @@ int mf_solve(ens_ctx* c, cudaStream_t s, const double* r, double* z) {
             return ENS_ENOMEM;
         }
         ENS_CK(cudaMemset(c->ticket, 0, tbytes));
+        // front geometry on the host: children, per-row forward assembly flags
+        const int nf = (int)c->p.nfront;
+        std::vector<int32_t> fm(nf), fk(nf), par(nf);
+        c->idx_off_h.assign((size_t)nf + 1, 0);
+        ENS_CK(cudaMemcpy(fm.data(), c->p.f_m, sizeof(int32_t) * nf, cudaMemcpyDeviceToHost));
+        ENS_CK(cudaMemcpy(fk.data(), c->p.f_k, sizeof(int32_t) * nf, cudaMemcpyDeviceToHost));
+        ENS_CK(cudaMemcpy(par.data(), c->p.f_parent, sizeof(int32_t) * nf, cudaMemcpyDeviceToHost));
+        ENS_CK(cudaMemcpy(c->idx_off_h.data(), c->p.f_idx_off, sizeof(int64_t) * (nf + 1), cudaMemcpyDeviceToHost));
+        std::vector<uint8_t> hasch(nf, 0);
+        for (int f = 0; f < nf; ++f)
+            if (par[f] >= 0 && par[f] < nf) hasch[par[f]] = 1;
+        // per level: the rows k_finit assembles (pivot rows flagged in bit 31)
+        const int nlev = (int)c->level_front_off.size() - 1;
+        std::vector<int32_t> rows;
+        c->finit_off.assign((size_t)nlev + 1, 0);
+        for (int L = 0; L < nlev; ++L) {
+            c->finit_off[L] = (int64_t)rows.size();
+            for (int f = c->level_front_off[L]; f < c->level_front_off[L + 1]; ++f)
+                for (int t = 0; t < fm[f]; ++t)
+                    if (t < fk[f] || hasch[f])
+                        rows.push_back((int32_t)(c->idx_off_h[f] + t) | (t < fk[f] ? (int32_t)0x80000000 : 0));
+        }
+        c->finit_off[nlev] = (int64_t)rows.size();
+        const int64_t nidx = (int64_t)rows.size();
+        uint8_t* d_hasch = nullptr;
+        ENS_CK(cudaMalloc(&c->finit_rows, sizeof(int32_t) * (size_t)(nidx > 0 ? nidx : 1)));
+        ENS_CK(cudaMemcpy(c->finit_rows, rows.data(), sizeof(int32_t) * (size_t)nidx, cudaMemcpyHostToDevice));
+        ENS_CK(cudaMalloc(&d_hasch, (size_t)(nf > 0 ? nf : 1)));
+        ENS_CK(cudaMemcpy(d_hasch, hasch.data(), (size_t)nf, cudaMemcpyHostToDevice));
         const int64_t nw = c->p.n_work;
         ENS_CK(cudaMalloc(&c->sitem, sizeof(int4) * 3 * (size_t)(nw > 0 ? nw : 1)));
         if (nw > 0) {
-            k_build_sitem<<<(unsigned)((nw + 255) / 256), 256, 0, s>>>(mfdev(c), nw, (int)c->p.nfront, c->sitem);
+            k_build_sitem<<<(unsigned)((nw + 255) / 256), 256, 0, s>>>(mfdev(c), nw, nf, d_hasch, c->sitem);
             ENS_CKL();
         }
-        c->ws_bytes += pbytes + tbytes + sizeof(int4) * 3 * (size_t)nw;
+        ENS_CK(cudaStreamSynchronize(s));
+        cudaFree(d_hasch);
+        c->ws_bytes += pbytes + tbytes + sizeof(int4) * 3 * (size_t)nw + sizeof(int32_t) * (size_t)nidx;
     }
     SolveIO* io = (SolveIO*)c->solve_io;
     k_set_io<<<1, 1, 0, s>>>(io, r, z);

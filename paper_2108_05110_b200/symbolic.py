@@ -404,7 +404,7 @@ def analyse(disc, leaf=LEAF_NODES, pw=PW):
 # op codes (must match csrc/mf.cu)
 OP_ZERO, OP_ORIG, OP_EXTADD, OP_DIAG, OP_HPANEL, OP_UPDATE, OP_GPANEL = range(7)
 SOP_FINIT, SOP_FEXT, SOP_FGEMM, SOP_BGATHER, SOP_BGEMM, SOP_FRED, SOP_BRED = range(7)
-SPLIT_K = int(__import__("os").environ.get("ENS_SPLIT_K", "64"))  # inner length per solve-GEMM work item
+SPLIT_K = int(__import__("os").environ.get("ENS_SPLIT_K", "256"))  # inner length per solve-GEMM work item
 MAX_GSRC = 4      # child contribution rows gathered per front-vector row
 EXT_ROWS = 8      # child-CB rows per extend-add work item
 VEC_ROWS = 64     # front-vector rows per init/gather/scatter work item
