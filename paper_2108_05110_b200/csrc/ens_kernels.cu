@@ -66,6 +66,11 @@ __device__ __forceinline__ void grad_phi(const double* gl, int q, int a, double&
     gy = d0 * gl[1] + d1 * gl[3] + d2 * gl[5];
 }
 
+static bool red_vec_ok(int J, const void* a, const void* b) {
+    return (J & 1) == 0 && J <= 512 && (reinterpret_cast<uintptr_t>(a) & 15) == 0 &&
+           (reinterpret_cast<uintptr_t>(b) & 15) == 0;
+}
+
 static inline int next_pow2(int x) {
     int s = 1;
     while (s < x) s <<= 1;
@@ -91,7 +96,31 @@ __global__ void k_member_sums(const double* __restrict__ X, double* __restrict__
     if (sl == 0) sums[r] = acc;
 }
 
+// thread per row (even J): H 16-byte loads, fixed sequential member order
+__global__ void __launch_bounds__(256) k_member_sums2(const double* __restrict__ X, double* __restrict__ sums,
+                                                      int nvel, int64_t N, int J) {
+    const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= 2 * (int64_t)nvel) return;
+    const int mat = (int)(r / nvel);
+    const int64_t row = r - (int64_t)mat * nvel;
+    const double2* xr = reinterpret_cast<const double2*>(X + (int64_t)mat * N * J + row * J);
+    double a0 = 0.0, a1 = 0.0;
+#pragma unroll 4
+    for (int i = 0; i < (J >> 1); ++i) {
+        const double2 v = xr[i];
+        a0 += v.x;
+        a1 += v.y;
+    }
+    sums[r] = a0 + a1;
+}
+
 int launch_member_sums(ens_ctx* c, cudaStream_t s, const double* x, double* sums) {
+    if ((c->J & 1) == 0 && (reinterpret_cast<uintptr_t>(x) & 15) == 0) {
+        const int64_t rows = 2LL * c->n_vel;
+        k_member_sums2<<<(unsigned)((rows + 255) / 256), 256, 0, s>>>(x, sums, c->n_vel, c->n_total, c->J);
+        ENS_CKL();
+        return ENS_OK;
+    }
     const int S = c->J >= 32 ? 32 : next_pow2(c->J);
     const int64_t rows = 2LL * c->n_vel;
     const int64_t warps = (rows + (32 / S) - 1) / (32 / S);
@@ -533,12 +562,66 @@ __global__ void k_axpy_norm_part(double* __restrict__ W, const double* __restric
     }
 }
 
+__global__ void __launch_bounds__(256) k_axpy_norm_part2(double* __restrict__ W, const double* __restrict__ V,
+                                                         int64_t lstride, int L, const double* __restrict__ h,
+                                                         int64_t rows, int64_t matstride, int J,
+                                                         double* __restrict__ part) {
+    __shared__ double2 red[256];
+    const int mat = blockIdx.z;
+    const int H = J >> 1;
+    const int64_t per = (rows + gridDim.x - 1) / gridDim.x;
+    const int64_t r0 = (int64_t)blockIdx.x * per;
+    const int64_t r1 = min(rows, r0 + per);
+    const int RPB = 256 / H;
+    const int jp = threadIdx.x % H, ro = threadIdx.x / H;
+    double2 hl[ENS_MAX_RESTART + 1];
+    for (int l = 0; l < L; ++l)
+        hl[l] = ro < RPB ? reinterpret_cast<const double2*>(h + ((int64_t)mat * L + l) * J)[jp] : make_double2(0, 0);
+    double2* w2 = reinterpret_cast<double2*>(W + (int64_t)mat * matstride);
+    const double2* v2 = reinterpret_cast<const double2*>(V + (int64_t)mat * matstride);
+    double2 acc[2] = {{0.0, 0.0}, {0.0, 0.0}};
+    if (ro < RPB) {
+        int64_t r = r0 + ro;
+        for (int u = 0; r < r1; r += RPB, u ^= 1) {
+            const int64_t i = r * H + jp;
+            double2 sum = make_double2(0.0, 0.0);
+            for (int l = 0; l < L; ++l) {
+                const double2 v = v2[(int64_t)l * (lstride >> 1) + i];
+                sum.x += v.x * hl[l].x;
+                sum.y += v.y * hl[l].y;
+            }
+            double2 w = w2[i];
+            w.x -= sum.x;
+            w.y -= sum.y;
+            w2[i] = w;
+            acc[u].x += w.x * w.x;
+            acc[u].y += w.y * w.y;
+        }
+    }
+    red[threadIdx.x] = make_double2(acc[0].x + acc[1].x, acc[0].y + acc[1].y);
+    __syncthreads();
+    if (threadIdx.x < H) {
+        double2 sum = make_double2(0.0, 0.0);
+        for (int k = 0; k < RPB; ++k) {
+            sum.x += red[k * H + threadIdx.x].x;
+            sum.y += red[k * H + threadIdx.x].y;
+        }
+        double* o = part + ((int64_t)blockIdx.x * 2 + mat) * J + 2 * threadIdx.x;
+        o[0] = sum.x;
+        o[1] = sum.y;
+    }
+}
+
 int launch_axpy_norm(ens_ctx* c, cudaStream_t s, double* W, const double* V, int64_t lstride, int L,
                      const double* h, int64_t rows, double* out) {
     const int RB = ENS_RED_BLOCKS;
     if (L > ENS_MAX_RESTART + 1) return ENS_EINVAL;
-    k_axpy_norm_part<<<dim3(RB, 1, 2), 256, 0, s>>>(W, V, lstride, L, h, rows, (int64_t)c->n_total * c->J, c->J,
-                                                   c->red_part);
+    if (red_vec_ok(c->J, W, V) && (lstride & 1) == 0)
+        k_axpy_norm_part2<<<dim3(RB, 1, 2), 256, 0, s>>>(W, V, lstride, L, h, rows, (int64_t)c->n_total * c->J, c->J,
+                                                        c->red_part);
+    else
+        k_axpy_norm_part<<<dim3(RB, 1, 2), 256, 0, s>>>(W, V, lstride, L, h, rows, (int64_t)c->n_total * c->J, c->J,
+                                                       c->red_part);
     ENS_CKL();
     const int tot = 2 * c->J;
     k_coldot_fin<<<(tot * 32 + 255) / 256, 256, 0, s>>>(c->red_part, RB, 1, c->J, out);
@@ -559,11 +642,63 @@ __global__ void k_coldot_fin(const double* __restrict__ part, int RB, int L, int
     if (lane == 0) out[t] = s;
 }
 
+// even J: 16-byte lanes (member pairs), 4 independent row streams per thread.
+// Fixed row partition and summation order => deterministic, identical columns agree.
+__global__ void __launch_bounds__(256) k_coldot_part2(const double* __restrict__ A, int64_t lstride,
+                                                      const double* __restrict__ B, int64_t rows, int64_t matstride,
+                                                      int J, int L, double* __restrict__ part) {
+    __shared__ double2 red[256];
+    const int l = blockIdx.y, mat = blockIdx.z;
+    const int H = J >> 1;
+    const double2* a = reinterpret_cast<const double2*>(A + (int64_t)l * lstride + (int64_t)mat * matstride);
+    const double2* b = reinterpret_cast<const double2*>(B + (int64_t)mat * matstride);
+    const int64_t per = (rows + gridDim.x - 1) / gridDim.x;
+    const int64_t r0 = (int64_t)blockIdx.x * per;
+    const int64_t r1 = min(rows, r0 + per);
+    const int RPB = 256 / H;
+    const int jp = threadIdx.x % H, ro = threadIdx.x / H;
+    double2 acc[4] = {{0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}};
+    if (ro < RPB) {
+        int64_t r = r0 + ro;
+        for (; r + 3 * RPB < r1; r += 4 * RPB) {
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int64_t i = (r + u * RPB) * H + jp;
+                const double2 x = a[i], y = b[i];
+                acc[u].x += x.x * y.x;
+                acc[u].y += x.y * y.y;
+            }
+        }
+        for (int u = 0; r < r1; r += RPB, ++u) {
+            const int64_t i = r * H + jp;
+            const double2 x = a[i], y = b[i];
+            acc[u].x += x.x * y.x;
+            acc[u].y += x.y * y.y;
+        }
+    }
+    red[threadIdx.x] = make_double2((acc[0].x + acc[1].x) + (acc[2].x + acc[3].x),
+                                    (acc[0].y + acc[1].y) + (acc[2].y + acc[3].y));
+    __syncthreads();
+    if (threadIdx.x < H) {
+        double2 sum = make_double2(0.0, 0.0);
+        for (int k = 0; k < RPB; ++k) {
+            sum.x += red[k * H + threadIdx.x].x;
+            sum.y += red[k * H + threadIdx.x].y;
+        }
+        double* o = part + (((int64_t)blockIdx.x * 2 + mat) * L + l) * J + 2 * threadIdx.x;
+        o[0] = sum.x;
+        o[1] = sum.y;
+    }
+}
+
 int launch_coldot(ens_ctx* c, cudaStream_t s, const double* A, int64_t lstride, int L, const double* B,
                   int64_t rows, double* out) {
     const int RB = ENS_RED_BLOCKS;
     dim3 grid(RB, L, 2);
-    k_coldot_part<<<grid, 256, 0, s>>>(A, lstride, B, rows, (int64_t)c->n_total * c->J, c->J, L, c->red_part);
+    if (red_vec_ok(c->J, A, B) && (lstride & 1) == 0)
+        k_coldot_part2<<<grid, 256, 0, s>>>(A, lstride, B, rows, (int64_t)c->n_total * c->J, c->J, L, c->red_part);
+    else
+        k_coldot_part<<<grid, 256, 0, s>>>(A, lstride, B, rows, (int64_t)c->n_total * c->J, c->J, L, c->red_part);
     ENS_CKL();
     const int tot = 2 * L * c->J;
     k_coldot_fin<<<(tot * 32 + 255) / 256, 256, 0, s>>>(c->red_part, RB, L, c->J, out);

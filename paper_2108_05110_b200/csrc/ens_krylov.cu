@@ -1,3 +1,4 @@
+#include <algorithm>
 // Column-batched right-preconditioned FGMRES over both saddle systems.
 //
 // Every ensemble member is an independent column (no block Krylov mixing, so
@@ -83,6 +84,56 @@ __global__ void k_scale_cols(double* __restrict__ dst, const double* __restrict_
     const int mat = (int)(t / per);
     const int j = (int)((t - mat * per) % J);
     dst[t] = src[t] * scale[mat * J + j];
+}
+
+// even J: 16-byte lanes over (mat, member pair); 32-bit index math, grid-stride
+__global__ void __launch_bounds__(256) k_scale_cols2(double* __restrict__ dst, const double* __restrict__ src,
+                                                     const double* __restrict__ scale, int per2, int H) {
+    const int mat = blockIdx.y;
+    const double2* s2 = reinterpret_cast<const double2*>(src) + (int64_t)mat * per2;
+    double2* d2 = reinterpret_cast<double2*>(dst) + (int64_t)mat * per2;
+    const double2* sc = reinterpret_cast<const double2*>(scale + (int64_t)mat * 2 * H);
+    for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < per2; t += gridDim.x * blockDim.x) {
+        const double2 a = s2[t], f = sc[t % H];
+        d2[t] = make_double2(a.x * f.x, a.y * f.y);
+    }
+}
+
+__global__ void __launch_bounds__(256) k_axpy_multi2(double* __restrict__ W, const double* __restrict__ V,
+                                                     int64_t lstride, int L, const double* __restrict__ h, double sign,
+                                                     int per2, int H) {
+    const int mat = blockIdx.y;
+    double2* w2 = reinterpret_cast<double2*>(W) + (int64_t)mat * per2;
+    for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < per2; t += gridDim.x * blockDim.x) {
+        const int jp = t % H;
+        double2 acc = make_double2(0.0, 0.0);
+        for (int l = 0; l < L; ++l) {
+            const double2 v = reinterpret_cast<const double2*>(V + (int64_t)l * lstride)[(int64_t)mat * per2 + t];
+            const double2 y = reinterpret_cast<const double2*>(h + ((int64_t)mat * L + l) * 2 * H)[jp];
+            acc.x += v.x * y.x;
+            acc.y += v.y * y.y;
+        }
+        double2 w = w2[t];
+        w.x += sign * acc.x;
+        w.y += sign * acc.y;
+        w2[t] = w;
+    }
+}
+
+static unsigned vec_blocks(int64_t n) { return (unsigned)std::min<int64_t>((n + 255) / 256, 148 * 16); }
+
+static bool vec_ok(int J, int64_t N, const void* a, const void* b) {
+    return (J & 1) == 0 && N * J / 2 < (1LL << 31) && (reinterpret_cast<uintptr_t>(a) & 15) == 0 &&
+           (reinterpret_cast<uintptr_t>(b) & 15) == 0;
+}
+
+static void scale_cols(cudaStream_t s, double* dst, const double* src, const double* scale, int64_t N, int J) {
+    if (vec_ok(J, N, dst, src)) {
+        const int per2 = (int)(N * J / 2);
+        k_scale_cols2<<<dim3(vec_blocks(per2), 2), 256, 0, s>>>(dst, src, scale, per2, J / 2);
+    } else {
+        k_scale_cols<<<(unsigned)((2 * N * J + 255) / 256), 256, 0, s>>>(dst, src, scale, N, J);
+    }
 }
 
 // W -= sum_l V_l h[mat][l][j]  (sign = -1) or X += sum_l Z_l y (sign = +1)
@@ -221,7 +272,7 @@ int gmres_solve(ens_ctx* c, cudaStream_t s, const double* as_vals, const double*
             *iters = total_it;
             return active == 0 ? ENS_OK : ENS_ENOCONV;
         }
-        k_scale_cols<<<eb, 256, 0, s>>>(V, Rb, kb.scale, N, J);
+        scale_cols(s, V, Rb, kb.scale, N, J);
         ENS_CKL();
         int used = 0;
         for (int i = 0; i < restart; ++i) {
@@ -237,7 +288,7 @@ int gmres_solve(ens_ctx* c, cudaStream_t s, const double* as_vals, const double*
             ENS_CK(cudaMemsetAsync(c->d_count, 0, sizeof(int32_t), s));
             k_gm_givens<<<cb, 128, 0, s>>>(c->cols, kb.h1, nullptr, kb.hn2, i, kb.scale, c->d_count, n, J);
             ENS_CKL();
-            k_scale_cols<<<eb, 256, 0, s>>>(V + blk * (i + 1), Wb, kb.scale, N, J);
+            scale_cols(s, V + blk * (i + 1), Wb, kb.scale, N, J);
             ENS_CKL();
             used = i + 1;
             ++total_it;
@@ -246,7 +297,12 @@ int gmres_solve(ens_ctx* c, cudaStream_t s, const double* as_vals, const double*
         }
         k_gm_solve_y<<<cb, 128, 0, s>>>(c->cols, kb.y, used, n, J);
         ENS_CKL();
-        k_axpy_multi<<<eb, 256, 0, s>>>(x, Z, blk, used, kb.y, 1.0, N, J);
+        if (vec_ok(J, N, x, Z) && (blk & 1) == 0) {
+            const int per2 = (int)(N * J / 2);
+            k_axpy_multi2<<<dim3(vec_blocks(per2), 2), 256, 0, s>>>(x, Z, blk, used, kb.y, 1.0, per2, J / 2);
+        } else {
+            k_axpy_multi<<<eb, 256, 0, s>>>(x, Z, blk, used, kb.y, 1.0, N, J);
+        }
         ENS_CKL();
     }
     return ENS_ENOCONV;
