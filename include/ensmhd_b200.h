@@ -86,6 +86,11 @@ typedef struct {
     double area;               /* domain area                           */
     int32_t mean_zero;         /* subtract the pressure mean after solve */
     int32_t pad1;
+    /* deterministic scatter-free assembly (element buffers gathered per row / slot) */
+    const int32_t* n2e_ptr;    /* ns+1: velocity node -> element-local entries  */
+    const int32_t* n2e;        /* nt*6: entries e*6 + a, element order per node */
+    const int32_t* s2e_ptr;    /* nnz_s+1: CSR slot -> element-local entries     */
+    const int32_t* s2e;        /* nt*36: entries ab*nt + e                        */
 } ens_mesh_desc;
 
 /* Multifrontal plan produced once per mesh by symbolic.py. */

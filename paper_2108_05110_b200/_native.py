@@ -29,6 +29,7 @@ class MeshDesc(C.Structure):
         ("e_nodes", P), ("e_geo", P), ("e_slots", P), ("color_off_host", P),
         ("cons_row", P), ("cons_bidx", P), ("pres_int", P),
         ("area", F64), ("mean_zero", I32), ("pad1", I32),
+        ("n2e_ptr", P), ("n2e", P), ("s2e_ptr", P), ("s2e", P),
     ]
 
 

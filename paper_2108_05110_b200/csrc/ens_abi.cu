@@ -122,6 +122,8 @@ void ens_destroy(ens_ctx* c) {
     cudaFree(c->ticket);
     cudaFree(c->sitem);
     cudaFree(c->finit_rows);
+    cudaFree(c->ec);
+    cudaFree(c->el);
     delete c;
 }
 

@@ -62,6 +62,8 @@ struct ens_ctx {
     double* partial = nullptr;     // split-K partial products of the solve GEMMs
     int* ticket = nullptr;         // split-K arrival counters (last CTA reduces)
     int4* sitem = nullptr;         // solve work items with their front's geometry (3 x int4 per item)
+    double* ec = nullptr;          // member-pass element buffer [2][nt][6][2][J]
+    double* el = nullptr;          // assembly element buffer [2][36][nt]
     int32_t* finit_rows = nullptr; // per level: front rows k_finit assembles (bit 31: pivot row)
     std::vector<int64_t> finit_off;   // level offsets into finit_rows
     std::vector<int64_t> idx_off_h;   // host copy of the plan's f_idx_off

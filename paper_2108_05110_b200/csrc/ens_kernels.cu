@@ -239,7 +239,8 @@ int launch_rhs(ens_ctx* c, cudaStream_t s, const double* x, const double* coef, 
 // ---------------------------------------------------------------------------
 __global__ void k_member_pass(const int32_t* __restrict__ enodes, const double* __restrict__ egeo, int e0, int ne,
                               const double* __restrict__ X, const double* __restrict__ means, double* __restrict__ rhs,
-                              unsigned long long* __restrict__ maxsq, int nt, int nvel, int64_t N, int J, int JB) {
+                              unsigned long long* __restrict__ maxsq, int nt, int nvel, int64_t N, int J, int JB,
+                              double* __restrict__ ec) {
     extern __shared__ double sh_sq[];   // [EPB][2][7][JB]
     const int EPB = blockDim.x / JB;
     const int el = threadIdx.x / JB, jj = threadIdx.x % JB;
@@ -313,13 +314,24 @@ __global__ void k_member_pass(const int32_t* __restrict__ enodes, const double* 
                 rw[a][1] += cw1 * ph;
             }
         }
+        if (ec) {   // element buffer [mat][e][a][cc][j], gathered per row by k_member_gather
+            const int64_t eb = (int64_t)e * 12 * J + j, ms = (int64_t)nt * 12 * J;
 #pragma unroll
-        for (int a = 0; a < 6; ++a) {
+            for (int a = 0; a < 6; ++a)
 #pragma unroll
-            for (int cc = 0; cc < 2; ++cc) {
-                const int64_t row = 2LL * nd[a] + cc;
-                rhs[row * J + j] -= rv[a][cc];
-                rhs[N * J + row * J + j] -= rw[a][cc];
+                for (int cc = 0; cc < 2; ++cc) {
+                    ec[eb + (2 * a + cc) * J] = rv[a][cc];
+                    ec[ms + eb + (2 * a + cc) * J] = rw[a][cc];
+                }
+        } else {
+#pragma unroll
+            for (int a = 0; a < 6; ++a) {
+#pragma unroll
+                for (int cc = 0; cc < 2; ++cc) {
+                    const int64_t row = 2LL * nd[a] + cc;
+                    rhs[row * J + j] -= rv[a][cc];
+                    rhs[N * J + row * J + j] -= rw[a][cc];
+                }
             }
         }
     } else if (el < EPB) {
@@ -342,8 +354,59 @@ __global__ void k_member_pass(const int32_t* __restrict__ enodes, const double* 
     }
 }
 
+// rhs[mat][row][j] -= sum over the node's element entries (fixed order) -- even J, 16-byte lanes
+__global__ void __launch_bounds__(256) k_member_gather(const int32_t* __restrict__ n2e_ptr,
+                                                       const int32_t* __restrict__ n2e, const double* __restrict__ ec,
+                                                       double* __restrict__ rhs, int ns, int nt, int64_t N, int J) {
+    const int H = J >> 1;
+    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= 2LL * ns * H) return;
+    const int mat = blockIdx.y;
+    const int64_t row = t / H;                   // velocity row 2*node + cc
+    const int jp = (int)(t - row * H);
+    const int node = (int)(row >> 1), cc = (int)(row & 1);
+    const double2* e2 = reinterpret_cast<const double2*>(ec + (int64_t)mat * nt * 12 * J);
+    double2 acc = make_double2(0.0, 0.0);
+    const int k0 = n2e_ptr[node], k1 = n2e_ptr[node + 1];
+    for (int k = k0; k < k1; ++k) {
+        const int ea = n2e[k];                   // e*6 + a
+        const double2 v = e2[((int64_t)ea * 2 + cc) * H + jp];
+        acc.x += v.x;
+        acc.y += v.y;
+    }
+    double2* r2 = reinterpret_cast<double2*>(rhs + (int64_t)mat * N * J);
+    double2 r = r2[row * H + jp];
+    r.x -= acc.x;
+    r.y -= acc.y;
+    r2[row * H + jp] = r;
+}
+
 int launch_member_pass(ens_ctx* c, cudaStream_t s, const double* x, const double* means, double* rhs,
                        double* maxsq) {
+    if (c->m.n2e && (c->J & 1) == 0) {
+        // all elements in one launch into an element buffer, then one ordered gather per row
+        const int J = c->J;
+        const int JB = J < 128 ? J : 128;
+        const int EPB = 128 / JB > 0 ? 128 / JB : 1;
+        const int threads = EPB * JB;
+        const size_t shm = sizeof(double) * (size_t)EPB * 2 * ENS_NQ * JB;
+        const size_t ecb = sizeof(double) * 2 * (size_t)c->m.nt * 12 * J;
+        if (!c->ec) {
+            ENS_CK(cudaMalloc(&c->ec, ecb));
+            c->ws_bytes += ecb;
+        }
+        ENS_CK(cudaMemsetAsync(maxsq, 0, sizeof(double) * 2 * (size_t)c->m.nt * ENS_NQ, s));
+        dim3 grid((c->m.nt + EPB - 1) / EPB, (J + JB - 1) / JB);
+        k_member_pass<<<grid, threads, shm, s>>>(c->m.e_nodes, c->m.e_geo, 0, c->m.nt, x, means, rhs,
+                                                  reinterpret_cast<unsigned long long*>(maxsq), c->m.nt, c->n_vel,
+                                                  c->n_total, J, JB, c->ec);
+        ENS_CKL();
+        const int64_t tot = 2LL * c->m.ns * (J / 2);
+        k_member_gather<<<dim3((unsigned)((tot + 255) / 256), 2), 256, 0, s>>>(c->m.n2e_ptr, c->m.n2e, c->ec, rhs,
+                                                                             c->m.ns, c->m.nt, c->n_total, J);
+        ENS_CKL();
+        return ENS_OK;
+    }
     const int J = c->J;
     const int JB = J < 128 ? J : 128;
     const int EPB = 128 / JB > 0 ? 128 / JB : 1;
@@ -356,7 +419,7 @@ int launch_member_pass(ens_ctx* c, cudaStream_t s, const double* x, const double
         dim3 grid((ne + EPB - 1) / EPB, (J + JB - 1) / JB);
         k_member_pass<<<grid, threads, shm, s>>>(c->m.e_nodes, c->m.e_geo, e0, ne, x, means, rhs,
                                                   reinterpret_cast<unsigned long long*>(maxsq), c->m.nt, c->n_vel,
-                                                  c->n_total, J, JB);
+                                                  c->n_total, J, JB, nullptr);
         ENS_CKL();
     }
     return ENS_OK;
@@ -421,7 +484,7 @@ int launch_copy_cons(ens_ctx* c, cudaStream_t s, const double* src, double* dst)
 __global__ void k_assemble(const int32_t* __restrict__ enodes, const double* __restrict__ egeo,
                            const int32_t* __restrict__ eslots, int e0, int ne, const double* __restrict__ means,
                            const double* __restrict__ maxsq, double two_mu_dt, double* __restrict__ vals, int nt,
-                           int nvel, int nnz) {
+                           int nvel, int nnz, double* __restrict__ el) {
     const int e = e0 + blockIdx.x * blockDim.x + threadIdx.x;
     if (e >= e0 + ne) return;
     const int mat = blockIdx.y;
@@ -463,6 +526,14 @@ __global__ void k_assemble(const int32_t* __restrict__ enodes, const double* __r
             for (int a = 0; a < 6; ++a) loc[a][b] += tb * c_phi[q][a] + cq * (gx[a] * gx[b] + gy[a] * gy[b]);
         }
     }
+    if (el) {   // element-local buffer [mat][ab][e], gathered per CSR slot by k_assemble_gather
+        double* o = el + (int64_t)mat * 36 * nt + e;
+#pragma unroll
+        for (int a = 0; a < 6; ++a)
+#pragma unroll
+            for (int b = 0; b < 6; ++b) o[(int64_t)(a * 6 + b) * nt] = loc[a][b];
+        return;
+    }
     const int32_t* sl = eslots + (int64_t)e * 36;
 #pragma unroll
     for (int a = 0; a < 6; ++a)
@@ -470,8 +541,39 @@ __global__ void k_assemble(const int32_t* __restrict__ enodes, const double* __r
         for (int b = 0; b < 6; ++b) out[sl[a * 6 + b]] += loc[a][b];
 }
 
+// vals[mat][slot] = base[slot] + sum of the slot's element-local entries (fixed order)
+__global__ void __launch_bounds__(256) k_assemble_gather(const int32_t* __restrict__ s2e_ptr,
+                                                         const int32_t* __restrict__ s2e,
+                                                         const double* __restrict__ el,
+                                                         const double* __restrict__ base, double* __restrict__ vals,
+                                                         int nnz, int nt) {
+    const int sidx = blockIdx.x * blockDim.x + threadIdx.x;
+    if (sidx >= nnz) return;
+    const int mat = blockIdx.y;
+    const double* elm = el + (int64_t)mat * 36 * nt;
+    double acc = base[sidx];
+    const int k0 = s2e_ptr[sidx], k1 = s2e_ptr[sidx + 1];
+    for (int k = k0; k < k1; ++k) acc += elm[s2e[k]];
+    vals[(int64_t)mat * nnz + sidx] = acc;
+}
+
 int launch_assemble(ens_ctx* c, cudaStream_t s, const double* base, const double* means, const double* maxsq,
                     double two_mu_dt, double* as_vals) {
+    if (c->m.s2e) {
+        const size_t elb = sizeof(double) * 2 * 36 * (size_t)c->m.nt;
+        if (!c->el) {
+            ENS_CK(cudaMalloc(&c->el, elb));
+            c->ws_bytes += elb;
+        }
+        dim3 grid((c->m.nt + 127) / 128, 2);
+        k_assemble<<<grid, 128, 0, s>>>(c->m.e_nodes, c->m.e_geo, c->m.e_slots, 0, c->m.nt, means, maxsq, two_mu_dt,
+                                       as_vals, c->m.nt, c->n_vel, c->m.nnz_s, c->el);
+        ENS_CKL();
+        k_assemble_gather<<<dim3((unsigned)((c->m.nnz_s + 255) / 256), 2), 256, 0, s>>>(
+            c->m.s2e_ptr, c->m.s2e, c->el, base, as_vals, c->m.nnz_s, c->m.nt);
+        ENS_CKL();
+        return ENS_OK;
+    }
     const size_t nb = sizeof(double) * (size_t)c->m.nnz_s;
     ENS_CK(cudaMemcpyAsync(as_vals, base, nb, cudaMemcpyDeviceToDevice, s));
     ENS_CK(cudaMemcpyAsync(as_vals + c->m.nnz_s, base, nb, cudaMemcpyDeviceToDevice, s));
@@ -480,7 +582,7 @@ int launch_assemble(ens_ctx* c, cudaStream_t s, const double* base, const double
         if (ne == 0) continue;
         dim3 grid((ne + 127) / 128, 2);
         k_assemble<<<grid, 128, 0, s>>>(c->m.e_nodes, c->m.e_geo, c->m.e_slots, e0, ne, means, maxsq, two_mu_dt,
-                                       as_vals, c->m.nt, c->n_vel, c->m.nnz_s);
+                                       as_vals, c->m.nt, c->n_vel, c->m.nnz_s, nullptr);
         ENS_CKL();
     }
     return ENS_OK;

@@ -140,6 +140,15 @@ class HostMesh:
         b_idx = np.tile(self.e_nodes, (1, 6))
         self.e_slots = self._slot(a_idx.ravel(), b_idx.ravel()).astype(np.int32)
         self.eorder = eorder
+        # gather lists for the scatter-free member pass / assembly (fixed element order)
+        nt = len(self.e_nodes)
+        en = self.e_nodes.ravel()
+        o = np.argsort(en, kind="stable")
+        self.n2e = o.astype(np.int32)                                   # e*6 + a
+        self.n2e_ptr = np.searchsorted(en[o], np.arange(ns + 1)).astype(np.int32)
+        o = np.argsort(self.e_slots, kind="stable")
+        self.s2e = ((o % 36) * nt + o // 36).astype(np.int32)          # ab*nt + e
+        self.s2e_ptr = np.searchsorted(self.e_slots[o], np.arange(self.nnz_s + 1)).astype(np.int32)
         self.pres_int = np.empty(npres)
         self.pres_int[pperm] = disc.pressure_integrals
 
@@ -317,7 +326,8 @@ class Engine:
             e_geo=up(hm.e_geo, torch.float64), e_slots=up(hm.e_slots, i32),
             cons_row=up(hm.cons_row if len(hm.cons_row) else np.zeros(1, np.int32), i32),
             cons_bidx=up(hm.cons_bidx if len(hm.cons_bidx) else np.zeros(1, np.int32), i32),
-            pres_int=up(hm.pres_int, torch.float64))
+            pres_int=up(hm.pres_int, torch.float64), n2e_ptr=up(hm.n2e_ptr, i32), n2e=up(hm.n2e, i32),
+            s2e_ptr=up(hm.s2e_ptr, i32), s2e=up(hm.s2e, i32))
         self.mesh_t = mesh_t
         self._color_off = np.ascontiguousarray(hm.color_off, dtype=np.int32)
         md = N.MeshDesc()
