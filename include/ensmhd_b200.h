@@ -169,6 +169,10 @@ int  ens_set_pivoting(ens_ctx* ctx, int on);
 /* Install the SpMM row blocking (arrays are device pointers owned by the caller). */
 int  ens_set_spmm_blocks(ens_ctx* ctx, const ens_spmm_blocks* blocks);
 
+/* y = a x + b y over one iterate block set (2 x n_total x J); used for the
+ * extrapolated FGMRES initial iterate 2 x^n - x^{n-1}. */
+int  ens_lincomb(ens_ctx* ctx, void* stream, double a, const double* x, double b, double* y);
+
 /* Member sums over the J local columns: sum_v[r] = sum_j Xv[r][j] (r < n_vel), same for w. */
 int  ens_member_sums(ens_ctx* ctx, void* stream, const double* x, double* sums);
 

@@ -61,7 +61,7 @@ class DataDesc(C.Structure):
 SYMBOLS = [
     "ens_abi_version", "ens_last_error", "ens_kernel_launches", "ens_create", "ens_set_pivoting",
     "ens_set_spmm_blocks", "ens_destroy", "ens_workspace_bytes",
-    "ens_member_sums", "ens_rhs", "ens_member_pass", "ens_apply_bc", "ens_assemble", "ens_factor",
+    "ens_lincomb", "ens_member_sums", "ens_rhs", "ens_member_pass", "ens_apply_bc", "ens_assemble", "ens_factor",
     "ens_solve", "ens_spmm", "ens_precond_apply", "ens_epilogue", "ens_diagnostics",
 ]
 
@@ -87,6 +87,7 @@ def load(path: str = LIB_PATH):
     lib.ens_set_pivoting.argtypes = [P, C.c_int]
     lib.ens_set_spmm_blocks.argtypes = [P, C.POINTER(SpmmBlocks)]
     lib.ens_member_sums.argtypes = [P, P, P, P]
+    lib.ens_lincomb.argtypes = [P, P, F64, P, F64, P]
     lib.ens_rhs.argtypes = [P, P, P, P, F64, C.POINTER(DataDesc), P]
     lib.ens_member_pass.argtypes = [P, P, P, P, P, P]
     lib.ens_apply_bc.argtypes = [P, P, C.POINTER(DataDesc), P]

@@ -156,6 +156,11 @@ int ens_workspace_bytes(const ens_ctx* c, int64_t* bytes) {
     return ENS_OK;
 }
 
+int ens_lincomb(ens_ctx* c, void* stream, double a, const double* x, double b, double* y) {
+    if (!c || !x || !y) return ENS_EINVAL;
+    return launch_lincomb(c, (cudaStream_t)stream, a, x, b, y);
+}
+
 int ens_member_sums(ens_ctx* c, void* stream, const double* x, double* sums) {
     if (!c || !x || !sums) return ENS_EINVAL;
     return launch_member_sums(c, (cudaStream_t)stream, x, sums);

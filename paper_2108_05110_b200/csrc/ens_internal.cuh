@@ -81,6 +81,7 @@ struct ens_ctx {
 
 // ---- kernels launchers (ens_kernels.cu) ----
 int launch_member_sums(ens_ctx* c, cudaStream_t s, const double* x, double* sums);
+int launch_lincomb(ens_ctx* c, cudaStream_t s, double a, const double* x, double b, double* y);
 int launch_rhs(ens_ctx* c, cudaStream_t s, const double* x, const double* coef, double inv_dt,
                const ens_data_desc* loads, double* rhs);
 int launch_member_pass(ens_ctx* c, cudaStream_t s, const double* x, const double* means, double* rhs, double* maxsq);

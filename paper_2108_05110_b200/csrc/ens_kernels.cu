@@ -1,3 +1,4 @@
+#include <algorithm>
 // Element, member, right-hand-side, SpMM and reduction kernels (sm_100a, fp64).
 //
 // Layout (see include/ensmhd_b200.h): a field block has n_total rows in the
@@ -96,6 +97,37 @@ __global__ void k_member_sums(const double* __restrict__ X, double* __restrict__
     if (sl == 0) sums[r] = acc;
 }
 
+__global__ void __launch_bounds__(256) k_lincomb2(double a, const double2* __restrict__ x, double b,
+                                                  double2* __restrict__ y, int64_t n2) {
+    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < n2; t += (int64_t)gridDim.x * blockDim.x) {
+        const double2 u = x[t];
+        double2 v = y[t];
+        v.x = a * u.x + b * v.x;
+        v.y = a * u.y + b * v.y;
+        y[t] = v;
+    }
+}
+
+__global__ void __launch_bounds__(256) k_lincomb(double a, const double* __restrict__ x, double b,
+                                                 double* __restrict__ y, int64_t n) {
+    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x)
+        y[t] = a * x[t] + b * y[t];
+}
+
+int launch_lincomb(ens_ctx* c, cudaStream_t s, double a, const double* x, double b, double* y) {
+    const int64_t n = 2LL * c->n_total * c->J;
+    if ((n & 1) == 0 && (reinterpret_cast<uintptr_t>(x) & 15) == 0 && (reinterpret_cast<uintptr_t>(y) & 15) == 0) {
+        const int64_t n2 = n / 2;
+        const unsigned nb = (unsigned)std::min<int64_t>((n2 + 255) / 256, 148 * 16);
+        k_lincomb2<<<nb, 256, 0, s>>>(a, reinterpret_cast<const double2*>(x), b, reinterpret_cast<double2*>(y), n2);
+    } else {
+        const unsigned nb = (unsigned)std::min<int64_t>((n + 255) / 256, 148 * 16);
+        k_lincomb<<<nb, 256, 0, s>>>(a, x, b, y, n);
+    }
+    ENS_CKL();
+    return ENS_OK;
+}
+
 // thread per row (even J): H 16-byte loads, fixed sequential member order
 __global__ void __launch_bounds__(256) k_member_sums2(const double* __restrict__ X, double* __restrict__ sums,
                                                       int nvel, int64_t N, int J) {
@@ -191,8 +223,116 @@ __global__ void k_rhs(const int32_t* __restrict__ rp, const int32_t* __restrict_
     }
 }
 
+// even J: a velocity row's 2J values over L lanes x V2 double2, 32/L rows per warp
+// (as k_spmm_vel_v); mass and stiffness products of both families in one pass
+template <int V2>
+__global__ void __launch_bounds__(256) k_rhs_v(const int32_t* __restrict__ rp, const int32_t* __restrict__ col,
+                                               const double* __restrict__ mass, const double* __restrict__ stiff,
+                                               const double* __restrict__ X, const double* __restrict__ coef,
+                                               double inv_dt, int K, const double* __restrict__ lbasis,
+                                               const double* __restrict__ lcoef, const double* __restrict__ ldense,
+                                               double* __restrict__ rhs, int ns, int64_t N, int J, int L) {
+    const int lane = threadIdx.x & 31;
+    const int R = 32 / L;
+    const int r = lane / L, part = lane - r * L;
+    const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t node = gw * R + r;
+    if (r >= R || node >= ns) return;
+    const int H = J >> 1;
+    const double2* Xv = reinterpret_cast<const double2*>(X);
+    const double2* Xw = reinterpret_cast<const double2*>(X + N * J);
+    double2 mv[V2], kv[V2], mw[V2], kw[V2];
+#pragma unroll
+    for (int v = 0; v < V2; ++v) mv[v] = kv[v] = mw[v] = kw[v] = make_double2(0.0, 0.0);
+    const int k0 = rp[node], k1 = rp[node + 1];
+    int k = k0;
+    for (; k + 2 <= k1; k += 2) {
+        const int64_t q0 = col[k], q1 = col[k + 1];
+        const double a0 = mass[k], b0 = stiff[k], a1 = mass[k + 1], b1 = stiff[k + 1];
+#pragma unroll
+        for (int v = 0; v < V2; ++v) {
+            const int i = V2 * part + v;
+            if (i < J) {
+                const double2 x0 = Xv[q0 * J + i], w0 = Xw[q0 * J + i], x1 = Xv[q1 * J + i], w1 = Xw[q1 * J + i];
+                mv[v].x += a0 * x0.x; mv[v].y += a0 * x0.y; kv[v].x += b0 * x0.x; kv[v].y += b0 * x0.y;
+                mw[v].x += a0 * w0.x; mw[v].y += a0 * w0.y; kw[v].x += b0 * w0.x; kw[v].y += b0 * w0.y;
+                mv[v].x += a1 * x1.x; mv[v].y += a1 * x1.y; kv[v].x += b1 * x1.x; kv[v].y += b1 * x1.y;
+                mw[v].x += a1 * w1.x; mw[v].y += a1 * w1.y; kw[v].x += b1 * w1.x; kw[v].y += b1 * w1.y;
+            }
+        }
+    }
+    for (; k < k1; ++k) {
+        const int64_t q0 = col[k];
+        const double a0 = mass[k], b0 = stiff[k];
+#pragma unroll
+        for (int v = 0; v < V2; ++v) {
+            const int i = V2 * part + v;
+            if (i < J) {
+                const double2 x0 = Xv[q0 * J + i], w0 = Xw[q0 * J + i];
+                mv[v].x += a0 * x0.x; mv[v].y += a0 * x0.y; kv[v].x += b0 * x0.x; kv[v].y += b0 * x0.y;
+                mw[v].x += a0 * w0.x; mw[v].y += a0 * w0.y; kw[v].x += b0 * w0.x; kw[v].y += b0 * w0.y;
+            }
+        }
+    }
+    const int64_t nvel = 2LL * ns;
+#pragma unroll
+    for (int v = 0; v < V2; ++v) {
+        const int i = V2 * part + v;
+        if (i >= J) continue;
+        const int cc = i >= H ? 1 : 0;
+        const int64_t row = 2 * node + cc;
+        double ov[2], ow[2];
+        const double mvv[2] = {mv[v].x, mv[v].y}, kvv[2] = {kv[v].x, kv[v].y};
+        const double mww[2] = {mw[v].x, mw[v].y}, kww[2] = {kw[v].x, kw[v].y};
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+            const int j = 2 * (i - cc * H) + e;
+            const double ls = coef[j], lc = coef[J + j];
+            double lv = 0.0, lw = 0.0;
+            for (int kk = 0; kk < K; ++kk) {
+                const double bval = lbasis[(int64_t)kk * nvel + row];
+                lv += lcoef[(int64_t)kk * J + j] * bval;
+                lw += lcoef[(int64_t)(K + kk) * J + j] * bval;
+            }
+            if (ldense) {
+                lv += ldense[row * J + j];
+                lw += ldense[nvel * J + row * J + j];
+            }
+            ov[e] = (mvv[e] * inv_dt - ls * kvv[e] - lc * kww[e]) + lv;
+            ow[e] = (mww[e] * inv_dt - ls * kww[e] - lc * kvv[e]) + lw;
+        }
+        reinterpret_cast<double2*>(rhs)[node * J + i] = make_double2(ov[0], ov[1]);
+        reinterpret_cast<double2*>(rhs + N * J)[node * J + i] = make_double2(ow[0], ow[1]);
+    }
+}
+
 int launch_rhs(ens_ctx* c, cudaStream_t s, const double* x, const double* coef, double inv_dt,
                const ens_data_desc* loads, double* rhs) {
+    if ((c->J & 1) == 0 && c->J <= 512 && (reinterpret_cast<uintptr_t>(x) & 15) == 0 &&
+        (reinterpret_cast<uintptr_t>(rhs) & 15) == 0) {
+        const int J = c->J;
+        const int64_t N = c->n_total;
+        for (int mat = 0; mat < 2; ++mat)
+            ENS_CK(cudaMemsetAsync(rhs + mat * N * J + (int64_t)c->n_vel * J, 0,
+                                   sizeof(double) * (size_t)c->m.n_pres * J, s));
+        const int V2 = J <= 64 ? 2 : (J <= 128 ? 4 : 8);
+        const int L = (J + V2 - 1) / V2, R = 32 / L;
+        const int64_t warps = ((int64_t)c->m.ns + R - 1) / R;
+        const unsigned blocks = (unsigned)((warps * 32 + 255) / 256);
+        const int K = loads ? loads->K : 0;
+        const double* lb = loads ? loads->basis : nullptr;
+        const double* lc = loads ? loads->coef : nullptr;
+        const double* ld = loads ? loads->dense : nullptr;
+#define RHV(V)                                                                                                    \
+    k_rhs_v<V><<<blocks, 256, 0, s>>>(c->m.s_rowptr, c->m.s_col, c->m.s_mass, c->m.s_stiff, x, coef, inv_dt, K, lb, \
+                                      lc, ld, rhs, c->m.ns, N, J, L)
+        if (V2 == 2) RHV(2);
+        else if (V2 == 4) RHV(4);
+        else RHV(8);
+#undef RHV
+        ENS_CKL();
+        return ENS_OK;
+    }
     const int J = c->J, W2 = 2 * J;
     const int S = W2 >= 32 ? 32 : next_pow2(W2);
     const int opl = (W2 + S - 1) / S;

@@ -635,7 +635,7 @@ class Engine:
         self._retire(nxt)
         Xn = self.X[nxt]
         if self.guess == "extrapolate" and self.prev_valid:
-            Xn.neg_().add_(X, alpha=2.0)              # 2 x^n - x^{n-1} (Xn holds level n-1)
+            N.check(lib.ens_lincomb(ctx, s, 2.0, _dptr(X), -1.0, _dptr(Xn)), "ens_lincomb")   # 2 x^n - x^{n-1}
         else:
             Xn.copy_(X)                               # warm start from level n
         code, iters, rel = self._solve(Xn)
