@@ -155,91 +155,65 @@ __global__ void __launch_bounds__(256) k_spmm_vel_v(const int32_t* __restrict__ 
                                                     const double* __restrict__ btv, const uint8_t* __restrict__ cflag,
                                                     const double* __restrict__ X, const double* __restrict__ Bv,
                                                     double* __restrict__ Y, int ns, int64_t N, int J, int L, int mode) {
+    // both systems per thread: one index stream feeds two independent gathers
     const int lane = threadIdx.x & 31;
     const int R = 32 / L;
     const int r = lane / L, part = lane - r * L;
     const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int64_t node = gw * R + r;
     if (r >= R || node >= ns) return;
-    const int mat = blockIdx.y;
     const int H = J >> 1;                       // double2 per component
-    const double* Am = A + (int64_t)mat * nnz;
-    const double2* X2 = reinterpret_cast<const double2*>(X + (int64_t)mat * N * J);
-    double2* Y2 = reinterpret_cast<double2*>(Y + (int64_t)mat * N * J);
-    const double2* B2 = reinterpret_cast<const double2*>(Bv + (int64_t)mat * N * J);
+    const int64_t MS = N * H;                   // double2 per system block
+    const double2* X2 = reinterpret_cast<const double2*>(X);
+    double2* Y2 = reinterpret_cast<double2*>(Y);
+    const double2* B2 = reinterpret_cast<const double2*>(Bv);
     const int64_t nvel = 2LL * ns;
-    // epilogue operands first (independent of the row sum)
-    double2 self[V2], bval[V2];
-    bool ident[V2];
+    double2 acc[2][V2];
 #pragma unroll
-    for (int v = 0; v < V2; ++v) {
-        const int i = V2 * part + v;
-        const int ic = i < J ? i : 0;
-        const int64_t o = node * J + ic;
-        self[v] = X2[o];
-        bval[v] = mode == 1 ? B2[o] : make_double2(0.0, 0.0);
-        ident[v] = cflag[2 * node + (ic >= H ? 1 : 0)] != 0;
-    }
-    double2 acc[V2];
+    for (int m = 0; m < 2; ++m)
 #pragma unroll
-    for (int v = 0; v < V2; ++v) acc[v] = make_double2(0.0, 0.0);
+        for (int v = 0; v < V2; ++v) acc[m][v] = make_double2(0.0, 0.0);
     const int k0 = rp[node], k1 = rp[node + 1];
     int k = k0;
-    for (; k + 4 <= k1; k += 4) {
-        const int64_t c0 = col[k], c1 = col[k + 1], c2 = col[k + 2], c3 = col[k + 3];
-        const double a0 = Am[k], a1 = Am[k + 1], a2 = Am[k + 2], a3 = Am[k + 3];
+    for (; k + 2 <= k1; k += 2) {
+        const int64_t c0 = col[k], c1 = col[k + 1];
+        const double a00 = A[k], a01 = A[k + 1], a10 = A[nnz + k], a11 = A[nnz + k + 1];
 #pragma unroll
         for (int v = 0; v < V2; ++v) {
             const int i = V2 * part + v;
             if (i < J) {
-                const double2 x0 = X2[c0 * J + i], x1 = X2[c1 * J + i], x2 = X2[c2 * J + i], x3 = X2[c3 * J + i];
-                acc[v].x = fma(a0, x0.x, acc[v].x);
-                acc[v].y = fma(a0, x0.y, acc[v].y);
-                acc[v].x = fma(a1, x1.x, acc[v].x);
-                acc[v].y = fma(a1, x1.y, acc[v].y);
-                acc[v].x = fma(a2, x2.x, acc[v].x);
-                acc[v].y = fma(a2, x2.y, acc[v].y);
-                acc[v].x = fma(a3, x3.x, acc[v].x);
-                acc[v].y = fma(a3, x3.y, acc[v].y);
+                const double2 x00 = X2[c0 * J + i], x01 = X2[c1 * J + i];
+                const double2 x10 = X2[MS + c0 * J + i], x11 = X2[MS + c1 * J + i];
+                acc[0][v].x = fma(a00, x00.x, acc[0][v].x);
+                acc[0][v].y = fma(a00, x00.y, acc[0][v].y);
+                acc[1][v].x = fma(a10, x10.x, acc[1][v].x);
+                acc[1][v].y = fma(a10, x10.y, acc[1][v].y);
+                acc[0][v].x = fma(a01, x01.x, acc[0][v].x);
+                acc[0][v].y = fma(a01, x01.y, acc[0][v].y);
+                acc[1][v].x = fma(a11, x11.x, acc[1][v].x);
+                acc[1][v].y = fma(a11, x11.y, acc[1][v].y);
             }
         }
     }
     for (; k < k1; ++k) {
         const int64_t c0 = col[k];
-        const double a0 = Am[k];
+        const double a00 = A[k], a10 = A[nnz + k];
 #pragma unroll
         for (int v = 0; v < V2; ++v) {
             const int i = V2 * part + v;
             if (i < J) {
-                const double2 x0 = X2[c0 * J + i];
-                acc[v].x = fma(a0, x0.x, acc[v].x);
-                acc[v].y = fma(a0, x0.y, acc[v].y);
+                const double2 x00 = X2[c0 * J + i], x10 = X2[MS + c0 * J + i];
+                acc[0][v].x = fma(a00, x00.x, acc[0][v].x);
+                acc[0][v].y = fma(a00, x00.y, acc[0][v].y);
+                acc[1][v].x = fma(a10, x10.x, acc[1][v].x);
+                acc[1][v].y = fma(a10, x10.y, acc[1][v].y);
             }
         }
     }
-    // pressure couplings: pressure rows are J wide (H double2) at row nvel + p
+    // pressure couplings (same B^T for both systems): pressure rows are J wide at row nvel + p
     const int t0 = btp[node], t1 = btp[node + 1];
     const double2* P2 = X2 + nvel * H;
-    int t = t0;
-    for (; t + 2 <= t1; t += 2) {
-        const double2 b0 = reinterpret_cast<const double2*>(btv)[t], b1 = reinterpret_cast<const double2*>(btv)[t + 1];
-        const int64_t p0 = btc[t], p1 = btc[t + 1];
-#pragma unroll
-        for (int v = 0; v < V2; ++v) {
-            const int i = V2 * part + v;
-            if (i < J) {
-                const bool ycomp = i >= H;
-                const int ip = ycomp ? i - H : i;
-                const double2 x0 = P2[p0 * H + ip], x1 = P2[p1 * H + ip];
-                const double f0 = ycomp ? b0.y : b0.x, f1 = ycomp ? b1.y : b1.x;
-                acc[v].x -= f0 * x0.x;
-                acc[v].y -= f0 * x0.y;
-                acc[v].x -= f1 * x1.x;
-                acc[v].y -= f1 * x1.y;
-            }
-        }
-    }
-    for (; t < t1; ++t) {
+    for (int t = t0; t < t1; ++t) {
         const double2 b0 = reinterpret_cast<const double2*>(btv)[t];
         const int64_t p0 = btc[t];
 #pragma unroll
@@ -247,10 +221,13 @@ __global__ void __launch_bounds__(256) k_spmm_vel_v(const int32_t* __restrict__ 
             const int i = V2 * part + v;
             if (i < J) {
                 const bool ycomp = i >= H;
-                const double2 x0 = P2[p0 * H + (ycomp ? i - H : i)];
+                const int64_t o = p0 * H + (ycomp ? i - H : i);
+                const double2 x0 = P2[o], x1 = P2[MS + o];
                 const double f0 = ycomp ? b0.y : b0.x;
-                acc[v].x -= f0 * x0.x;
-                acc[v].y -= f0 * x0.y;
+                acc[0][v].x -= f0 * x0.x;
+                acc[0][v].y -= f0 * x0.y;
+                acc[1][v].x -= f0 * x1.x;
+                acc[1][v].y -= f0 * x1.y;
             }
         }
     }
@@ -258,9 +235,17 @@ __global__ void __launch_bounds__(256) k_spmm_vel_v(const int32_t* __restrict__ 
     for (int v = 0; v < V2; ++v) {
         const int i = V2 * part + v;
         if (i >= J) continue;
-        double2 val = ident[v] ? self[v] : acc[v];
-        if (mode == 1) val = make_double2(bval[v].x - val.x, bval[v].y - val.y);
-        Y2[node * J + i] = val;
+        const int64_t o = node * J + i;
+        const bool ident = cflag[2 * node + (i >= H ? 1 : 0)] != 0;
+#pragma unroll
+        for (int m = 0; m < 2; ++m) {
+            double2 val = ident ? X2[m * MS + o] : acc[m][v];
+            if (mode == 1) {
+                const double2 bb = B2[m * MS + o];
+                val = make_double2(bb.x - val.x, bb.y - val.y);
+            }
+            Y2[m * MS + o] = val;
+        }
     }
 }
 
@@ -276,60 +261,49 @@ __global__ void __launch_bounds__(256) k_spmm_pres_v(const int32_t* __restrict__
     const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int64_t p = gw * R + r;
     if (r >= R || p >= npres) return;
-    const int mat = blockIdx.y;
     const int H = J >> 1;
-    const double2* X2 = reinterpret_cast<const double2*>(X + (int64_t)mat * N * J);
-    double2* Y2 = reinterpret_cast<double2*>(Y + (int64_t)mat * N * J);
-    const double2* B2 = reinterpret_cast<const double2*>(Bv + (int64_t)mat * N * J);
+    const int64_t MS = N * H;
+    const double2* X2 = reinterpret_cast<const double2*>(X);
+    double2* Y2 = reinterpret_cast<double2*>(Y);
+    const double2* B2 = reinterpret_cast<const double2*>(Bv);
     const int64_t row = nvel + p;
-    const bool ident = cflag[row] != 0;
-    double2 self[V2], bval[V2], acc[V2];
+    double2 acc[2][V2];
 #pragma unroll
-    for (int v = 0; v < V2; ++v) {
-        const int i = V2 * part + v;
-        const int64_t o = row * H + (i < H ? i : 0);
-        self[v] = X2[o];
-        bval[v] = mode == 1 ? B2[o] : make_double2(0.0, 0.0);
-        acc[v] = make_double2(0.0, 0.0);
-    }
+    for (int m = 0; m < 2; ++m)
+#pragma unroll
+        for (int v = 0; v < V2; ++v) acc[m][v] = make_double2(0.0, 0.0);
     const int t0 = bp[p], t1 = bp[p + 1];
-    int t = t0;
-    for (; t + 2 <= t1; t += 2) {
-        const double2 b0 = reinterpret_cast<const double2*>(bv)[t], b1 = reinterpret_cast<const double2*>(bv)[t + 1];
-        const int64_t n0 = bc[t], n1 = bc[t + 1];
-#pragma unroll
-        for (int v = 0; v < V2; ++v) {
-            const int i = V2 * part + v;
-            if (i < H) {
-                const double2 u0 = X2[n0 * J + i], w0 = X2[n0 * J + H + i];
-                const double2 u1 = X2[n1 * J + i], w1 = X2[n1 * J + H + i];
-                acc[v].x += b0.x * u0.x + b0.y * w0.x;
-                acc[v].y += b0.x * u0.y + b0.y * w0.y;
-                acc[v].x += b1.x * u1.x + b1.y * w1.x;
-                acc[v].y += b1.x * u1.y + b1.y * w1.y;
-            }
-        }
-    }
-    for (; t < t1; ++t) {
+    for (int t = t0; t < t1; ++t) {
         const double2 b0 = reinterpret_cast<const double2*>(bv)[t];
         const int64_t n0 = bc[t];
 #pragma unroll
         for (int v = 0; v < V2; ++v) {
             const int i = V2 * part + v;
             if (i < H) {
-                const double2 u0 = X2[n0 * J + i], w0 = X2[n0 * J + H + i];
-                acc[v].x += b0.x * u0.x + b0.y * w0.x;
-                acc[v].y += b0.x * u0.y + b0.y * w0.y;
+#pragma unroll
+                for (int m = 0; m < 2; ++m) {
+                    const double2 u0 = X2[m * MS + n0 * J + i], w0 = X2[m * MS + n0 * J + H + i];
+                    acc[m][v].x += b0.x * u0.x + b0.y * w0.x;
+                    acc[m][v].y += b0.x * u0.y + b0.y * w0.y;
+                }
             }
         }
     }
+    const bool ident = cflag[row] != 0;
 #pragma unroll
     for (int v = 0; v < V2; ++v) {
         const int i = V2 * part + v;
         if (i >= H) continue;
-        double2 val = ident ? self[v] : acc[v];
-        if (mode == 1) val = make_double2(bval[v].x - val.x, bval[v].y - val.y);
-        Y2[row * H + i] = val;
+#pragma unroll
+        for (int m = 0; m < 2; ++m) {
+            const int64_t o = m * MS + row * H + i;
+            double2 val = ident ? X2[o] : acc[m][v];
+            if (mode == 1) {
+                const double2 bb = B2[o];
+                val = make_double2(bb.x - val.x, bb.y - val.y);
+            }
+            Y2[o] = val;
+        }
     }
 }
 
@@ -340,7 +314,7 @@ static int launch_spmm_vec(ens_ctx* c, cudaStream_t s, const double* as_vals, co
         const int V2 = J <= 64 ? 2 : (J <= 128 ? 4 : 8);
         const int L = (J + V2 - 1) / V2, R = 32 / L;
         const int64_t warps = ((int64_t)c->m.ns + R - 1) / R;
-        dim3 grid((unsigned)((warps * 32 + 255) / 256), 2);
+        dim3 grid((unsigned)((warps * 32 + 255) / 256), 1);
 #define SPV(V)                                                                                                      \
     k_spmm_vel_v<V><<<grid, 256, 0, s>>>(c->m.s_rowptr, c->m.s_col, as_vals, c->m.nnz_s, c->m.bt_rowptr, c->m.bt_col, \
                                          c->m.bt_val, c->m.cflag, x, b ? b : x, y, c->m.ns, c->n_total, J, L, mode)
@@ -355,7 +329,7 @@ static int launch_spmm_vec(ens_ctx* c, cudaStream_t s, const double* as_vals, co
         const int V2 = H <= 64 ? 2 : (H <= 128 ? 4 : 8);
         const int L = (H + V2 - 1) / V2, R = 32 / L;
         const int64_t warps = ((int64_t)c->m.n_pres + R - 1) / R;
-        dim3 grid((unsigned)((warps * 32 + 255) / 256), 2);
+        dim3 grid((unsigned)((warps * 32 + 255) / 256), 1);
 #define SPP(V)                                                                                                      \
     k_spmm_pres_v<V><<<grid, 256, 0, s>>>(c->m.b_rowptr, c->m.b_col, c->m.b_val, c->m.cflag, x, b ? b : x, y,        \
                                           c->m.n_pres, c->n_vel, c->n_total, J, L, mode)
