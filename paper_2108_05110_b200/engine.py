@@ -268,9 +268,8 @@ class DeviceState:
             return self._host[name]
         if not self.valid:
             raise RuntimeError("device state was overwritten before it was read")
-        arr = self.engine.field_to_host(self.buf, name)
-        self._host[name] = arr
-        return arr
+        self._host.update(self.engine.fields_to_host(self.buf))   # all four fields, one sync
+        return self._host[name]
 
 
 class Engine:
@@ -450,62 +449,103 @@ class Engine:
         if getattr(self, "_stg", None) is None:
             hm, J, d = self.hm, self.J, self.dev
             self._stg = dict(
-                h_vel=torch.empty(2, J, self.nvel, dtype=torch.float64, pin_memory=True),
-                h_pres=torch.empty(2, J, self.npres, dtype=torch.float64, pin_memory=True),
                 d_vel=torch.empty(2, J, self.nvel, dtype=torch.float64, device=d),
                 d_pres=torch.empty(2, J, self.npres, dtype=torch.float64, device=d),
+                x_in=torch.empty(2, self.ntot, J, dtype=torch.float64, device=d),
+                t_vel=torch.empty(self.nvel, J, dtype=torch.float64, device=d),
+                t_pres=torch.empty(self.npres, J, dtype=torch.float64, device=d),
                 ref_of_int_v=torch.as_tensor(hm.ref_of_int[:self.nvel]).to(d),
                 ref_of_int_p=torch.as_tensor(hm.ref_of_int[self.nvel:] - self.nvel).to(d),
                 int_of_ref_v=torch.as_tensor(hm.int_id[:self.nvel]).to(d),
                 int_of_ref_p=torch.as_tensor(hm.int_id[self.nvel:] - self.nvel).to(d))
         return self._stg
 
+    @staticmethod
+    def _host_tensor(a):
+        """torch view of a (J, n) float64 host array (no copy when already contiguous float64)."""
+        arr = np.ascontiguousarray(np.asarray(a, dtype=np.float64))
+        return torch.from_numpy(arr)
+
     def load_state(self, v, w, q, r):
         """Upload a host state (reference layout, this rank's members) into the current buffer set.
 
-        Pinned H2D copies of the (J, n) arrays; the member-minor transpose and
-        the internal dof permutation run on the device.
+        H2D copies of the (J, n) arrays -- straight from the caller's buffers
+        when they are pinned (e.g. the arrays a previous step returned), else
+        from pageable memory -- then the member-minor transpose and the internal
+        dof permutation on the device.  When the uploaded state equals the one
+        already resident in the current buffer set (a caller passing a step's
+        output straight back in), the resident trajectory is kept, so the
+        extrapolated initial iterate stays available.
         """
         g = self._staging()
-        self._retire(self.cur)
-        X = self.X[self.cur]
         s = self.stream
-        np.copyto(g["h_vel"][0].numpy(), np.asarray(v, dtype=float))
-        np.copyto(g["h_vel"][1].numpy(), np.asarray(w, dtype=float))
+        nv = self.nvel
+        hv, hw = self._host_tensor(v), self._host_tensor(w)
+        has_p = q is not None and np.asarray(q).size > 0
         with torch.cuda.stream(s):
-            g["d_vel"].copy_(g["h_vel"], non_blocking=True)
+            g["d_vel"][0].copy_(hv, non_blocking=hv.is_pinned())
+            g["d_vel"][1].copy_(hw, non_blocking=hw.is_pinned())
+            Xs = g["x_in"]
             for m in range(2):
-                X[m, :self.nvel] = g["d_vel"][m].t().index_select(0, g["ref_of_int_v"])
-            if q is not None and np.asarray(q).size:
-                np.copyto(g["h_pres"][0].numpy(), np.asarray(q, dtype=float))
-                np.copyto(g["h_pres"][1].numpy(), np.asarray(r, dtype=float))
-                g["d_pres"].copy_(g["h_pres"], non_blocking=True)
+                torch.index_select(g["d_vel"][m].t(), 0, g["ref_of_int_v"], out=Xs[m, :nv])
+            if has_p:
+                hq, hr = self._host_tensor(q), self._host_tensor(r)
+                g["d_pres"][0].copy_(hq, non_blocking=hq.is_pinned())
+                g["d_pres"][1].copy_(hr, non_blocking=hr.is_pinned())
                 for m in range(2):
-                    X[m, self.nvel:] = g["d_pres"][m].t().index_select(0, g["ref_of_int_p"])
-                self.Pq[self.cur].copy_(X[:, self.nvel:])
+                    torch.index_select(g["d_pres"][m].t(), 0, g["ref_of_int_p"], out=Xs[m, nv:])
             else:
-                X[:, self.nvel:] = 0.0
-                self.Pq[self.cur].zero_()
-        s.synchronize()          # staging buffers are reused by the next upload
-        self.gen[self.cur] += 1
+                Xs[:, nv:] = 0.0
+            cur = self.cur
+            same = (self.gen[cur] > 0 and torch.equal(Xs[:, :nv], self.X[cur][:, :nv])
+                    and torch.equal(Xs[:, nv:], self.Pq[cur]))
+        keep = (hv, hw) + ((hq, hr) if has_p else ())
+        if same:
+            s.synchronize()      # caller buffers may be reused once we return
+            del keep
+            return
+        self._retire(cur)
+        with torch.cuda.stream(s):
+            self.X[cur].copy_(Xs)
+            self.Pq[cur].copy_(Xs[:, nv:])
+        s.synchronize()
+        del keep
+        self.gen[cur] += 1
         self.means_valid = False
         self.prev_valid = False
 
-    def field_to_host(self, buf, name):
-        """(J, n) reference-layout numpy copy of one field of buffer set ``buf``."""
+    def fields_to_host(self, buf):
+        """{v, w, q, r}: (J, n) reference-layout numpy arrays of buffer set ``buf``.
+
+        One device transpose per field, D2H straight into freshly allocated
+        pinned buffers (the returned arrays are views of them -- no host copy,
+        and a later upload of the same arrays is a direct DMA), one sync.
+        """
         g = self._staging()
         s = self.stream
-        m = 0 if name in "vq" else 1
+        J, nv, npr = self.J, self.nvel, self.npres
+        out = {}
         with torch.cuda.stream(s):
-            if name in "vw":
-                dst, hst = g["d_vel"][m], g["h_vel"][m]
-                dst.copy_(self.X[buf][m, :self.nvel].index_select(0, g["int_of_ref_v"]).t())
-            else:
-                dst, hst = g["d_pres"][m], g["h_pres"][m]
-                dst.copy_(self.Pq[buf][m].index_select(0, g["int_of_ref_p"]).t())
-            hst.copy_(dst, non_blocking=True)
+            for m, name in ((0, "v"), (1, "w")):
+                dst = g["d_vel"][m]
+                torch.index_select(self.X[buf][m, :nv], 0, g["int_of_ref_v"], out=g["t_vel"])
+                dst.copy_(g["t_vel"].t())
+                h = torch.empty(J, nv, dtype=torch.float64, pin_memory=True)
+                h.copy_(dst, non_blocking=True)
+                out[name] = h
+            for m, name in ((0, "q"), (1, "r")):
+                dst = g["d_pres"][m]
+                torch.index_select(self.Pq[buf][m], 0, g["int_of_ref_p"], out=g["t_pres"])
+                dst.copy_(g["t_pres"].t())
+                h = torch.empty(J, npr, dtype=torch.float64, pin_memory=True)
+                h.copy_(dst, non_blocking=True)
+                out[name] = h
         s.synchronize()
-        return hst.numpy().copy()
+        return {k: t.numpy() for k, t in out.items()}
+
+    def field_to_host(self, buf, name):
+        """(J, n) reference-layout numpy copy of one field of buffer set ``buf``."""
+        return self.fields_to_host(buf)[name]
 
     def state_handle(self):
         h = DeviceState(self, self.cur, self.gen[self.cur], self.J)
