@@ -62,6 +62,7 @@ struct ens_ctx {
     double* partial = nullptr;     // split-K partial products of the solve GEMMs
     int* ticket = nullptr;         // split-K arrival counters (last CTA reduces)
     int4* sitem = nullptr;         // solve work items with their front's geometry (3 x int4 per item)
+    void* df = nullptr;            // dataflow solve plan (ens_mfsolve_df.cu)
     double* ec = nullptr;          // member-pass element buffer [2][nt][6][2][J]
     double* el = nullptr;          // assembly element buffer [2][36][nt]
     int32_t* finit_rows = nullptr; // per level: front rows k_finit assembles (bit 31: pivot row)
@@ -107,6 +108,11 @@ int launch_axpy_norm(ens_ctx* c, cudaStream_t s, double* W, const double* V, int
 int mf_factor(ens_ctx* c, cudaStream_t s, const double* as_vals, int32_t* n_pert);
 int mf_solve(ens_ctx* c, cudaStream_t s, const double* r, double* z);
 int mf_setup(ens_ctx* c);
+bool df_enabled(const ens_ctx* c);
+int df_build(ens_ctx* c, cudaStream_t s);
+void df_free(ens_ctx* c);
+int df_solve_launches(ens_ctx* c, cudaStream_t s, const void* io, int64_t* nlaunch);
+int df_error(ens_ctx* c);
 
 // ---- Krylov (ens_krylov.cu) ----
 int gmres_solve(ens_ctx* c, cudaStream_t s, const double* as_vals, const double* rhs, double* x, double rtol,

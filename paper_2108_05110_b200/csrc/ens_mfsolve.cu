@@ -56,7 +56,9 @@ __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wai
 
 #define SG_R 64     // rows per CTA (= symbolic.SOLVE_ROWS)
 #define SG_C 32     // member columns per CTA
-#define SG_KMAX 512 // max inner range per work item (>= symbolic.SPLIT_K)
+#ifndef SG_KMAX
+#define SG_KMAX 256 // max inner range per work item (>= the plan's split lengths)
+#endif
 #define SG_KC 32    // inner chunk of the pipelined mainloop
 #define SG_LDA 36   // A stage row stride (= 4 mod 16: conflict-free fragment reads)
 #define SG_STAGE (SG_R * SG_LDA + SG_KC * 36)   // doubles per pipeline stage (A + B)
@@ -193,8 +195,11 @@ __device__ __forceinline__ void cp_async_wait_n(int n) {
 // runs on the fp64 tensor cores (mma.sync m8n8k4, warp w owns rows 8w..8w+7).
 //   forward : B = fr[P] rows (assembled by k_finit), C rows fr[C] -= A B
 //   backward: B = [fr[P]; x[C]] rows,                x[P] = -A B
+#ifndef SG_MINB
+#define SG_MINB 3
+#endif
 template <int NCT>
-__global__ void __launch_bounds__(SG_T, 3) k_sgemm(MfDev d, const int4* __restrict__ sitem, int item0,
+__global__ void __launch_bounds__(SG_T, SG_MINB) k_sgemm(MfDev d, const int4* __restrict__ sitem, int item0,
                                                 const double* __restrict__ F, double* __restrict__ FR,
                                                 const SolveIO* __restrict__ io, int64_t N, int J, int64_t nidx,
                                                 int bwd, int split_k, int nstage, double* __restrict__ partial,
@@ -298,7 +303,9 @@ __global__ void __launch_bounds__(SG_T, 3) k_sgemm(MfDev d, const int4* __restri
         const double* ap = As + row * SG_LDA + q;
         const double* bp = As + SG_R * SG_LDA + q * SG_LDB + g;
         const int ksteps = (min(SG_KC, kc - c * SG_KC) + 3) >> 2;
-        if (ksteps == SG_KC / 4) {
+        if (8 * warp >= nr) {
+            // no valid row in this warp: skip the tensor-core work (barriers above/below still hit)
+        } else if (ksteps == SG_KC / 4) {
 #pragma unroll
             for (int u = 0; u < SG_KC / 4; ++u) {
                 const double av = ap[4 * u];
@@ -407,7 +414,6 @@ static int mf_solve_launches(ens_ctx* c, cudaStream_t s, SolveIO* io, int64_t* n
     const int J = c->J;
     const int64_t N = c->n_total, nidx = c->p.n_idx;
     const unsigned zc = (unsigned)((J + SG_C - 1) / SG_C);
-    const int sk = c->p.split_k;
     const int64_t nslot = c->p.n_slot;
     int64_t cnt = 0;
     if (c->m.ncons > 0) {
@@ -432,6 +438,11 @@ static int mf_solve_launches(ens_ctx* c, cudaStream_t s, SolveIO* io, int64_t* n
         lab.push_back(std::string(tag) + " n=" + std::to_string(a) + " kmax=" + std::to_string(b2));
     };
     mark("start", 0, 0);
+    if (df_enabled(c)) {   // dataflow path: one persistent launch per sweep
+        const int rc = df_solve_launches(c, s, io, &cnt);
+        if (rc != ENS_OK) return rc;
+        mark("dataflow fwd+bwd", 2, 0);
+    } else
     for (const std::vector<int64_t>* sched : {&c->sched_fwd, &c->sched_bwd}) {
         const int64_t nrow = (int64_t)sched->size() / 5;
         for (int64_t i = 0; i < nrow; ++i) {
@@ -463,7 +474,7 @@ static int mf_solve_launches(ens_ctx* c, cudaStream_t s, SolveIO* io, int64_t* n
                 const int zfull = J / SG_C, rem = J - zfull * SG_C;
 #define SGL(NC, ZN, Z0)                                                                                        \
     k_sgemm<NC><<<dim3(n, 2, ZN), SG_T, sg_smem(nst), s>>>(d, c->sitem, off, c->fronts, c->frvec, io, N, J, nidx, \
-                                                          op == SOP_BGEMM, sk, nst, c->partial, c->ticket, nslot, Z0)
+                                                          op == SOP_BGEMM, kmax, nst, c->partial, c->ticket, nslot, Z0)
                 if (zfull > 0) {
                     SGL(4, (unsigned)zfull, 0);
                     ENS_CKL();
@@ -561,6 +572,10 @@ int mf_solve(ens_ctx* c, cudaStream_t s, const double* r, double* z) {
         ENS_CK(cudaStreamSynchronize(s));
         cudaFree(d_hasch);
         c->ws_bytes += pbytes + tbytes + sizeof(int4) * 3 * (size_t)nw + sizeof(int32_t) * (size_t)nidx;
+        if (df_enabled(c)) {   // task lists are built before any graph capture
+            const int rc = df_build(c, s);
+            if (rc != ENS_OK) return rc;
+        }
     }
     SolveIO* io = (SolveIO*)c->solve_io;
     k_set_io<<<1, 1, 0, s>>>(io, r, z);

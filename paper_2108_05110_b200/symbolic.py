@@ -39,7 +39,7 @@ import scipy.sparse as sp
 
 PW = 64          # panel width (max pivots per diagonal block)
 TILE = 64        # GEMM tile edge in the numeric kernels
-LEAF_NODES = 24  # stop dissecting below this many P2 nodes
+LEAF_NODES = int(__import__("os").environ.get("ENS_LEAF", "24"))  # stop dissecting below this many P2 nodes
 
 
 # ----------------------------------------------------------------------
@@ -404,7 +404,28 @@ def analyse(disc, leaf=LEAF_NODES, pw=PW):
 # op codes (must match csrc/mf.cu)
 OP_ZERO, OP_ORIG, OP_EXTADD, OP_DIAG, OP_HPANEL, OP_UPDATE, OP_GPANEL = range(7)
 SOP_FINIT, SOP_FEXT, SOP_FGEMM, SOP_BGATHER, SOP_BGEMM, SOP_FRED, SOP_BRED = range(7)
-SPLIT_K = int(__import__("os").environ.get("ENS_SPLIT_K", "256"))  # inner length per solve-GEMM work item
+# inner length per solve-GEMM work item: 0 = chosen per level (see _choose_split),
+# else a fixed length for every level (tests, experiments: ENS_SPLIT_K)
+SPLIT_K = int(__import__("os").environ.get("ENS_SPLIT_K", "256"))
+SPLIT_CANDIDATES = (64, 128, 192, 256, 384, 512)
+# per-level launch model of the solve GEMM (measured on B200 at C2): resident CTAs,
+# fixed CTA latency, per-32-column chunk time, extra latency of a split group's reduction
+_SLOTS, _T0, _TCHUNK, _TRED = 3 * 148, 3.5, 1.1, 3.0
+
+
+def _choose_split(Ks, rows):
+    """Inner split minimising waves x CTA latency for one level (both systems)."""
+    if SPLIT_K > 0:
+        return SPLIT_K
+    best, best_t = SPLIT_CANDIDATES[-1], None
+    kmax = max(Ks) if len(Ks) else 1
+    for s_ in SPLIT_CANDIDATES:
+        ncta = 2 * sum(-(-r // SOLVE_ROWS) * max(1, -(-K // s_)) for K, r in zip(Ks, rows))
+        waves = -(-ncta // _SLOTS)
+        t = waves * (_T0 + _TCHUNK * -(-min(kmax, s_) // 32) + (_TRED if kmax > s_ else 0.0))
+        if best_t is None or t < best_t - 1e-9:
+            best, best_t = s_, t
+    return best
 MAX_GSRC = 4      # child contribution rows gathered per front-vector row
 EXT_ROWS = 8      # child-CB rows per extend-add work item
 VEC_ROWS = 64     # front-vector rows per init/gather/scatter work item
@@ -491,17 +512,21 @@ def build_schedule(plan: FactorPlan, pw=PW):
     #   order (deterministic, no atomics) and applies the update.
     fwd, bwd = [], []
     nslot = [0]
+    splits = []
 
     # Forward items gather their own inputs (b at the pivots + children's
     # contribution rows via gsrc), so there is no separate FINIT pass; a front
     # without a contribution block gets one pivot-only item (r0 = -1).  Split
     # items (slot >= 0) are reduced by the last-arriving CTA of their group.
-    # The launch's 5th field is the largest inner range of its items (sizes smem).
+    # The launch's 5th field is the largest inner range of its items; when a level
+    # has split items it equals that level's split length (the kernels use it so).
     def gemm_items(fronts, rows_of, K_of, pivot_only):
         g, kmax = [], 1
+        split = _choose_split([int(K_of(f)) for f in fronts], [max(1, int(rows_of(f))) for f in fronts])
+        splits.append(split)
         for f in fronts:
             K = int(K_of(f))
-            ns_ = max(1, -(-K // SPLIT_K))
+            ns_ = max(1, -(-K // split))
             rws = int(rows_of(f))
             if rws == 0 and pivot_only:
                 # pivot rows only, in chunks of SOLVE_ROWS (r0 = -1 - first pivot row)
@@ -516,7 +541,7 @@ def build_schedule(plan: FactorPlan, pw=PW):
                     nslot[0] += ns_
                     for ks in range(ns_):
                         g.append((f, r0, ks, s0 + ks))
-            kmax = max(kmax, min(K, SPLIT_K))
+            kmax = max(kmax, min(K, split))
         return g, kmax
 
     for L in range(plan.nlevels):
@@ -547,7 +572,7 @@ def build_schedule(plan: FactorPlan, pw=PW):
     assert nidx < 2 ** 31
     work = np.vstack(items) if items else np.zeros((0, 4), np.int32)
     return dict(work=np.ascontiguousarray(work.astype(np.int32)), gsrc=np.ascontiguousarray(gsrc.astype(np.int32)),
-                nslot=int(nslot[0]), split_k=int(SPLIT_K), solve_rows=int(SOLVE_ROWS),
+                nslot=int(nslot[0]), split_k=int(max(splits) if splits else 1), solve_rows=int(SOLVE_ROWS),
                 factor=np.array(fl, dtype=np.int64).reshape(-1, 5),
                 fwd=np.array(fwd, dtype=np.int64).reshape(-1, 5),
                 bwd=np.array(bwd, dtype=np.int64).reshape(-1, 5))

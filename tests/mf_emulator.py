@@ -67,7 +67,6 @@ def solve(plan, st, rhs):
     """Apply the factorisation to rhs (n_total_internal, J); returns x (free rows)."""
     work = plan.schedule["work"]
     gsrc = plan.schedule["gsrc"]
-    sk = plan.schedule["split_k"]
     R = plan.schedule["solve_rows"]
     fm, fk, off, io_ = plan.f_m, plan.f_k, plan.f_off, plan.f_idx_off
     J = rhs.shape[1]
@@ -96,8 +95,8 @@ def solve(plan, st, rhs):
                 t1 = min(k, t0 + R)
                 fr[base + t0:base + t1] = gathered(base + np.arange(t0, t1), np.ones(t1 - t0, dtype=bool))
                 continue
-            kb = 0 if slot < 0 else ks * sk
-            ke = k if slot < 0 else min(k, kb + sk)
+            kb = 0 if slot < 0 else ks * kmax          # split items: kmax is the level's split
+            ke = k if slot < 0 else min(k, kb + kmax)
             assert ke - kb <= kmax
             piv = gathered(base + np.arange(kb, ke), np.ones(ke - kb, dtype=bool))
             if r0 == 0:
@@ -121,8 +120,8 @@ def solve(plan, st, rhs):
             base, k, m = io_[f], fk[f], fm[f]
             rows = np.arange(r0, min(r0 + R, k))
             bop = np.vstack([fr[base:base + k], x[plan.f_idx[base + k:base + m]]])
-            kb = 0 if slot < 0 else ks * sk
-            ke = m if slot < 0 else min(m, kb + sk)
+            kb = 0 if slot < 0 else ks * kmax
+            ke = m if slot < 0 else min(m, kb + kmax)
             assert ke - kb <= kmax
             prod = front(f)[rows, kb:ke] @ bop[kb:ke]
             if slot < 0:

@@ -21,6 +21,11 @@ Z = torch.zeros_like(X)
 for _ in range(3):
     N.check(eng.lib.ens_precond_apply(eng.ctx, eng.sptr, _dptr(X), _dptr(Z)), "p")
 torch.cuda.synchronize()
+dfo = os.environ.get("ENS_DF_PROBE_OUT")
+if dfo and hasattr(eng.lib, "ens_df_probe_dump"):    # DF_PROBE build
+    eng.lib.ens_df_probe_dump(b"/dev/null")
+    N.check(eng.lib.ens_precond_apply(eng.ctx, eng.sptr, _dptr(X), _dptr(Z)), "p")
+    print("df probe records", eng.lib.ens_df_probe_dump(dfo.encode()))
 out = os.environ.get("ENS_PROBE_OUT")
 if out and hasattr(eng.lib, "ens_probe_dump"):      # SG_PROBE build: one clean solve, then dump
     eng.lib.ens_probe_dump(b"/dev/null")
