@@ -136,6 +136,16 @@ def run_reference(args):
     print(json.dumps(line), flush=True)
 
 
+def spmm_traffic():
+    """DRAM bytes per SpMM launch from the committed ncu --set full capture (profiles/), or None."""
+    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r01_spmm_traffic.json")
+    try:
+        with open(path) as fh:
+            return int(json.load(fh)["traffic_bytes_per_launch"])
+    except (OSError, KeyError, ValueError):
+        return None
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -314,7 +324,7 @@ def main():
             "value_refactor_every_step": always,
             "roofline": {"bound": "hbm", "kernel": "ens_spmm (saddle SpMM, both systems)", "achieved": spmm_gbs,
                          "peak": hbm, "peak_kind": peak_kind, "unit": "GB/s", "frac": spmm_gbs / hbm,
-                         "traffic": None, "bytes_per_launch": bytes_spmm, "ms_per_launch": spmm_ms},
+                         "traffic": spmm_traffic(), "bytes_per_launch": bytes_spmm, "ms_per_launch": spmm_ms},
             "phases_ms": {"spmm": spmm_ms, "factor": factor_ms, "lu_solve": solve_ms,
                           "factor_tflops_fp64": factor_tflops, "lu_solve_gbs": solve_gbs},
             "clocks": clocks,
