@@ -202,7 +202,10 @@ int  ens_factor(ens_ctx* ctx, void* stream, const double* as_vals, int32_t* n_pe
 
 /* Column-batched right-preconditioned FGMRES on both systems.  x holds the
  * initial guess (identity rows are overwritten from rhs) and returns the
- * solution; relres_host[m] = max_j ||b_j - K x_j|| / max(||b_j||, tiny). */
+ * solution; relres_host[m] = max_j ||b_j - K x_j|| / max(||b_j||, tiny).
+ * iters_host: in = predicted iteration count p >= 0 (the first cycle runs p
+ * iterations without host round trips, then the true residual decides; 0 =
+ * check after every iteration), out = iterations performed. */
 int  ens_solve(ens_ctx* ctx, void* stream, const double* as_vals, const double* rhs, double* x,
                double rtol, int32_t restart, int32_t max_restarts, int32_t* iters_host, double* relres_host);
 

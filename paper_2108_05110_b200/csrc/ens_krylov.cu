@@ -247,6 +247,9 @@ int gmres_solve(ens_ctx* c, cudaStream_t s, const double* as_vals, const double*
     // identity rows of the iterate carry the data exactly (stepper.py:214-215, 250-251)
     RET(launch_copy_cons(c, s, rhs, x));
     RET(launch_coldot(c, s, rhs, 0, 1, rhs, N, kb.bn2));
+    // predicted iteration count: the first cycle runs that many iterations without
+    // host round trips; the true residual of the restart then decides (as always)
+    const int predict = std::max(0, std::min(*iters, restart));
     int total_it = 0;
     for (int cyc = 0; cyc <= max_restarts; ++cyc) {
         RET(launch_spmm(c, s, as_vals, x, rhs, Rb, 1));
@@ -254,12 +257,17 @@ int gmres_solve(ens_ctx* c, cudaStream_t s, const double* as_vals, const double*
         ENS_CK(cudaMemsetAsync(c->d_count, 0, sizeof(int32_t), s));
         k_gm_init<<<cb, 128, 0, s>>>(c->cols, kb.bn2, kb.rn2, rtol, kb.scale, c->d_count, n);
         ENS_CKL();
-        int active = 0;
-        RET(read_count(c, s, &active));
-        if (active == 0 || cyc == max_restarts) {
-            // true relative residual per matrix (linalg.py:111-118)
+        const bool blind = cyc == 0 && predict > 0;
+        int active = 1;
+        if (!blind) {
+            // one round trip: active-column count and the residual norms
+            ENS_CK(cudaMemcpyAsync(c->h_count, c->d_count, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
             ENS_CK(cudaMemcpyAsync(c->h_small, kb.bn2, sizeof(double) * 2 * n, cudaMemcpyDeviceToHost, s));
             ENS_CK(cudaStreamSynchronize(s));
+            active = *c->h_count;
+        }
+        if (!blind && (active == 0 || cyc == max_restarts)) {
+            // true relative residual per matrix (linalg.py:111-118)
             for (int mat = 0; mat < 2; ++mat) {
                 double worst = 0.0;
                 for (int j = 0; j < J; ++j) {
@@ -292,6 +300,10 @@ int gmres_solve(ens_ctx* c, cudaStream_t s, const double* as_vals, const double*
             ENS_CKL();
             used = i + 1;
             ++total_it;
+            if (blind) {
+                if (used == predict) break;
+                continue;
+            }
             RET(read_count(c, s, &active));
             if (active == 0) break;
         }

@@ -682,7 +682,7 @@ class Engine:
         if code == N.ENS_ENOCONV and not need:        # stale preconditioner: rebuild and retry once
             self._factor()
             Xn.copy_(X)
-            code, iters2, rel = self._solve(Xn)
+            code, iters2, rel = self._solve(Xn, predict=1)
             iters += iters2
         self.last_iters, self.last_relres = iters, rel
         N.check(code, "ens_solve")
@@ -707,8 +707,11 @@ class Engine:
         self.since_factor = 0
         self.n_factor += 1
 
-    def _solve(self, Xn):
-        iters = N.I32(0)
+    def _solve(self, Xn, predict=1):
+        # first FGMRES cycle: `predict` iterations without host round trips, then the
+        # true residual decides (one iteration is the steady state with the
+        # extrapolated guess; otherwise the next cycles check every iteration)
+        iters = N.I32(predict)
         rel = (N.F64 * 2)()
         code = self.lib.ens_solve(self.ctx, self.sptr, _dptr(self.as_vals), _dptr(self.rhs), _dptr(Xn), self.rtol,
                                   self.restart, self.max_restarts, C.byref(iters), rel)
