@@ -63,6 +63,8 @@ struct ens_ctx {
     int* ticket = nullptr;         // split-K arrival counters (last CTA reduces)
     int4* sitem = nullptr;         // solve work items with their front's geometry (3 x int4 per item)
     void* df = nullptr;            // dataflow solve plan (ens_mfsolve_df.cu)
+    std::vector<uint8_t> fwd_multi;   // per level: forward GEMM runs the multi-unit kernel
+    int sg_slots = 0;              // resident CTAs of the multi-unit kernel (all SMs)
     double* ec = nullptr;          // member-pass element buffer [2][nt][6][2][J]
     double* el = nullptr;          // assembly element buffer [2][36][nt]
     int32_t* finit_rows = nullptr; // per level: front rows k_finit assembles (bit 31: pivot row)

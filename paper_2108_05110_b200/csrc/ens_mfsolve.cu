@@ -390,6 +390,135 @@ __global__ void __launch_bounds__(SG_T, SG_MINB) k_sgemm(MfDev d, const int4* __
     SG_END(slot >= 0 ? 2 : 0);
 }
 
+// ---------------------------------------------------------------------------
+// Forward levels without split items (every item covers its front's whole pivot
+// range -- the lower tree levels): persistent CTAs walk units u = blockIdx.x,
+// +gridDim.x, ... (unit = item x system) and the 2-stage cp.async pipeline runs
+// straight across unit boundaries: the next unit's first chunk loads while the
+// current unit computes and stores.  Same arithmetic as k_sgemm (deterministic).
+// ---------------------------------------------------------------------------
+struct SgUnit {
+    const double* base;   // front entries of this system
+    double* fr;           // front vector rows of this system (FR + fo*J)
+    int m, k, hasch, rbase, nr, nch;
+};
+
+__device__ __forceinline__ SgUnit sg_unit(const int4* __restrict__ sitem, int item0, int nitem, int u,
+                                          const double* __restrict__ F, int64_t storage, double* __restrict__ FR,
+                                          int64_t nidx, int J) {
+    SgUnit g;
+    const int item = u >> 1, mat = u & 1;
+    const int4* rec = sitem + 3LL * (item0 + min(item, nitem - 1));
+    const int4 w0 = rec[0], w1 = rec[1], w2 = rec[2];
+    const int64_t off = (int64_t)(unsigned)w2.x | ((int64_t)w2.y << 32);
+    const int64_t fo = (int64_t)(unsigned)w2.z | ((int64_t)w2.w << 32);
+    g.m = w1.x;
+    g.k = w1.y;
+    g.hasch = w1.z;
+    g.base = F + (int64_t)mat * storage + off;
+    g.fr = FR + (int64_t)mat * nidx * J + fo * J;
+    g.rbase = g.k + w0.y;
+    g.nr = min(SG_R, g.m - g.rbase);
+    g.nch = (g.k + SG_KC - 1) / SG_KC;
+    return g;
+}
+
+template <int NCT>
+__global__ void __launch_bounds__(SG_T, SG_MINB) k_sgemm_fwd_multi(const int4* __restrict__ sitem, int item0,
+                                                                int nitem, const double* __restrict__ F,
+                                                                int64_t storage, double* __restrict__ FR, int J,
+                                                                int64_t nidx, int zbase) {
+    extern __shared__ double sm[];
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, g = lane >> 2, q = lane & 3;
+    const int j0 = (zbase + blockIdx.z) * SG_C;
+    const int jn = min(SG_C, J - j0);
+    const int nunit = 2 * nitem;
+    const int row = 8 * warp + g;
+    int u = blockIdx.x;
+    if (u >= nunit) return;
+    SgUnit cu = sg_unit(sitem, item0, nitem, u, F, storage, FR, nidx, J);
+    SgUnit nu = sg_unit(sitem, item0, nitem, u + gridDim.x, F, storage, FR, nidx, J);
+    auto issue = [&](const SgUnit& w, int c, int buf) {
+        double* As = sm + buf * SG_STAGE;
+        double* Bsb = As + SG_R * SG_LDA;
+#pragma unroll
+        for (int i = 0; i < SG_R * SG_KC / SG_T; ++i) {
+            const int e = tid + SG_T * i, r = e / SG_KC, kk = e % SG_KC, kg = c * SG_KC + kk;
+            const bool ok = r < w.nr && kg < w.k;
+            cp_async8(&As[r * SG_LDA + kk], ok ? w.base + (int64_t)(w.rbase + r) * w.m + kg : w.base, ok);
+        }
+#pragma unroll
+        for (int i = 0; i < SG_KC * SG_C / SG_T; ++i) {
+            const int e = tid + SG_T * i, kk = e / SG_C, j = e % SG_C, kg = c * SG_KC + kk;
+            const bool ok = j < jn && kg < w.k;
+            cp_async8(&Bsb[kk * SG_LDB + j], ok ? w.fr + (int64_t)kg * J + j0 + j : w.base, ok);
+        }
+    };
+    // pipeline over the CTA's chunk stream: (unit, chunk) pairs in order
+    int buf = 0;
+    issue(cu, 0, 0);
+    cp_async_commit();
+    int c = 0;
+    double dacc[4][2] = {{0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}};
+    for (;;) {
+        cp_async_wait_n(0);
+        __syncthreads();
+        // issue the next chunk of the stream (possibly the next unit's first)
+        const bool last_of_unit = c + 1 >= cu.nch;
+        const bool has_next_unit = u + (int)gridDim.x < nunit;
+        if (!last_of_unit) issue(cu, c + 1, buf ^ 1);
+        else if (has_next_unit) issue(nu, 0, buf ^ 1);
+        cp_async_commit();
+        const double* As = sm + buf * SG_STAGE;
+        const double* ap = As + row * SG_LDA + q;
+        const double* bp = As + SG_R * SG_LDA + q * SG_LDB + g;
+        const int ksteps = (min(SG_KC, cu.k - c * SG_KC) + 3) >> 2;
+        if (8 * warp < cu.nr) {
+            if (ksteps == SG_KC / 4) {
+#pragma unroll
+                for (int uu = 0; uu < SG_KC / 4; ++uu) {
+                    const double av = ap[4 * uu];
+#pragma unroll
+                    for (int ct = 0; ct < NCT; ++ct) dmma8(dacc[ct][0], dacc[ct][1], av, bp[4 * uu * SG_LDB + 8 * ct]);
+                }
+            } else {
+#pragma unroll 2
+                for (int uu = 0; uu < ksteps; ++uu) {
+                    const double av = ap[4 * uu];
+#pragma unroll
+                    for (int ct = 0; ct < NCT; ++ct) dmma8(dacc[ct][0], dacc[ct][1], av, bp[4 * uu * SG_LDB + 8 * ct]);
+                }
+            }
+        }
+        buf ^= 1;
+        if (!last_of_unit) {
+            ++c;
+            continue;
+        }
+        // unit done: fr[C rows] = children rows (assembled by k_finit, leaf fronts: 0) - A B
+        if (row < cu.nr) {
+            double* pc = cu.fr + (int64_t)(cu.rbase + row) * J + j0;
+#pragma unroll
+            for (int ct = 0; ct < NCT; ++ct)
+#pragma unroll
+                for (int e = 0; e < 2; ++e) {
+                    const int col = 8 * ct + 2 * q + e;
+                    if (col >= jn) continue;
+                    const double init = cu.hasch ? pc[col] : 0.0;
+                    pc[col] = init - dacc[ct][e];
+                }
+        }
+#pragma unroll
+        for (int ct = 0; ct < 4; ++ct) dacc[ct][0] = dacc[ct][1] = 0.0;
+        if (!has_next_unit) break;
+        u += gridDim.x;
+        cu = nu;
+        nu = sg_unit(sitem, item0, nitem, u + gridDim.x, F, storage, FR, nidx, J);
+        c = 0;
+    }
+    cp_async_wait_n(0);
+}
+
 static size_t sg_smem(int nstage) { return sizeof(double) * (size_t)nstage * SG_STAGE; }
 
 static int sg_stages(int kmax) {
@@ -400,6 +529,11 @@ static int sg_stages(int kmax) {
     }
     if (env > 0) return env;
     return kmax <= 2 * SG_KC ? 2 : 3;
+}
+
+static bool multi_enabled() {   // opt-in: measured no faster than one CTA per item at C2 (831 vs 834 us)
+    const char* e = std::getenv("ENS_SOLVE_MULTI");
+    return e && e[0] == '1';
 }
 
 static bool capturing(cudaStream_t s) {
@@ -468,6 +602,33 @@ static int mf_solve_launches(ens_ctx* c, cudaStream_t s, SolveIO* io, int64_t* n
                 }
             }
             if (n == 0 || kmax == 0) continue;
+            if (op == SOP_FGEMM && L < (int)c->fwd_multi.size() && c->fwd_multi[L] && multi_enabled()) {
+                const int zfull = J / SG_C, rem = J - zfull * SG_C;
+                const unsigned units = (unsigned)(2 * n);
+                const unsigned g = std::min<unsigned>(units, (unsigned)c->sg_slots);
+                for (int rep = 0; rep < (timing ? trep : 1); ++rep) {
+#define SGM(NC, ZN, Z0)                                                                                              \
+    k_sgemm_fwd_multi<NC><<<dim3(g, 1, ZN), SG_T, sg_smem(2), s>>>(c->sitem, off, n, c->fronts, c->p.front_storage, \
+                                                                   c->frvec, J, nidx, Z0)
+                    if (zfull > 0) {
+                        SGM(4, (unsigned)zfull, 0);
+                        ENS_CKL();
+                        if (rep == 0) ++cnt;
+                    }
+                    if (rem > 0) {
+                        const int nct = (rem + 7) / 8;
+                        if (nct == 1) SGM(1, 1, zfull);
+                        else if (nct == 2) SGM(2, 1, zfull);
+                        else if (nct == 3) SGM(3, 1, zfull);
+                        else SGM(4, 1, zfull);
+                        ENS_CKL();
+                        if (rep == 0) ++cnt;
+                    }
+#undef SGM
+                }
+                mark("fwd-multi", n, kmax);
+                continue;
+            }
             const int nst = sg_stages(kmax);
             for (int rep = 0; rep < (timing ? trep : 1); ++rep) {   // launches are idempotent
                 // member column blocks: full 32-wide blocks use 4 column tiles, the remainder fewer
@@ -572,6 +733,28 @@ int mf_solve(ens_ctx* c, cudaStream_t s, const double* r, double* z) {
         ENS_CK(cudaStreamSynchronize(s));
         cudaFree(d_hasch);
         c->ws_bytes += pbytes + tbytes + sizeof(int4) * 3 * (size_t)nw + sizeof(int32_t) * (size_t)nidx;
+        {   // forward levels without split or pivot-only items run the multi-unit kernel
+            std::vector<int32_t> work((size_t)c->p.n_work * 4);
+            if (c->p.n_work > 0)
+                ENS_CK(cudaMemcpy(work.data(), c->p.work, sizeof(int32_t) * work.size(), cudaMemcpyDeviceToHost));
+            const int nlev = (int)c->level_front_off.size() - 1;
+            c->fwd_multi.assign((size_t)nlev, 0);
+            for (size_t i = 0; i + 5 <= c->sched_fwd.size(); i += 5) {
+                const int L = (int)c->sched_fwd[i + 1], o = (int)c->sched_fwd[i + 2], n = (int)c->sched_fwd[i + 3];
+                bool ok = n > 0;
+                for (int u = 0; u < n && ok; ++u) ok = work[4 * (o + u) + 1] >= 0 && work[4 * (o + u) + 3] < 0;
+                if (L >= 0 && L < nlev) c->fwd_multi[L] = ok ? 1 : 0;
+            }
+            int occ = 0, dev = 0, sms = 0;
+            ENS_CK(cudaFuncSetAttribute(k_sgemm_fwd_multi<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sg_smem(2)));
+            ENS_CK(cudaFuncSetAttribute(k_sgemm_fwd_multi<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sg_smem(2)));
+            ENS_CK(cudaFuncSetAttribute(k_sgemm_fwd_multi<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sg_smem(2)));
+            ENS_CK(cudaFuncSetAttribute(k_sgemm_fwd_multi<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sg_smem(2)));
+            ENS_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_sgemm_fwd_multi<3>, SG_T, sg_smem(2)));
+            cudaGetDevice(&dev);
+            cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+            c->sg_slots = std::max(1, occ) * sms;
+        }
         if (df_enabled(c)) {   // task lists are built before any graph capture
             const int rc = df_build(c, s);
             if (rc != ENS_OK) return rc;
