@@ -254,3 +254,22 @@ def test_pressure_mean_zero():
     new, _ = P.advance(st, cfg, disc, PaperMmsForcing(), PaperMmsBoundary())
     means = new.q @ disc.pressure_integrals / disc.area
     assert np.max(np.abs(means)) < 1e-12
+
+
+@pytest.mark.parametrize("case,over", [
+    ("C3", dict(n=8, J=4, steps=3)),                              # lid-driven cavity, lid (1 + eta_j)
+    ("C4", dict(k=2, J=4, steps=3, dt=0.05, length=8.0)),         # channel: do-nothing outflow, no pin
+    ("C1", dict(n=6, J=40, steps=2)),                             # J > 32: two member-column blocks
+    ("C1", dict(n=6, J=32, steps=2)),                             # exactly one full column block
+])
+def test_case_runs_match_oracle(case, over):
+    """Small instances of the BASELINE problem kinds and member counts against the CPU oracle."""
+    disc, cfg, prob = P.build_case(case, **over)
+    report, state, _ = P.run(cfg, prob)
+    ost, _, _, ores = O.run(cfg, disc, prob.initial_v, prob.initial_w, prob.forcing, prob.boundary,
+                            with_record=False)
+    for f in "vw":
+        assert rel(getattr(state, f), getattr(ost, f)) < 1e-9, f
+    for f in "qr":
+        assert rel(getattr(state, f), getattr(ost, f)) < 1e-8, f
+    assert np.all(report.residuals[1:] < 1e-11)
