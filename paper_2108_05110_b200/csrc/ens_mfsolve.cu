@@ -59,7 +59,9 @@ __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wai
 #ifndef SG_KMAX
 #define SG_KMAX 256 // max inner range per work item (>= the plan's split lengths)
 #endif
+#ifndef SG_KC
 #define SG_KC 32    // inner chunk of the pipelined mainloop
+#endif
 #define SG_LDA 36   // A stage row stride (= 4 mod 16: conflict-free fragment reads)
 #define SG_STAGE (SG_R * SG_LDA + SG_KC * 36)   // doubles per pipeline stage (A + B)
 #define SG_T 256    // threads
@@ -179,7 +181,9 @@ __global__ void __launch_bounds__(256) k_finit(const int32_t* __restrict__ rows,
 __device__ __forceinline__ void cp_async_wait_n(int n) {
     if (n <= 0) asm volatile("cp.async.wait_group 0;\n" ::);
     else if (n == 1) asm volatile("cp.async.wait_group 1;\n" ::);
-    else asm volatile("cp.async.wait_group 2;\n" ::);
+    else if (n == 2) asm volatile("cp.async.wait_group 2;\n" ::);
+    else if (n == 3) asm volatile("cp.async.wait_group 3;\n" ::);
+    else asm volatile("cp.async.wait_group 4;\n" ::);
 }
 
 // item = (f, r0, ks, slot)
@@ -519,16 +523,17 @@ __global__ void __launch_bounds__(SG_T, SG_MINB) k_sgemm_fwd_multi(const int4* _
     cp_async_wait_n(0);
 }
 
+#define SG_MAXST 5
 static size_t sg_smem(int nstage) { return sizeof(double) * (size_t)nstage * SG_STAGE; }
 
 static int sg_stages(int kmax) {
     static int env = -1;
     if (env < 0) {
         const char* e = std::getenv("ENS_SOLVE_STAGES");
-        env = e ? std::max(2, std::min(3, std::atoi(e))) : 0;
+        env = e ? std::max(2, std::min(SG_MAXST, std::atoi(e))) : 0;
     }
-    if (env > 0) return env;
-    return kmax <= 2 * SG_KC ? 2 : 3;
+    if (env > 0) return std::min(env, std::max(2, (kmax + SG_KC - 1) / SG_KC));
+    return 2;   // measured: a shallow pipeline with more resident CTAs wins (stage sweep, profiles/)
 }
 
 static bool multi_enabled() {   // opt-in: measured no faster than one CTA per item at C2 (831 vs 834 us)
@@ -683,10 +688,10 @@ int mf_solve(ens_ctx* c, cudaStream_t s, const double* r, double* z) {
             return ENS_EINVAL;
         }
         ENS_CK(cudaMalloc(&c->solve_io, sizeof(SolveIO)));
-        ENS_CK(cudaFuncSetAttribute(k_sgemm<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sg_smem(3)));
-        ENS_CK(cudaFuncSetAttribute(k_sgemm<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sg_smem(3)));
-        ENS_CK(cudaFuncSetAttribute(k_sgemm<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sg_smem(3)));
-        ENS_CK(cudaFuncSetAttribute(k_sgemm<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sg_smem(3)));
+        ENS_CK(cudaFuncSetAttribute(k_sgemm<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sg_smem(SG_MAXST)));
+        ENS_CK(cudaFuncSetAttribute(k_sgemm<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sg_smem(SG_MAXST)));
+        ENS_CK(cudaFuncSetAttribute(k_sgemm<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sg_smem(SG_MAXST)));
+        ENS_CK(cudaFuncSetAttribute(k_sgemm<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sg_smem(SG_MAXST)));
         const int64_t ns = c->p.n_slot > 0 ? c->p.n_slot : 1;
         const size_t pbytes = sizeof(double) * 2 * (size_t)ns * SG_R * c->J;
         const size_t tbytes = sizeof(int) * 2 * (size_t)ns * ((c->J + SG_C - 1) / SG_C);
