@@ -407,7 +407,7 @@ SOP_FINIT, SOP_FEXT, SOP_FGEMM, SOP_BGATHER, SOP_BGEMM, SOP_FRED, SOP_BRED = ran
 # inner length per solve-GEMM work item: 0 = chosen per level (see _choose_split),
 # else a fixed length for every level (tests, experiments: ENS_SPLIT_K)
 SPLIT_K = int(__import__("os").environ.get("ENS_SPLIT_K", "256"))
-SPLIT_CANDIDATES = (64, 128, 192, 256, 384, 512)
+SPLIT_CANDIDATES = (64, 128, 192, 256)   # <= the solve kernel's SG_KMAX
 # per-level launch model of the solve GEMM (measured on B200 at C2): resident CTAs,
 # fixed CTA latency, per-32-column chunk time, extra latency of a split group's reduction
 _SLOTS, _T0, _TCHUNK, _TRED = 3 * 148, 3.5, 1.1, 3.0
