@@ -180,7 +180,7 @@ __global__ void __launch_bounds__(256) k_spmm_vel_v(const int32_t* __restrict__ 
         const double a00 = A[k], a01 = A[k + 1], a10 = A[nnz + k], a11 = A[nnz + k + 1];
 #pragma unroll
         for (int v = 0; v < V2; ++v) {
-            const int i = V2 * part + v;
+            const int i = part + L * v;   // lane-contiguous per v: fewer L1 lines per load
             if (i < J) {
                 const double2 x00 = X2[c0 * J + i], x01 = X2[c1 * J + i];
                 const double2 x10 = X2[MS + c0 * J + i], x11 = X2[MS + c1 * J + i];
@@ -200,7 +200,7 @@ __global__ void __launch_bounds__(256) k_spmm_vel_v(const int32_t* __restrict__ 
         const double a00 = A[k], a10 = A[nnz + k];
 #pragma unroll
         for (int v = 0; v < V2; ++v) {
-            const int i = V2 * part + v;
+            const int i = part + L * v;   // lane-contiguous per v: fewer L1 lines per load
             if (i < J) {
                 const double2 x00 = X2[c0 * J + i], x10 = X2[MS + c0 * J + i];
                 acc[0][v].x = fma(a00, x00.x, acc[0][v].x);
@@ -218,7 +218,7 @@ __global__ void __launch_bounds__(256) k_spmm_vel_v(const int32_t* __restrict__ 
         const int64_t p0 = btc[t];
 #pragma unroll
         for (int v = 0; v < V2; ++v) {
-            const int i = V2 * part + v;
+            const int i = part + L * v;   // lane-contiguous per v: fewer L1 lines per load
             if (i < J) {
                 const bool ycomp = i >= H;
                 const int64_t o = p0 * H + (ycomp ? i - H : i);
@@ -233,7 +233,7 @@ __global__ void __launch_bounds__(256) k_spmm_vel_v(const int32_t* __restrict__ 
     }
 #pragma unroll
     for (int v = 0; v < V2; ++v) {
-        const int i = V2 * part + v;
+        const int i = part + L * v;   // lane-contiguous per v: fewer L1 lines per load
         if (i >= J) continue;
         const int64_t o = node * J + i;
         const bool ident = cflag[2 * node + (i >= H ? 1 : 0)] != 0;
