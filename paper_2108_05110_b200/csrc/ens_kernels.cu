@@ -976,33 +976,43 @@ __global__ void k_pres_dot(const double* __restrict__ X, const double* __restric
     }
 }
 
-__global__ void k_pres_sub(const double* __restrict__ X, const double* __restrict__ part, int RB, double inv_area,
-                           int mean_zero, int64_t nvel, int npres, int64_t N, int J, double* __restrict__ P) {
+// means[mat][j] = sum of the RB partials (fixed order, warp per output) / area
+__global__ void k_pres_fin(const double* __restrict__ part, int RB, int J, double inv_area, double* __restrict__ mean) {
+    const int t = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (t >= 2 * J) return;
+    const int mat = t / J, j = t % J;
+    double s = 0.0;
+    for (int b = lane; b < RB; b += 32) s += part[((int64_t)b * 2 + mat) * J + j];
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (lane == 0) mean[t] = s * inv_area;
+}
+
+__global__ void k_pres_sub(const double* __restrict__ X, const double* __restrict__ mean, int64_t nvel, int npres,
+                           int64_t N, int J, double* __restrict__ P) {
     const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const int64_t per = (int64_t)npres * J;
     if (t >= 2 * per) return;
     const int mat = (int)(t / per);
     const int64_t u = t - mat * per;
     const int j = (int)(u % J);
-    double mean = 0.0;
-    if (mean_zero) {
-        double s = 0.0;
-        for (int b = 0; b < RB; ++b) s += part[((int64_t)b * 2 + mat) * J + j];
-        mean = s * inv_area;
-    }
-    P[t] = X[(int64_t)mat * N * J + nvel * J + u] - mean;
+    P[t] = X[(int64_t)mat * N * J + nvel * J + u] - (mean ? mean[mat * J + j] : 0.0);
 }
 
 int launch_epilogue(ens_ctx* c, cudaStream_t s, const double* x, double* p_out) {
-    const int RB = 64;
+    const int RB = 148;
+    double* mean = nullptr;
     if (c->m.mean_zero) {
         dim3 grid(RB, 1, 2);
         k_pres_dot<<<grid, 256, 0, s>>>(x, c->m.pres_int, c->n_vel, c->m.n_pres, c->n_total, c->J, c->red_part);
         ENS_CKL();
+        // 2J doubles past the Krylov scalars [bn2|rn2|h1|h2|hn2|scale|y] of the small-output area
+        mean = c->red_out + 2 * (size_t)c->J * (4 + 3 * (ENS_MAX_RESTART + 1));
+        k_pres_fin<<<(2 * c->J * 32 + 255) / 256, 256, 0, s>>>(c->red_part, RB, c->J, 1.0 / c->m.area, mean);
+        ENS_CKL();
     }
     const int64_t tot = 2LL * c->m.n_pres * c->J;
-    k_pres_sub<<<(unsigned)((tot + 255) / 256), 256, 0, s>>>(x, c->red_part, RB, 1.0 / c->m.area, c->m.mean_zero,
-                                                             c->n_vel, c->m.n_pres, c->n_total, c->J, p_out);
+    k_pres_sub<<<(unsigned)((tot + 255) / 256), 256, 0, s>>>(x, mean, c->n_vel, c->m.n_pres, c->n_total, c->J, p_out);
     ENS_CKL();
     return ENS_OK;
 }
