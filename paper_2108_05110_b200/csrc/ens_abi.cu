@@ -123,6 +123,7 @@ void ens_destroy(ens_ctx* c) {
     cudaFree(c->sitem);
     cudaFree(c->finit_rows);
     cudaFree(c->ec);
+    cudaFree(c->nrm_part);
     df_free(c);
     cudaFree(c->el);
     delete c;

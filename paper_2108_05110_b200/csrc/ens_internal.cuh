@@ -65,6 +65,7 @@ struct ens_ctx {
     void* df = nullptr;            // dataflow solve plan (ens_mfsolve_df.cu)
     std::vector<uint8_t> fwd_multi;   // per level: forward GEMM runs the multi-unit kernel
     int sg_slots = 0;              // resident CTAs of the multi-unit kernel (all SMs)
+    double* nrm_part = nullptr;    // fused residual-norm partials of the SpMM
     double* ec = nullptr;          // member-pass element buffer [2][nt][6][2][J]
     double* el = nullptr;          // assembly element buffer [2][36][nt]
     int32_t* finit_rows = nullptr; // per level: front rows k_finit assembles (bit 31: pivot row)
@@ -96,6 +97,9 @@ int launch_spmm(ens_ctx* c, cudaStream_t s, const double* as_vals, const double*
 int launch_spmm_blocked(ens_ctx* c, cudaStream_t s, const double* as_vals, const double* x, const double* b,
                         double* y, int mode);
 int spmm_blocked_setup(ens_ctx* c);
+bool spmm_resnorm_ok(const ens_ctx* c);
+int launch_spmm_resnorm(ens_ctx* c, cudaStream_t s, const double* as_vals, const double* x, const double* b,
+                        double* y, double* bn2, double* rn2);
 int launch_epilogue(ens_ctx* c, cudaStream_t s, const double* x, double* p_out);
 int launch_diagnostics(ens_ctx* c, cudaStream_t s, const double* x, const double* means, double* out);
 int launch_copy_cons(ens_ctx* c, cudaStream_t s, const double* src, double* dst);

@@ -246,14 +246,19 @@ int gmres_solve(ens_ctx* c, cudaStream_t s, const double* as_vals, const double*
     const unsigned cb = (unsigned)((n + 127) / 128);
     // identity rows of the iterate carry the data exactly (stepper.py:214-215, 250-251)
     RET(launch_copy_cons(c, s, rhs, x));
-    RET(launch_coldot(c, s, rhs, 0, 1, rhs, N, kb.bn2));
+    const bool fused = spmm_resnorm_ok(c);   // residual SpMM also yields ||b||^2 and ||r||^2
+    if (!fused) RET(launch_coldot(c, s, rhs, 0, 1, rhs, N, kb.bn2));
     // predicted iteration count: the first cycle runs that many iterations without
     // host round trips; the true residual of the restart then decides (as always)
     const int predict = std::max(0, std::min(*iters, restart));
     int total_it = 0;
     for (int cyc = 0; cyc <= max_restarts; ++cyc) {
-        RET(launch_spmm(c, s, as_vals, x, rhs, Rb, 1));
-        RET(launch_coldot(c, s, Rb, 0, 1, Rb, N, kb.rn2));
+        if (fused) {
+            RET(launch_spmm_resnorm(c, s, as_vals, x, rhs, Rb, kb.bn2, kb.rn2));
+        } else {
+            RET(launch_spmm(c, s, as_vals, x, rhs, Rb, 1));
+            RET(launch_coldot(c, s, Rb, 0, 1, Rb, N, kb.rn2));
+        }
         ENS_CK(cudaMemsetAsync(c->d_count, 0, sizeof(int32_t), s));
         k_gm_init<<<cb, 128, 0, s>>>(c->cols, kb.bn2, kb.rn2, rtol, kb.scale, c->d_count, n);
         ENS_CKL();

@@ -8,6 +8,8 @@
 // summation order is fixed per row and identical for every member column.
 // (A variant that preloads the row's indices lane-parallel and broadcasts them
 // with shuffles measured slower at C2: 0.24 ms vs 0.17 ms per launch pair.)
+#include <cstdlib>
+
 #include "ens_internal.cuh"
 
 static inline int next_pow2(int x) {
@@ -148,20 +150,60 @@ __global__ void __launch_bounds__(256) k_spmm_pres(const int32_t* __restrict__ b
 // scalar kernel's instructions per row at J = 20 (10 lanes x 3 rows per warp).
 // Summation order per output is unchanged (CSR order, then B^T in order).
 // ---------------------------------------------------------------------------
-template <int V2>
+// fixed-order reduction of per-lane member-pair squares: row groups of the warp
+// (lanes part + L*rr), then the block's warps; one partial row per block
+__device__ __forceinline__ void nrm_block_reduce(double2 (&sq)[2][2], int lane, int part, int L, int R, int J,
+                                                 double* __restrict__ nrm) {
+    __shared__ double2 red[8][2][2][32];
+    const int warp = threadIdx.x >> 5;
+#pragma unroll
+    for (int m = 0; m < 2; ++m)
+#pragma unroll
+        for (int br = 0; br < 2; ++br) {
+            double2 t = make_double2(0.0, 0.0);
+            for (int rr = 0; rr < R; ++rr) {
+                const double x = __shfl_sync(0xffffffffu, sq[m][br].x, part + L * rr);
+                const double y = __shfl_sync(0xffffffffu, sq[m][br].y, part + L * rr);
+                t.x += x;
+                t.y += y;
+            }
+            if (lane < L) red[warp][m][br][lane] = t;
+        }
+    __syncthreads();
+    const int nw = blockDim.x >> 5;
+    for (int e = threadIdx.x; e < 2 * 2 * L; e += blockDim.x) {
+        const int m = e / (2 * L), br = (e / L) & 1, p = e % L;
+        double2 t = make_double2(0.0, 0.0);
+        for (int w = 0; w < nw; ++w) {
+            t.x += red[w][m][br][p].x;
+            t.y += red[w][m][br][p].y;
+        }
+        double* o = nrm + (((int64_t)blockIdx.x * 2 + m) * 2 + br) * J + 2 * p;
+        o[0] = t.x;
+        o[1] = t.y;
+    }
+}
+
+// NRM (mode 1, V2 == 2, L == J/2): also the per-column squares of b and b - K x,
+// reduced in fixed order (row groups of the warp, warps of the block) to one
+// partial per block: nrm[blk][mat][{b, r}][J]
+template <int V2, bool NRM>
 __global__ void __launch_bounds__(256) k_spmm_vel_v(const int32_t* __restrict__ rp, const int32_t* __restrict__ col,
                                                     const double* __restrict__ A, int nnz,
                                                     const int32_t* __restrict__ btp, const int32_t* __restrict__ btc,
                                                     const double* __restrict__ btv, const uint8_t* __restrict__ cflag,
                                                     const double* __restrict__ X, const double* __restrict__ Bv,
-                                                    double* __restrict__ Y, int ns, int64_t N, int J, int L, int mode) {
+                                                    double* __restrict__ Y, int ns, int64_t N, int J, int L, int mode,
+                                                    double* __restrict__ nrm) {
     // both systems per thread: one index stream feeds two independent gathers
     const int lane = threadIdx.x & 31;
     const int R = 32 / L;
     const int r = lane / L, part = lane - r * L;
     const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int64_t node = gw * R + r;
-    if (r >= R || node >= ns) return;
+    double2 sq[2][2] = {{{0.0, 0.0}, {0.0, 0.0}}, {{0.0, 0.0}, {0.0, 0.0}}};   // [mat][b, r]
+    if (!NRM && (r >= R || node >= ns)) return;
+    if (r < R && node < ns) {
     const int H = J >> 1;                       // double2 per component
     const int64_t MS = N * H;                   // double2 per system block
     const double2* X2 = reinterpret_cast<const double2*>(X);
@@ -243,24 +285,35 @@ __global__ void __launch_bounds__(256) k_spmm_vel_v(const int32_t* __restrict__ 
             if (mode == 1) {
                 const double2 bb = B2[m * MS + o];
                 val = make_double2(bb.x - val.x, bb.y - val.y);
+                if (NRM) {
+                    sq[m][0].x += bb.x * bb.x;
+                    sq[m][0].y += bb.y * bb.y;
+                    sq[m][1].x += val.x * val.x;
+                    sq[m][1].y += val.y * val.y;
+                }
             }
             Y2[m * MS + o] = val;
         }
     }
+    }   // live row
+    if (NRM) nrm_block_reduce(sq, lane, part, L, R, J, nrm);
 }
 
-template <int V2>
+// NRM: as k_spmm_vel_v; a lane holds member pairs 2*part + v (v = 0, 1)
+template <int V2, bool NRM>
 __global__ void __launch_bounds__(256) k_spmm_pres_v(const int32_t* __restrict__ bp, const int32_t* __restrict__ bc,
                                                      const double* __restrict__ bv, const uint8_t* __restrict__ cflag,
                                                      const double* __restrict__ X, const double* __restrict__ Bv,
                                                      double* __restrict__ Y, int npres, int64_t nvel, int64_t N, int J,
-                                                     int L, int mode) {
+                                                     int L, int mode, double* __restrict__ nrm) {
     const int lane = threadIdx.x & 31;
     const int R = 32 / L;
     const int r = lane / L, part = lane - r * L;
     const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int64_t p = gw * R + r;
-    if (r >= R || p >= npres) return;
+    double2 sq[2][2][2] = {};   // [v][mat][b, r]
+    if (!NRM && (r >= R || p >= npres)) return;
+    if (r < R && p < npres) {
     const int H = J >> 1;
     const int64_t MS = N * H;
     const double2* X2 = reinterpret_cast<const double2*>(X);
@@ -301,28 +354,72 @@ __global__ void __launch_bounds__(256) k_spmm_pres_v(const int32_t* __restrict__
             if (mode == 1) {
                 const double2 bb = B2[o];
                 val = make_double2(bb.x - val.x, bb.y - val.y);
+                if (NRM && v < 2) {
+                    sq[v][m][0].x += bb.x * bb.x;
+                    sq[v][m][0].y += bb.y * bb.y;
+                    sq[v][m][1].x += val.x * val.x;
+                    sq[v][m][1].y += val.y * val.y;
+                }
             }
             Y2[o] = val;
+        }
+    }
+    }   // live row
+    if (NRM) {
+        // pairs 2*part + v: reduce each v as its own "part" stream, interleaved into one row
+        __shared__ double2 redp[8][2][2][2][32];
+        const int warp = threadIdx.x >> 5;
+#pragma unroll
+        for (int v = 0; v < 2; ++v)
+#pragma unroll
+            for (int m = 0; m < 2; ++m)
+#pragma unroll
+                for (int br = 0; br < 2; ++br) {
+                    double2 t = make_double2(0.0, 0.0);
+                    for (int rr = 0; rr < R; ++rr) {
+                        t.x += __shfl_sync(0xffffffffu, sq[v][m][br].x, part + L * rr);
+                        t.y += __shfl_sync(0xffffffffu, sq[v][m][br].y, part + L * rr);
+                    }
+                    if (lane < L) redp[warp][v][m][br][lane] = t;
+                }
+        __syncthreads();
+        const int nw = blockDim.x >> 5;
+        const int H2 = J >> 1;
+        for (int e = threadIdx.x; e < 2 * 2 * H2; e += blockDim.x) {
+            const int m = e / (2 * H2), br = (e / H2) & 1, pr = e % H2;   // member pair pr = 2*part + v
+            const int pp = pr >> 1, v = pr & 1;
+            double2 t = make_double2(0.0, 0.0);
+            for (int w = 0; w < nw; ++w) {
+                t.x += redp[w][v][m][br][pp].x;
+                t.y += redp[w][v][m][br][pp].y;
+            }
+            double* o = nrm + (((int64_t)blockIdx.x * 2 + m) * 2 + br) * J + 2 * pr;
+            o[0] = t.x;
+            o[1] = t.y;
         }
     }
 }
 
 static int launch_spmm_vec(ens_ctx* c, cudaStream_t s, const double* as_vals, const double* x, const double* b,
-                           double* y, int mode) {
+                           double* y, int mode, double* nrm, int* nblk) {
     const int J = c->J;
+    int blocks_total = 0;
     {
         const int V2 = J <= 64 ? 2 : (J <= 128 ? 4 : 8);
         const int L = (J + V2 - 1) / V2, R = 32 / L;
         const int64_t warps = ((int64_t)c->m.ns + R - 1) / R;
         dim3 grid((unsigned)((warps * 32 + 255) / 256), 1);
-#define SPV(V)                                                                                                      \
-    k_spmm_vel_v<V><<<grid, 256, 0, s>>>(c->m.s_rowptr, c->m.s_col, as_vals, c->m.nnz_s, c->m.bt_rowptr, c->m.bt_col, \
-                                         c->m.bt_val, c->m.cflag, x, b ? b : x, y, c->m.ns, c->n_total, J, L, mode)
-        if (V2 == 2) SPV(2);
-        else if (V2 == 4) SPV(4);
-        else SPV(8);
+#define SPV(V, NR)                                                                                                 \
+    k_spmm_vel_v<V, NR><<<grid, 256, 0, s>>>(c->m.s_rowptr, c->m.s_col, as_vals, c->m.nnz_s, c->m.bt_rowptr,        \
+                                             c->m.bt_col, c->m.bt_val, c->m.cflag, x, b ? b : x, y, c->m.ns,        \
+                                             c->n_total, J, L, mode, nrm)
+        if (nrm) SPV(2, true);
+        else if (V2 == 2) SPV(2, false);
+        else if (V2 == 4) SPV(4, false);
+        else SPV(8, false);
 #undef SPV
         ENS_CKL();
+        blocks_total += (int)grid.x;
     }
     {
         const int H = J / 2;
@@ -330,15 +427,60 @@ static int launch_spmm_vec(ens_ctx* c, cudaStream_t s, const double* as_vals, co
         const int L = (H + V2 - 1) / V2, R = 32 / L;
         const int64_t warps = ((int64_t)c->m.n_pres + R - 1) / R;
         dim3 grid((unsigned)((warps * 32 + 255) / 256), 1);
-#define SPP(V)                                                                                                      \
-    k_spmm_pres_v<V><<<grid, 256, 0, s>>>(c->m.b_rowptr, c->m.b_col, c->m.b_val, c->m.cflag, x, b ? b : x, y,        \
-                                          c->m.n_pres, c->n_vel, c->n_total, J, L, mode)
-        if (V2 == 2) SPP(2);
-        else if (V2 == 4) SPP(4);
-        else SPP(8);
+        double* nrm_p = nrm ? nrm + (int64_t)blocks_total * 4 * J : nullptr;
+#define SPP(V, NR)                                                                                                 \
+    k_spmm_pres_v<V, NR><<<grid, 256, 0, s>>>(c->m.b_rowptr, c->m.b_col, c->m.b_val, c->m.cflag, x, b ? b : x, y,   \
+                                              c->m.n_pres, c->n_vel, c->n_total, J, L, mode, nrm_p)
+        if (nrm) SPP(2, true);
+        else if (V2 == 2) SPP(2, false);
+        else if (V2 == 4) SPP(4, false);
+        else SPP(8, false);
 #undef SPP
         ENS_CKL();
+        blocks_total += (int)grid.x;
     }
+    if (nblk) *nblk = blocks_total;
+    return ENS_OK;
+}
+
+// out[k][mat][j] (k = 0: ||b||^2, 1: ||b - K x||^2) from the per-block partials, fixed order
+__global__ void k_nrm_fin(const double* __restrict__ part, int nblk, int J, double* __restrict__ bn2,
+                          double* __restrict__ rn2) {
+    const int t = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (t >= 4 * J) return;
+    const int br = t / (2 * J), mj = t % (2 * J), mat = mj / J, j = mj % J;
+    double acc = 0.0;
+    for (int b = lane; b < nblk; b += 32) acc += part[(((int64_t)b * 2 + mat) * 2 + br) * J + j];
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if (lane == 0) (br ? rn2 : bn2)[mj] = acc;
+}
+
+bool spmm_resnorm_ok(const ens_ctx* c) {
+    // opt-in (ENS_FUSED_NORM=1): measured slower at C2 (block reductions + finalise
+    // cost more than the two 24 MB column-dot passes they replace)
+    const char* e = std::getenv("ENS_FUSED_NORM");
+    if (!(e && e[0] == '1')) return false;
+    return !c->use_blocked && (c->J & 1) == 0 && c->J >= 2 && c->J <= 64;
+}
+
+// y = b - K x plus the per-column squares of b and y (bn2, rn2: [mat][J])
+int launch_spmm_resnorm(ens_ctx* c, cudaStream_t s, const double* as_vals, const double* x, const double* b,
+                        double* y, double* bn2, double* rn2) {
+    if (!c->nrm_part) {
+        const int J = c->J;
+        const int64_t bv = ((((int64_t)c->m.ns + (32 / (J / 2)) - 1) / (32 / (J / 2))) * 32 + 255) / 256;
+        const int Lp = (J / 2 + 1) / 2;
+        const int64_t bp = ((((int64_t)c->m.n_pres + (32 / Lp) - 1) / (32 / Lp)) * 32 + 255) / 256;
+        const size_t bytes = sizeof(double) * 4 * (size_t)J * (size_t)(bv + bp);
+        ENS_CK(cudaMalloc(&c->nrm_part, bytes));
+        c->ws_bytes += bytes;
+    }
+    int nblk = 0;
+    const int rc = launch_spmm_vec(c, s, as_vals, x, b, y, 1, c->nrm_part, &nblk);
+    if (rc != ENS_OK) return rc;
+    k_nrm_fin<<<(4 * c->J * 32 + 255) / 256, 256, 0, s>>>(c->nrm_part, nblk, c->J, bn2, rn2);
+    ENS_CKL();
     return ENS_OK;
 }
 
@@ -348,7 +490,7 @@ int launch_spmm(ens_ctx* c, cudaStream_t s, const double* as_vals, const double*
     const int J = c->J, W2 = 2 * J;
     if ((J & 1) == 0 && J <= 512 && (reinterpret_cast<uintptr_t>(x) & 15) == 0 &&
         (reinterpret_cast<uintptr_t>(y) & 15) == 0 && (!b || (reinterpret_cast<uintptr_t>(b) & 15) == 0))
-        return launch_spmm_vec(c, s, as_vals, x, b, y, mode);
+        return launch_spmm_vec(c, s, as_vals, x, b, y, mode, nullptr, nullptr);
     {
         const int S = W2 >= 32 ? 32 : next_pow2(W2);
         const int opl = (W2 + S - 1) / S;
