@@ -411,6 +411,91 @@ __global__ void __launch_bounds__(256) k_update(MfDev d, int item0, double* __re
     }
 }
 
+// UPDATE on the fp64 tensor cores with one asynchronous staging round trip:
+// the output tile C (64 x 64, rows/cols outside the panel) is prefetched into the
+// accumulator fragments while A = F[Q-rows, P] and B = F[P, Q-cols] stream into
+// shared memory by cp.async (zero-filled past the panel width); then
+// C += (-A) B with mma.sync m8n8k4 (warp w: rows 8w..8w+7, all 8 column tiles)
+// and C is stored straight from the fragments.
+#define UP_LD 68   // = 4 (mod 16) doubles: conflict-free m8n8k4 fragment reads
+__device__ __forceinline__ void up_cp8(double* sdst, const double* g, bool pred) {
+    const unsigned sa = (unsigned)__cvta_generic_to_shared(sdst);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(sa), "l"(g), "r"(pred ? 8 : 0));
+}
+__device__ __forceinline__ void up_mma(double& d0, double& d1, double a, double b) {
+    asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+        : "+d"(d0), "+d"(d1)
+        : "d"(a), "d"(b));
+}
+
+__global__ void __launch_bounds__(256, 2) k_update2(MfDev d, int item0, double* __restrict__ F) {
+    extern __shared__ double sm[];
+    double* As = sm;                    // [64 rows][UP_LD]   A[r][k]
+    double* Bs = sm + 64 * UP_LD;       // [64 k][UP_LD]      B[k][c]
+    const int* it = d.work + 4LL * (item0 + blockIdx.x);
+    const int f = it[0], a = it[1], r0 = it[2], c0 = it[3];
+    const int mat = blockIdx.y;
+    const int m = d.m[f];
+    const int pw = min(ENS_PW, d.k[f] - a);
+    const int t = m - pw;
+    const int nr = min(ENS_TILE, t - r0), nc = min(ENS_TILE, t - c0);
+    double* base = F + (int64_t)mat * d.storage + d.off[f];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, g = lane >> 2, q = lane & 3;
+    // (1) operands -> shared memory (one commit group); row r = e >> 6, inner kk = e & 63
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+        const int e = tid + 256 * i, r = e >> 6, kk = e & 63;
+        const bool ok = r < nr && kk < pw;
+        up_cp8(&As[r * UP_LD + kk], ok ? base + (int64_t)outside(r0 + r, a, pw) * m + a + kk : base, ok);
+    }
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+        const int e = tid + 256 * i, kk = e >> 6, cc = e & 63;
+        const bool ok = kk < pw && cc < nc;
+        up_cp8(&Bs[kk * UP_LD + cc], ok ? base + (int64_t)(a + kk) * m + outside(c0 + cc, a, pw) : base, ok);
+    }
+    asm volatile("cp.async.commit_group;\n" ::);
+    // (2) C fragments (row 8w+g, cols 8ct + 2q + {0,1}) in flight meanwhile
+    const int row = 8 * warp + g;
+    const bool row_ok = row < nr;
+    double* crow = base + (int64_t)outside(r0 + (row_ok ? row : 0), a, pw) * m;
+    double acc[8][2];
+#pragma unroll
+    for (int ct = 0; ct < 8; ++ct)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+            const int cc = 8 * ct + 2 * q + e;
+            acc[ct][e] = (row_ok && cc < nc) ? crow[outside(c0 + cc, a, pw)] : 0.0;
+        }
+    asm volatile("cp.async.wait_group 0;\n" ::);
+    __syncthreads();
+    // (3) C -= A B
+    const double* ap = As + row * UP_LD + q;
+    const double* bp = Bs + q * UP_LD + g;
+    const int ksteps = (pw + 3) >> 2;
+#pragma unroll 4
+    for (int u = 0; u < ksteps; ++u) {
+        const double av = -ap[4 * u];
+#pragma unroll
+        for (int ct = 0; ct < 8; ++ct) up_mma(acc[ct][0], acc[ct][1], av, bp[4 * u * UP_LD + 8 * ct]);
+    }
+    // (4) store
+    if (!row_ok) return;
+#pragma unroll
+    for (int ct = 0; ct < 8; ++ct)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+            const int cc = 8 * ct + 2 * q + e;
+            if (cc < nc) crow[outside(c0 + cc, a, pw)] = acc[ct][e];
+        }
+}
+static const size_t SM_UP2 = sizeof(double) * 2 * 64 * UP_LD;
+
+static bool update2_enabled() {
+    const char* e = std::getenv("ENS_UPDATE_OLD");
+    return !(e && e[0] == '1');
+}
+
 // GPANEL: F[Q-tile, P] <- F[Q-tile, P] D^-1
 __global__ void __launch_bounds__(256) k_gpanel(MfDev d, int item0, double* __restrict__ F) {
     extern __shared__ double sm[];
@@ -464,6 +549,7 @@ void launch_gpanel_mma(const MfDev& d, int off, int n, double* F, cudaStream_t s
 int mf_setup(ens_ctx* c) {
     ENS_CK(cudaFuncSetAttribute(k_hpanel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SM_HP));
     ENS_CK(cudaFuncSetAttribute(k_update, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SM_UP));
+    ENS_CK(cudaFuncSetAttribute(k_update2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SM_UP2));
     ENS_CK(cudaFuncSetAttribute(k_gpanel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SM_GP));
     const char* e = std::getenv("ENS_MMA");
     // DMMA panel kernels measured slower than the DFMA ones at C2 (15.0 vs 10.4 ms
@@ -514,6 +600,8 @@ static int mf_factor_launches(ens_ctx* c, cudaStream_t s, const double* as_vals,
             case OP_UPDATE:
                 if (c->use_mma)
                     launch_update_mma(d, off, n, c->fronts, s);
+                else if (update2_enabled())
+                    k_update2<<<dim3(n, 2), 256, SM_UP2, s>>>(d, off, c->fronts);
                 else
                     k_update<<<dim3(n, 2), 256, SM_UP, s>>>(d, off, c->fronts);
                 break;
