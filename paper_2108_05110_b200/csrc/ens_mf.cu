@@ -491,6 +491,73 @@ __global__ void __launch_bounds__(256, 2) k_update2(MfDev d, int item0, double* 
 }
 static const size_t SM_UP2 = sizeof(double) * 2 * 64 * UP_LD;
 
+// HPANEL / GPANEL with the same staging + tensor-core pattern (in place: the
+// operand being overwritten is staged completely before any store).
+//   HPANEL: F[P, Q-tile] <- (-F[P,P]) F[P, Q-tile]      (D^-1 = -F[P,P])
+//   GPANEL: F[Q-tile, P] <- F[Q-tile, P] (-F[P,P])
+template <bool H>
+__global__ void __launch_bounds__(256, 2) k_panel2(MfDev d, int item0, double* __restrict__ F) {
+    extern __shared__ double sm[];
+    double* As = sm;                    // [64][UP_LD]
+    double* Bs = sm + 64 * UP_LD;       // [64][UP_LD]
+    const int* it = d.work + 4LL * (item0 + blockIdx.x);
+    const int f = it[0], a = it[1], x0 = it[2];
+    const int mat = blockIdx.y;
+    const int m = d.m[f];
+    const int pw = min(ENS_PW, d.k[f] - a);
+    const int t = m - pw;
+    const int nx = min(ENS_TILE, t - x0);          // HPANEL: tile columns, GPANEL: tile rows
+    double* base = F + (int64_t)mat * d.storage + d.off[f];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, g = lane >> 2, q = lane & 3;
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+        const int e = tid + 256 * i, r = e >> 6, cc = e & 63;
+        // D = F[P,P] (A of HPANEL, B of GPANEL)
+        const bool okd = r < pw && cc < pw;
+        up_cp8(&(H ? As : Bs)[r * UP_LD + cc], okd ? base + (int64_t)(a + r) * m + a + cc : base, okd);
+        if (H) {   // B = F[P, Q-tile]: rows r < pw, cols cc < nx
+            const bool ok = r < pw && cc < nx;
+            up_cp8(&Bs[r * UP_LD + cc], ok ? base + (int64_t)(a + r) * m + outside(x0 + cc, a, pw) : base, ok);
+        } else {   // A = F[Q-tile, P]: rows r < nx, cols cc < pw
+            const bool ok = r < nx && cc < pw;
+            up_cp8(&As[r * UP_LD + cc], ok ? base + (int64_t)outside(x0 + r, a, pw) * m + a + cc : base, ok);
+        }
+    }
+    asm volatile("cp.async.commit_group;\n" ::);
+    asm volatile("cp.async.wait_group 0;\n" ::);
+    __syncthreads();
+    const int row = 8 * warp + g;
+    const double* ap = As + row * UP_LD + q;
+    const double* bp = Bs + q * UP_LD + g;
+    double acc[8][2];
+#pragma unroll
+    for (int ct = 0; ct < 8; ++ct) acc[ct][0] = acc[ct][1] = 0.0;
+    const int ksteps = (pw + 3) >> 2;
+#pragma unroll 4
+    for (int u = 0; u < ksteps; ++u) {
+        const double av = -ap[4 * u];   // one operand is -F[P,P]: negate A (HPANEL) ...
+#pragma unroll
+        for (int ct = 0; ct < 8; ++ct) {
+            const double bv = bp[4 * u * UP_LD + 8 * ct];
+            up_mma(acc[ct][0], acc[ct][1], H ? av : -av, H ? bv : -bv);   // ... or B (GPANEL)
+        }
+    }
+    const int nrow = H ? pw : nx, ncol = H ? nx : pw;
+    if (row >= nrow) return;
+#pragma unroll
+    for (int ct = 0; ct < 8; ++ct)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+            const int cc = 8 * ct + 2 * q + e;
+            if (cc >= ncol) continue;
+            if (H)
+                base[(int64_t)(a + row) * m + outside(x0 + cc, a, pw)] = acc[ct][e];
+            else
+                base[(int64_t)outside(x0 + row, a, pw) * m + a + cc] = acc[ct][e];
+        }
+}
+
+
 static bool update2_enabled() {
     const char* e = std::getenv("ENS_UPDATE_OLD");
     return !(e && e[0] == '1');
@@ -550,6 +617,8 @@ int mf_setup(ens_ctx* c) {
     ENS_CK(cudaFuncSetAttribute(k_hpanel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SM_HP));
     ENS_CK(cudaFuncSetAttribute(k_update, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SM_UP));
     ENS_CK(cudaFuncSetAttribute(k_update2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SM_UP2));
+    ENS_CK(cudaFuncSetAttribute(k_panel2<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SM_UP2));
+    ENS_CK(cudaFuncSetAttribute(k_panel2<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SM_UP2));
     ENS_CK(cudaFuncSetAttribute(k_gpanel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SM_GP));
     const char* e = std::getenv("ENS_MMA");
     // DMMA panel kernels measured slower than the DFMA ones at C2 (15.0 vs 10.4 ms
@@ -594,6 +663,8 @@ static int mf_factor_launches(ens_ctx* c, cudaStream_t s, const double* as_vals,
             case OP_HPANEL:
                 if (c->use_mma)
                     launch_hpanel_mma(d, off, n, c->fronts, s);
+                else if (update2_enabled())
+                    k_panel2<true><<<dim3(n, 2), 256, SM_UP2, s>>>(d, off, c->fronts);
                 else
                     k_hpanel<<<dim3(n, 2), 256, SM_HP, s>>>(d, off, c->fronts);
                 break;
@@ -608,6 +679,8 @@ static int mf_factor_launches(ens_ctx* c, cudaStream_t s, const double* as_vals,
             case OP_GPANEL:
                 if (c->use_mma)
                     launch_gpanel_mma(d, off, n, c->fronts, s);
+                else if (update2_enabled())
+                    k_panel2<false><<<dim3(n, 2), 256, SM_UP2, s>>>(d, off, c->fronts);
                 else
                     k_gpanel<<<dim3(n, 2), 256, SM_GP, s>>>(d, off, c->fronts);
                 break;
