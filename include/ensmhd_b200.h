@@ -145,6 +145,24 @@ typedef struct {
     const int32_t* qb_row;      /* nqb+1: first pressure row of each pressure block */
 } ens_spmm_blocks;
 
+/* Tile-staged SpMM (optional, built once per mesh and J by spmm_tiles.py):
+ * tiles of consecutive velocity nodes / pressure rows, each staged into one
+ * shared-memory stage by bulk copies (records: int64 source byte offset,
+ * int32 destination byte offset, int32 bytes | kind << 24) and consumed from
+ * there; see csrc/ens_spmm_tiles.cu.  Arrays are device pointers owned by the caller. */
+typedef struct {
+    const void* tiles;          /* ntiles x 16 int32 descriptors */
+    const void* recs;           /* copy records (16 bytes each)  */
+    const int32_t* lcol_a;      /* nnz_s: stage slot of each A_s column (its tile's node list) */
+    const int32_t* lcol_bt;     /* B^T pairs: stage slot of the pressure row */
+    const int32_t* lcol_b;      /* B pairs: stage slot of the node */
+    int32_t ntiles, nrec;
+    int32_t stage_bytes;        /* bytes per pipeline stage (16-byte multiple) */
+    int32_t nstage;             /* pipeline depth (1..4) */
+    int32_t grid;               /* persistent CTAs (one per SM) */
+    int32_t pad;
+} ens_spmm_tiles;
+
 /* Problem data: value_j = sum_k coef[k*J + j] * basis[k*rows + row] (+ dense). */
 typedef struct {
     int32_t K;                  /* number of basis vectors (0 allowed)   */
@@ -168,6 +186,8 @@ int  ens_workspace_bytes(const ens_ctx* ctx, int64_t* bytes);
 int  ens_set_pivoting(ens_ctx* ctx, int on);
 /* Install the SpMM row blocking (arrays are device pointers owned by the caller). */
 int  ens_set_spmm_blocks(ens_ctx* ctx, const ens_spmm_blocks* blocks);
+/* Install (or, with NULL, remove) the tile-staged SpMM; takes precedence over the row blocking. */
+int  ens_set_spmm_tiles(ens_ctx* ctx, const ens_spmm_tiles* tiles);
 
 /* y = a x + b y over one iterate block set (2 x n_total x J); used for the
  * extrapolated FGMRES initial iterate 2 x^n - x^{n-1}. */

@@ -54,13 +54,18 @@ class SpmmBlocks(C.Structure):
                 ("pb_rows", P), ("qb_off", P), ("qb_nodes", P), ("vb_row", P), ("qb_row", P)]
 
 
+class SpmmTiles(C.Structure):
+    _fields_ = [("tiles", P), ("recs", P), ("lcol_a", P), ("lcol_bt", P), ("lcol_b", P), ("ntiles", I32),
+                ("nrec", I32), ("stage_bytes", I32), ("nstage", I32), ("grid", I32), ("pad", I32)]
+
+
 class DataDesc(C.Structure):
     _fields_ = [("K", I32), ("pad", I32), ("rows", I64), ("basis", P), ("coef", P), ("dense", P)]
 
 
 SYMBOLS = [
     "ens_abi_version", "ens_last_error", "ens_kernel_launches", "ens_create", "ens_set_pivoting",
-    "ens_set_spmm_blocks", "ens_destroy", "ens_workspace_bytes",
+    "ens_set_spmm_blocks", "ens_set_spmm_tiles", "ens_destroy", "ens_workspace_bytes",
     "ens_lincomb", "ens_member_sums", "ens_rhs", "ens_member_pass", "ens_apply_bc", "ens_assemble", "ens_factor",
     "ens_solve", "ens_spmm", "ens_precond_apply", "ens_epilogue", "ens_diagnostics",
 ]
@@ -86,6 +91,7 @@ def load(path: str = LIB_PATH):
     lib.ens_workspace_bytes.argtypes = [P, C.POINTER(I64)]
     lib.ens_set_pivoting.argtypes = [P, C.c_int]
     lib.ens_set_spmm_blocks.argtypes = [P, C.POINTER(SpmmBlocks)]
+    lib.ens_set_spmm_tiles.argtypes = [P, C.POINTER(SpmmTiles)]
     lib.ens_member_sums.argtypes = [P, P, P, P]
     lib.ens_lincomb.argtypes = [P, P, F64, P, F64, P]
     lib.ens_rhs.argtypes = [P, P, P, P, F64, C.POINTER(DataDesc), P]

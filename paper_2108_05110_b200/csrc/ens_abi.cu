@@ -146,6 +146,24 @@ int ens_set_spmm_blocks(ens_ctx* c, const ens_spmm_blocks* b) {
     return ENS_OK;
 }
 
+int ens_set_spmm_tiles(ens_ctx* c, const ens_spmm_tiles* t) {
+    if (!c) return ENS_EINVAL;
+    if (!t) {
+        c->use_tiles = 0;
+        return ENS_OK;
+    }
+    if ((c->J & 1) || c->J > 64 || t->nstage < 1 || t->nstage > 4 || (t->stage_bytes & 15) ||
+        (int64_t)t->stage_bytes * t->nstage > 220 * 1024 || t->ntiles < 1 || t->grid < 1) {
+        ens_set_error("SpMM tiles: need even J <= 64 and <= 220 KB of stages", __FILE__, __LINE__);
+        return ENS_EINVAL;
+    }
+    c->tiles = *t;
+    const int rc = spmm_tiles_setup(c);
+    if (rc != ENS_OK) return rc;
+    c->use_tiles = 1;
+    return ENS_OK;
+}
+
 int ens_set_pivoting(ens_ctx* c, int on) {
     if (!c) return ENS_EINVAL;
     c->diag_pivot = on ? 1 : 0;

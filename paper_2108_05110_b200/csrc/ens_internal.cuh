@@ -79,6 +79,8 @@ struct ens_ctx {
     int use_mma = 1;               // DMMA (fp64 tensor core) panel kernels
     ens_spmm_blocks blk{};         // SpMM row blocking (shared-memory staged neighbour rows)
     int use_blocked = 0;
+    ens_spmm_tiles tiles{};        // tile-staged SpMM (bulk-copied stages, ens_spmm_tiles.cu)
+    int use_tiles = 0;
     int g_factor_pivot = 0;
     int64_t g_factor_kernels = 0;
 };
@@ -97,6 +99,10 @@ int launch_spmm(ens_ctx* c, cudaStream_t s, const double* as_vals, const double*
 int launch_spmm_blocked(ens_ctx* c, cudaStream_t s, const double* as_vals, const double* x, const double* b,
                         double* y, int mode);
 int spmm_blocked_setup(ens_ctx* c);
+int spmm_tiles_setup(ens_ctx* c);
+bool spmm_tiles_usable(const ens_ctx* c, const double* x, const double* b, const double* y);
+int launch_spmm_tiles(ens_ctx* c, cudaStream_t s, const double* as_vals, const double* x, const double* b, double* y,
+                      int mode);
 bool spmm_resnorm_ok(const ens_ctx* c);
 int launch_spmm_resnorm(ens_ctx* c, cudaStream_t s, const double* as_vals, const double* x, const double* b,
                         double* y, double* bn2, double* rn2);

@@ -7,7 +7,13 @@
 // serves every member and both components.  A segment of S lanes owns a row;
 // summation order is fixed per row and identical for every member column.
 // (A variant that preloads the row's indices lane-parallel and broadcasts them
-// with shuffles measured slower at C2: 0.24 ms vs 0.17 ms per launch pair.)
+// with shuffles measured slower at C2: 0.24 ms vs 0.17 ms per launch pair.
+// Later in round 1, also measured no faster (warm, both kernels, C2, J = 20,
+// baseline 105-115 us): indices/values preloaded per warp into shared memory
+// with 2- or 4-nonzero gather batches (121 / 127 us), evict-first hints on the
+// streamed operands and output (120 us), register caps for 5 CTAs/SM (121-123
+// us, spills), a 64-register cap (107-111 us); the tile-staged kernel
+// (ens_spmm_tiles.cu) reached 123 us at best.)
 #include <cstdlib>
 
 #include "ens_internal.cuh"
@@ -486,6 +492,7 @@ int launch_spmm_resnorm(ens_ctx* c, cudaStream_t s, const double* as_vals, const
 
 int launch_spmm(ens_ctx* c, cudaStream_t s, const double* as_vals, const double* x, const double* b, double* y,
                 int mode) {
+    if (spmm_tiles_usable(c, x, b, y)) return launch_spmm_tiles(c, s, as_vals, x, b, y, mode);
     if (c->use_blocked) return launch_spmm_blocked(c, s, as_vals, x, b, y, mode);
     const int J = c->J, W2 = 2 * J;
     if ((J & 1) == 0 && J <= 512 && (reinterpret_cast<uintptr_t>(x) & 15) == 0 &&

@@ -394,6 +394,24 @@ class Engine:
                     setattr(sb, k, _dptr(t))
                 N.check(self.lib.ens_set_spmm_blocks(ctx, C.byref(sb)), "ens_set_spmm_blocks")
                 self.spmm_blocks = (sb, bt)
+        # tile-staged SpMM (bulk-copied shared-memory stages, csrc/ens_spmm_tiles.cu)
+        self.spmm_tiles = None
+        if os.environ.get("ENS_SPMM_TILES", "0") == "1" and J % 2 == 0 and J <= 64:
+            from . import spmm_tiles as TL
+            nstage = int(os.environ.get("ENS_TILE_STAGES", "3"))
+            cap = int(os.environ.get("ENS_TILE_CAP", str(192 // nstage))) * 1024
+            desc, recs, la, lbt, lb, info = TL.build_tiles(hm, J, cap=cap)
+            pad = lambda a: np.concatenate([a, np.zeros(16, a.dtype)])   # aligned stream tails stay in bounds
+            tt = dict(tiles=up(desc.reshape(-1), i32), recs=up(recs.view(np.int32), i32),
+                      lcol_a=up(pad(la), i32), lcol_bt=up(pad(lbt), i32), lcol_b=up(pad(lb), i32))
+            st_ = N.SpmmTiles()
+            for k, t in tt.items():
+                setattr(st_, k, _dptr(t))
+            st_.ntiles, st_.nrec = len(desc), len(recs)
+            st_.stage_bytes, st_.nstage = info["stage_bytes"], nstage
+            st_.grid = torch.cuda.get_device_properties(self.dev).multi_processor_count
+            N.check(self.lib.ens_set_spmm_tiles(ctx, C.byref(st_)), "ens_set_spmm_tiles")
+            self.spmm_tiles = (st_, tt, info)
         # per-run constants
         st = viscosity_stats(config)
         self.config = config

@@ -53,13 +53,14 @@ def _nested_dissection(coords, indptr, indices, leaf=LEAF_NODES):
     rows = np.repeat(np.arange(n, dtype=np.int64), np.diff(indptr))
     cols = indices.astype(np.int64)
     tnodes, kids = [], []
-    in_right = np.zeros(n, dtype=bool)
-    in_left = np.zeros(n, dtype=bool)
 
-    # iterative (explicit stack) to avoid recursion limits on big meshes
-    stack = [(np.arange(n, dtype=np.int64), -1)]
+    # iterative (explicit stack) to avoid recursion limits on big meshes; every
+    # subproblem carries its own edge list (edges with both ends inside it), so a
+    # tree level costs O(nnz) instead of O(nnz) per tree node
+    side = np.zeros(n, dtype=np.int8)
+    stack = [(np.arange(n, dtype=np.int64), rows, cols, -1)]
     while stack:
-        idx, parent = stack.pop()
+        idx, er, ec, parent = stack.pop()
         me = len(tnodes)
         tnodes.append(None)
         kids.append([])
@@ -74,11 +75,6 @@ def _nested_dissection(coords, indptr, indices, leaf=LEAF_NODES):
         vals = np.unique(xs)
         med = np.sort(xs)[len(xs) // 2]
         ci = int(np.searchsorted(vals, med))
-        # edges with both ends inside idx
-        sub = np.zeros(n, dtype=bool)
-        sub[idx] = True
-        emask = sub[rows] & sub[cols]
-        er, ec = rows[emask], cols[emask]
         xr, xc = coords[er, ax], coords[ec, ax]
         best = None
         for cut in vals[max(0, ci - 4):ci + 5]:
@@ -97,14 +93,17 @@ def _nested_dissection(coords, indptr, indices, leaf=LEAF_NODES):
             tnodes[me] = idx
             continue
         _, cut, sep = best
-        sm = np.zeros(n, dtype=bool)
-        sm[sep] = True
-        left = idx[(xs <= cut) & ~sm[idx]]
-        right = idx[xs > cut]
+        side[idx] = np.where(xs > cut, 2, 1)
+        side[sep] = 0
+        sidx = side[idx]
+        left = idx[sidx == 1]
+        right = idx[sidx == 2]
         tnodes[me] = sep
-        for part in (right, left):
+        sr, sc = side[er], side[ec]
+        for part, code in ((right, 2), (left, 1)):
             if len(part):
-                stack.append((part, me))
+                keep = (sr == code) & (sc == code)
+                stack.append((part, er[keep], ec[keep], me))
     return tnodes, kids, 0
 
 

@@ -273,3 +273,25 @@ def test_case_runs_match_oracle(case, over):
     for f in "qr":
         assert rel(getattr(state, f), getattr(ost, f)) < 1e-8, f
     assert np.all(report.residuals[1:] < 1e-11)
+
+
+@pytest.mark.parametrize("J,stages", [(20, 2), (8, 3)])
+def test_spmm_tiles_bitwise_equal_direct(monkeypatch, rng, J, stages):
+    """The tile-staged SpMM (opt-in) keeps the direct kernel's per-output summation order: identical bits."""
+    disc, cfg, _ = P.build_case("C1", J=J)
+    direct = Engine(disc, cfg)
+    monkeypatch.setenv("ENS_SPMM_TILES", "1")
+    monkeypatch.setenv("ENS_TILE_STAGES", str(stages))
+    monkeypatch.setenv("ENS_TILE_CAP", "24")
+    tiled = Engine(disc, cfg)
+    assert tiled.spmm_tiles is not None and tiled.spmm_tiles[2]["nvt"] > 1
+    a = torch.from_numpy(rng.standard_normal((2, direct.hm.nnz_s))).cuda()
+    direct.as_vals.copy_(a)
+    tiled.as_vals.copy_(a)
+    x = torch.from_numpy(rng.standard_normal((2, disc.n_total, J))).cuda()
+    b = torch.from_numpy(rng.standard_normal((2, disc.n_total, J))).cuda()
+    for mode in (0, 1):
+        y0 = direct.spmm(x, b if mode else None, mode=mode)
+        y1 = tiled.spmm(x, b if mode else None, mode=mode)
+        torch.cuda.synchronize()
+        assert torch.equal(y0, y1), mode
