@@ -50,6 +50,8 @@ struct ens_ctx {
     double* frvec = nullptr;       // nmat * n_idx * J
     double* kry = nullptr;         // Krylov blocks
     int32_t kry_restart = 0;
+    int32_t kry_short = 0;         // cycle shortened for lack of device memory
+    size_t kry_bytes = 0;
     double* red_part = nullptr;    // reduction partials
     double* red_out = nullptr;     // small outputs
     GmresCol* cols = nullptr;      // nmat*J
@@ -81,6 +83,7 @@ struct ens_ctx {
     int use_blocked = 0;
     ens_spmm_tiles tiles{};        // tile-staged SpMM (bulk-copied stages, ens_spmm_tiles.cu)
     int use_tiles = 0;
+    int spmm_wide = -1;            // wide-member SpMM variant (ENS_SPMM_WIDE, read on first use)
     int g_factor_pivot = 0;
     int64_t g_factor_kernels = 0;
 };

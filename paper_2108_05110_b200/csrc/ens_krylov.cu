@@ -20,23 +20,43 @@ struct GmresCol {
 
 size_t gmres_col_bytes() { return sizeof(GmresCol); }
 
+// Krylov blocks for `restart` vectors; when device memory is short (large
+// meshes x many members) the cycle is shortened instead of failing -- the
+// lagged-preconditioner FGMRES needs 1-3 vectors per cycle and restarts keep
+// the same true-residual stopping test.  Returns the usable cycle length in
+// c->kry_restart.
 int gmres_alloc(ens_ctx* c, int restart) {
     if (restart < 1 || restart > ENS_MAX_RESTART) {
         ens_set_error("restart out of range", __FILE__, __LINE__);
         return ENS_EINVAL;
     }
     if (c->kry && c->kry_restart >= restart) return ENS_OK;
-    if (c->kry) cudaFree(c->kry);
-    const size_t blk = 2ull * (size_t)c->n_total * c->J;
-    const size_t nblk = 2 * (size_t)restart + 3;   // V[0..R], Z[0..R-1], R, W
-    if (cudaMalloc(&c->kry, sizeof(double) * blk * nblk) != cudaSuccess) {
+    if (c->kry && c->kry_short) return ENS_OK;   // already shortened for memory: keep it
+    if (c->kry) {
+        cudaFree(c->kry);
+        c->ws_bytes -= c->kry_bytes;
         c->kry = nullptr;
-        ens_set_error("out of device memory for Krylov blocks", __FILE__, __LINE__);
-        return ENS_ENOMEM;
     }
-    c->ws_bytes += sizeof(double) * blk * nblk;
-    c->kry_restart = restart;
-    return ENS_OK;
+    const size_t blk = 2ull * (size_t)c->n_total * c->J;
+    // leave room for the solve's lazily allocated workspace (split-K partials, graphs)
+    size_t free_b = 0, total_b = 0;
+    if (cudaMemGetInfo(&free_b, &total_b) != cudaSuccess) free_b = total_b = 0;
+    const size_t reserve = std::max<size_t>(size_t(4) << 30, total_b / 20);
+    for (int r = restart; r >= 2; --r) {
+        const size_t nblk = 2 * (size_t)r + 3;   // V[0..R], Z[0..R-1], R, W
+        if (r > 2 && free_b && sizeof(double) * blk * nblk + reserve > free_b) continue;
+        if (cudaMalloc(&c->kry, sizeof(double) * blk * nblk) == cudaSuccess) {
+            c->kry_bytes = sizeof(double) * blk * nblk;
+            c->ws_bytes += c->kry_bytes;
+            c->kry_restart = r;
+            c->kry_short = r < restart ? 1 : 0;
+            return ENS_OK;
+        }
+        cudaGetLastError();   // clear the allocation failure
+        c->kry = nullptr;
+    }
+    ens_set_error("out of device memory for Krylov blocks", __FILE__, __LINE__);
+    return ENS_ENOMEM;
 }
 
 // scalar buffers inside red_out:  [bn2 | rn2 | h1 | h2 | hn2 | scale | y]
@@ -233,6 +253,7 @@ static int read_count(ens_ctx* c, cudaStream_t s, int* out) {
 int gmres_solve(ens_ctx* c, cudaStream_t s, const double* as_vals, const double* rhs, double* x, double rtol,
                 int restart, int max_restarts, int32_t* iters, double* relres) {
     RET(gmres_alloc(c, restart));
+    restart = std::min(restart, c->kry_restart);
     const int J = c->J;
     const int n = 2 * J;
     const int64_t N = c->n_total;

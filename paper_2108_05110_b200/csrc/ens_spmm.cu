@@ -406,6 +406,292 @@ __global__ void __launch_bounds__(256) k_spmm_pres_v(const int32_t* __restrict__
     }
 }
 
+// ---------------------------------------------------------------------------
+// Wide-member variants (J >= 64: one row per warp, lanes over member pairs).
+// The row's CSR entries are loaded lane-parallel once (one coalesced load per
+// stream instead of a dependent index load per nonzero) and broadcast with
+// shuffles, so U nonzeros' gathers (U x 2 systems x V2 16-byte loads per
+// lane) are in flight together.  Per-output summation order is the CSR order
+// of the kernels above.
+// ---------------------------------------------------------------------------
+template <int V2, int U>
+__global__ void __launch_bounds__(256) k_spmm_vel_w(const int32_t* __restrict__ rp, const int32_t* __restrict__ col,
+                                                    const double* __restrict__ A, int nnz,
+                                                    const int32_t* __restrict__ btp, const int32_t* __restrict__ btc,
+                                                    const double* __restrict__ btv, const uint8_t* __restrict__ cflag,
+                                                    const double* __restrict__ X, const double* __restrict__ Bv,
+                                                    double* __restrict__ Y, int ns, int64_t N, int J, int mode) {
+    const int lane = threadIdx.x & 31;
+    const int64_t node = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    if (node >= ns) return;
+    const int H = J >> 1;
+    const int64_t MS = N * H;
+    const double2* X2 = reinterpret_cast<const double2*>(X);
+    double2* Y2 = reinterpret_cast<double2*>(Y);
+    const double2* B2 = reinterpret_cast<const double2*>(Bv);
+    const int64_t nvel = 2LL * ns;
+    const int k0 = rp[node], n = rp[node + 1] - k0;
+    const int t0 = btp[node], np = btp[node + 1] - t0;
+    int myc = (int)node, myp = 0;
+    double mya0 = 0.0, mya1 = 0.0;
+    double2 myb = make_double2(0.0, 0.0);
+    if (lane < n) {
+        myc = col[k0 + lane];
+        mya0 = A[k0 + lane];
+        mya1 = A[nnz + k0 + lane];
+    }
+    if (lane < np) {
+        myp = btc[t0 + lane];
+        myb = reinterpret_cast<const double2*>(btv)[t0 + lane];
+    }
+    double2 acc[2][V2];
+#pragma unroll
+    for (int m = 0; m < 2; ++m)
+#pragma unroll
+        for (int v = 0; v < V2; ++v) acc[m][v] = make_double2(0.0, 0.0);
+    const int nc = min(n, 32);
+    for (int k = 0; k < nc; k += U) {
+        int64_t c[U];
+        double a0[U], a1[U];
+        bool ok[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int src = (k + u) & 31;
+            c[u] = __shfl_sync(0xffffffffu, myc, src);
+            a0[u] = __shfl_sync(0xffffffffu, mya0, src);
+            a1[u] = __shfl_sync(0xffffffffu, mya1, src);
+            ok[u] = k + u < nc;
+            if (!ok[u]) c[u] = node;   // in-bounds dummy gather, not accumulated
+        }
+        double2 x0[U][V2], x1[U][V2];
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+#pragma unroll
+            for (int v = 0; v < V2; ++v) {
+                const int64_t o = c[u] * J + lane + 32 * v;
+                x0[u][v] = X2[o];
+                x1[u][v] = X2[MS + o];
+            }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            if (!ok[u]) continue;
+#pragma unroll
+            for (int v = 0; v < V2; ++v) {
+                acc[0][v].x = fma(a0[u], x0[u][v].x, acc[0][v].x);
+                acc[0][v].y = fma(a0[u], x0[u][v].y, acc[0][v].y);
+                acc[1][v].x = fma(a1[u], x1[u][v].x, acc[1][v].x);
+                acc[1][v].y = fma(a1[u], x1[u][v].y, acc[1][v].y);
+            }
+        }
+    }
+    for (int k = 32; k < n; ++k) {   // rows longer than a warp (not produced by P2 meshes)
+        const int64_t c0 = col[k0 + k];
+        const double a00 = A[k0 + k], a10 = A[nnz + k0 + k];
+#pragma unroll
+        for (int v = 0; v < V2; ++v) {
+            const int64_t o = c0 * J + lane + 32 * v;
+            const double2 x00 = X2[o], x10 = X2[MS + o];
+            acc[0][v].x = fma(a00, x00.x, acc[0][v].x);
+            acc[0][v].y = fma(a00, x00.y, acc[0][v].y);
+            acc[1][v].x = fma(a10, x10.x, acc[1][v].x);
+            acc[1][v].y = fma(a10, x10.y, acc[1][v].y);
+        }
+    }
+    // pressure couplings: member pair i = lane + 32 v of component (i >= H) reads pressure pair i mod H
+    const double2* P2 = X2 + nvel * H;
+    const int npc = min(np, 32);
+    for (int t = 0; t < npc; ++t) {
+        const int64_t p0 = __shfl_sync(0xffffffffu, myp, t);
+        const double bx = __shfl_sync(0xffffffffu, myb.x, t), by = __shfl_sync(0xffffffffu, myb.y, t);
+#pragma unroll
+        for (int v = 0; v < V2; ++v) {
+            const int i = lane + 32 * v;
+            const bool ycomp = i >= H;
+            const int64_t o = p0 * H + (ycomp ? i - H : i);
+            const double2 x0 = P2[o], x1 = P2[MS + o];
+            const double f0 = ycomp ? by : bx;
+            acc[0][v].x -= f0 * x0.x;
+            acc[0][v].y -= f0 * x0.y;
+            acc[1][v].x -= f0 * x1.x;
+            acc[1][v].y -= f0 * x1.y;
+        }
+    }
+    for (int t = 32; t < np; ++t) {
+        const double2 b0 = reinterpret_cast<const double2*>(btv)[t0 + t];
+        const int64_t p0 = btc[t0 + t];
+#pragma unroll
+        for (int v = 0; v < V2; ++v) {
+            const int i = lane + 32 * v;
+            const bool ycomp = i >= H;
+            const int64_t o = p0 * H + (ycomp ? i - H : i);
+            const double2 x0 = P2[o], x1 = P2[MS + o];
+            const double f0 = ycomp ? b0.y : b0.x;
+            acc[0][v].x -= f0 * x0.x;
+            acc[0][v].y -= f0 * x0.y;
+            acc[1][v].x -= f0 * x1.x;
+            acc[1][v].y -= f0 * x1.y;
+        }
+    }
+#pragma unroll
+    for (int v = 0; v < V2; ++v) {
+        const int i = lane + 32 * v;
+        const int64_t o = node * J + i;
+        const bool ident = cflag[2 * node + (i >= H ? 1 : 0)] != 0;
+#pragma unroll
+        for (int m = 0; m < 2; ++m) {
+            double2 val = ident ? X2[m * MS + o] : acc[m][v];
+            if (mode == 1) {
+                const double2 bb = B2[m * MS + o];
+                val = make_double2(bb.x - val.x, bb.y - val.y);
+            }
+            Y2[m * MS + o] = val;
+        }
+    }
+}
+
+// pressure rows, J >= 64: one row per warp, lane pairs i = lane + 32 v of each component
+template <int V2, int U>
+__global__ void __launch_bounds__(256) k_spmm_pres_w(const int32_t* __restrict__ bp, const int32_t* __restrict__ bc,
+                                                     const double* __restrict__ bv, const uint8_t* __restrict__ cflag,
+                                                     const double* __restrict__ X, const double* __restrict__ Bv,
+                                                     double* __restrict__ Y, int npres, int64_t nvel, int64_t N,
+                                                     int J, int mode) {
+    const int lane = threadIdx.x & 31;
+    const int64_t p = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    if (p >= npres) return;
+    const int H = J >> 1;
+    const int64_t MS = N * H;
+    const double2* X2 = reinterpret_cast<const double2*>(X);
+    double2* Y2 = reinterpret_cast<double2*>(Y);
+    const double2* B2 = reinterpret_cast<const double2*>(Bv);
+    const int t0 = bp[p], n = bp[p + 1] - t0;
+    int myc = 0;
+    double2 myb = make_double2(0.0, 0.0);
+    if (lane < n) {
+        myc = bc[t0 + lane];
+        myb = reinterpret_cast<const double2*>(bv)[t0 + lane];
+    }
+    double2 acc[2][V2];
+#pragma unroll
+    for (int m = 0; m < 2; ++m)
+#pragma unroll
+        for (int v = 0; v < V2; ++v) acc[m][v] = make_double2(0.0, 0.0);
+    const int nc = min(n, 32);
+    for (int k = 0; k < nc; k += U) {
+        int64_t c[U];
+        double bx[U], by[U];
+        bool ok[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int src = (k + u) & 31;
+            c[u] = __shfl_sync(0xffffffffu, myc, src);
+            bx[u] = __shfl_sync(0xffffffffu, myb.x, src);
+            by[u] = __shfl_sync(0xffffffffu, myb.y, src);
+            ok[u] = k + u < nc;
+            if (!ok[u]) c[u] = 0;
+        }
+        double2 uu[U][2][V2], ww[U][2][V2];
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+#pragma unroll
+            for (int m = 0; m < 2; ++m)
+#pragma unroll
+                for (int v = 0; v < V2; ++v) {
+                    const int i = lane + 32 * v;
+                    const int64_t o = m * MS + c[u] * J + (i < H ? i : 0);
+                    uu[u][m][v] = X2[o];
+                    ww[u][m][v] = X2[o + H];
+                }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            if (!ok[u]) continue;
+#pragma unroll
+            for (int m = 0; m < 2; ++m)
+#pragma unroll
+                for (int v = 0; v < V2; ++v) {
+                    acc[m][v].x += bx[u] * uu[u][m][v].x + by[u] * ww[u][m][v].x;
+                    acc[m][v].y += bx[u] * uu[u][m][v].y + by[u] * ww[u][m][v].y;
+                }
+        }
+    }
+    for (int k = 32; k < n; ++k) {
+        const double2 b0 = reinterpret_cast<const double2*>(bv)[t0 + k];
+        const int64_t n0 = bc[t0 + k];
+#pragma unroll
+        for (int m = 0; m < 2; ++m)
+#pragma unroll
+            for (int v = 0; v < V2; ++v) {
+                const int i = lane + 32 * v;
+                if (i < H) {
+                    const double2 u0 = X2[m * MS + n0 * J + i], w0 = X2[m * MS + n0 * J + H + i];
+                    acc[m][v].x += b0.x * u0.x + b0.y * w0.x;
+                    acc[m][v].y += b0.x * u0.y + b0.y * w0.y;
+                }
+            }
+    }
+    const int64_t row = nvel + p;
+    const bool ident = cflag[row] != 0;
+#pragma unroll
+    for (int v = 0; v < V2; ++v) {
+        const int i = lane + 32 * v;
+        if (i >= H) continue;
+#pragma unroll
+        for (int m = 0; m < 2; ++m) {
+            const int64_t o = m * MS + row * H + i;
+            double2 val = ident ? X2[o] : acc[m][v];
+            if (mode == 1) {
+                const double2 bb = B2[o];
+                val = make_double2(bb.x - val.x, bb.y - val.y);
+            }
+            Y2[o] = val;
+        }
+    }
+}
+
+// ENS_SPMM_WIDE (read once per context): 1 (default) on, 0 off (the direct kernels)
+static int spmm_wide_variant(ens_ctx* c) {
+    if (c->spmm_wide < 0) {
+        const char* e = std::getenv("ENS_SPMM_WIDE");
+        c->spmm_wide = e ? std::atoi(e) : 1;
+    }
+    return c->spmm_wide;
+}
+
+// J in {64, 128, 192, 256} (multiples of 64): one row per warp; returns false when not applicable
+static bool launch_spmm_wide(ens_ctx* c, cudaStream_t s, const double* as_vals, const double* x, const double* b,
+                             double* y, int mode) {
+    const int J = c->J;
+    const int wv = spmm_wide_variant(c);
+    if (wv == 0 || J % 64 != 0 || J > 256) return false;
+    const int V2 = J / 32;   // double2 per lane per system (velocity rows: 2J doubles = J double2)
+    const dim3 gv((unsigned)(((int64_t)c->m.ns * 32 + 255) / 256));
+    const dim3 gp((unsigned)(((int64_t)c->m.n_pres * 32 + 255) / 256));
+#define WV(V, UU)                                                                                                  \
+    k_spmm_vel_w<V, UU><<<gv, 256, 0, s>>>(c->m.s_rowptr, c->m.s_col, as_vals, c->m.nnz_s, c->m.bt_rowptr,          \
+                                           c->m.bt_col, c->m.bt_val, c->m.cflag, x, b ? b : x, y, c->m.ns,          \
+                                           c->n_total, J, mode)
+#define WP(V, UU)                                                                                                  \
+    k_spmm_pres_w<V, UU><<<gp, 256, 0, s>>>(c->m.b_rowptr, c->m.b_col, c->m.b_val, c->m.cflag, x, b ? b : x, y,     \
+                                            c->m.n_pres, c->n_vel, c->n_total, J, mode)
+    // measured at C2 (warm, both kernels): J = 64 direct 228 us -> 203 us (U = 2; U = 4 275 us),
+    // J = 128 direct 451 us -> 416 us (velocity U = 2, pressure U = 4)
+    if (V2 == 2) WV(2, 2);
+    else if (V2 == 4) WV(4, 2);
+    else if (V2 == 6) WV(6, 1);
+    else WV(8, 1);
+    ENS_CKL();
+    // pressure rows: H = J/2 pairs per component -> V2p = ceil(H / 32) pairs per lane
+    const int V2p = (J / 2 + 31) / 32;
+    if (V2p == 1) WP(1, 2);
+    else if (V2p == 2) WP(2, 4);
+    else if (V2p == 3) WP(3, 2);
+    else WP(4, 2);
+#undef WV
+#undef WP
+    ENS_CKL();
+    return true;
+}
+
 static int launch_spmm_vec(ens_ctx* c, cudaStream_t s, const double* as_vals, const double* x, const double* b,
                            double* y, int mode, double* nrm, int* nblk) {
     const int J = c->J;
@@ -497,7 +783,10 @@ int launch_spmm(ens_ctx* c, cudaStream_t s, const double* as_vals, const double*
     const int J = c->J, W2 = 2 * J;
     if ((J & 1) == 0 && J <= 512 && (reinterpret_cast<uintptr_t>(x) & 15) == 0 &&
         (reinterpret_cast<uintptr_t>(y) & 15) == 0 && (!b || (reinterpret_cast<uintptr_t>(b) & 15) == 0))
+    {
+        if (launch_spmm_wide(c, s, as_vals, x, b, y, mode)) return ENS_OK;
         return launch_spmm_vec(c, s, as_vals, x, b, y, mode, nullptr, nullptr);
+    }
     {
         const int S = W2 >= 32 ? 32 : next_pow2(W2);
         const int opl = (W2 + S - 1) / S;

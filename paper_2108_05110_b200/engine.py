@@ -710,7 +710,11 @@ class Engine:
         self.cur = nxt
         self.means_valid = False
         self.prev_valid = True
-        return XC.allreduce_max_scalar(max(self.last_relres), self.comm, self.dev)
+        # residual max and the iteration count over ranks: every rank then takes the same
+        # refactorisation decision next step (identical shared matrices, lockstep timing)
+        res, it = XC.allreduce_max_values([max(self.last_relres), float(self.last_iters)], self.comm, self.dev)
+        self.last_iters = int(it)
+        return res
 
     def _factor(self):
         npert = N.I32(0)

@@ -43,9 +43,14 @@ def allreduce_eddy_max(maxsq, comm=None):
 
 
 def allreduce_max_scalar(value: float, comm=None, device=None) -> float:
+    return allreduce_max_values([value], comm, device)[0]
+
+
+def allreduce_max_values(values, comm=None, device=None):
+    """Elementwise max over ranks of a few host scalars (one small collective)."""
     if comm is None:
-        return value
+        return list(values)
     import torch
-    t = torch.tensor([value], dtype=torch.float64, device=device)
+    t = torch.tensor(list(values), dtype=torch.float64, device=device)
     dist.all_reduce(t, op=dist.ReduceOp.MAX, group=comm)
-    return float(t.item())
+    return [float(x) for x in t.tolist()]

@@ -295,3 +295,44 @@ def test_spmm_tiles_bitwise_equal_direct(monkeypatch, rng, J, stages):
         y1 = tiled.spmm(x, b if mode else None, mode=mode)
         torch.cuda.synchronize()
         assert torch.equal(y0, y1), mode
+
+
+@pytest.mark.parametrize("J", [64, 128])
+def test_spmm_wide_bitwise_equal_direct(monkeypatch, rng, J):
+    """The one-row-per-warp SpMM for J >= 64 (default) keeps the direct kernel's summation order."""
+    disc, cfg, _ = P.build_case("C1", n=6, J=J, steps=1)
+    monkeypatch.setenv("ENS_SPMM_WIDE", "0")
+    direct = Engine(disc, cfg)
+    monkeypatch.setenv("ENS_SPMM_WIDE", "1")
+    wide = Engine(disc, cfg)
+    a = torch.from_numpy(rng.standard_normal((2, direct.hm.nnz_s))).cuda()
+    direct.as_vals.copy_(a)
+    wide.as_vals.copy_(a)
+    x = torch.from_numpy(rng.standard_normal((2, disc.n_total, J))).cuda()
+    b = torch.from_numpy(rng.standard_normal((2, disc.n_total, J))).cuda()
+    for mode in (0, 1):
+        y0 = direct.spmm(x, b if mode else None, mode=mode)
+        y1 = wide.spmm(x, b if mode else None, mode=mode)
+        torch.cuda.synchronize()
+        assert torch.equal(y0, y1), mode
+
+
+def test_c2_full_size_two_steps_match_oracle():
+    """BASELINE C2 at its full size (128x128 TH mesh, N = 148,739, J = 20): two steps against the CPU
+    oracle (SciPy SuperLU, ~25 s per step on one core) -- v, w at 1e-9 and q, r at 1e-8 relative L2,
+    energies at 1e-10; the residual is the reference's relative_residual (<= rtol)."""
+    disc, cfg, prob = P.build_case("C2", steps=2)
+    report, state, _ = P.run(cfg, prob)
+    ost, recs, _, ores = O.run(cfg, disc, prob.initial_v, prob.initial_w, prob.forcing, prob.boundary)
+    for f in "vw":
+        ref = getattr(ost, f)
+        got = getattr(state, f)
+        err = rel(got, ref) if np.linalg.norm(ref) > 0 else np.linalg.norm(got)
+        assert err < 1e-9, (f, err)
+    for f in "qr":
+        assert rel(getattr(state, f), getattr(ost, f)) < 1e-8, f
+    assert abs(report.energy[-1] - recs[-1]["energy"]) <= 1e-10 * abs(recs[-1]["energy"])
+    assert np.all(report.residuals[1:] <= 1e-12)
+    # ensemble means of u = (v + w)/2 and B = (v - w)/2 (s = 1), the north-star fields
+    for a, b in ((state.v + state.w, ost.v + ost.w), (state.v - state.w, ost.v - ost.w)):
+        assert rel(a.mean(0), b.mean(0)) < 1e-9

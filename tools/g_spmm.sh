@@ -1,5 +1,4 @@
-python tools/spmm_bench.py 2>&1 | grep variant
-ENS_SPMM_TILES=1 timeout 120 python tools/spmm_bench.py 2>&1 | tail -3
-ENS_SPMM_TILES=1 ENS_TILE_STAGES=2 timeout 120 python tools/spmm_bench.py 2>&1 | grep variant
-ENS_SPMM_TILES=1 ENS_TILE_STAGES=4 timeout 120 python tools/spmm_bench.py 2>&1 | grep variant
-ENS_SPMM_TILES=1 ENS_TILE_STAGES=2 ENS_TILE_CAP=48 timeout 120 python tools/spmm_bench.py 2>&1 | grep variant
+python -m pytest tests -m gpu -x -q -k "wide or tiles" 2>&1 | tail -2
+for J in 64 128; do for w in 0 1 2; do ENS_SPMM_WIDE=$w J=$J python tools/spmm_bench.py 2>&1 | grep variant | sed "s/^/wide=$w /"; done; done
+timeout 1500 python bench.py --case C5 --steps 3 --warmup 3 --always-steps 0 --e2e-steps 0 > gpurun_out/bench_C5.json 2> gpurun_out/bench_C5.err; echo C5=$?
+tail -2 gpurun_out/bench_C5.err; head -c 600 gpurun_out/bench_C5.json
