@@ -324,15 +324,15 @@ def test_c2_full_size_two_steps_match_oracle():
     disc, cfg, prob = P.build_case("C2", steps=2)
     report, state, _ = P.run(cfg, prob)
     ost, recs, _, ores = O.run(cfg, disc, prob.initial_v, prob.initial_w, prob.forcing, prob.boundary)
-    for f in "vw":
-        ref = getattr(ost, f)
-        got = getattr(state, f)
-        err = rel(got, ref) if np.linalg.norm(ref) > 0 else np.linalg.norm(got)
-        assert err < 1e-9, (f, err)
+    # the north-star fields: per-member and ensemble-mean u = (v + w)/2, B = (v - w)/2
+    # (s = 1).  This MMS has w = 0 exactly (u = B), so w alone is pure discretisation error and is
+    # compared relative to the size of v.
+    for a, b in ((state.v + state.w, ost.v + ost.w), (state.v - state.w, ost.v - ost.w)):
+        assert rel(a, b) < 1e-9
+        assert rel(a.mean(0), b.mean(0)) < 1e-9
+    assert rel(state.v, ost.v) < 1e-9
+    assert np.linalg.norm(state.w - ost.w) < 1e-9 * np.linalg.norm(ost.v)
     for f in "qr":
         assert rel(getattr(state, f), getattr(ost, f)) < 1e-8, f
     assert abs(report.energy[-1] - recs[-1]["energy"]) <= 1e-10 * abs(recs[-1]["energy"])
     assert np.all(report.residuals[1:] <= 1e-12)
-    # ensemble means of u = (v + w)/2 and B = (v - w)/2 (s = 1), the north-star fields
-    for a, b in ((state.v + state.w, ost.v + ost.w), (state.v - state.w, ost.v - ost.w)):
-        assert rel(a.mean(0), b.mean(0)) < 1e-9
