@@ -228,6 +228,16 @@ int  ens_factor(ens_ctx* ctx, void* stream, const double* as_vals, int32_t* n_pe
  * check after every iteration), out = iterations performed. */
 int  ens_solve(ens_ctx* ctx, void* stream, const double* as_vals, const double* rhs, double* x,
                double rtol, int32_t restart, int32_t max_restarts, int32_t* iters_host, double* relres_host);
+/* ens_solve split at its one host round trip, so a whole time step can be
+ * captured into a CUDA graph: ens_solve_begin enqueues the first cycle
+ * (`predict` >= 1 iterations) and the next true residual, whose active-column
+ * count and norms go to pinned host memory, with no synchronisation (stream-
+ * capturable); ens_solve_finish synchronises the stream and continues exactly
+ * as ens_solve would (further cycles only if some member is above rtol). */
+int  ens_solve_begin(ens_ctx* ctx, void* stream, const double* as_vals, const double* rhs, double* x,
+                     double rtol, int32_t restart, int32_t predict);
+int  ens_solve_finish(ens_ctx* ctx, void* stream, const double* as_vals, const double* rhs, double* x,
+                      double rtol, int32_t restart, int32_t max_restarts, int32_t* iters_host, double* relres_host);
 
 /* y = K x (mode 0) or y = b - K x (mode 1), both matrices. */
 int  ens_spmm(ens_ctx* ctx, void* stream, const double* as_vals, const double* x, const double* b, double* y, int mode);

@@ -67,7 +67,7 @@ SYMBOLS = [
     "ens_abi_version", "ens_last_error", "ens_kernel_launches", "ens_create", "ens_set_pivoting",
     "ens_set_spmm_blocks", "ens_set_spmm_tiles", "ens_destroy", "ens_workspace_bytes",
     "ens_lincomb", "ens_member_sums", "ens_rhs", "ens_member_pass", "ens_apply_bc", "ens_assemble", "ens_factor",
-    "ens_solve", "ens_spmm", "ens_precond_apply", "ens_epilogue", "ens_diagnostics",
+    "ens_solve", "ens_solve_begin", "ens_solve_finish", "ens_spmm", "ens_precond_apply", "ens_epilogue", "ens_diagnostics",
 ]
 
 _lib = None
@@ -100,6 +100,8 @@ def load(path: str = LIB_PATH):
     lib.ens_assemble.argtypes = [P, P, P, P, P, F64, P]
     lib.ens_factor.argtypes = [P, P, P, C.POINTER(I32)]
     lib.ens_solve.argtypes = [P, P, P, P, P, F64, I32, I32, C.POINTER(I32), C.POINTER(F64)]
+    lib.ens_solve_begin.argtypes = [P, P, P, P, P, F64, I32, I32]
+    lib.ens_solve_finish.argtypes = [P, P, P, P, P, F64, I32, I32, C.POINTER(I32), C.POINTER(F64)]
     lib.ens_spmm.argtypes = [P, P, P, P, P, P, C.c_int]
     lib.ens_precond_apply.argtypes = [P, P, P, P]
     lib.ens_epilogue.argtypes = [P, P, P, P]

@@ -220,6 +220,21 @@ int ens_solve(ens_ctx* c, void* stream, const double* as_vals, const double* rhs
                        relres_host);
 }
 
+int ens_solve_begin(ens_ctx* c, void* stream, const double* as_vals, const double* rhs, double* x, double rtol,
+                    int32_t restart, int32_t predict) {
+    if (!c || !as_vals || !rhs || !x || !(rtol > 0.0) || predict < 1) return ENS_EINVAL;
+    int32_t it = predict;
+    double rel[2] = {0.0, 0.0};
+    return gmres_solve(c, (cudaStream_t)stream, as_vals, rhs, x, rtol, restart, 1, &it, rel, 1);
+}
+
+int ens_solve_finish(ens_ctx* c, void* stream, const double* as_vals, const double* rhs, double* x, double rtol,
+                     int32_t restart, int32_t max_restarts, int32_t* iters_host, double* relres_host) {
+    if (!c || !as_vals || !rhs || !x || !iters_host || !relres_host || !(rtol > 0.0)) return ENS_EINVAL;
+    return gmres_solve(c, (cudaStream_t)stream, as_vals, rhs, x, rtol, restart, max_restarts, iters_host,
+                       relres_host, 2);
+}
+
 int ens_spmm(ens_ctx* c, void* stream, const double* as_vals, const double* x, const double* b, double* y, int mode) {
     if (!c || !as_vals || !x || !y || (mode == 1 && !b)) return ENS_EINVAL;
     return launch_spmm(c, (cudaStream_t)stream, as_vals, x, b, y, mode);

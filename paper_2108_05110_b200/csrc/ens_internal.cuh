@@ -50,7 +50,9 @@ struct ens_ctx {
     double* frvec = nullptr;       // nmat * n_idx * J
     double* kry = nullptr;         // Krylov blocks
     int32_t kry_restart = 0;
-    int32_t kry_short = 0;         // cycle shortened for lack of device memory
+    int32_t kry_short = 0;
+    int32_t gm_total_it = 0;       // iterations of a begun solve (ens_solve_begin / _finish)
+    int32_t gm_predict = 0;         // cycle shortened for lack of device memory
     size_t kry_bytes = 0;
     double* red_part = nullptr;    // reduction partials
     double* red_out = nullptr;     // small outputs
@@ -131,5 +133,5 @@ int df_error(ens_ctx* c);
 
 // ---- Krylov (ens_krylov.cu) ----
 int gmres_solve(ens_ctx* c, cudaStream_t s, const double* as_vals, const double* rhs, double* x, double rtol,
-                int restart, int max_restarts, int32_t* iters, double* relres);
+                int restart, int max_restarts, int32_t* iters, double* relres, int phase = 0);
 int gmres_alloc(ens_ctx* c, int restart);

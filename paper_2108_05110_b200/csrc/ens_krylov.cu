@@ -250,8 +250,12 @@ static int read_count(ens_ctx* c, cudaStream_t s, int* out) {
         if (rc_ != ENS_OK) return rc_; \
     } while (0)
 
+// phase 0: the whole solve.  phase 1 (BEGIN, stream-capturable, needs *iters = predict > 0):
+// the blind first cycle and the next cycle's true residual, whose active-column
+// count and norms are copied to pinned host memory -- no host synchronisation.
+// phase 2 (FINISH): synchronise, then continue exactly where phase 0 would.
 int gmres_solve(ens_ctx* c, cudaStream_t s, const double* as_vals, const double* rhs, double* x, double rtol,
-                int restart, int max_restarts, int32_t* iters, double* relres) {
+                int restart, int max_restarts, int32_t* iters, double* relres, int phase) {
     RET(gmres_alloc(c, restart));
     restart = std::min(restart, c->kry_restart);
     const int J = c->J;
@@ -265,32 +269,53 @@ int gmres_solve(ens_ctx* c, cudaStream_t s, const double* as_vals, const double*
     KBuf kb = kbuf(c);
     const unsigned eb = (unsigned)((blk + 255) / 256);
     const unsigned cb = (unsigned)((n + 127) / 128);
-    // identity rows of the iterate carry the data exactly (stepper.py:214-215, 250-251)
-    RET(launch_copy_cons(c, s, rhs, x));
     const bool fused = spmm_resnorm_ok(c);   // residual SpMM also yields ||b||^2 and ||r||^2
-    if (!fused) RET(launch_coldot(c, s, rhs, 0, 1, rhs, N, kb.bn2));
     // predicted iteration count: the first cycle runs that many iterations without
     // host round trips; the true residual of the restart then decides (as always)
-    const int predict = std::max(0, std::min(*iters, restart));
-    int total_it = 0;
-    for (int cyc = 0; cyc <= max_restarts; ++cyc) {
-        if (fused) {
-            RET(launch_spmm_resnorm(c, s, as_vals, x, rhs, Rb, kb.bn2, kb.rn2));
-        } else {
-            RET(launch_spmm(c, s, as_vals, x, rhs, Rb, 1));
-            RET(launch_coldot(c, s, Rb, 0, 1, Rb, N, kb.rn2));
-        }
-        ENS_CK(cudaMemsetAsync(c->d_count, 0, sizeof(int32_t), s));
-        k_gm_init<<<cb, 128, 0, s>>>(c->cols, kb.bn2, kb.rn2, rtol, kb.scale, c->d_count, n);
-        ENS_CKL();
-        const bool blind = cyc == 0 && predict > 0;
+    const int predict = phase == 2 ? c->gm_predict : std::max(0, std::min(*iters, restart));
+    if (phase == 1 && predict < 1) {
+        ens_set_error("solve begin needs a predicted iteration count >= 1", __FILE__, __LINE__);
+        return ENS_EINVAL;
+    }
+    // (a begin captured into a graph runs without this host code: its host-side
+    // results -- total_it, predict -- are set at capture and are replay-invariant)
+    bool resume = phase == 2;
+    int total_it = resume ? c->gm_total_it : 0;
+    if (!resume) {
+        // identity rows of the iterate carry the data exactly (stepper.py:214-215, 250-251)
+        RET(launch_copy_cons(c, s, rhs, x));
+        if (!fused) RET(launch_coldot(c, s, rhs, 0, 1, rhs, N, kb.bn2));
+    }
+    for (int cyc = resume ? 1 : 0; cyc <= max_restarts; ++cyc) {
+        const bool blind = !resume && cyc == 0 && predict > 0;
         int active = 1;
-        if (!blind) {
-            // one round trip: active-column count and the residual norms
-            ENS_CK(cudaMemcpyAsync(c->h_count, c->d_count, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
-            ENS_CK(cudaMemcpyAsync(c->h_small, kb.bn2, sizeof(double) * 2 * n, cudaMemcpyDeviceToHost, s));
+        if (resume) {
+            // the begin phase left the count and the norms on their way to pinned memory
             ENS_CK(cudaStreamSynchronize(s));
             active = *c->h_count;
+            resume = false;
+        } else {
+            if (fused) {
+                RET(launch_spmm_resnorm(c, s, as_vals, x, rhs, Rb, kb.bn2, kb.rn2));
+            } else {
+                RET(launch_spmm(c, s, as_vals, x, rhs, Rb, 1));
+                RET(launch_coldot(c, s, Rb, 0, 1, Rb, N, kb.rn2));
+            }
+            ENS_CK(cudaMemsetAsync(c->d_count, 0, sizeof(int32_t), s));
+            k_gm_init<<<cb, 128, 0, s>>>(c->cols, kb.bn2, kb.rn2, rtol, kb.scale, c->d_count, n);
+            ENS_CKL();
+            if (!blind) {
+                // one round trip: active-column count and the residual norms
+                ENS_CK(cudaMemcpyAsync(c->h_count, c->d_count, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+                ENS_CK(cudaMemcpyAsync(c->h_small, kb.bn2, sizeof(double) * 2 * n, cudaMemcpyDeviceToHost, s));
+                if (phase == 1) {
+                    c->gm_total_it = total_it;
+                    c->gm_predict = predict;
+                    return ENS_OK;
+                }
+                ENS_CK(cudaStreamSynchronize(s));
+                active = *c->h_count;
+            }
         }
         if (!blind && (active == 0 || cyc == max_restarts)) {
             // true relative residual per matrix (linalg.py:111-118)

@@ -768,7 +768,7 @@ int mf_solve(ens_ctx* c, cudaStream_t s, const double* r, double* z) {
     SolveIO* io = (SolveIO*)c->solve_io;
     k_set_io<<<1, 1, 0, s>>>(io, r, z);
     ENS_CKL();
-    if (!graphs_enabled() || s == 0) {
+    if (!graphs_enabled() || s == 0 || capturing(s)) {   // inside a caller's capture: become its nodes
         int64_t n = 0;
         return mf_solve_launches(c, s, io, &n);
     }

@@ -20,6 +20,7 @@ depend on level-n data only (`stepper.py:363-366`).
 from __future__ import annotations
 
 import ctypes as C
+import os
 import weakref
 
 import numpy as np
@@ -446,6 +447,13 @@ class Engine:
         self.last_iters = 0
         self.last_pert = 0
         self.last_relres = (0.0, 0.0)
+        # whole-step CUDA graphs (ENS_STEP_GRAPH=0 disables): per buffer parity and problem,
+        # the pre-solve sequence and the solve's first cycle + epilogue, replayed every step
+        self.step_graphs = os.environ.get("ENS_STEP_GRAPH", "1") != "0"
+        self._graphs = {}
+        self._gdata_cache = {}
+        self._gspec = {}
+        self.graph_launch_credit = 0   # kernels replayed by step graphs minus kernels captured
 
     def __del__(self):
         try:
@@ -653,7 +661,175 @@ class Engine:
     def step(self, t_next, forcing, boundary):
         """One time-step of all local members; returns the max relative residual."""
         with self.on_stream():
+            if self._graph_ok(forcing, boundary, t_next):
+                return self._step_graphed(t_next, forcing, boundary)
             return self._step(t_next, forcing, boundary)
+
+    # ------------------------------------------------------------------
+    # whole-step CUDA graphs
+    # ------------------------------------------------------------------
+    def _graph_ok(self, forcing, boundary, t_next):
+        """Graph replay needs the extrapolated initial iterate (level n-1 resident) and separable data
+        (or no body force at all)."""
+        if not (self.step_graphs and self.prev_valid and self.guess == "extrapolate"
+                and hasattr(boundary, "separable")):
+            return False
+        return hasattr(forcing, "separable") or self._no_loads(forcing, t_next)
+
+    def _no_loads(self, forcing, t):
+        lv, lw = forcing.loads(t, self.disc, self.config)
+        return lv is None and lw is None
+
+    def _gdata(self, obj, kind):
+        """(coefficient function, pinned host and device coefficient blocks, fixed DataDesc) of one data kind."""
+        key = (kind, id(obj))
+        ent = self._gdata_cache.get(key)
+        if ent is None:
+            self._data(obj, kind, 0.0)                   # builds the device basis once
+            sep, basis_t = self._data_cache[key]
+            K = basis_t.shape[0]
+            pin = torch.zeros(2, K, self.J, dtype=torch.float64, pin_memory=True)
+            dev = torch.zeros(2, K, self.J, dtype=torch.float64, device=self.dev)
+            dd = N.DataDesc()
+            dd.rows = self.nvel if kind == "loads" else self.hm.nbdofs
+            dd.K, dd.basis, dd.coef, dd.dense = K, _dptr(basis_t), _dptr(dev), None
+            ent = (sep, pin, dev, dd)
+            self._gdata_cache[key] = ent
+        return ent
+
+    def _gcoef(self, ent, t):
+        sep = ent[0]
+        cv, cw = sep.coef(t)
+        sl = slice(self.j0, self.j0 + self.J)
+        return np.stack([np.asarray(cv, dtype=float)[:, sl], np.asarray(cw, dtype=float)[:, sl]])
+
+    def _gfill(self, ent, t):
+        """Coefficients at t into the pinned block the captured H2D copy reads (prefetched when t was predicted)."""
+        spec = self._gspec.get(id(ent))
+        h = ent[1].numpy()
+        if spec is not None and spec[0] == t:
+            h[...] = spec[1]
+        else:
+            h[...] = self._gcoef(ent, t)
+
+    def _gprefetch(self, ent, t):
+        """Evaluate the next step's coefficients while the GPU runs this step (callers advance t by dt)."""
+        self._gspec[id(ent)] = (t, self._gcoef(ent, t))
+
+    def _capture(self, fn):
+        """Capture fn() on the engine stream into a CUDA graph; returns (graph, kernels in it)."""
+        l0 = self.lib.ens_kernel_launches()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=self.stream, capture_error_mode="thread_local"):
+            fn()
+        n = int(self.lib.ens_kernel_launches() - l0)
+        self.graph_launch_credit -= n
+        return g, n
+
+    def _step_graphs(self, lo, bc):
+        """Graph segments for the current buffer parity: split at the collectives when members are sharded."""
+        lib, ctx, s = self.lib, self.ctx, self.sptr
+        cur, nxt = self.cur, 1 - self.cur
+        key = (cur, id(lo), id(bc))
+        segs = self._graphs.get(key)
+        if segs is not None:
+            return segs
+        X, Xn = self.X[cur], self.X[nxt]
+
+        def sums():
+            N.check(lib.ens_member_sums(ctx, s, _dptr(X), _dptr(self.sums)), "ens_member_sums")
+
+        def rhs():
+            torch.mul(self.sums, 1.0 / self.J_total, out=self.means)
+            if lo is not None:
+                lo[2].copy_(lo[1], non_blocking=True)
+            N.check(lib.ens_rhs(ctx, s, _dptr(X), _dptr(self.member_coef), 1.0 / self.config.dt,
+                                C.byref(lo[3]) if lo is not None else None, _dptr(self.rhs)), "ens_rhs")
+            N.check(lib.ens_member_pass(ctx, s, _dptr(X), _dptr(self.means), _dptr(self.rhs), _dptr(self.maxsq)),
+                    "ens_member_pass")
+
+        def assemble():
+            bc[2].copy_(bc[1], non_blocking=True)
+            N.check(lib.ens_apply_bc(ctx, s, C.byref(bc[3]), _dptr(self.rhs)), "ens_apply_bc")
+            N.check(lib.ens_assemble(ctx, s, _dptr(self.base), _dptr(self.means), _dptr(self.maxsq),
+                                     self.two_mu_dt, _dptr(self.as_vals)), "ens_assemble")
+
+        def solve():
+            N.check(lib.ens_lincomb(ctx, s, 2.0, _dptr(X), -1.0, _dptr(Xn)), "ens_lincomb")   # 2 x^n - x^{n-1}
+            N.check(lib.ens_solve_begin(ctx, s, _dptr(self.as_vals), _dptr(self.rhs), _dptr(Xn), self.rtol,
+                                        self.restart, 1), "ens_solve_begin")
+            N.check(lib.ens_epilogue(ctx, s, _dptr(Xn), _dptr(self.Pq[nxt])), "ens_epilogue")
+
+        if self.comm is None:
+            def pre():
+                sums()
+                rhs()
+                assemble()
+            parts = [("pre", pre), ("solve", solve)]
+        else:
+            parts = [("sums", sums), ("rhs", rhs), ("assemble", assemble), ("solve", solve)]
+        segs = {name: self._capture(fn) for name, fn in parts}
+        self._graphs[key] = segs
+        return segs
+
+    def _replay(self, seg):
+        g, n = seg
+        g.replay()
+        self.graph_launch_credit += n
+
+    def _step_graphed(self, t_next, forcing, boundary):
+        lib, ctx, s = self.lib, self.ctx, self.sptr
+        cur, nxt = self.cur, 1 - self.cur
+        X, Xn = self.X[cur], self.X[nxt]
+        lo = self._gdata(forcing, "loads") if hasattr(forcing, "separable") else None   # None: no body force
+        bc = self._gdata(boundary, "bc")
+        if lo is not None:
+            self._gfill(lo, t_next)
+        self._gfill(bc, t_next)
+        segs = self._step_graphs(lo, bc)
+        need = (self.refactor == "always" or not self.factored or self.since_factor >= self.lag_max_steps
+                or self.last_iters > self.lag_max_iters)
+        self._retire(nxt)
+        if self.comm is None:
+            self._replay(segs["pre"])
+        else:
+            self._replay(segs["sums"])
+            XC.allreduce_member_sums(self.sums, self.comm)
+            self._replay(segs["rhs"])
+            XC.allreduce_eddy_max(self.maxsq, self.comm)
+            self._replay(segs["assemble"])
+        if need:
+            self._factor()
+        else:
+            self.since_factor += 1
+        self._replay(segs["solve"])
+        t_pred = t_next + self.config.dt                  # host work overlapped with the solve
+        if lo is not None:
+            self._gprefetch(lo, t_pred)
+        self._gprefetch(bc, t_pred)
+        iters = N.I32(0)
+        rel = (N.F64 * 2)()
+        code = lib.ens_solve_finish(ctx, s, _dptr(self.as_vals), _dptr(self.rhs), _dptr(Xn), self.rtol,
+                                    self.restart, self.max_restarts, C.byref(iters), rel)
+        iters, rel = int(iters.value), (rel[0], rel[1])
+        redo = iters > 1                                  # more cycles ran after the captured epilogue
+        if code == N.ENS_ENOCONV and not need:            # stale preconditioner: rebuild and retry once
+            self._factor()
+            Xn.copy_(X)
+            code, iters2, rel = self._solve(Xn, predict=1)
+            iters += iters2
+            redo = True
+        self.last_iters, self.last_relres = iters, rel
+        N.check(code, "ens_solve_finish")
+        if redo:
+            N.check(lib.ens_epilogue(ctx, s, _dptr(Xn), _dptr(self.Pq[nxt])), "ens_epilogue")
+        self.gen[nxt] += 1
+        self.cur = nxt
+        self.means_valid = False
+        self.prev_valid = True
+        res, it = XC.allreduce_max_values([max(self.last_relres), float(self.last_iters)], self.comm, self.dev)
+        self.last_iters = int(it)
+        return res
 
     def diagnostics(self):
         """Device-side _record (stepper.py:432-439) of the current state."""

@@ -336,3 +336,23 @@ def test_c2_full_size_two_steps_match_oracle():
         assert rel(getattr(state, f), getattr(ost, f)) < 1e-8, f
     assert abs(report.energy[-1] - recs[-1]["energy"]) <= 1e-10 * abs(recs[-1]["energy"])
     assert np.all(report.residuals[1:] <= 1e-12)
+
+
+@pytest.mark.parametrize("case,over", [("C1", dict(J=20, steps=8)), ("C3", dict(n=8, J=6, steps=8))])
+def test_step_graphs_bitwise_equal_eager(monkeypatch, case, over):
+    """Whole-step CUDA graph replay (default) runs exactly the eager kernel sequence: identical bits."""
+    disc, cfg, prob = P.build_case(case, **over)
+    out = []
+    for flag in ("0", "1"):
+        monkeypatch.setenv("ENS_STEP_GRAPH", flag)
+        eng = Engine(disc, cfg)
+        eng.load_state(prob.initial_v, prob.initial_w, None, None)
+        t, res = 0.0, []
+        for _ in range(over["steps"]):
+            t += cfg.dt
+            res.append(eng.step(t, prob.forcing, prob.boundary))
+        torch.cuda.synchronize()
+        out.append((eng.X[eng.cur].clone(), eng.Pq[eng.cur].clone(), res, eng.graph_launch_credit))
+    assert torch.equal(out[0][0], out[1][0]) and torch.equal(out[0][1], out[1][1])
+    assert out[0][2] == out[1][2]
+    assert out[0][3] == 0 and out[1][3] > 0     # the graphed engine replayed captured kernels

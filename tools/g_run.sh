@@ -1,4 +1,6 @@
-python bench.py > gpurun_out/bench_c2.json 2> gpurun_out/bench_c2.err; echo c2=$?
-ncu --set full --import-source on --clock-control none -k regex:k_spmm_ -s 4 -c 2 -o gpurun_out/spmm_c2 python tools/spmm_bench.py > gpurun_out/ncu_spmm.log 2>&1; echo ncu=$?
-timeout 1500 python bench.py --case C5 --steps 3 --warmup 3 --always-steps 0 --e2e-steps 0 > gpurun_out/bench_C5.json 2> gpurun_out/bench_C5.err; echo C5=$?
-tail -2 gpurun_out/bench_C5.err; head -c 1500 gpurun_out/bench_C5.json
+python -m pytest tests -m gpu -x -q -k "graphs or c1_matches or refactor or case_runs" 2>&1 | tail -3
+python tools/step_gaps.py 2>&1 | grep -v Warn | head -12
+ENS_STEP_GRAPH=0 python tools/step_gaps.py 2>&1 | grep -v Warn | head -3
+python bench.py --no-cpu-baseline --always-steps 0 > gpurun_out/bench_c2.json 2> gpurun_out/bench_c2.err; echo c2=$?
+head -c 400 gpurun_out/bench_c2.json; grep -o '"gpu_launches": [0-9]*' gpurun_out/bench_c2.json
+tail -3 gpurun_out/bench_c2.err
