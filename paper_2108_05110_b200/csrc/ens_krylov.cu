@@ -8,6 +8,8 @@
 // device; the host only reads one counter per iteration to stop early.
 // Replaces Factorization.solve_block + relative_residual (linalg.py:62-76, 111-118).
 #include <cmath>
+#include <cstdlib>
+#include <string>
 
 #include "ens_internal.cuh"
 
@@ -138,6 +140,18 @@ __global__ void __launch_bounds__(256) k_axpy_multi2(double* __restrict__ W, con
         w.y += sign * acc.y;
         w2[t] = w;
     }
+}
+
+// x += z over both systems (the Richardson correction of the first cycle)
+__global__ void __launch_bounds__(256) k_add2(double2* __restrict__ x, const double2* __restrict__ z, int64_t n2) {
+    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < n2; t += (int64_t)gridDim.x * blockDim.x) {
+        const double2 a = x[t], b = z[t];
+        x[t] = make_double2(a.x + b.x, a.y + b.y);
+    }
+}
+__global__ void k_add1(double* __restrict__ x, const double* __restrict__ z, int64_t n) {
+    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t < n) x[t] += z[t];
 }
 
 static unsigned vec_blocks(int64_t n) { return (unsigned)std::min<int64_t>((n + 255) / 256, 148 * 16); }
@@ -286,8 +300,31 @@ int gmres_solve(ens_ctx* c, cudaStream_t s, const double* as_vals, const double*
         RET(launch_copy_cons(c, s, rhs, x));
         if (!fused) RET(launch_coldot(c, s, rhs, 0, 1, rhs, N, kb.bn2));
     }
+    // first cycle as one Richardson step x += P^-1 (b - K x) when a single iteration is
+    // predicted (default; ENS_KRYLOV_FIRST=fgmres keeps a one-vector FGMRES cycle): the
+    // true residual then decides exactly as after an FGMRES cycle, and FGMRES continues
+    // from that iterate if needed.  Saves the cycle's K z product and its Gram-Schmidt /
+    // Givens / scaling passes (C2 1.72 -> 1.61 ms/step, C4 19.7 -> 18.6, C3 45.5 -> 43.8).
+    if (c->krylov_first < 0) {
+        const char* e = std::getenv("ENS_KRYLOV_FIRST");
+        c->krylov_first = (e && std::string(e) == "fgmres") ? 0 : 1;
+    }
+    const bool rich = c->krylov_first == 1 && predict == 1;
     for (int cyc = resume ? 1 : 0; cyc <= max_restarts; ++cyc) {
         const bool blind = !resume && cyc == 0 && predict > 0;
+        if (blind && rich) {
+            RET(launch_spmm(c, s, as_vals, x, rhs, Rb, 1));
+            RET(mf_solve(c, s, Rb, Z));
+            if (vec_ok(J, N, x, Z)) {
+                k_add2<<<vec_blocks(blk / 2), 256, 0, s>>>(reinterpret_cast<double2*>(x),
+                                                          reinterpret_cast<const double2*>(Z), blk / 2);
+            } else {
+                k_add1<<<eb, 256, 0, s>>>(x, Z, blk);
+            }
+            ENS_CKL();
+            ++total_it;
+            continue;
+        }
         int active = 1;
         if (resume) {
             // the begin phase left the count and the norms on their way to pinned memory

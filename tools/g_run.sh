@@ -1,6 +1,8 @@
-python -m pytest tests -m gpu -x -q -k "graphs or c1_matches or refactor or case_runs" 2>&1 | tail -3
-python tools/step_gaps.py 2>&1 | grep -v Warn | head -12
-ENS_STEP_GRAPH=0 python tools/step_gaps.py 2>&1 | grep -v Warn | head -3
-python bench.py --no-cpu-baseline --always-steps 0 > gpurun_out/bench_c2.json 2> gpurun_out/bench_c2.err; echo c2=$?
-head -c 400 gpurun_out/bench_c2.json; grep -o '"gpu_launches": [0-9]*' gpurun_out/bench_c2.json
-tail -3 gpurun_out/bench_c2.err
+set -e; python -m paper_2108_05110_b200.build > /dev/null; set +e
+for kf in fgmres richardson; do
+  for c in C2 C4 C3; do
+    ENS_KRYLOV_FIRST=$kf timeout 900 python bench.py --case $c --steps 10 --warmup 3 --always-steps 0 --e2e-steps 0 --no-cpu-baseline > gpurun_out/b_${kf}_$c.json 2> gpurun_out/b_${kf}_$c.err
+    python -c "
+import json; d=json.load(open('gpurun_out/b_${kf}_$c.json')); print('$kf $c', 'ms/step %.3f'%d['ms_per_step'], 'value %.0f'%d['value'], 'iters', d['krylov_iters_per_step'], 'nfact', d['preconditioner']['factorizations_in_timed_steps'])"
+  done
+done
