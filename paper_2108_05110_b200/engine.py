@@ -34,6 +34,10 @@ from . import symbolic as S
 from .ensemble import viscosity_stats
 
 
+_RENEW_DEBUG = os.environ.get("ENS_RENEW_DEBUG", "0") == "1"
+RENEW_WINDOW = 6   # factorisation lifetimes a per-position step cost stays usable as a prediction
+
+
 def _dptr(t: torch.Tensor) -> int:
     return t.data_ptr()
 
@@ -277,11 +281,13 @@ class Engine:
     """Device-resident ensemble on one GPU (member columns [j0, j0+J) of J_total)."""
 
     def __init__(self, disc, config, j0=0, J=None, device=None, comm=None, restart=8, max_restarts=20, rtol=1e-12,
-                 refactor="adaptive", lag_max_iters=3, lag_max_steps=50, guess="extrapolate"):
+                 refactor="adaptive", lag_max_iters=8, lag_max_steps=500, guess="extrapolate"):
         """``refactor``: "always" rebuilds the LU preconditioner every step (the
         reference refactorises every sub-step, `stepper.py:216`); "adaptive"
-        keeps the last factorisation while FGMRES needs <= ``lag_max_iters``
-        iterations (at most ``lag_max_steps`` steps).  Either way every solve is
+        keeps the last factorisation until the renewal rule (``_cost_end``: the last
+        step's device time exceeds the average cost per step of the current
+        factorisation's lifetime, factorisation included) fires, FGMRES needs more
+        than ``lag_max_iters`` iterations, or ``lag_max_steps`` steps have passed.  Either way every solve is
         converged to the same true residual ``rtol`` on the *current* matrix.
 
         ``guess``: FGMRES initial iterate -- "extrapolate" (2 x^n - x^{n-1} when
@@ -297,6 +303,12 @@ class Engine:
         self.factored = False
         self.since_factor = 0
         self.n_factor = 0
+        self._renew = False        # renewal rule fired (adaptive policy), agreed over ranks
+        self._ev = None            # step / factorisation CUDA events of the renewal rule
+        self._cyc = None           # [factorisation ms, step ms since, steps since]
+        self._prof = []            # [step ms, lifetime] by position within a factorisation's lifetime
+        self._life = 0             # factorisations so far
+        self._fac_this = False
         self.pivoting = False
         if not torch.cuda.is_available():
             raise RuntimeError("the B200 time-step engine needs a CUDA device (no CPU fallback)")
@@ -787,8 +799,8 @@ class Engine:
             self._gfill(lo, t_next)
         self._gfill(bc, t_next)
         segs = self._step_graphs(lo, bc)
-        need = (self.refactor == "always" or not self.factored or self.since_factor >= self.lag_max_steps
-                or self.last_iters > self.lag_max_iters)
+        self._cost_begin()
+        need = self._need_factor()
         self._retire(nxt)
         if self.comm is None:
             self._replay(segs["pre"])
@@ -799,7 +811,7 @@ class Engine:
             XC.allreduce_eddy_max(self.maxsq, self.comm)
             self._replay(segs["assemble"])
         if need:
-            self._factor()
+            self._factor_timed()
         else:
             self.since_factor += 1
         self._replay(segs["solve"])
@@ -814,7 +826,7 @@ class Engine:
         iters, rel = int(iters.value), (rel[0], rel[1])
         redo = iters > 1                                  # more cycles ran after the captured epilogue
         if code == N.ENS_ENOCONV and not need:            # stale preconditioner: rebuild and retry once
-            self._factor()
+            self._factor_timed()
             Xn.copy_(X)
             code, iters2, rel = self._solve(Xn, predict=1)
             iters += iters2
@@ -827,8 +839,11 @@ class Engine:
         self.cur = nxt
         self.means_valid = False
         self.prev_valid = True
-        res, it = XC.allreduce_max_values([max(self.last_relres), float(self.last_iters)], self.comm, self.dev)
+        renew = self._cost_end()
+        res, it, rn = XC.allreduce_max_values([max(self.last_relres), float(self.last_iters), float(renew)],
+                                              self.comm, self.dev)
         self.last_iters = int(it)
+        self._renew = rn > 0.0
         return res
 
     def diagnostics(self):
@@ -848,6 +863,7 @@ class Engine:
         lib, ctx, s = self.lib, self.ctx, self.sptr
         cur, nxt = self.cur, 1 - self.cur
         X = self.X[cur]
+        self._cost_begin()
         if not self.means_valid:
             self._compute_means()
         loads, keep1 = self._data(forcing, "loads", t_next)
@@ -860,10 +876,9 @@ class Engine:
         N.check(lib.ens_apply_bc(ctx, s, C.byref(bvals), _dptr(self.rhs)), "ens_apply_bc")
         N.check(lib.ens_assemble(ctx, s, _dptr(self.base), _dptr(self.means), _dptr(self.maxsq), self.two_mu_dt,
                                  _dptr(self.as_vals)), "ens_assemble")
-        need = (self.refactor == "always" or not self.factored or self.since_factor >= self.lag_max_steps
-                or self.last_iters > self.lag_max_iters)
+        need = self._need_factor()
         if need:
-            self._factor()
+            self._factor_timed()
         else:
             self.since_factor += 1
         self._retire(nxt)
@@ -874,7 +889,7 @@ class Engine:
             Xn.copy_(X)                               # warm start from level n
         code, iters, rel = self._solve(Xn)
         if code == N.ENS_ENOCONV and not need:        # stale preconditioner: rebuild and retry once
-            self._factor()
+            self._factor_timed()
             Xn.copy_(X)
             code, iters2, rel = self._solve(Xn, predict=1)
             iters += iters2
@@ -886,11 +901,79 @@ class Engine:
         self.cur = nxt
         self.means_valid = False
         self.prev_valid = True
-        # residual max and the iteration count over ranks: every rank then takes the same
-        # refactorisation decision next step (identical shared matrices, lockstep timing)
-        res, it = XC.allreduce_max_values([max(self.last_relres), float(self.last_iters)], self.comm, self.dev)
+        # residual max, iteration count and the renewal decision over ranks: every rank then
+        # takes the same refactorisation decision next step (identical shared matrices, lockstep timing)
+        renew = self._cost_end()
+        res, it, rn = XC.allreduce_max_values([max(self.last_relres), float(self.last_iters), float(renew)],
+                                              self.comm, self.dev)
         self.last_iters = int(it)
+        self._renew = rn > 0.0
         return res
+
+    # ------------------------------------------------------------------
+    # preconditioner renewal (adaptive policy)
+    # ------------------------------------------------------------------
+    def _need_factor(self):
+        return (self.refactor == "always" or not self.factored or self.since_factor >= self.lag_max_steps
+                or self.last_iters > self.lag_max_iters or self._renew)
+
+    def _cost_begin(self):
+        if self._ev is None:
+            self._ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+        self._ev[0].record(self.stream)
+        self._fac_this = False
+
+    def _factor_timed(self):
+        self._ev[1].record(self.stream)
+        self._factor()
+        self._ev[2].record(self.stream)
+        self._fac_this = True
+
+    def _cost_end(self):
+        """Renewal rule of the adaptive policy: with F the last factorisation's time and A_1..A_L the
+        device times of the steps since (factorisation excluded), rebuild before the next step when
+        the next step would cost more than the lifetime's average cost per step,
+        A_{L+1} > (F + sum A) / L -- the optimal stopping rule for a renewal whose per-step cost
+        grows as the factorisation ages.
+        The next step's cost is predicted from the cost at the same position of earlier
+        lifetimes when known (so a factorisation that goes stale after one step is rebuilt every
+        step), else from this step.  Whatever the policy, every solve is converged to rtol on the
+        current matrix."""
+        ev = self._ev
+        ev[3].record(self.stream)
+        ev[3].synchronize()
+        step_ms = ev[0].elapsed_time(ev[3])
+        if self._fac_this:
+            f = ev[1].elapsed_time(ev[2])
+            self._cyc = [f, step_ms - f, 1]
+            self._life += 1
+            a = step_ms - f
+        elif self._cyc is not None:
+            self._cyc[1] += step_ms
+            self._cyc[2] += 1
+            a = step_ms
+        else:
+            return False
+        steps = self._cyc[2]
+        # per-position step costs of recent factorisation lifetimes (exponential average, so one
+        # iteration spike does not shorten every later lifetime; the first lifetime -- the start-up
+        # transient -- and entries older than RENEW_WINDOW lifetimes are not used)
+        fresh = max(2, self._life - RENEW_WINDOW)
+        if len(self._prof) < steps:
+            self._prof.append([a, self._life])
+        else:
+            old = self._prof[steps - 1]
+            self._prof[steps - 1] = [0.5 * (old[0] + a) if old[1] >= fresh else a, self._life]
+        if self.refactor != "adaptive":
+            return False
+        # next step's cost: what the same position cost in a recent lifetime, else this step's
+        nxt = a
+        if steps < len(self._prof) and self._prof[steps][1] >= fresh:
+            nxt = self._prof[steps][0]
+        if _RENEW_DEBUG:
+            print(f"renew: pos {steps} step {step_ms:.2f} ms (F {self._cyc[0]:.2f}) iters {self.last_iters} "
+                  f"pred {nxt:.2f} avg {(self._cyc[0] + self._cyc[1]) / steps:.2f}", flush=True)
+        return nxt > (self._cyc[0] + self._cyc[1]) / steps
 
     def _factor(self):
         npert = N.I32(0)

@@ -102,8 +102,8 @@ class Problem:
 # engine cache
 # ----------------------------------------------------------------------
 
-_SOLVER_OPTS = dict(rtol=DEFAULT_RTOL, restart=8, max_restarts=20, refactor="adaptive", lag_max_iters=3,
-                    lag_max_steps=50, guess="extrapolate")
+_SOLVER_OPTS = dict(rtol=DEFAULT_RTOL, restart=8, max_restarts=20, refactor="adaptive", lag_max_iters=8,
+                    lag_max_steps=500, guess="extrapolate")
 
 
 def set_solver_options(**kw):
@@ -112,8 +112,10 @@ def set_solver_options(**kw):
     rtol: per-member true relative residual of every sub-step solve;
     restart / max_restarts: FGMRES cycle length and count;
     refactor: "always" (rebuild the LU preconditioner each step, as the
-    reference refactorises each sub-step) or "adaptive" (reuse it while FGMRES
-    needs <= lag_max_iters iterations, at most lag_max_steps steps);
+    reference refactorises each sub-step) or "adaptive" (reuse it until the
+    renewal rule of Engine._cost_end fires -- the last step cost more than the
+    average per step of the factorisation's lifetime -- or FGMRES needs more
+    than lag_max_iters iterations, or lag_max_steps steps have passed);
     guess: FGMRES initial iterate, "extrapolate" (2 x^n - x^{n-1}) or "previous" (x^n).
     """
     unknown = set(kw) - set(_SOLVER_OPTS)
