@@ -35,7 +35,8 @@ from .ensemble import viscosity_stats
 
 
 _RENEW_DEBUG = os.environ.get("ENS_RENEW_DEBUG", "0") == "1"
-RENEW_WINDOW = 6   # factorisation lifetimes a per-position step cost stays usable as a prediction
+RENEW_WINDOW = int(os.environ.get("ENS_RENEW_WINDOW", "6"))   # lifetimes a per-position cost stays usable
+RENEW_PRED = os.environ.get("ENS_RENEW_PRED", "last")   # next-step cost when no recent profile: last step ("mean3", "min2" measured worse at C3/C4)
 
 
 def _dptr(t: torch.Tensor) -> int:
@@ -308,6 +309,7 @@ class Engine:
         self._cyc = None           # [factorisation ms, step ms since, steps since]
         self._prof = []            # [step ms, lifetime] by position within a factorisation's lifetime
         self._life = 0             # factorisations so far
+        self._recent = []          # step ms of this lifetime's last steps
         self._fac_this = False
         self.pivoting = False
         if not torch.cuda.is_available():
@@ -967,7 +969,13 @@ class Engine:
         if self.refactor != "adaptive":
             return False
         # next step's cost: what the same position cost in a recent lifetime, else this step's
-        nxt = a
+        self._recent = ([] if self._fac_this else self._recent[-2:]) + [a]
+        if RENEW_PRED == "mean3":
+            nxt = sum(self._recent) / len(self._recent)
+        elif RENEW_PRED == "min2":
+            nxt = min(self._recent[-2:])
+        else:
+            nxt = a
         if steps < len(self._prof) and self._prof[steps][1] >= fresh:
             nxt = self._prof[steps][0]
         if _RENEW_DEBUG:
