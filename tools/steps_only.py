@@ -1,0 +1,28 @@
+"""C2 warm steps for an ncu launch list: 6 steps, then 5 inside cudaProfilerStart/Stop (run from the repo root).
+
+    ncu --profile-from-start off --metrics gpu__time_duration.sum --clock-control none --csv python tools/steps_only.py
+"""
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch
+
+import paper_2108_05110_b200 as P
+from paper_2108_05110_b200 import stepper as ST
+
+disc, cfg, prob = P.build_case(os.environ.get("CASE", "C2"))
+eng = ST.get_engine(disc, cfg)
+eng.load_state(prob.initial_v, prob.initial_w, None, None)
+t = 0.0
+for _ in range(6):
+    t += cfg.dt
+    eng.step(t, prob.forcing, prob.boundary)
+torch.cuda.synchronize()
+torch.cuda.profiler.start()
+for _ in range(5):
+    t += cfg.dt
+    eng.step(t, prob.forcing, prob.boundary)
+torch.cuda.synchronize()
+torch.cuda.profiler.stop()
+print("iters", eng.last_iters, "factorizations", eng.n_factor)
