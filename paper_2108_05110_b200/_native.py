@@ -10,7 +10,7 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libensmhd_b200.so")
+LIB_PATH = os.environ.get("ENS_LIB", os.path.join(HERE, "libensmhd_b200.so"))   # ENS_LIB: A/B builds only
 
 ENS_OK, ENS_EINVAL, ENS_ENOMEM, ENS_ENOCONV, ENS_ECUDA = range(5)
 

@@ -237,34 +237,51 @@ __global__ void __launch_bounds__(SG_T, SG_MINB) k_sgemm(MfDev d, const int4* __
     const int nch = (kc + SG_KC - 1) / SG_KC;
     const int row = 8 * warp + g;
     const bool row_ok = row < nr;
-    auto issue_a = [&](int c) {
+    // Load issue with per-thread invariants hoisted (thread = row warp + 8 i, column lane;
+    // SG_KC = SG_C = 32, SG_T = 256) and the stage passed in (no runtime modulo): the leaf
+    // levels were issue-bound on this address arithmetic (ncu: ~50 % of the instructions).
+    static_assert(SG_KC == 32 && SG_C == 32 && SG_T == 256, "k_sgemm load mapping");
+    const uint32_t sm_u32 = (uint32_t)__cvta_generic_to_shared(sm);
+    const double* a_src = base + (int64_t)(rbase + warp) * m + kbeg + lane;
+    const int64_t a_rstep = 8LL * m;
+    const uint32_t a_dst = sm_u32 + 8u * (uint32_t)(warp * SG_LDA + lane);
+    const uint32_t b_dst = sm_u32 + 8u * (uint32_t)(SG_R * SG_LDA + warp * SG_LDB + lane);
+    const bool jok = lane < jn;
+    const double* b_fr = fr + j0 + lane;
+    const double* b_x = x + j0 + lane;
+    auto cpa8 = [](uint32_t s, const double* gp, bool pred) {
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(s), "l"(gp), "r"(pred ? 8 : 0));
+    };
+    auto issue_a = [&](int c, int st) {
 #ifdef SG_NOA
         return;
 #endif
-        double* As = sm + (c % nstage) * SG_STAGE;
+        const uint32_t dst = a_dst + 8u * (uint32_t)(st * SG_STAGE);
+        const bool kok = c * SG_KC + lane < kc;
+        const double* src = a_src + c * SG_KC;
 #pragma unroll
-        for (int i = 0; i < SG_R * SG_KC / SG_T; ++i) {
-            const int e = tid + SG_T * i, r = e / SG_KC, kk = e % SG_KC, kg = c * SG_KC + kk;
-            const bool ok = r < nr && kg < kc;
-            cp_async8(&As[r * SG_LDA + kk], ok ? base + (int64_t)(rbase + r) * m + kbeg + kg : base, ok);
+        for (int i = 0; i < SG_R / 8; ++i) {
+            const bool ok = kok && warp + 8 * i < nr;
+            cpa8(dst + 8u * (uint32_t)(8 * i * SG_LDA), ok ? src + i * a_rstep : base, ok);
         }
     };
-    auto issue_b = [&](int c) {
+    auto issue_b = [&](int c, int st) {
 #ifdef SG_NOB
         return;
 #endif
-        double* Bsb = sm + (c % nstage) * SG_STAGE + SG_R * SG_LDA;
+        if (lane >= 8 * NCT) return;   // member columns no column tile of this launch reads
+        const uint32_t dst = b_dst + 8u * (uint32_t)(st * SG_STAGE);
 #pragma unroll
-        for (int i = 0; i < SG_KC * SG_C / SG_T; ++i) {
-            const int e = tid + SG_T * i, kk = e / SG_C, j = e % SG_C, kg = c * SG_KC + kk;
-            const bool ok = j < jn && kg < kc;
+        for (int i = 0; i < SG_KC / 8; ++i) {
+            const int kg = c * SG_KC + warp + 8 * i;
+            const bool ok = jok && kg < kc;
             const int kq = min(kg, kc - 1), t = kbeg + kq;
-            const double* src = (!bwd || t < k) ? fr + (int64_t)t * J + j0 + j : x + (int64_t)s_idx[kq] * J + j0 + j;
-            cp_async8(&Bsb[kk * SG_LDB + j], ok ? src : base, ok);
+            const double* src = (!bwd || t < k) ? b_fr + (int64_t)t * J : b_x + (int64_t)s_idx[kq] * J;
+            cpa8(dst + 8u * (uint32_t)(8 * i * SG_LDB), ok ? src : base, ok);
         }
     };
     // (1) first A chunk, epilogue operands, backward gather descriptors
-    issue_a(0);
+    issue_a(0, 0);
     const int xrow = (bwd && row_ok) ? d.idx[fo + rbase + row] : 0;
     double init[4][2] = {{0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}};
     if (!bwd && hasch && row_ok) {
@@ -282,28 +299,31 @@ __global__ void __launch_bounds__(SG_T, SG_MINB) k_sgemm(MfDev d, const int4* __
     __syncthreads();
     SG_T_(1);
     // (2) pipeline prologue: stages 0 .. nstage-2, one commit group each
-    issue_b(0);
+    issue_b(0, 0);
     cp_async_commit();
     for (int c = 1; c < nstage - 1; ++c) {
         if (c < nch) {
-            issue_a(c);
-            issue_b(c);
+            issue_a(c, c);
+            issue_b(c, c);
         }
         cp_async_commit();
     }
     SG_T_(2);
     // (3) mainloop
     double dacc[4][2] = {{0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}};
+    int ust = 0;   // stage of chunk c (= c mod nstage); chunk c + nstage - 1 goes to the stage before it
     for (int c = 0; c < nch; ++c) {
         cp_async_wait_n(nstage - 2);
         __syncthreads();
         const int cn = c + nstage - 1;
         if (cn < nch) {
-            issue_a(cn);
-            issue_b(cn);
+            const int ist = ust == 0 ? nstage - 1 : ust - 1;
+            issue_a(cn, ist);
+            issue_b(cn, ist);
         }
         cp_async_commit();
-        const double* As = sm + (c % nstage) * SG_STAGE;
+        const double* As = sm + ust * SG_STAGE;
+        ust = ust + 1 == nstage ? 0 : ust + 1;
         const double* ap = As + row * SG_LDA + q;
         const double* bp = As + SG_R * SG_LDA + q * SG_LDB + g;
         const int ksteps = (min(SG_KC, kc - c * SG_KC) + 3) >> 2;
