@@ -381,18 +381,26 @@ __global__ void k_member_pass(const int32_t* __restrict__ enodes, const double* 
                               const double* __restrict__ X, const double* __restrict__ means, double* __restrict__ rhs,
                               unsigned long long* __restrict__ maxsq, int nt, int nvel, int64_t N, int J, int JB,
                               double* __restrict__ ec) {
-    extern __shared__ double sh_sq[];   // [EPB][2][7][JB]
+    extern __shared__ double sh_sq[];   // [EPB][2][7][JB], then the elements' nodal means [EPB][2][6][2]
     const int EPB = blockDim.x / JB;
     const int el = threadIdx.x / JB, jj = threadIdx.x % JB;
     const int e = e0 + blockIdx.x * EPB + el;
     const int j = blockIdx.y * JB + jj;
     const bool live = (el < EPB) && (e < e0 + ne) && (j < J);
     double* sq = sh_sq + (size_t)el * 2 * ENS_NQ * JB;
+    // the ensemble means at the element's nodes are member-independent: staged once per
+    // element in shared memory instead of 24 per-thread registers (occupancy)
+    double* smn = sh_sq + (size_t)EPB * 2 * ENS_NQ * JB + (size_t)el * 24;
+    if (el < EPB && e < e0 + ne) {
+        for (int t = jj; t < 24; t += JB) {
+            const int fam = t / 12, a = (t % 12) >> 1, cc = t & 1;
+            smn[t] = means[(int64_t)fam * nvel + 2LL * enodes[(int64_t)e * 6 + a] + cc];
+        }
+    }
+    __syncthreads();
     if (live) {
         const double* Xv = X;
         const double* Xw = X + N * J;
-        const double* mv = means;
-        const double* mw = means + nvel;
         int nd[6];
 #pragma unroll
         for (int a = 0; a < 6; ++a) nd[a] = enodes[(int64_t)e * 6 + a];
@@ -400,7 +408,7 @@ __global__ void k_member_pass(const int32_t* __restrict__ enodes, const double* 
         const double area = egeo[(int64_t)e * 8];
 #pragma unroll
         for (int i = 0; i < 6; ++i) gl[i] = egeo[(int64_t)e * 8 + 1 + i];
-        double v[6][2], w[6][2], fv[6][2], fw[6][2];
+        double v[6][2], w[6][2];
 #pragma unroll
         for (int a = 0; a < 6; ++a) {
 #pragma unroll
@@ -408,8 +416,6 @@ __global__ void k_member_pass(const int32_t* __restrict__ enodes, const double* 
                 const int64_t row = 2LL * nd[a] + cc;
                 v[a][cc] = Xv[row * J + j];
                 w[a][cc] = Xw[row * J + j];
-                fv[a][cc] = v[a][cc] - mv[row];
-                fw[a][cc] = w[a][cc] - mw[row];
             }
         }
         double rv[6][2], rw[6][2];
@@ -424,10 +430,10 @@ __global__ void k_member_pass(const int32_t* __restrict__ enodes, const double* 
                 const double ph = c_phi[q][a];
                 double gx, gy;
                 grad_phi(gl, q, a, gx, gy);
-                fvq0 += fv[a][0] * ph;
-                fvq1 += fv[a][1] * ph;
-                fwq0 += fw[a][0] * ph;
-                fwq1 += fw[a][1] * ph;
+                fvq0 += (v[a][0] - smn[2 * a]) * ph;
+                fvq1 += (v[a][1] - smn[2 * a + 1]) * ph;
+                fwq0 += (w[a][0] - smn[12 + 2 * a]) * ph;
+                fwq1 += (w[a][1] - smn[12 + 2 * a + 1]) * ph;
                 gv00 += v[a][0] * gx;
                 gv01 += v[a][0] * gy;
                 gv10 += v[a][1] * gx;
@@ -529,7 +535,7 @@ int launch_member_pass(ens_ctx* c, cudaStream_t s, const double* x, const double
         const int JB = J < 128 ? J : 128;
         const int EPB = 128 / JB > 0 ? 128 / JB : 1;
         const int threads = EPB * JB;
-        const size_t shm = sizeof(double) * (size_t)EPB * 2 * ENS_NQ * JB;
+        const size_t shm = sizeof(double) * ((size_t)EPB * 2 * ENS_NQ * JB + (size_t)EPB * 24);
         const size_t ecb = sizeof(double) * 2 * (size_t)c->m.nt * 12 * J;
         if (!c->ec) {
             ENS_CK(cudaMalloc(&c->ec, ecb));
@@ -551,7 +557,7 @@ int launch_member_pass(ens_ctx* c, cudaStream_t s, const double* x, const double
     const int JB = J < 128 ? J : 128;
     const int EPB = 128 / JB > 0 ? 128 / JB : 1;
     const int threads = EPB * JB;
-    const size_t shm = sizeof(double) * (size_t)EPB * 2 * ENS_NQ * JB;
+    const size_t shm = sizeof(double) * ((size_t)EPB * 2 * ENS_NQ * JB + (size_t)EPB * 24);
     ENS_CK(cudaMemsetAsync(maxsq, 0, sizeof(double) * 2 * (size_t)c->m.nt * ENS_NQ, s));
     for (int col = 0; col < c->m.ncolor; ++col) {
         const int e0 = c->color_off[col], ne = c->color_off[col + 1] - e0;
