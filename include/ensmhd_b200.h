@@ -209,6 +209,13 @@ int  ens_rhs(ens_ctx* ctx, void* stream, const double* x, const double* member_c
  * maxsq (nmat x nt x 7; matrix V uses w', W uses v') (ensemble.py:227-238). */
 int  ens_member_pass(ens_ctx* ctx, void* stream, const double* x, const double* means, double* rhs, double* maxsq);
 
+/* ens_rhs + ens_member_pass in one element pass (even J): every element's whole
+ * right-hand side of both sub-steps, M same/dt - N(z') same - K(ls same + lc other),
+ * at the 7 quadrature points that assemble M and K exactly, summed per row in a
+ * fixed order with the loads added; maxsq as ens_member_pass (stepper.py:223-252). */
+int  ens_rhs_fused(ens_ctx* ctx, void* stream, const double* x, const double* means, const double* member_coef,
+                   double inv_dt, const ens_data_desc* loads, double* rhs, double* maxsq);
+
 /* Identity-row values: rhs[cons] = Dirichlet data (stepper.py:250) or 0 (pin, stepper.py:251). */
 int  ens_apply_bc(ens_ctx* ctx, void* stream, const ens_data_desc* bvals, double* rhs);
 

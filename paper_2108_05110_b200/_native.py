@@ -66,7 +66,7 @@ class DataDesc(C.Structure):
 SYMBOLS = [
     "ens_abi_version", "ens_last_error", "ens_kernel_launches", "ens_create", "ens_set_pivoting",
     "ens_set_spmm_blocks", "ens_set_spmm_tiles", "ens_destroy", "ens_workspace_bytes",
-    "ens_lincomb", "ens_member_sums", "ens_rhs", "ens_member_pass", "ens_apply_bc", "ens_assemble", "ens_factor",
+    "ens_lincomb", "ens_member_sums", "ens_rhs", "ens_member_pass", "ens_rhs_fused", "ens_apply_bc", "ens_assemble", "ens_factor",
     "ens_solve", "ens_solve_begin", "ens_solve_finish", "ens_spmm", "ens_precond_apply", "ens_epilogue", "ens_diagnostics",
 ]
 
@@ -96,6 +96,7 @@ def load(path: str = LIB_PATH):
     lib.ens_lincomb.argtypes = [P, P, F64, P, F64, P]
     lib.ens_rhs.argtypes = [P, P, P, P, F64, C.POINTER(DataDesc), P]
     lib.ens_member_pass.argtypes = [P, P, P, P, P, P]
+    lib.ens_rhs_fused.argtypes = [P, P, P, P, P, F64, C.POINTER(DataDesc), P, P]
     lib.ens_apply_bc.argtypes = [P, P, C.POINTER(DataDesc), P]
     lib.ens_assemble.argtypes = [P, P, P, P, P, F64, P]
     lib.ens_factor.argtypes = [P, P, P, C.POINTER(I32)]

@@ -197,6 +197,12 @@ int ens_member_pass(ens_ctx* c, void* stream, const double* x, const double* mea
     return launch_member_pass(c, (cudaStream_t)stream, x, means, rhs, maxsq);
 }
 
+int ens_rhs_fused(ens_ctx* c, void* stream, const double* x, const double* means, const double* member_coef,
+                  double inv_dt, const ens_data_desc* loads, double* rhs, double* maxsq) {
+    if (!c || !x || !means || !member_coef || !rhs || !maxsq) return ENS_EINVAL;
+    return launch_rhs_fused(c, (cudaStream_t)stream, x, means, member_coef, inv_dt, loads, rhs, maxsq);
+}
+
 int ens_apply_bc(ens_ctx* c, void* stream, const ens_data_desc* bvals, double* rhs) {
     if (!c || !rhs) return ENS_EINVAL;
     return launch_apply_bc(c, (cudaStream_t)stream, bvals, rhs);

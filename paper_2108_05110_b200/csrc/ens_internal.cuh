@@ -97,6 +97,8 @@ int launch_lincomb(ens_ctx* c, cudaStream_t s, double a, const double* x, double
 int launch_rhs(ens_ctx* c, cudaStream_t s, const double* x, const double* coef, double inv_dt,
                const ens_data_desc* loads, double* rhs);
 int launch_member_pass(ens_ctx* c, cudaStream_t s, const double* x, const double* means, double* rhs, double* maxsq);
+int launch_rhs_fused(ens_ctx* c, cudaStream_t s, const double* x, const double* means, const double* coef,
+                     double inv_dt, const ens_data_desc* loads, double* rhs, double* maxsq);
 int launch_apply_bc(ens_ctx* c, cudaStream_t s, const ens_data_desc* bv, double* rhs);
 int launch_assemble(ens_ctx* c, cudaStream_t s, const double* base, const double* means, const double* maxsq,
                     double two_mu_dt, double* as_vals);

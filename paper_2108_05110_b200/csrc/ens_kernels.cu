@@ -377,10 +377,15 @@ int launch_rhs(ens_ctx* c, cudaStream_t s, const double* x, const double* coef, 
 //   (fem.py:411-420, ensemble.py:227-238); one thread per (element, member),
 //   elements of one colour touch disjoint dofs -> plain read-modify-write.
 // ---------------------------------------------------------------------------
+// FULL (ens_rhs_fused): the element buffer receives the whole element right-hand side of
+// both sub-steps, M same/dt - N(z') same - K(ls same + lc other) (stepper.py:235-247 with
+// fem.py:411-420), evaluated at the 7 quadrature points that assemble M and K exactly;
+// k_member_gather<true> then sums it per row and adds the loads -- no CSR pass.
+template <bool FULL>
 __global__ void k_member_pass(const int32_t* __restrict__ enodes, const double* __restrict__ egeo, int e0, int ne,
                               const double* __restrict__ X, const double* __restrict__ means, double* __restrict__ rhs,
                               unsigned long long* __restrict__ maxsq, int nt, int nvel, int64_t N, int J, int JB,
-                              double* __restrict__ ec) {
+                              double* __restrict__ ec, const double* __restrict__ mcoef, double inv_dt) {
     extern __shared__ double sh_sq[];   // [EPB][2][7][JB], then the elements' nodal means [EPB][2][6][2]
     const int EPB = blockDim.x / JB;
     const int el = threadIdx.x / JB, jj = threadIdx.x % JB;
@@ -421,9 +426,11 @@ __global__ void k_member_pass(const int32_t* __restrict__ enodes, const double* 
         double rv[6][2], rw[6][2];
 #pragma unroll
         for (int a = 0; a < 6; ++a) rv[a][0] = rv[a][1] = rw[a][0] = rw[a][1] = 0.0;
+        const double ls = FULL ? mcoef[j] : 0.0, lc = FULL ? mcoef[J + j] : 0.0;
 #pragma unroll 1
         for (int q = 0; q < ENS_NQ; ++q) {
             double fvq0 = 0, fvq1 = 0, fwq0 = 0, fwq1 = 0;
+            double vq0 = 0, vq1 = 0, wq0 = 0, wq1 = 0;
             double gv00 = 0, gv01 = 0, gv10 = 0, gv11 = 0, gw00 = 0, gw01 = 0, gw10 = 0, gw11 = 0;
 #pragma unroll
             for (int a = 0; a < 6; ++a) {
@@ -434,6 +441,12 @@ __global__ void k_member_pass(const int32_t* __restrict__ enodes, const double* 
                 fvq1 += (v[a][1] - smn[2 * a + 1]) * ph;
                 fwq0 += (w[a][0] - smn[12 + 2 * a]) * ph;
                 fwq1 += (w[a][1] - smn[12 + 2 * a + 1]) * ph;
+                if (FULL) {
+                    vq0 += v[a][0] * ph;
+                    vq1 += v[a][1] * ph;
+                    wq0 += w[a][0] * ph;
+                    wq1 += w[a][1] * ph;
+                }
                 gv00 += v[a][0] * gx;
                 gv01 += v[a][0] * gy;
                 gv10 += v[a][1] * gx;
@@ -451,13 +464,34 @@ __global__ void k_member_pass(const int32_t* __restrict__ enodes, const double* 
             const double cv1 = wd * (fwq0 * gv10 + fwq1 * gv11);
             const double cw0 = wd * (fvq0 * gw00 + fvq1 * gw01);
             const double cw1 = wd * (fvq0 * gw10 + fvq1 * gw11);
+            if (FULL) {
+                // value part (M same/dt - convection) and gradient part (K terms) of both systems
+                const double wdt = wd * inv_dt;
+                const double tv0 = wdt * vq0 - cv0, tv1 = wdt * vq1 - cv1;
+                const double tw0 = wdt * wq0 - cw0, tw1 = wdt * wq1 - cw1;
+                const double hv0x = wd * (ls * gv00 + lc * gw00), hv0y = wd * (ls * gv01 + lc * gw01);
+                const double hv1x = wd * (ls * gv10 + lc * gw10), hv1y = wd * (ls * gv11 + lc * gw11);
+                const double hw0x = wd * (ls * gw00 + lc * gv00), hw0y = wd * (ls * gw01 + lc * gv01);
+                const double hw1x = wd * (ls * gw10 + lc * gv10), hw1y = wd * (ls * gw11 + lc * gv11);
 #pragma unroll
-            for (int a = 0; a < 6; ++a) {
-                const double ph = c_phi[q][a];
-                rv[a][0] += cv0 * ph;
-                rv[a][1] += cv1 * ph;
-                rw[a][0] += cw0 * ph;
-                rw[a][1] += cw1 * ph;
+                for (int a = 0; a < 6; ++a) {
+                    const double ph = c_phi[q][a];
+                    double gx, gy;
+                    grad_phi(gl, q, a, gx, gy);
+                    rv[a][0] += ph * tv0 - (gx * hv0x + gy * hv0y);
+                    rv[a][1] += ph * tv1 - (gx * hv1x + gy * hv1y);
+                    rw[a][0] += ph * tw0 - (gx * hw0x + gy * hw0y);
+                    rw[a][1] += ph * tw1 - (gx * hw1x + gy * hw1y);
+                }
+            } else {
+#pragma unroll
+                for (int a = 0; a < 6; ++a) {
+                    const double ph = c_phi[q][a];
+                    rv[a][0] += cv0 * ph;
+                    rv[a][1] += cv1 * ph;
+                    rw[a][0] += cw0 * ph;
+                    rw[a][1] += cw1 * ph;
+                }
             }
         }
         if (ec) {   // element buffer [mat][e][a][cc][j], gathered per row by k_member_gather
@@ -501,9 +535,14 @@ __global__ void k_member_pass(const int32_t* __restrict__ enodes, const double* 
 }
 
 // rhs[mat][row][j] -= sum over the node's element entries (fixed order) -- even J, 16-byte lanes
+// FULL: rhs[mat][row][j] = sum of the entries + loads (basis x coefficients and/or dense)
+template <bool FULL>
 __global__ void __launch_bounds__(256) k_member_gather(const int32_t* __restrict__ n2e_ptr,
                                                        const int32_t* __restrict__ n2e, const double* __restrict__ ec,
-                                                       double* __restrict__ rhs, int ns, int nt, int64_t N, int J) {
+                                                       double* __restrict__ rhs, int ns, int nt, int64_t N, int J,
+                                                       int K, const double* __restrict__ lbasis,
+                                                       const double* __restrict__ lcoef,
+                                                       const double* __restrict__ ldense) {
     const int H = J >> 1;
     const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (t >= 2LL * ns * H) return;
@@ -521,6 +560,23 @@ __global__ void __launch_bounds__(256) k_member_gather(const int32_t* __restrict
         acc.y += v.y;
     }
     double2* r2 = reinterpret_cast<double2*>(rhs + (int64_t)mat * N * J);
+    if (FULL) {
+        const int64_t nvel = 2LL * ns;
+        const int j = 2 * jp;
+        for (int kk = 0; kk < K; ++kk) {
+            const double bval = lbasis[(int64_t)kk * nvel + row];
+            const double* cf = lcoef + ((int64_t)mat * K + kk) * J + j;
+            acc.x += cf[0] * bval;
+            acc.y += cf[1] * bval;
+        }
+        if (ldense) {
+            const double2 dd = reinterpret_cast<const double2*>(ldense + (int64_t)mat * nvel * J)[row * H + jp];
+            acc.x += dd.x;
+            acc.y += dd.y;
+        }
+        r2[row * H + jp] = acc;
+        return;
+    }
     double2 r = r2[row * H + jp];
     r.x -= acc.x;
     r.y -= acc.y;
@@ -543,13 +599,13 @@ int launch_member_pass(ens_ctx* c, cudaStream_t s, const double* x, const double
         }
         ENS_CK(cudaMemsetAsync(maxsq, 0, sizeof(double) * 2 * (size_t)c->m.nt * ENS_NQ, s));
         dim3 grid((c->m.nt + EPB - 1) / EPB, (J + JB - 1) / JB);
-        k_member_pass<<<grid, threads, shm, s>>>(c->m.e_nodes, c->m.e_geo, 0, c->m.nt, x, means, rhs,
-                                                  reinterpret_cast<unsigned long long*>(maxsq), c->m.nt, c->n_vel,
-                                                  c->n_total, J, JB, c->ec);
+        k_member_pass<false><<<grid, threads, shm, s>>>(c->m.e_nodes, c->m.e_geo, 0, c->m.nt, x, means, rhs,
+                                                         reinterpret_cast<unsigned long long*>(maxsq), c->m.nt,
+                                                         c->n_vel, c->n_total, J, JB, c->ec, nullptr, 0.0);
         ENS_CKL();
         const int64_t tot = 2LL * c->m.ns * (J / 2);
-        k_member_gather<<<dim3((unsigned)((tot + 255) / 256), 2), 256, 0, s>>>(c->m.n2e_ptr, c->m.n2e, c->ec, rhs,
-                                                                             c->m.ns, c->m.nt, c->n_total, J);
+        k_member_gather<false><<<dim3((unsigned)((tot + 255) / 256), 2), 256, 0, s>>>(
+            c->m.n2e_ptr, c->m.n2e, c->ec, rhs, c->m.ns, c->m.nt, c->n_total, J, 0, nullptr, nullptr, nullptr);
         ENS_CKL();
         return ENS_OK;
     }
@@ -563,11 +619,50 @@ int launch_member_pass(ens_ctx* c, cudaStream_t s, const double* x, const double
         const int e0 = c->color_off[col], ne = c->color_off[col + 1] - e0;
         if (ne == 0) continue;
         dim3 grid((ne + EPB - 1) / EPB, (J + JB - 1) / JB);
-        k_member_pass<<<grid, threads, shm, s>>>(c->m.e_nodes, c->m.e_geo, e0, ne, x, means, rhs,
-                                                  reinterpret_cast<unsigned long long*>(maxsq), c->m.nt, c->n_vel,
-                                                  c->n_total, J, JB, nullptr);
+        k_member_pass<false><<<grid, threads, shm, s>>>(c->m.e_nodes, c->m.e_geo, e0, ne, x, means, rhs,
+                                                         reinterpret_cast<unsigned long long*>(maxsq), c->m.nt,
+                                                         c->n_vel, c->n_total, J, JB, nullptr, nullptr, 0.0);
         ENS_CKL();
     }
+    return ENS_OK;
+}
+
+// whole velocity right-hand side of both sub-steps and the eddy-viscosity maxima in one element
+// pass + one ordered row gather (replaces launch_rhs + launch_member_pass for even J)
+int launch_rhs_fused(ens_ctx* c, cudaStream_t s, const double* x, const double* means, const double* coef,
+                     double inv_dt, const ens_data_desc* loads, double* rhs, double* maxsq) {
+    const int J = c->J;
+    const bool aligned = ((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(rhs) |
+                           (loads && loads->dense ? reinterpret_cast<uintptr_t>(loads->dense) : 0)) & 15) == 0;
+    if (!c->m.n2e || (J & 1) || !aligned) {
+        const int rc = launch_rhs(c, s, x, coef, inv_dt, loads, rhs);
+        if (rc != ENS_OK) return rc;
+        return launch_member_pass(c, s, x, means, rhs, maxsq);
+    }
+    const int64_t N = c->n_total;
+    for (int mat = 0; mat < 2; ++mat)   // pressure rows of the right-hand side are zero (stepper.py:245-246)
+        ENS_CK(cudaMemsetAsync(rhs + mat * N * J + (int64_t)c->n_vel * J, 0,
+                               sizeof(double) * (size_t)c->m.n_pres * J, s));
+    const int JB = J < 128 ? J : 128;
+    const int EPB = 128 / JB > 0 ? 128 / JB : 1;
+    const int threads = EPB * JB;
+    const size_t shm = sizeof(double) * ((size_t)EPB * 2 * ENS_NQ * JB + (size_t)EPB * 24);
+    const size_t ecb = sizeof(double) * 2 * (size_t)c->m.nt * 12 * J;
+    if (!c->ec) {
+        ENS_CK(cudaMalloc(&c->ec, ecb));
+        c->ws_bytes += ecb;
+    }
+    ENS_CK(cudaMemsetAsync(maxsq, 0, sizeof(double) * 2 * (size_t)c->m.nt * ENS_NQ, s));
+    dim3 grid((c->m.nt + EPB - 1) / EPB, (J + JB - 1) / JB);
+    k_member_pass<true><<<grid, threads, shm, s>>>(c->m.e_nodes, c->m.e_geo, 0, c->m.nt, x, means, rhs,
+                                                    reinterpret_cast<unsigned long long*>(maxsq), c->m.nt, c->n_vel,
+                                                    N, J, JB, c->ec, coef, inv_dt);
+    ENS_CKL();
+    const int64_t tot = 2LL * c->m.ns * (J / 2);
+    k_member_gather<true><<<dim3((unsigned)((tot + 255) / 256), 2), 256, 0, s>>>(
+        c->m.n2e_ptr, c->m.n2e, c->ec, rhs, c->m.ns, c->m.nt, N, J, loads ? loads->K : 0,
+        loads ? loads->basis : nullptr, loads ? loads->coef : nullptr, loads ? loads->dense : nullptr);
+    ENS_CKL();
     return ENS_OK;
 }
 

@@ -464,6 +464,7 @@ class Engine:
         # whole-step CUDA graphs (ENS_STEP_GRAPH=0 disables): per buffer parity and problem,
         # the pre-solve sequence and the solve's first cycle + epilogue, replayed every step
         self.step_graphs = os.environ.get("ENS_STEP_GRAPH", "1") != "0"
+        self.rhs_fused = os.environ.get("ENS_RHS_FUSED", "1") != "0"
         self._graphs = {}
         self._gdata_cache = {}
         self._gspec = {}
@@ -757,10 +758,7 @@ class Engine:
             torch.mul(self.sums, 1.0 / self.J_total, out=self.means)
             if lo is not None:
                 lo[2].copy_(lo[1], non_blocking=True)
-            N.check(lib.ens_rhs(ctx, s, _dptr(X), _dptr(self.member_coef), 1.0 / self.config.dt,
-                                C.byref(lo[3]) if lo is not None else None, _dptr(self.rhs)), "ens_rhs")
-            N.check(lib.ens_member_pass(ctx, s, _dptr(X), _dptr(self.means), _dptr(self.rhs), _dptr(self.maxsq)),
-                    "ens_member_pass")
+            self._rhs_and_member_pass(X, C.byref(lo[3]) if lo is not None else None)
 
         def assemble():
             bc[2].copy_(bc[1], non_blocking=True)
@@ -869,10 +867,7 @@ class Engine:
         if not self.means_valid:
             self._compute_means()
         loads, keep1 = self._data(forcing, "loads", t_next)
-        N.check(lib.ens_rhs(ctx, s, _dptr(X), _dptr(self.member_coef), 1.0 / self.config.dt,
-                            C.byref(loads) if loads is not None else None, _dptr(self.rhs)), "ens_rhs")
-        N.check(lib.ens_member_pass(ctx, s, _dptr(X), _dptr(self.means), _dptr(self.rhs), _dptr(self.maxsq)),
-                "ens_member_pass")
+        self._rhs_and_member_pass(X, C.byref(loads) if loads is not None else None)
         XC.allreduce_eddy_max(self.maxsq, self.comm)
         bvals, keep2 = self._data(boundary, "bc", t_next)
         N.check(lib.ens_apply_bc(ctx, s, C.byref(bvals), _dptr(self.rhs)), "ens_apply_bc")
@@ -982,6 +977,20 @@ class Engine:
             print(f"renew: pos {steps} step {step_ms:.2f} ms (F {self._cyc[0]:.2f}) iters {self.last_iters} "
                   f"pred {nxt:.2f} avg {(self._cyc[0] + self._cyc[1]) / steps:.2f}", flush=True)
         return nxt > (self._cyc[0] + self._cyc[1]) / steps
+
+    def _rhs_and_member_pass(self, X, loads_ref):
+        """Right-hand sides of both sub-steps + eddy-viscosity maxima (one element pass by default;
+        ENS_RHS_FUSED=0: the CSR mass/stiffness pass followed by the fluctuation-transport pass)."""
+        lib, ctx, s = self.lib, self.ctx, self.sptr
+        if self.rhs_fused:
+            N.check(lib.ens_rhs_fused(ctx, s, _dptr(X), _dptr(self.means), _dptr(self.member_coef),
+                                      1.0 / self.config.dt, loads_ref, _dptr(self.rhs), _dptr(self.maxsq)),
+                    "ens_rhs_fused")
+            return
+        N.check(lib.ens_rhs(ctx, s, _dptr(X), _dptr(self.member_coef), 1.0 / self.config.dt, loads_ref,
+                            _dptr(self.rhs)), "ens_rhs")
+        N.check(lib.ens_member_pass(ctx, s, _dptr(X), _dptr(self.means), _dptr(self.rhs), _dptr(self.maxsq)),
+                "ens_member_pass")
 
     def _factor(self):
         npert = N.I32(0)

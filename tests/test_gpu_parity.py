@@ -82,8 +82,11 @@ def test_spmm_matches_scipy(c1, rng):
         assert np.max(np.abs(r[m][hm.int_id] - (b[m] - ref))) <= 1e-13 * np.abs(ref).max()
 
 
-def test_member_pass_assembly_rhs(c1, rng):
+@pytest.mark.parametrize("fused", [False, True])
+def test_member_pass_assembly_rhs(c1, rng, fused):
     disc, cfg, prob = c1
+    if fused:   # ens_rhs_fused needs even J: same case with 4 members
+        disc, cfg, prob = P.build_case("C1", J=4)
     eng = Engine(disc, cfg)
     hm = eng.hm
     v, w = perturbed_state(disc, cfg, rng, 1.0)
@@ -96,10 +99,14 @@ def test_member_pass_assembly_rhs(c1, rng):
     from paper_2108_05110_b200.engine import _dptr
     X = eng.X[eng.cur]
     loads, k1 = eng._data(prob.forcing, "loads", t)
-    N.check(eng.lib.ens_rhs(eng.ctx, eng.sptr, _dptr(X), _dptr(eng.member_coef), 1.0 / cfg.dt, C.byref(loads),
-                            _dptr(eng.rhs)), "rhs")
-    N.check(eng.lib.ens_member_pass(eng.ctx, eng.sptr, _dptr(X), _dptr(eng.means), _dptr(eng.rhs),
-                                    _dptr(eng.maxsq)), "mp")
+    if fused:
+        N.check(eng.lib.ens_rhs_fused(eng.ctx, eng.sptr, _dptr(X), _dptr(eng.means), _dptr(eng.member_coef),
+                                      1.0 / cfg.dt, C.byref(loads), _dptr(eng.rhs), _dptr(eng.maxsq)), "fused")
+    else:
+        N.check(eng.lib.ens_rhs(eng.ctx, eng.sptr, _dptr(X), _dptr(eng.member_coef), 1.0 / cfg.dt,
+                                C.byref(loads), _dptr(eng.rhs)), "rhs")
+        N.check(eng.lib.ens_member_pass(eng.ctx, eng.sptr, _dptr(X), _dptr(eng.means), _dptr(eng.rhs),
+                                        _dptr(eng.maxsq)), "mp")
     bv, k2 = eng._data(prob.boundary, "bc", t)
     N.check(eng.lib.ens_apply_bc(eng.ctx, eng.sptr, C.byref(bv), _dptr(eng.rhs)), "bc")
     N.check(eng.lib.ens_assemble(eng.ctx, eng.sptr, _dptr(eng.base), _dptr(eng.means), _dptr(eng.maxsq),
