@@ -24,6 +24,13 @@
 #include "ens_internal.cuh"
 #include "ens_mf_common.cuh"
 
+// Programmatic dependent launch (sm_90+): a kernel launched with programmatic stream
+// serialisation may start while its predecessor drains; everything before pdl_wait() must
+// read only data that no in-flight kernel writes (here: factor entries, descriptors, index
+// lists).  Both are no-ops for kernels launched normally.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
 struct SolveIO {
     const double* r;
     double* z;
@@ -138,6 +145,7 @@ __global__ void __launch_bounds__(256) k_finit(const int32_t* __restrict__ rows,
                                                double* __restrict__ FR, const SolveIO* __restrict__ io, int64_t N,
                                                int J, int64_t nidx) {
     const int mat = blockIdx.y;
+    pdl_wait();   // children's contribution rows come from the previous level's GEMM
     const double* b = io->r + (int64_t)mat * N * J;
     double* FRm = FR + (int64_t)mat * nidx * J;
     if ((J & 1) == 0) {
@@ -176,6 +184,7 @@ __global__ void __launch_bounds__(256) k_finit(const int32_t* __restrict__ rows,
             FRm[row * J + j] = e < 0 ? bv + v : v;
         }
     }
+    pdl_trigger();
 }
 
 __device__ __forceinline__ void cp_async_wait_n(int n) {
@@ -280,9 +289,11 @@ __global__ void __launch_bounds__(SG_T, SG_MINB) k_sgemm(MfDev d, const int4* __
             cpa8(dst + 8u * (uint32_t)(8 * i * SG_LDB), ok ? src : base, ok);
         }
     };
-    // (1) first A chunk, epilogue operands, backward gather descriptors
+    // (1) first A chunk (factor entries: safe before the dependency wait), epilogue operands,
+    // backward gather descriptors
     issue_a(0, 0);
     const int xrow = (bwd && row_ok) ? d.idx[fo + rbase + row] : 0;
+    pdl_wait();   // front rows / the iterate come from the previous launch
     double init[4][2] = {{0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}};
     if (!bwd && hasch && row_ok) {
         const double* pr = FRm + (fo + rbase + row) * J + j0;
@@ -345,6 +356,7 @@ __global__ void __launch_bounds__(SG_T, SG_MINB) k_sgemm(MfDev d, const int4* __
             }
         }
     }
+    pdl_trigger();   // the next launch may start its prologue while this epilogue runs
 #ifdef SG_PROBE
     __syncthreads();
     SG_T_(3);
@@ -567,6 +579,33 @@ static bool capturing(cudaStream_t s) {
     return st != cudaStreamCaptureStatusNone;
 }
 
+static bool pdl_enabled() {
+    static int v = -1;
+    if (v < 0) {
+        const char* e = std::getenv("ENS_PDL");
+        v = e ? std::atoi(e) : 1;
+    }
+    return v != 0;
+}
+
+// launch with programmatic stream serialisation (overlaps this launch's prologue with the
+// predecessor's tail; see pdl_wait)
+template <typename... KArgs, typename... Args>
+static cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                              Args... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
+}
+
 // record the launch sequence of one solve (io table fixed)
 static int mf_solve_launches(ens_ctx* c, cudaStream_t s, SolveIO* io, int64_t* nlaunch) {
     MfDev d = mfdev(c);
@@ -618,8 +657,8 @@ static int mf_solve_launches(ens_ctx* c, cudaStream_t s, SolveIO* io, int64_t* n
                 if (nr > 0) {
                     const unsigned nb = (unsigned)std::min<int64_t>((tot + 255) / 256, 148 * 8);
                     for (int rep = 0; rep < (timing ? trep : 1); ++rep) {
-                        k_finit<<<dim3(nb, 2), 256, 0, s>>>(c->finit_rows + a, nr, c->p.f_idx, c->p.gsrc, c->frvec, io,
-                                                            N, J, nidx);
+                        ENS_CK(launch_pdl(k_finit, dim3(nb, 2), dim3(256), 0, s, c->finit_rows + a, nr, c->p.f_idx,
+                                          c->p.gsrc, c->frvec, io, N, J, nidx));
                         ENS_CKL();
                     }
                     ++cnt;
@@ -658,9 +697,10 @@ static int mf_solve_launches(ens_ctx* c, cudaStream_t s, SolveIO* io, int64_t* n
             for (int rep = 0; rep < (timing ? trep : 1); ++rep) {   // launches are idempotent
                 // member column blocks: full 32-wide blocks use 4 column tiles, the remainder fewer
                 const int zfull = J / SG_C, rem = J - zfull * SG_C;
-#define SGL(NC, ZN, Z0)                                                                                        \
-    k_sgemm<NC><<<dim3(n, 2, ZN), SG_T, sg_smem(nst), s>>>(d, c->sitem, off, c->fronts, c->frvec, io, N, J, nidx, \
-                                                          op == SOP_BGEMM, kmax, nst, c->partial, c->ticket, nslot, Z0)
+#define SGL(NC, ZN, Z0)                                                                                       \
+    ENS_CK(launch_pdl(k_sgemm<NC>, dim3(n, 2, ZN), dim3(SG_T), sg_smem(nst), s, d, c->sitem, off, c->fronts,    \
+                      c->frvec, io, N, J, nidx, (int)(op == SOP_BGEMM), kmax, nst, c->partial, c->ticket, nslot, \
+                      (int)(Z0)))
                 if (zfull > 0) {
                     SGL(4, (unsigned)zfull, 0);
                     ENS_CKL();

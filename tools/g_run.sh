@@ -1,4 +1,7 @@
-ENS_SOLVE_DEEP_CTAS=0 python tools/precond_ab.py 2>&1 | tail -1
-for st in 3 4 5; do for th in 296 444 888; do
-echo -n "stages $st ctas<=$th: "; ENS_SOLVE_DEEP_STAGES=$st ENS_SOLVE_DEEP_CTAS=$th python tools/precond_ab.py 2>&1 | tail -1
-done; done
+for i in 1 2; do
+ENS_LIB=$PWD/paper_2108_05110_b200/libensmhd_b200_old.so python tools/precond_ab.py 2>&1 | tail -1
+ENS_PDL=0 python tools/precond_ab.py 2>&1 | tail -1
+python tools/precond_ab.py 2>&1 | tail -1
+done
+python tools/step_ab.py 2>&1 | tail -1
+ENS_LIB=$PWD/paper_2108_05110_b200/libensmhd_b200_old.so python tools/step_ab.py 2>&1 | tail -1
