@@ -363,3 +363,28 @@ def test_step_graphs_bitwise_equal_eager(monkeypatch, case, over):
     assert torch.equal(out[0][0], out[1][0]) and torch.equal(out[0][1], out[1][1])
     assert out[0][2] == out[1][2]
     assert out[0][3] == 0 and out[1][3] > 0     # the graphed engine replayed captured kernels
+
+
+def test_sharded_path_single_rank_nccl():
+    """The member-sharded step (graph segments split at the collectives, eager NCCL allreduces,
+    rebuild decision agreed over ranks) on a 1-rank NCCL group reproduces the unsharded run
+    bitwise (an allreduce over one rank is the identity)."""
+    import os
+    import socket
+    import torch.distributed as dist
+    if dist.is_initialized():
+        pytest.skip("a process group is already initialised")
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    try:
+        disc, cfg, prob = P.build_case("C1", J=6, steps=8)
+        ref_report, ref_state, _ = P.run(cfg, prob)
+        report, state, _ = P.run(cfg, prob, comm=dist.group.WORLD)
+        assert np.array_equal(state.v, ref_state.v) and np.array_equal(state.w, ref_state.w)
+        assert np.array_equal(report.energy, ref_report.energy)
+        assert np.array_equal(report.residuals, ref_report.residuals)
+    finally:
+        dist.destroy_process_group()
