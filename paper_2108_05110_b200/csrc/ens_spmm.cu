@@ -159,7 +159,7 @@ __global__ void __launch_bounds__(256) k_spmm_pres(const int32_t* __restrict__ b
 // fixed-order reduction of per-lane member-pair squares: row groups of the warp
 // (lanes part + L*rr), then the block's warps; one partial row per block
 __device__ __forceinline__ void nrm_block_reduce(double2 (&sq)[2][2], int lane, int part, int L, int R, int J,
-                                                 double* __restrict__ nrm) {
+                                                 double* __restrict__ nrm, int bid) {
     __shared__ double2 red[8][2][2][32];
     const int warp = threadIdx.x >> 5;
 #pragma unroll
@@ -184,7 +184,7 @@ __device__ __forceinline__ void nrm_block_reduce(double2 (&sq)[2][2], int lane, 
             t.x += red[w][m][br][p].x;
             t.y += red[w][m][br][p].y;
         }
-        double* o = nrm + (((int64_t)blockIdx.x * 2 + m) * 2 + br) * J + 2 * p;
+        double* o = nrm + (((int64_t)bid * 2 + m) * 2 + br) * J + 2 * p;
         o[0] = t.x;
         o[1] = t.y;
     }
@@ -194,18 +194,18 @@ __device__ __forceinline__ void nrm_block_reduce(double2 (&sq)[2][2], int lane, 
 // reduced in fixed order (row groups of the warp, warps of the block) to one
 // partial per block: nrm[blk][mat][{b, r}][J]
 template <int V2, bool NRM>
-__global__ void __launch_bounds__(256) k_spmm_vel_v(const int32_t* __restrict__ rp, const int32_t* __restrict__ col,
+__device__ __forceinline__ void spmm_vel_body(const int32_t* __restrict__ rp, const int32_t* __restrict__ col,
                                                     const double* __restrict__ A, int nnz,
                                                     const int32_t* __restrict__ btp, const int32_t* __restrict__ btc,
                                                     const double* __restrict__ btv, const uint8_t* __restrict__ cflag,
                                                     const double* __restrict__ X, const double* __restrict__ Bv,
                                                     double* __restrict__ Y, int ns, int64_t N, int J, int L, int mode,
-                                                    double* __restrict__ nrm) {
+                                                    double* __restrict__ nrm, int bid) {
     // both systems per thread: one index stream feeds two independent gathers
     const int lane = threadIdx.x & 31;
     const int R = 32 / L;
     const int r = lane / L, part = lane - r * L;
-    const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t gw = ((int64_t)bid * blockDim.x + threadIdx.x) >> 5;
     const int64_t node = gw * R + r;
     double2 sq[2][2] = {{{0.0, 0.0}, {0.0, 0.0}}, {{0.0, 0.0}, {0.0, 0.0}}};   // [mat][b, r]
     if (!NRM && (r >= R || node >= ns)) return;
@@ -302,20 +302,31 @@ __global__ void __launch_bounds__(256) k_spmm_vel_v(const int32_t* __restrict__ 
         }
     }
     }   // live row
-    if (NRM) nrm_block_reduce(sq, lane, part, L, R, J, nrm);
+    if (NRM) nrm_block_reduce(sq, lane, part, L, R, J, nrm, bid);
+}
+
+template <int V2, bool NRM>
+__global__ void __launch_bounds__(256) k_spmm_vel_v(const int32_t* __restrict__ rp, const int32_t* __restrict__ col,
+                                                    const double* __restrict__ A, int nnz,
+                                                    const int32_t* __restrict__ btp, const int32_t* __restrict__ btc,
+                                                    const double* __restrict__ btv, const uint8_t* __restrict__ cflag,
+                                                    const double* __restrict__ X, const double* __restrict__ Bv,
+                                                    double* __restrict__ Y, int ns, int64_t N, int J, int L, int mode,
+                                                    double* __restrict__ nrm) {
+    spmm_vel_body<V2, NRM>(rp, col, A, nnz, btp, btc, btv, cflag, X, Bv, Y, ns, N, J, L, mode, nrm, blockIdx.x);
 }
 
 // NRM: as k_spmm_vel_v; a lane holds member pairs 2*part + v (v = 0, 1)
 template <int V2, bool NRM>
-__global__ void __launch_bounds__(256) k_spmm_pres_v(const int32_t* __restrict__ bp, const int32_t* __restrict__ bc,
+__device__ __forceinline__ void spmm_pres_body(const int32_t* __restrict__ bp, const int32_t* __restrict__ bc,
                                                      const double* __restrict__ bv, const uint8_t* __restrict__ cflag,
                                                      const double* __restrict__ X, const double* __restrict__ Bv,
                                                      double* __restrict__ Y, int npres, int64_t nvel, int64_t N, int J,
-                                                     int L, int mode, double* __restrict__ nrm) {
+                                                     int L, int mode, double* __restrict__ nrm, int bid) {
     const int lane = threadIdx.x & 31;
     const int R = 32 / L;
     const int r = lane / L, part = lane - r * L;
-    const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t gw = ((int64_t)bid * blockDim.x + threadIdx.x) >> 5;
     const int64_t p = gw * R + r;
     double2 sq[2][2][2] = {};   // [v][mat][b, r]
     if (!NRM && (r >= R || p >= npres)) return;
@@ -399,11 +410,40 @@ __global__ void __launch_bounds__(256) k_spmm_pres_v(const int32_t* __restrict__
                 t.x += redp[w][v][m][br][pp].x;
                 t.y += redp[w][v][m][br][pp].y;
             }
-            double* o = nrm + (((int64_t)blockIdx.x * 2 + m) * 2 + br) * J + 2 * pr;
+            double* o = nrm + (((int64_t)bid * 2 + m) * 2 + br) * J + 2 * pr;
             o[0] = t.x;
             o[1] = t.y;
         }
     }
+}
+
+template <int V2, bool NRM>
+__global__ void __launch_bounds__(256) k_spmm_pres_v(const int32_t* __restrict__ bp, const int32_t* __restrict__ bc,
+                                                     const double* __restrict__ bv, const uint8_t* __restrict__ cflag,
+                                                     const double* __restrict__ X, const double* __restrict__ Bv,
+                                                     double* __restrict__ Y, int npres, int64_t nvel, int64_t N, int J,
+                                                     int L, int mode, double* __restrict__ nrm) {
+    spmm_pres_body<V2, NRM>(bp, bc, bv, cflag, X, Bv, Y, npres, nvel, N, J, L, mode, nrm, blockIdx.x);
+}
+
+// velocity and pressure rows in one launch: blocks [0, nbv) take velocity rows, the rest pressure
+// rows (the pressure blocks fill the velocity kernel's last wave; one launch instead of two)
+template <int V2>
+__global__ void __launch_bounds__(256) k_spmm_both_v(const int32_t* __restrict__ rp, const int32_t* __restrict__ col,
+                                                     const double* __restrict__ A, int nnz,
+                                                     const int32_t* __restrict__ btp, const int32_t* __restrict__ btc,
+                                                     const double* __restrict__ btv,
+                                                     const int32_t* __restrict__ bp, const int32_t* __restrict__ bc,
+                                                     const double* __restrict__ bv, const uint8_t* __restrict__ cflag,
+                                                     const double* __restrict__ X, const double* __restrict__ Bv,
+                                                     double* __restrict__ Y, int ns, int npres, int64_t N, int J,
+                                                     int Lv, int Lp, int nbv, int mode) {
+    if ((int)blockIdx.x < nbv)
+        spmm_vel_body<V2, false>(rp, col, A, nnz, btp, btc, btv, cflag, X, Bv, Y, ns, N, J, Lv, mode, nullptr,
+                                 blockIdx.x);
+    else
+        spmm_pres_body<V2, false>(bp, bc, bv, cflag, X, Bv, Y, npres, 2LL * ns, N, J, Lp, mode, nullptr,
+                                  blockIdx.x - nbv);
 }
 
 // ---------------------------------------------------------------------------
@@ -692,10 +732,32 @@ static bool launch_spmm_wide(ens_ctx* c, cudaStream_t s, const double* as_vals, 
     return true;
 }
 
+static bool spmm_merge() {
+    static int v = -1;
+    if (v < 0) {
+        const char* e = std::getenv("ENS_SPMM_MERGE");
+        v = e ? std::atoi(e) : 1;
+    }
+    return v != 0;
+}
+
 static int launch_spmm_vec(ens_ctx* c, cudaStream_t s, const double* as_vals, const double* x, const double* b,
                            double* y, int mode, double* nrm, int* nblk) {
     const int J = c->J;
     int blocks_total = 0;
+    if (!nrm && J <= 64 && J / 2 <= 64 && spmm_merge()) {
+        const int Lv = (J + 1) / 2, Rv = 32 / Lv;
+        const int H = J / 2, Lp = (H + 1) / 2, Rp = 32 / Lp;
+        const int nbv = (int)(((((int64_t)c->m.ns + Rv - 1) / Rv) * 32 + 255) / 256);
+        const int nbp = (int)(((((int64_t)c->m.n_pres + Rp - 1) / Rp) * 32 + 255) / 256);
+        k_spmm_both_v<2><<<nbv + nbp, 256, 0, s>>>(c->m.s_rowptr, c->m.s_col, as_vals, c->m.nnz_s, c->m.bt_rowptr,
+                                                   c->m.bt_col, c->m.bt_val, c->m.b_rowptr, c->m.b_col, c->m.b_val,
+                                                   c->m.cflag, x, b ? b : x, y, c->m.ns, c->m.n_pres, c->n_total, J,
+                                                   Lv, Lp, nbv, mode);
+        ENS_CKL();
+        if (nblk) *nblk = nbv + nbp;
+        return ENS_OK;
+    }
     {
         const int V2 = J <= 64 ? 2 : (J <= 128 ? 4 : 8);
         const int L = (J + V2 - 1) / V2, R = 32 / L;

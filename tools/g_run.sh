@@ -1,7 +1,6 @@
 for i in 1 2; do
-ENS_LIB=$PWD/paper_2108_05110_b200/libensmhd_b200_old.so python tools/precond_ab.py 2>&1 | tail -1
-ENS_PDL=0 python tools/precond_ab.py 2>&1 | tail -1
-python tools/precond_ab.py 2>&1 | tail -1
+ENS_SPMM_MERGE=0 python tools/spmm_bench.py 2>&1 | grep variant | sed 's/^/merge0 /'
+python tools/spmm_bench.py 2>&1 | grep variant | sed 's/^/merge1 /'
 done
+ENS_SPMM_MERGE=0 python tools/step_ab.py 2>&1 | tail -1
 python tools/step_ab.py 2>&1 | tail -1
-ENS_LIB=$PWD/paper_2108_05110_b200/libensmhd_b200_old.so python tools/step_ab.py 2>&1 | tail -1
