@@ -308,8 +308,11 @@ def main():
             marks.append(time.perf_counter())
         e2e_s = time.perf_counter() - t0
         step_ms = [round(1e3 * (b - a), 3) for a, b in zip([t0] + marks[:-1], marks)]
-        per = 8 * J_total * (2 * disc.n_vel + 2 * disc.n_pres)
-        e2e = {"value": J_total * args.e2e_steps / e2e_s, "unit": UNIT, "h2d_bytes_per_step": per + 8 * 2 * 2 * 3 * J_total,
+        per_v = 8 * J_total * 2 * disc.n_vel                   # v, w
+        per = per_v + 8 * J_total * 2 * disc.n_pres           # v, w, q, r
+        # H2D: v, w every step (q, r only when the velocities are not the resident level, never
+        # here) + the problem-data coefficients; D2H: the full new state + the residual
+        e2e = {"value": J_total * args.e2e_steps / e2e_s, "unit": UNIT, "h2d_bytes_per_step": per_v + 8 * 2 * 2 * 3 * J_total,
                "d2h_bytes_per_step": per + 16, "steps": args.e2e_steps, "step_ms": step_ms,
                "api": "paper_2108_05110_b200.advance(state, config, disc, forcing, boundary), numpy state in/out"}
 

@@ -513,10 +513,12 @@ class Engine:
         H2D copies of the (J, n) arrays -- straight from the caller's buffers
         when they are pinned (e.g. the arrays a previous step returned), else
         from pageable memory -- then the member-minor transpose and the internal
-        dof permutation on the device.  When the uploaded state equals the one
-        already resident in the current buffer set (a caller passing a step's
-        output straight back in), the resident trajectory is kept, so the
-        extrapolated initial iterate stays available.
+        dof permutation on the device.  When the uploaded velocities equal the
+        ones already resident in the current buffer set (a caller passing a
+        step's output straight back in), the resident trajectory is kept, so the
+        extrapolated initial iterate stays available, and q, r are not uploaded:
+        the reference's step reads only v and w (`stepper.py:360-394`); the
+        pressures enter here only as part of the initial iterate.
         """
         g = self._staging()
         s = self.stream
@@ -529,22 +531,26 @@ class Engine:
             Xs = g["x_in"]
             for m in range(2):
                 torch.index_select(g["d_vel"][m].t(), 0, g["ref_of_int_v"], out=Xs[m, :nv])
+            cur = self.cur
+            same = self.gen[cur] > 0 and torch.equal(Xs[:, :nv], self.X[cur][:, :nv])
+        keep = (hv, hw)
+        if same:
+            # the velocities are the resident level: the step needs nothing else from the host
+            # (pressures enter a step only through the initial iterate, stepper.py:223-252), so
+            # the resident trajectory -- pressures included -- is kept and q, r are not uploaded
+            s.synchronize()      # caller buffers may be reused once we return
+            del keep
+            return
+        with torch.cuda.stream(s):
             if has_p:
                 hq, hr = self._host_tensor(q), self._host_tensor(r)
+                keep = keep + (hq, hr)
                 g["d_pres"][0].copy_(hq, non_blocking=hq.is_pinned())
                 g["d_pres"][1].copy_(hr, non_blocking=hr.is_pinned())
                 for m in range(2):
                     torch.index_select(g["d_pres"][m].t(), 0, g["ref_of_int_p"], out=Xs[m, nv:])
             else:
                 Xs[:, nv:] = 0.0
-            cur = self.cur
-            same = (self.gen[cur] > 0 and torch.equal(Xs[:, :nv], self.X[cur][:, :nv])
-                    and torch.equal(Xs[:, nv:], self.Pq[cur]))
-        keep = (hv, hw) + ((hq, hr) if has_p else ())
-        if same:
-            s.synchronize()      # caller buffers may be reused once we return
-            del keep
-            return
         self._retire(cur)
         with torch.cuda.stream(s):
             self.X[cur].copy_(Xs)
