@@ -1,6 +1,5 @@
-for c in C2 C4 C3; do
-for r in 0 1; do
-  ENS_ROUND_FACTOR=$r timeout 900 python bench.py --case $c --steps 20 --warmup 3 --always-steps 0 --e2e-steps 0 --no-cpu-baseline > gpurun_out/b_$c.json 2> gpurun_out/b_$c.err
-  python -c "
-import json; d=json.load(open('gpurun_out/b_$c.json')); print('round $r $c', 'ms/step %.3f'%d['ms_per_step'], 'iters', d['krylov_iters_per_step'], 'nfact', d['preconditioner']['factorizations_in_timed_steps'])"
-done; done
+for c in C4 C3; do
+  timeout 900 python bench.py --case $c --steps 20 --warmup 3 --always-steps 2 --e2e-steps 0 > gpurun_out/bench_$c.json 2> gpurun_out/bench_$c.err; echo $c=$?
+done
+timeout 1500 python bench.py --case C5 --steps 5 --warmup 3 --always-steps 0 --e2e-steps 0 > gpurun_out/bench_C5.json 2> gpurun_out/bench_C5.err; echo C5=$?
+python bench.py > gpurun_out/bench_c2.json 2> gpurun_out/bench_c2.err; echo c2=$?
