@@ -1,5 +1,7 @@
-for c in C4 C3; do
-  timeout 900 python bench.py --case $c --steps 20 --warmup 3 --always-steps 2 --e2e-steps 0 > gpurun_out/bench_$c.json 2> gpurun_out/bench_$c.err; echo $c=$?
+for i in 1 2; do
+ENS_LIB=$PWD/paper_2108_05110_b200/libensmhd_b200_old.so python tools/precond_ab.py 2>&1 | tail -1
+python tools/precond_ab.py 2>&1 | tail -1
 done
-timeout 1500 python bench.py --case C5 --steps 5 --warmup 3 --always-steps 0 --e2e-steps 0 > gpurun_out/bench_C5.json 2> gpurun_out/bench_C5.err; echo C5=$?
-python bench.py > gpurun_out/bench_c2.json 2> gpurun_out/bench_c2.err; echo c2=$?
+CASE=C4 ENS_LIB=$PWD/paper_2108_05110_b200/libensmhd_b200_old.so python tools/precond_ab.py 2>&1 | tail -1
+CASE=C4 python tools/precond_ab.py 2>&1 | tail -1
+python -m pytest tests -m gpu -x -q 2>&1 | tail -2
