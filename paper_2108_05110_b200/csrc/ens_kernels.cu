@@ -396,10 +396,20 @@ __global__ void k_member_pass(const int32_t* __restrict__ enodes, const double* 
     // the ensemble means at the element's nodes are member-independent: staged once per
     // element in shared memory instead of 24 per-thread registers (occupancy)
     double* smn = sh_sq + (size_t)EPB * 2 * ENS_NQ * JB + (size_t)el * 24;
+    // physical shape-function gradients at the quadrature points, member-independent too:
+    // computed once per element into shared memory ([EPB][7][6][2]) instead of per thread
+    double* sgr = sh_sq + (size_t)EPB * 2 * ENS_NQ * JB + (size_t)EPB * 24 + (size_t)el * ENS_NQ * 12;
     if (el < EPB && e < e0 + ne) {
         for (int t = jj; t < 24; t += JB) {
             const int fam = t / 12, a = (t % 12) >> 1, cc = t & 1;
             smn[t] = means[(int64_t)fam * nvel + 2LL * enodes[(int64_t)e * 6 + a] + cc];
+        }
+        double gle[6];
+#pragma unroll
+        for (int i = 0; i < 6; ++i) gle[i] = egeo[(int64_t)e * 8 + 1 + i];
+        for (int t = jj; t < ENS_NQ * 6; t += JB) {
+            const int q = t / 6, a = t % 6;
+            grad_phi(gle, q, a, sgr[2 * t], sgr[2 * t + 1]);
         }
     }
     __syncthreads();
@@ -409,10 +419,7 @@ __global__ void k_member_pass(const int32_t* __restrict__ enodes, const double* 
         int nd[6];
 #pragma unroll
         for (int a = 0; a < 6; ++a) nd[a] = enodes[(int64_t)e * 6 + a];
-        double gl[6];
         const double area = egeo[(int64_t)e * 8];
-#pragma unroll
-        for (int i = 0; i < 6; ++i) gl[i] = egeo[(int64_t)e * 8 + 1 + i];
         double v[6][2], w[6][2];
 #pragma unroll
         for (int a = 0; a < 6; ++a) {
@@ -435,8 +442,7 @@ __global__ void k_member_pass(const int32_t* __restrict__ enodes, const double* 
 #pragma unroll
             for (int a = 0; a < 6; ++a) {
                 const double ph = c_phi[q][a];
-                double gx, gy;
-                grad_phi(gl, q, a, gx, gy);
+                const double gx = sgr[(q * 6 + a) * 2], gy = sgr[(q * 6 + a) * 2 + 1];
                 fvq0 += (v[a][0] - smn[2 * a]) * ph;
                 fvq1 += (v[a][1] - smn[2 * a + 1]) * ph;
                 fwq0 += (w[a][0] - smn[12 + 2 * a]) * ph;
@@ -476,8 +482,7 @@ __global__ void k_member_pass(const int32_t* __restrict__ enodes, const double* 
 #pragma unroll
                 for (int a = 0; a < 6; ++a) {
                     const double ph = c_phi[q][a];
-                    double gx, gy;
-                    grad_phi(gl, q, a, gx, gy);
+                    const double gx = sgr[(q * 6 + a) * 2], gy = sgr[(q * 6 + a) * 2 + 1];
                     rv[a][0] += ph * tv0 - (gx * hv0x + gy * hv0y);
                     rv[a][1] += ph * tv1 - (gx * hv1x + gy * hv1y);
                     rw[a][0] += ph * tw0 - (gx * hw0x + gy * hw0y);
@@ -583,15 +588,31 @@ __global__ void __launch_bounds__(256) k_member_gather(const int32_t* __restrict
     r2[row * H + jp] = r;
 }
 
+// the member pass stages per-element tables in dynamic shared memory (small J => many elements
+// per block => more than the default 48 KB)
+static int member_pass_smem_setup() {
+    static bool done = false;
+    if (!done) {
+        ENS_CK(cudaFuncSetAttribute(k_member_pass<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024));
+        ENS_CK(cudaFuncSetAttribute(k_member_pass<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024));
+        done = true;
+    }
+    return ENS_OK;
+}
+
 int launch_member_pass(ens_ctx* c, cudaStream_t s, const double* x, const double* means, double* rhs,
                        double* maxsq) {
+    {
+        const int rc = member_pass_smem_setup();
+        if (rc != ENS_OK) return rc;
+    }
     if (c->m.n2e && (c->J & 1) == 0) {
         // all elements in one launch into an element buffer, then one ordered gather per row
         const int J = c->J;
         const int JB = J < 128 ? J : 128;
         const int EPB = 128 / JB > 0 ? 128 / JB : 1;
         const int threads = EPB * JB;
-        const size_t shm = sizeof(double) * ((size_t)EPB * 2 * ENS_NQ * JB + (size_t)EPB * 24);
+        const size_t shm = sizeof(double) * ((size_t)EPB * 2 * ENS_NQ * JB + (size_t)EPB * 24 + (size_t)EPB * ENS_NQ * 12);
         const size_t ecb = sizeof(double) * 2 * (size_t)c->m.nt * 12 * J;
         if (!c->ec) {
             ENS_CK(cudaMalloc(&c->ec, ecb));
@@ -613,7 +634,7 @@ int launch_member_pass(ens_ctx* c, cudaStream_t s, const double* x, const double
     const int JB = J < 128 ? J : 128;
     const int EPB = 128 / JB > 0 ? 128 / JB : 1;
     const int threads = EPB * JB;
-    const size_t shm = sizeof(double) * ((size_t)EPB * 2 * ENS_NQ * JB + (size_t)EPB * 24);
+    const size_t shm = sizeof(double) * ((size_t)EPB * 2 * ENS_NQ * JB + (size_t)EPB * 24 + (size_t)EPB * ENS_NQ * 12);
     ENS_CK(cudaMemsetAsync(maxsq, 0, sizeof(double) * 2 * (size_t)c->m.nt * ENS_NQ, s));
     for (int col = 0; col < c->m.ncolor; ++col) {
         const int e0 = c->color_off[col], ne = c->color_off[col + 1] - e0;
@@ -640,13 +661,17 @@ int launch_rhs_fused(ens_ctx* c, cudaStream_t s, const double* x, const double* 
         return launch_member_pass(c, s, x, means, rhs, maxsq);
     }
     const int64_t N = c->n_total;
+    {
+        const int rc = member_pass_smem_setup();
+        if (rc != ENS_OK) return rc;
+    }
     for (int mat = 0; mat < 2; ++mat)   // pressure rows of the right-hand side are zero (stepper.py:245-246)
         ENS_CK(cudaMemsetAsync(rhs + mat * N * J + (int64_t)c->n_vel * J, 0,
                                sizeof(double) * (size_t)c->m.n_pres * J, s));
     const int JB = J < 128 ? J : 128;
     const int EPB = 128 / JB > 0 ? 128 / JB : 1;
     const int threads = EPB * JB;
-    const size_t shm = sizeof(double) * ((size_t)EPB * 2 * ENS_NQ * JB + (size_t)EPB * 24);
+    const size_t shm = sizeof(double) * ((size_t)EPB * 2 * ENS_NQ * JB + (size_t)EPB * 24 + (size_t)EPB * ENS_NQ * 12);
     const size_t ecb = sizeof(double) * 2 * (size_t)c->m.nt * 12 * J;
     if (!c->ec) {
         ENS_CK(cudaMalloc(&c->ec, ecb));
