@@ -211,8 +211,10 @@ __device__ __forceinline__ void cp_async_wait_n(int n) {
 #ifndef SG_MINB
 #define SG_MINB 3
 #endif
-template <int NCT>
-__global__ void __launch_bounds__(SG_T, SG_MINB) k_sgemm(MfDev d, const int4* __restrict__ sitem, int item0,
+// CW: member columns per CTA (32, or 64 for wide ensembles: each staged factor chunk then
+// feeds twice the tensor-core work); NCT <= CW / 8 column tiles are computed.
+template <int NCT, int CW = 32>
+__global__ void __launch_bounds__(SG_T, CW == 64 ? 2 : SG_MINB) k_sgemm(MfDev d, const int4* __restrict__ sitem, int item0,
                                                 const double* __restrict__ F, double* __restrict__ FR,
                                                 const SolveIO* __restrict__ io, int64_t N, int J, int64_t nidx,
                                                 int bwd, int split_k, int nstage, double* __restrict__ partial,
@@ -230,8 +232,11 @@ __global__ void __launch_bounds__(SG_T, SG_MINB) k_sgemm(MfDev d, const int4* __
     const int64_t fo = (int64_t)(unsigned)w2.z | ((int64_t)w2.w << 32);
     const int mat = blockIdx.y;
     const int zb = zbase + blockIdx.z;
-    const int j0 = zb * SG_C;
-    const int jn = min(SG_C, J - j0);
+    constexpr int LDB = CW + 4;                        // = 4 (mod 16): conflict-free fragment reads
+    constexpr int STAGE = SG_R * SG_LDA + SG_KC * LDB;  // doubles per pipeline stage
+    constexpr int NB = CW / 8;                         // column tiles a CTA can hold
+    const int j0 = zb * CW;
+    const int jn = min(CW, J - j0);
     const double* base = F + (int64_t)mat * d.storage + off;
     double* FRm = FR + (int64_t)mat * nidx * J;
     double* fr = FRm + fo * J;
@@ -247,14 +252,14 @@ __global__ void __launch_bounds__(SG_T, SG_MINB) k_sgemm(MfDev d, const int4* __
     const int row = 8 * warp + g;
     const bool row_ok = row < nr;
     // Load issue with per-thread invariants hoisted (thread = row warp + 8 i, column lane;
-    // SG_KC = SG_C = 32, SG_T = 256) and the stage passed in (no runtime modulo): the leaf
+    // SG_KC = 32, SG_T = 256) and the stage passed in (no runtime modulo): the leaf
     // levels were issue-bound on this address arithmetic (ncu: ~50 % of the instructions).
-    static_assert(SG_KC == 32 && SG_C == 32 && SG_T == 256, "k_sgemm load mapping");
+    static_assert(SG_KC == 32 && SG_T == 256 && (CW == 32 || CW == 64) && NCT <= CW / 8, "k_sgemm load mapping");
     const uint32_t sm_u32 = (uint32_t)__cvta_generic_to_shared(sm);
     const double* a_src = base + (int64_t)(rbase + warp) * m + kbeg + lane;
     const int64_t a_rstep = 8LL * m;
     const uint32_t a_dst = sm_u32 + 8u * (uint32_t)(warp * SG_LDA + lane);
-    const uint32_t b_dst = sm_u32 + 8u * (uint32_t)(SG_R * SG_LDA + warp * SG_LDB + lane);
+    const uint32_t b_dst = sm_u32 + 8u * (uint32_t)(SG_R * SG_LDA + warp * LDB + lane);
     const bool jok = lane < jn;
     const double* b_fr = fr + j0 + lane;
     const double* b_x = x + j0 + lane;
@@ -265,7 +270,7 @@ __global__ void __launch_bounds__(SG_T, SG_MINB) k_sgemm(MfDev d, const int4* __
 #ifdef SG_NOA
         return;
 #endif
-        const uint32_t dst = a_dst + 8u * (uint32_t)(st * SG_STAGE);
+        const uint32_t dst = a_dst + 8u * (uint32_t)(st * STAGE);
         const bool kok = c * SG_KC + lane < kc;
         const double* src = a_src + c * SG_KC;
 #pragma unroll
@@ -278,15 +283,21 @@ __global__ void __launch_bounds__(SG_T, SG_MINB) k_sgemm(MfDev d, const int4* __
 #ifdef SG_NOB
         return;
 #endif
-        if (lane >= 8 * NCT) return;   // member columns no column tile of this launch reads
-        const uint32_t dst = b_dst + 8u * (uint32_t)(st * SG_STAGE);
+        const uint32_t dst = b_dst + 8u * (uint32_t)(st * STAGE);
 #pragma unroll
-        for (int i = 0; i < SG_KC / 8; ++i) {
-            const int kg = c * SG_KC + warp + 8 * i;
-            const bool ok = jok && kg < kc;
-            const int kq = min(kg, kc - 1), t = kbeg + kq;
-            const double* src = (!bwd || t < k) ? b_fr + (int64_t)t * J : b_x + (int64_t)s_idx[kq] * J;
-            cpa8(dst + 8u * (uint32_t)(8 * i * SG_LDB), ok ? src : base, ok);
+        for (int h = 0; h < CW / 32; ++h) {
+            const int col = lane + 32 * h;
+            if (col >= 8 * NCT) break;   // member columns no column tile of this launch reads
+            const bool cok = col < jn;
+#pragma unroll
+            for (int i = 0; i < SG_KC / 8; ++i) {
+                const int kg = c * SG_KC + warp + 8 * i;
+                const bool ok = cok && kg < kc;
+                const int kq = min(kg, kc - 1), t = kbeg + kq;
+                const double* src = (!bwd || t < k) ? b_fr + 32 * h + (int64_t)t * J
+                                                    : b_x + 32 * h + (int64_t)s_idx[kq] * J;
+                cpa8(dst + 8u * (uint32_t)(8 * i * LDB + 32 * h), ok ? src : base, ok);
+            }
         }
     };
     // (1) first A chunk (factor entries: safe before the dependency wait), epilogue operands,
@@ -294,11 +305,13 @@ __global__ void __launch_bounds__(SG_T, SG_MINB) k_sgemm(MfDev d, const int4* __
     issue_a(0, 0);
     const int xrow = (bwd && row_ok) ? d.idx[fo + rbase + row] : 0;
     pdl_wait();   // front rows / the iterate come from the previous launch
-    double init[4][2] = {{0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}};
+    double init[NB][2];
+#pragma unroll
+    for (int ct = 0; ct < NB; ++ct) init[ct][0] = init[ct][1] = 0.0;
     if (!bwd && hasch && row_ok) {
         const double* pr = FRm + (fo + rbase + row) * J + j0;
 #pragma unroll
-        for (int ct = 0; ct < 4; ++ct)
+        for (int ct = 0; ct < NB; ++ct)
 #pragma unroll
             for (int e = 0; e < 2; ++e) {
                 const int col = min(8 * ct + 2 * q + e, jn - 1);
@@ -321,7 +334,9 @@ __global__ void __launch_bounds__(SG_T, SG_MINB) k_sgemm(MfDev d, const int4* __
     }
     SG_T_(2);
     // (3) mainloop
-    double dacc[4][2] = {{0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}};
+    double dacc[NB][2];
+#pragma unroll
+    for (int ct = 0; ct < NB; ++ct) dacc[ct][0] = dacc[ct][1] = 0.0;
     int ust = 0;   // stage of chunk c (= c mod nstage); chunk c + nstage - 1 goes to the stage before it
     for (int c = 0; c < nch; ++c) {
         cp_async_wait_n(nstage - 2);
@@ -333,10 +348,10 @@ __global__ void __launch_bounds__(SG_T, SG_MINB) k_sgemm(MfDev d, const int4* __
             issue_b(cn, ist);
         }
         cp_async_commit();
-        const double* As = sm + ust * SG_STAGE;
+        const double* As = sm + ust * STAGE;
         ust = ust + 1 == nstage ? 0 : ust + 1;
         const double* ap = As + row * SG_LDA + q;
-        const double* bp = As + SG_R * SG_LDA + q * SG_LDB + g;
+        const double* bp = As + SG_R * SG_LDA + q * LDB + g;
         const int ksteps = (min(SG_KC, kc - c * SG_KC) + 3) >> 2;
         if (8 * warp >= nr) {
             // no valid row in this warp: skip the tensor-core work (barriers above/below still hit)
@@ -345,14 +360,14 @@ __global__ void __launch_bounds__(SG_T, SG_MINB) k_sgemm(MfDev d, const int4* __
             for (int u = 0; u < SG_KC / 4; ++u) {
                 const double av = ap[4 * u];
 #pragma unroll
-                for (int ct = 0; ct < NCT; ++ct) dmma8(dacc[ct][0], dacc[ct][1], av, bp[4 * u * SG_LDB + 8 * ct]);
+                for (int ct = 0; ct < NCT; ++ct) dmma8(dacc[ct][0], dacc[ct][1], av, bp[4 * u * LDB + 8 * ct]);
             }
         } else {
 #pragma unroll 2
             for (int u = 0; u < ksteps; ++u) {
                 const double av = ap[4 * u];
 #pragma unroll
-                for (int ct = 0; ct < NCT; ++ct) dmma8(dacc[ct][0], dacc[ct][1], av, bp[4 * u * SG_LDB + 8 * ct]);
+                for (int ct = 0; ct < NCT; ++ct) dmma8(dacc[ct][0], dacc[ct][1], av, bp[4 * u * LDB + 8 * ct]);
             }
         }
     }
@@ -379,7 +394,7 @@ __global__ void __launch_bounds__(SG_T, SG_MINB) k_sgemm(MfDev d, const int4* __
         double* pw = partial + (((int64_t)mat * nslot + slot) * SG_R + row) * J + j0;
         if (row_ok) {
 #pragma unroll
-            for (int ct = 0; ct < 4; ++ct)
+            for (int ct = 0; ct < NB; ++ct)
 #pragma unroll
                 for (int e = 0; e < 2; ++e)
                     if (8 * ct + 2 * q + e < jn) pw[8 * ct + 2 * q + e] = dacc[ct][e];
@@ -401,11 +416,11 @@ __global__ void __launch_bounds__(SG_T, SG_MINB) k_sgemm(MfDev d, const int4* __
         const double* pr = partial + (((int64_t)mat * nslot + s0) * SG_R + row) * J + j0;
         const int64_t pst = (int64_t)SG_R * J;
 #pragma unroll
-        for (int ct = 0; ct < 4; ++ct) dacc[ct][0] = dacc[ct][1] = 0.0;
+        for (int ct = 0; ct < NB; ++ct) dacc[ct][0] = dacc[ct][1] = 0.0;
 #pragma unroll 4
         for (int qq = 0; qq < ns; ++qq) {
 #pragma unroll
-            for (int ct = 0; ct < 4; ++ct)
+            for (int ct = 0; ct < NB; ++ct)
 #pragma unroll
                 for (int e = 0; e < 2; ++e)
                     if (8 * ct + 2 * q + e < jn) dacc[ct][e] += __ldcg(pr + qq * pst + 8 * ct + 2 * q + e);
@@ -413,7 +428,7 @@ __global__ void __launch_bounds__(SG_T, SG_MINB) k_sgemm(MfDev d, const int4* __
     }
     if (!row_ok) return;
 #pragma unroll
-    for (int ct = 0; ct < 4; ++ct)
+    for (int ct = 0; ct < NB; ++ct)
 #pragma unroll
         for (int e = 0; e < 2; ++e) {
             const int col = 8 * ct + 2 * q + e;
@@ -556,7 +571,19 @@ __global__ void __launch_bounds__(SG_T, SG_MINB) k_sgemm_fwd_multi(const int4* _
 }
 
 #define SG_MAXST 5
-static size_t sg_smem(int nstage) { return sizeof(double) * (size_t)nstage * SG_STAGE; }
+static size_t sg_smem(int nstage, int cw = 32) {
+    return sizeof(double) * (size_t)nstage * (SG_R * SG_LDA + SG_KC * (cw + 4));
+}
+
+// 64-member column blocks for J >= 64 (ENS_SOLVE_CW64=0 keeps 32)
+static bool sg_wide(int J) {
+    static int v = -1;
+    if (v < 0) {
+        const char* e = std::getenv("ENS_SOLVE_CW64");
+        v = e ? std::atoi(e) : 1;
+    }
+    return v != 0 && J >= 64;
+}
 
 static int sg_stages(int kmax) {
     static int env = -1;
@@ -694,24 +721,32 @@ static int mf_solve_launches(ens_ctx* c, cudaStream_t s, SolveIO* io, int64_t* n
                 continue;
             }
             const int nst = sg_stages(kmax);
+            const bool wide = sg_wide(J);
             for (int rep = 0; rep < (timing ? trep : 1); ++rep) {   // launches are idempotent
-                // member column blocks: full 32-wide blocks use 4 column tiles, the remainder fewer
-                const int zfull = J / SG_C, rem = J - zfull * SG_C;
-#define SGL(NC, ZN, Z0)                                                                                       \
-    ENS_CK(launch_pdl(k_sgemm<NC>, dim3(n, 2, ZN), dim3(SG_T), sg_smem(nst), s, d, c->sitem, off, c->fronts,    \
-                      c->frvec, io, N, J, nidx, (int)(op == SOP_BGEMM), kmax, nst, c->partial, c->ticket, nslot, \
-                      (int)(Z0)))
+                // member column blocks of CW = 32 (or 64 for wide ensembles): full blocks use all their
+                // column tiles, the remainder fewer
+                const int CWd = wide ? 64 : 32;
+                const int zfull = J / CWd, rem = J - zfull * CWd;
+#define SGL(NC, CWT, ZN, Z0)                                                                                      \
+    ENS_CK(launch_pdl(k_sgemm<NC, CWT>, dim3(n, 2, ZN), dim3(SG_T), sg_smem(nst, CWT), s, d, c->sitem, off,       \
+                      c->fronts, c->frvec, io, N, J, nidx, (int)(op == SOP_BGEMM), kmax, nst, c->partial,         \
+                      c->ticket, nslot, (int)(Z0)))
                 if (zfull > 0) {
-                    SGL(4, (unsigned)zfull, 0);
+                    if (wide) SGL(8, 64, (unsigned)zfull, 0);
+                    else SGL(4, 32, (unsigned)zfull, 0);
                     ENS_CKL();
                     if (rep == 0) ++cnt;
                 }
                 if (rem > 0) {
                     const int nct = (rem + 7) / 8;
-                    if (nct == 1) SGL(1, 1, zfull);
-                    else if (nct == 2) SGL(2, 1, zfull);
-                    else if (nct == 3) SGL(3, 1, zfull);
-                    else SGL(4, 1, zfull);
+                    if (wide) {
+                        if (nct <= 4) SGL(4, 64, 1, zfull);
+                        else if (nct <= 6) SGL(6, 64, 1, zfull);
+                        else SGL(8, 64, 1, zfull);
+                    } else if (nct == 1) SGL(1, 32, 1, zfull);
+                    else if (nct == 2) SGL(2, 32, 1, zfull);
+                    else if (nct == 3) SGL(3, 32, 1, zfull);
+                    else SGL(4, 32, 1, zfull);
                     ENS_CKL();
                     if (rep == 0) ++cnt;
                 }
@@ -752,6 +787,12 @@ int mf_solve(ens_ctx* c, cudaStream_t s, const double* r, double* z) {
         ENS_CK(cudaFuncSetAttribute(k_sgemm<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sg_smem(SG_MAXST)));
         ENS_CK(cudaFuncSetAttribute(k_sgemm<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sg_smem(SG_MAXST)));
         ENS_CK(cudaFuncSetAttribute(k_sgemm<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sg_smem(SG_MAXST)));
+        ENS_CK(cudaFuncSetAttribute(k_sgemm<4, 64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)sg_smem(SG_MAXST, 64)));
+        ENS_CK(cudaFuncSetAttribute(k_sgemm<6, 64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)sg_smem(SG_MAXST, 64)));
+        ENS_CK(cudaFuncSetAttribute(k_sgemm<8, 64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)sg_smem(SG_MAXST, 64)));
         const int64_t ns = c->p.n_slot > 0 ? c->p.n_slot : 1;
         const size_t pbytes = sizeof(double) * 2 * (size_t)ns * SG_R * c->J;
         const size_t tbytes = sizeof(int) * 2 * (size_t)ns * ((c->J + SG_C - 1) / SG_C);
