@@ -163,6 +163,19 @@ typedef struct {
     int32_t pad;
 } ens_spmm_tiles;
 
+/* Row-pair SpMM (optional, built once per mesh by spmm_tiles.row_pairs): velocity rows
+ * 2p, 2p+1 processed together over the sorted union of their column lists; per union
+ * entry the CSR slot of each row or -1 (int32 pairs).  Device pointers owned by the caller. */
+typedef struct {
+    const int32_t* a_ptr;       /* npairs+1: union ranges over the A_s pattern */
+    const int32_t* a_col;       /* union column (node) */
+    const int32_t* a_slot;      /* 2 per entry: CSR slot of row 2p / 2p+1, or -1 */
+    const int32_t* t_ptr;       /* npairs+1: union ranges over the B^T pairs */
+    const int32_t* t_col;       /* union pressure row */
+    const int32_t* t_slot;      /* 2 per entry: B^T pair index of row 2p / 2p+1, or -1 */
+    int64_t npairs;
+} ens_spmm_pairs;
+
 /* Problem data: value_j = sum_k coef[k*J + j] * basis[k*rows + row] (+ dense). */
 typedef struct {
     int32_t K;                  /* number of basis vectors (0 allowed)   */
@@ -186,6 +199,8 @@ int  ens_workspace_bytes(const ens_ctx* ctx, int64_t* bytes);
 int  ens_set_pivoting(ens_ctx* ctx, int on);
 /* Install the SpMM row blocking (arrays are device pointers owned by the caller). */
 int  ens_set_spmm_blocks(ens_ctx* ctx, const ens_spmm_blocks* blocks);
+/* Install (or, with NULL, remove) the row-pair SpMM (even J <= 64; used when no tile staging is set). */
+int  ens_set_spmm_pairs(ens_ctx* ctx, const ens_spmm_pairs* pairs);
 /* Install (or, with NULL, remove) the tile-staged SpMM; takes precedence over the row blocking. */
 int  ens_set_spmm_tiles(ens_ctx* ctx, const ens_spmm_tiles* tiles);
 

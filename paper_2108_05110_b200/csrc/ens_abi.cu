@@ -146,6 +146,21 @@ int ens_set_spmm_blocks(ens_ctx* c, const ens_spmm_blocks* b) {
     return ENS_OK;
 }
 
+int ens_set_spmm_pairs(ens_ctx* c, const ens_spmm_pairs* p) {
+    if (!c) return ENS_EINVAL;
+    if (!p) {
+        c->use_pairs = 0;
+        return ENS_OK;
+    }
+    if ((c->J & 1) || c->J > 64 || p->npairs != ((int64_t)c->m.ns + 1) / 2) {
+        ens_set_error("SpMM row pairs: need even J <= 64 and (ns + 1) / 2 pairs", __FILE__, __LINE__);
+        return ENS_EINVAL;
+    }
+    c->pairs = *p;
+    c->use_pairs = 1;
+    return ENS_OK;
+}
+
 int ens_set_spmm_tiles(ens_ctx* c, const ens_spmm_tiles* t) {
     if (!c) return ENS_EINVAL;
     if (!t) {

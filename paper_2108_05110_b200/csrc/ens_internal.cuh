@@ -86,6 +86,8 @@ struct ens_ctx {
     int use_blocked = 0;
     ens_spmm_tiles tiles{};        // tile-staged SpMM (bulk-copied stages, ens_spmm_tiles.cu)
     int use_tiles = 0;
+    ens_spmm_pairs pairs{};        // row-pair SpMM (ens_spmm.cu)
+    int use_pairs = 0;
     int spmm_wide = -1;            // wide-member SpMM variant (ENS_SPMM_WIDE, read on first use)
     int g_factor_pivot = 0;
     int64_t g_factor_kernels = 0;

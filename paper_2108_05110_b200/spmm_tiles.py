@@ -272,3 +272,27 @@ def emulate(hm, J, desc, recs, lcol_a, lcol_bt, lcol_b, as_vals, X, B=None, mode
     if mode == 1:
         Y = B.reshape(2, N, J) - Y
     return Y
+
+
+def _pair_union(row_ptr, cols, ncol, nrows):
+    """Union of the column lists of rows 2p, 2p+1 (sorted), with each row's entry index or -1."""
+    npair = (nrows + 1) // 2
+    row_of = np.repeat(np.arange(nrows, dtype=np.int64), np.diff(row_ptr))
+    k = np.arange(len(cols), dtype=np.int64)
+    pair, h = row_of >> 1, row_of & 1
+    key = pair * ncol + cols.astype(np.int64)
+    o = np.lexsort((h, key))
+    ukey, inv = np.unique(key[o], return_inverse=True)
+    slots = np.full((len(ukey), 2), -1, dtype=np.int32)
+    slots[inv, h[o]] = k[o]
+    ptr = np.searchsorted(ukey // ncol, np.arange(npair + 1)).astype(np.int32)
+    return ptr, (ukey % ncol).astype(np.int32), slots
+
+
+def row_pairs(hm):
+    """Row-pair structure of the velocity rows for the paired SpMM kernel (csrc/ens_spmm.cu)."""
+    a = _pair_union(hm.s_rowptr, hm.s_col, hm.ns, hm.ns)
+    t = _pair_union(hm.bt_rowptr, hm.bt_col, hm.npres, hm.ns)
+    info = dict(npairs=(hm.ns + 1) // 2, a_union=len(a[1]), a_nnz=int(hm.nnz_s), t_union=len(t[1]),
+                t_nnz=len(hm.bt_col))
+    return a, t, info

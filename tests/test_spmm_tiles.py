@@ -56,3 +56,22 @@ def test_tile_records_obey_bulk_copy_rules():
         assert cover.max() == 1 and nb[d[3]:d[3] + d[4]].sum() == d[5]
     with pytest.raises(ValueError):
         T.build_tiles(hm, 7)
+
+
+@pytest.mark.parametrize("case,over", [("C1", dict(n=6, J=4)), ("C4", dict(k=1, J=6, length=6.0))])
+def test_row_pairs_keep_each_rows_csr_order(case, over):
+    """The paired SpMM's union lists hold, for each row of a pair, exactly its CSR entries in CSR order."""
+    disc, cfg, _ = P.build_case(case, **over)
+    hm = host_mesh(disc)
+    (ap, ac, asl), (tp, tc, tsl), info = T.row_pairs(hm)
+    assert info["a_union"] < info["a_nnz"] and info["t_union"] <= info["t_nnz"]
+    for r in range(hm.ns):
+        p, h = r >> 1, r & 1
+        e = np.arange(ap[p], ap[p + 1])
+        e = e[asl[e, h] >= 0]
+        assert np.array_equal(asl[e, h], np.arange(hm.s_rowptr[r], hm.s_rowptr[r + 1]))
+        assert np.array_equal(ac[e], hm.s_col[hm.s_rowptr[r]:hm.s_rowptr[r + 1]])
+        e = np.arange(tp[p], tp[p + 1])
+        e = e[tsl[e, h] >= 0]
+        assert np.array_equal(tsl[e, h], np.arange(hm.bt_rowptr[r], hm.bt_rowptr[r + 1]))
+        assert np.array_equal(tc[e], hm.bt_col[hm.bt_rowptr[r]:hm.bt_rowptr[r + 1]])
