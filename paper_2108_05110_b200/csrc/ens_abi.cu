@@ -124,6 +124,7 @@ void ens_destroy(ens_ctx* c) {
     cudaFree(c->finit_rows);
     cudaFree(c->ec);
     cudaFree(c->nrm_part);
+    cudaFree(c->diag_part);
     df_free(c);
     cudaFree(c->el);
     delete c;

@@ -71,6 +71,8 @@ struct ens_ctx {
     std::vector<uint8_t> fwd_multi;   // per level: forward GEMM runs the multi-unit kernel
     int sg_slots = 0;              // resident CTAs of the multi-unit kernel (all SMs)
     double* nrm_part = nullptr;    // fused residual-norm partials of the SpMM
+    double* diag_part = nullptr;   // per-block partials of the diagnostics (launch_diagnostics)
+    size_t diag_part_n = 0;
     double* ec = nullptr;          // member-pass element buffer [2][nt][6][2][J]
     double* el = nullptr;          // assembly element buffer [2][36][nt]
     int32_t* finit_rows = nullptr; // per level: front rows k_finit assembles (bit 31: pivot row)

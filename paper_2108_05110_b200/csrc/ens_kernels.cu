@@ -1199,14 +1199,18 @@ __global__ void k_quadforms(const int32_t* __restrict__ rp, const int32_t* __res
 }
 
 // energy of the means: mean^T M mean for v and w (single block per family, ordered)
+// grid (RBm, 2): block b of family fam sums a fixed node range -> part[fam][b]; k_diag_fin adds the
+// partials in order
 __global__ void k_mean_energy(const int32_t* __restrict__ rp, const int32_t* __restrict__ col,
                               const double* __restrict__ mass, const double* __restrict__ means, int ns,
-                              double* __restrict__ out) {
+                              double* __restrict__ part) {
     __shared__ double red[256];
-    const int fam = blockIdx.x;
+    const int fam = blockIdx.y;
     const double* m = means + (int64_t)fam * 2 * ns;
+    const int64_t per = ((int64_t)ns + gridDim.x - 1) / gridDim.x;
+    const int64_t n0 = (int64_t)blockIdx.x * per, n1 = min((int64_t)ns, n0 + per);
     double acc = 0.0;
-    for (int64_t i = threadIdx.x; i < ns; i += blockDim.x) {
+    for (int64_t i = n0 + threadIdx.x; i < n1; i += blockDim.x) {
         for (int cc = 0; cc < 2; ++cc) {
             double s = 0.0;
             for (int k = rp[i]; k < rp[i + 1]; ++k) s += mass[k] * m[2LL * col[k] + cc];
@@ -1218,7 +1222,7 @@ __global__ void k_mean_energy(const int32_t* __restrict__ rp, const int32_t* __r
     if (threadIdx.x == 0) {
         double s = 0.0;
         for (int k = 0; k < (int)blockDim.x; ++k) s += red[k];
-        out[fam] = s;
+        part[(int64_t)fam * gridDim.x + blockIdx.x] = s;
     }
 }
 
@@ -1234,8 +1238,10 @@ __global__ void k_divergence(const int32_t* __restrict__ enodes, const double* _
         for (int e = blockIdx.x * EPB + el; e < nt; e += gridDim.x * EPB) {
             double gl[6];
             const double area = egeo[(int64_t)e * 8];
+#pragma unroll
             for (int i = 0; i < 6; ++i) gl[i] = egeo[(int64_t)e * 8 + 1 + i];
             double vx[6], vy[6], wx[6], wy[6];
+#pragma unroll
             for (int a = 0; a < 6; ++a) {
                 const int64_t nd = enodes[(int64_t)e * 6 + a];
                 vx[a] = X[(2 * nd) * J + j];
@@ -1245,6 +1251,7 @@ __global__ void k_divergence(const int32_t* __restrict__ enodes, const double* _
             }
             for (int q = 0; q < ENS_NQ; ++q) {
                 double dv = 0.0, dw = 0.0;
+#pragma unroll
                 for (int a = 0; a < 6; ++a) {
                     double gx, gy;
                     grad_phi(gl, q, a, gx, gy);
@@ -1272,9 +1279,16 @@ __global__ void k_divergence(const int32_t* __restrict__ enodes, const double* _
 }
 
 __global__ void k_diag_fin(const double* __restrict__ pq, int RBq, const double* __restrict__ pd, int RBd, int J,
-                           double* __restrict__ out) {
+                           const double* __restrict__ pm, int RBm, double* __restrict__ out) {
     const int t = blockIdx.x * blockDim.x + threadIdx.x;
-    if (t >= 6 * J) return;
+    if (t >= 6 * J + 2) return;
+    if (t >= 6 * J) {   // mean energies <v> M <v>, <w> M <w>
+        const int fam = t - 6 * J;
+        double s = 0.0;
+        for (int b = 0; b < RBm; ++b) s += pm[(int64_t)fam * RBm + b];
+        out[fam] = s;
+        return;
+    }
     const int f = t / J, j = t % J;
     double s = 0.0;
     if (f < 4) {
@@ -1287,23 +1301,33 @@ __global__ void k_diag_fin(const double* __restrict__ pq, int RBq, const double*
 }
 
 int launch_diagnostics(ens_ctx* c, cudaStream_t s, const double* x, const double* means, double* out) {
+    // fixed grids (deterministic partial orders) sized to fill the GPU: these run every step of
+    // run() (`_record`, stepper.py:432-439)
     const int J = c->J;
-    const int RBq = 148;
+    const int RBq = 148 * 8, RBd = 148 * 8, RBm = 148 * 2;
+    const size_t need = (size_t)RBq * 4 * J + (size_t)RBd * 2 * J + (size_t)RBm * 2;
+    if (c->diag_part_n < need) {
+        cudaFree(c->diag_part);
+        c->diag_part = nullptr;
+        ENS_CK(cudaMalloc(&c->diag_part, sizeof(double) * need));
+        c->diag_part_n = need;
+    }
+    double* pq = c->diag_part;
+    double* pd = pq + (size_t)RBq * 4 * J;
+    double* pm = pd + (size_t)RBd * 2 * J;
     k_quadforms<<<RBq, 256, 0, s>>>(c->m.s_rowptr, c->m.s_col, c->m.s_mass, c->m.s_stiff, x, c->m.ns, c->n_total, J,
-                                    c->red_part);
+                                    pq);
     ENS_CKL();
     const int JB = J < 128 ? J : 128;
     const int EPB = 128 / JB > 0 ? 128 / JB : 1;
-    const int RBd = 148;
-    double* pd = c->red_part + (size_t)RBq * 4 * J;
     dim3 grid(RBd, (J + JB - 1) / JB);
     // the y-dimension splits members; partial index uses blockIdx.x only (members disjoint per y)
     k_divergence<<<grid, EPB * JB, sizeof(double) * 2 * EPB * JB, s>>>(c->m.e_nodes, c->m.e_geo, c->m.nt, x,
                                                                       c->n_total, J, JB, pd);
     ENS_CKL();
-    k_diag_fin<<<(6 * J + 255) / 256, 256, 0, s>>>(c->red_part, RBq, pd, RBd, J, out);
+    k_mean_energy<<<dim3(RBm, 2), 256, 0, s>>>(c->m.s_rowptr, c->m.s_col, c->m.s_mass, means, c->m.ns, pm);
     ENS_CKL();
-    k_mean_energy<<<2, 256, 0, s>>>(c->m.s_rowptr, c->m.s_col, c->m.s_mass, means, c->m.ns, out);
+    k_diag_fin<<<(6 * J + 2 + 255) / 256, 256, 0, s>>>(pq, RBq, pd, RBd, J, pm, RBm, out);
     ENS_CKL();
     return ENS_OK;
 }
