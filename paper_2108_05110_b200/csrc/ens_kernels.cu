@@ -1146,58 +1146,6 @@ int launch_epilogue(ens_ctx* c, cudaStream_t s, const double* x, double* p_out) 
 // ---------------------------------------------------------------------------
 // diagnostics (stepper.py:397-439, fem.py:508-514)
 // ---------------------------------------------------------------------------
-// per-member quadratic forms with M and K for v (mat 0) and w (mat 1):
-// part[blk][4][J]: (vMv, wMw, vKv, wKw)
-__global__ void k_quadforms(const int32_t* __restrict__ rp, const int32_t* __restrict__ col,
-                            const double* __restrict__ mass, const double* __restrict__ stiff,
-                            const double* __restrict__ X, int ns, int64_t N, int J, double* __restrict__ part) {
-    // block handles a node range; thread -> (node offset, member); J <= 256 per pass
-    __shared__ double red[4][256];
-    const int64_t per = ((int64_t)ns + gridDim.x - 1) / gridDim.x;
-    const int64_t n0 = (int64_t)blockIdx.x * per, n1 = min((int64_t)ns, n0 + per);
-    for (int jc = 0; jc < J; jc += 256) {
-        const int JB = min(256, J - jc);
-        const int RPB = 256 / JB;
-        const int jj = threadIdx.x % JB, ro = threadIdx.x / JB;
-        double a0 = 0, a1 = 0, a2 = 0, a3 = 0;
-        if (ro < RPB) {
-            const int j = jc + jj;
-            for (int64_t i = n0 + ro; i < n1; i += RPB) {
-                for (int cc = 0; cc < 2; ++cc) {
-                    double mv = 0, kv = 0, mw = 0, kw = 0;
-                    for (int k = rp[i]; k < rp[i + 1]; ++k) {
-                        const int64_t r = (2LL * col[k] + cc) * J + j;
-                        const double v = X[r], w = X[N * J + r];
-                        mv += mass[k] * v;
-                        kv += stiff[k] * v;
-                        mw += mass[k] * w;
-                        kw += stiff[k] * w;
-                    }
-                    const int64_t r = (2 * i + cc) * J + j;
-                    const double v = X[r], w = X[N * J + r];
-                    a0 += v * mv;
-                    a1 += w * mw;
-                    a2 += v * kv;
-                    a3 += w * kw;
-                }
-            }
-        }
-        red[0][threadIdx.x] = a0;
-        red[1][threadIdx.x] = a1;
-        red[2][threadIdx.x] = a2;
-        red[3][threadIdx.x] = a3;
-        __syncthreads();
-        if (threadIdx.x < JB) {
-            for (int f = 0; f < 4; ++f) {
-                double s = 0.0;
-                for (int k = 0; k < RPB; ++k) s += red[f][k * JB + threadIdx.x];
-                part[((int64_t)blockIdx.x * 4 + f) * J + jc + threadIdx.x] = s;
-            }
-        }
-        __syncthreads();
-    }
-}
-
 // energy of the means: mean^T M mean for v and w (single block per family, ordered)
 // grid (RBm, 2): block b of family fam sums a fixed node range -> part[fam][b]; k_diag_fin adds the
 // partials in order
@@ -1226,60 +1174,76 @@ __global__ void k_mean_energy(const int32_t* __restrict__ rp, const int32_t* __r
     }
 }
 
-// ||div z_j||^2 by quadrature, thread per (element, member), per-block partials
-__global__ void k_divergence(const int32_t* __restrict__ enodes, const double* __restrict__ egeo, int nt,
-                             const double* __restrict__ X, int64_t N, int J, int JB, double* __restrict__ part) {
-    extern __shared__ double red2[];   // [2][blockDim]
+// Per-member quadratic forms by element quadrature, thread per (element, member), per-block
+// partials part[blk][6][J]: v.Mv, w.Mw, v.Kv, w.Kw (K applied per component), ||div v||^2, ||div w||^2.
+// The 7-point rule integrates the P2 mass (degree 4) and stiffness (degree 2) integrands exactly,
+// so these equal the assembled-matrix forms (stepper.py:113-114, 397-439; fem.py:508-514) up to
+// rounding.
+__global__ void k_member_quad(const int32_t* __restrict__ enodes, const double* __restrict__ egeo, int nt,
+                              const double* __restrict__ X, int64_t N, int J, int JB, double* __restrict__ part) {
+    extern __shared__ double red6[];   // [6][blockDim]
     const int EPB = blockDim.x / JB;
     const int el = threadIdx.x / JB, jj = threadIdx.x % JB;
     const int j = blockIdx.y * JB + jj;
-    double sv = 0.0, sw = 0.0;
+    double acc[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
     if (el < EPB && j < J) {
         for (int e = blockIdx.x * EPB + el; e < nt; e += gridDim.x * EPB) {
             double gl[6];
             const double area = egeo[(int64_t)e * 8];
 #pragma unroll
             for (int i = 0; i < 6; ++i) gl[i] = egeo[(int64_t)e * 8 + 1 + i];
-            double vx[6], vy[6], wx[6], wy[6];
+            double z[2][6][2];   // [field v/w][node][comp]
 #pragma unroll
             for (int a = 0; a < 6; ++a) {
                 const int64_t nd = enodes[(int64_t)e * 6 + a];
-                vx[a] = X[(2 * nd) * J + j];
-                vy[a] = X[(2 * nd + 1) * J + j];
-                wx[a] = X[N * J + (2 * nd) * J + j];
-                wy[a] = X[N * J + (2 * nd + 1) * J + j];
+#pragma unroll
+                for (int f = 0; f < 2; ++f)
+#pragma unroll
+                    for (int cc = 0; cc < 2; ++cc) z[f][a][cc] = X[(int64_t)f * N * J + (2 * nd + cc) * J + j];
             }
             for (int q = 0; q < ENS_NQ; ++q) {
-                double dv = 0.0, dw = 0.0;
+                double val[2][2] = {{0.0, 0.0}, {0.0, 0.0}}, grd[2][2][2] = {{{0.0, 0.0}, {0.0, 0.0}},
+                                                                           {{0.0, 0.0}, {0.0, 0.0}}};
 #pragma unroll
                 for (int a = 0; a < 6; ++a) {
+                    const double ph = c_phi[q][a];
                     double gx, gy;
                     grad_phi(gl, q, a, gx, gy);
-                    dv += vx[a] * gx + vy[a] * gy;
-                    dw += wx[a] * gx + wy[a] * gy;
+#pragma unroll
+                    for (int f = 0; f < 2; ++f)
+#pragma unroll
+                        for (int cc = 0; cc < 2; ++cc) {
+                            val[f][cc] += z[f][a][cc] * ph;
+                            grd[f][cc][0] += z[f][a][cc] * gx;
+                            grd[f][cc][1] += z[f][a][cc] * gy;
+                        }
                 }
                 const double wd = area * c_qw[q];
-                sv += wd * dv * dv;
-                sw += wd * dw * dw;
+#pragma unroll
+                for (int f = 0; f < 2; ++f) {
+                    acc[f] += wd * (val[f][0] * val[f][0] + val[f][1] * val[f][1]);
+                    acc[2 + f] += wd * (grd[f][0][0] * grd[f][0][0] + grd[f][0][1] * grd[f][0][1] +
+                                        grd[f][1][0] * grd[f][1][0] + grd[f][1][1] * grd[f][1][1]);
+                    const double dv = grd[f][0][0] + grd[f][1][1];
+                    acc[4 + f] += wd * dv * dv;
+                }
             }
         }
     }
-    red2[threadIdx.x] = sv;
-    red2[blockDim.x + threadIdx.x] = sw;
+#pragma unroll
+    for (int f = 0; f < 6; ++f) red6[f * blockDim.x + threadIdx.x] = acc[f];
     __syncthreads();
     if (threadIdx.x < JB && j < J) {
-        double a = 0.0, b = 0.0;
-        for (int k = 0; k < EPB; ++k) {
-            a += red2[k * JB + threadIdx.x];
-            b += red2[blockDim.x + k * JB + threadIdx.x];
+        for (int f = 0; f < 6; ++f) {
+            double a = 0.0;
+            for (int k = 0; k < EPB; ++k) a += red6[f * blockDim.x + k * JB + threadIdx.x];
+            part[((int64_t)blockIdx.x * 6 + f) * J + j] = a;
         }
-        part[((int64_t)blockIdx.x * 2 + 0) * J + j] = a;
-        part[((int64_t)blockIdx.x * 2 + 1) * J + j] = b;
     }
 }
 
-__global__ void k_diag_fin(const double* __restrict__ pq, int RBq, const double* __restrict__ pd, int RBd, int J,
-                           const double* __restrict__ pm, int RBm, double* __restrict__ out) {
+__global__ void k_diag_fin(const double* __restrict__ pd, int RBd, int J, const double* __restrict__ pm, int RBm,
+                           double* __restrict__ out) {
     const int t = blockIdx.x * blockDim.x + threadIdx.x;
     if (t >= 6 * J + 2) return;
     if (t >= 6 * J) {   // mean energies <v> M <v>, <w> M <w>
@@ -1291,11 +1255,7 @@ __global__ void k_diag_fin(const double* __restrict__ pq, int RBq, const double*
     }
     const int f = t / J, j = t % J;
     double s = 0.0;
-    if (f < 4) {
-        for (int b = 0; b < RBq; ++b) s += pq[((int64_t)b * 4 + f) * J + j];
-    } else {
-        for (int b = 0; b < RBd; ++b) s += pd[((int64_t)b * 2 + (f - 4)) * J + j];
-    }
+    for (int b = 0; b < RBd; ++b) s += pd[((int64_t)b * 6 + f) * J + j];
     // out layout: vMv, wMw, vKv, wKw, div_v^2, div_w^2
     out[2 + (int64_t)f * J + j] = s;
 }
@@ -1304,30 +1264,26 @@ int launch_diagnostics(ens_ctx* c, cudaStream_t s, const double* x, const double
     // fixed grids (deterministic partial orders) sized to fill the GPU: these run every step of
     // run() (`_record`, stepper.py:432-439)
     const int J = c->J;
-    const int RBq = 148 * 8, RBd = 148 * 8, RBm = 148 * 2;
-    const size_t need = (size_t)RBq * 4 * J + (size_t)RBd * 2 * J + (size_t)RBm * 2;
+    const int RBd = 148 * 8, RBm = 148 * 2;
+    const size_t need = (size_t)RBd * 6 * J + (size_t)RBm * 2;
     if (c->diag_part_n < need) {
         cudaFree(c->diag_part);
         c->diag_part = nullptr;
         ENS_CK(cudaMalloc(&c->diag_part, sizeof(double) * need));
         c->diag_part_n = need;
     }
-    double* pq = c->diag_part;
-    double* pd = pq + (size_t)RBq * 4 * J;
-    double* pm = pd + (size_t)RBd * 2 * J;
-    k_quadforms<<<RBq, 256, 0, s>>>(c->m.s_rowptr, c->m.s_col, c->m.s_mass, c->m.s_stiff, x, c->m.ns, c->n_total, J,
-                                    pq);
-    ENS_CKL();
+    double* pd = c->diag_part;
+    double* pm = pd + (size_t)RBd * 6 * J;
     const int JB = J < 128 ? J : 128;
     const int EPB = 128 / JB > 0 ? 128 / JB : 1;
     dim3 grid(RBd, (J + JB - 1) / JB);
     // the y-dimension splits members; partial index uses blockIdx.x only (members disjoint per y)
-    k_divergence<<<grid, EPB * JB, sizeof(double) * 2 * EPB * JB, s>>>(c->m.e_nodes, c->m.e_geo, c->m.nt, x,
-                                                                      c->n_total, J, JB, pd);
+    k_member_quad<<<grid, EPB * JB, sizeof(double) * 6 * EPB * JB, s>>>(c->m.e_nodes, c->m.e_geo, c->m.nt, x,
+                                                                       c->n_total, J, JB, pd);
     ENS_CKL();
     k_mean_energy<<<dim3(RBm, 2), 256, 0, s>>>(c->m.s_rowptr, c->m.s_col, c->m.s_mass, means, c->m.ns, pm);
     ENS_CKL();
-    k_diag_fin<<<(6 * J + 2 + 255) / 256, 256, 0, s>>>(pq, RBq, pd, RBd, J, pm, RBm, out);
+    k_diag_fin<<<(6 * J + 2 + 255) / 256, 256, 0, s>>>(pd, RBd, J, pm, RBm, out);
     ENS_CKL();
     return ENS_OK;
 }
