@@ -630,14 +630,15 @@ class Engine:
         rows = self.nvel if kind == "loads" else hm.nbdofs
         sep = None
         if hasattr(obj, "separable"):
+            # keyed by id(obj); the entry keeps obj alive, so the id cannot be reused by another object
             key = (kind, id(obj))
             if key not in self._data_cache:
                 s = obj.separable(self.disc, self.config)
                 basis = np.asarray(s.basis, dtype=float).reshape(len(s.basis), -1)
                 if kind == "loads":
                     basis = basis[:, hm.ref_of_int[:self.nvel]]
-                self._data_cache[key] = (s, torch.as_tensor(np.ascontiguousarray(basis)).to(self.dev))
-            sep = self._data_cache[key]
+                self._data_cache[key] = (s, torch.as_tensor(np.ascontiguousarray(basis)).to(self.dev), obj)
+            sep = self._data_cache[key][:2]
         dd = N.DataDesc()
         dd.rows = rows
         keep = []
@@ -721,7 +722,7 @@ class Engine:
         ent = self._gdata_cache.get(key)
         if ent is None:
             self._data(obj, kind, 0.0)                   # builds the device basis once
-            sep, basis_t = self._data_cache[key]
+            sep, basis_t = self._data_cache[key][:2]
             K = basis_t.shape[0]
             pin = torch.zeros(2, K, self.J, dtype=torch.float64, pin_memory=True)
             dev = torch.zeros(2, K, self.J, dtype=torch.float64, device=self.dev)
