@@ -259,20 +259,35 @@ __global__ void __launch_bounds__(256, 3) k_diag_np(MfDev d, int item0, double* 
             pert = 1;
         }
         const double inv = 1.0 / piv;
+        // plain rank-1 update of all 16 entries (no per-entry pivot tests: the step was issue-bound
+        // on them), then the pivot column and row of the owning threads are overwritten -- the
+        // same values as before: column k gets 0 - fr * inv, row k gets row * inv (inv on the pivot)
+        const int kk = k & 15, kh = k >> 4;
+        double np[4], fr[4];
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
-            const int c = tx + 16 * j;
-            const double np = (c == k ? 1.0 : s_row[buf][c]) * inv;
+        for (int j = 0; j < 4; ++j) np[j] = s_row[buf][tx + 16 * j] * inv;
 #pragma unroll
-            for (int i = 0; i < 4; ++i) {
-                const int r = ty + 16 * i;
-                if (r == k) {
-                    a[i][j] = np;
-                } else {
-                    const double fr = s_col[buf][r];
-                    a[i][j] = (c == k ? 0.0 : a[i][j]) - fr * np;
+        for (int i = 0; i < 4; ++i) fr[i] = s_col[buf][ty + 16 * i];
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+            for (int j = 0; j < 4; ++j) a[i][j] -= fr[i] * np[j];
+        if (tx == kk) {   // column k (the thread's column slot kh): -fr * inv
+#pragma unroll
+            for (int j = 0; j < 4; ++j)
+                if (j == kh) {
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) a[i][j] = -(fr[i] * inv);
+                    np[j] = inv;
                 }
-            }
+        }
+        if (ty == kk) {   // row k (the thread's row slot kh): row * inv, inv on the pivot
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+                if (i == kh) {
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) a[i][j] = np[j];
+                }
         }
         const int k1 = k + 1;
         if (k1 < pw) {
