@@ -698,8 +698,23 @@ class Engine:
         """One time-step of all local members; returns the max relative residual."""
         with self.on_stream():
             if self._graph_ok(forcing, boundary, t_next):
+                try:
+                    self._ensure_graphs(forcing, boundary)
+                except (RuntimeError, N.NativeError) as exc:   # capture unsupported here: eager steps
+                    import logging
+                    logging.getLogger(__name__).warning("step graphs disabled (%s)", exc)
+                    self.step_graphs = False
+                    self._graphs.clear()
+                    torch.cuda.synchronize(self.dev)
+                    return self._step(t_next, forcing, boundary)
                 return self._step_graphed(t_next, forcing, boundary)
             return self._step(t_next, forcing, boundary)
+
+    def _ensure_graphs(self, forcing, boundary):
+        """Capture this parity's step graphs (no-op once captured); no state is modified."""
+        lo = self._gdata(forcing, "loads") if hasattr(forcing, "separable") else None
+        bc = self._gdata(boundary, "bc")
+        self._step_graphs(lo, bc)
 
     # ------------------------------------------------------------------
     # whole-step CUDA graphs
