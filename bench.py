@@ -188,7 +188,8 @@ def main():
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
     comm = None
-    if world > 1:
+    # BENCH_FORCE_DIST=1 (testing only): take the sharded code path even on one rank
+    if world > 1 or os.environ.get("BENCH_FORCE_DIST") == "1":
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
         comm = dist.group.WORLD
     import paper_2108_05110_b200 as P

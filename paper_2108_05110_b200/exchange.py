@@ -46,11 +46,33 @@ def allreduce_max_scalar(value: float, comm=None, device=None) -> float:
     return allreduce_max_values([value], comm, device)[0]
 
 
+_SCALAR_BUFS = {}
+
+
 def allreduce_max_values(values, comm=None, device=None):
-    """Elementwise max over ranks of a few host scalars (one small collective)."""
+    """Elementwise max over ranks of a few host scalars (one small collective).
+
+    Persistent pinned host / device buffers per (device, count): one async H2D, the
+    collective, one async D2H and a single stream synchronisation."""
     if comm is None:
         return list(values)
     import torch
-    t = torch.tensor(list(values), dtype=torch.float64, device=device)
-    dist.all_reduce(t, op=dist.ReduceOp.MAX, group=comm)
-    return [float(x) for x in t.tolist()]
+    if device is None or torch.device(device).type != "cuda":   # gloo / CPU tensors (tests)
+        t = torch.tensor(list(values), dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX, group=comm)
+        return [float(x) for x in t.tolist()]
+    n = len(values)
+    key = (str(device), n)
+    bufs = _SCALAR_BUFS.get(key)
+    if bufs is None:
+        bufs = (torch.zeros(n, dtype=torch.float64, pin_memory=True),
+                torch.zeros(n, dtype=torch.float64, device=device),
+                torch.zeros(n, dtype=torch.float64, pin_memory=True))
+        _SCALAR_BUFS[key] = bufs
+    h_in, d, h_out = bufs
+    h_in.numpy()[:] = values
+    d.copy_(h_in, non_blocking=True)
+    dist.all_reduce(d, op=dist.ReduceOp.MAX, group=comm)
+    h_out.copy_(d, non_blocking=True)
+    torch.cuda.current_stream(d.device).synchronize()
+    return [float(x) for x in h_out.numpy()]

@@ -16,7 +16,12 @@ from paper_2108_05110_b200 import stepper as ST
 case = os.environ.get("CASE", "C2")
 n = int(os.environ.get("STEPS", "5"))
 disc, cfg, prob = P.build_case(case)
-eng = ST.get_engine(disc, cfg)
+comm = None
+if os.environ.get("FORCE_DIST") == "1":   # sharded code path on one rank (run under torchrun)
+    import torch.distributed as dist
+    dist.init_process_group("nccl", device_id=torch.device("cuda", 0))
+    comm = dist.group.WORLD
+eng = ST.get_engine(disc, cfg, comm=comm)
 eng.load_state(prob.initial_v, prob.initial_w, None, None)
 t = 0.0
 for _ in range(6):
