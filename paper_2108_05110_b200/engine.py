@@ -464,7 +464,17 @@ class Engine:
         self.sums = torch.zeros(2 * nvel, **f64)
         self.means = torch.zeros(2 * nvel, **f64)
         self.means_valid = False
-        self.maxsq = torch.zeros(2, self.nt, 7, **f64)
+        # eddy maxima of both families, plus a 3-double tail on which the sharded step sends the
+        # previous step's (residual, iterations, renewal flag) through the same MAX exchange
+        self.maxsq_ext = torch.zeros(2 * self.nt * 7 + 3, **f64)
+        self.maxsq = self.maxsq_ext[:2 * self.nt * 7].view(2, self.nt, 7)
+        self._tail = self.maxsq_ext[2 * self.nt * 7:]
+        self._tail_in = torch.zeros(3, dtype=torch.float64, pin_memory=True)
+        self._tail_out = torch.zeros(3, dtype=torch.float64, pin_memory=True)
+        self._tail_ev = torch.cuda.Event()
+        self._prev_local = None        # (residual, iterations, renew) of the last step, this rank
+        self._nstep = 0
+        self.global_residuals = {}     # engine step index -> residual max over ranks (sharded runs)
         self.as_vals = torch.zeros(2, hm.nnz_s, **f64)
         self.diag_out = torch.zeros(2 + 6 * J, **f64)
         # a dedicated (non-default) stream: the factorisation and solve sequences
@@ -836,16 +846,30 @@ class Engine:
         self._gfill(bc, t_next)
         segs = self._step_graphs(lo, bc)
         self._cost_begin()
-        need = self._need_factor()
         self._retire(nxt)
         if self.comm is None:
+            need = self._need_factor()
             self._replay(segs["pre"])
         else:
             self._replay(segs["sums"])
             XC.allreduce_member_sums(self.sums, self.comm)
             self._replay(segs["rhs"])
-            XC.allreduce_eddy_max(self.maxsq, self.comm)
+            # the previous step's (residual, iterations, renewal flag) ride on the MAX exchange:
+            # no separate scalar collective and no extra synchronisation per step
+            prev = self._prev_local if self._prev_local is not None else (0.0, 0.0, 0.0)
+            self._tail_in.numpy()[:] = prev
+            self._tail.copy_(self._tail_in, non_blocking=True)
+            XC.allreduce_eddy_max(self.maxsq_ext, self.comm)
+            self._tail_out.copy_(self._tail, non_blocking=True)
+            self._tail_ev.record(self.stream)
             self._replay(segs["assemble"])
+            self._tail_ev.synchronize()            # the assembly keeps the GPU busy meanwhile
+            g = self._tail_out.numpy().copy()
+            if self._prev_local is not None:
+                self.global_residuals[self._nstep - 1] = float(g[0])
+                self.last_iters = int(g[1])
+                self._renew = g[2] > 0.0
+            need = self._need_factor()
         if need:
             self._factor_timed()
         else:
@@ -876,10 +900,23 @@ class Engine:
         self.means_valid = False
         self.prev_valid = True
         renew = self._cost_end()
-        res, it, rn = XC.allreduce_max_values([max(self.last_relres), float(self.last_iters), float(renew)],
-                                              self.comm, self.dev)
-        self.last_iters = int(it)
-        self._renew = rn > 0.0
+        self._nstep += 1
+        if self.comm is None:
+            self._renew = renew
+            return max(self.last_relres)
+        # sharded: this rank's values travel with the next step's MAX exchange (or flush_global)
+        self._prev_local = (max(self.last_relres), float(self.last_iters), float(renew))
+        return max(self.last_relres)
+
+    def flush_global(self):
+        """Sharded runs: agree on the last step's (residual, iterations, renewal) now instead of in
+        the next step's exchange; returns the residual max over ranks."""
+        if self.comm is None or self._prev_local is None:
+            return None
+        res, it, rn = XC.allreduce_max_values(list(self._prev_local), self.comm, self.dev)
+        self.global_residuals[self._nstep - 1] = res
+        self.last_iters, self._renew = int(it), rn > 0.0
+        self._prev_local = None
         return res
 
     def diagnostics(self):
@@ -899,6 +936,7 @@ class Engine:
         lib, ctx, s = self.lib, self.ctx, self.sptr
         cur, nxt = self.cur, 1 - self.cur
         X = self.X[cur]
+        self.flush_global()        # sharded: agree on the previous graphed step's values first
         self._cost_begin()
         if not self.means_valid:
             self._compute_means()
@@ -937,6 +975,7 @@ class Engine:
         # residual max, iteration count and the renewal decision over ranks: every rank then
         # takes the same refactorisation decision next step (identical shared matrices, lockstep timing)
         renew = self._cost_end()
+        self._nstep += 1
         res, it, rn = XC.allreduce_max_values([max(self.last_relres), float(self.last_iters), float(renew)],
                                               self.comm, self.dev)
         self.last_iters = int(it)
