@@ -188,8 +188,14 @@ def main():
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
     comm = None
+    _stdout_fd = None
     # BENCH_FORCE_DIST=1 (testing only): take the sharded code path even on one rank
     if world > 1 or os.environ.get("BENCH_FORCE_DIST") == "1":
+        # library banners printed to the process's stdout (NCCL / c10d communicator set-up) are sent
+        # to stderr until the result line, so rank 0's stdout is exactly one JSON line
+        sys.stdout.flush()
+        _stdout_fd = os.dup(1)
+        os.dup2(2, 1)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
         comm = dist.group.WORLD
     import paper_2108_05110_b200 as P
@@ -381,6 +387,9 @@ def main():
             "e2e": e2e,
             "cpu_baseline": cpu,
         }
+        if _stdout_fd is not None:
+            sys.stdout.flush()
+            os.dup2(_stdout_fd, 1)
         print(json.dumps(line), flush=True)
     if comm is not None:
         dist.destroy_process_group()
