@@ -137,7 +137,7 @@ def run_reference(args):
     os.environ.setdefault("OMP_NUM_THREADS", str(os.cpu_count()))
     import paper_2108_05110_b200 as P
     disc, cfg, prob = P.build_case(CASE, J=J_PER_GPU * args.gpus)
-    steps = max(1, min(args.steps, 2))
+    steps = max(1, min(args.steps, 2 if args.gpus <= 2 else 1))   # bounded sample: a few minutes at any N
     value, secs = cpu_baseline(disc, cfg, prob, steps)
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "impl": "reference", "n_gpus": args.gpus, "steps": steps,
