@@ -648,14 +648,24 @@ static int mf_factor_launches(ens_ctx* c, cudaStream_t s, const double* as_vals,
     int64_t cnt = 0;
     ENS_CK(cudaMemsetAsync(c->d_count, 0, sizeof(int32_t), s));
     const int64_t nrow = (int64_t)c->sched_factor.size() / 5;
+    bool zeroed = false;
     for (int64_t i = 0; i < nrow; ++i) {
         const int64_t* r = &c->sched_factor[5 * i];
         const int op = (int)r[0], L = (int)r[1], off = (int)r[2], n = (int)r[3];
         switch (op) {
             case OP_ZERO: {
-                const int64_t a = c->level_storage_off[L], b = c->level_storage_off[L + 1];
-                for (int mat = 0; mat < 2; ++mat)
-                    ENS_CK(cudaMemsetAsync(c->fronts + mat * st + a, 0, sizeof(double) * (size_t)(b - a), s));
+                // the level ranges are disjoint and only ever accumulated into after their own zeroing,
+                // so the first OP_ZERO clears every level of both systems at once (one memset instead
+                // of two per level when the levels tile the storage)
+                if (zeroed) continue;
+                zeroed = true;
+                const int64_t top = c->level_storage_off.back();
+                if (top == st) {
+                    ENS_CK(cudaMemsetAsync(c->fronts, 0, sizeof(double) * (size_t)(2 * st), s));
+                } else {
+                    for (int mat = 0; mat < 2; ++mat)
+                        ENS_CK(cudaMemsetAsync(c->fronts + mat * st, 0, sizeof(double) * (size_t)top, s));
+                }
                 continue;   // a memset, not a kernel launch
             }
             case OP_ORIG: {
