@@ -270,6 +270,8 @@ def test_pressure_mean_zero():
     ("C1", dict(n=6, J=32, steps=2)),                             # exactly one full column block
     ("C1", dict(n=4, J=64, steps=3)),                             # C3's member count: wide SpMM, 2 column blocks
     ("C4", dict(k=1, J=128, steps=2, dt=0.05, length=6.0)),       # C4/C5-shard member count, 4 column blocks
+    ("C1", dict(n=6, J=1, steps=3)),                              # a single member: zero fluctuations, odd J
+    ("C1", dict(n=6, J=7, steps=3)),                              # ragged odd J: scalar (non-pair) vector paths
 ])
 def test_case_runs_match_oracle(case, over):
     """Small instances of the BASELINE problem kinds and member counts against the CPU oracle."""
