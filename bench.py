@@ -334,6 +334,27 @@ def main():
         e2e = {"value": J_total * args.e2e_steps / e2e_s, "unit": UNIT, "h2d_bytes_per_step": per_v + 8 * 2 * 2 * 3 * J_total,
                "d2h_bytes_per_step": per + 16, "steps": args.e2e_steps, "step_ms": step_ms,
                "api": "paper_2108_05110_b200.advance(state, config, disc, forcing, boundary), numpy state in/out"}
+        # the transfer floor the e2e step runs against: pinned host<->device copy bandwidth measured here
+        # (CUDA events, best of 5, one buffer of the per-step state size), plus the device-timed step
+        hb = torch.empty(per // 8, dtype=torch.float64, pin_memory=True)
+        db = torch.empty(per // 8, dtype=torch.float64, device="cuda")
+        pe0, pe1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        bw = {}
+        for name, dst, src in (("h2d", db, hb), ("d2h", hb, db)):
+            best = None
+            for _ in range(5):
+                pe0.record()
+                dst.copy_(src, non_blocking=True)
+                pe1.record()
+                pe1.synchronize()
+                t = pe0.elapsed_time(pe1)
+                best = t if best is None else min(best, t)
+            bw[name] = per / (best * 1e-3) / 1e9
+        del hb, db
+        ms_step = ms / args.steps
+        floor = ms_step + 1e3 * (e2e["h2d_bytes_per_step"] / (bw["h2d"] * 1e9) + e2e["d2h_bytes_per_step"] / (bw["d2h"] * 1e9))
+        e2e["transfer_floor"] = {"h2d_gbs": bw["h2d"], "d2h_gbs": bw["d2h"], "device_step_ms": ms_step,
+                                 "floor_ms": floor, "frac": floor / float(np.median(step_ms))}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
