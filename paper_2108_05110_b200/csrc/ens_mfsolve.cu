@@ -148,7 +148,32 @@ __global__ void __launch_bounds__(256) k_finit(const int32_t* __restrict__ rows,
     pdl_wait();   // children's contribution rows come from the previous level's GEMM
     const double* b = io->r + (int64_t)mat * N * J;
     double* FRm = FR + (int64_t)mat * nidx * J;
-    if ((J & 1) == 0) {
+    if ((J & 1) == 0 && nrows * (J >> 1) < (int64_t)INT32_MAX - (int64_t)gridDim.x * blockDim.x) {
+        // 32-bit (row, column-pair) split: the 64-bit division by H dominated the index math
+        const int H = J >> 1;
+        const double2* b2 = reinterpret_cast<const double2*>(b);
+        double2* F2 = reinterpret_cast<double2*>(FRm);
+        const int tot = (int)(nrows * H);
+        for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < tot; t += gridDim.x * blockDim.x) {
+            const int rq = t / H;
+            const int e = rows[rq];
+            const int i = t - rq * H;
+            const int64_t row = e & 0x7fffffff;
+            const int4 g = *reinterpret_cast<const int4*>(gsrc + 4 * row);
+            const double2 bv = b2[(int64_t)max(idx[row], 0) * H + i];
+            double2 v = make_double2(0.0, 0.0);
+            const int src[4] = {g.x, g.y, g.z, g.w};
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const double2 c = F2[(int64_t)max(src[u], 0) * H + i];
+                if (src[u] >= 0) {
+                    v.x += c.x;
+                    v.y += c.y;
+                }
+            }
+            F2[row * H + i] = e < 0 ? make_double2(bv.x + v.x, bv.y + v.y) : v;
+        }
+    } else if ((J & 1) == 0) {
         const int H = J >> 1;
         const double2* b2 = reinterpret_cast<const double2*>(b);
         double2* F2 = reinterpret_cast<double2*>(FRm);
