@@ -36,6 +36,7 @@ from .ensemble import viscosity_stats
 
 _RENEW_DEBUG = os.environ.get("ENS_RENEW_DEBUG", "0") == "1"
 RENEW_WINDOW = int(os.environ.get("ENS_RENEW_WINDOW", "6"))   # lifetimes a per-position cost stays usable
+RENEW_STALE = int(os.environ.get("ENS_RENEW_STALE", str(4 * RENEW_WINDOW)))
 RENEW_PRED = os.environ.get("ENS_RENEW_PRED", "last")   # next-step cost when no recent profile: last step ("mean3", "min2" measured worse at C3/C4)
 
 
@@ -1046,7 +1047,9 @@ class Engine:
             nxt = min(self._recent[-2:])
         else:
             nxt = a
-        if steps < len(self._prof) and self._prof[steps][1] >= fresh:
+        # a position entry older than RENEW_WINDOW lifetimes still predicts (re-exploring a lag that
+        # measured worse costs a whole slow step) until it is RENEW_STALE lifetimes old
+        if steps < len(self._prof) and self._prof[steps][1] >= max(2, self._life - RENEW_STALE):
             nxt = self._prof[steps][0]
         if _RENEW_DEBUG:
             print(f"renew: pos {steps} step {step_ms:.2f} ms (F {self._cyc[0]:.2f}) iters {self.last_iters} "
