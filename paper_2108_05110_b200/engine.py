@@ -37,7 +37,52 @@ from .ensemble import viscosity_stats
 _RENEW_DEBUG = os.environ.get("ENS_RENEW_DEBUG", "0") == "1"
 RENEW_WINDOW = int(os.environ.get("ENS_RENEW_WINDOW", "6"))   # lifetimes a per-position cost stays usable
 RENEW_STALE = int(os.environ.get("ENS_RENEW_STALE", str(4 * RENEW_WINDOW)))
-RENEW_PRED = os.environ.get("ENS_RENEW_PRED", "last")   # next-step cost when no recent profile: last step ("mean3", "min2" measured worse at C3/C4)
+
+
+# Cost model of the renewal rule, fitted to the round-1 kernels on B200: a
+# factorisation costs a fixed latency per tree level plus its flops at an effective DMMA rate; an
+# apply costs a latency per level and direction plus the larger of its bytes and flops terms.  The
+# constants are fixed, so the rule built on them is a deterministic function of the plan, J and the
+# iteration counts (fit: C2 8.4 / 0.71 ms, C3 44 / 5.5 ms, C4 8.9 / 3.0 ms factor / apply).
+FACTOR_LEVEL_S = 0.28e-3       # per tree level (panel, update and extend-add launches)
+RATE_FACTOR_FLOPS = 8.0e12     # sweep factorisation, fp64 DMMA
+APPLY_LEVEL_S = 10e-6          # per tree level and sweep direction
+RATE_APPLY_BYTES = 2.2e12      # preconditioner apply, algorithmic bytes
+RATE_APPLY_FLOPS = 11.0e12     # preconditioner apply at large J (fp64 DMMA)
+RATE_SPMM_BYTES = 1.39e12      # saddle SpMM, algorithmic bytes
+
+
+def spmm_bytes(hm, J):
+    """Algorithmic HBM bytes of one ens_spmm launch (both systems)."""
+    ns, npres, ntot, nnz = hm.ns, hm.npres, hm.ntot, hm.nnz_s
+    npairs = len(hm.b_col)
+    per_mat = (12 * nnz + 4 * (ns + 1)            # A_s values + column indices + row pointers
+               + 20 * npairs + 4 * (ns + 1)       # B^T (p, bx, by) by node
+               + 20 * npairs + 4 * (npres + 1)    # B (node, bx, by) by pressure row
+               + ntot                             # identity-row flags
+               + 16 * ntot * J)                   # X read once, Y written once
+    return 2 * per_mat
+
+
+def apply_bytes(hm, J):
+    """Algorithmic bytes of one preconditioner apply (both systems): factor entries read once per
+    sweep direction pair, right-hand side / iterate traffic of the forward and backward sweeps."""
+    nnz_lu = hm.plan.stats["nnz_lu"]
+    return 2 * 8 * nnz_lu + 2 * 2 * 8 * hm.ntot * J * 2
+
+
+def apply_flops(hm, J):
+    return 2.0 * 2 * hm.plan.stats["nnz_lu"] * J
+
+
+def cost_model(hm, J):
+    """Modelled seconds of a factorisation and of one Krylov iteration (apply + SpMM), both systems."""
+    nlev = hm.plan.nlevels
+    t_f = nlev * FACTOR_LEVEL_S + 2 * hm.plan.stats["factor_flops"] / RATE_FACTOR_FLOPS
+    t_apply = 2 * nlev * APPLY_LEVEL_S + max(apply_bytes(hm, J) / RATE_APPLY_BYTES,
+                                             apply_flops(hm, J) / RATE_APPLY_FLOPS)
+    t_it = t_apply + spmm_bytes(hm, J) / RATE_SPMM_BYTES
+    return dict(t_factor=t_f, t_iter=t_it, rho=t_f / t_it)
 
 
 def _dptr(t: torch.Tensor) -> int:
@@ -286,17 +331,19 @@ class Engine:
                  refactor="adaptive", lag_max_iters=8, lag_max_steps=500, guess="extrapolate"):
         """``refactor``: "always" rebuilds the LU preconditioner every step (the
         reference refactorises every sub-step, `stepper.py:216`); "adaptive"
-        keeps the last factorisation until the renewal rule (``_cost_end``: the last
-        step's device time exceeds the average cost per step of the current
-        factorisation's lifetime, factorisation included) fires, FGMRES needs more
-        than ``lag_max_iters`` iterations, or ``lag_max_steps`` steps have passed.  Either way every solve is
-        converged to the same true residual ``rtol`` on the *current* matrix.
+        keeps the last factorisation until the deterministic renewal rule
+        (``_renewal``: iteration counts against the modelled factorisation cost)
+        fires, FGMRES needs more than ``lag_max_iters`` iterations, or
+        ``lag_max_steps`` steps have passed; "timed" is "adaptive" with the rule fed
+        by measured device times (``_cost_end``; not reproducible run to run).
+        Whatever the policy every solve is converged to the same true residual
+        ``rtol`` on the *current* matrix.
 
         ``guess``: FGMRES initial iterate -- "extrapolate" (2 x^n - x^{n-1} when
         the previous level is resident, an O(dt^2) guess that usually saves one
         preconditioned iteration) or "previous" (x^n)."""
-        if refactor not in ("always", "adaptive"):
-            raise ValueError("refactor must be 'always' or 'adaptive'")
+        if refactor not in ("always", "adaptive", "timed"):
+            raise ValueError("refactor must be 'always', 'adaptive' or 'timed'")
         if guess not in ("extrapolate", "previous"):
             raise ValueError("guess must be 'extrapolate' or 'previous'")
         self.guess = guess
@@ -310,7 +357,8 @@ class Engine:
         self._cyc = None           # [factorisation ms, step ms since, steps since]
         self._prof = []            # [step ms, lifetime] by position within a factorisation's lifetime
         self._life = 0             # factorisations so far
-        self._recent = []          # step ms of this lifetime's last steps
+        self._lk = None            # iteration counts of the current factorisation's lifetime
+        self._pending = None       # sharded: renewal waiting for the agreed iteration count
         self._fac_this = False
         self.pivoting = False
         if not torch.cuda.is_available():
@@ -322,6 +370,7 @@ class Engine:
         self.J_total = config.num_members
         self.j0 = j0
         self.J = J = self.J_total if J is None else J
+        self.rho = cost_model(hm, J)["rho"]
         self.comm = comm
         self.restart, self.max_restarts, self.rtol = restart, max_restarts, rtol
         self.ntot, self.nvel, self.npres = hm.ntot, hm.nvel, hm.npres
@@ -709,11 +758,20 @@ class Engine:
         """One time-step of all local members; returns the max relative residual."""
         with self.on_stream():
             if self._graph_ok(forcing, boundary, t_next):
+                failed = None
                 try:
-                    self._ensure_graphs(forcing, boundary)
+                    fresh = self._ensure_graphs(forcing, boundary)
                 except (RuntimeError, N.NativeError) as exc:   # capture unsupported here: eager steps
+                    failed, fresh = exc, True
+                if fresh and self.comm is not None:
+                    # every rank must take the same (graphed or eager) path: the two paths issue
+                    # different collectives, so a capture failure on one rank disables graphs on all
+                    bad = XC.allreduce_max_values([1.0 if failed is not None else 0.0], self.comm, self.dev)[0]
+                    if bad > 0.0 and failed is None:
+                        failed = RuntimeError("step-graph capture failed on another rank")
+                if failed is not None:
                     import logging
-                    logging.getLogger(__name__).warning("step graphs disabled (%s)", exc)
+                    logging.getLogger(__name__).warning("step graphs disabled (%s)", failed)
                     self.step_graphs = False
                     self._graphs.clear()
                     torch.cuda.synchronize(self.dev)
@@ -722,10 +780,13 @@ class Engine:
             return self._step(t_next, forcing, boundary)
 
     def _ensure_graphs(self, forcing, boundary):
-        """Capture this parity's step graphs (no-op once captured); no state is modified."""
+        """Capture this parity's step graphs; returns True when they were captured now.  No state
+        is modified."""
         lo = self._gdata(forcing, "loads") if hasattr(forcing, "separable") else None
         bc = self._gdata(boundary, "bc")
+        n = len(self._graphs)
         self._step_graphs(lo, bc)
+        return len(self._graphs) != n
 
     # ------------------------------------------------------------------
     # whole-step CUDA graphs
@@ -868,8 +929,10 @@ class Engine:
             g = self._tail_out.numpy().copy()
             if self._prev_local is not None:
                 self.global_residuals[self._nstep - 1] = float(g[0])
-                self.last_iters = int(g[1])
-                self._renew = g[2] > 0.0
+                self._agreed(g[1])
+                if self.refactor == "timed":
+                    self._renew = g[2] > 0.0
+                self._prev_local = None
             need = self._need_factor()
         if need:
             self._factor_timed()
@@ -900,13 +963,13 @@ class Engine:
         self.cur = nxt
         self.means_valid = False
         self.prev_valid = True
-        renew = self._cost_end()
+        renew = self._step_done(iters)
         self._nstep += 1
         if self.comm is None:
             self._renew = renew
             return max(self.last_relres)
         # sharded: this rank's values travel with the next step's MAX exchange (or flush_global)
-        self._prev_local = (max(self.last_relres), float(self.last_iters), float(renew))
+        self._prev_local = (max(self.last_relres), float(self.last_iters), float(bool(renew)))
         return max(self.last_relres)
 
     def flush_global(self):
@@ -916,7 +979,9 @@ class Engine:
             return None
         res, it, rn = XC.allreduce_max_values(list(self._prev_local), self.comm, self.dev)
         self.global_residuals[self._nstep - 1] = res
-        self.last_iters, self._renew = int(it), rn > 0.0
+        self._agreed(it)
+        if self.refactor == "timed":
+            self._renew = rn > 0.0
         self._prev_local = None
         return res
 
@@ -975,43 +1040,107 @@ class Engine:
         self.prev_valid = True
         # residual max, iteration count and the renewal decision over ranks: every rank then
         # takes the same refactorisation decision next step (identical shared matrices, lockstep timing)
-        renew = self._cost_end()
+        renew = self._step_done(iters)
         self._nstep += 1
-        res, it, rn = XC.allreduce_max_values([max(self.last_relres), float(self.last_iters), float(renew)],
+        if self.comm is None:
+            self._renew = renew
+            return max(self.last_relres)
+        res, it, rn = XC.allreduce_max_values([max(self.last_relres), float(self.last_iters), float(bool(renew))],
                                               self.comm, self.dev)
-        self.last_iters = int(it)
-        self._renew = rn > 0.0
+        self._agreed(it)
+        if self.refactor == "timed":
+            self._renew = rn > 0.0
         return res
 
     # ------------------------------------------------------------------
-    # preconditioner renewal (adaptive policy)
+    # preconditioner renewal
     # ------------------------------------------------------------------
     def _need_factor(self):
         return (self.refactor == "always" or not self.factored or self.since_factor >= self.lag_max_steps
                 or self.last_iters > self.lag_max_iters or self._renew)
 
     def _cost_begin(self):
+        self._fac_this = False
+        if self.refactor != "timed":
+            return
         if self._ev is None:
             self._ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
         self._ev[0].record(self.stream)
-        self._fac_this = False
 
     def _factor_timed(self):
-        self._ev[1].record(self.stream)
+        if self.refactor == "timed":
+            self._ev[1].record(self.stream)
         self._factor()
-        self._ev[2].record(self.stream)
+        if self.refactor == "timed":
+            self._ev[2].record(self.stream)
         self._fac_this = True
 
+    def _step_done(self, iters):
+        """End of a step: the renewal decision for the next step.
+
+        "adaptive" (default) decides from the step's Krylov iteration count only
+        (agreed over ranks first when members are sharded, see ``_renewal``), so a
+        run is a deterministic function of its inputs.  "timed" keeps the
+        measured-device-time rule (``_cost_end``).  Returns the renewal flag this
+        rank proposes, or None when the decision waits for the agreed count."""
+        fac = self._fac_this
+        if self.refactor == "timed":
+            return self._cost_end()
+        if self.comm is not None:
+            self._pending = fac      # decided once the iteration count is agreed over ranks
+            return None
+        return self._renewal(iters, fac)
+
+    def _agreed(self, iters):
+        """Sharded runs: the step's iteration count maxed over ranks has arrived."""
+        self.last_iters = int(iters)
+        if self.refactor != "timed" and self._pending is not None:
+            self._renew = self._renewal(int(iters), self._pending)
+            self._pending = None
+
+    def _renewal(self, k, fac):
+        """Deterministic renewal rule (the optimal stopping rule of a renewal process).
+
+        A factorisation costs F, a step whose solve needs k preconditioned Krylov
+        iterations costs c0 + k c_it (``cost_model``).  With k_1..k_L the counts of
+        the current factorisation's lifetime, rebuilding before step L+1 lowers the
+        average cost per step iff  c0 + k_{L+1} c_it > (F + sum_i (c0 + k_i c_it)) / L,
+        i.e. iff  sum_i (k_{L+1} - k_i) > rho = F / c_it  (c0 cancels).  k_{L+1} is
+        predicted from the count at the same lifetime position in recent lifetimes
+        (exponentially averaged), else from k_L.  Only iteration counts enter, which
+        every rank agrees on, so two runs on the same inputs rebuild at the same
+        steps and are bitwise identical."""
+        if fac:
+            self._life += 1
+            self._lk = [k]
+        elif self._lk is None:
+            return False
+        else:
+            self._lk.append(k)
+        pos = len(self._lk)
+        fresh = max(2, self._life - RENEW_WINDOW)
+        if len(self._prof) < pos:
+            self._prof.append([float(k), self._life])
+        else:
+            old = self._prof[pos - 1]
+            self._prof[pos - 1] = [0.5 * (old[0] + k) if old[1] >= fresh else float(k), self._life]
+        if self.refactor != "adaptive":
+            return False
+        nxt = float(k)
+        if pos < len(self._prof) and self._prof[pos][1] >= max(2, self._life - RENEW_STALE):
+            nxt = self._prof[pos][0]
+        excess = sum(nxt - ki for ki in self._lk)
+        if _RENEW_DEBUG:
+            print(f"renew: pos {pos} k {k} pred {nxt:.2f} excess {excess:.2f} rho {self.rho:.2f}", flush=True)
+        return excess > self.rho
+
     def _cost_end(self):
-        """Renewal rule of the adaptive policy: with F the last factorisation's time and A_1..A_L the
-        device times of the steps since (factorisation excluded), rebuild before the next step when
-        the next step would cost more than the lifetime's average cost per step,
-        A_{L+1} > (F + sum A) / L -- the optimal stopping rule for a renewal whose per-step cost
-        grows as the factorisation ages.
-        The next step's cost is predicted from the cost at the same position of earlier
-        lifetimes when known (so a factorisation that goes stale after one step is rebuilt every
-        step), else from this step.  Whatever the policy, every solve is converged to rtol on the
-        current matrix."""
+        """Timed renewal rule (refactor="timed", opt-in): with F the last factorisation's device
+        time and A_1..A_L the device times of the steps since (factorisation excluded), rebuild
+        before the next step when the next step would cost more than the lifetime's average cost
+        per step, A_{L+1} > (F + sum A) / L.  The next step's cost is predicted from the cost at
+        the same position of earlier lifetimes when known, else from this step.  Decisions depend
+        on measured times, so runs are reproducible only up to the solver tolerance."""
         ev = self._ev
         ev[3].record(self.stream)
         ev[3].synchronize()
@@ -1028,32 +1157,15 @@ class Engine:
         else:
             return False
         steps = self._cyc[2]
-        # per-position step costs of recent factorisation lifetimes (exponential average, so one
-        # iteration spike does not shorten every later lifetime; the first lifetime -- the start-up
-        # transient -- and entries older than RENEW_WINDOW lifetimes are not used)
         fresh = max(2, self._life - RENEW_WINDOW)
         if len(self._prof) < steps:
             self._prof.append([a, self._life])
         else:
             old = self._prof[steps - 1]
             self._prof[steps - 1] = [0.5 * (old[0] + a) if old[1] >= fresh else a, self._life]
-        if self.refactor != "adaptive":
-            return False
-        # next step's cost: what the same position cost in a recent lifetime, else this step's
-        self._recent = ([] if self._fac_this else self._recent[-2:]) + [a]
-        if RENEW_PRED == "mean3":
-            nxt = sum(self._recent) / len(self._recent)
-        elif RENEW_PRED == "min2":
-            nxt = min(self._recent[-2:])
-        else:
-            nxt = a
-        # a position entry older than RENEW_WINDOW lifetimes still predicts (re-exploring a lag that
-        # measured worse costs a whole slow step) until it is RENEW_STALE lifetimes old
+        nxt = a
         if steps < len(self._prof) and self._prof[steps][1] >= max(2, self._life - RENEW_STALE):
             nxt = self._prof[steps][0]
-        if _RENEW_DEBUG:
-            print(f"renew: pos {steps} step {step_ms:.2f} ms (F {self._cyc[0]:.2f}) iters {self.last_iters} "
-                  f"pred {nxt:.2f} avg {(self._cyc[0] + self._cyc[1]) / steps:.2f}", flush=True)
         return nxt > (self._cyc[0] + self._cyc[1]) / steps
 
     def _rhs_and_member_pass(self, X, loads_ref):

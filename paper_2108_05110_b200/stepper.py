@@ -112,10 +112,12 @@ def set_solver_options(**kw):
     rtol: per-member true relative residual of every sub-step solve;
     restart / max_restarts: FGMRES cycle length and count;
     refactor: "always" (rebuild the LU preconditioner each step, as the
-    reference refactorises each sub-step) or "adaptive" (reuse it until the
-    renewal rule of Engine._cost_end fires -- the last step cost more than the
-    average per step of the factorisation's lifetime -- or FGMRES needs more
-    than lag_max_iters iterations, or lag_max_steps steps have passed);
+    reference refactorises each sub-step), "adaptive" (default: reuse it until
+    the deterministic renewal rule of Engine._renewal fires -- the iteration
+    counts since the last rebuild say a rebuild now lowers the modelled average
+    cost per step -- or FGMRES needs more than lag_max_iters iterations, or
+    lag_max_steps steps have passed; bitwise reproducible) or "timed" (the same
+    rule on measured device times; opt-in, not reproducible run to run);
     guess: FGMRES initial iterate, "extrapolate" (2 x^n - x^{n-1}) or "previous" (x^n).
     """
     unknown = set(kw) - set(_SOLVER_OPTS)

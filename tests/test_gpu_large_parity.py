@@ -1,0 +1,127 @@
+"""GPU parity at the BASELINE configurations as stated, against the REAL reference.
+
+Fixtures `tests/golden/large_*.npz` come from `tests/golden/make_golden_large.py`
+(the unmodified reference `ensmhd`, SuperLU, TH shim; C4 with the do-nothing
+outflow variant wrapped around the reference code):
+
+  * C2  128x128, J=20, dt=0.005: all 100 steps (checkpoint at step 10 and 100);
+  * C3  256x256 cavity, J=64, dt=0.01, s in {1, 0.1, 0.01}: 2 steps;
+  * C4  30-long channel h=1/8, J=128, dt=0.02, delta in {0.01, 0.1}: 3 steps.
+
+Compared: every member's v, w (so u = (v+w)/2 and
+B = (v-w)/(2 sqrt s)) and the ensemble means at a fixed subsample of dofs,
+four Gaussian projections of every full member field, the energy and member
+L2/H1 series (full-field quadratic forms) at 1e-9; pressures at 1e-8.  The
+north-star bar is 1e-8.  Also: two consecutive runs of C3 and C4 at full size
+are bitwise identical (deterministic preconditioner renewal).
+"""
+
+import os
+import sys
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+if not torch.cuda.is_available():  # pragma: no cover - GPU box only
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, os.path.join(HERE, "golden"))
+
+import make_golden_large as G  # noqa: E402
+import paper_2108_05110_b200 as P  # noqa: E402
+
+TOL_VEL = 1e-9
+TOL_PRES = 1e-8
+
+_CASE_ARGS = {"mms": ("C2", ("n", "J", "dt", "steps")),
+              "cavity": ("C3", ("n", "J", "dt", "steps", "coupling")),
+              "channel": ("C4", ("k", "J", "dt", "steps", "delta", "length"))}
+
+
+def build(case):
+    spec = G.CASES[case]
+    name, keys = _CASE_ARGS[spec["kind"]]
+    return P.build_case(name, **{k: spec[k] for k in keys if k in spec})
+
+
+def rel(a, b):
+    return float(np.linalg.norm(np.asarray(a) - np.asarray(b)) / max(np.linalg.norm(b), 1e-300))
+
+
+def compare_state(fx, prefix, state, scale_ref):
+    """Subsampled fields, means and projections of one state against the fixture."""
+    got = G.summarize(prefix, state.v, state.w, state.q, state.r, members=f"{prefix}v_sub" in fx)
+    errs = {}
+    for k, v in got.items():
+        ref = fx[k]
+        field = k[len(prefix)]
+        # w (and r) can vanish identically in the MMS (w = 0): measure against the v-sized scale
+        denom = max(np.linalg.norm(ref), scale_ref.get((k[len(prefix) + 1:], field), 0.0), 1e-300)
+        errs[k] = float(np.linalg.norm(v - ref) / denom)
+    return errs
+
+
+def scales(fx, prefix):
+    """Per-summary scales: w is measured against max(|w|, |v|), r against max(|r|, |q|) -- the MMS
+    has w = 0 exactly, so its discrete w is pure discretisation error (as in test_gpu_parity)."""
+    out = {}
+    for kind in ("_mean_sub", "_sub", "_proj"):
+        for fam, other in (("w", "v"), ("r", "q"), ("v", "v"), ("q", "q")):
+            key = f"{prefix}{other}{kind}"
+            if key in fx:
+                out[(kind, fam)] = float(np.linalg.norm(fx[key]))
+    return out
+
+
+CASES = ["C2", "C3s1", "C3s0.1", "C3s0.01", "C4d0.01", "C4d0.1", "C3tiny", "C4tiny"]
+
+
+@pytest.mark.parametrize("case", CASES)
+def test_baseline_config_matches_reference(case):
+    path = G.fixture_path(case)
+    if not os.path.exists(path):
+        pytest.skip(f"fixture {os.path.basename(path)} not generated")
+    fx = np.load(path)
+    disc, cfg, prob = build(case)
+    steps = int(fx["steps"])
+    snaps = tuple(int(s) for s in fx["snaps"])
+    report, final, snap = P.run(cfg, prob, snapshot_steps=snaps)
+    assert report.num_steps == steps
+    states = dict(snap)
+    states[steps] = final
+    for k, st in states.items():
+        prefix = f"s{k}_"
+        errs = compare_state(fx, prefix, st, scales(fx, prefix))
+        for name, e in errs.items():
+            tol = TOL_VEL if name[len(prefix)] in "vw" else TOL_PRES
+            assert e < tol, (case, name, e)
+    # full-field quadratic forms, every step
+    assert rel(report.energy, fx["energy"]) < TOL_VEL
+    for k, ref in (("member_l2v_sq", "l2v"), ("member_l2w_sq", "l2w"), ("member_gradv_sq", "gradv"),
+                   ("member_gradw_sq", "gradw")):
+        scale = max(np.linalg.norm(fx[ref]), np.linalg.norm(fx["l2v" if "l2" in ref else "gradv"]))
+        assert np.linalg.norm(getattr(report, k) - fx[ref]) < TOL_VEL * scale, (case, k)
+    assert np.all(report.residuals[1:] <= 1e-11)
+
+
+@pytest.mark.parametrize("case,over", [("C3", dict(steps=12)), ("C4", dict(steps=20))])
+def test_consecutive_runs_bitwise_identical(case, over):
+    """The default (deterministic) preconditioner renewal: two runs of the same full-size config on
+    fresh engines rebuild at the same steps and give identical bits."""
+    from paper_2108_05110_b200 import stepper as ST
+    out = []
+    for _ in range(2):
+        disc, cfg, prob = P.build_case(case, **over)
+        rep, fin, _ = P.run(cfg, prob)
+        eng = ST.get_engine(disc, cfg)
+        out.append((fin.v.copy(), fin.w.copy(), fin.q.copy(), rep.energy.copy(), rep.residuals.copy(),
+                    eng.n_factor))
+        del eng, disc, prob, fin
+    a, b = out
+    assert a[5] == b[5]
+    for x, y in zip(a[:5], b[:5]):
+        assert np.array_equal(x, y)

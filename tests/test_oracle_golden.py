@@ -4,6 +4,9 @@ Fixtures in tests/golden/reference_golden.npz were produced by the unmodified
 reference (tests/golden/make_golden.py).  These tests run on CPU only.
 """
 
+import os
+import sys
+
 import numpy as np
 import pytest
 
@@ -106,3 +109,50 @@ def test_run_th_baseline(golden, prefix, n, steps):
     e = np.array([r["energy"] for r in recs])
     assert rel(e, golden[prefix + "run_energy"]) < 1e-12
     assert np.all(res < 1e-12)
+
+
+# ----------------------------------------------------------------------
+# the BASELINE problem set-ups (C3 cavity, C4 do-nothing channel) against the
+# real reference: tiny twins of tests/golden/make_golden_large.py's cases
+# ----------------------------------------------------------------------
+
+
+@pytest.mark.parametrize("case,name,over", [
+    ("C3tiny", "C3", dict(n=6, J=4, dt=0.01, steps=2, coupling=0.1)),
+    ("C4tiny", "C4", dict(k=1, J=3, dt=0.02, steps=2, delta=0.1, length=8.0)),
+])
+def test_case_setup_matches_reference_variant(case, name, over):
+    """build_case's C3/C4 problems run through the oracle reproduce the reference run of the same
+    configuration (C4: the reference with the do-nothing outflow variant wrapped around it -- no pin,
+    no mean-zeroing, Dirichlet on WALL+INLET) to round-off."""
+    sys.path.insert(0, os.path.join(os.path.dirname(__file__), "golden"))
+    import make_golden_large as G
+    from paper_2108_05110_b200.problems import build_case
+    fx = np.load(G.fixture_path(case))
+    disc, cfg, prob = build_case(name, **over)
+    st, recs, _, res = O.run(cfg, disc, prob.initial_v, prob.initial_w, prob.forcing, prob.boundary)
+    got = G.summarize("s2_", st.v, st.w, st.q, st.r)
+    assert set(got) == {k for k in fx.files if k.startswith("s2_")}
+    for k, v in got.items():
+        assert np.linalg.norm(v - fx[k]) <= 1e-12 * max(np.linalg.norm(fx[k]), 1e-300), k
+    assert np.allclose([r["energy"] for r in recs], fx["energy"], rtol=1e-13, atol=0)
+
+
+def test_do_nothing_channel_step_matches_dense_solve():
+    """The no-pin / do-nothing branch of the oracle (`oracle/ensmhd_oracle.py` saddle_matrix with
+    pin_pressure=False): the saddle system is nonsingular (the outflow fixes the pressure level) and
+    SuperLU's block solve equals a dense LU solve, per member."""
+    from paper_2108_05110_b200.problems import build_case
+    disc, cfg, prob = build_case("C4", k=1, J=3, dt=0.02, steps=1, delta=0.1, length=8.0)
+    assert not disc.pin_pressure
+    v, w = np.asarray(prob.initial_v), np.asarray(prob.initial_w)
+    bv, bw = prob.boundary.values(cfg.dt, disc, cfg)
+    for kind, bvals in (("v", bv), ("w", bw)):
+        mat = O.shared_matrix(kind, v, w, cfg, disc)
+        rhs = O.rhs_block(kind, v, w, None, bvals, cfg, disc)
+        dense = mat.toarray()
+        assert np.linalg.cond(dense) < 1e12
+        x_dense = np.linalg.solve(dense, rhs)
+        x = O.solve_block(mat, rhs)
+        assert np.linalg.norm(x - x_dense) <= 1e-11 * np.linalg.norm(x_dense)
+        assert O.relative_residual(mat, x, rhs) < 1e-13
