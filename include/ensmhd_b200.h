@@ -124,58 +124,6 @@ typedef struct {
     int64_t n_slot;             /* split-K partial slots (64 rows x J each)          */
 } ens_plan_desc;
 
-/* Row blocking of the saddle SpMM (optional, built once per mesh and J):
- * rows are grouped in blocks of consecutive internal nodes / pressure rows; the
- * unique neighbour rows of a block are staged once in shared memory and the
- * CSR column indices are pre-remapped to local slots. */
-typedef struct {
-    int32_t bn, bp;             /* nodes per velocity block, pressure rows per pressure block */
-    int32_t nvb, nqb;           /* block counts */
-    int64_t smem_vel, smem_pres;/* dynamic shared memory (bytes) per CTA */
-    const int32_t* a_lcol;      /* nnz_s: local slot of each A_s column in its row's block */
-    const int32_t* bt_lcol;     /* B^T pairs: local pressure slot */
-    const int32_t* b_lcol;      /* B pairs: local node slot */
-    const int32_t* vb_off;      /* nvb+1 */
-    const int32_t* vb_nodes;    /* staged velocity node rows per velocity block */
-    const int32_t* pb_off;      /* nvb+1 */
-    const int32_t* pb_rows;     /* staged pressure rows (0-based) per velocity block */
-    const int32_t* qb_off;      /* nqb+1 */
-    const int32_t* qb_nodes;    /* staged velocity node rows per pressure block */
-    const int32_t* vb_row;      /* nvb+1: first node of each velocity block (variable-size blocks) */
-    const int32_t* qb_row;      /* nqb+1: first pressure row of each pressure block */
-} ens_spmm_blocks;
-
-/* Tile-staged SpMM (optional, built once per mesh and J by spmm_tiles.py):
- * tiles of consecutive velocity nodes / pressure rows, each staged into one
- * shared-memory stage by bulk copies (records: int64 source byte offset,
- * int32 destination byte offset, int32 bytes | kind << 24) and consumed from
- * there; see csrc/ens_spmm_tiles.cu.  Arrays are device pointers owned by the caller. */
-typedef struct {
-    const void* tiles;          /* ntiles x 16 int32 descriptors */
-    const void* recs;           /* copy records (16 bytes each)  */
-    const int32_t* lcol_a;      /* nnz_s: stage slot of each A_s column (its tile's node list) */
-    const int32_t* lcol_bt;     /* B^T pairs: stage slot of the pressure row */
-    const int32_t* lcol_b;      /* B pairs: stage slot of the node */
-    int32_t ntiles, nrec;
-    int32_t stage_bytes;        /* bytes per pipeline stage (16-byte multiple) */
-    int32_t nstage;             /* pipeline depth (1..4) */
-    int32_t grid;               /* persistent CTAs (one per SM) */
-    int32_t pad;
-} ens_spmm_tiles;
-
-/* Row-pair SpMM (optional, built once per mesh by spmm_tiles.row_pairs): velocity rows
- * 2p, 2p+1 processed together over the sorted union of their column lists; per union
- * entry the CSR slot of each row or -1 (int32 pairs).  Device pointers owned by the caller. */
-typedef struct {
-    const int32_t* a_ptr;       /* npairs+1: union ranges over the A_s pattern */
-    const int32_t* a_col;       /* union column (node) */
-    const int32_t* a_slot;      /* 2 per entry: CSR slot of row 2p / 2p+1, or -1 */
-    const int32_t* t_ptr;       /* npairs+1: union ranges over the B^T pairs */
-    const int32_t* t_col;       /* union pressure row */
-    const int32_t* t_slot;      /* 2 per entry: B^T pair index of row 2p / 2p+1, or -1 */
-    int64_t npairs;
-} ens_spmm_pairs;
-
 /* Problem data: value_j = sum_k coef[k*J + j] * basis[k*rows + row] (+ dense). */
 typedef struct {
     int32_t K;                  /* number of basis vectors (0 allowed)   */
@@ -197,12 +145,6 @@ int  ens_workspace_bytes(const ens_ctx* ctx, int64_t* bytes);
 /* Panel inverses with in-panel partial pivoting (1) or diagonal pivots (0, default;
  * the symbolic ordering guarantees nonsingular leading blocks in exact arithmetic). */
 int  ens_set_pivoting(ens_ctx* ctx, int on);
-/* Install the SpMM row blocking (arrays are device pointers owned by the caller). */
-int  ens_set_spmm_blocks(ens_ctx* ctx, const ens_spmm_blocks* blocks);
-/* Install (or, with NULL, remove) the row-pair SpMM (even J <= 64; used when no tile staging is set). */
-int  ens_set_spmm_pairs(ens_ctx* ctx, const ens_spmm_pairs* pairs);
-/* Install (or, with NULL, remove) the tile-staged SpMM; takes precedence over the row blocking. */
-int  ens_set_spmm_tiles(ens_ctx* ctx, const ens_spmm_tiles* tiles);
 
 /* y = a x + b y over one iterate block set (2 x n_total x J); used for the
  * extrapolated FGMRES initial iterate 2 x^n - x^{n-1}. */

@@ -48,29 +48,13 @@ class PlanDesc(C.Structure):
     ]
 
 
-class SpmmBlocks(C.Structure):
-    _fields_ = [("bn", I32), ("bp", I32), ("nvb", I32), ("nqb", I32), ("smem_vel", I64), ("smem_pres", I64),
-                ("a_lcol", P), ("bt_lcol", P), ("b_lcol", P), ("vb_off", P), ("vb_nodes", P), ("pb_off", P),
-                ("pb_rows", P), ("qb_off", P), ("qb_nodes", P), ("vb_row", P), ("qb_row", P)]
-
-
-class SpmmTiles(C.Structure):
-    _fields_ = [("tiles", P), ("recs", P), ("lcol_a", P), ("lcol_bt", P), ("lcol_b", P), ("ntiles", I32),
-                ("nrec", I32), ("stage_bytes", I32), ("nstage", I32), ("grid", I32), ("pad", I32)]
-
-
-class SpmmPairs(C.Structure):
-    _fields_ = [("a_ptr", P), ("a_col", P), ("a_slot", P), ("t_ptr", P), ("t_col", P), ("t_slot", P),
-                ("npairs", I64)]
-
-
 class DataDesc(C.Structure):
     _fields_ = [("K", I32), ("pad", I32), ("rows", I64), ("basis", P), ("coef", P), ("dense", P)]
 
 
 SYMBOLS = [
     "ens_abi_version", "ens_last_error", "ens_kernel_launches", "ens_create", "ens_set_pivoting",
-    "ens_set_spmm_blocks", "ens_set_spmm_tiles", "ens_set_spmm_pairs", "ens_destroy", "ens_workspace_bytes",
+    "ens_destroy", "ens_workspace_bytes",
     "ens_lincomb", "ens_member_sums", "ens_rhs", "ens_member_pass", "ens_rhs_fused", "ens_apply_bc", "ens_assemble", "ens_factor",
     "ens_solve", "ens_solve_begin", "ens_solve_finish", "ens_spmm", "ens_precond_apply", "ens_epilogue", "ens_diagnostics",
 ]
@@ -95,9 +79,6 @@ def load(path: str = LIB_PATH):
     lib.ens_destroy.restype = None
     lib.ens_workspace_bytes.argtypes = [P, C.POINTER(I64)]
     lib.ens_set_pivoting.argtypes = [P, C.c_int]
-    lib.ens_set_spmm_blocks.argtypes = [P, C.POINTER(SpmmBlocks)]
-    lib.ens_set_spmm_tiles.argtypes = [P, C.POINTER(SpmmTiles)]
-    lib.ens_set_spmm_pairs.argtypes = [P, C.POINTER(SpmmPairs)]
     lib.ens_member_sums.argtypes = [P, P, P, P]
     lib.ens_lincomb.argtypes = [P, P, F64, P, F64, P]
     lib.ens_rhs.argtypes = [P, P, P, P, F64, C.POINTER(DataDesc), P]

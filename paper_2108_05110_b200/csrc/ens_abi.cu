@@ -125,59 +125,8 @@ void ens_destroy(ens_ctx* c) {
     cudaFree(c->ec);
     cudaFree(c->nrm_part);
     cudaFree(c->diag_part);
-    df_free(c);
     cudaFree(c->el);
     delete c;
-}
-
-int ens_set_spmm_blocks(ens_ctx* c, const ens_spmm_blocks* b) {
-    if (!c) return ENS_EINVAL;
-    if (!b) {
-        c->use_blocked = 0;
-        return ENS_OK;
-    }
-    if (b->smem_vel > 200 * 1024 || b->smem_pres > 200 * 1024 || 2 * c->J > 256) {
-        ens_set_error("SpMM blocks need too much shared memory", __FILE__, __LINE__);
-        return ENS_EINVAL;
-    }
-    c->blk = *b;
-    const int rc = spmm_blocked_setup(c);
-    if (rc != ENS_OK) return rc;
-    c->use_blocked = 1;
-    return ENS_OK;
-}
-
-int ens_set_spmm_pairs(ens_ctx* c, const ens_spmm_pairs* p) {
-    if (!c) return ENS_EINVAL;
-    if (!p) {
-        c->use_pairs = 0;
-        return ENS_OK;
-    }
-    if ((c->J & 1) || c->J > 64 || p->npairs != ((int64_t)c->m.ns + 1) / 2) {
-        ens_set_error("SpMM row pairs: need even J <= 64 and (ns + 1) / 2 pairs", __FILE__, __LINE__);
-        return ENS_EINVAL;
-    }
-    c->pairs = *p;
-    c->use_pairs = 1;
-    return ENS_OK;
-}
-
-int ens_set_spmm_tiles(ens_ctx* c, const ens_spmm_tiles* t) {
-    if (!c) return ENS_EINVAL;
-    if (!t) {
-        c->use_tiles = 0;
-        return ENS_OK;
-    }
-    if ((c->J & 1) || c->J > 64 || t->nstage < 1 || t->nstage > 4 || (t->stage_bytes & 15) ||
-        (int64_t)t->stage_bytes * t->nstage > 220 * 1024 || t->ntiles < 1 || t->grid < 1) {
-        ens_set_error("SpMM tiles: need even J <= 64 and <= 220 KB of stages", __FILE__, __LINE__);
-        return ENS_EINVAL;
-    }
-    c->tiles = *t;
-    const int rc = spmm_tiles_setup(c);
-    if (rc != ENS_OK) return rc;
-    c->use_tiles = 1;
-    return ENS_OK;
 }
 
 int ens_set_pivoting(ens_ctx* c, int on) {

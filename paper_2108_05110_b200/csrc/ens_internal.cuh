@@ -67,9 +67,6 @@ struct ens_ctx {
     double* partial = nullptr;     // split-K partial products of the solve GEMMs
     int* ticket = nullptr;         // split-K arrival counters (last CTA reduces)
     int4* sitem = nullptr;         // solve work items with their front's geometry (3 x int4 per item)
-    void* df = nullptr;            // dataflow solve plan (ens_mfsolve_df.cu)
-    std::vector<uint8_t> fwd_multi;   // per level: forward GEMM runs the multi-unit kernel
-    int sg_slots = 0;              // resident CTAs of the multi-unit kernel (all SMs)
     double* nrm_part = nullptr;    // fused residual-norm partials of the SpMM
     double* diag_part = nullptr;   // per-block partials of the diagnostics (launch_diagnostics)
     size_t diag_part_n = 0;
@@ -83,13 +80,6 @@ struct ens_ctx {
     void* g_factor = nullptr;      // cudaGraphExec_t
     const double* g_factor_key = nullptr;
     int diag_pivot = 0;            // 1: in-panel partial pivoting in DIAG (k_diag), 0: k_diag_np
-    int use_mma = 1;               // DMMA (fp64 tensor core) panel kernels
-    ens_spmm_blocks blk{};         // SpMM row blocking (shared-memory staged neighbour rows)
-    int use_blocked = 0;
-    ens_spmm_tiles tiles{};        // tile-staged SpMM (bulk-copied stages, ens_spmm_tiles.cu)
-    int use_tiles = 0;
-    ens_spmm_pairs pairs{};        // row-pair SpMM (ens_spmm.cu)
-    int use_pairs = 0;
     int spmm_wide = -1;            // wide-member SpMM variant (ENS_SPMM_WIDE, read on first use)
     int g_factor_pivot = 0;
     int64_t g_factor_kernels = 0;
@@ -108,13 +98,6 @@ int launch_assemble(ens_ctx* c, cudaStream_t s, const double* base, const double
                     double two_mu_dt, double* as_vals);
 int launch_spmm(ens_ctx* c, cudaStream_t s, const double* as_vals, const double* x, const double* b, double* y,
                 int mode);
-int launch_spmm_blocked(ens_ctx* c, cudaStream_t s, const double* as_vals, const double* x, const double* b,
-                        double* y, int mode);
-int spmm_blocked_setup(ens_ctx* c);
-int spmm_tiles_setup(ens_ctx* c);
-bool spmm_tiles_usable(const ens_ctx* c, const double* x, const double* b, const double* y);
-int launch_spmm_tiles(ens_ctx* c, cudaStream_t s, const double* as_vals, const double* x, const double* b, double* y,
-                      int mode);
 bool spmm_resnorm_ok(const ens_ctx* c);
 int launch_spmm_resnorm(ens_ctx* c, cudaStream_t s, const double* as_vals, const double* x, const double* b,
                         double* y, double* bn2, double* rn2);
@@ -132,11 +115,6 @@ int launch_axpy_norm(ens_ctx* c, cudaStream_t s, double* W, const double* V, int
 int mf_factor(ens_ctx* c, cudaStream_t s, const double* as_vals, int32_t* n_pert);
 int mf_solve(ens_ctx* c, cudaStream_t s, const double* r, double* z);
 int mf_setup(ens_ctx* c);
-bool df_enabled(const ens_ctx* c);
-int df_build(ens_ctx* c, cudaStream_t s);
-void df_free(ens_ctx* c);
-int df_solve_launches(ens_ctx* c, cudaStream_t s, const void* io, int64_t* nlaunch);
-int df_error(ens_ctx* c);
 
 // ---- Krylov (ens_krylov.cu) ----
 int gmres_solve(ens_ctx* c, cudaStream_t s, const double* as_vals, const double* rhs, double* x, double rtol,

@@ -326,106 +326,6 @@ __global__ void __launch_bounds__(256, 3) k_diag_np(MfDev d, int item0, double* 
         }
 }
 
-// ---------------------------------------------------------------------------
-// register-tiled 64x64 (rows) x 64 (cols) GEMM piece from shared memory:
-// acc[i][j] += sum_t A[ty+16i][t] * B[t][tx+16j]
-// ---------------------------------------------------------------------------
-#define LDA (ENS_TILE + 1)
-
-__device__ __forceinline__ void tile_mma(const double* __restrict__ As, const double* __restrict__ Bs, int K,
-                                         double acc[4][4], int tx, int ty) {
-    // As: row-major [64][LDA] indexed As[r*LDA + t]; Bs: [K][64]
-    for (int t = 0; t < K; ++t) {
-        double av[4], bv[4];
-#pragma unroll
-        for (int i = 0; i < 4; ++i) av[i] = As[(ty + 16 * i) * LDA + t];
-#pragma unroll
-        for (int j = 0; j < 4; ++j) bv[j] = Bs[t * ENS_TILE + tx + 16 * j];
-#pragma unroll
-        for (int i = 0; i < 4; ++i)
-#pragma unroll
-            for (int j = 0; j < 4; ++j) acc[i][j] = fma(av[i], bv[j], acc[i][j]);
-    }
-}
-
-// HPANEL: F[P, Q-tile] <- D^-1 F[P, Q-tile]   (D^-1 = -F[P,P])
-__global__ void __launch_bounds__(256) k_hpanel(MfDev d, int item0, double* __restrict__ F) {
-    extern __shared__ double sm[];
-    const int* it = d.work + 4LL * (item0 + blockIdx.x);
-    const int f = it[0], a = it[1], c0 = it[2];
-    const int mat = blockIdx.y;
-    const int m = d.m[f];
-    const int pw = min(ENS_PW, d.k[f] - a);
-    const int t = m - pw;
-    const int nc = min(ENS_TILE, t - c0);
-    double* Ds = sm;                       // [64][LDA]  (D^-1)
-    double* Rs = sm + ENS_PW * LDA;        // [pw][64]
-    double* base = F + (int64_t)mat * d.storage + d.off[f];
-    for (int e = threadIdx.x; e < ENS_PW * ENS_PW; e += blockDim.x) {
-        const int r = e / ENS_PW, cc = e % ENS_PW;
-        Ds[r * LDA + cc] = (r < pw && cc < pw) ? -base[(int64_t)(a + r) * m + a + cc] : 0.0;
-    }
-    for (int e = threadIdx.x; e < pw * ENS_TILE; e += blockDim.x) {
-        const int r = e / ENS_TILE, cc = e % ENS_TILE;
-        Rs[e] = cc < nc ? base[(int64_t)(a + r) * m + outside(c0 + cc, a, pw)] : 0.0;
-    }
-    __syncthreads();
-    const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
-    double acc[4][4] = {};
-    tile_mma(Ds, Rs, pw, acc, tx, ty);
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-        const int r = ty + 16 * i;
-        if (r >= pw) continue;
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-            const int cc = tx + 16 * j;
-            if (cc < nc) base[(int64_t)(a + r) * m + outside(c0 + cc, a, pw)] = acc[i][j];
-        }
-    }
-}
-
-// UPDATE: F[Q-rows, Q-cols] -= F[Q-rows, P] F[P, Q-cols]
-__global__ void __launch_bounds__(256) k_update(MfDev d, int item0, double* __restrict__ F) {
-    extern __shared__ double sm[];
-    const int* it = d.work + 4LL * (item0 + blockIdx.x);
-    const int f = it[0], a = it[1], r0 = it[2], c0 = it[3];
-    const int mat = blockIdx.y;
-    const int m = d.m[f];
-    const int pw = min(ENS_PW, d.k[f] - a);
-    const int t = m - pw;
-    const int nr = min(ENS_TILE, t - r0), nc = min(ENS_TILE, t - c0);
-    double* Cs = sm;                       // [64][LDA]
-    double* Hs = sm + ENS_TILE * LDA;      // [pw][64]
-    double* base = F + (int64_t)mat * d.storage + d.off[f];
-    for (int e = threadIdx.x; e < ENS_TILE * pw; e += blockDim.x) {
-        const int r = e / pw, kk = e % pw;
-        Cs[r * LDA + kk] = r < nr ? base[(int64_t)outside(r0 + r, a, pw) * m + a + kk] : 0.0;
-    }
-    for (int e = threadIdx.x; e < pw * ENS_TILE; e += blockDim.x) {
-        const int kk = e / ENS_TILE, cc = e % ENS_TILE;
-        Hs[e] = cc < nc ? base[(int64_t)(a + kk) * m + outside(c0 + cc, a, pw)] : 0.0;
-    }
-    __syncthreads();
-    const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
-    double acc[4][4] = {};
-    tile_mma(Cs, Hs, pw, acc, tx, ty);
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-        const int r = ty + 16 * i;
-        if (r >= nr) continue;
-        double* row = base + (int64_t)outside(r0 + r, a, pw) * m;
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-            const int cc = tx + 16 * j;
-            if (cc < nc) {
-                const int col = outside(c0 + cc, a, pw);
-                row[col] -= acc[i][j];
-            }
-        }
-    }
-}
-
 // UPDATE on the fp64 tensor cores with one asynchronous staging round trip:
 // the output tile C (64 x 64, rows/cols outside the panel) is prefetched into the
 // accumulator fragments while A = F[Q-rows, P] and B = F[P, Q-cols] stream into
@@ -573,73 +473,15 @@ __global__ void __launch_bounds__(256, 2) k_panel2(MfDev d, int item0, double* _
 }
 
 
-static bool update2_enabled() {
-    const char* e = std::getenv("ENS_UPDATE_OLD");
-    return !(e && e[0] == '1');
-}
-
-// GPANEL: F[Q-tile, P] <- F[Q-tile, P] D^-1
-__global__ void __launch_bounds__(256) k_gpanel(MfDev d, int item0, double* __restrict__ F) {
-    extern __shared__ double sm[];
-    const int* it = d.work + 4LL * (item0 + blockIdx.x);
-    const int f = it[0], a = it[1], r0 = it[2];
-    const int mat = blockIdx.y;
-    const int m = d.m[f];
-    const int pw = min(ENS_PW, d.k[f] - a);
-    const int t = m - pw;
-    const int nr = min(ENS_TILE, t - r0);
-    double* Cs = sm;                       // [64][LDA]
-    double* Ds = sm + ENS_TILE * LDA;      // [pw][64]  (D^-1)
-    double* base = F + (int64_t)mat * d.storage + d.off[f];
-    for (int e = threadIdx.x; e < ENS_TILE * pw; e += blockDim.x) {
-        const int r = e / pw, kk = e % pw;
-        Cs[r * LDA + kk] = r < nr ? base[(int64_t)outside(r0 + r, a, pw) * m + a + kk] : 0.0;
-    }
-    for (int e = threadIdx.x; e < pw * ENS_TILE; e += blockDim.x) {
-        const int kk = e / ENS_TILE, cc = e % ENS_TILE;
-        Ds[e] = cc < pw ? -base[(int64_t)(a + kk) * m + a + cc] : 0.0;
-    }
-    __syncthreads();
-    const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
-    double acc[4][4] = {};
-    tile_mma(Cs, Ds, pw, acc, tx, ty);
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-        const int r = ty + 16 * i;
-        if (r >= nr) continue;
-        double* row = base + (int64_t)outside(r0 + r, a, pw) * m + a;
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-            const int cc = tx + 16 * j;
-            if (cc < pw) row[cc] = acc[i][j];
-        }
-    }
-}
-
 // ---------------------------------------------------------------------------
 // host drivers
 // ---------------------------------------------------------------------------
-static const size_t SM_HP = sizeof(double) * (ENS_PW * LDA + ENS_PW * ENS_TILE);
-static const size_t SM_UP = sizeof(double) * (ENS_TILE * LDA + ENS_PW * ENS_TILE);
-static const size_t SM_GP = sizeof(double) * (ENS_TILE * LDA + ENS_PW * ENS_TILE);
-
-int mf_mma_setup();
-void launch_update_mma(const MfDev& d, int off, int n, double* F, cudaStream_t s);
-void launch_hpanel_mma(const MfDev& d, int off, int n, double* F, cudaStream_t s);
-void launch_gpanel_mma(const MfDev& d, int off, int n, double* F, cudaStream_t s);
-
 int mf_setup(ens_ctx* c) {
-    ENS_CK(cudaFuncSetAttribute(k_hpanel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SM_HP));
-    ENS_CK(cudaFuncSetAttribute(k_update, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SM_UP));
+    (void)c;
     ENS_CK(cudaFuncSetAttribute(k_update2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SM_UP2));
     ENS_CK(cudaFuncSetAttribute(k_panel2<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SM_UP2));
     ENS_CK(cudaFuncSetAttribute(k_panel2<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SM_UP2));
-    ENS_CK(cudaFuncSetAttribute(k_gpanel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SM_GP));
-    const char* e = std::getenv("ENS_MMA");
-    // DMMA panel kernels measured slower than the DFMA ones at C2 (15.0 vs 10.4 ms
-    // per factorisation pair); opt-in with ENS_MMA=1 until that is understood
-    c->use_mma = (e && e[0] == '1');
-    return mf_mma_setup();
+    return ENS_OK;
 }
 
 static int mf_factor_launches(ens_ctx* c, cudaStream_t s, const double* as_vals, int64_t* nlaunch) {
@@ -686,28 +528,13 @@ static int mf_factor_launches(ens_ctx* c, cudaStream_t s, const double* as_vals,
                     k_diag_np<<<dim3(n, 2), 256, 0, s>>>(d, off, c->fronts, c->d_count);
                 break;
             case OP_HPANEL:
-                if (c->use_mma)
-                    launch_hpanel_mma(d, off, n, c->fronts, s);
-                else if (update2_enabled())
-                    k_panel2<true><<<dim3(n, 2), 256, SM_UP2, s>>>(d, off, c->fronts);
-                else
-                    k_hpanel<<<dim3(n, 2), 256, SM_HP, s>>>(d, off, c->fronts);
+                k_panel2<true><<<dim3(n, 2), 256, SM_UP2, s>>>(d, off, c->fronts);
                 break;
             case OP_UPDATE:
-                if (c->use_mma)
-                    launch_update_mma(d, off, n, c->fronts, s);
-                else if (update2_enabled())
-                    k_update2<<<dim3(n, 2), 256, SM_UP2, s>>>(d, off, c->fronts);
-                else
-                    k_update<<<dim3(n, 2), 256, SM_UP, s>>>(d, off, c->fronts);
+                k_update2<<<dim3(n, 2), 256, SM_UP2, s>>>(d, off, c->fronts);
                 break;
             case OP_GPANEL:
-                if (c->use_mma)
-                    launch_gpanel_mma(d, off, n, c->fronts, s);
-                else if (update2_enabled())
-                    k_panel2<false><<<dim3(n, 2), 256, SM_UP2, s>>>(d, off, c->fronts);
-                else
-                    k_gpanel<<<dim3(n, 2), 256, SM_GP, s>>>(d, off, c->fronts);
+                k_panel2<false><<<dim3(n, 2), 256, SM_UP2, s>>>(d, off, c->fronts);
                 break;
             default:
                 ens_set_error("bad factor op", __FILE__, __LINE__);

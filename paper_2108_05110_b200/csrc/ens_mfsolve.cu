@@ -53,13 +53,7 @@ __global__ void k_copy_cons_io(const int32_t* __restrict__ crow, int ncons, cons
     io->z[idx] = io->r[idx];
 }
 
-__device__ __forceinline__ void cp_async8(double* smem, const double* gmem, bool pred) {
-    const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
-    const int sz = pred ? 8 : 0;   // src-size 0 -> zero fill
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(s), "l"(gmem), "r"(sz));
-}
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
-__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::); }
 
 #define SG_R 64     // rows per CTA (= symbolic.SOLVE_ROWS)
 #define SG_C 32     // member columns per CTA
@@ -70,40 +64,7 @@ __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wai
 #define SG_KC 32    // inner chunk of the pipelined mainloop
 #endif
 #define SG_LDA 36   // A stage row stride (= 4 mod 16: conflict-free fragment reads)
-#define SG_STAGE (SG_R * SG_LDA + SG_KC * 36)   // doubles per pipeline stage (A + B)
 #define SG_T 256    // threads
-#define SG_LDB 36   // Bs row stride (= 4 mod 16)
-
-#ifdef SG_PROBE   // diagnostic build: per-CTA phase timestamps of sampled CTAs to stdout
-__device__ __forceinline__ unsigned long long gtime() {
-    unsigned long long t;
-    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
-    return t;
-}
-#define SG_T_(i) const unsigned long long tp##i = gtime()
-#define SG_PROBE_MAX (1 << 16)
-__device__ unsigned long long g_probe[SG_PROBE_MAX][8];
-__device__ unsigned int g_probe_n;
-extern "C" int ens_probe_dump(const char* path) {   // diagnostic build only
-    static unsigned long long h[SG_PROBE_MAX][8];
-    unsigned int n = 0;
-    cudaDeviceSynchronize();
-    cudaMemcpyFromSymbol(&n, g_probe_n, sizeof(n));
-    n = n < SG_PROBE_MAX ? n : SG_PROBE_MAX;
-    cudaMemcpyFromSymbol(h, g_probe, sizeof(unsigned long long) * 8 * n);
-    FILE* f = fopen(path, "w");
-    if (!f) return -1;
-    for (unsigned i = 0; i < n; ++i)
-        fprintf(f, "probe %llu %llu %llu %llu %llu %llu %llu %llu\n", h[i][0], h[i][1], h[i][2], h[i][3], h[i][4],
-                h[i][5], h[i][6], h[i][7]);
-    fclose(f);
-    unsigned int z = 0;
-    cudaMemcpyToSymbol(g_probe_n, &z, sizeof(z));
-    return (int)n;
-}
-#else
-#define SG_T_(i)
-#endif
 
 __device__ __forceinline__ void dmma8(double& d0, double& d1, double a, double b) {
     asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
@@ -244,7 +205,6 @@ __global__ void __launch_bounds__(SG_T, CW == 64 ? 2 : SG_MINB) k_sgemm(MfDev d,
                                                 const SolveIO* __restrict__ io, int64_t N, int J, int64_t nidx,
                                                 int bwd, int split_k, int nstage, double* __restrict__ partial,
                                                 int* __restrict__ ticket, int64_t nslot, int zbase) {
-    SG_T_(0);
     extern __shared__ double sm[];
     __shared__ int s_last;
     __shared__ int s_idx[SG_KMAX];
@@ -292,9 +252,6 @@ __global__ void __launch_bounds__(SG_T, CW == 64 ? 2 : SG_MINB) k_sgemm(MfDev d,
         asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(s), "l"(gp), "r"(pred ? 8 : 0));
     };
     auto issue_a = [&](int c, int st) {
-#ifdef SG_NOA
-        return;
-#endif
         const uint32_t dst = a_dst + 8u * (uint32_t)(st * STAGE);
         const bool kok = c * SG_KC + lane < kc;
         const double* src = a_src + c * SG_KC;
@@ -305,9 +262,6 @@ __global__ void __launch_bounds__(SG_T, CW == 64 ? 2 : SG_MINB) k_sgemm(MfDev d,
         }
     };
     auto issue_b = [&](int c, int st) {
-#ifdef SG_NOB
-        return;
-#endif
         const uint32_t dst = b_dst + 8u * (uint32_t)(st * STAGE);
 #pragma unroll
         for (int h = 0; h < CW / 32; ++h) {
@@ -346,7 +300,6 @@ __global__ void __launch_bounds__(SG_T, CW == 64 ? 2 : SG_MINB) k_sgemm(MfDev d,
     if (bwd)
         for (int t = tid; t < kc; t += SG_T) s_idx[t] = (kbeg + t >= k) ? d.idx[fo + kbeg + t] : 0;
     __syncthreads();
-    SG_T_(1);
     // (2) pipeline prologue: stages 0 .. nstage-2, one commit group each
     issue_b(0, 0);
     cp_async_commit();
@@ -357,7 +310,6 @@ __global__ void __launch_bounds__(SG_T, CW == 64 ? 2 : SG_MINB) k_sgemm(MfDev d,
         }
         cp_async_commit();
     }
-    SG_T_(2);
     // (3) mainloop
     double dacc[NB][2];
 #pragma unroll
@@ -397,22 +349,6 @@ __global__ void __launch_bounds__(SG_T, CW == 64 ? 2 : SG_MINB) k_sgemm(MfDev d,
         }
     }
     pdl_trigger();   // the next launch may start its prologue while this epilogue runs
-#ifdef SG_PROBE
-    __syncthreads();
-    SG_T_(3);
-#define SG_END(tag)                                                                                      \
-    if (tid == 0 && blockIdx.y == 0 && blockIdx.z == 0) {                                                \
-        const unsigned i_ = atomicAdd(&g_probe_n, 1u);                                                   \
-        if (i_ < SG_PROBE_MAX) {                                                                         \
-            unsigned long long* o_ = g_probe[i_];                                                        \
-            o_[0] = (unsigned long long)bwd * 1000000 + (unsigned long long)min(kc, 999) * 1000 + (tag);         \
-            o_[1] = blockIdx.x; o_[2] = kc; o_[3] = tp0; o_[4] = tp1 - tp0; o_[5] = tp2 - tp1;            \
-            o_[6] = tp3 - tp2; o_[7] = gtime() - tp3;                                                    \
-        }                                                                                                \
-    }
-#else
-#define SG_END(tag)
-#endif
     if (slot >= 0) {
         // split: publish the partial; the last CTA of the group sums the group's
         // partials in ks order (deterministic) and applies the epilogue
@@ -432,7 +368,6 @@ __global__ void __launch_bounds__(SG_T, CW == 64 ? 2 : SG_MINB) k_sgemm(MfDev d,
         if (tid == 0) s_last = (atomicAdd(ticket + tk, 1) == ns - 1);
         __syncthreads();
         if (!s_last) {
-            SG_END(1);
             return;
         }
         __threadfence();
@@ -463,136 +398,6 @@ __global__ void __launch_bounds__(SG_T, CW == 64 ? 2 : SG_MINB) k_sgemm(MfDev d,
             else
                 FRm[(fo + rbase + row) * J + j0 + col] = init[ct][e] - dacc[ct][e];
         }
-    SG_END(slot >= 0 ? 2 : 0);
-}
-
-// ---------------------------------------------------------------------------
-// Forward levels without split items (every item covers its front's whole pivot
-// range -- the lower tree levels): persistent CTAs walk units u = blockIdx.x,
-// +gridDim.x, ... (unit = item x system) and the 2-stage cp.async pipeline runs
-// straight across unit boundaries: the next unit's first chunk loads while the
-// current unit computes and stores.  Same arithmetic as k_sgemm (deterministic).
-// ---------------------------------------------------------------------------
-struct SgUnit {
-    const double* base;   // front entries of this system
-    double* fr;           // front vector rows of this system (FR + fo*J)
-    int m, k, hasch, rbase, nr, nch;
-};
-
-__device__ __forceinline__ SgUnit sg_unit(const int4* __restrict__ sitem, int item0, int nitem, int u,
-                                          const double* __restrict__ F, int64_t storage, double* __restrict__ FR,
-                                          int64_t nidx, int J) {
-    SgUnit g;
-    const int item = u >> 1, mat = u & 1;
-    const int4* rec = sitem + 3LL * (item0 + min(item, nitem - 1));
-    const int4 w0 = rec[0], w1 = rec[1], w2 = rec[2];
-    const int64_t off = (int64_t)(unsigned)w2.x | ((int64_t)w2.y << 32);
-    const int64_t fo = (int64_t)(unsigned)w2.z | ((int64_t)w2.w << 32);
-    g.m = w1.x;
-    g.k = w1.y;
-    g.hasch = w1.z;
-    g.base = F + (int64_t)mat * storage + off;
-    g.fr = FR + (int64_t)mat * nidx * J + fo * J;
-    g.rbase = g.k + w0.y;
-    g.nr = min(SG_R, g.m - g.rbase);
-    g.nch = (g.k + SG_KC - 1) / SG_KC;
-    return g;
-}
-
-template <int NCT>
-__global__ void __launch_bounds__(SG_T, SG_MINB) k_sgemm_fwd_multi(const int4* __restrict__ sitem, int item0,
-                                                                int nitem, const double* __restrict__ F,
-                                                                int64_t storage, double* __restrict__ FR, int J,
-                                                                int64_t nidx, int zbase) {
-    extern __shared__ double sm[];
-    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, g = lane >> 2, q = lane & 3;
-    const int j0 = (zbase + blockIdx.z) * SG_C;
-    const int jn = min(SG_C, J - j0);
-    const int nunit = 2 * nitem;
-    const int row = 8 * warp + g;
-    int u = blockIdx.x;
-    if (u >= nunit) return;
-    SgUnit cu = sg_unit(sitem, item0, nitem, u, F, storage, FR, nidx, J);
-    SgUnit nu = sg_unit(sitem, item0, nitem, u + gridDim.x, F, storage, FR, nidx, J);
-    auto issue = [&](const SgUnit& w, int c, int buf) {
-        double* As = sm + buf * SG_STAGE;
-        double* Bsb = As + SG_R * SG_LDA;
-#pragma unroll
-        for (int i = 0; i < SG_R * SG_KC / SG_T; ++i) {
-            const int e = tid + SG_T * i, r = e / SG_KC, kk = e % SG_KC, kg = c * SG_KC + kk;
-            const bool ok = r < w.nr && kg < w.k;
-            cp_async8(&As[r * SG_LDA + kk], ok ? w.base + (int64_t)(w.rbase + r) * w.m + kg : w.base, ok);
-        }
-#pragma unroll
-        for (int i = 0; i < SG_KC * SG_C / SG_T; ++i) {
-            const int e = tid + SG_T * i, kk = e / SG_C, j = e % SG_C, kg = c * SG_KC + kk;
-            const bool ok = j < jn && kg < w.k;
-            cp_async8(&Bsb[kk * SG_LDB + j], ok ? w.fr + (int64_t)kg * J + j0 + j : w.base, ok);
-        }
-    };
-    // pipeline over the CTA's chunk stream: (unit, chunk) pairs in order
-    int buf = 0;
-    issue(cu, 0, 0);
-    cp_async_commit();
-    int c = 0;
-    double dacc[4][2] = {{0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}};
-    for (;;) {
-        cp_async_wait_n(0);
-        __syncthreads();
-        // issue the next chunk of the stream (possibly the next unit's first)
-        const bool last_of_unit = c + 1 >= cu.nch;
-        const bool has_next_unit = u + (int)gridDim.x < nunit;
-        if (!last_of_unit) issue(cu, c + 1, buf ^ 1);
-        else if (has_next_unit) issue(nu, 0, buf ^ 1);
-        cp_async_commit();
-        const double* As = sm + buf * SG_STAGE;
-        const double* ap = As + row * SG_LDA + q;
-        const double* bp = As + SG_R * SG_LDA + q * SG_LDB + g;
-        const int ksteps = (min(SG_KC, cu.k - c * SG_KC) + 3) >> 2;
-        if (8 * warp < cu.nr) {
-            if (ksteps == SG_KC / 4) {
-#pragma unroll
-                for (int uu = 0; uu < SG_KC / 4; ++uu) {
-                    const double av = ap[4 * uu];
-#pragma unroll
-                    for (int ct = 0; ct < NCT; ++ct) dmma8(dacc[ct][0], dacc[ct][1], av, bp[4 * uu * SG_LDB + 8 * ct]);
-                }
-            } else {
-#pragma unroll 2
-                for (int uu = 0; uu < ksteps; ++uu) {
-                    const double av = ap[4 * uu];
-#pragma unroll
-                    for (int ct = 0; ct < NCT; ++ct) dmma8(dacc[ct][0], dacc[ct][1], av, bp[4 * uu * SG_LDB + 8 * ct]);
-                }
-            }
-        }
-        buf ^= 1;
-        if (!last_of_unit) {
-            ++c;
-            continue;
-        }
-        // unit done: fr[C rows] = children rows (assembled by k_finit, leaf fronts: 0) - A B
-        if (row < cu.nr) {
-            double* pc = cu.fr + (int64_t)(cu.rbase + row) * J + j0;
-#pragma unroll
-            for (int ct = 0; ct < NCT; ++ct)
-#pragma unroll
-                for (int e = 0; e < 2; ++e) {
-                    const int col = 8 * ct + 2 * q + e;
-                    if (col >= jn) continue;
-                    const double init = cu.hasch ? pc[col] : 0.0;
-                    pc[col] = init - dacc[ct][e];
-                }
-        }
-#pragma unroll
-        for (int ct = 0; ct < 4; ++ct) dacc[ct][0] = dacc[ct][1] = 0.0;
-        if (!has_next_unit) break;
-        u += gridDim.x;
-        cu = nu;
-        nu = sg_unit(sitem, item0, nitem, u + gridDim.x, F, storage, FR, nidx, J);
-        c = 0;
-    }
-    cp_async_wait_n(0);
 }
 
 #define SG_MAXST 5
@@ -618,11 +423,6 @@ static int sg_stages(int kmax) {
     }
     if (env > 0) return std::min(env, std::max(2, (kmax + SG_KC - 1) / SG_KC));
     return 2;   // measured: a shallow pipeline with more resident CTAs wins (stage sweep, profiles/)
-}
-
-static bool multi_enabled() {   // opt-in: measured no faster than one CTA per item at C2 (831 vs 834 us)
-    const char* e = std::getenv("ENS_SOLVE_MULTI");
-    return e && e[0] == '1';
 }
 
 static bool capturing(cudaStream_t s) {
@@ -688,11 +488,6 @@ static int mf_solve_launches(ens_ctx* c, cudaStream_t s, SolveIO* io, int64_t* n
         lab.push_back(std::string(tag) + " n=" + std::to_string(a) + " kmax=" + std::to_string(b2));
     };
     mark("start", 0, 0);
-    if (df_enabled(c)) {   // dataflow path: one persistent launch per sweep
-        const int rc = df_solve_launches(c, s, io, &cnt);
-        if (rc != ENS_OK) return rc;
-        mark("dataflow fwd+bwd", 2, 0);
-    } else
     for (const std::vector<int64_t>* sched : {&c->sched_fwd, &c->sched_bwd}) {
         const int64_t nrow = (int64_t)sched->size() / 5;
         for (int64_t i = 0; i < nrow; ++i) {
@@ -718,33 +513,6 @@ static int mf_solve_launches(ens_ctx* c, cudaStream_t s, SolveIO* io, int64_t* n
                 }
             }
             if (n == 0 || kmax == 0) continue;
-            if (op == SOP_FGEMM && L < (int)c->fwd_multi.size() && c->fwd_multi[L] && multi_enabled()) {
-                const int zfull = J / SG_C, rem = J - zfull * SG_C;
-                const unsigned units = (unsigned)(2 * n);
-                const unsigned g = std::min<unsigned>(units, (unsigned)c->sg_slots);
-                for (int rep = 0; rep < (timing ? trep : 1); ++rep) {
-#define SGM(NC, ZN, Z0)                                                                                              \
-    k_sgemm_fwd_multi<NC><<<dim3(g, 1, ZN), SG_T, sg_smem(2), s>>>(c->sitem, off, n, c->fronts, c->p.front_storage, \
-                                                                   c->frvec, J, nidx, Z0)
-                    if (zfull > 0) {
-                        SGM(4, (unsigned)zfull, 0);
-                        ENS_CKL();
-                        if (rep == 0) ++cnt;
-                    }
-                    if (rem > 0) {
-                        const int nct = (rem + 7) / 8;
-                        if (nct == 1) SGM(1, 1, zfull);
-                        else if (nct == 2) SGM(2, 1, zfull);
-                        else if (nct == 3) SGM(3, 1, zfull);
-                        else SGM(4, 1, zfull);
-                        ENS_CKL();
-                        if (rep == 0) ++cnt;
-                    }
-#undef SGM
-                }
-                mark("fwd-multi", n, kmax);
-                continue;
-            }
             const int nst = sg_stages(kmax);
             const bool wide = sg_wide(J);
             for (int rep = 0; rep < (timing ? trep : 1); ++rep) {   // launches are idempotent
@@ -864,32 +632,6 @@ int mf_solve(ens_ctx* c, cudaStream_t s, const double* r, double* z) {
         ENS_CK(cudaStreamSynchronize(s));
         cudaFree(d_hasch);
         c->ws_bytes += pbytes + tbytes + sizeof(int4) * 3 * (size_t)nw + sizeof(int32_t) * (size_t)nidx;
-        {   // forward levels without split or pivot-only items run the multi-unit kernel
-            std::vector<int32_t> work((size_t)c->p.n_work * 4);
-            if (c->p.n_work > 0)
-                ENS_CK(cudaMemcpy(work.data(), c->p.work, sizeof(int32_t) * work.size(), cudaMemcpyDeviceToHost));
-            const int nlev = (int)c->level_front_off.size() - 1;
-            c->fwd_multi.assign((size_t)nlev, 0);
-            for (size_t i = 0; i + 5 <= c->sched_fwd.size(); i += 5) {
-                const int L = (int)c->sched_fwd[i + 1], o = (int)c->sched_fwd[i + 2], n = (int)c->sched_fwd[i + 3];
-                bool ok = n > 0;
-                for (int u = 0; u < n && ok; ++u) ok = work[4 * (o + u) + 1] >= 0 && work[4 * (o + u) + 3] < 0;
-                if (L >= 0 && L < nlev) c->fwd_multi[L] = ok ? 1 : 0;
-            }
-            int occ = 0, dev = 0, sms = 0;
-            ENS_CK(cudaFuncSetAttribute(k_sgemm_fwd_multi<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sg_smem(2)));
-            ENS_CK(cudaFuncSetAttribute(k_sgemm_fwd_multi<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sg_smem(2)));
-            ENS_CK(cudaFuncSetAttribute(k_sgemm_fwd_multi<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sg_smem(2)));
-            ENS_CK(cudaFuncSetAttribute(k_sgemm_fwd_multi<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sg_smem(2)));
-            ENS_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_sgemm_fwd_multi<3>, SG_T, sg_smem(2)));
-            cudaGetDevice(&dev);
-            cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-            c->sg_slots = std::max(1, occ) * sms;
-        }
-        if (df_enabled(c)) {   // task lists are built before any graph capture
-            const int rc = df_build(c, s);
-            if (rc != ENS_OK) return rc;
-        }
     }
     SolveIO* io = (SolveIO*)c->solve_io;
     k_set_io<<<1, 1, 0, s>>>(io, r, z);

@@ -566,25 +566,6 @@ __device__ __forceinline__ void spmm_pair_body(const int32_t* __restrict__ pp, c
     }
 }
 
-// row pairs + pressure rows in one launch (blocks [0, nbv) take velocity row pairs)
-__global__ void __launch_bounds__(256) k_spmm_both_pairs(const int32_t* __restrict__ pp,
-                                                         const int32_t* __restrict__ pc, const int2* __restrict__ ps,
-                                                         const double* __restrict__ A, int nnz,
-                                                         const int32_t* __restrict__ tp,
-                                                         const int32_t* __restrict__ tc, const int2* __restrict__ ts,
-                                                         const double* __restrict__ btv,
-                                                         const int32_t* __restrict__ bp, const int32_t* __restrict__ bc,
-                                                         const double* __restrict__ bv, const uint8_t* __restrict__ cflag,
-                                                         const double* __restrict__ X, const double* __restrict__ Bv,
-                                                         double* __restrict__ Y, int ns, int npres, int64_t N, int J,
-                                                         int Lv, int Lp, int nbv, int mode) {
-    if ((int)blockIdx.x < nbv)
-        spmm_pair_body(pp, pc, ps, A, nnz, tp, tc, ts, btv, cflag, X, Bv, Y, ns, N, J, Lv, mode, blockIdx.x);
-    else
-        spmm_pres_body<2, false>(bp, bc, bv, cflag, X, Bv, Y, npres, 2LL * ns, N, J, Lp, mode, nullptr,
-                                 blockIdx.x - nbv);
-}
-
 // ---------------------------------------------------------------------------
 // Wide-member variants (J >= 64: one row per warp, lanes over member pairs).
 // The row's CSR entries are loaded lane-parallel once (one coalesced load per
@@ -884,22 +865,6 @@ static int launch_spmm_vec(ens_ctx* c, cudaStream_t s, const double* as_vals, co
                            double* y, int mode, double* nrm, int* nblk) {
     const int J = c->J;
     int blocks_total = 0;
-    if (!nrm && J <= 64 && c->use_pairs) {
-        const ens_spmm_pairs& PR = c->pairs;
-        const int Lv = (J + 1) / 2, Rv = 32 / Lv;
-        const int H = J / 2, Lp = (H + 1) / 2, Rp = 32 / Lp;
-        const int64_t npair = ((int64_t)c->m.ns + 1) / 2;
-        const int nbv = (int)((((npair + Rv - 1) / Rv) * 32 + 255) / 256);
-        const int nbp = (int)(((((int64_t)c->m.n_pres + Rp - 1) / Rp) * 32 + 255) / 256);
-        k_spmm_both_pairs<<<nbv + nbp, 256, 0, s>>>(PR.a_ptr, PR.a_col, reinterpret_cast<const int2*>(PR.a_slot),
-                                                    as_vals, c->m.nnz_s, PR.t_ptr, PR.t_col,
-                                                    reinterpret_cast<const int2*>(PR.t_slot), c->m.bt_val,
-                                                    c->m.b_rowptr, c->m.b_col, c->m.b_val, c->m.cflag, x, b ? b : x, y,
-                                                    c->m.ns, c->m.n_pres, c->n_total, J, Lv, Lp, nbv, mode);
-        ENS_CKL();
-        if (nblk) *nblk = nbv + nbp;
-        return ENS_OK;
-    }
     if (!nrm && J <= 64 && J / 2 <= 64 && spmm_merge()) {
         const int Lv = (J + 1) / 2, Rv = 32 / Lv;
         const int H = J / 2, Lp = (H + 1) / 2, Rp = 32 / Lp;
@@ -970,7 +935,7 @@ bool spmm_resnorm_ok(const ens_ctx* c) {
     // cost more than the two 24 MB column-dot passes they replace)
     const char* e = std::getenv("ENS_FUSED_NORM");
     if (!(e && e[0] == '1')) return false;
-    return !c->use_blocked && (c->J & 1) == 0 && c->J >= 2 && c->J <= 64;
+    return (c->J & 1) == 0 && c->J >= 2 && c->J <= 64;
 }
 
 // y = b - K x plus the per-column squares of b and y (bn2, rn2: [mat][J])
@@ -995,8 +960,6 @@ int launch_spmm_resnorm(ens_ctx* c, cudaStream_t s, const double* as_vals, const
 
 int launch_spmm(ens_ctx* c, cudaStream_t s, const double* as_vals, const double* x, const double* b, double* y,
                 int mode) {
-    if (spmm_tiles_usable(c, x, b, y)) return launch_spmm_tiles(c, s, as_vals, x, b, y, mode);
-    if (c->use_blocked) return launch_spmm_blocked(c, s, as_vals, x, b, y, mode);
     const int J = c->J, W2 = 2 * J;
     if ((J & 1) == 0 && J <= 512 && (reinterpret_cast<uintptr_t>(x) & 15) == 0 &&
         (reinterpret_cast<uintptr_t>(y) & 15) == 0 && (!b || (reinterpret_cast<uintptr_t>(b) & 15) == 0))
@@ -1037,204 +1000,5 @@ int launch_spmm(ens_ctx* c, cudaStream_t s, const double* as_vals, const double*
 #undef SPP
         ENS_CKL();
     }
-    return ENS_OK;
-}
-
-// ---------------------------------------------------------------------------
-// Blocked variant (default when the staged rows fit in shared memory).
-// Rows are grouped into blocks of consecutive internal nodes (nested-dissection
-// order => spatially compact patches); each block's unique neighbour rows are
-// staged ONCE in shared memory with 16-byte cp.async, and the CSR column
-// indices are pre-remapped to local slots (symbolic, once per mesh).  L2/HBM
-// then sees each neighbour row about (block + halo) / block times instead of
-// once per nonzero.
-// ---------------------------------------------------------------------------
-__device__ __forceinline__ void cp16(void* smem, const void* gmem) {
-    const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
-}
-__device__ __forceinline__ void cp8(void* smem, const void* gmem) {
-    const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(gmem));
-}
-
-// stage rows src_row(i) of `width` doubles into dst[i*width ...]
-__device__ __forceinline__ void stage_rows(double* dst, const double* __restrict__ X, const int32_t* __restrict__ rows,
-                                           int nrows, int64_t row_base, int width) {
-    // 16-byte copies need 16-byte aligned rows: even width and an aligned block base
-    // (the second system's block starts N*J doubles in, odd when N*J is odd)
-    if ((width & 1) == 0 && (reinterpret_cast<uintptr_t>(X) & 15) == 0) {
-        const int hw = width >> 1;   // 16-byte chunks per row
-        for (int e = threadIdx.x; e < nrows * hw; e += blockDim.x) {
-            const int i = e / hw, c = e % hw;
-            cp16(dst + (int64_t)i * width + 2 * c, X + (row_base + rows[i]) * (int64_t)width + 2 * c);
-        }
-    } else {
-        for (int e = threadIdx.x; e < nrows * width; e += blockDim.x) {
-            const int i = e / width, c = e % width;
-            cp8(dst + (int64_t)i * width + c, X + (row_base + rows[i]) * (int64_t)width + c);
-        }
-    }
-}
-
-template <int OPL>
-__global__ void __launch_bounds__(256) k_spmm_vel_blk(const int32_t* __restrict__ rp, const int32_t* __restrict__ lcol,
-                                                      const double* __restrict__ A, int nnz,
-                                                      const int32_t* __restrict__ btp, const int32_t* __restrict__ btl,
-                                                      const double* __restrict__ btv, const uint8_t* __restrict__ cflag,
-                                                      const int32_t* __restrict__ vb_off, const int32_t* __restrict__ vb_nodes,
-                                                      const int32_t* __restrict__ pb_off, const int32_t* __restrict__ pb_rows,
-                                                      const int32_t* __restrict__ vb_row,
-                                                      const double* __restrict__ X, const double* __restrict__ Bv,
-                                                      double* __restrict__ Y, int ns, int64_t N, int J, int mode) {
-    extern __shared__ double sm[];
-    const int blk = blockIdx.x, mat = blockIdx.y;
-    const int W2 = 2 * J;
-    const int nv = vb_off[blk + 1] - vb_off[blk], np = pb_off[blk + 1] - pb_off[blk];
-    double* Xs = sm;                          // [nv][2J]
-    double* Ps = sm + (int64_t)nv * W2;       // [np][J]
-    const double* Xm = X + (int64_t)mat * N * J;
-    const int64_t nvel = 2LL * ns;
-    // velocity node rows are 2J wide starting at node 0; pressure rows J wide starting at row nvel
-    stage_rows(Xs, Xm, vb_nodes + vb_off[blk], nv, 0, W2);
-    stage_rows(Ps, Xm + nvel * J, pb_rows + pb_off[blk], np, 0, J);
-    asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::);
-    __syncthreads();
-    const double* Am = A + (int64_t)mat * nnz;
-    double* Ym = Y + (int64_t)mat * N * J;
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int n0 = vb_row[blk], n1 = vb_row[blk + 1];
-    for (int node = n0 + warp; node < n1; node += 8) {
-        double acc[OPL];
-#pragma unroll
-        for (int o = 0; o < OPL; ++o) acc[o] = 0.0;
-        const int k0 = rp[node], k1 = rp[node + 1];
-        for (int k = k0; k < k1; ++k) {
-            const double a = Am[k];
-            const double* xr = Xs + (int64_t)lcol[k] * W2;
-#pragma unroll
-            for (int o = 0; o < OPL; ++o) {
-                const int l = lane + 32 * o;
-                if (l < W2) acc[o] = fma(a, xr[l], acc[o]);
-            }
-        }
-        const int t0 = btp[node], t1 = btp[node + 1];
-        for (int t = t0; t < t1; ++t) {
-            const double bxv = btv[2 * t], byv = btv[2 * t + 1];
-            const double* pr = Ps + (int64_t)btl[t] * J;
-#pragma unroll
-            for (int o = 0; o < OPL; ++o) {
-                const int l = lane + 32 * o;
-                if (l < W2) {
-                    const int c2 = l >= J ? 1 : 0;
-                    acc[o] = fma(-(c2 ? byv : bxv), pr[l - c2 * J], acc[o]);
-                }
-            }
-        }
-#pragma unroll
-        for (int o = 0; o < OPL; ++o) {
-            const int l = lane + 32 * o;
-            if (l >= W2) continue;
-            const int c2 = l >= J ? 1 : 0;
-            const int64_t idx = 2LL * node * J + l;
-            double val = cflag[2 * node + c2] ? Xm[idx] : acc[o];
-            if (mode == 1) val = Bv[(int64_t)mat * N * J + idx] - val;
-            Ym[idx] = val;
-        }
-    }
-}
-
-template <int OPL>
-__global__ void __launch_bounds__(256) k_spmm_pres_blk(const int32_t* __restrict__ bp, const int32_t* __restrict__ bl,
-                                                       const double* __restrict__ bv, const uint8_t* __restrict__ cflag,
-                                                       const int32_t* __restrict__ qb_off,
-                                                       const int32_t* __restrict__ qb_nodes,
-                                                       const int32_t* __restrict__ qb_row,
-                                                       const double* __restrict__ X, const double* __restrict__ Bv,
-                                                       double* __restrict__ Y, int npres, int64_t nvel, int64_t N,
-                                                       int J, int mode) {
-    extern __shared__ double sm[];
-    const int blk = blockIdx.x, mat = blockIdx.y;
-    const int W2 = 2 * J;
-    const int nv = qb_off[blk + 1] - qb_off[blk];
-    double* Xs = sm;   // [nv][2J]
-    const double* Xm = X + (int64_t)mat * N * J;
-    stage_rows(Xs, Xm, qb_nodes + qb_off[blk], nv, 0, W2);
-    asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::);
-    __syncthreads();
-    double* Ym = Y + (int64_t)mat * N * J;
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int p0 = qb_row[blk], p1 = qb_row[blk + 1];
-    for (int p = p0 + warp; p < p1; p += 8) {
-        double acc[OPL];
-#pragma unroll
-        for (int o = 0; o < OPL; ++o) acc[o] = 0.0;
-        const int t0 = bp[p], t1 = bp[p + 1];
-        for (int t = t0; t < t1; ++t) {
-            const double bxv = bv[2 * t], byv = bv[2 * t + 1];
-            const double* xr = Xs + (int64_t)bl[t] * W2;
-#pragma unroll
-            for (int o = 0; o < OPL; ++o) {
-                const int l = lane + 32 * o;
-                if (l < J) acc[o] = fma(bxv, xr[l], fma(byv, xr[J + l], acc[o]));
-            }
-        }
-        const int64_t row = nvel + p;
-#pragma unroll
-        for (int o = 0; o < OPL; ++o) {
-            const int l = lane + 32 * o;
-            if (l >= J) continue;
-            const int64_t idx = row * J + l;
-            double val = cflag[row] ? Xm[idx] : acc[o];
-            if (mode == 1) val = Bv[(int64_t)mat * N * J + idx] - val;
-            Ym[idx] = val;
-        }
-    }
-}
-
-int launch_spmm_blocked(ens_ctx* c, cudaStream_t s, const double* as_vals, const double* x, const double* b,
-                        double* y, int mode) {
-    const ens_spmm_blocks& B = c->blk;
-    const int J = c->J, W2 = 2 * J;
-    const int opl = (W2 + 31) / 32;
-    {
-        dim3 grid((unsigned)B.nvb, 2);
-#define SPVB(V)                                                                                                   \
-    k_spmm_vel_blk<V><<<grid, 256, B.smem_vel, s>>>(c->m.s_rowptr, B.a_lcol, as_vals, c->m.nnz_s, c->m.bt_rowptr,  \
-                                                    B.bt_lcol, c->m.bt_val, c->m.cflag, B.vb_off, B.vb_nodes,      \
-                                                    B.pb_off, B.pb_rows, B.vb_row, x, b, y, c->m.ns, c->n_total, J, mode)
-        if (opl <= 1) SPVB(1);
-        else if (opl <= 2) SPVB(2);
-        else if (opl <= 4) SPVB(4);
-        else SPVB(8);
-#undef SPVB
-        ENS_CKL();
-    }
-    {
-        const int oplp = (J + 31) / 32;
-        dim3 grid((unsigned)B.nqb, 2);
-#define SPPB(V)                                                                                                     \
-    k_spmm_pres_blk<V><<<grid, 256, B.smem_pres, s>>>(c->m.b_rowptr, B.b_lcol, c->m.b_val, c->m.cflag, B.qb_off,   \
-                                                      B.qb_nodes, B.qb_row, x, b, y, c->m.n_pres, c->n_vel,      \
-                                                      c->n_total, J, mode)
-        if (oplp <= 1) SPPB(1);
-        else if (oplp <= 2) SPPB(2);
-        else SPPB(4);
-#undef SPPB
-        ENS_CKL();
-    }
-    return ENS_OK;
-}
-
-int spmm_blocked_setup(ens_ctx* c) {
-    const int J = c->J, W2 = 2 * J;
-    if (W2 > 256) return ENS_OK;   // OPL template range
-    const int opl = (W2 + 31) / 32, oplp = (J + 31) / 32;
-    const void* kv = opl <= 1 ? (const void*)k_spmm_vel_blk<1> : opl <= 2 ? (const void*)k_spmm_vel_blk<2>
-                   : opl <= 4 ? (const void*)k_spmm_vel_blk<4> : (const void*)k_spmm_vel_blk<8>;
-    const void* kp = oplp <= 1 ? (const void*)k_spmm_pres_blk<1> : oplp <= 2 ? (const void*)k_spmm_pres_blk<2>
-                   : (const void*)k_spmm_pres_blk<4>;
-    ENS_CK(cudaFuncSetAttribute(kv, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->blk.smem_vel));
-    ENS_CK(cudaFuncSetAttribute(kp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->blk.smem_pres));
     return ENS_OK;
 }

@@ -223,72 +223,6 @@ class HostMesh:
         return np.ascontiguousarray(np.asarray(arr_ref, dtype=float).T[self.ref_of_int[self.nvel:] - self.nvel])
 
 
-def _greedy_row_blocks(row_ptrs, colss, widths, nrows, cap_doubles, max_rows=128):
-    """Cut rows [0, nrows) greedily into blocks whose staged rows fit ``cap_doubles``.
-
-    ``row_ptrs``/``colss``/``widths``: one CSR per staged operand (e.g. A_s
-    columns of width 2J and B^T pressure columns of width J).  Returns the block
-    row offsets.
-    """
-    starts = [0]
-    seen = [set() for _ in row_ptrs]
-    used = 0
-    r0 = 0
-    rp_l = [rp.tolist() for rp in row_ptrs]
-    cl_l = [c.tolist() for c in colss]
-    for r in range(nrows):
-        add = []
-        cost = 0
-        for q in range(len(row_ptrs)):
-            new = {c for c in cl_l[q][rp_l[q][r]:rp_l[q][r + 1]] if c not in seen[q]}
-            add.append(new)
-            cost += len(new) * widths[q]
-        if r > r0 and (used + cost > cap_doubles or r - r0 >= max_rows):
-            starts.append(r)
-            r0 = r
-            seen = [set() for _ in row_ptrs]
-            used = 0
-            add = [set(cl_l[q][rp_l[q][r]:rp_l[q][r + 1]]) for q in range(len(row_ptrs))]
-            cost = sum(len(a) * widths[q] for q, a in enumerate(add))
-        for q in range(len(row_ptrs)):
-            seen[q] |= add[q]
-        used += cost
-    starts.append(nrows)
-    return np.array(starts, dtype=np.int64)
-
-
-def _block_lists(row_ptr, cols, row_starts):
-    """Per row block: sorted unique columns (offsets, list) and each nonzero's local slot."""
-    nrows = len(row_ptr) - 1
-    row_of = np.repeat(np.arange(nrows, dtype=np.int64), np.diff(row_ptr))
-    blk = np.searchsorted(row_starts, row_of, side="right") - 1
-    ncol = int(cols.max()) + 1 if len(cols) else 1
-    key = blk * ncol + cols.astype(np.int64)
-    ukey = np.unique(key)
-    nblk = len(row_starts) - 1
-    off = np.searchsorted(ukey // ncol, np.arange(nblk + 1)).astype(np.int32)
-    lst = (ukey % ncol).astype(np.int32)
-    lcol = (np.searchsorted(ukey, key) - off[blk]).astype(np.int32)
-    return off, lst, lcol
-
-
-def spmm_blocking(hm, J, cap_bytes=64 * 1024):
-    """Variable-size row blocking of the saddle SpMM; staged rows per block fit ``cap_bytes``."""
-    W2 = 2 * J
-    if W2 > 256 or 16 * W2 * 8 > cap_bytes:
-        return None
-    cap = cap_bytes // 8
-    vstart = _greedy_row_blocks([hm.s_rowptr, hm.bt_rowptr], [hm.s_col, hm.bt_col], [W2, J], hm.ns, cap)
-    voff, vlst, alcol = _block_lists(hm.s_rowptr, hm.s_col, vstart)
-    poff, plst, btl = _block_lists(hm.bt_rowptr, hm.bt_col, vstart)
-    smv = int((np.diff(voff) * W2 + np.diff(poff) * J).max()) * 8
-    qstart = _greedy_row_blocks([hm.b_rowptr], [hm.b_col], [W2], hm.npres, cap)
-    qoff, qlst, bl = _block_lists(hm.b_rowptr, hm.b_col, qstart)
-    smp = int(np.diff(qoff).max()) * W2 * 8
-    return (vstart.astype(np.int32), voff, vlst, alcol, poff, plst, btl, smv), (qstart.astype(np.int32), qoff, qlst,
-                                                                                 bl, smp)
-
-
 def host_mesh(disc) -> HostMesh:
     key = "b200-hostmesh"
     if key not in disc._cache:
@@ -440,57 +374,6 @@ class Engine:
         with torch.cuda.device(self.dev):
             N.check(self.lib.ens_create(C.byref(md), C.byref(pd), self.dev.index, C.byref(ctx)), "ens_create")
         self.ctx = ctx
-        # SpMM row blocking (shared-memory staged neighbour rows), opt-in with
-        # ENS_SPMM_BLOCKED=1: measured slower at C2 (190 vs 139 us cold for the
-        # velocity rows; the kernel is bound by index->gather latency, not L2 bytes)
-        import os
-        self.spmm_blocks = None
-        if os.environ.get("ENS_SPMM_BLOCKED", "0") == "1":
-            blk = spmm_blocking(hm, J)
-            if blk is not None:
-                (vst, voff, vlst, alcol, poff, plst, btl, smv), (qst, qoff, qlst, bl, smp) = blk
-                bt = dict(a_lcol=up(alcol, i32), bt_lcol=up(btl, i32), b_lcol=up(bl, i32), vb_off=up(voff, i32),
-                          vb_nodes=up(vlst, i32), pb_off=up(poff, i32), pb_rows=up(plst, i32),
-                          qb_off=up(qoff, i32), qb_nodes=up(qlst, i32), vb_row=up(vst, i32), qb_row=up(qst, i32))
-                sb = N.SpmmBlocks()
-                sb.bn, sb.bp, sb.nvb, sb.nqb = 0, 0, len(voff) - 1, len(qoff) - 1
-                sb.smem_vel, sb.smem_pres = smv, smp
-                for k, t in bt.items():
-                    setattr(sb, k, _dptr(t))
-                N.check(self.lib.ens_set_spmm_blocks(ctx, C.byref(sb)), "ens_set_spmm_blocks")
-                self.spmm_blocks = (sb, bt)
-        # tile-staged SpMM (bulk-copied shared-memory stages, csrc/ens_spmm_tiles.cu)
-        self.spmm_tiles = None
-        if os.environ.get("ENS_SPMM_TILES", "0") == "1" and J % 2 == 0 and J <= 64:
-            from . import spmm_tiles as TL
-            nstage = int(os.environ.get("ENS_TILE_STAGES", "3"))
-            cap = int(os.environ.get("ENS_TILE_CAP", str(192 // nstage))) * 1024
-            desc, recs, la, lbt, lb, info = TL.build_tiles(hm, J, cap=cap)
-            pad = lambda a: np.concatenate([a, np.zeros(16, a.dtype)])   # aligned stream tails stay in bounds
-            tt = dict(tiles=up(desc.reshape(-1), i32), recs=up(recs.view(np.int32), i32),
-                      lcol_a=up(pad(la), i32), lcol_bt=up(pad(lbt), i32), lcol_b=up(pad(lb), i32))
-            st_ = N.SpmmTiles()
-            for k, t in tt.items():
-                setattr(st_, k, _dptr(t))
-            st_.ntiles, st_.nrec = len(desc), len(recs)
-            st_.stage_bytes, st_.nstage = info["stage_bytes"], nstage
-            st_.grid = torch.cuda.get_device_properties(self.dev).multi_processor_count
-            N.check(self.lib.ens_set_spmm_tiles(ctx, C.byref(st_)), "ens_set_spmm_tiles")
-            self.spmm_tiles = (st_, tt, info)
-        # row-pair SpMM (velocity rows 2p, 2p+1 over the union of their columns), even J <= 64;
-        # opt-in (ENS_SPMM_PAIRS=1): 27 % fewer gathers but measured slower at C2 (107.5 vs 102.9 us)
-        self.spmm_pairs = None
-        if os.environ.get("ENS_SPMM_PAIRS", "0") == "1" and J % 2 == 0 and J <= 64 and self.spmm_tiles is None:
-            from . import spmm_tiles as TL
-            (ap, ac, asl), (tp_, tc, tsl), _ = TL.row_pairs(hm)
-            pt = dict(a_ptr=up(ap, i32), a_col=up(ac, i32), a_slot=up(asl.reshape(-1), i32), t_ptr=up(tp_, i32),
-                      t_col=up(tc, i32), t_slot=up(tsl.reshape(-1), i32))
-            sp_ = N.SpmmPairs()
-            for k_, t_ in pt.items():
-                setattr(sp_, k_, _dptr(t_))
-            sp_.npairs = (hm.ns + 1) // 2
-            N.check(self.lib.ens_set_spmm_pairs(ctx, C.byref(sp_)), "ens_set_spmm_pairs")
-            self.spmm_pairs = (sp_, pt)
         # per-run constants
         st = viscosity_stats(config)
         self.config = config

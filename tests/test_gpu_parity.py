@@ -286,28 +286,6 @@ def test_case_runs_match_oracle(case, over):
     assert np.all(report.residuals[1:] < 1e-11)
 
 
-@pytest.mark.parametrize("J,stages", [(20, 2), (8, 3)])
-def test_spmm_tiles_bitwise_equal_direct(monkeypatch, rng, J, stages):
-    """The tile-staged SpMM (opt-in) keeps the direct kernel's per-output summation order: identical bits."""
-    disc, cfg, _ = P.build_case("C1", J=J)
-    direct = Engine(disc, cfg)
-    monkeypatch.setenv("ENS_SPMM_TILES", "1")
-    monkeypatch.setenv("ENS_TILE_STAGES", str(stages))
-    monkeypatch.setenv("ENS_TILE_CAP", "24")
-    tiled = Engine(disc, cfg)
-    assert tiled.spmm_tiles is not None and tiled.spmm_tiles[2]["nvt"] > 1
-    a = torch.from_numpy(rng.standard_normal((2, direct.hm.nnz_s))).cuda()
-    direct.as_vals.copy_(a)
-    tiled.as_vals.copy_(a)
-    x = torch.from_numpy(rng.standard_normal((2, disc.n_total, J))).cuda()
-    b = torch.from_numpy(rng.standard_normal((2, disc.n_total, J))).cuda()
-    for mode in (0, 1):
-        y0 = direct.spmm(x, b if mode else None, mode=mode)
-        y1 = tiled.spmm(x, b if mode else None, mode=mode)
-        torch.cuda.synchronize()
-        assert torch.equal(y0, y1), mode
-
-
 @pytest.mark.parametrize("J", [64, 128])
 def test_spmm_wide_bitwise_equal_direct(monkeypatch, rng, J):
     """The one-row-per-warp SpMM for J >= 64 (default) keeps the direct kernel's summation order."""
@@ -392,27 +370,6 @@ def test_sharded_path_single_rank_nccl():
         assert np.array_equal(report.residuals, ref_report.residuals)
     finally:
         dist.destroy_process_group()
-
-
-@pytest.mark.parametrize("J", [20, 6])
-def test_spmm_pairs_bitwise_equal_direct(monkeypatch, rng, J):
-    """The row-pair SpMM (opt-in, even J < 64) keeps each row's CSR summation order: identical bits."""
-    disc, cfg, _ = P.build_case("C1", J=J, steps=1)
-    monkeypatch.setenv("ENS_SPMM_PAIRS", "0")
-    direct = Engine(disc, cfg)
-    monkeypatch.setenv("ENS_SPMM_PAIRS", "1")
-    paired = Engine(disc, cfg)
-    assert paired.spmm_pairs is not None and direct.spmm_pairs is None
-    a = torch.from_numpy(rng.standard_normal((2, direct.hm.nnz_s))).cuda()
-    direct.as_vals.copy_(a)
-    paired.as_vals.copy_(a)
-    x = torch.from_numpy(rng.standard_normal((2, disc.n_total, J))).cuda()
-    b = torch.from_numpy(rng.standard_normal((2, disc.n_total, J))).cuda()
-    for mode in (0, 1):
-        y0 = direct.spmm(x, b if mode else None, mode=mode)
-        y1 = paired.spmm(x, b if mode else None, mode=mode)
-        torch.cuda.synchronize()
-        assert torch.equal(y0, y1), mode
 
 
 def test_engine_reuse_with_new_problem_objects(monkeypatch):
