@@ -13,8 +13,10 @@ from .ensemble import (EnsembleConfig, EnsembleState, MemberParams, elsasser_fro
 from .mesh import Marker, Mesh, barycentric_refine, build_step_channel, build_structured_square
 from .problems import (BaselineMms, PaperMmsBoundary, PaperMmsForcing, ScaledProfileBoundary, ZeroBoundary,
                        ZeroForcing, build_case, paper_mms_initial_fields)
-from .stepper import (Problem, RunReport, StepFailure, StepKind, advance, check_preconditions, energy, run,
-                      set_solver_options, verify_stability_bound)
+from .linalg import Factorization, SingularMatrixError, factorize, relative_residual
+from .stepper import (Problem, RunReport, StepFailure, StepKind, StepSystem, advance, assemble_member_rhs,
+                      assemble_shared_lhs, check_preconditions, energy, run, set_solver_options,
+                      verify_stability_bound)
 
 __all__ = [
     "Discretization", "EnsembleConfig", "EnsembleState", "MemberParams", "Marker", "Mesh", "Problem",
@@ -23,7 +25,8 @@ __all__ = [
     "primitive_from_elsasser", "run", "sample_viscosities", "verify_stability_bound", "viscosity_stats",
     "perturbation_factor", "perturbation_factors", "BaselineMms", "PaperMmsForcing", "PaperMmsBoundary",
     "ZeroForcing", "ZeroBoundary", "ScaledProfileBoundary", "build_case", "paper_mms_initial_fields",
-    "set_solver_options",
+    "set_solver_options", "StepSystem", "assemble_shared_lhs", "assemble_member_rhs", "Factorization",
+    "SingularMatrixError", "factorize", "relative_residual",
 ]
 
 __version__ = "0.1.0"

@@ -1099,6 +1099,97 @@ class Engine:
         return dict(energy=0.5 * (out[0] + out[1]), l2v=series[0], l2w=series[1], gradv=series[2], gradw=series[3],
                     div_v=np.sqrt(np.maximum(series[4], 0.0)), div_w=np.sqrt(np.maximum(series[5], 0.0)))
 
+    # ------------------------------------------------------------------
+    # lower seams of the reference API: stepper.assemble_shared_lhs / assemble_member_rhs and
+    # linalg.factorize (`stepper.py:181-278`, `linalg.py:46-108`).  Same kernels as the step.
+    # ------------------------------------------------------------------
+    def block_to_internal(self, blk_ref):
+        """(n_total, J) reference-order rows -> (n_total, J) internal rows (numpy)."""
+        out = np.empty_like(np.asarray(blk_ref, dtype=float))
+        out[self.hm.int_id] = blk_ref
+        return out
+
+    def block_to_ref(self, blk_int):
+        return np.asarray(blk_int)[self.hm.int_id]
+
+    def _seam_state(self, v, w):
+        self.load_state(v, w, None, None)
+        self.prev_valid = False
+
+    def shared_block_values(self, system, mean_adv, flucts):
+        """A_s values (internal slot order) of one sub-step matrix: system 0 = V (advected by the
+        given mean, eddy viscosity of the given fluctuations), 1 = W; `stepper.py:195-206`."""
+        hm, J = self.hm, self.J
+        flucts = np.asarray(flucts, dtype=float)
+        if flucts.shape != (J, self.nvel):
+            raise ValueError(f"fluctuations shape {flucts.shape} != ({J}, {self.nvel})")
+        fields = np.asarray(mean_adv, dtype=float)[None, :] + flucts
+        self._seam_state(fields, fields)
+        mean_int = hm.vel_to_internal(np.asarray(mean_adv, dtype=float)[None, :])[:, 0]
+        lib, ctx, s = self.lib, self.ctx, self.sptr
+        with self.on_stream():
+            m = torch.as_tensor(mean_int).to(self.dev)
+            self.means[:self.nvel].copy_(m)
+            self.means[self.nvel:].copy_(m)
+            self._rhs_and_member_pass(self.X[self.cur], None)
+            N.check(lib.ens_assemble(ctx, s, _dptr(self.base), _dptr(self.means), _dptr(self.maxsq),
+                                     self.two_mu_dt, _dptr(self.as_vals)), "ens_assemble")
+            out = self.as_vals[system].cpu().numpy()
+        self.means_valid = False
+        return out
+
+    def member_rhs_block(self, system, v, w, loads, bvals):
+        """(n_total, J) right-hand sides of one sub-step in reference order (`stepper.py:223-252`):
+        ``loads`` (J, n_vel) or None and ``bvals`` (J, nb) of that sub-step."""
+        hm, J = self.hm, self.J
+        self._seam_state(v, w)
+        lib, ctx, s = self.lib, self.ctx, self.sptr
+        with self.on_stream():
+            self._compute_means()
+            keep = []
+            lref = None
+            if loads is not None:
+                dense = np.zeros((2, self.nvel, J))
+                dense[system] = hm.vel_to_internal(np.asarray(loads, dtype=float))
+                lt = torch.as_tensor(dense).to(self.dev)
+                keep.append(lt)
+                ld = N.DataDesc()
+                ld.rows, ld.K, ld.basis, ld.coef, ld.dense = self.nvel, 0, None, None, _dptr(lt)
+                lref = C.byref(ld)
+            self._rhs_and_member_pass(self.X[self.cur], lref)
+            dense = np.zeros((2, hm.nbdofs, J))
+            dense[system] = np.asarray(bvals, dtype=float).reshape(J, hm.nbdofs).T
+            bt = torch.as_tensor(dense).to(self.dev)
+            bd = N.DataDesc()
+            bd.rows, bd.K, bd.basis, bd.coef, bd.dense = hm.nbdofs, 0, None, None, _dptr(bt)
+            N.check(lib.ens_apply_bc(ctx, s, C.byref(bd), _dptr(self.rhs)), "ens_apply_bc")
+            out = self.rhs[system].cpu().numpy()
+            del keep, bt
+        self.means_valid = False
+        return self.block_to_ref(out)
+
+    def solve_values(self, a_vals, rhs_ref, factor=True):
+        """Solve the saddle system with A_s = ``a_vals`` (internal slots) for the (n_total, J) block
+        ``rhs_ref`` (reference order): the same factorisation-preconditioned column-batched Krylov
+        as the step, converged to ``rtol`` per column.  Returns (x_ref, relres)."""
+        J = self.J
+        rhs_int = self.block_to_internal(np.asarray(rhs_ref, dtype=float).reshape(self.ntot, J))
+        lib, ctx, s = self.lib, self.ctx, self.sptr
+        with self.on_stream():
+            a = torch.as_tensor(np.asarray(a_vals, dtype=float)).to(self.dev)
+            self.as_vals[0].copy_(a)
+            self.as_vals[1].copy_(a)
+            if factor:
+                self._factor()
+            self.rhs.zero_()
+            self.rhs[0].copy_(torch.as_tensor(rhs_int))
+            x = torch.zeros_like(self.rhs)
+            code, iters, rel = self._solve(x, predict=0)
+            N.check(code, "ens_solve")
+            out = x[0].cpu().numpy()
+        self.last_relres = rel
+        return self.block_to_ref(out), rel[0]
+
     # raw access for tests
     def spmm(self, x, b=None, mode=0, out=None):
         out = torch.empty_like(x) if out is None else out

@@ -179,6 +179,74 @@ def energy(state: EnsembleState, disc: Discretization) -> float:
     return 0.5 * float(mv @ disc.apply_mass(mv) + mw @ disc.apply_mass(mw))
 
 
+# ----------------------------------------------------------------------
+# lower seams (`stepper.py:126-138, 181-278`): one sub-step's shared matrix and member right-hand
+# sides, computed by the step's own kernels and read back in reference order
+# ----------------------------------------------------------------------
+
+
+@dataclass
+class StepSystem:
+    """Shared saddle system of one sub-step (`stepper.py:126-138`)."""
+
+    step_kind: StepKind
+    matrix: object
+    factorization: object
+    rhs: np.ndarray
+
+
+def _system_index(kind: StepKind) -> int:
+    if kind is StepKind.V_STEP:
+        return 0
+    if kind is StepKind.W_STEP:
+        return 1
+    raise ValueError(f"unknown step kind {kind!r}")
+
+
+def assemble_shared_lhs(step_kind: StepKind, mean_advecting, fluctuations, config: EnsembleConfig,
+                        disc: Discretization) -> StepSystem:
+    """Build and factorise the shared sub-step matrix (`stepper.py:181-220`).
+
+    Velocity block M/dt + N(mean) + (nu_bar + nu_m_bar)/2 K + K(2 nu_T(fluctuations)) assembled
+    by the GPU element kernels; divergence blocks, Dirichlet identity rows and the pin as in the
+    reference; factorised by the GPU multifrontal sweep (``linalg.factorize``).  The matrix is the
+    CSR read-back in reference dof order."""
+    from . import linalg
+    flucts = np.atleast_2d(np.asarray(fluctuations, dtype=float))
+    cfg = config
+    if flucts.shape[0] != config.num_members:
+        raise ValueError(f"{flucts.shape[0]} fluctuation rows for {config.num_members} members")
+    eng = get_engine(disc, cfg)
+    vals = eng.shared_block_values(_system_index(step_kind), mean_advecting, flucts)
+    matrix = linalg.saddle_matrix(disc, vals)
+    if not isinstance(disc.saddle_symbolic, linalg.SaddleSymbolic):
+        disc.saddle_symbolic = linalg.SaddleSymbolic(disc)
+    fact = linalg.Factorization(matrix.shape, "b200", (disc, vals), disc.saddle_symbolic)
+    return StepSystem(step_kind, matrix, fact, np.zeros((disc.n_total, config.num_members)))
+
+
+def _rhs_block(step_kind: StepKind, state: EnsembleState, loads, boundary_values, config: EnsembleConfig,
+               disc: Discretization) -> np.ndarray:
+    """(n_total, J) right-hand sides of one sub-step (`stepper.py:223-252`), on the GPU."""
+    eng = get_engine(disc, config)
+    return eng.member_rhs_block(_system_index(step_kind), state.v, state.w, loads, boundary_values)
+
+
+def assemble_member_rhs(step_kind: StepKind, member: int, state: EnsembleState, load, boundary_values,
+                        config: EnsembleConfig, disc: Discretization) -> np.ndarray:
+    """Right-hand-side column of one member (`stepper.py:255-278`): ``load`` is the member's load
+    vector (or None), ``boundary_values`` its Dirichlet values on ``disc.bdofs``."""
+    if load is None:
+        loads = None
+    else:
+        load = np.asarray(load, dtype=float)
+        if load.shape != (disc.n_vel,):
+            raise ValueError(f"load vector shape {load.shape} != ({disc.n_vel},)")
+        loads = np.tile(load, (config.num_members, 1))
+    bvals = np.tile(np.asarray(boundary_values, dtype=float), (config.num_members, 1))
+    return _rhs_block(step_kind, state, loads, bvals, config, disc)[:, member]
+
+
 @dataclass
 class RunReport:
     """Per-step diagnostics (`stepper.py:404-429`); entry 0 is the initial state."""
@@ -202,24 +270,47 @@ class RunReport:
         return len(self.times) - 1
 
 
-def _record(report, n, engine, comm=None):
+_MEMBER_KEYS = ("l2v", "l2w", "gradv", "gradw", "div_v", "div_w")
+
+
+def _record(report, n, engine, local=None):
+    """Per-level diagnostics (`stepper.py:432-439`).  Sharded runs (``local`` is a list) keep this
+    rank's member values on the host and gather them once at the end (``_gather_records``)."""
     d = engine.diagnostics()
-    if comm is not None:
-        import torch
-        import torch.distributed as dist
-        parts = [None] * dist.get_world_size(comm)
-        dist.all_gather_object(parts, {k: d[k] for k in ("l2v", "l2w", "gradv", "gradw", "div_v", "div_w")},
-                               group=comm)
-        for k in ("l2v", "l2w", "gradv", "gradw", "div_v", "div_w"):
-            d[k] = np.concatenate([p[k] for p in parts])
-        del torch
-    report.energy[n] = d["energy"]
+    report.energy[n] = d["energy"]            # from the replicated means: the same on every rank
+    if local is not None:
+        local.append(np.stack([np.asarray(d[k], dtype=float) for k in _MEMBER_KEYS]))
+        return
+    _fill_members(report, n, {k: d[k] for k in _MEMBER_KEYS})
+
+
+def _fill_members(report, n, d):
     report.div_v[n] = float(np.max(d["div_v"]))
     report.div_w[n] = float(np.max(d["div_w"]))
     report.member_l2v_sq[n] = d["l2v"]
     report.member_l2w_sq[n] = d["l2w"]
     report.member_gradv_sq[n] = d["gradv"]
     report.member_gradw_sq[n] = d["gradw"]
+
+
+def _gather_records(report, local, comm, J):
+    """One all_gather of every rank's (levels, 6, J_local) member diagnostics (padded to the largest
+    shard) instead of a host-synchronising collective per step."""
+    import torch
+    import torch.distributed as dist
+    world = dist.get_world_size(comm)
+    shards = [member_slice(J, r, world) for r in range(world)]
+    jmax = max(c for _, c in shards)
+    arr = np.stack(local) if local else np.zeros((0, len(_MEMBER_KEYS), 0))
+    pad = np.zeros((arr.shape[0], len(_MEMBER_KEYS), jmax))
+    pad[:, :, :arr.shape[2]] = arr
+    dev = torch.device("cuda", torch.cuda.current_device()) if dist.get_backend(comm) == "nccl" else "cpu"
+    t = torch.from_numpy(pad).to(dev)
+    parts = [torch.empty_like(t) for _ in range(world)]
+    dist.all_gather(parts, t, group=comm)
+    full = np.concatenate([p.cpu().numpy()[:, :, :c] for p, (_, c) in zip(parts, shards)], axis=2)
+    for n in range(full.shape[0]):
+        _fill_members(report, n, dict(zip(_MEMBER_KEYS, full[n])))
 
 
 from .exchange import member_slice  # noqa: E402  (re-exported)
@@ -260,8 +351,9 @@ def run(config: EnsembleConfig, problem: Problem, observer=None, snapshot_steps=
     w0 = np.asarray(problem.initial_w, dtype=float)[j0:j0 + jl]
     engine.load_state(v0, w0, None, None)
     state = EnsembleState(step=0, time=0.0, device=engine.state_handle())
+    local = [] if comm is not None else None
     if record:
-        _record(report, 0, engine, comm)
+        _record(report, 0, engine, local)
     snaps = {}
     if 0 in snapshot_steps:
         snaps[0] = state
@@ -274,7 +366,7 @@ def run(config: EnsembleConfig, problem: Problem, observer=None, snapshot_steps=
         report.wall_clock[n + 1] = _time.perf_counter() - tic
         report.residuals[n + 1] = res
         if record:
-            _record(report, n + 1, engine, comm)
+            _record(report, n + 1, engine, local)
         if state.step in snapshot_steps:
             state.device_state.materialize()
             snaps[state.step] = state
@@ -287,6 +379,8 @@ def run(config: EnsembleConfig, problem: Problem, observer=None, snapshot_steps=
             g = engine.global_residuals.pop(n0 + n, None)
             if g is not None:
                 report.residuals[n + 1] = g
+        if record:
+            _gather_records(report, local, comm, J)
     return report, state, snaps
 
 
@@ -340,6 +434,7 @@ def _dual_sums(report, config, disc, forcing):
 
 __all__ = [
     "Discretization", "Problem", "RunReport", "StepKind", "StepFailure", "PreconditionReport",
-    "StabilityCheck", "advance", "run", "energy", "check_preconditions", "verify_stability_bound",
+    "StabilityCheck", "StepSystem", "advance", "run", "energy", "check_preconditions", "verify_stability_bound",
+    "assemble_shared_lhs", "assemble_member_rhs",
     "ZeroForcing", "ZeroBoundary", "ScaledProfileBoundary", "member_slice", "set_solver_options",
 ]

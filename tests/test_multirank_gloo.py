@@ -112,3 +112,49 @@ def test_sharded_exchanges_reproduce_ensemble(world):
         assert np.max(np.abs(r[:, free] - ref[:, free])) <= 1e-12 * np.abs(ref).max()
         assert res == world - 1
     assert covered == list(range(cfg.num_members))
+
+
+def _gather_worker(rank, world, port, J, steps, out_q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import sys
+        sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+        from paper_2108_05110_b200 import stepper as ST
+        j0, jl = ST.member_slice(J, rank, world)
+        # member diagnostics this rank would record per level: value = 1000*level + 10*member + key
+        local = [np.array([[1000.0 * n + 10.0 * (j0 + j) + k for j in range(jl)] for k in range(6)])
+                 for n in range(steps + 1)]
+        rep = ST.RunReport(times=np.zeros(steps + 1), energy=np.zeros(steps + 1), div_v=np.zeros(steps + 1),
+                           div_w=np.zeros(steps + 1), residuals=np.zeros(steps + 1), wall_clock=np.zeros(steps + 1),
+                           alpha=np.zeros(J), mu=1.0, dt=1.0, member_l2v_sq=np.zeros((steps + 1, J)),
+                           member_l2w_sq=np.zeros((steps + 1, J)), member_gradv_sq=np.zeros((steps + 1, J)),
+                           member_gradw_sq=np.zeros((steps + 1, J)))
+        ST._gather_records(rep, local, dist.group.WORLD, J)
+        out_q.put((rank, rep.member_l2v_sq, rep.member_gradw_sq, rep.div_v, rep.div_w))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_run_records_gathered_once_uneven_shards():
+    """Sharded run(): per-member diagnostics stay rank-local during the run and are gathered once at
+    the end (padded all_gather), in member order, with uneven shards (J = 7 over 2 ranks)."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    J, steps, world = 7, 3, 2
+    procs = [ctx.Process(target=_gather_worker, args=(r, world, port, J, steps, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    outs = [q.get(timeout=240) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    n = np.arange(steps + 1)[:, None]
+    j = np.arange(J)[None, :]
+    for _, l2v, gradw, div_v, div_w in outs:
+        assert np.array_equal(l2v, 1000.0 * n + 10.0 * j + 0)
+        assert np.array_equal(gradw, 1000.0 * n + 10.0 * j + 3)
+        assert np.array_equal(div_v, 1000.0 * n[:, 0] + 10.0 * (J - 1) + 4)
+        assert np.array_equal(div_w, 1000.0 * n[:, 0] + 10.0 * (J - 1) + 5)
