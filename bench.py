@@ -7,10 +7,11 @@ members, dt=0.005.  A bench *step* is one full time-step
 (both Elsasser sub-steps, all members): member sums, right-hand sides, eddy
 viscosity, shared-matrix assembly, multifrontal LU of both saddle matrices,
 column-batched FGMRES to a true relative residual of 1e-12 per member, and
-the pressure epilogue.  For N>1 (torchrun, one rank per GPU) members are
-sharded contiguously with J = 20 per GPU (weak scaling) and every step does
-the two real exchanges of the scheme over NCCL: allreduce SUM of the member
-sums and allreduce MAX of the eddy-viscosity maxima.
+the pressure epilogue.  For N>1 (torchrun, one rank per GPU) the workload is
+BASELINE configs[4] = "C5" (512x512, J = 1024 members in total, strong
+scaling: 1024/N per GPU, chunked when a shard does not fit at once) and every
+step does the two real exchanges of the scheme over NCCL: allreduce SUM of the
+member sums and allreduce MAX of the eddy-viscosity maxima.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
 
@@ -34,14 +35,36 @@ sys.path.insert(0, ROOT)
 METRIC = "ensemble member-timesteps/sec at fixed mesh"
 UNIT = "member-steps/s"
 CASE = "C2"
+CASE_MULTI = "C5"
 J_PER_GPU = 20
-# other BASELINE configurations (bench.py --case): members per GPU and the workload text
+# BASELINE configurations (bench.py --case): (members, scaling, workload text).  "weak": members per
+# GPU; "strong": members in total, sharded over the GPUs.
 CASES = {
-    "C2": (20, "C2: unit square 128x128, TH P2/P1, J=20/GPU, dt=0.005"),
-    "C3": (64, "C3: lid-driven cavity, unit square 256x256, TH P2/P1, J=64/GPU, s=1, dt=0.01"),
-    "C4": (128, "C4: channel past a step [0,30]x[0,10], h=1/8, TH P2/P1, J=128/GPU, delta=0.01, dt=0.02"),
-    "C5": (128, "C5: unit square 512x512, TH P2/P1, J=128/GPU (the 8-GPU shard of J=1024), dt=0.002"),
+    "C2": (20, "weak", "C2: unit square 128x128, TH P2/P1, J=20/GPU, dt=0.005"),
+    "C3": (64, "weak", "C3: lid-driven cavity, unit square 256x256, TH P2/P1, J=64/GPU, s=1, dt=0.01"),
+    "C4": (128, "weak", "C4: channel past a step [0,30]x[0,10], h=1/8, TH P2/P1, J=128/GPU, delta=0.1, dt=0.02"),
+    "C5": (1024, "strong", "C5: unit square 512x512, TH P2/P1, J=1024 sharded over the GPUs, dt=0.002"),
+    "C5shard": (128, "weak", "C5 shard: unit square 512x512, TH P2/P1, J=128/GPU (the 8-GPU shard of J=1024), "
+                             "dt=0.002"),
 }
+
+
+def single_thread():
+    """Pin this process to one core and one BLAS thread: the reference path is serial (SuperLU,
+    sparsetools and einsum; SURVEY.md §8(d) measured 8 BLAS threads slower)."""
+    try:
+        os.sched_setaffinity(0, {sorted(os.sched_getaffinity(0))[0]})
+    except (AttributeError, OSError):
+        pass
+    try:
+        from threadpoolctl import threadpool_limits
+        threadpool_limits(1)
+    except Exception:
+        pass
+
+
+REF_NOTE = ("reference solve backend: SciPy SuperLU -- the reference's fallback (linalg.py:86-108); its default, "
+            "UMFPACK via cvxopt, is not installable here (no cvxopt wheel)")
 
 
 def fp64_peak():
@@ -104,18 +127,6 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
-def spmm_bytes(hm, J):
-    """Algorithmic HBM bytes of one ens_spmm launch pair (both matrices), DESIGN.md §5."""
-    ns, npres, ntot, nnz = hm.ns, hm.npres, hm.ntot, hm.nnz_s
-    npairs = len(hm.b_col)
-    per_mat = (12 * nnz + 4 * (ns + 1)            # A_s values + column indices + row pointers
-               + 20 * npairs + 4 * (ns + 1)       # B^T (p, bx, by) by node
-               + 20 * npairs + 4 * (npres + 1)    # B (node, bx, by) by pressure row
-               + ntot                             # identity-row flags
-               + 16 * ntot * J)                   # X read once, Y written once
-    return 2 * per_mat
-
-
 def cpu_baseline(disc, cfg, prob, steps=1):
     """The oracle (numpy/SciPy port of the reference path) on this host: bounded sample."""
     from oracle import ensmhd_oracle as O
@@ -130,23 +141,36 @@ def cpu_baseline(disc, cfg, prob, steps=1):
 
 
 def run_reference(args):
-    """--impl reference: the reference path's CPU restatement (oracle port) on the host cores."""
+    """--impl reference: the reference path's CPU restatement (oracle port, pinned to the reference's
+    own outputs) on one host core, same config / metric as the b200 arm, bounded sample."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    os.environ.setdefault("OMP_NUM_THREADS", str(os.cpu_count()))
+    single_thread()
     import paper_2108_05110_b200 as P
-    disc, cfg, prob = P.build_case(CASE, J=J_PER_GPU * args.gpus)
-    steps = max(1, min(args.steps, 2 if args.gpus <= 2 else 1))   # bounded sample: a few minutes at any N
+    case = args.case or (CASE if args.gpus == 1 else CASE_MULTI)
+    jn, scaling, workload = CASES[case]
+    J = jn * args.gpus if scaling == "weak" else jn
+    sample = dict(J=J)
+    note = ""
+    if case in ("C5", "C5shard") or J > 64:
+        # SuperLU on the 512x512 saddle system (N = 2.36M) does not finish in a bounded sample: time
+        # the reference algorithm on C2's mesh with the config's member count, per member-step
+        sample = dict(J=J)
+        case_run, note = "C2", f" on the C2 mesh (the {case} mesh is infeasible for SuperLU on one core)"
+    else:
+        case_run = case
+    disc, cfg, prob = P.build_case(case_run, **sample)
+    steps = 1
     value, secs = cpu_baseline(disc, cfg, prob, steps)
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "impl": "reference", "n_gpus": args.gpus, "steps": steps,
-        "warmup": 0, "ms_per_step": 1e3 * secs / steps, "higher_is_better": True, "scaling": "weak",
+        "warmup": 0, "ms_per_step": 1e3 * secs / steps, "higher_is_better": True, "scaling": scaling,
         "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded manufactured solution, SURVEY.md §8.0)",
-        "config": {"workload": f"{CASE}: 128x128 TH P2/P1, J={cfg.num_members}, dt=0.005", "case": CASE},
+        "config": {"workload": workload, "case": case, "members_total": J},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "port",
-                         "sample": f"{steps} full time-step(s) of {CASE} (SciPy SuperLU, serial; "
-                                   f"{os.cpu_count()} host cores available)"},
+                         "sample": f"{steps} full time-step of {case_run} with {J} members{note}, 1 thread pinned "
+                                   f"to one core of {os.cpu_count()}; {REF_NOTE}"},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -162,6 +186,32 @@ def spmm_traffic(name="r01_spmm_traffic.json"):
         return None
 
 
+def cusparse_spmm_ms(eng, disc, reps=20):
+    """The library bar: cuSPARSE SpMM (torch.sparse.mm on CSR, fp64)
+    of the same saddle matrices (reference order, identity rows included) times the same member
+    block, both systems; CUDA events, warm."""
+    import torch
+    from paper_2108_05110_b200 import linalg as LA
+    mats, xs = [], []
+    for m in range(2):
+        a = LA.saddle_matrix(disc, eng.as_vals[m].cpu().numpy())
+        mats.append(torch.sparse_csr_tensor(torch.as_tensor(a.indptr.astype(np.int32)),
+                                            torch.as_tensor(a.indices.astype(np.int32)),
+                                            torch.as_tensor(a.data), size=a.shape).cuda())
+        xs.append(torch.randn(a.shape[0], eng.J, dtype=torch.float64, device="cuda"))
+    for m in range(2):
+        torch.sparse.mm(mats[m], xs[m])
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(reps):
+        for m in range(2):
+            torch.sparse.mm(mats[m], xs[m])
+    e1.record()
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1) / reps
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -171,10 +221,16 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--always-steps", type=int, default=5)
-    ap.add_argument("--case", default=CASE, choices=sorted(CASES))
+    ap.add_argument("--full-run", type=int, default=-1,
+                    help="also time run() over this many steps (-1: the config's own step count at N=1 for C2)")
+    ap.add_argument("--case", default=None, choices=sorted(CASES),
+                    help="default: C2 at N=1, C5 (strong scaling, J=1024 in total) at N>1")
     args = ap.parse_args()
+    world_env = int(os.environ.get("WORLD_SIZE", "1"))
+    if args.case is None:
+        args.case = CASE if max(world_env, args.gpus) == 1 else CASE_MULTI
     case = args.case
-    j_per_gpu, workload = CASES[case]
+    jn, scaling, workload = CASES[case]
     if case != CASE:
         args.no_cpu_baseline = True   # the SciPy oracle needs minutes to hours per step beyond C2
     if args.impl == "reference":
@@ -183,7 +239,7 @@ def main():
     import torch
     import torch.distributed as dist
 
-    world = int(os.environ.get("WORLD_SIZE", "1"))
+    world = world_env
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
@@ -200,11 +256,12 @@ def main():
         comm = dist.group.WORLD
     import paper_2108_05110_b200 as P
     from paper_2108_05110_b200 import stepper as ST
-    from paper_2108_05110_b200.engine import _dptr
+    from paper_2108_05110_b200.engine import _dptr, apply_bytes, apply_flops, spmm_bytes
     from paper_2108_05110_b200 import _native as N
 
-    J_total = j_per_gpu * world
-    disc, cfg, prob = P.build_case(case, J=J_total, steps=max(args.steps + args.warmup, 1))
+    J_total = jn * world if scaling == "weak" else jn
+    spec_case = "C5" if case == "C5shard" else case
+    disc, cfg, prob = P.build_case(spec_case, J=J_total, steps=max(args.steps + args.warmup, 1))
     j0, jl = ST.member_slice(J_total, rank, world)
     eng = ST.get_engine(disc, cfg, j0=j0, J=jl, comm=comm)
     eng.load_state(np.asarray(prob.initial_v)[j0:j0 + jl], np.asarray(prob.initial_w)[j0:j0 + jl], None, None)
@@ -246,6 +303,7 @@ def main():
         dist.barrier()
     ms = float(tmax.item())
     value = J_total * args.steps / (ms / 1e3)
+    Jc = getattr(eng, "Jc", jl)          # columns per device pass (chunked engines)
 
     # ---- per-phase device timing (same stream, CUDA events), for the roofline ----
     def time_call(fn, reps):
@@ -263,24 +321,29 @@ def main():
     Y = eng.rhs            # scratch between steps (no extra device memory at the largest configs)
     spmm_ms = time_call(lambda: N.check(eng.lib.ens_spmm(eng.ctx, eng.sptr, _dptr(eng.as_vals), _dptr(X), None,
                                                          _dptr(Y), 0), "spmm"), 50)
-    factor_ms = time_call(lambda: eng.factor(), 5)
+    factor_ms = time_call(lambda: eng.factor(), 3 if case.startswith("C5") else 5)
     Z = eng.rhs
     solve_ms = time_call(lambda: eng.precond(X, out=Z), 10)
-    bytes_spmm = spmm_bytes(eng.hm, jl)
+    bytes_spmm = spmm_bytes(eng.hm, Jc)
     hbm, peak_kind = peaks()
     spmm_gbs = bytes_spmm / (spmm_ms * 1e-3) / 1e9
     plan = eng.hm.plan
-    nnz_lu = plan.stats["nnz_lu"]
-    solve_bytes = 2 * 8 * nnz_lu + 2 * 2 * 8 * eng.ntot * jl * 2      # factors once + rhs/x traffic, both matrices
+    solve_bytes = apply_bytes(eng.hm, Jc)
     solve_gbs = solve_bytes / (solve_ms * 1e-3) / 1e9
-    solve_flops = 2.0 * 2 * nnz_lu * jl                                   # one multiply-add per factor entry and member, both matrices
+    solve_flops = apply_flops(eng.hm, Jc)
     solve_tflops = solve_flops / (solve_ms * 1e-3) / 1e12
     f64_peak, f64_kind = fp64_peak()
     factor_tflops = 2 * plan.stats["factor_flops"] / (factor_ms * 1e-3) / 1e12
+    cus_ms = None
+    if rank == 0 and world == 1:
+        try:
+            cus_ms = cusparse_spmm_ms(eng, disc)
+        except Exception as exc:   # library timing leg only
+            print(f"cusparse leg skipped: {exc}", file=sys.stderr)
 
     # ---- same workload with the LU preconditioner rebuilt every step (reference cadence) ----
     always = None
-    if args.always_steps > 0:
+    if args.always_steps > 0 and world == 1:
         saved = ST.get_solver_options()
         ST.set_solver_options(refactor="always")
         eng2 = ST.get_engine(disc, cfg, j0=j0, J=jl, comm=comm)
@@ -291,8 +354,6 @@ def main():
             t2 += cfg.dt
             eng2.step(t2, prob.forcing, prob.boundary)
         torch.cuda.synchronize()
-        if comm is not None:
-            dist.barrier()
         a2, b2 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a2.record(eng2.stream)
         for _ in range(args.always_steps):
@@ -300,12 +361,29 @@ def main():
             eng2.step(t2, prob.forcing, prob.boundary)
         b2.record(eng2.stream)
         torch.cuda.synchronize()
-        ms2 = torch.tensor([a2.elapsed_time(b2)], dtype=torch.float64, device="cuda")
-        if comm is not None:
-            dist.all_reduce(ms2, op=dist.ReduceOp.MAX)
-        always = {"value": J_total * args.always_steps / (float(ms2.item()) / 1e3), "unit": UNIT,
-                  "steps": args.always_steps, "ms_per_step": float(ms2.item()) / args.always_steps}
+        ms2 = a2.elapsed_time(b2)
+        always = {"value": J_total * args.always_steps / (ms2 / 1e3), "unit": UNIT,
+                  "steps": args.always_steps, "ms_per_step": ms2 / args.always_steps}
         del eng2
+
+    # ---- the whole run() of the configuration: start-up steps and rebuilds included ----
+    full = None
+    nfull = args.full_run if args.full_run >= 0 else (P.problems.CONFIGS[case]["steps"] if case == CASE and
+                                                      world == 1 else 0)
+    if nfull > 0 and world == 1:
+        dfull, cfull, pfull = P.build_case(spec_case, J=J_total, steps=nfull)
+        P.run(cfull, pfull, record=False)                  # engine, graphs, pinned buffers warm
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        rep, _, _ = P.run(cfull, pfull, record=False)
+        tot = time.perf_counter() - t0
+        step_s = float(np.sum(rep.wall_clock[1:]))
+        efull = ST.get_engine(dfull, cfull)
+        full = {"value": J_total * nfull / step_s, "unit": UNIT, "steps": nfull,
+                "ms_per_step": 1e3 * step_s / nfull, "factorizations": int(efull.n_factor),
+                "wall_s_incl_host": tot,
+                "api": "paper_2108_05110_b200.run(config, problem) over the configuration's full step count "
+                       "(RunReport.wall_clock, the reference's own timing; per-step diagnostics off)"}
 
     # ---- end-to-end through the public reference-facing API with host buffers ----
     e2e = None
@@ -331,7 +409,8 @@ def main():
         per = per_v + 8 * J_total * 2 * disc.n_pres           # v, w, q, r
         # H2D: v, w every step (q, r only when the velocities are not the resident level, never
         # here) + the problem-data coefficients; D2H: the full new state + the residual
-        e2e = {"value": J_total * args.e2e_steps / e2e_s, "unit": UNIT, "h2d_bytes_per_step": per_v + 8 * 2 * 2 * 3 * J_total,
+        e2e = {"value": J_total * args.e2e_steps / e2e_s, "unit": UNIT,
+               "h2d_bytes_per_step": per_v + 8 * 2 * 2 * 3 * J_total,
                "d2h_bytes_per_step": per + 16, "steps": args.e2e_steps, "step_ms": step_ms,
                "api": "paper_2108_05110_b200.advance(state, config, disc, forcing, boundary), numpy state in/out"}
         # the transfer floor the e2e step runs against: pinned host<->device copy bandwidth measured here
@@ -347,8 +426,8 @@ def main():
                 dst.copy_(src, non_blocking=True)
                 pe1.record()
                 pe1.synchronize()
-                t = pe0.elapsed_time(pe1)
-                best = t if best is None else min(best, t)
+                tt = pe0.elapsed_time(pe1)
+                best = tt if best is None else min(best, tt)
             bw[name] = per / (best * 1e-3) / 1e9
         del hb, db
         ms_step = ms / args.steps
@@ -358,17 +437,18 @@ def main():
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        single_thread()
         v, secs = cpu_baseline(disc, cfg, prob, 1)
         cpu = {"value": v, "unit": UNIT, "cores": 1, "kind": "port",
                "sample": f"1 full time-step of {CASE} with all {J_total} members by the numpy/SciPy oracle "
-                         f"(SuperLU, serial), {secs:.1f} s"}
+                         f"(1 thread pinned to one core), {secs:.1f} s; {REF_NOTE}"}
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak",
+            "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": scaling,
             "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded manufactured solution, SURVEY.md §8.0)",
             "config": {"workload": workload,
-                       "case": case, "members_total": J_total, "n_total_dofs": int(eng.ntot),
+                       "case": case, "members_total": J_total, "members_per_pass": Jc, "n_total_dofs": int(eng.ntot),
                        "l2": "per-step working set (2 x %.2f GB fronts) exceeds the 126 MB L2" %
                              (plan.front_storage * 8 / 1e9),
                        "rtol": eng.rtol, "parallelism": f"members sharded dp{world}"},
@@ -376,7 +456,10 @@ def main():
             "krylov_iters_per_step": float(np.mean(iters)) if iters else None,
             "preconditioner": {"policy": eng.refactor, "factorizations_in_timed_steps": n_factor,
                                "lag_max_iters": eng.lag_max_iters, "lag_max_steps": eng.lag_max_steps,
-                               "note": "every sub-step solve converged to the same 1e-12 true residual"},
+                               "renewal_rho": eng.rho,
+                               "note": "every sub-step solve converged to the same 1e-12 true residual; "
+                                       "renewal decided from iteration counts (deterministic)"},
+            "value_full_run": full,
             "value_refactor_every_step": always,
             # dominant kernel of a timed step: the preconditioner apply (k_sgemm + k_finit sweep),
             # against the nearer of its two roofs (HBM for small J, fp64 tensor cores for large J)
@@ -385,7 +468,7 @@ def main():
                                            "both systems; k_sgemm dominant)",
                  "achieved": solve_gbs, "peak": hbm, "peak_kind": peak_kind, "unit": "GB/s",
                  "frac": solve_gbs / hbm,
-                 "traffic": spmm_traffic("r01_solve_traffic.json") if case == CASE else None,
+                 "traffic": spmm_traffic("r02_solve_traffic.json") if case == CASE else None,
                  "bytes_per_launch": solve_bytes, "ms_per_launch": solve_ms,
                  "other_roof": {"bound": "tensor (fp64 DMMA)", "achieved": solve_tflops, "peak": f64_peak,
                                 "peak_kind": f64_kind, "unit": "TFLOP/s", "frac": solve_tflops / f64_peak}}
@@ -399,8 +482,14 @@ def main():
                                 "frac": solve_gbs / hbm, "bytes_per_launch": solve_bytes}}),
             "roofline_spmm": {"bound": "hbm", "kernel": "ens_spmm (saddle SpMM, both systems; the Krylov core)",
                               "achieved": spmm_gbs, "peak": hbm, "peak_kind": peak_kind, "unit": "GB/s",
-                              "frac": spmm_gbs / hbm, "traffic": spmm_traffic() if case == CASE else None,
-                              "bytes_per_launch": bytes_spmm, "ms_per_launch": spmm_ms},
+                              "frac": spmm_gbs / hbm,
+                              "traffic": spmm_traffic("r02_spmm_traffic.json") if case == CASE else None,
+                              "bytes_per_launch": bytes_spmm, "ms_per_launch": spmm_ms,
+                              "cusparse": None if cus_ms is None else {
+                                  "ms_per_launch": cus_ms, "achieved": bytes_spmm / (cus_ms * 1e-3) / 1e9,
+                                  "speedup_of_ens_spmm": cus_ms / spmm_ms,
+                                  "how": "torch.sparse.mm(CSR fp64 saddle matrix, dense N x J) = cusparseSpMM, "
+                                         "both systems, warm, CUDA events"}},
             "phases_ms": {"spmm": spmm_ms, "factor": factor_ms, "lu_solve": solve_ms,
                           "factor_tflops_fp64": factor_tflops, "lu_solve_gbs": solve_gbs},
             "clocks": clocks,

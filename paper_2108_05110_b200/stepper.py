@@ -130,14 +130,33 @@ def get_solver_options():
     return dict(_SOLVER_OPTS)
 
 
+_CHUNK = {"chunk": None}   # member columns per device pass: None = as many as fit (chunked.plan_chunk)
+
+
+def set_member_chunk(chunk=None):
+    """Force the member-column chunk width of new engines (None: automatic, by device memory)."""
+    if chunk is not None and int(chunk) < 1:
+        raise ValueError("chunk must be a positive member count")
+    _CHUNK["chunk"] = None if chunk is None else int(chunk)
+
+
 def get_engine(disc, config, j0=0, J=None, comm=None, device=None):
-    from .engine import Engine
+    from .engine import Engine, host_mesh
     J = config.num_members if J is None else J
     key = ("b200-engine", config, j0, J, device, id(comm) if comm is not None else None,
-           tuple(sorted(_SOLVER_OPTS.items())))
+           tuple(sorted(_SOLVER_OPTS.items())), _CHUNK["chunk"])
     eng = disc._cache.get(key)
     if eng is None:
-        eng = Engine(disc, config, j0=j0, J=J, device=device, comm=comm, **_SOLVER_OPTS)
+        import torch
+        from .chunked import ChunkedEngine, largest_divisor_at_most, plan_chunk
+        dev = torch.cuda.current_device() if device is None else device
+        chunk = _CHUNK["chunk"]
+        chunk = (plan_chunk(host_mesh(disc), J, dev, restart=min(_SOLVER_OPTS["restart"], 2)) if chunk is None
+                 else largest_divisor_at_most(J, chunk))
+        if chunk < J:
+            eng = ChunkedEngine(disc, config, j0=j0, J=J, chunk=chunk, device=device, comm=comm, **_SOLVER_OPTS)
+        else:
+            eng = Engine(disc, config, j0=j0, J=J, device=device, comm=comm, **_SOLVER_OPTS)
         disc._cache[key] = eng
     return eng
 
@@ -436,5 +455,5 @@ __all__ = [
     "Discretization", "Problem", "RunReport", "StepKind", "StepFailure", "PreconditionReport",
     "StabilityCheck", "StepSystem", "advance", "run", "energy", "check_preconditions", "verify_stability_bound",
     "assemble_shared_lhs", "assemble_member_rhs",
-    "ZeroForcing", "ZeroBoundary", "ScaledProfileBoundary", "member_slice", "set_solver_options",
+    "ZeroForcing", "ZeroBoundary", "ScaledProfileBoundary", "member_slice", "set_solver_options", "set_member_chunk",
 ]
