@@ -218,6 +218,12 @@ int  ens_epilogue(ens_ctx* ctx, void* stream, const double* x, double* p_out);
  *   [2+3J..] = w_j^T K w_j, [2+4J..] = ||div v_j||^2, [2+5J..] = ||div w_j||^2 */
 int  ens_diagnostics(ens_ctx* ctx, void* stream, const double* x, const double* means, double* out);
 
+/* Squared errors of the ensemble means against a separable exact field (device):
+ * out = [d_v^T M d_v, d_v^T K d_v, d_w^T M d_w, d_w^T K d_w], d = <z> - sum_k coef[fam][k] basis[k]
+ * (exact->rows = n_vel internal rows, exact->coef = 2 x K): the summands of the discrete
+ * L2(0,T;H1) error norm of experiments.error_norm_21 (experiments.py:59-73, fem.py:502-505). */
+int  ens_mean_error(ens_ctx* ctx, void* stream, const double* means, const ens_data_desc* exact, double* out);
+
 #ifdef __cplusplus
 }
 #endif

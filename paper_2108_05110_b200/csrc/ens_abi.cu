@@ -121,6 +121,13 @@ void ens_destroy(ens_ctx* c) {
     cudaFree(c->partial);
     cudaFree(c->ticket);
     cudaFree(c->sitem);
+    cudaFree(c->sstream);
+    cudaFree(c->stiles);
+    cudaFree(c->scta);
+    cudaFree(c->sfr);
+    cudaFree(c->sbg_rows);
+    cudaFree(c->ssc_off);
+    cudaFree(c->ssc_row);
     cudaFree(c->finit_rows);
     cudaFree(c->ec);
     cudaFree(c->nrm_part);
@@ -219,6 +226,13 @@ int ens_precond_apply(ens_ctx* c, void* stream, const double* r, double* z) {
 int ens_epilogue(ens_ctx* c, void* stream, const double* x, double* p_out) {
     if (!c || !x || !p_out) return ENS_EINVAL;
     return launch_epilogue(c, (cudaStream_t)stream, x, p_out);
+}
+
+int ens_mean_error(ens_ctx* c, void* stream, const double* means, const ens_data_desc* exact, double* out) {
+    if (!c || !means || !exact || !out || exact->K < 1 || !exact->basis || !exact->coef ||
+        exact->rows != (int64_t)c->n_vel)
+        return ENS_EINVAL;
+    return launch_mean_error(c, (cudaStream_t)stream, means, exact, out);
 }
 
 int ens_diagnostics(ens_ctx* c, void* stream, const double* x, const double* means, double* out) {

@@ -67,6 +67,23 @@ struct ens_ctx {
     double* partial = nullptr;     // split-K partial products of the solve GEMMs
     int* ticket = nullptr;         // split-K arrival counters (last CTA reduces)
     int4* sitem = nullptr;         // solve work items with their front's geometry (3 x int4 per item)
+    // streamed solve (ens_mfsolve.cu, "stream" path): factor entries re-laid out per work tile in
+    // DMMA fragment order after each factorisation, read by bulk copies in a producer/consumer pipeline
+    int stream_mode = -1;          // -1 undecided, 0 classic k_sgemm path, 1 streamed
+    double* sstream = nullptr;     // [2][stream_len] packed factor tiles
+    int64_t stream_len = 0;        // doubles per system
+    void* stiles = nullptr;        // STile[n]
+    int64_t n_stiles = 0;
+    int32_t* scta = nullptr;       // per launch: CTA unit offsets
+    std::vector<int64_t> slaunch;  // per launch: (dir, level, cta_off index, ngrid)
+    double* sfr = nullptr;         // blocked front vectors [2][ncb][n_idx][ldb]
+    int32_t* sbg_rows = nullptr;   // per level: pivot rows the forward assembly fills
+    std::vector<int64_t> sbg_off;  // level offsets into sbg_rows
+    int32_t* ssc_off = nullptr;    // per front-row position: backward scatter targets (CSR offsets)
+    int32_t* ssc_row = nullptr;    // descendants' contribution rows holding the same dof
+    int scw = 0, sncb = 0, sldb = 0, snst = 0, skc = 0;
+    size_t sstage = 0;
+    size_t sdesc = 0;              // shared-memory bytes for a CTA's tile descriptors
     double* nrm_part = nullptr;    // fused residual-norm partials of the SpMM
     double* diag_part = nullptr;   // per-block partials of the diagnostics (launch_diagnostics)
     size_t diag_part_n = 0;
@@ -103,6 +120,7 @@ int launch_spmm_resnorm(ens_ctx* c, cudaStream_t s, const double* as_vals, const
                         double* y, double* bn2, double* rn2);
 int launch_epilogue(ens_ctx* c, cudaStream_t s, const double* x, double* p_out);
 int launch_diagnostics(ens_ctx* c, cudaStream_t s, const double* x, const double* means, double* out);
+int launch_mean_error(ens_ctx* c, cudaStream_t s, const double* means, const ens_data_desc* exact, double* out);
 int launch_copy_cons(ens_ctx* c, cudaStream_t s, const double* src, double* dst);
 // column reductions: out[mat][l][j] = sum_r A_l[mat][r][j] * B[mat][r][j]; A_l = A + l*lstride
 int launch_coldot(ens_ctx* c, cudaStream_t s, const double* A, int64_t lstride, int L, const double* B,
@@ -115,6 +133,9 @@ int launch_axpy_norm(ens_ctx* c, cudaStream_t s, double* W, const double* V, int
 int mf_factor(ens_ctx* c, cudaStream_t s, const double* as_vals, int32_t* n_pert);
 int mf_solve(ens_ctx* c, cudaStream_t s, const double* r, double* z);
 int mf_setup(ens_ctx* c);
+int mf_stream_pack(ens_ctx* c, cudaStream_t s);   // after a factorisation (no-op on the classic path)
+int mf_stream_prepare(ens_ctx* c);                 // tiles + stream buffer, before any capture
+bool mf_stream_on(ens_ctx* c);
 
 // ---- Krylov (ens_krylov.cu) ----
 int gmres_solve(ens_ctx* c, cudaStream_t s, const double* as_vals, const double* rhs, double* x, double rtol,

@@ -1174,6 +1174,76 @@ __global__ void k_mean_energy(const int32_t* __restrict__ rp, const int32_t* __r
     }
 }
 
+// Error of the ensemble means against a separable exact field, in the mass and stiffness forms
+// (the squared H1 norm of the mean error, experiments.py:59-73 / fem.py:502-505):
+//   d = <z> - sum_k coef[fam][k] basis[k]   (internal order, both components interleaved)
+//   part[(fam*2 + 0)][blk] = d^T M d,  part[(fam*2 + 1)][blk] = d^T K d   (M, K per component)
+// Fixed row partition and block order: deterministic.
+__global__ void k_mean_error(const int32_t* __restrict__ rp, const int32_t* __restrict__ col,
+                             const double* __restrict__ mass, const double* __restrict__ stiff,
+                             const double* __restrict__ means, int ns, const double* __restrict__ basis,
+                             const double* __restrict__ coef, int K, double* __restrict__ part) {
+    __shared__ double red[2][256];
+    const int fam = blockIdx.y;
+    const int64_t nv = 2LL * ns;
+    const double* m = means + (int64_t)fam * nv;
+    const double* cf = coef + (int64_t)fam * K;
+    auto d = [&](int64_t r) {
+        double v = m[r];
+        for (int k = 0; k < K; ++k) v -= cf[k] * basis[(int64_t)k * nv + r];
+        return v;
+    };
+    const int64_t per = ((int64_t)ns + gridDim.x - 1) / gridDim.x;
+    const int64_t n0 = (int64_t)blockIdx.x * per, n1 = min((int64_t)ns, n0 + per);
+    double am = 0.0, ak = 0.0;
+    for (int64_t i = n0 + threadIdx.x; i < n1; i += blockDim.x) {
+        for (int cc = 0; cc < 2; ++cc) {
+            double sm = 0.0, sk = 0.0;
+            for (int k = rp[i]; k < rp[i + 1]; ++k) {
+                const double dj = d(2LL * col[k] + cc);
+                sm += mass[k] * dj;
+                sk += stiff[k] * dj;
+            }
+            const double di = d(2 * i + cc);
+            am += di * sm;
+            ak += di * sk;
+        }
+    }
+    red[0][threadIdx.x] = am;
+    red[1][threadIdx.x] = ak;
+    __syncthreads();
+    if (threadIdx.x < 2) {
+        double t = 0.0;
+        for (int k = 0; k < (int)blockDim.x; ++k) t += red[threadIdx.x][k];
+        part[(int64_t)(fam * 2 + threadIdx.x) * gridDim.x + blockIdx.x] = t;
+    }
+}
+
+__global__ void k_mean_error_fin(const double* __restrict__ part, int nblk, double* __restrict__ out) {
+    const int t = threadIdx.x;
+    if (t >= 4) return;
+    double s = 0.0;
+    for (int b = 0; b < nblk; ++b) s += part[(int64_t)t * nblk + b];
+    out[t] = s;
+}
+
+int launch_mean_error(ens_ctx* c, cudaStream_t s, const double* means, const ens_data_desc* exact, double* out) {
+    const int RB = 148 * 2;
+    const size_t need = (size_t)RB * 4;
+    if (c->diag_part_n < need) {
+        cudaFree(c->diag_part);
+        c->diag_part = nullptr;
+        ENS_CK(cudaMalloc(&c->diag_part, sizeof(double) * need));
+        c->diag_part_n = need;
+    }
+    k_mean_error<<<dim3(RB, 2), 256, 0, s>>>(c->m.s_rowptr, c->m.s_col, c->m.s_mass, c->m.s_stiff, means, c->m.ns,
+                                            exact->basis, exact->coef, exact->K, c->diag_part);
+    ENS_CKL();
+    k_mean_error_fin<<<1, 32, 0, s>>>(c->diag_part, RB, out);
+    ENS_CKL();
+    return ENS_OK;
+}
+
 // Per-member quadratic forms by element quadrature, thread per (element, member), per-block
 // partials part[blk][6][J]: v.Mv, w.Mw, v.Kv, w.Kw (K applied per component), ||div v||^2, ||div w||^2.
 // The 7-point rule integrates the P2 mass (degree 4) and stiffness (degree 2) integrands exactly,

@@ -543,6 +543,11 @@ static int mf_factor_launches(ens_ctx* c, cudaStream_t s, const double* as_vals,
         ENS_CKL();
         ++cnt;
     }
+    {   // streamed solve: factor entries re-laid out per work tile (ens_mfsolve.cu)
+        const int rc = mf_stream_pack(c, s);
+        if (rc != ENS_OK) return rc;
+        if (c->stiles) ++cnt;
+    }
     *nlaunch = cnt;
     return ENS_OK;
 }
@@ -550,6 +555,10 @@ static int mf_factor_launches(ens_ctx* c, cudaStream_t s, const double* as_vals,
 // The factorisation's launch sequence is fixed per mesh: capture it once into a
 // CUDA graph (keyed on the value buffer) and replay it every sub-step.
 int mf_factor(ens_ctx* c, cudaStream_t s, const double* as_vals, int32_t* n_pert) {
+    {
+        const int rc = mf_stream_prepare(c);   // allocations happen outside any graph capture
+        if (rc != ENS_OK) return rc;
+    }
     const char* e = std::getenv("ENS_NO_GRAPH");
     const bool graphs = !(e && e[0] == '1') && s != 0;
     if (!graphs) {

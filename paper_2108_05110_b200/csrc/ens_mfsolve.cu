@@ -458,6 +458,697 @@ static cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, siz
     return cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
 }
 
+#ifndef RET
+#define RET(x)                         \
+    do {                               \
+        int rc_ = (x);                 \
+        if (rc_ != ENS_OK) return rc_; \
+    } while (0)
+#endif
+
+// ===========================================================================
+// Streamed solve (default for even J): the same forward / backward products,
+// restructured as a pure HBM stream.
+//
+//  * Work tiles of <= 32 rows (4 groups of 8) x the front's whole inner range,
+//    built once per plan.  After every factorisation k_stream_pack copies each
+//    tile's factor entries out of the fronts into one contiguous stream per
+//    system, in the exact order the DMMA A-fragments consume them: for k-step u
+//    (4 inner columns) and row group w, the 32 values A[8w+g][4u+q] in lane order
+//    (g = lane/4, q = lane%4); padding is zero.  A warp's fragment load is then
+//    one conflict-free 256-byte shared-memory read, and a chunk of KC inner
+//    columns of a tile is one contiguous cp.async.bulk copy.
+//  * Front vectors live in their own blocked layout FRS[system][column block]
+//    [row][ldb] (ldb >= the block's columns, = 4 mod 16: conflict-free DMMA
+//    B-fragment reads), so a chunk's B operand -- consecutive front rows -- is
+//    one contiguous region: the forward pivot rows assembled by s_finit, and in
+//    the backward sweep the front's rows after s_bgather has copied the
+//    ancestors' solution rows x[C] next to fr[P].
+//  * Persistent CTAs per level launch: one producer warp streams stages
+//    (A chunk + B rows, two cp.async.bulk copies) through an mbarrier ring,
+//    running several tiles ahead of the four consumer warps, which accumulate
+//    with mma.sync m8n8k4 (fp64 tensor cores) and store their rows.  Units
+//    (tile, system, column block) are split over the CTAs in contiguous ranges
+//    of equal bytes (host side), so per-tile latency is hidden by the pipeline
+//    instead of by CTA count.
+//  * Every output element sums its inner range in a fixed order (k-step by
+//    k-step): deterministic, identical columns stay identical.
+// ===========================================================================
+namespace {
+
+struct STile {
+    int a_lo, a_hi;   // offset (doubles) of the tile in its system's stream
+    int fo;           // front's first index-list position (f_idx_off)
+    int K;            // inner length (fwd: k, bwd: m)
+    int kp;           // pivot count k of the front
+    int r0;           // first row of the tile (fwd: within the C rows, bwd: within the pivots)
+    int ng;           // row groups of 8 (1..4)
+    int flags;        // bit0: backward, bit1: forward init rows carry children's contributions
+    int src_lo, src_hi;   // front's storage offset (f_off)
+    int m;            // front size
+    int row0;         // first front row of the tile
+    int kb, ke;       // inner range of the unit ([0, K))
+};
+static_assert(sizeof(STile) == 56, "STile layout");
+
+constexpr int ST_ROWS = 32;     // rows per tile
+constexpr int ST_MAXST = 12;    // pipeline stages (upper bound)
+constexpr int ST_THREADS = 160; // 4 consumer warps + 1 producer warp
+constexpr int ST_CTAS = 4;      // resident CTAs per SM (shared memory per CTA sized for it)
+
+__device__ __forceinline__ uint32_t st_smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void st_mbar_init(uint32_t bar, int count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
+}
+__device__ __forceinline__ void st_mbar_expect_tx(uint32_t bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void st_mbar_arrive(uint32_t bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ void st_mbar_wait(uint32_t bar, uint32_t parity) {
+    uint32_t done;
+    do {
+        asm volatile(
+            "{\n\t.reg .pred p;\n\t"
+            "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+            "selp.u32 %0, 1, 0, p;\n\t}"
+            : "=r"(done)
+            : "r"(bar), "r"(parity)
+            : "memory");
+    } while (!done);
+}
+__device__ __forceinline__ void st_bulk_g2s(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+                 "l"(src), "r"(bytes), "r"(bar)
+                 : "memory");
+}
+__device__ __forceinline__ double st_lds(uint32_t a) {
+    double v;
+    asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(a));
+    return v;
+}
+__device__ __forceinline__ int64_t st_i64(int lo, int hi) { return (int64_t)(unsigned)lo | ((int64_t)hi << 32); }
+
+}  // namespace
+
+#ifdef ST_PROBE   // diagnostic build: per-CTA timeline of consumer warp 0 (wait vs. work), launch 0 only
+__device__ unsigned long long g_stp[2048][6];
+__device__ __forceinline__ unsigned long long st_gt() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+__device__ unsigned long long g_lvl[256][2];   // per launch id: first CTA start, last CTA end
+__device__ int g_probe_target;                 // launch id whose per-CTA consumer timeline is kept
+extern "C" int ens_stream_probe_target(int id) { return (int)cudaMemcpyToSymbol(g_probe_target, &id, sizeof(int)); }
+__device__ __forceinline__ void st_span_begin(int id) {
+    if (threadIdx.x == 0 && id >= 0 && id < 256) atomicMin(&g_lvl[id][0], st_gt());
+}
+__device__ __forceinline__ void st_span_end(int id) {   // every thread: the last one out sets the end
+    if (id >= 0 && id < 256) atomicMax(&g_lvl[id][1], st_gt());
+}
+extern "C" int ens_stream_probe_reset() {
+    static unsigned long long h[256][2];
+    for (int i = 0; i < 256; ++i) {
+        h[i][0] = ~0ull;
+        h[i][1] = 0;
+    }
+    return (int)cudaMemcpyToSymbol(g_lvl, h, sizeof(h));
+}
+extern "C" int ens_stream_probe_levels(const char* path) {
+    static unsigned long long h[256][2];
+    cudaDeviceSynchronize();
+    cudaMemcpyFromSymbol(h, g_lvl, sizeof(h));
+    FILE* f = fopen(path, "w");
+    if (!f) return -1;
+    for (int i = 0; i < 256; ++i) fprintf(f, "%d %llu %llu\n", i, h[i][0], h[i][1]);
+    fclose(f);
+    return 0;
+}
+extern "C" int ens_stream_probe_dump(const char* path) {
+    static unsigned long long h[2048][6];
+    cudaDeviceSynchronize();
+    cudaMemcpyFromSymbol(h, g_stp, sizeof(h));
+    FILE* f = fopen(path, "w");
+    if (!f) return -1;
+    for (int i = 0; i < 2048; ++i)
+        fprintf(f, "%d %llu %llu %llu %llu %llu %llu\n", i, h[i][0], h[i][1], h[i][2], h[i][3], h[i][4], h[i][5]);
+    fclose(f);
+    return 0;
+}
+#define ST_SPAN_BEGIN(id) st_span_begin(id)
+#define ST_SPAN_END(id) st_span_end(id)
+#else
+#define ST_SPAN_BEGIN(id)
+#define ST_SPAN_END(id)
+#endif
+
+// factor entries -> fragment-ordered tile stream (one CTA per tile and system)
+__global__ void __launch_bounds__(256) k_stream_pack(const STile* __restrict__ tiles, const double* __restrict__ F,
+                                                     int64_t storage, double* __restrict__ S, int64_t slen) {
+    const STile T = tiles[blockIdx.x];
+    const int mat = blockIdx.y;
+    const int Kp = (T.K + 3) & ~3;
+    const int rows_total = (T.flags & 1) ? T.kp : T.m - T.kp;
+    const int nr = min(ST_ROWS, rows_total - T.r0);
+    const double* base = F + (int64_t)mat * storage + st_i64(T.src_lo, T.src_hi);
+    double* out = S + (int64_t)mat * slen + st_i64(T.a_lo, T.a_hi);
+    const int total = Kp * T.ng * 8;
+    for (int e = threadIdx.x; e < total; e += blockDim.x) {
+        const int lane = e & 31, grp = e >> 5;
+        const int u = grp / T.ng, w = grp - u * T.ng;
+        const int r = 8 * w + (lane >> 2), col = 4 * u + (lane & 3);
+        out[e] = (r < nr && col < T.K) ? base[(int64_t)(T.row0 + r) * T.m + col] : 0.0;
+    }
+}
+
+// One level and direction of the streamed solve; units [cta_off[b], cta_off[b+1]) per CTA,
+// unit u = (tile * 2 + system) * ncb + column block.
+template <int NCT, int KC>
+__global__ void __launch_bounds__(ST_THREADS, ST_CTAS)
+    k_stream_gemm(const STile* __restrict__ tiles, int tile0, const int32_t* __restrict__ cta_off, int ncb, int cw,
+                  int ldb, const double* __restrict__ S, int64_t slen, double* __restrict__ FRS,
+                  const SolveIO* __restrict__ io, const int32_t* __restrict__ fidx,
+                  const int32_t* __restrict__ gsrc, const int32_t* __restrict__ sc_off,
+                  const int32_t* __restrict__ sc_row, int64_t N, int J, int64_t nidx, int nst,
+                  uint32_t stage_bytes, int probe_id) {
+    extern __shared__ __align__(128) unsigned char smem[];
+    ST_SPAN_BEGIN(probe_id);
+    __shared__ __align__(8) uint64_t bars[2 * ST_MAXST];   // full[0..nst), empty[ST_MAXST..)
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t sbase = st_smem_u32(smem);
+    const uint32_t bbase = st_smem_u32(bars);
+    constexpr uint32_t A_BYTES = KC * ST_ROWS * 8;        // A region of a stage (max)
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < nst; ++s) {
+            st_mbar_init(bbase + 8 * s, 1);
+            st_mbar_init(bbase + 8 * (ST_MAXST + s), 4);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    // B regions start finite (rows past a tile's inner range meet zero A entries: 0 * finite = 0)
+    for (uint32_t i = threadIdx.x; i < (uint32_t)nst * stage_bytes / 8; i += blockDim.x)
+        reinterpret_cast<double*>(smem)[i] = 0.0;
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    // this CTA's tile descriptors into shared memory (static data: before the dependency wait), so
+    // neither the producer nor the consumers pay a global-load latency per unit
+    const int ub = cta_off[blockIdx.x], ue = cta_off[blockIdx.x + 1];
+    const int per_tile = 2 * ncb;
+    STile* sT = reinterpret_cast<STile*>(smem + (size_t)nst * stage_bytes);
+    const int tb = ub / per_tile, te = ue > ub ? (ue - 1) / per_tile + 1 : tb;
+    for (int i = threadIdx.x; i < (te - tb) * (int)(sizeof(STile) / 4); i += blockDim.x)
+        reinterpret_cast<int*>(sT)[i] = __ldg(reinterpret_cast<const int*>(tiles + tile0 + tb) + i);
+    __syncthreads();
+    pdl_trigger();
+#ifdef ST_PROBE
+    const unsigned long long tp0 = st_gt();
+    unsigned long long twait = 0, nwait = 0;
+#endif
+    pdl_wait();   // front rows / the iterate come from the previous launch
+#ifdef ST_PROBE
+    const unsigned long long tp1 = st_gt();
+#endif
+    if (warp == 4) {
+        // ---------------- producer (one lane issues; the others idle) ----------------
+        if (lane != 0) return;
+        int s = 0;
+        uint32_t ph = 0;
+        for (int u = ub; u < ue; ++u) {
+            const STile& T = sT[u / per_tile - tb];
+            const int mat = (u % per_tile) / ncb, cb = u % ncb;
+            const double* Ab = S + (int64_t)mat * slen + st_i64(T.a_lo, T.a_hi);
+            const double* Bb = FRS + ((int64_t)(mat * ncb + cb) * nidx + T.fo) * ldb;
+            const int nch = (T.ke - T.kb + KC - 1) / KC;
+            for (int c = 0; c < nch; ++c) {
+                const int k0 = T.kb + c * KC, kr = min(KC, T.ke - k0);
+                const uint32_t a_bytes = (uint32_t)((kr + 3) >> 2) * T.ng * 256u;
+                const uint32_t b_bytes = (uint32_t)kr * ldb * 8u;
+                st_mbar_wait(bbase + 8 * (ST_MAXST + s), ph ^ 1);
+                const uint32_t full = bbase + 8 * s;
+                const uint32_t st = sbase + (uint32_t)s * stage_bytes;
+                st_mbar_expect_tx(full, a_bytes + b_bytes);
+                st_bulk_g2s(st, Ab + (int64_t)k0 * T.ng * 8, a_bytes, full);
+                st_bulk_g2s(st + A_BYTES, Bb + (int64_t)k0 * ldb, b_bytes, full);
+                s = s + 1 == nst ? 0 : s + 1;
+                if (s == 0) ph ^= 1;
+            }
+        }
+        return;
+    }
+    // ---------------- consumers (warps 0..3: row group = warp) ----------------
+    const int g = lane >> 2, q = lane & 3;
+    int s = 0;
+    uint32_t ph = 0;
+    for (int u = ub; u < ue; ++u) {
+        const STile T = sT[u / per_tile - tb];
+        const int mat = (u % per_tile) / ncb, cb = u % ncb;
+        const int j0 = cb * cw, jn = min(cw, J - j0);
+        const bool bwd = T.flags & 1;
+        const int rows_total = bwd ? T.kp : T.m - T.kp;
+        const int nr = min(ST_ROWS, rows_total - T.r0);
+        const int row = 8 * warp + g;
+        const bool active = warp < T.ng;
+        const bool row_ok = active && row < nr;
+        // epilogue operands in flight during the mainloop
+        double* FRm = FRS + (int64_t)(mat * ncb + cb) * nidx * ldb;
+        double* out_row = nullptr;
+        int sc0 = 0, sc1 = 0;   // backward: descendants' contribution rows this row's solution fills
+        double init[NCT][2];
+#pragma unroll
+        for (int ct = 0; ct < NCT; ++ct) init[ct][0] = init[ct][1] = 0.0;
+        if (row_ok) {
+            const int64_t prow = T.fo + T.r0 + row + (bwd ? 0 : T.kp);
+            if (bwd) {
+                out_row = io->z + (int64_t)mat * N * J + (int64_t)__ldg(fidx + prow) * J + j0;
+                sc0 = __ldg(sc_off + prow);
+                sc1 = __ldg(sc_off + prow + 1);
+            } else {
+                out_row = FRm + prow * ldb;
+                if (T.flags & 2) {   // children's contribution rows mapped onto this row (<= 4)
+                    const int4 gs = *reinterpret_cast<const int4*>(gsrc + 4 * prow);
+                    const int src[4] = {gs.x, gs.y, gs.z, gs.w};
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) {
+                        if (src[u] < 0) break;
+                        const double* pr = FRm + (int64_t)src[u] * ldb;
+#pragma unroll
+                        for (int ct = 0; ct < NCT; ++ct)
+#pragma unroll
+                            for (int e = 0; e < 2; ++e) init[ct][e] += pr[min(8 * ct + 2 * q + e, ldb - 1)];
+                    }
+                }
+            }
+        }
+        // two accumulator sets (even / odd k-steps, summed at the end): twice the independent
+        // DMMA chains per warp -- the leaf levels are bound by the tensor-core dependency latency
+        double acc[NCT][2], acc2[NCT][2];
+#pragma unroll
+        for (int ct = 0; ct < NCT; ++ct) acc[ct][0] = acc[ct][1] = acc2[ct][0] = acc2[ct][1] = 0.0;
+        const int nch = (T.ke - T.kb + KC - 1) / KC;
+        for (int c = 0; c < nch; ++c) {
+#ifdef ST_PROBE
+            const unsigned long long tw0 = st_gt();
+#endif
+            st_mbar_wait(bbase + 8 * s, ph);
+#ifdef ST_PROBE
+            twait += st_gt() - tw0;
+            ++nwait;
+#endif
+            if (active) {
+                const int kr = min(KC, T.ke - T.kb - c * KC);
+                const int ksteps = (kr + 3) >> 2;
+                const double* stg = reinterpret_cast<const double*>(smem + (size_t)s * stage_bytes);
+                const double* ap = stg + warp * 32 + lane;
+                const double* bp = stg + A_BYTES / 8 + q * ldb + g;
+                const int astep = T.ng * 32, bstep = 4 * ldb;
+                if (ksteps == KC / 4) {
+#pragma unroll
+                    for (int uu = 0; uu < KC / 4; uu += 2) {
+                        const double a0 = ap[uu * astep], a1 = ap[(uu + 1) * astep];
+#pragma unroll
+                        for (int ct = 0; ct < NCT; ++ct) {
+                            dmma8(acc[ct][0], acc[ct][1], a0, bp[uu * bstep + 8 * ct]);
+                            dmma8(acc2[ct][0], acc2[ct][1], a1, bp[(uu + 1) * bstep + 8 * ct]);
+                        }
+                    }
+                } else {
+                    int uu = 0;
+                    for (; uu + 1 < ksteps; uu += 2) {
+                        const double a0 = ap[uu * astep], a1 = ap[(uu + 1) * astep];
+#pragma unroll
+                        for (int ct = 0; ct < NCT; ++ct) {
+                            dmma8(acc[ct][0], acc[ct][1], a0, bp[uu * bstep + 8 * ct]);
+                            dmma8(acc2[ct][0], acc2[ct][1], a1, bp[(uu + 1) * bstep + 8 * ct]);
+                        }
+                    }
+                    if (uu < ksteps) {
+                        const double a0 = ap[uu * astep];
+#pragma unroll
+                        for (int ct = 0; ct < NCT; ++ct) dmma8(acc[ct][0], acc[ct][1], a0, bp[uu * bstep + 8 * ct]);
+                    }
+                }
+            }
+            __syncwarp();
+            if (lane == 0) st_mbar_arrive(bbase + 8 * (ST_MAXST + s));
+            s = s + 1 == nst ? 0 : s + 1;
+            if (s == 0) ph ^= 1;
+        }
+        if (!row_ok) continue;
+        double res[NCT][2];
+#pragma unroll
+        for (int ct = 0; ct < NCT; ++ct)
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+                const int col = 8 * ct + 2 * q + e;
+                const double v = acc[ct][e] + acc2[ct][e];
+                res[ct][e] = bwd ? -v : init[ct][e] - v;
+                if (col < jn) out_row[col] = res[ct][e];
+            }
+        for (int t = sc0; t < sc1; ++t) {   // backward: the solution row into every descendant that reads it
+            double* dr = FRm + (int64_t)__ldg(sc_row + t) * ldb;
+#pragma unroll
+            for (int ct = 0; ct < NCT; ++ct)
+#pragma unroll
+                for (int e = 0; e < 2; ++e) {
+                    const int col = 8 * ct + 2 * q + e;
+                    if (col < jn) dr[col] = res[ct][e];
+                }
+        }
+    }
+#ifdef ST_PROBE
+    if (lane == 0) ST_SPAN_END(probe_id);
+    if (warp == 0 && lane == 0 && blockIdx.x < 2048 && probe_id == g_probe_target) {
+        g_stp[blockIdx.x][0] = tp0;
+        g_stp[blockIdx.x][1] = tp1 - tp0;
+        g_stp[blockIdx.x][2] = st_gt() - tp1;
+        g_stp[blockIdx.x][3] = twait;
+        g_stp[blockIdx.x][4] = nwait;
+        g_stp[blockIdx.x][5] = ue - ub;
+    }
+#endif
+}
+
+// Forward assembly of one level's PIVOT rows into the blocked front vectors (the B operand of the
+// level's GEMM): FRS[row] = b[idx[row]] + the <= 4 children's contribution rows mapped onto it.
+// (Contribution rows of the level are not assembled here: the GEMM epilogue adds their children's
+// rows itself.)  One thread per (row, member pair).
+__global__ void __launch_bounds__(256) k_sfinit(const int32_t* __restrict__ rows, int nrows,
+                                                const int32_t* __restrict__ idx, const int32_t* __restrict__ gsrc,
+                                                double* __restrict__ FRS, const SolveIO* __restrict__ io, int64_t N,
+                                                int J, int64_t nidx, int ncb, int cw, int ldb, int probe_id) {
+    const int mat = blockIdx.y;
+    ST_SPAN_BEGIN(probe_id);
+    pdl_wait();   // children's contribution rows come from the previous level's GEMM
+    const int hw = cw >> 1, per = ncb * hw;
+    const double* b = io->r + (int64_t)mat * N * J;
+    const int tot = nrows * per;
+    for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < tot; t += gridDim.x * blockDim.x) {
+        const int rq = t / per, rem = t - rq * per, cb = rem / hw, i = rem - cb * hw;
+        const int col = cb * cw + 2 * i;
+        if (col >= J) continue;
+        const int64_t row = rows[rq];
+        const int4 g = *reinterpret_cast<const int4*>(gsrc + 4 * row);
+        const double2* F2 = reinterpret_cast<const double2*>(FRS + (int64_t)(mat * ncb + cb) * nidx * ldb);
+        const int h = ldb >> 1;
+        double2 v = *reinterpret_cast<const double2*>(b + (int64_t)idx[row] * J + col);
+        if (g.x >= 0) {   // rows without children's contributions (all leaf rows) load nothing else
+            const int src[4] = {g.x, g.y, g.z, g.w};
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const double2 c = F2[(int64_t)max(src[u], 0) * h + i];
+                if (src[u] >= 0) {
+                    v.x += c.x;
+                    v.y += c.y;
+                }
+            }
+        }
+        reinterpret_cast<double2*>(FRS + (int64_t)(mat * ncb + cb) * nidx * ldb)[row * h + i] = v;
+    }
+#ifdef ST_PROBE
+    __syncthreads();
+    if (threadIdx.x == 0) ST_SPAN_END(probe_id);
+#endif
+    pdl_trigger();
+}
+
+// ---------------------------------------------------------------------------
+// host side of the streamed solve
+// ---------------------------------------------------------------------------
+bool mf_stream_on(ens_ctx* c) {
+    if (c->stream_mode < 0) {
+        // streamed path for even J up to 48 (C2: 0.705 -> 0.593 ms per apply); for wider ensembles the
+        // classic k_sgemm path measured equal or faster (C3 J=64: 5.50 vs 5.63 ms, C4 J=128: 3.04 vs
+        // 3.05 ms).  ENS_SOLVE_STREAM=0/1 forces a path (A/B measurements, tools/apply_ab.py).
+        const char* e = std::getenv("ENS_SOLVE_STREAM");
+        const bool want = e ? e[0] != '0' : c->J <= 48;
+        c->stream_mode = ((c->J & 1) == 0 && want) ? 1 : 0;
+    }
+    return c->stream_mode == 1;
+}
+
+template <int NCT>
+static cudaError_t stream_attr(size_t smem) {
+    return cudaFuncSetAttribute(k_stream_gemm<NCT, 32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+}
+
+// tiles, per-launch CTA partitions and the stream buffer (once per context; J-dependent only in
+// the column blocking and the partition weights)
+static int stream_setup(ens_ctx* c) {
+    const int nf = (int)c->p.nfront;
+    std::vector<int32_t> fm(nf), fk(nf), par(nf);
+    std::vector<int64_t> foff(nf), fio((size_t)nf + 1);
+    ENS_CK(cudaMemcpy(fm.data(), c->p.f_m, sizeof(int32_t) * nf, cudaMemcpyDeviceToHost));
+    ENS_CK(cudaMemcpy(fk.data(), c->p.f_k, sizeof(int32_t) * nf, cudaMemcpyDeviceToHost));
+    ENS_CK(cudaMemcpy(par.data(), c->p.f_parent, sizeof(int32_t) * nf, cudaMemcpyDeviceToHost));
+    ENS_CK(cudaMemcpy(foff.data(), c->p.f_off, sizeof(int64_t) * nf, cudaMemcpyDeviceToHost));
+    ENS_CK(cudaMemcpy(fio.data(), c->p.f_idx_off, sizeof(int64_t) * (nf + 1), cudaMemcpyDeviceToHost));
+    std::vector<uint8_t> hasch(nf, 0);
+    for (int f = 0; f < nf; ++f)
+        if (par[f] >= 0 && par[f] < nf) hasch[par[f]] = 1;
+    const int J = c->J;
+    const int ncb = (J + 63) / 64;
+    int cw = (J + ncb - 1) / ncb;
+    cw += cw & 1;
+    const int ldb = cw + (((4 - cw) % 16) + 16) % 16;
+    const int KC = 32;
+    const size_t stage = ((size_t)KC * ST_ROWS * 8 + ((size_t)KC * ldb + 8) * 8 + 127) & ~(size_t)127;
+    const int nst = (int)std::max<size_t>(2, std::min<size_t>(ST_MAXST, (216 * 1024 / ST_CTAS - 2048) / stage));
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    std::vector<STile> tiles;
+    std::vector<int32_t> cta;
+    c->slaunch.clear();
+    int64_t aoff = 0;
+    auto add_tile = [&](int f, int r0, int rows, int K, int flags, int row0) {
+        STile t;
+        const int ng = (std::min(ST_ROWS, rows - r0) + 7) / 8;
+        t.a_lo = (int)(aoff & 0xffffffff);
+        t.a_hi = (int)(aoff >> 32);
+        t.fo = (int)fio[f];
+        t.K = K;
+        t.kp = fk[f];
+        t.r0 = r0;
+        t.ng = ng;
+        t.flags = flags;
+        t.src_lo = (int)(foff[f] & 0xffffffff);
+        t.src_hi = (int)(foff[f] >> 32);
+        t.m = fm[f];
+        t.row0 = row0;
+        t.kb = 0;
+        t.ke = K;
+        aoff += (int64_t)((K + 3) & ~3) * ng * 8;
+        tiles.push_back(t);
+    };
+    int max_cta_tiles = 1;
+    auto close_launch = [&](int dir, int L, size_t t0) {
+        if (tiles.size() == t0) return;
+        const int64_t nt = (int64_t)(tiles.size() - t0);
+        const int64_t U = nt * 2 * ncb;
+        std::vector<double> cost((size_t)U);
+        double tot = 0.0;
+        for (int64_t u = 0; u < U; ++u) {
+            const STile& t = tiles[t0 + u / (2 * ncb)];
+            const int cb = (int)(u % ncb), jn = std::min(cw, J - cb * cw);
+            const int kl = t.ke - t.kb;
+            cost[u] = (double)t.ng * ((kl + 3) & ~3) * 64.0 + (double)kl * jn * 8.0 + 2048.0;
+            tot += cost[u];
+        }
+        const int64_t G = std::min<int64_t>(U, (int64_t)ST_CTAS * sms);
+        const size_t base = cta.size();
+        cta.push_back(0);
+        double acc = 0.0;
+        int64_t b = 1;
+        for (int64_t u = 0; u < U && b < G; ++u) {
+            acc += cost[u];
+            if (acc >= tot * (double)b / (double)G) {
+                cta.push_back((int32_t)(u + 1));
+                ++b;
+            }
+        }
+        while ((int64_t)(cta.size() - base) < G) cta.push_back((int32_t)U);   // degenerate tails
+        cta.push_back((int32_t)U);
+        for (int64_t i = 0; i < G; ++i) {   // tiles a CTA touches (descriptors staged in shared memory)
+            const int64_t a = cta[base + i], b = cta[base + i + 1];
+            if (b > a) max_cta_tiles = std::max<int>(max_cta_tiles, (int)((b - 1) / (2 * ncb) - a / (2 * ncb) + 1));
+        }
+        c->slaunch.insert(c->slaunch.end(), {dir, L, (int64_t)t0, (int64_t)base, G});
+    };
+    const int nlev = (int)c->level_front_off.size() - 1;
+    for (int L = 0; L < nlev; ++L) {   // forward: contribution rows of every front
+        const size_t t0 = tiles.size();
+        for (int f = c->level_front_off[L]; f < c->level_front_off[L + 1]; ++f) {
+            const int rows = fm[f] - fk[f];
+            if (rows <= 0 || fk[f] <= 0) continue;
+            for (int r0 = 0; r0 < rows; r0 += ST_ROWS) add_tile(f, r0, rows, fk[f], hasch[f] ? 2 : 0, fk[f] + r0);
+        }
+        close_launch(0, L, t0);
+    }
+    for (int L = nlev - 1; L >= 0; --L) {   // backward: pivot rows over the whole front
+        const size_t t0 = tiles.size();
+        for (int f = c->level_front_off[L]; f < c->level_front_off[L + 1]; ++f)
+            for (int r0 = 0; r0 < fk[f]; r0 += ST_ROWS) add_tile(f, r0, fk[f], fm[f], 1, r0);
+        close_launch(1, L, t0);
+    }
+    // forward assembly rows: the pivot rows of every front, per level
+    std::vector<int32_t> bg;
+    c->sbg_off.assign((size_t)nlev + 1, 0);
+    for (int L = 0; L < nlev; ++L) {
+        c->sbg_off[L] = (int64_t)bg.size();
+        for (int f = c->level_front_off[L]; f < c->level_front_off[L + 1]; ++f)
+            for (int t = 0; t < fk[f]; ++t) bg.push_back((int32_t)(fio[f] + t));
+    }
+    c->sbg_off[nlev] = (int64_t)bg.size();
+    // backward scatter lists: for every pivot position, the contribution rows of descendant fronts
+    // that hold the same dof (the backward epilogue writes the solution row straight into them)
+    const int64_t nidx_h = c->p.n_idx;
+    std::vector<int32_t> fidx_h((size_t)nidx_h);
+    ENS_CK(cudaMemcpy(fidx_h.data(), c->p.f_idx, sizeof(int32_t) * nidx_h, cudaMemcpyDeviceToHost));
+    std::vector<int32_t> piv_of((size_t)c->n_total, -1);
+    for (int f = 0; f < nf; ++f)
+        for (int t = 0; t < fk[f]; ++t) piv_of[fidx_h[fio[f] + t]] = (int32_t)(fio[f] + t);
+    std::vector<int32_t> sc_off((size_t)nidx_h + 1, 0), sc_row;
+    for (int f = 0; f < nf; ++f)
+        for (int t = fk[f]; t < fm[f]; ++t) ++sc_off[piv_of[fidx_h[fio[f] + t]] + 1];
+    for (int64_t i = 0; i < nidx_h; ++i) sc_off[i + 1] += sc_off[i];
+    sc_row.resize((size_t)sc_off[nidx_h]);
+    {
+        std::vector<int32_t> fill(sc_off.begin(), sc_off.end() - 1);
+        for (int f = 0; f < nf; ++f)
+            for (int t = fk[f]; t < fm[f]; ++t) sc_row[fill[piv_of[fidx_h[fio[f] + t]]]++] = (int32_t)(fio[f] + t);
+    }
+    const size_t sbytes = sizeof(double) * 2 * (size_t)std::max<int64_t>(aoff, 32);
+    const size_t frbytes = sizeof(double) * 2 * (size_t)ncb * (size_t)c->p.n_idx * ldb;
+    if (cudaMalloc(&c->sstream, sbytes) != cudaSuccess || cudaMalloc(&c->stiles, sizeof(STile) * tiles.size()) !=
+                                                              cudaSuccess ||
+        cudaMalloc(&c->scta, sizeof(int32_t) * cta.size()) != cudaSuccess ||
+        cudaMalloc(&c->sfr, frbytes) != cudaSuccess ||
+        cudaMalloc(&c->sbg_rows, sizeof(int32_t) * std::max<size_t>(bg.size(), 1)) != cudaSuccess ||
+        cudaMalloc(&c->ssc_off, sizeof(int32_t) * sc_off.size()) != cudaSuccess ||
+
+        cudaMalloc(&c->ssc_row, sizeof(int32_t) * std::max<size_t>(sc_row.size(), 1)) != cudaSuccess) {
+        cudaGetLastError();
+        cudaFree(c->sstream);
+        cudaFree(c->stiles);
+        cudaFree(c->scta);
+        cudaFree(c->sfr);
+        c->sstream = nullptr;
+        c->stiles = nullptr;
+        c->scta = nullptr;
+        c->sfr = nullptr;
+        ens_set_error("out of device memory for the solve stream", __FILE__, __LINE__);
+        return ENS_ENOMEM;
+    }
+    ENS_CK(cudaMemset(c->sstream, 0, sbytes));
+    ENS_CK(cudaMemset(c->sfr, 0, frbytes));   // pad columns stay zero (B stages must be finite)
+    ENS_CK(cudaMemcpy(c->stiles, tiles.data(), sizeof(STile) * tiles.size(), cudaMemcpyHostToDevice));
+    ENS_CK(cudaMemcpy(c->scta, cta.data(), sizeof(int32_t) * cta.size(), cudaMemcpyHostToDevice));
+    if (!bg.empty())
+        ENS_CK(cudaMemcpy(c->sbg_rows, bg.data(), sizeof(int32_t) * bg.size(), cudaMemcpyHostToDevice));
+    ENS_CK(cudaMemcpy(c->ssc_off, sc_off.data(), sizeof(int32_t) * sc_off.size(), cudaMemcpyHostToDevice));
+
+    if (!sc_row.empty())
+        ENS_CK(cudaMemcpy(c->ssc_row, sc_row.data(), sizeof(int32_t) * sc_row.size(), cudaMemcpyHostToDevice));
+    c->ws_bytes += sbytes + frbytes + sizeof(STile) * tiles.size() +
+                   sizeof(int32_t) * (cta.size() + bg.size() + sc_off.size() + sc_row.size());
+    // the classic front vectors are not used on this path
+    c->ws_bytes -= sizeof(double) * 2 * (size_t)c->p.n_idx * c->J;
+    cudaFree(c->frvec);
+    c->frvec = nullptr;
+    c->stream_len = std::max<int64_t>(aoff, 32);
+    c->n_stiles = (int64_t)tiles.size();
+    c->scw = cw;
+    c->sncb = ncb;
+    c->sldb = ldb;
+    c->snst = nst;
+    c->skc = KC;
+    c->sstage = stage;
+    c->sdesc = (size_t)max_cta_tiles * sizeof(STile);
+    const size_t smem = stage * nst + c->sdesc;
+    if (smem > 220 * 1024) {
+        ens_set_error("streamed solve: a CTA's tile descriptors do not fit shared memory", __FILE__, __LINE__);
+        return ENS_EINVAL;
+    }
+    ENS_CK(stream_attr<1>(smem));
+    ENS_CK(stream_attr<2>(smem));
+    ENS_CK(stream_attr<3>(smem));
+    ENS_CK(stream_attr<4>(smem));
+    ENS_CK(stream_attr<5>(smem));
+    ENS_CK(stream_attr<6>(smem));
+    ENS_CK(stream_attr<7>(smem));
+    ENS_CK(stream_attr<8>(smem));
+    return ENS_OK;
+}
+
+int mf_stream_prepare(ens_ctx* c) {
+    if (!mf_stream_on(c) || c->stiles) return ENS_OK;
+    const int rc = stream_setup(c);
+    if (rc != ENS_OK) c->stream_mode = 0;   // no room for the stream: the classic path
+    return ENS_OK;
+}
+
+int mf_stream_pack(ens_ctx* c, cudaStream_t s) {
+    if (!mf_stream_on(c) || !c->stiles || c->n_stiles == 0) return ENS_OK;
+    k_stream_pack<<<dim3((unsigned)c->n_stiles, 2), 256, 0, s>>>((const STile*)c->stiles, c->fronts,
+                                                                 c->p.front_storage, c->sstream, c->stream_len);
+    ENS_CKL();
+    return ENS_OK;
+}
+
+// launch sequence of one streamed solve (after the identity-row copy)
+static int stream_launches(ens_ctx* c, cudaStream_t s, SolveIO* io, int64_t* cnt) {
+    const int J = c->J;
+    const int64_t N = c->n_total, nidx = c->p.n_idx;
+    const int nct = (c->scw + 7) / 8;
+    const size_t smem = c->sstage * c->snst + c->sdesc;
+    const int nlev = (int)c->level_front_off.size() - 1;
+    std::vector<int> fwd_at(nlev, -1), bwd_at(nlev, -1);
+    for (size_t i = 0; i + 5 <= c->slaunch.size(); i += 5)
+        (c->slaunch[i] == 0 ? fwd_at : bwd_at)[c->slaunch[i + 1]] = (int)i;
+    auto gemm = [&](int li) -> int {
+        const int64_t* r = &c->slaunch[li];
+        const int t0 = (int)r[2], cb = (int)r[3];
+        const unsigned G = (unsigned)r[4];
+#define SGS(NC)                                                                                                    \
+    ENS_CK(launch_pdl(k_stream_gemm<NC, 32>, dim3(G), dim3(ST_THREADS), smem, s, (const STile*)c->stiles, t0,     \
+                      (const int32_t*)(c->scta + cb), c->sncb, c->scw, c->sldb, (const double*)c->sstream,      \
+                      c->stream_len, c->sfr, (const SolveIO*)io, (const int32_t*)c->p.f_idx,                   \
+                      (const int32_t*)c->p.gsrc, (const int32_t*)c->ssc_off, (const int32_t*)c->ssc_row,        \
+                      N, J, nidx, c->snst, (uint32_t)c->sstage, (int)*cnt))
+        switch (nct) {
+            case 1: SGS(1); break;
+            case 2: SGS(2); break;
+            case 3: SGS(3); break;
+            case 4: SGS(4); break;
+            case 5: SGS(5); break;
+            case 6: SGS(6); break;
+            case 7: SGS(7); break;
+            default: SGS(8); break;
+        }
+#undef SGS
+        ENS_CKL();
+        ++*cnt;
+        return ENS_OK;
+    };
+    for (int L = 0; L < nlev; ++L) {
+        const int64_t a = c->sbg_off[L], nr = c->sbg_off[L + 1] - a;
+        if (nr > 0) {
+            const int64_t tot = nr * c->sncb * (c->scw / 2);
+            ENS_CK(launch_pdl(k_sfinit, dim3((unsigned)((tot + 255) / 256), 2), dim3(256), 0, s,
+                              (const int32_t*)(c->sbg_rows + a), (int)nr, (const int32_t*)c->p.f_idx,
+                              (const int32_t*)c->p.gsrc, c->sfr, (const SolveIO*)io, N, J, nidx, c->sncb, c->scw,
+                              c->sldb, (int)*cnt));
+            ENS_CKL();
+            ++*cnt;
+        }
+        if (fwd_at[L] >= 0) RET(gemm(fwd_at[L]));
+    }
+    for (int L = nlev - 1; L >= 0; --L)
+        if (bwd_at[L] >= 0) RET(gemm(bwd_at[L]));
+    return ENS_OK;
+}
+
 // record the launch sequence of one solve (io table fixed)
 static int mf_solve_launches(ens_ctx* c, cudaStream_t s, SolveIO* io, int64_t* nlaunch) {
     MfDev d = mfdev(c);
@@ -488,6 +1179,11 @@ static int mf_solve_launches(ens_ctx* c, cudaStream_t s, SolveIO* io, int64_t* n
         lab.push_back(std::string(tag) + " n=" + std::to_string(a) + " kmax=" + std::to_string(b2));
     };
     mark("start", 0, 0);
+    if (mf_stream_on(c) && c->stiles) {
+        const int rc = stream_launches(c, s, io, &cnt);
+        *nlaunch = cnt;
+        return rc;
+    }
     for (const std::vector<int64_t>* sched : {&c->sched_fwd, &c->sched_bwd}) {
         const int64_t nrow = (int64_t)sched->size() / 5;
         for (int64_t i = 0; i < nrow; ++i) {
@@ -632,6 +1328,10 @@ int mf_solve(ens_ctx* c, cudaStream_t s, const double* r, double* z) {
         ENS_CK(cudaStreamSynchronize(s));
         cudaFree(d_hasch);
         c->ws_bytes += pbytes + tbytes + sizeof(int4) * 3 * (size_t)nw + sizeof(int32_t) * (size_t)nidx;
+    }
+    {
+        const int rc = mf_stream_prepare(c);
+        if (rc != ENS_OK) return rc;
     }
     SolveIO* io = (SolveIO*)c->solve_io;
     k_set_io<<<1, 1, 0, s>>>(io, r, z);

@@ -873,6 +873,32 @@ class Engine:
         with self.on_stream():
             return self._diagnostics()
 
+    def mean_error(self, exact, t):
+        """Squared H1 errors (||d_v||^2, ||d_w||^2) of the current ensemble means against a separable
+        exact field (``exact.mean_separable(disc, config)``), computed on the device
+        (ens_mean_error; the summands of experiments.error_norm_21, `experiments.py:59-73`)."""
+        key = ("mean-exact", id(exact))
+        ent = self._data_cache.get(key)
+        if ent is None:
+            sep = exact.mean_separable(self.disc, self.config)
+            basis = np.asarray(sep.basis, dtype=float).reshape(len(sep.basis), -1)[:, self.hm.ref_of_int[:self.nvel]]
+            ent = (sep, torch.as_tensor(np.ascontiguousarray(basis)).to(self.dev), exact,
+                   torch.zeros(4, dtype=torch.float64, device=self.dev))
+            self._data_cache[key] = ent
+        sep, basis_t, _, out = ent
+        cv, cw = sep.coef(t)
+        coef_t = torch.as_tensor(np.stack([np.asarray(cv, float).reshape(-1), np.asarray(cw, float).reshape(-1)]))
+        with self.on_stream():
+            if not self.means_valid:
+                self._compute_means()
+            coef_d = coef_t.to(self.dev, non_blocking=False)
+            dd = N.DataDesc()
+            dd.rows, dd.K, dd.basis, dd.coef, dd.dense = self.nvel, basis_t.shape[0], _dptr(basis_t), _dptr(coef_d), None
+            N.check(self.lib.ens_mean_error(self.ctx, self.sptr, _dptr(self.means), C.byref(dd), _dptr(out)),
+                    "ens_mean_error")
+            r = out.cpu().numpy()
+        return float(r[0] + r[1]), float(r[2] + r[3])
+
     def _compute_means(self):
         lib, ctx, s = self.lib, self.ctx, self.sptr
         X = self.X[self.cur]

@@ -248,6 +248,39 @@ class BaselineMms:
         return np.outer(2.0 * (1.0 + self.eps(config)) * (1.0 + 0.01 * t), base)
 
 
+class BaselineMmsExact:
+    """Exact ensemble means of the BASELINE MMS for run(..., exact=...): <v>(t) = 2(1+<e>)(1+0.01t)
+    (cos y, sin x), <w> = 0 (nodal interpolants, `experiments.py:59-73`)."""
+
+    def __init__(self, nu0: float = 0.01):
+        self.nu0 = nu0
+
+    def mean_separable(self, disc, config):
+        base = fe.interpolate(_cs, 0.0, disc.velocity)[None, :]
+        e = float(np.mean(config.nu / self.nu0 - 1.0))
+        return Separable(base, lambda t: (np.array([2.0 * (1.0 + e) * (1.0 + 0.01 * t)]), np.zeros(1)),
+                         "baseline-mms-exact")
+
+    def mean_v(self, x, y, t, config):
+        a = 2.0 * (1.0 + float(np.mean(config.nu / self.nu0 - 1.0))) * (1.0 + 0.01 * t)
+        return a * np.cos(y), a * np.sin(x)
+
+
+class PaperMmsExact:
+    """The reference's convergence targets for the paper MMS: base_v, base_w (`experiments.py:146-147`,
+    `mms.py:26-37`): (cos y, sin x) +- g(t) (sin y, cos x), g = 1 + e^t."""
+
+    def mean_separable(self, disc, config):
+        e1 = fe.interpolate(lambda x, y, t: (np.cos(y), np.sin(x)), 0.0, disc.velocity)
+        e2 = fe.interpolate(lambda x, y, t: (np.sin(y), np.cos(x)), 0.0, disc.velocity)
+
+        def coef(t):
+            g = 1.0 + math.exp(t)
+            return np.array([1.0, g]), np.array([1.0, -g])
+
+        return Separable(np.stack([e1, e2]), coef, "paper-mms-exact")
+
+
 class _ForcingView:
     def __init__(self, owner):
         self.owner = owner

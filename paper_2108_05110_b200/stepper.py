@@ -283,10 +283,21 @@ class RunReport:
     member_l2w_sq: np.ndarray
     member_gradv_sq: np.ndarray
     member_gradw_sq: np.ndarray
+    # run(..., exact=...): squared H1 errors of the ensemble means per level, computed on the device
+    err_v_h1_sq: np.ndarray = None
+    err_w_h1_sq: np.ndarray = None
 
     @property
     def num_steps(self) -> int:
         return len(self.times) - 1
+
+    def error_norm_21(self):
+        """(||<e_v>||_{2,1}, ||<e_w>||_{2,1}) of a run with ``exact`` (`experiments.py:59-73`)."""
+        if self.err_v_h1_sq is None:
+            raise ValueError("the run was not given an exact solution")
+        from .reporting import error_norm_21_from_series
+        return (error_norm_21_from_series(self.err_v_h1_sq, self.dt),
+                error_norm_21_from_series(self.err_w_h1_sq, self.dt))
 
 
 _MEMBER_KEYS = ("l2v", "l2w", "gradv", "gradw", "div_v", "div_w")
@@ -335,14 +346,18 @@ def _gather_records(report, local, comm, J):
 from .exchange import member_slice  # noqa: E402  (re-exported)
 
 
-def run(config: EnsembleConfig, problem: Problem, observer=None, snapshot_steps=(), comm=None, record=True):
+def run(config: EnsembleConfig, problem: Problem, observer=None, snapshot_steps=(), comm=None, record=True,
+        exact=None):
     """Integrate to t_end with M = round(t_end/dt) steps (`stepper.py:442-502`).
 
     ``comm``: optional torch.distributed process group; members are then sharded
     contiguously over its ranks (one GPU each) with an allreduce SUM of the
     member sums and an allreduce MAX of the eddy-viscosity maxima per step.
     Returns (report, final_state, snapshots); with ``comm`` the final state and
-    snapshots hold this rank's members.
+    snapshots hold this rank's members.  ``exact``: optional exact solution with
+    ``mean_separable(disc, config)`` (e.g. ``problems.BaselineMmsExact``); the report then
+    carries the squared H1 errors of the ensemble means per level, computed on the
+    device, and ``report.error_norm_21()`` (`experiments.py:59-73`).
     """
     ratio = config.t_end / config.dt
     m = int(round(ratio))
@@ -371,6 +386,9 @@ def run(config: EnsembleConfig, problem: Problem, observer=None, snapshot_steps=
     engine.load_state(v0, w0, None, None)
     state = EnsembleState(step=0, time=0.0, device=engine.state_handle())
     local = [] if comm is not None else None
+    if exact is not None:
+        report.err_v_h1_sq, report.err_w_h1_sq = np.zeros(shape), np.zeros(shape)
+        report.err_v_h1_sq[0], report.err_w_h1_sq[0] = engine.mean_error(exact, 0.0)
     if record:
         _record(report, 0, engine, local)
     snaps = {}
@@ -384,6 +402,8 @@ def run(config: EnsembleConfig, problem: Problem, observer=None, snapshot_steps=
         state, res = _step(engine, state, config, problem.forcing, problem.boundary)
         report.wall_clock[n + 1] = _time.perf_counter() - tic
         report.residuals[n + 1] = res
+        if exact is not None:
+            report.err_v_h1_sq[n + 1], report.err_w_h1_sq[n + 1] = engine.mean_error(exact, state.time)
         if record:
             _record(report, n + 1, engine, local)
         if state.step in snapshot_steps:
