@@ -117,11 +117,11 @@ class ChunkedEngine(Engine):
             with torch.cuda.stream(s):
                 Xs = g["x_in"]
                 for m, a in enumerate((v, w)):
-                    g["d_vel"][m].copy_(torch.from_numpy(np.ascontiguousarray(a[sl])))
+                    g["d_vel"][m].copy_(self._host_tensor(a[sl]))
                     torch.index_select(g["d_vel"][m].t(), 0, g["ref_of_int_v"], out=Xs[m, :nv])
                 if has_p:
                     for m, a in enumerate((q, r)):
-                        g["d_pres"][m].copy_(torch.from_numpy(np.ascontiguousarray(np.asarray(a, float)[sl])))
+                        g["d_pres"][m].copy_(self._host_tensor(np.asarray(a, float)[sl]))
                         torch.index_select(g["d_pres"][m].t(), 0, g["ref_of_int_p"], out=Xs[m, nv:])
                 else:
                     Xs[:, nv:] = 0.0
@@ -150,6 +150,10 @@ class ChunkedEngine(Engine):
             out["v"][sl], out["w"][sl] = g["d_vel"][0].cpu().numpy(), g["d_vel"][1].cpu().numpy()
             out["q"][sl], out["r"][sl] = g["d_pres"][0].cpu().numpy(), g["d_pres"][1].cpu().numpy()
         return out
+
+    def release(self):
+        super().release()
+        self.Xc = self.Pqc = None
 
     def state_handle(self):
         import weakref

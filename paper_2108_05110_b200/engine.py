@@ -22,6 +22,7 @@ from __future__ import annotations
 import ctypes as C
 import os
 import weakref
+from collections import OrderedDict
 
 import numpy as np
 import scipy.sparse as sp
@@ -35,6 +36,7 @@ from .ensemble import viscosity_stats
 
 
 _RENEW_DEBUG = os.environ.get("ENS_RENEW_DEBUG", "0") == "1"
+MAX_PROBLEM_OBJECTS = 8   # forcing / boundary / exact objects whose device data and step graphs an engine keeps
 RENEW_WINDOW = int(os.environ.get("ENS_RENEW_WINDOW", "6"))   # lifetimes a per-position cost stays usable
 RENEW_STALE = int(os.environ.get("ENS_RENEW_STALE", str(4 * RENEW_WINDOW)))
 
@@ -254,7 +256,12 @@ class DeviceState:
             return self._host[name]
         if not self.valid:
             raise RuntimeError("device state was overwritten before it was read")
-        self._host.update(self.engine.fields_to_host(self.buf))   # all four fields, one sync
+        fields = self.engine.fields_to_host(self.buf)   # all four fields, one sync
+        for a in fields.values():
+            # an EnsembleState is immutable (`ensemble.py:183-190`): a caller editing a returned field in
+            # place would otherwise be silently ignored by a device-resident next step
+            a.setflags(write=False)
+        self._host.update(fields)
         return self._host[name]
 
 
@@ -424,6 +431,7 @@ class Engine:
         self.rhs_fused = os.environ.get("ENS_RHS_FUSED", "1") != "0"
         self._graphs = {}
         self._gdata_cache = {}
+        self._lru = OrderedDict()        # problem-data objects with cached device data, least recent first
         self._gspec = {}
         self.graph_launch_credit = 0   # kernels replayed by step graphs minus kernels captured
 
@@ -460,8 +468,14 @@ class Engine:
 
     @staticmethod
     def _host_tensor(a):
-        """torch view of a (J, n) float64 host array (no copy when already contiguous float64)."""
+        """torch view of a (J, n) float64 host array (no copy when already contiguous float64; read
+        only -- states a step returns are write-protected host views)."""
         arr = np.ascontiguousarray(np.asarray(a, dtype=np.float64))
+        if not arr.flags.writeable:
+            import warnings
+            with warnings.catch_warnings():
+                warnings.simplefilter("ignore", UserWarning)
+                return torch.from_numpy(arr)
         return torch.from_numpy(arr)
 
     def load_state(self, v, w, q, r):
@@ -574,6 +588,7 @@ class Engine:
         sep = None
         if hasattr(obj, "separable"):
             # keyed by id(obj); the entry keeps obj alive, so the id cannot be reused by another object
+            self._touch(obj)
             key = (kind, id(obj))
             if key not in self._data_cache:
                 s = obj.separable(self.disc, self.config)
@@ -688,6 +703,7 @@ class Engine:
 
     def _gdata(self, obj, kind):
         """(coefficient function, pinned host and device coefficient blocks, fixed DataDesc) of one data kind."""
+        self._touch(obj)
         key = (kind, id(obj))
         ent = self._gdata_cache.get(key)
         if ent is None:
@@ -702,6 +718,41 @@ class Engine:
             ent = (sep, pin, dev, dd)
             self._gdata_cache[key] = ent
         return ent
+
+    def _touch(self, obj):
+        """LRU bookkeeping of problem-data objects: beyond MAX_PROBLEM_OBJECTS the least recently used
+        object's device data, coefficient blocks and step graphs are released."""
+        oid = id(obj)
+        if oid in self._lru:
+            self._lru.move_to_end(oid)
+            return
+        self._lru[oid] = True
+        while len(self._lru) > MAX_PROBLEM_OBJECTS:
+            old, _ = self._lru.popitem(last=False)
+            gone = set()
+            for k in [k for k in self._gdata_cache if k[1] == old]:
+                ent = self._gdata_cache.pop(k)
+                gone.add(id(ent))
+                self._gspec.pop(id(ent), None)
+            for k in [k for k in self._data_cache if k[1] == old]:
+                del self._data_cache[k]
+            for k in [k for k in self._graphs if k[1] in gone or k[2] in gone]:
+                del self._graphs[k]
+
+    def release(self):
+        """Free the device context and buffers (live states are copied to the host first)."""
+        for b in (0, 1):
+            self._retire(b)
+        self._graphs.clear()
+        self._gdata_cache.clear()
+        self._data_cache.clear()
+        if getattr(self, "ctx", None):
+            torch.cuda.synchronize(self.dev)
+            self.lib.ens_destroy(self.ctx)
+            self.ctx = None
+        for name in ("X", "Pq", "rhs", "as_vals", "mesh_t", "plan_t", "_stg"):
+            if hasattr(self, name):
+                setattr(self, name, None)
 
     def _gcoef(self, ent, t):
         sep = ent[0]
@@ -790,8 +841,8 @@ class Engine:
             self._gfill(lo, t_next)
         self._gfill(bc, t_next)
         segs = self._step_graphs(lo, bc)
+        self._retire(nxt)          # (a caller's copy of the state about to be overwritten: not step cost)
         self._cost_begin()
-        self._retire(nxt)
         if self.comm is None:
             need = self._need_factor()
             self._replay(segs["pre"])
@@ -877,6 +928,7 @@ class Engine:
         """Squared H1 errors (||d_v||^2, ||d_w||^2) of the current ensemble means against a separable
         exact field (``exact.mean_separable(disc, config)``), computed on the device
         (ens_mean_error; the summands of experiments.error_norm_21, `experiments.py:59-73`)."""
+        self._touch(exact)
         key = ("mean-exact", id(exact))
         ent = self._data_cache.get(key)
         if ent is None:
@@ -912,6 +964,7 @@ class Engine:
         cur, nxt = self.cur, 1 - self.cur
         X = self.X[cur]
         self.flush_global()        # sharded: agree on the previous graphed step's values first
+        self._retire(1 - cur)
         self._cost_begin()
         if not self.means_valid:
             self._compute_means()

@@ -131,6 +131,14 @@ def get_solver_options():
 
 
 _CHUNK = {"chunk": None}   # member columns per device pass: None = as many as fit (chunked.plan_chunk)
+MAX_ENGINES = 4            # engines (device contexts) kept per Discretization, least recently used released
+
+
+def _evict_engines(disc, keep):
+    keys = [k for k in disc._cache if isinstance(k, tuple) and k and k[0] == "b200-engine"]
+    for k in keys[:max(0, len(keys) - keep)]:
+        eng = disc._cache.pop(k)
+        eng.release()
 
 
 def set_member_chunk(chunk=None):
@@ -146,7 +154,10 @@ def get_engine(disc, config, j0=0, J=None, comm=None, device=None):
     key = ("b200-engine", config, j0, J, device, id(comm) if comm is not None else None,
            tuple(sorted(_SOLVER_OPTS.items())), _CHUNK["chunk"])
     eng = disc._cache.get(key)
+    if eng is not None:
+        disc._cache[key] = disc._cache.pop(key)   # most recently used last
     if eng is None:
+        _evict_engines(disc, keep=MAX_ENGINES - 1)
         import torch
         from .chunked import ChunkedEngine, largest_divisor_at_most, plan_chunk
         dev = torch.cuda.current_device() if device is None else device

@@ -209,3 +209,39 @@ def test_decay_run_properties_and_stability_bound(tiny_disc):
     assert len(report.times) == len(report.residuals) == len(report.wall_clock) == 6
     assert seen == list(range(6))
     assert P.verify_stability_bound(report, config, tiny_disc).holds
+
+
+def test_returned_state_is_write_protected(tiny_disc):
+    """Advance's host views are read-only (`ensemble.py:183-190`: states are immutable), so an
+    in-place edit cannot be silently ignored by the next device-resident step."""
+    config = simple_config(dt=0.05, t_end=0.1)
+    st = zero_state(config, tiny_disc)
+    new, _ = P.advance(st, config, tiny_disc, ZeroForcing(), ZeroBoundary())
+    for f in (new.v, new.w, new.q, new.r):
+        assert not f.flags.writeable
+        with pytest.raises(ValueError):
+            f[0, 0] = 1.0
+    edited = EnsembleState(v=np.array(new.v) + 1.0, w=np.array(new.w), q=np.array(new.q), r=np.array(new.r), step=1,
+                           time=new.time)
+    nxt, _ = P.advance(edited, config, tiny_disc, ZeroForcing(), ZeroBoundary())
+    assert np.abs(nxt.v).max() > 0.0     # the edited (host) state was uploaded, not the resident one
+
+
+def test_engine_caches_are_bounded():
+    """Fresh problem objects on one engine: device data and step graphs of the least recently used
+    objects are released (engine.MAX_PROBLEM_OBJECTS), engines per discretisation are bounded."""
+    from paper_2108_05110_b200 import engine as EN
+    from paper_2108_05110_b200 import stepper as ST
+    from paper_2108_05110_b200.problems import BaselineMms, _BoundaryView, _ForcingView
+    disc, cfg, prob = P.build_case("C1", J=4, steps=3)
+    for k in range(EN.MAX_PROBLEM_OBJECTS + 4):
+        mms = BaselineMms(nu0=0.01 + 1e-4 * k)
+        P.run(cfg, P.Problem(disc, prob.initial_v, prob.initial_w, _ForcingView(mms), _BoundaryView(mms)))
+    eng = ST.get_engine(disc, cfg)
+    assert len(eng._lru) <= EN.MAX_PROBLEM_OBJECTS
+    assert len(eng._gdata_cache) <= 2 * EN.MAX_PROBLEM_OBJECTS
+    assert len(eng._graphs) <= 2 * EN.MAX_PROBLEM_OBJECTS
+    for k in range(ST.MAX_ENGINES + 2):
+        c2 = P.EnsembleConfig(members=cfg.members, coupling=1.0, mu=1.0, dt=cfg.dt * (1 + 0.1 * k), t_end=cfg.dt * 2)
+        P.run(c2, prob)
+    assert sum(1 for key in disc._cache if isinstance(key, tuple) and key[0] == "b200-engine") <= ST.MAX_ENGINES
