@@ -623,83 +623,47 @@ __global__ void __launch_bounds__(256) k_stream_pack(const STile* __restrict__ t
     }
 }
 
-// One level and direction of the streamed solve; units [cta_off[b], cta_off[b+1]) per CTA,
-// unit u = (tile * 2 + system) * ncb + column block.
+// Producer of a unit range: streams every chunk of units [ub, ue) through the stage ring
+// (state s / ph carried across ranges by the persistent kernel).
+template <int KC>
+__device__ __forceinline__ void st_produce(const STile* sT, int tb, int ub, int ue, int per_tile, int ncb, int ldb,
+                                           const double* __restrict__ S, int64_t slen,
+                                           const double* __restrict__ FRS, int64_t nidx, int nst, uint32_t stage_bytes,
+                                           uint32_t sbase, uint32_t bbase, int& s, uint32_t& ph) {
+    constexpr uint32_t A_BYTES = KC * ST_ROWS * 8;
+    for (int u = ub; u < ue; ++u) {
+        const STile& T = sT[u / per_tile - tb];
+        const int mat = (u % per_tile) / ncb, cb = u % ncb;
+        const double* Ab = S + (int64_t)mat * slen + st_i64(T.a_lo, T.a_hi);
+        const double* Bb = FRS + ((int64_t)(mat * ncb + cb) * nidx + T.fo) * ldb;
+        const int nch = (T.ke - T.kb + KC - 1) / KC;
+        for (int c = 0; c < nch; ++c) {
+            const int k0 = T.kb + c * KC, kr = min(KC, T.ke - k0);
+            const uint32_t a_bytes = (uint32_t)((kr + 3) >> 2) * T.ng * 256u;
+            const uint32_t b_bytes = (uint32_t)kr * ldb * 8u;
+            st_mbar_wait(bbase + 8 * (ST_MAXST + s), ph ^ 1);
+            const uint32_t full = bbase + 8 * s;
+            const uint32_t st = sbase + (uint32_t)s * stage_bytes;
+            st_mbar_expect_tx(full, a_bytes + b_bytes);
+            st_bulk_g2s(st, Ab + (int64_t)k0 * T.ng * 8, a_bytes, full);
+            st_bulk_g2s(st + A_BYTES, Bb + (int64_t)k0 * ldb, b_bytes, full);
+            s = s + 1 == nst ? 0 : s + 1;
+            if (s == 0) ph ^= 1;
+        }
+    }
+}
+
+// Consumers (warps 0..3, row group = warp) of a unit range: DMMA mainloop and epilogue.
 template <int NCT, int KC>
-__global__ void __launch_bounds__(ST_THREADS, ST_CTAS)
-    k_stream_gemm(const STile* __restrict__ tiles, int tile0, const int32_t* __restrict__ cta_off, int ncb, int cw,
-                  int ldb, const double* __restrict__ S, int64_t slen, double* __restrict__ FRS,
-                  const SolveIO* __restrict__ io, const int32_t* __restrict__ fidx,
-                  const int32_t* __restrict__ gsrc, const int32_t* __restrict__ sc_off,
-                  const int32_t* __restrict__ sc_row, int64_t N, int J, int64_t nidx, int nst,
-                  uint32_t stage_bytes, int probe_id) {
-    extern __shared__ __align__(128) unsigned char smem[];
-    ST_SPAN_BEGIN(probe_id);
-    __shared__ __align__(8) uint64_t bars[2 * ST_MAXST];   // full[0..nst), empty[ST_MAXST..)
+__device__ __forceinline__ void st_consume(const STile* sT, int tb, int ub, int ue, int per_tile, int ncb, int cw,
+                                           int ldb, double* __restrict__ FRS, const SolveIO* __restrict__ io,
+                                           const int32_t* __restrict__ fidx, const int32_t* __restrict__ gsrc,
+                                           const int32_t* __restrict__ sc_off, const int32_t* __restrict__ sc_row,
+                                           int64_t N, int J, int64_t nidx, int nst, uint32_t stage_bytes,
+                                           const unsigned char* smem, uint32_t bbase, int& s, uint32_t& ph) {
+    constexpr uint32_t A_BYTES = KC * ST_ROWS * 8;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const uint32_t sbase = st_smem_u32(smem);
-    const uint32_t bbase = st_smem_u32(bars);
-    constexpr uint32_t A_BYTES = KC * ST_ROWS * 8;        // A region of a stage (max)
-    if (threadIdx.x == 0) {
-        for (int s = 0; s < nst; ++s) {
-            st_mbar_init(bbase + 8 * s, 1);
-            st_mbar_init(bbase + 8 * (ST_MAXST + s), 4);
-        }
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    }
-    // B regions start finite (rows past a tile's inner range meet zero A entries: 0 * finite = 0)
-    for (uint32_t i = threadIdx.x; i < (uint32_t)nst * stage_bytes / 8; i += blockDim.x)
-        reinterpret_cast<double*>(smem)[i] = 0.0;
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-    // this CTA's tile descriptors into shared memory (static data: before the dependency wait), so
-    // neither the producer nor the consumers pay a global-load latency per unit
-    const int ub = cta_off[blockIdx.x], ue = cta_off[blockIdx.x + 1];
-    const int per_tile = 2 * ncb;
-    STile* sT = reinterpret_cast<STile*>(smem + (size_t)nst * stage_bytes);
-    const int tb = ub / per_tile, te = ue > ub ? (ue - 1) / per_tile + 1 : tb;
-    for (int i = threadIdx.x; i < (te - tb) * (int)(sizeof(STile) / 4); i += blockDim.x)
-        reinterpret_cast<int*>(sT)[i] = __ldg(reinterpret_cast<const int*>(tiles + tile0 + tb) + i);
-    __syncthreads();
-    pdl_trigger();
-#ifdef ST_PROBE
-    const unsigned long long tp0 = st_gt();
-    unsigned long long twait = 0, nwait = 0;
-#endif
-    pdl_wait();   // front rows / the iterate come from the previous launch
-#ifdef ST_PROBE
-    const unsigned long long tp1 = st_gt();
-#endif
-    if (warp == 4) {
-        // ---------------- producer (one lane issues; the others idle) ----------------
-        if (lane != 0) return;
-        int s = 0;
-        uint32_t ph = 0;
-        for (int u = ub; u < ue; ++u) {
-            const STile& T = sT[u / per_tile - tb];
-            const int mat = (u % per_tile) / ncb, cb = u % ncb;
-            const double* Ab = S + (int64_t)mat * slen + st_i64(T.a_lo, T.a_hi);
-            const double* Bb = FRS + ((int64_t)(mat * ncb + cb) * nidx + T.fo) * ldb;
-            const int nch = (T.ke - T.kb + KC - 1) / KC;
-            for (int c = 0; c < nch; ++c) {
-                const int k0 = T.kb + c * KC, kr = min(KC, T.ke - k0);
-                const uint32_t a_bytes = (uint32_t)((kr + 3) >> 2) * T.ng * 256u;
-                const uint32_t b_bytes = (uint32_t)kr * ldb * 8u;
-                st_mbar_wait(bbase + 8 * (ST_MAXST + s), ph ^ 1);
-                const uint32_t full = bbase + 8 * s;
-                const uint32_t st = sbase + (uint32_t)s * stage_bytes;
-                st_mbar_expect_tx(full, a_bytes + b_bytes);
-                st_bulk_g2s(st, Ab + (int64_t)k0 * T.ng * 8, a_bytes, full);
-                st_bulk_g2s(st + A_BYTES, Bb + (int64_t)k0 * ldb, b_bytes, full);
-                s = s + 1 == nst ? 0 : s + 1;
-                if (s == 0) ph ^= 1;
-            }
-        }
-        return;
-    }
-    // ---------------- consumers (warps 0..3: row group = warp) ----------------
     const int g = lane >> 2, q = lane & 3;
-    int s = 0;
-    uint32_t ph = 0;
     for (int u = ub; u < ue; ++u) {
         const STile T = sT[u / per_tile - tb];
         const int mat = (u % per_tile) / ncb, cb = u % ncb;
@@ -729,9 +693,9 @@ __global__ void __launch_bounds__(ST_THREADS, ST_CTAS)
                     const int4 gs = *reinterpret_cast<const int4*>(gsrc + 4 * prow);
                     const int src[4] = {gs.x, gs.y, gs.z, gs.w};
 #pragma unroll
-                    for (int u = 0; u < 4; ++u) {
-                        if (src[u] < 0) break;
-                        const double* pr = FRm + (int64_t)src[u] * ldb;
+                    for (int v = 0; v < 4; ++v) {
+                        if (src[v] < 0) break;
+                        const double* pr = FRm + (int64_t)src[v] * ldb;
 #pragma unroll
                         for (int ct = 0; ct < NCT; ++ct)
 #pragma unroll
@@ -747,14 +711,7 @@ __global__ void __launch_bounds__(ST_THREADS, ST_CTAS)
         for (int ct = 0; ct < NCT; ++ct) acc[ct][0] = acc[ct][1] = acc2[ct][0] = acc2[ct][1] = 0.0;
         const int nch = (T.ke - T.kb + KC - 1) / KC;
         for (int c = 0; c < nch; ++c) {
-#ifdef ST_PROBE
-            const unsigned long long tw0 = st_gt();
-#endif
             st_mbar_wait(bbase + 8 * s, ph);
-#ifdef ST_PROBE
-            twait += st_gt() - tw0;
-            ++nwait;
-#endif
             if (active) {
                 const int kr = min(KC, T.ke - T.kb - c * KC);
                 const int ksteps = (kr + 3) >> 2;
@@ -816,16 +773,62 @@ __global__ void __launch_bounds__(ST_THREADS, ST_CTAS)
                 }
         }
     }
+}
+
+// stage ring set-up shared by both streamed kernels
+__device__ __forceinline__ void st_ring_init(unsigned char* smem, uint32_t bbase, int nst, uint32_t stage_bytes) {
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < nst; ++s) {
+            st_mbar_init(bbase + 8 * s, 1);
+            st_mbar_init(bbase + 8 * (ST_MAXST + s), 4);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    // B regions start finite (rows past a tile's inner range meet zero A entries: 0 * finite = 0)
+    for (uint32_t i = threadIdx.x; i < (uint32_t)nst * stage_bytes / 8; i += blockDim.x)
+        reinterpret_cast<double*>(smem)[i] = 0.0;
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
+// One level and direction of the streamed solve; units [cta_off[b], cta_off[b+1]) per CTA,
+// unit u = (tile * 2 + system) * ncb + column block.
+template <int NCT, int KC>
+__global__ void __launch_bounds__(ST_THREADS, ST_CTAS)
+    k_stream_gemm(const STile* __restrict__ tiles, int tile0, const int32_t* __restrict__ cta_off, int ncb, int cw,
+                  int ldb, const double* __restrict__ S, int64_t slen, double* __restrict__ FRS,
+                  const SolveIO* __restrict__ io, const int32_t* __restrict__ fidx,
+                  const int32_t* __restrict__ gsrc, const int32_t* __restrict__ sc_off,
+                  const int32_t* __restrict__ sc_row, int64_t N, int J, int64_t nidx, int nst,
+                  uint32_t stage_bytes, int probe_id) {
+    extern __shared__ __align__(128) unsigned char smem[];
+    __shared__ __align__(8) uint64_t bars[2 * ST_MAXST];   // full[0..nst), empty[ST_MAXST..)
+    ST_SPAN_BEGIN(probe_id);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t sbase = st_smem_u32(smem);
+    const uint32_t bbase = st_smem_u32(bars);
+    st_ring_init(smem, bbase, nst, stage_bytes);
+    // this CTA's tile descriptors into shared memory (static data: before the dependency wait), so
+    // neither the producer nor the consumers pay a global-load latency per unit
+    const int ub = cta_off[blockIdx.x], ue = cta_off[blockIdx.x + 1];
+    const int per_tile = 2 * ncb;
+    STile* sT = reinterpret_cast<STile*>(smem + (size_t)nst * stage_bytes);
+    const int tb = ub / per_tile, te = ue > ub ? (ue - 1) / per_tile + 1 : tb;
+    for (int i = threadIdx.x; i < (te - tb) * (int)(sizeof(STile) / 4); i += blockDim.x)
+        reinterpret_cast<int*>(sT)[i] = __ldg(reinterpret_cast<const int*>(tiles + tile0 + tb) + i);
+    __syncthreads();
+    pdl_trigger();
+    pdl_wait();   // front rows / the iterate come from the previous launch
+    int s = 0;
+    uint32_t ph = 0;
+    if (warp == 4) {
+        if (lane == 0) st_produce<KC>(sT, tb, ub, ue, per_tile, ncb, ldb, S, slen, FRS, nidx, nst, stage_bytes, sbase,
+                                      bbase, s, ph);
+        return;
+    }
+    st_consume<NCT, KC>(sT, tb, ub, ue, per_tile, ncb, cw, ldb, FRS, io, fidx, gsrc, sc_off, sc_row, N, J, nidx, nst,
+                        stage_bytes, smem, bbase, s, ph);
 #ifdef ST_PROBE
     if (lane == 0) ST_SPAN_END(probe_id);
-    if (warp == 0 && lane == 0 && blockIdx.x < 2048 && probe_id == g_probe_target) {
-        g_stp[blockIdx.x][0] = tp0;
-        g_stp[blockIdx.x][1] = tp1 - tp0;
-        g_stp[blockIdx.x][2] = st_gt() - tp1;
-        g_stp[blockIdx.x][3] = twait;
-        g_stp[blockIdx.x][4] = nwait;
-        g_stp[blockIdx.x][5] = ue - ub;
-    }
 #endif
 }
 
