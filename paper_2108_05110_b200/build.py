@@ -17,8 +17,25 @@ LIB = os.path.join(HERE, "libensmhd_b200.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
 
+HOST_LIB = os.path.join(HERE, "libensmhd_host.so")
+HOST_SRC = os.path.join(HERE, "csrc", "host_symbolic.cpp")
+
+
 def sources():
     return sorted(glob.glob(os.path.join(HERE, "csrc", "*.cu")))
+
+
+def build_host(force: bool = False) -> str:
+    """The host-side setup helpers (csrc/host_symbolic.cpp): plain C++, g++ -O2."""
+    if not force and os.path.exists(HOST_LIB) and os.path.getmtime(HOST_LIB) >= os.path.getmtime(HOST_SRC):
+        return HOST_LIB
+    cmd = ["g++", "-O2", "-std=c++17", "-fPIC", "-shared", "-o", HOST_LIB + ".tmp", HOST_SRC]
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    if r.returncode != 0:
+        sys.stderr.write(r.stdout + r.stderr)
+        raise RuntimeError("g++ failed building libensmhd_host.so")
+    os.replace(HOST_LIB + ".tmp", HOST_LIB)
+    return HOST_LIB
 
 
 def deps():
@@ -34,6 +51,7 @@ def up_to_date() -> bool:
 
 
 def build(force: bool = False, verbose: bool = False) -> str:
+    build_host(force)
     if not force and up_to_date():
         return LIB
     cmd = [NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",

@@ -47,7 +47,56 @@ LEAF_NODES = int(__import__("os").environ.get("ENS_LEAF", "24"))  # stop dissect
 # ----------------------------------------------------------------------
 
 
+_HOST = None
+
+
+def _host():
+    """ctypes handle on libensmhd_host.so (csrc/host_symbolic.cpp), built on first use."""
+    global _HOST
+    if _HOST is None:
+        import ctypes as C
+        from . import build as B
+        lib = C.CDLL(B.build_host())
+        P = C.c_void_p
+        lib.ens_host_nested_dissection.restype = C.c_int64
+        lib.ens_host_nested_dissection.argtypes = [C.c_int64, P, C.c_int64, P, P, C.c_int64, C.c_int64, P, P, P]
+        lib.ens_host_symbolic_cb.restype = C.c_int64
+        lib.ens_host_symbolic_cb.argtypes = [C.c_int64, P, P, P, P, P, P, P]
+        lib.ens_host_front_local.restype = None
+        lib.ens_host_front_local.argtypes = [C.c_int64, P, P, P, P, P]
+        _HOST = lib
+    return _HOST
+
+
+def _ptr(a):
+    return a.ctypes.data
+
+
 def _nested_dissection(coords, indptr, indices, leaf=LEAF_NODES):
+    """Return (tree_nodes: list of node arrays, children: list of lists, root).
+
+    Runs csrc/host_symbolic.cpp (ens_host_nested_dissection), the C++ restatement of
+    `_nested_dissection_py` below (which remains the specification)."""
+    n = coords.shape[0]
+    rows = np.ascontiguousarray(np.repeat(np.arange(n, dtype=np.int64), np.diff(indptr)))
+    cols = np.ascontiguousarray(indices, dtype=np.int64)
+    xy = np.ascontiguousarray(coords, dtype=np.float64)
+    cap = 2 * n + 16
+    off = np.zeros(cap + 1, dtype=np.int64)
+    nodes = np.zeros(n, dtype=np.int64)
+    par = np.zeros(cap, dtype=np.int64)
+    T = _host().ens_host_nested_dissection(n, _ptr(xy), len(rows), _ptr(rows), _ptr(cols), int(leaf), cap,
+                                           _ptr(off), _ptr(nodes), _ptr(par))
+    if T < 0:
+        raise RuntimeError("nested dissection: tree capacity exceeded")
+    tnodes = [nodes[off[t]:off[t + 1]].copy() for t in range(T)]
+    kids = [[] for _ in range(T)]
+    for t in range(1, T):
+        kids[par[t]].append(t)
+    return tnodes, kids, 0
+
+
+def _nested_dissection_py(coords, indptr, indices, leaf=LEAF_NODES):
     """Return (tree_nodes: list of node arrays, children: list of lists, root)."""
     n = coords.shape[0]
     rows = np.repeat(np.arange(n, dtype=np.int64), np.diff(indptr))
@@ -269,16 +318,20 @@ def analyse(disc, leaf=LEAF_NODES, pw=PW):
         if fparent[f] >= 0:
             children[fparent[f]].append(f)
 
-    # symbolic factorisation: CB(f) = (later neighbours of pivots U children CBs) \ pivots
-    cb = [None] * F
-    for f in range(F):                               # postorder: children first
-        s, e = fs[f], fe_[f]
-        cols = fp.indices[fp.indptr[s]:fp.indptr[e]]
-        parts = [cols[cols >= e]]
-        for c in children[f]:
-            parts.append(cb[c][cb[c] >= e])
-        u = np.unique(np.concatenate(parts)) if parts else np.zeros(0, dtype=np.int64)
-        cb[f] = u.astype(np.int64)
+    # symbolic factorisation: CB(f) = (later neighbours of pivots U children CBs) \ pivots, postorder
+    # (children first); csrc/host_symbolic.cpp ens_host_symbolic_cb, the C++ restatement of
+    #   cols = fp.indices[fp.indptr[s]:fp.indptr[e]];  cb[f] = unique(cols[cols >= e] U cb[c][cb[c] >= e])
+    fs64, fe64 = np.ascontiguousarray(fs, dtype=np.int64), np.ascontiguousarray(fe_, dtype=np.int64)
+    fpar64 = np.ascontiguousarray(fparent, dtype=np.int64)
+    ip64 = np.ascontiguousarray(fp.indptr, dtype=np.int64)
+    ind32 = np.ascontiguousarray(fp.indices, dtype=np.int32)
+    cb_off = np.zeros(F + 1, dtype=np.int64)
+    lib = _host()
+    tot = lib.ens_host_symbolic_cb(F, _ptr(fs64), _ptr(fe64), _ptr(fpar64), _ptr(ip64), _ptr(ind32), _ptr(cb_off), None)
+    cb_all = np.zeros(max(int(tot), 1), dtype=np.int64)
+    lib.ens_host_symbolic_cb(F, _ptr(fs64), _ptr(fe64), _ptr(fpar64), _ptr(ip64), _ptr(ind32), _ptr(cb_off),
+                             _ptr(cb_all))
+    cb = [cb_all[cb_off[f]:cb_off[f + 1]] for f in range(F)]
     k = (fe_ - fs).astype(np.int64)
     cbn = np.array([len(c) for c in cb], dtype=np.int64)
     m = k + cbn
@@ -312,30 +365,26 @@ def analyse(disc, leaf=LEAF_NODES, pw=PW):
     f_idx_elim = np.concatenate(lists)
     f_idx = elim_to_int[f_idx_elim].astype(np.int32)
 
-    # local position lookup: key = front * nf + elimpos
-    keys = np.repeat(np.arange(F, dtype=np.int64), f_m) * nf + f_idx_elim
-    korder = np.argsort(keys, kind="stable")
-    skeys = keys[korder]
-    local_of = (np.arange(len(keys)) - np.repeat(f_idx_off[:-1], f_m))[korder]
+    # local position of an elimination index in a front: every front's index list is ascending
+    # (pivot range, then the sorted contribution block) -> binary search per query (C++)
+    f_idx_elim = np.ascontiguousarray(f_idx_elim, dtype=np.int64)
+    f_idx_off = np.ascontiguousarray(f_idx_off, dtype=np.int64)
 
     def lookup(front, epos):
-        kk = front.astype(np.int64) * nf + epos
-        i = np.searchsorted(skeys, kk)
-        assert np.all(skeys[i] == kk), "symbolic lookup failed"
-        return local_of[i]
+        fq = np.ascontiguousarray(front, dtype=np.int64)
+        eq = np.ascontiguousarray(epos, dtype=np.int64)
+        out = np.empty(len(fq), dtype=np.int64)
+        _host().ens_host_front_local(len(fq), _ptr(fq), _ptr(eq), _ptr(f_idx_off), _ptr(f_idx_elim), _ptr(out))
+        assert np.all(out >= 0), "symbolic lookup failed"
+        return out
 
-    # child CB -> parent local map
-    cmaps, cmap_off = [], np.zeros(F + 1, dtype=np.int64)
-    for i in range(F):
-        if f_parent[i] >= 0:
-            cbl = f_idx_elim[f_idx_off[i] + f_k[i]: f_idx_off[i + 1]]
-            mp = lookup(np.full(len(cbl), f_parent[i]), cbl)
-        else:
-            mp = np.zeros(0, dtype=np.int64)
-            assert f_m[i] == f_k[i], "root front must have an empty CB"
-        cmaps.append(mp)
-        cmap_off[i + 1] = cmap_off[i] + len(mp)
-    f_cmap = np.concatenate(cmaps).astype(np.int32) if cmaps else np.zeros(0, np.int32)
+    # child CB -> parent local map (all fronts in one lookup: positions in front order)
+    pos_front = np.repeat(np.arange(F, dtype=np.int64), f_m)
+    pos_local = np.arange(len(f_idx_elim), dtype=np.int64) - np.repeat(f_idx_off[:-1], f_m)
+    is_cb = pos_local >= f_k[pos_front]
+    assert np.all(f_parent[pos_front[is_cb]] >= 0), "root front must have an empty CB"
+    f_cmap = lookup(f_parent[pos_front[is_cb]], f_idx_elim[is_cb]).astype(np.int32)
+    cmap_off = np.concatenate([[0], np.cumsum(f_m - f_k)]).astype(np.int64)
 
     # original entries: A_s (both components) and B / -B^T, between free dofs
     nnz_s = As.nnz
@@ -365,8 +414,7 @@ def analyse(disc, leaf=LEAF_NODES, pw=PW):
     first = np.minimum(er, ec)
     # front owning elimination position `first`
     piv_front_of_e = np.empty(nf, dtype=np.int64)
-    for i in range(F):
-        piv_front_of_e[f_idx_elim[f_idx_off[i]:f_idx_off[i] + f_k[i]]] = i
+    piv_front_of_e[f_idx_elim[~is_cb]] = pos_front[~is_cb]
     fr = piv_front_of_e[first]
     lr = lookup(fr, er)
     lc = lookup(fr, ec)
@@ -386,10 +434,11 @@ def analyse(disc, leaf=LEAF_NODES, pw=PW):
         schedule={}, stats={},
     )
     plan.schedule = build_schedule(plan, pw)
-    flops = 0.0
-    for i in range(F):
-        mm, kk = int(f_m[i]), int(f_k[i])
-        flops += sum(2.0 * (mm - t - 1) ** 2 for t in range(0, kk, 1)) if kk < 4096 else 0.0
+    # sweep flops: sum_{t<k} 2 (m - 1 - t)^2 = 2 (S(m - 1) - S(m - k - 1)), S(n) = n (n + 1) (2n + 1) / 6
+    def sq_sum(n):
+        n = n.astype(np.float64)
+        return n * (n + 1.0) * (2.0 * n + 1.0) / 6.0
+    flops = float(np.sum(2.0 * (sq_sum(f_m - 1) - sq_sum(f_m - f_k - 1))))
     plan.stats = dict(fronts=F, levels=nlevels, n_free=nf, max_m=int(f_m.max()), max_k=int(f_k.max()),
                       storage_doubles=storage, factor_flops=flops,
                       nnz_lu=float(np.sum(f_m.astype(np.float64) ** 2 - (f_m - f_k).astype(np.float64) ** 2)))

@@ -112,3 +112,21 @@ def test_split_k_schedule(rng, monkeypatch):
     x = E.solve(plan, st, bi)[iid]
     res = np.linalg.norm(K @ x - b, axis=0) / np.linalg.norm(b, axis=0)
     assert res.max() < 1e-11, res
+
+
+@pytest.mark.parametrize("n", [4, 16, 40])
+def test_host_nested_dissection_matches_python_spec(n):
+    """csrc/host_symbolic.cpp's nested dissection = symbolic._nested_dissection_py (node sets, tree
+    shape, numbering), on the P2 node graph of an n x n square."""
+    from paper_2108_05110_b200 import fe
+    from paper_2108_05110_b200 import symbolic as S
+    disc = Discretization.from_mesh(build_structured_square(n), pressure="th")
+    g = fe.scalar_pattern(disc.velocity).copy()
+    g.setdiag(0)
+    g.eliminate_zeros()
+    g.sort_indices()
+    a = S._nested_dissection(disc.velocity.dof_coords, g.indptr, g.indices, 24)
+    b = S._nested_dissection_py(disc.velocity.dof_coords, g.indptr, g.indices, 24)
+    assert len(a[0]) == len(b[0]) and a[1] == b[1]
+    for x, y in zip(a[0], b[0]):
+        assert np.array_equal(np.sort(x), np.sort(y)) and np.array_equal(x, y)
