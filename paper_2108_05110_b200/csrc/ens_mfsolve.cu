@@ -604,6 +604,15 @@ extern "C" int ens_stream_probe_dump(const char* path) {
 #define ST_SPAN_END(id)
 #endif
 
+// ENS_BOUNDS_CHECK builds (tools/sanitize_run.py; compute-sanitizer is not available on the GPU
+// pool): device asserts on every index the streamed solve derives from the plan
+#ifdef ENS_BOUNDS_CHECK
+#include <cassert>
+#define ST_ASSERT(c) assert(c)
+#else
+#define ST_ASSERT(c)
+#endif
+
 // factor entries -> fragment-ordered tile stream (one CTA per tile and system)
 __global__ void __launch_bounds__(256) k_stream_pack(const STile* __restrict__ tiles, const double* __restrict__ F,
                                                      int64_t storage, double* __restrict__ S, int64_t slen) {
@@ -615,6 +624,10 @@ __global__ void __launch_bounds__(256) k_stream_pack(const STile* __restrict__ t
     const double* base = F + (int64_t)mat * storage + st_i64(T.src_lo, T.src_hi);
     double* out = S + (int64_t)mat * slen + st_i64(T.a_lo, T.a_hi);
     const int total = Kp * T.ng * 8;
+    ST_ASSERT(st_i64(T.a_lo, T.a_hi) + total <= slen);
+    ST_ASSERT(st_i64(T.src_lo, T.src_hi) + (int64_t)T.m * T.m <= storage);
+    ST_ASSERT(T.row0 + nr <= T.m && T.K <= T.m && T.ng >= 1 && T.ng <= 4);
+    // thread e writes stream entry e (coalesced); entry e = k-step u, row group w, lane (g, q)
     for (int e = threadIdx.x; e < total; e += blockDim.x) {
         const int lane = e & 31, grp = e >> 5;
         const int u = grp / T.ng, w = grp - u * T.ng;
@@ -623,8 +636,7 @@ __global__ void __launch_bounds__(256) k_stream_pack(const STile* __restrict__ t
     }
 }
 
-// Producer of a unit range: streams every chunk of units [ub, ue) through the stage ring
-// (state s / ph carried across ranges by the persistent kernel).
+// Producer of a unit range: streams every chunk of units [ub, ue) through the stage ring.
 template <int KC>
 __device__ __forceinline__ void st_produce(const STile* sT, int tb, int ub, int ue, int per_tile, int ncb, int ldb,
                                            const double* __restrict__ S, int64_t slen,
@@ -641,6 +653,8 @@ __device__ __forceinline__ void st_produce(const STile* sT, int tb, int ub, int 
             const int k0 = T.kb + c * KC, kr = min(KC, T.ke - k0);
             const uint32_t a_bytes = (uint32_t)((kr + 3) >> 2) * T.ng * 256u;
             const uint32_t b_bytes = (uint32_t)kr * ldb * 8u;
+            ST_ASSERT(st_i64(T.a_lo, T.a_hi) + (int64_t)k0 * T.ng * 8 + a_bytes / 8 <= slen);
+            ST_ASSERT(T.fo + k0 + kr <= nidx && a_bytes <= A_BYTES);
             st_mbar_wait(bbase + 8 * (ST_MAXST + s), ph ^ 1);
             const uint32_t full = bbase + 8 * s;
             const uint32_t st = sbase + (uint32_t)s * stage_bytes;
@@ -683,7 +697,9 @@ __device__ __forceinline__ void st_consume(const STile* sT, int tb, int ub, int 
         for (int ct = 0; ct < NCT; ++ct) init[ct][0] = init[ct][1] = 0.0;
         if (row_ok) {
             const int64_t prow = T.fo + T.r0 + row + (bwd ? 0 : T.kp);
+            ST_ASSERT(prow < nidx);
             if (bwd) {
+                ST_ASSERT(__ldg(fidx + prow) >= 0 && __ldg(fidx + prow) < N);
                 out_row = io->z + (int64_t)mat * N * J + (int64_t)__ldg(fidx + prow) * J + j0;
                 sc0 = __ldg(sc_off + prow);
                 sc1 = __ldg(sc_off + prow + 1);
@@ -763,6 +779,7 @@ __device__ __forceinline__ void st_consume(const STile* sT, int tb, int ub, int 
                 if (col < jn) out_row[col] = res[ct][e];
             }
         for (int t = sc0; t < sc1; ++t) {   // backward: the solution row into every descendant that reads it
+            ST_ASSERT(__ldg(sc_row + t) >= 0 && __ldg(sc_row + t) < nidx);
             double* dr = FRm + (int64_t)__ldg(sc_row + t) * ldb;
 #pragma unroll
             for (int ct = 0; ct < NCT; ++ct)
@@ -851,7 +868,9 @@ __global__ void __launch_bounds__(256) k_sfinit(const int32_t* __restrict__ rows
         const int col = cb * cw + 2 * i;
         if (col >= J) continue;
         const int64_t row = rows[rq];
+        ST_ASSERT(row >= 0 && row < nidx && idx[row] >= 0 && idx[row] < N);
         const int4 g = *reinterpret_cast<const int4*>(gsrc + 4 * row);
+        ST_ASSERT(g.x < nidx && g.y < nidx && g.z < nidx && g.w < nidx);
         const double2* F2 = reinterpret_cast<const double2*>(FRS + (int64_t)(mat * ncb + cb) * nidx * ldb);
         const int h = ldb >> 1;
         double2 v = *reinterpret_cast<const double2*>(b + (int64_t)idx[row] * J + col);
