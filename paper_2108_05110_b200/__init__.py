@@ -12,7 +12,7 @@ from .ensemble import (EnsembleConfig, EnsembleState, MemberParams, elsasser_fro
                        viscosity_stats)
 from .mesh import Marker, Mesh, barycentric_refine, build_step_channel, build_structured_square
 from .problems import (BaselineMms, PaperMmsBoundary, PaperMmsForcing, ScaledProfileBoundary, ZeroBoundary,
-                       ZeroForcing, build_case, paper_mms_initial_fields)
+                       ZeroForcing, build_case, paper_mms_initial_fields, RankOneMembers, member_rows)
 from .linalg import Factorization, SingularMatrixError, factorize, relative_residual
 from .stepper import (Problem, RunReport, StepFailure, StepKind, StepSystem, advance, assemble_member_rhs,
                       assemble_shared_lhs, check_preconditions, energy, run, set_solver_options,
@@ -24,7 +24,7 @@ __all__ = [
     "build_structured_square", "check_preconditions", "elsasser_from_primitive", "energy",
     "primitive_from_elsasser", "run", "sample_viscosities", "verify_stability_bound", "viscosity_stats",
     "perturbation_factor", "perturbation_factors", "BaselineMms", "PaperMmsForcing", "PaperMmsBoundary",
-    "ZeroForcing", "ZeroBoundary", "ScaledProfileBoundary", "build_case", "paper_mms_initial_fields",
+    "ZeroForcing", "ZeroBoundary", "ScaledProfileBoundary", "build_case", "paper_mms_initial_fields", "RankOneMembers", "member_rows",
     "set_solver_options", "StepSystem", "assemble_shared_lhs", "assemble_member_rhs", "Factorization",
     "SingularMatrixError", "factorize", "relative_residual",
 ]

@@ -26,10 +26,10 @@ def sources():
 
 
 def build_host(force: bool = False) -> str:
-    """The host-side setup helpers (csrc/host_symbolic.cpp): plain C++, g++ -O2."""
+    """The host-side setup helpers (csrc/host_symbolic.cpp): C++ with OpenMP, g++ -O2 -fopenmp."""
     if not force and os.path.exists(HOST_LIB) and os.path.getmtime(HOST_LIB) >= os.path.getmtime(HOST_SRC):
         return HOST_LIB
-    cmd = ["g++", "-O2", "-std=c++17", "-fPIC", "-shared", "-o", HOST_LIB + ".tmp", HOST_SRC]
+    cmd = ["g++", "-O2", "-std=c++17", "-fopenmp", "-fPIC", "-shared", "-o", HOST_LIB + ".tmp", HOST_SRC]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         sys.stderr.write(r.stdout + r.stderr)

@@ -108,7 +108,8 @@ class ChunkedEngine(Engine):
         g = self._staging()
         s = self.stream
         nv, Jc = self.nvel, self.Jc
-        v, w = np.asarray(v, dtype=float), np.asarray(w, dtype=float)
+        from .problems import RankOneMembers
+        v, w = (a if isinstance(a, RankOneMembers) else np.asarray(a, dtype=float) for a in (v, w))
         has_p = q is not None and np.asarray(q).size > 0
         cur = self.cur
         self._retire(cur)
@@ -117,7 +118,7 @@ class ChunkedEngine(Engine):
             with torch.cuda.stream(s):
                 Xs = g["x_in"]
                 for m, a in enumerate((v, w)):
-                    g["d_vel"][m].copy_(self._host_tensor(a[sl]))
+                    self._copy_members(g["d_vel"][m], a[sl])
                     torch.index_select(g["d_vel"][m].t(), 0, g["ref_of_int_v"], out=Xs[m, :nv])
                 if has_p:
                     for m, a in enumerate((q, r)):

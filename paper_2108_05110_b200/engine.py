@@ -163,11 +163,11 @@ class HostMesh:
         bip, bcol, bx, by = fe.divergence_pair(vel, pres)
         brow = np.repeat(np.arange(npres), np.diff(bip))
         r_int, c_int = pperm[brow], nperm[bcol]
-        o = np.lexsort((c_int, r_int))
+        o = S.host_argsort(r_int * (ns + 1) + c_int)         # == lexsort((c_int, r_int))
         self.b_rowptr = np.concatenate([[0], np.cumsum(np.bincount(r_int, minlength=npres))]).astype(np.int32)
         self.b_col = c_int[o].astype(np.int32)
         self.b_val = np.stack([bx[o], by[o]], axis=1).ravel()
-        o2 = np.lexsort((r_int, c_int))
+        o2 = S.host_argsort(c_int * (npres + 1) + r_int)     # == lexsort((r_int, c_int))
         self.bt_rowptr = np.concatenate([[0], np.cumsum(np.bincount(c_int, minlength=ns))]).astype(np.int32)
         self.bt_col = r_int[o2].astype(np.int32)
         self.bt_val = np.stack([bx[o2], by[o2]], axis=1).ravel()
@@ -197,23 +197,26 @@ class HostMesh:
         # gather lists for the scatter-free member pass / assembly (fixed element order)
         nt = len(self.e_nodes)
         en = self.e_nodes.ravel()
-        o = np.argsort(en, kind="stable")
+        o = S.host_argsort(en)                                          # stable
         self.n2e = o.astype(np.int32)                                   # e*6 + a
-        self.n2e_ptr = np.searchsorted(en[o], np.arange(ns + 1)).astype(np.int32)
-        o = np.argsort(self.e_slots, kind="stable")
+        self.n2e_ptr = np.concatenate([[0], np.cumsum(np.bincount(en, minlength=ns))]).astype(np.int32)
+        o = S.host_argsort(self.e_slots)
         self.s2e = ((o % 36) * nt + o // 36).astype(np.int32)          # ab*nt + e
-        self.s2e_ptr = np.searchsorted(self.e_slots[o], np.arange(self.nnz_s + 1)).astype(np.int32)
+        self.s2e_ptr = np.concatenate([[0], np.cumsum(np.bincount(self.e_slots, minlength=self.nnz_s))]).astype(np.int32)
         self.pres_int = np.empty(npres)
         self.pres_int[pperm] = disc.pressure_integrals
+        self._allkey = None                                             # slot-lookup keys: setup only
 
     def _slot(self, rows, cols):
         rows = np.asarray(rows, dtype=np.int64)
         cols = np.asarray(cols, dtype=np.int64)
         key = rows * (self.ns + 1) + cols
-        allrows = np.repeat(np.arange(self.ns, dtype=np.int64), np.diff(self.s_rowptr))
-        allkey = allrows * (self.ns + 1) + self.s_col
-        pos = np.searchsorted(allkey, key)
-        assert np.all(allkey[pos] == key), "slot lookup failed"
+        if getattr(self, "_allkey", None) is None:
+            allrows = np.repeat(np.arange(self.ns, dtype=np.int64), np.diff(self.s_rowptr))
+            self._allkey = allrows * (self.ns + 1) + self.s_col
+        allkey = self._allkey
+        pos = S.host_searchsorted(allkey, key)
+        assert np.all(allkey[np.minimum(pos, allkey.size - 1)] == key), "slot lookup failed"
         return pos
 
     # host <-> internal conversions (numpy)
@@ -226,9 +229,12 @@ class HostMesh:
 
 
 def host_mesh(disc) -> HostMesh:
+    """The mesh's HostMesh, built once per Discretization (large meshes: through the on-disk
+    setup cache, setup_cache.py)."""
     key = "b200-hostmesh"
     if key not in disc._cache:
-        disc._cache[key] = HostMesh(disc)
+        from . import setup_cache
+        disc._cache[key] = setup_cache.host_mesh(disc)
     return disc._cache[key]
 
 
@@ -478,6 +484,21 @@ class Engine:
                 return torch.from_numpy(arr)
         return torch.from_numpy(arr)
 
+    def _copy_members(self, dst, a):
+        """dst (J, n) on the device <- a (J, n) member array.  A RankOneMembers (amp x base) is
+        expanded on the device -- the same IEEE products as np.outer -- so only amp and base cross
+        PCIe; anything else is copied from host memory.  Returns the host tensor to keep alive
+        until the copy completes (None for the device expansion)."""
+        from .problems import RankOneMembers
+        if isinstance(a, RankOneMembers):
+            amp = torch.from_numpy(np.ascontiguousarray(a.amp)).to(dst.device)
+            base = torch.from_numpy(np.ascontiguousarray(a.base)).to(dst.device)
+            torch.mul(amp[:, None], base[None, :], out=dst)
+            return None
+        h = self._host_tensor(a)
+        dst.copy_(h, non_blocking=h.is_pinned())
+        return h
+
     def load_state(self, v, w, q, r):
         """Upload a host state (reference layout, this rank's members) into the current buffer set.
 
@@ -494,11 +515,10 @@ class Engine:
         g = self._staging()
         s = self.stream
         nv = self.nvel
-        hv, hw = self._host_tensor(v), self._host_tensor(w)
         has_p = q is not None and np.asarray(q).size > 0
         with torch.cuda.stream(s):
-            g["d_vel"][0].copy_(hv, non_blocking=hv.is_pinned())
-            g["d_vel"][1].copy_(hw, non_blocking=hw.is_pinned())
+            hv = self._copy_members(g["d_vel"][0], v)
+            hw = self._copy_members(g["d_vel"][1], w)
             Xs = g["x_in"]
             for m in range(2):
                 torch.index_select(g["d_vel"][m].t(), 0, g["ref_of_int_v"], out=Xs[m, :nv])

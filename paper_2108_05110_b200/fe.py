@@ -96,7 +96,9 @@ class VelocitySpace:
         t = mesh.triangles
         nv = mesh.num_vertices
         pairs = np.sort(np.vstack([t[:, [0, 1]], t[:, [1, 2]], t[:, [2, 0]]]), axis=1)
-        self.edges, inv = np.unique(pairs, axis=0, return_inverse=True)
+        # == np.unique(pairs, axis=0, return_inverse=True): lexicographic pairs order as one int64 key
+        ukey, inv = np.unique(pairs[:, 0].astype(np.int64) * nv + pairs[:, 1], return_inverse=True)
+        self.edges = np.stack([ukey // nv, ukey % nv], axis=1).astype(pairs.dtype)
         inv = inv.reshape(-1)
         nt = mesh.num_triangles
         cell_edges = np.stack([inv[:nt], inv[nt:2 * nt], inv[2 * nt:]], axis=1)
@@ -196,11 +198,16 @@ def _scatter(rows_dofs, cols_dofs, local, shape) -> sp.csr_matrix:
 
 
 def scalar_pattern(vel: VelocitySpace) -> sp.csr_matrix:
-    """Element-connectivity pattern of the scalar P2 operators (values = 1)."""
+    """Element-connectivity pattern of the scalar P2 operators (values = 1); built once per space
+    (callers must not modify it)."""
+    cached = getattr(vel, "_pattern", None)
+    if cached is not None:
+        return cached
     nt = vel.mesh.num_triangles
     ns = vel.num_scalar_dofs
     a = _scatter(vel.cell_dofs, vel.cell_dofs, np.ones((nt, 6, 6)), (ns, ns))
     a.data[:] = 1.0
+    vel._pattern = a
     return a
 
 

@@ -40,6 +40,42 @@ class Separable:
     key: str = ""              # cache key for the uploaded basis
 
 
+class RankOneMembers:
+    """Member fields amp[j] * base as a lazy (J, n) array.
+
+    The BASELINE MMS initial fields are rank one; at C5 (J=1024, n_vel=2.1M) the dense
+    np.outer would be a 17 GB host array built only to be sliced per member chunk.  Row
+    slices (``x[a:b]``) build just those rows; ``np.asarray(x)`` materialises the whole array
+    (the reference's (J, n_vel) interface, identical values)."""
+
+    def __init__(self, amp, base):
+        self.amp = np.asarray(amp, dtype=float)
+        self.base = np.asarray(base, dtype=float)
+        self.shape = (self.amp.size, self.base.size)
+        self.dtype = np.dtype(float)
+        self.ndim = 2
+
+    def __len__(self):
+        return self.shape[0]
+
+    def __getitem__(self, idx):
+        if isinstance(idx, slice):
+            return np.outer(self.amp[idx], self.base)
+        return np.asarray(self)[idx]
+
+    def __array__(self, dtype=None, copy=None):
+        out = np.outer(self.amp, self.base)
+        return out if dtype is None else out.astype(dtype, copy=False)
+
+
+def member_rows(arr, j0, jl):
+    """Rows j0 .. j0+jl of a (J, n) member array: a float64 ndarray, or a RankOneMembers of those
+    rows (still lazy: the engines expand it on the device)."""
+    if isinstance(arr, RankOneMembers):
+        return RankOneMembers(arr.amp[j0:j0 + jl], arr.base)
+    return np.asarray(arr[j0:j0 + jl], dtype=float)
+
+
 class ZeroForcing:
     """No body forces (`stepper.py:286-290`)."""
 
@@ -241,7 +277,8 @@ class BaselineMms:
     def initial_fields(self, disc, config):
         base = fe.interpolate(_cs, 0.0, disc.velocity)
         amp = 2.0 * (1.0 + self.eps(config))
-        return np.outer(amp, base), np.zeros((config.num_members, disc.n_vel))
+        # <w>(0) = 0: a zero rank-one product (0 * +0 = +0, bitwise np.zeros)
+        return RankOneMembers(amp, base), RankOneMembers(np.zeros(config.num_members), np.zeros(disc.n_vel))
 
     def exact_v(self, t, disc, config):
         base = fe.interpolate(_cs, t, disc.velocity)

@@ -392,8 +392,9 @@ def run(config: EnsembleConfig, problem: Problem, observer=None, snapshot_steps=
                        alpha=st.alpha, mu=config.mu, dt=config.dt,
                        member_l2v_sq=np.zeros((m + 1, J)), member_l2w_sq=np.zeros((m + 1, J)),
                        member_gradv_sq=np.zeros((m + 1, J)), member_gradw_sq=np.zeros((m + 1, J)))
-    v0 = np.asarray(problem.initial_v, dtype=float)[j0:j0 + jl]
-    w0 = np.asarray(problem.initial_w, dtype=float)[j0:j0 + jl]
+    from .problems import member_rows
+    v0 = member_rows(problem.initial_v, j0, jl)
+    w0 = member_rows(problem.initial_w, j0, jl)
     engine.load_state(v0, w0, None, None)
     state = EnsembleState(step=0, time=0.0, device=engine.state_handle())
     local = [] if comm is not None else None

@@ -64,12 +64,42 @@ def _host():
         lib.ens_host_symbolic_cb.argtypes = [C.c_int64, P, P, P, P, P, P, P]
         lib.ens_host_front_local.restype = None
         lib.ens_host_front_local.argtypes = [C.c_int64, P, P, P, P, P]
+        lib.ens_host_argsort_i64.restype = None
+        lib.ens_host_argsort_i64.argtypes = [C.c_int64, P, P]
+        lib.ens_host_sort_i64.restype = None
+        lib.ens_host_sort_i64.argtypes = [C.c_int64, P]
+        lib.ens_host_searchsorted_i64.restype = None
+        lib.ens_host_searchsorted_i64.argtypes = [C.c_int64, P, C.c_int64, P, P]
         _HOST = lib
     return _HOST
 
 
 def _ptr(a):
     return a.ctypes.data
+
+
+def host_argsort(keys):
+    """np.argsort(keys, kind="stable") for int64 keys, on all host cores (ens_host_argsort_i64)."""
+    k = np.ascontiguousarray(keys, dtype=np.int64)
+    out = np.empty(k.size, dtype=np.int64)
+    _host().ens_host_argsort_i64(k.size, _ptr(k), _ptr(out))
+    return out
+
+
+def host_sort(keys):
+    """np.sort(keys) for int64 keys (a new array), on all host cores (ens_host_sort_i64)."""
+    k = np.array(keys, dtype=np.int64, copy=True, order="C")
+    _host().ens_host_sort_i64(k.size, _ptr(k))
+    return k
+
+
+def host_searchsorted(a, q):
+    """np.searchsorted(a, q) (left) for int64, on all host cores (ens_host_searchsorted_i64)."""
+    a = np.ascontiguousarray(a, dtype=np.int64)
+    q = np.ascontiguousarray(q, dtype=np.int64)
+    out = np.empty(q.size, dtype=np.int64)
+    _host().ens_host_searchsorted_i64(a.size, _ptr(a), q.size, _ptr(q), _ptr(out))
+    return out
 
 
 def _nested_dissection(coords, indptr, indices, leaf=LEAF_NODES):
@@ -218,19 +248,28 @@ def analyse(disc, leaf=LEAF_NODES, pw=PW):
     rank[post] = np.arange(T)
 
     # internal node numbering: tree nodes in postorder, nodes in coordinate order inside
-    node_perm = np.empty(ns, dtype=np.int64)
-    tnode_of_node = np.empty(ns, dtype=np.int64)
-    pos = 0
+    # (vectorised over tree nodes: inside a tree node, nodes are sorted along the node's main axis,
+    # then the other coordinate, then their position in the tree node -- SpMM locality)
     coords = vel.dof_coords
-    for t in post:
-        nd = tnodes[t]
-        if len(nd) > 1:   # spatial order inside a tree node (separators are lines): SpMM locality
-            c = coords[nd]
-            ax = int(np.argmax(c.max(0) - c.min(0)))
-            nd = nd[np.lexsort((c[:, 1 - ax], c[:, ax]))]
-        node_perm[nd] = pos + np.arange(len(nd))
-        tnode_of_node[nd] = t
-        pos += len(nd)
+    sizes = np.array([len(tnodes[t]) for t in post], dtype=np.int64)
+    cat = np.concatenate([tnodes[t] for t in post]).astype(np.int64)
+    grp = np.repeat(np.arange(T, dtype=np.int64), sizes)
+    within = np.arange(len(cat), dtype=np.int64) - np.repeat(np.cumsum(sizes) - sizes, sizes)
+    cc = coords[cat]
+    starts = np.cumsum(sizes) - sizes
+    nz = sizes > 0
+    ext = np.zeros((T, 2))
+    ext[nz] = np.maximum.reduceat(cc, starts[nz], axis=0) - np.minimum.reduceat(cc, starts[nz], axis=0)
+    ax_t = np.where(ext[:, 1] > ext[:, 0], 1, 0)
+    ax_n = ax_t[grp]
+    multi = sizes[grp] > 1
+    prim = np.where(multi, cc[np.arange(len(cat)), ax_n], 0.0)
+    sec = np.where(multi, cc[np.arange(len(cat)), 1 - ax_n], 0.0)
+    o = np.lexsort((within, sec, prim, grp))
+    node_perm = np.empty(ns, dtype=np.int64)
+    node_perm[cat[o]] = np.arange(len(cat))
+    tnode_of_node = np.empty(ns, dtype=np.int64)
+    tnode_of_node[cat] = post[grp]
 
     # free dofs (reference numbering): velocity x = s, y = ns + s ; pressure nvel + p
     cons = np.zeros(n_total, dtype=bool)
@@ -251,15 +290,15 @@ def analyse(disc, leaf=LEAF_NODES, pw=PW):
     # within a tree node, pressures are ordered along the node group's main axis
     # (moved-up pressures from both sides of a separator interleave spatially)
     pc = disc.pressure.dof_coords
-    key2 = np.zeros(npres)
     grp_order = np.argsort(best, kind="stable")
     bounds = np.searchsorted(best[grp_order], np.unique(best))
-    bounds = np.append(bounds, npres)
-    for a_, b_ in zip(bounds[:-1], bounds[1:]):
-        g = grp_order[a_:b_]
-        c = pc[g]
-        ax = int(np.argmax(c.max(0) - c.min(0))) if len(g) > 1 else 0
-        key2[g] = c[:, ax] * 4.0 + c[:, 1 - ax] * 1e-6
+    gsz = np.diff(np.append(bounds, npres))
+    pcs = pc[grp_order]
+    gext = np.maximum.reduceat(pcs, bounds, axis=0) - np.minimum.reduceat(pcs, bounds, axis=0)
+    gax = np.where((gsz > 1) & (gext[:, 1] > gext[:, 0]), 1, 0)
+    axp = np.repeat(gax, gsz)
+    key2 = np.empty(npres)
+    key2[grp_order] = pcs[np.arange(npres), axp] * 4.0 + pcs[np.arange(npres), 1 - axp] * 1e-6
     porder = np.lexsort((np.arange(npres), key2, best))
     pres_perm = np.empty(npres, dtype=np.int64)
     pres_perm[porder] = np.arange(npres)
@@ -283,12 +322,23 @@ def analyse(disc, leaf=LEAF_NODES, pw=PW):
     elim = np.full(n_total, -1, dtype=np.int64)
     elim[order] = np.arange(nf)
 
-    # free saddle pattern in elimination order (symmetric structure)
+    # free saddle pattern in elimination order (symmetric structure): the stored entries of
+    # [[A_s, 0, Bx^T], [0, A_s, By^T], [Bx, By, 0]] + its transpose (a B entry that is exactly
+    # zero cancels out of that sum and is not in the pattern), between free dofs, as CSR with
+    # sorted rows
     As = pat.tocsr()
-    full = sp.bmat([[As, None, B[:, :ns].T], [None, As, B[:, ns:].T], [B[:, :ns], B[:, ns:], None]], format="csr")
-    full = full + full.T
-    fp = full[order][:, order].tocsr()
-    fp.sort_indices()
+    a_r = np.repeat(np.arange(ns, dtype=np.int64), np.diff(As.indptr))
+    a_c = As.indices.astype(np.int64)
+    b_r = np.repeat(np.arange(npres, dtype=np.int64), np.diff(B.indptr))[B.data != 0.0] + nvel
+    b_c = B.indices.astype(np.int64)[B.data != 0.0]
+    pr_ = np.concatenate([a_r, a_r + ns, b_r, b_c])
+    pc_ = np.concatenate([a_c, a_c + ns, b_c, b_r])
+    pr_, pc_ = elim[pr_], elim[pc_]
+    keep_ = (pr_ >= 0) & (pc_ >= 0)
+    pkey = host_sort(pr_[keep_] * nf + pc_[keep_])
+    fp = sp.csr_matrix((np.ones(pkey.size), (pkey % nf).astype(np.int32),
+                        np.concatenate([[0], np.cumsum(np.bincount(pkey // nf, minlength=nf))])), shape=(nf, nf))
+    del pr_, pc_, keep_, pkey, a_r, a_c, b_r, b_c
 
     # tree nodes -> pivot ranges in elimination order; drop empty tree nodes
     t_of_e = rank[dof_t[order]]                      # postorder rank per eliminated dof
@@ -419,7 +469,7 @@ def analyse(disc, leaf=LEAF_NODES, pw=PW):
     lr = lookup(fr, er)
     lc = lookup(fr, ec)
     dst = f_off[fr] + lr * f_m[fr] + lc
-    o = np.lexsort((dst, f_level[fr]))
+    o = host_argsort(dst)        # == lexsort((dst, level)): dst is unique and grows with the level
     orig_dst = dst[o].astype(np.int64)
     orig_src = src[o].astype(np.int32)
     orig_level_off = np.searchsorted(f_level[fr][o], np.arange(nlevels + 1)).astype(np.int64)
@@ -493,61 +543,69 @@ def build_schedule(plan: FactorPlan, pw=PW):
       OP_GPANEL items (front, a, row0)
     solve launches: (op, level, item_off, n_items, arg)
     """
+    # (vectorised over fronts; the item order is the nested-loop order spelled out per op below)
     items = []
     nitems = [0]
 
-    def add(rows):
-        arr = np.asarray(rows, dtype=np.int32).reshape(len(rows), -1) if len(rows) else np.zeros((0, 4), np.int32)
-        if arr.shape[1] < 4:
-            arr = np.hstack([arr, np.zeros((arr.shape[0], 4 - arr.shape[1]), np.int32)])
+    def add(cols):
+        """Append work items given as equal-length int columns (padded to 4 with zeros)."""
+        n = len(cols[0])
+        arr = np.zeros((n, 4), np.int32)
+        for j, c in enumerate(cols):
+            arr[:, j] = c
         off = nitems[0]
         items.append(arr)
-        nitems[0] += arr.shape[0]
-        return off, arr.shape[0]
+        nitems[0] += n
+        return off, n
+
+    def expand(counts):
+        """(owner, k): owner i repeated counts[i] times, k = 0 .. counts[i] - 1."""
+        counts = np.asarray(counts, dtype=np.int64)
+        own = np.repeat(np.arange(len(counts), dtype=np.int64), counts)
+        return own, np.arange(own.size, dtype=np.int64) - np.repeat(np.cumsum(counts) - counts, counts)
 
     F = plan.nfront
-    fm, fk, lvl, par = plan.f_m, plan.f_k, plan.f_level, plan.f_parent
-    children = [[] for _ in range(F)]
-    for f in range(F):
-        if par[f] >= 0:
-            children[par[f]].append(f)
+    fm, fk, lvl, par = (plan.f_m.astype(np.int64), plan.f_k.astype(np.int64), plan.f_level,
+                        plan.f_parent.astype(np.int64))
+    # children of a front in ascending order; a child's rank among its siblings
+    cs = np.nonzero(par >= 0)[0]
+    cs = cs[np.argsort(par[cs], kind="stable")]
+    nkids = np.bincount(par[cs], minlength=F)
+    sib_rank = np.full(F, -1, dtype=np.int64)
+    sib_rank[cs] = expand(nkids)[1]
+    cbn_all = fm - fk
     fl, sl = [], []
     for L in range(plan.nlevels):
-        fronts = np.arange(plan.level_front_off[L], plan.level_front_off[L + 1])
+        lo, hi = int(plan.level_front_off[L]), int(plan.level_front_off[L + 1])
         fl.append((OP_ZERO, L, 0, 0, 0))
         fl.append((OP_ORIG, L, 0, 0, 0))
-        # extend-add by sibling rank (conflict-free within a launch)
-        maxr = max((len(children[f]) for f in fronts), default=0)
+        # extend-add by sibling rank r (conflict-free within a launch): for fronts f ascending,
+        # child c = children[f][r], rows r0 = 0, EXT_ROWS, .. < |CB(c)|  -> items (c, r0)
+        maxr = int(nkids[lo:hi].max()) if hi > lo else 0
         for r in range(maxr):
-            rows = []
-            for f in fronts:
-                if r < len(children[f]):
-                    c = children[f][r]
-                    cbn = fm[c] - fk[c]
-                    for r0 in range(0, cbn, EXT_ROWS):
-                        rows.append((c, r0))
-            if rows:
-                off, n = add(rows)
+            c = cs[(sib_rank[cs] == r) & (par[cs] >= lo) & (par[cs] < hi)]   # ascending parent
+            i, k = expand(-(-cbn_all[c] // EXT_ROWS))
+            if i.size:
+                off, n = add((c[i], k * EXT_ROWS))
                 fl.append((OP_EXTADD, L, off, n, r))
         # block sweep (Gauss-Jordan) over the front's pivot panels; the update
         # covers every row/column outside the panel (index r' -> r' < a ? r' : r' + pw)
-        npan = int(max((-(-fk[f] // pw) for f in fronts), default=0))
+        fr = np.arange(lo, hi, dtype=np.int64)
+        npan = int((-(-fk[fr] // pw)).max()) if hi > lo else 0
         for p in range(npan):
             a = p * pw
-            act = [f for f in fronts if fk[f] > a]
-            d, h, u, gg = [], [], [], []
-            for f in act:
-                pwf = min(pw, fk[f] - a)
-                t = fm[f] - pwf
-                d.append((f, a))
-                for c0 in range(0, t, TILE):
-                    h.append((f, a, c0))
-                    gg.append((f, a, c0))
-                    for r0 in range(0, t, TILE):
-                        u.append((f, a, r0, c0))
-            for op, rows in ((OP_DIAG, d), (OP_HPANEL, h), (OP_UPDATE, u), (OP_GPANEL, gg)):
-                if rows:
-                    off, n = add(rows)
+            act = fr[fk[fr] > a]
+            t = fm[act] - np.minimum(pw, fk[act] - a)
+            nt = -(-t // TILE)
+            d = (act, np.full(act.size, a))                               # (f, a)
+            i, k = expand(nt)                                             # f, then c0
+            h = (act[i], np.full(i.size, a), k * TILE)                    # (f, a, c0); GPANEL (f, a, row0)
+            i2, k2 = expand(nt * nt)                                      # f, then c0, then r0
+            ntr = nt[i2]
+            u = (act[i2], np.full(i2.size, a), (k2 % ntr) * TILE, (k2 // ntr) * TILE)   # (f, a, r0, c0)
+            for op, cols in ((OP_DIAG, d), (OP_HPANEL, h), (OP_UPDATE, u), (OP_GPANEL, h)):
+                if cols[0].size:
+                    off, n = add(cols)
                     fl.append((op, L, off, n, p))
     # solve schedule: after the sweep a front holds [-F11^-1, F11^-1 F12; F21 F11^-1, S]
     #   forward  fr[k:m] -= F_CP fr[0:k]           (SOP_FGEMM, rows of the CB)
@@ -568,55 +626,54 @@ def build_schedule(plan: FactorPlan, pw=PW):
     # items (slot >= 0) are reduced by the last-arriving CTA of their group.
     # The launch's 5th field is the largest inner range of its items; when a level
     # has split items it equals that level's split length (the kernels use it so).
-    def gemm_items(fronts, rows_of, K_of, pivot_only):
-        g, kmax = [], 1
-        split = _choose_split([int(K_of(f)) for f in fronts], [max(1, int(rows_of(f))) for f in fronts])
+    #   per front f (ascending): K = K_of(f), rws = rows_of(f), ns = max(1, ceil(K / split))
+    #     pivot-only (rws == 0 and pivot_only): t0 = 0, SOLVE_ROWS, .. < K -> (f, -1 - t0, 0, -1)
+    #     else r0 = 0, SOLVE_ROWS, .. < rws: ns == 1 -> (f, r0, 0, -1)
+    #                                         else   -> (f, r0, ks, next free slot) for ks < ns
+    def gemm_items(fronts, rws, K, pivot_only):
+        split = _choose_split([int(x) for x in K], [max(1, int(x)) for x in rws]) if SPLIT_K <= 0 else SPLIT_K
         splits.append(split)
-        for f in fronts:
-            K = int(K_of(f))
-            ns_ = max(1, -(-K // split))
-            rws = int(rows_of(f))
-            if rws == 0 and pivot_only:
-                # pivot rows only, in chunks of SOLVE_ROWS (r0 = -1 - first pivot row)
-                for t0 in range(0, K, SOLVE_ROWS):
-                    g.append((f, -1 - t0, 0, -1))
-                continue
-            for r0 in range(0, rws, SOLVE_ROWS):
-                if ns_ == 1:
-                    g.append((f, r0, 0, -1))
-                else:
-                    s0 = nslot[0]
-                    nslot[0] += ns_
-                    for ks in range(ns_):
-                        g.append((f, r0, ks, s0 + ks))
-            kmax = max(kmax, min(K, split))
-        return g, kmax
+        nsplit = np.maximum(1, -(-K // split))
+        piv = (rws == 0) & pivot_only
+        cnt = np.where(piv, -(-K // SOLVE_ROWS), -(-rws // SOLVE_ROWS) * nsplit)
+        i, k = expand(cnt)
+        pi, ns_i = piv[i], nsplit[i]
+        f_col = fronts[i]
+        r0 = np.where(pi, -1 - k * SOLVE_ROWS, (k // ns_i) * SOLVE_ROWS)
+        is_split = (~pi) & (ns_i > 1)
+        ks = np.where(is_split, k % ns_i, 0)
+        slot = np.where(is_split, nslot[0] + np.cumsum(is_split) - 1, -1)
+        nslot[0] += int(is_split.sum())
+        kk = np.minimum(K[~piv], split)
+        kmax = max(1, int(kk.max())) if kk.size else 1
+        return (f_col, r0, ks, slot), kmax
 
     for L in range(plan.nlevels):
-        fronts = np.arange(plan.level_front_off[L], plan.level_front_off[L + 1])
-        g, kmax = gemm_items(fronts, lambda f: fm[f] - fk[f], lambda f: fk[f], True)
+        fronts = np.arange(plan.level_front_off[L], plan.level_front_off[L + 1], dtype=np.int64)
+        g, kmax = gemm_items(fronts, fm[fronts] - fk[fronts], fk[fronts], True)
         off, n = add(g)
         fwd.append((SOP_FGEMM, L, off, n, kmax))
     for L in reversed(range(plan.nlevels)):
-        fronts = np.arange(plan.level_front_off[L], plan.level_front_off[L + 1])
-        g, kmax = gemm_items(fronts, lambda f: fk[f], lambda f: fm[f], False)
+        fronts = np.arange(plan.level_front_off[L], plan.level_front_off[L + 1], dtype=np.int64)
+        g, kmax = gemm_items(fronts, fk[fronts], fm[fronts], False)
         off, n = add(g)
         bwd.append((SOP_BGEMM, L, off, n, kmax))
-    # gather sources: gsrc[row of front p] = absolute f_idx rows of child CB entries mapped there
+    # gather sources: gsrc[row of front p] = absolute f_idx rows of child CB entries mapped there,
+    # in slot order = (child ascending, CB row ascending)
     nidx = int(plan.f_idx_off[-1])
     gsrc = np.full((nidx, MAX_GSRC), -1, dtype=np.int64)
-    fill = np.zeros(nidx, dtype=np.int64)
-    for c in range(F):
-        p = par[c]
-        if p < 0:
-            continue
-        mp = plan.f_cmap[plan.f_cmap_off[c]:plan.f_cmap_off[c + 1]]
-        dst = plan.f_idx_off[p] + mp
-        srcrow = plan.f_idx_off[c] + fk[c] + np.arange(len(mp))
-        slot = fill[dst]
-        assert np.all(slot < MAX_GSRC), "too many children contribute to one front row"
-        gsrc[dst, slot] = srcrow
-        fill[dst] += 1
+    ch = np.nonzero(par >= 0)[0]
+    ncb = plan.f_cmap_off[ch + 1] - plan.f_cmap_off[ch]
+    ci, crow = expand(ncb)
+    c_of = ch[ci]
+    dst = plan.f_idx_off[par[c_of]] + plan.f_cmap[plan.f_cmap_off[c_of] + crow]
+    srcrow = plan.f_idx_off[c_of] + fk[c_of] + crow
+    o = np.argsort(dst, kind="stable")
+    slot = np.empty(dst.size, dtype=np.int64)
+    _, first, cnt = np.unique(dst[o], return_index=True, return_counts=True)
+    slot[o] = np.arange(dst.size) - np.repeat(first, cnt)
+    assert np.all(slot < MAX_GSRC), "too many children contribute to one front row"
+    gsrc[dst, slot] = srcrow
     assert nidx < 2 ** 31
     work = np.vstack(items) if items else np.zeros((0, 4), np.int32)
     return dict(work=np.ascontiguousarray(work.astype(np.int32)), gsrc=np.ascontiguousarray(gsrc.astype(np.int32)),
