@@ -376,7 +376,9 @@ def main():
 
     # ---- same workload with the LU preconditioner rebuilt every step (reference cadence) ----
     always = None
-    if args.always_steps > 0 and world == 1:
+    from paper_2108_05110_b200.chunked import ChunkedEngine
+    # (a member-chunked engine fills the device: a second engine for this leg does not fit)
+    if args.always_steps > 0 and world == 1 and not isinstance(eng, ChunkedEngine):
         saved = ST.get_solver_options()
         ST.set_solver_options(refactor="always")
         eng2 = ST.get_engine(disc, cfg, j0=j0, J=jl, comm=comm)

@@ -108,7 +108,7 @@ class ChunkedEngine(Engine):
         g = self._staging()
         s = self.stream
         nv, Jc = self.nvel, self.Jc
-        from .problems import RankOneMembers
+        from .problems import RankOneMembers, member_rows
         v, w = (a if isinstance(a, RankOneMembers) else np.asarray(a, dtype=float) for a in (v, w))
         has_p = q is not None and np.asarray(q).size > 0
         cur = self.cur
@@ -118,7 +118,7 @@ class ChunkedEngine(Engine):
             with torch.cuda.stream(s):
                 Xs = g["x_in"]
                 for m, a in enumerate((v, w)):
-                    self._copy_members(g["d_vel"][m], a[sl])
+                    self._copy_members(g["d_vel"][m], member_rows(a, c * Jc, Jc))   # lazy stays lazy
                     torch.index_select(g["d_vel"][m].t(), 0, g["ref_of_int_v"], out=Xs[m, :nv])
                 if has_p:
                     for m, a in enumerate((q, r)):
