@@ -500,10 +500,10 @@ def main():
             # against the nearer of its two roofs (HBM for small J, fp64 tensor cores for large J)
             "roofline": (
                 {"bound": "hbm", "kernel": "ens_precond_apply (multifrontal forward+backward sweep, "
-                                           "both systems; k_sgemm dominant)",
+                                           "both systems; streamed k_stream_gemm dominant)",
                  "achieved": solve_gbs, "peak": hbm, "peak_kind": peak_kind, "unit": "GB/s",
                  "frac": solve_gbs / hbm,
-                 "traffic": spmm_traffic("r02_solve_traffic.json") if case == CASE else None,
+                 "traffic": spmm_traffic("r02_apply_traffic.json") if case == CASE else None,
                  "bytes_per_launch": solve_bytes, "ms_per_launch": solve_ms,
                  "other_roof": {"bound": "tensor (fp64 DMMA)", "achieved": solve_tflops, "peak": f64_peak,
                                 "peak_kind": f64_kind, "unit": "TFLOP/s", "frac": solve_tflops / f64_peak}}
