@@ -126,8 +126,8 @@ void ens_destroy(ens_ctx* c) {
     cudaFree(c->scta);
     cudaFree(c->sfr);
     cudaFree(c->sbg_rows);
-    cudaFree(c->ssc_off);
-    cudaFree(c->ssc_row);
+    cudaFree(c->ssc_ent);
+    cudaFree(c->spart);
     cudaFree(c->finit_rows);
     cudaFree(c->ec);
     cudaFree(c->nrm_part);

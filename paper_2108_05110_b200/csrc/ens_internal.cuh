@@ -75,15 +75,16 @@ struct ens_ctx {
     void* stiles = nullptr;        // STile[n]
     int64_t n_stiles = 0;
     int32_t* scta = nullptr;       // per launch: CTA unit offsets
-    std::vector<int64_t> slaunch;  // per launch: (dir, level, cta_off index, ngrid)
+    std::vector<int64_t> slaunch;  // per launch: (dir, level, first tile, cta_off index, grid, pieces per unit, units)
     double* sfr = nullptr;         // blocked front vectors [2][ncb][n_idx][ldb]
     int32_t* sbg_rows = nullptr;   // per level: pivot rows the forward assembly fills
     std::vector<int64_t> sbg_off;  // level offsets into sbg_rows
-    int32_t* ssc_off = nullptr;    // per front-row position: backward scatter targets (CSR offsets)
-    int32_t* ssc_row = nullptr;    // descendants' contribution rows holding the same dof
+    void* ssc_ent = nullptr;       // backward scatter pairs (int2: descendant's contribution row, source row in its tile)
+    double* spart = nullptr;       // fragment sums of the split launches' pieces
     int scw = 0, sncb = 0, sldb = 0, snst = 0, skc = 0;
     size_t sstage = 0;
     size_t sdesc = 0;              // shared-memory bytes for a CTA's tile descriptors
+    size_t srt = 0;                // ... for the backward epilogue's result tiles
     double* nrm_part = nullptr;    // fused residual-norm partials of the SpMM
     double* diag_part = nullptr;   // per-block partials of the diagnostics (launch_diagnostics)
     size_t diag_part_n = 0;

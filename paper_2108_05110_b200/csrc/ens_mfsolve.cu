@@ -508,8 +508,9 @@ struct STile {
     int m;            // front size
     int row0;         // first front row of the tile
     int kb, ke;       // inner range of the unit ([0, K))
+    int sc_lo, sc_n;  // backward: the tile's (destination row, source row) scatter pairs in sc_ent
 };
-static_assert(sizeof(STile) == 56, "STile layout");
+static_assert(sizeof(STile) == 64, "STile layout");
 
 constexpr int ST_ROWS = 32;     // rows per tile
 constexpr int ST_MAXST = 12;    // pipeline stages (upper bound)
@@ -549,11 +550,10 @@ __device__ __forceinline__ double st_lds(uint32_t a) {
     return v;
 }
 __device__ __forceinline__ int64_t st_i64(int lo, int hi) { return (int64_t)(unsigned)lo | ((int64_t)hi << 32); }
-
 }  // namespace
 
 #ifdef ST_PROBE   // diagnostic build: per-CTA timeline of consumer warp 0 (wait vs. work), launch 0 only
-__device__ unsigned long long g_stp[2048][6];
+__device__ unsigned long long g_stp[2048][10];
 __device__ __forceinline__ unsigned long long st_gt() {
     unsigned long long t;
     asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
@@ -574,6 +574,8 @@ extern "C" int ens_stream_probe_reset() {
         h[i][0] = ~0ull;
         h[i][1] = 0;
     }
+    static unsigned long long z[2048][10];
+    cudaMemcpyToSymbol(g_stp, z, sizeof(z));
     return (int)cudaMemcpyToSymbol(g_lvl, h, sizeof(h));
 }
 extern "C" int ens_stream_probe_levels(const char* path) {
@@ -587,21 +589,28 @@ extern "C" int ens_stream_probe_levels(const char* path) {
     return 0;
 }
 extern "C" int ens_stream_probe_dump(const char* path) {
-    static unsigned long long h[2048][6];
+    static unsigned long long h[2048][10];
     cudaDeviceSynchronize();
     cudaMemcpyFromSymbol(h, g_stp, sizeof(h));
     FILE* f = fopen(path, "w");
     if (!f) return -1;
     for (int i = 0; i < 2048; ++i)
-        fprintf(f, "%d %llu %llu %llu %llu %llu %llu\n", i, h[i][0], h[i][1], h[i][2], h[i][3], h[i][4], h[i][5]);
+        fprintf(f, "%d %llu %llu %llu %llu %llu %llu %llu %llu %llu %llu\n", i, h[i][0], h[i][1], h[i][2], h[i][3],
+                h[i][4], h[i][5], h[i][6], h[i][7], h[i][8], h[i][9]);
     fclose(f);
     return 0;
 }
 #define ST_SPAN_BEGIN(id) st_span_begin(id)
 #define ST_SPAN_END(id) st_span_end(id)
+// per-CTA timeline of consumer warp 0 (launch g_probe_target): slot k of row blockIdx.x
+#define ST_MARK(id, k)                                                                            \
+    do {                                                                                          \
+        if (threadIdx.x == 0 && (id) == g_probe_target && blockIdx.x < 2048) g_stp[blockIdx.x][k] = st_gt(); \
+    } while (0)
 #else
 #define ST_SPAN_BEGIN(id)
 #define ST_SPAN_END(id)
+#define ST_MARK(id, k)
 #endif
 
 // ENS_BOUNDS_CHECK builds (tools/sanitize_run.py; compute-sanitizer is not available on the GPU
@@ -637,102 +646,241 @@ __global__ void __launch_bounds__(256) k_stream_pack(const STile* __restrict__ t
 }
 
 // Producer of a unit range: streams every chunk of units [ub, ue) through the stage ring.
+// The factor stream is static during an apply, so the A copies of the first ring-full of chunks are
+// issued BEFORE the dependency wait (early pass: returns how many); the pass after the wait adds
+// those chunks' B copies (front rows written by the previous launch) and then streams normally.
 template <int KC>
-__device__ __forceinline__ void st_produce(const STile* sT, int tb, int ub, int ue, int per_tile, int ncb, int ldb,
-                                           const double* __restrict__ S, int64_t slen,
-                                           const double* __restrict__ FRS, int64_t nidx, int nst, uint32_t stage_bytes,
-                                           uint32_t sbase, uint32_t bbase, int& s, uint32_t& ph) {
+__device__ __forceinline__ int st_produce(const STile* sT, int tb, int ub, int ue, int per_tile, int ncb, int ldb,
+                                          const double* __restrict__ S, int64_t slen,
+                                          const double* __restrict__ FRS, int64_t nidx, int nst, uint32_t stage_bytes,
+                                          uint32_t sbase, uint32_t bbase, bool early, int pre) {
     constexpr uint32_t A_BYTES = KC * ST_ROWS * 8;
+    int s = 0, n = 0;
+    uint32_t ph = 0;
     for (int u = ub; u < ue; ++u) {
         const STile& T = sT[u / per_tile - tb];
         const int mat = (u % per_tile) / ncb, cb = u % ncb;
         const double* Ab = S + (int64_t)mat * slen + st_i64(T.a_lo, T.a_hi);
         const double* Bb = FRS + ((int64_t)(mat * ncb + cb) * nidx + T.fo) * ldb;
         const int nch = (T.ke - T.kb + KC - 1) / KC;
-        for (int c = 0; c < nch; ++c) {
+        for (int c = 0; c < nch; ++c, ++n) {
+            if (early && n == nst) return n;
             const int k0 = T.kb + c * KC, kr = min(KC, T.ke - k0);
             const uint32_t a_bytes = (uint32_t)((kr + 3) >> 2) * T.ng * 256u;
             const uint32_t b_bytes = (uint32_t)kr * ldb * 8u;
             ST_ASSERT(st_i64(T.a_lo, T.a_hi) + (int64_t)k0 * T.ng * 8 + a_bytes / 8 <= slen);
             ST_ASSERT(T.fo + k0 + kr <= nidx && a_bytes <= A_BYTES);
-            st_mbar_wait(bbase + 8 * (ST_MAXST + s), ph ^ 1);
             const uint32_t full = bbase + 8 * s;
             const uint32_t st = sbase + (uint32_t)s * stage_bytes;
-            st_mbar_expect_tx(full, a_bytes + b_bytes);
-            st_bulk_g2s(st, Ab + (int64_t)k0 * T.ng * 8, a_bytes, full);
-            st_bulk_g2s(st + A_BYTES, Bb + (int64_t)k0 * ldb, b_bytes, full);
+            if (early) {   // fresh ring: every stage is free
+                st_mbar_expect_tx(full, a_bytes + b_bytes);
+                st_bulk_g2s(st, Ab + (int64_t)k0 * T.ng * 8, a_bytes, full);
+            } else if (n < pre) {
+                st_bulk_g2s(st + A_BYTES, Bb + (int64_t)k0 * ldb, b_bytes, full);
+            } else {
+                st_mbar_wait(bbase + 8 * (ST_MAXST + s), ph ^ 1);
+                st_mbar_expect_tx(full, a_bytes + b_bytes);
+                st_bulk_g2s(st, Ab + (int64_t)k0 * T.ng * 8, a_bytes, full);
+                st_bulk_g2s(st + A_BYTES, Bb + (int64_t)k0 * ldb, b_bytes, full);
+            }
             s = s + 1 == nst ? 0 : s + 1;
             if (s == 0) ph ^= 1;
         }
     }
+    return n;
 }
 
-// Consumers (warps 0..3, row group = warp) of a unit range: DMMA mainloop and epilogue.
-template <int NCT, int KC>
+// Per-row epilogue metadata of a unit (static plan data): backward, the dof the row solves for;
+// forward, the <= 4 children's contribution rows mapped onto the row (else -1).
+__device__ __forceinline__ int4 st_row_meta(const STile& X, int grp, int g, const int32_t* __restrict__ fidx,
+                                            const int32_t* __restrict__ gsrc) {
+    int4 r = make_int4(-1, -1, -1, -1);
+    const int row = 8 * grp + g;
+    const bool bw = X.flags & 1;
+    const int nrr = min(ST_ROWS, (bw ? X.kp : X.m - X.kp) - X.r0);
+    if (grp >= X.ng || row >= nrr) return r;
+    const int64_t prow = X.fo + X.r0 + row + (bw ? 0 : X.kp);
+    if (bw)
+        r.x = __ldg(fidx + prow);
+    else if (X.flags & 2)
+        r = __ldg(reinterpret_cast<const int4*>(gsrc + 4 * prow));
+    return r;
+}
+
+// Forward: the sum of the children's contribution rows mapped onto this thread's row (its fragment
+// columns), from the row metadata.
+template <int NCT>
+__device__ __forceinline__ void st_child_rows(const int4 meta, const double* __restrict__ FRm, int ldb, int q,
+                                              double (&init)[NCT][2]) {
+    const int src[4] = {meta.x, meta.y, meta.z, meta.w};
+#pragma unroll
+    for (int v = 0; v < 4; ++v) {
+        if (src[v] < 0) break;
+        const double* pr = FRm + (int64_t)src[v] * ldb;
+#pragma unroll
+        for (int ct = 0; ct < NCT; ++ct)
+#pragma unroll
+            for (int e = 0; e < 2; ++e) init[ct][e] += pr[min(8 * ct + 2 * q + e, ldb - 1)];
+    }
+}
+
+// Epilogue of one unit, run by the four consumer warps (warp `grp` holds row group grp's sums in the
+// DMMA fragment layout: lane (g, q) has row 8 grp + g, columns 8 ct + 2 q + {0, 1}).
+//   forward : contribution rows  fr[C] = (children's rows) - sum        -> blocked front vectors
+//   backward: solution rows      x[P]  = -sum                           -> the iterate, and into the
+//             contribution rows of every descendant front that reads them (up to ~40 per row at the
+//             root).  A tile's rows are consecutive pivots, so its (destination row, source row) pairs
+//             are one contiguous range of sc_ent: the result tile is staged in shared memory (rt, two
+//             buffers alternating per unit) and the warps walk the range together, jn/2 lanes per pair
+//             with one 16-byte store each and the pair loads batched (independent).
+constexpr int ST_SCU = 8;   // scatter pairs in flight per lane
+__device__ __forceinline__ void st_scatter_load(int2 (&pr)[ST_SCU], const int2* __restrict__ sc_ent, int e, int e1,
+                                                int stride) {
+#pragma unroll
+    for (int v = 0; v < ST_SCU; ++v) {
+        const int ee = e + stride * v;
+        pr[v] = ee < e1 ? __ldg(sc_ent + ee) : make_int2(-1, 0);
+    }
+}
+
+template <int NCT>
+__device__ __forceinline__ void st_epilogue(const STile& T, int& nsc, int grp, int lane, double (&sum)[NCT][2],
+                                            const double (&init)[NCT][2], double* out_row, bool row_ok, int jn,
+                                            double* __restrict__ FRm, int ldb, const int2* __restrict__ sc_ent,
+                                            double* rtbuf, int64_t nidx, int sy = 0, int sn = 1,
+                                            const int2* pre = nullptr) {
+    const int g = lane >> 2, q = lane & 3;
+    const bool bwd = T.flags & 1;
+#pragma unroll
+    for (int ct = 0; ct < NCT; ++ct)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+            const int col = 8 * ct + 2 * q + e;
+            sum[ct][e] = bwd ? -sum[ct][e] : init[ct][e] - sum[ct][e];
+            if (row_ok && col < jn) out_row[col] = sum[ct][e];
+        }
+    if (!bwd || T.sc_n == 0) return;   // (uniform over the CTA's consumer warps)
+    // (the buffer alternates per scattering unit: a warp two units ahead of the slowest cannot exist,
+    // because the barrier below sits between them)
+    double* rt = rtbuf + (nsc & 1) * (ST_ROWS * NCT * 8);
+    ++nsc;
+    if (grp < T.ng) {
+        const int row = 8 * grp + g;
+#pragma unroll
+        for (int ct = 0; ct < NCT; ++ct)
+            *reinterpret_cast<double2*>(rt + row * (NCT * 8) + 8 * ct + 2 * q) = make_double2(sum[ct][0], sum[ct][1]);
+    }
+    asm volatile("bar.sync 1, 128;" ::: "memory");
+    const int lpp = jn >> 1, ppw = 32 / lpp;           // lanes per pair, pairs per warp and step
+    const int sub = lane / lpp, cp = lane - sub * lpp;
+    const int warp = (threadIdx.x >> 5) & 3;
+    const int e1 = T.sc_lo + T.sc_n;
+    if (sub >= ppw) return;
+    // (sy, sn): this CTA's share when several CTAs scatter one tile (k_stream_reduce)
+    const int stride = 4 * sn * ppw;
+    for (int e = T.sc_lo + (sy * 4 + warp) * ppw + sub; e < e1; e += ST_SCU * stride) {
+        int2 pr[ST_SCU];
+        if (pre && e == T.sc_lo + (sy * 4 + warp) * ppw + sub) {
+#pragma unroll
+            for (int v = 0; v < ST_SCU; ++v) pr[v] = pre[v];
+        } else {
+            st_scatter_load(pr, sc_ent, e, e1, stride);
+        }
+#pragma unroll
+        for (int v = 0; v < ST_SCU; ++v)
+            if (pr[v].x >= 0) {
+                ST_ASSERT(pr[v].x < nidx && pr[v].y >= 0 && pr[v].y < ST_ROWS);
+                *reinterpret_cast<double2*>(FRm + (int64_t)pr[v].x * ldb + 2 * cp) =
+                    *reinterpret_cast<const double2*>(rt + pr[v].y * (NCT * 8) + 2 * cp);
+            }
+    }
+}
+
+// Consumers (warps 0..3) of a unit range: DMMA mainloop, then the epilogue -- or, SPLIT, the unit is
+// one of `ks` pieces of a tile's inner range (one piece per CTA) and the fragment sums go to the
+// partial buffer for k_stream_reduce.
+template <int NCT, int KC, bool SPLIT>
 __device__ __forceinline__ void st_consume(const STile* sT, int tb, int ub, int ue, int per_tile, int ncb, int cw,
                                            int ldb, double* __restrict__ FRS, const SolveIO* __restrict__ io,
                                            const int32_t* __restrict__ fidx, const int32_t* __restrict__ gsrc,
-                                           const int32_t* __restrict__ sc_off, const int32_t* __restrict__ sc_row,
-                                           int64_t N, int J, int64_t nidx, int nst, uint32_t stage_bytes,
-                                           const unsigned char* smem, uint32_t bbase, int& s, uint32_t& ph) {
+                                           const int2* __restrict__ sc_ent, int64_t N, int J, int64_t nidx,
+                                           int nst, uint32_t stage_bytes, const unsigned char* smem, double* rtbuf,
+                                           uint32_t bbase, double* __restrict__ part, int probe_id) {
     constexpr uint32_t A_BYTES = KC * ST_ROWS * 8;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int g = lane >> 2, q = lane & 3;
+    int s = 0;
+    uint32_t ph = 0;
+    // Row groups go to the consumer warps round-robin across the CTA's units (rot = groups handed out
+    // so far): tiles with fewer than 4 groups (the 7-row tail tiles of the leaf fronts) would otherwise
+    // all land on warp 0, i.e. on one SM sub-partition's tensor pipe.
+    // The per-row metadata is fetched one unit ahead (mnext), so the loads that depend on it (the
+    // children's rows of the forward epilogue) are issued at the top of the unit, under the mainloop.
+    int rot = 0, nsc = 0;
+    int4 mnext = make_int4(-1, -1, -1, -1);
+    if (!SPLIT && ub < ue) mnext = st_row_meta(sT[ub / per_tile - tb], warp, g, fidx, gsrc);
+    ST_MARK(probe_id, 1);
+    pdl_wait();   // front rows / the iterate come from the previous launch
+    ST_MARK(probe_id, 2);
     for (int u = ub; u < ue; ++u) {
         const STile T = sT[u / per_tile - tb];
         const int mat = (u % per_tile) / ncb, cb = u % ncb;
         const int j0 = cb * cw, jn = min(cw, J - j0);
         const bool bwd = T.flags & 1;
-        const int rows_total = bwd ? T.kp : T.m - T.kp;
-        const int nr = min(ST_ROWS, rows_total - T.r0);
-        const int row = 8 * warp + g;
-        const bool active = warp < T.ng;
+        const int nr = min(ST_ROWS, (bwd ? T.kp : T.m - T.kp) - T.r0);
+#ifdef ST_NO_ROT
+        const int grp = warp;
+#else
+        const int grp = (warp - rot) & 3;
+#endif
+        const int row = 8 * grp + g;
+        const bool active = grp < T.ng;
         const bool row_ok = active && row < nr;
-        // epilogue operands in flight during the mainloop
         double* FRm = FRS + (int64_t)(mat * ncb + cb) * nidx * ldb;
         double* out_row = nullptr;
-        int sc0 = 0, sc1 = 0;   // backward: descendants' contribution rows this row's solution fills
         double init[NCT][2];
 #pragma unroll
         for (int ct = 0; ct < NCT; ++ct) init[ct][0] = init[ct][1] = 0.0;
-        if (row_ok) {
-            const int64_t prow = T.fo + T.r0 + row + (bwd ? 0 : T.kp);
-            ST_ASSERT(prow < nidx);
-            if (bwd) {
-                ST_ASSERT(__ldg(fidx + prow) >= 0 && __ldg(fidx + prow) < N);
-                out_row = io->z + (int64_t)mat * N * J + (int64_t)__ldg(fidx + prow) * J + j0;
-                sc0 = __ldg(sc_off + prow);
-                sc1 = __ldg(sc_off + prow + 1);
-            } else {
-                out_row = FRm + prow * ldb;
-                if (T.flags & 2) {   // children's contribution rows mapped onto this row (<= 4)
-                    const int4 gs = *reinterpret_cast<const int4*>(gsrc + 4 * prow);
-                    const int src[4] = {gs.x, gs.y, gs.z, gs.w};
-#pragma unroll
-                    for (int v = 0; v < 4; ++v) {
-                        if (src[v] < 0) break;
-                        const double* pr = FRm + (int64_t)src[v] * ldb;
-#pragma unroll
-                        for (int ct = 0; ct < NCT; ++ct)
-#pragma unroll
-                            for (int e = 0; e < 2; ++e) init[ct][e] += pr[min(8 * ct + 2 * q + e, ldb - 1)];
-                    }
+        if (!SPLIT) {
+#ifdef ST_NO_METAPF
+            const int4 meta = st_row_meta(T, grp, g, fidx, gsrc);
+#else
+            const int4 meta = mnext;
+#endif
+            rot = (rot + T.ng) & 3;
+#ifndef ST_NO_METAPF
+            if (u + 1 < ue) {
+#ifdef ST_NO_ROT
+                mnext = st_row_meta(sT[(u + 1) / per_tile - tb], warp, g, fidx, gsrc);
+#else
+                mnext = st_row_meta(sT[(u + 1) / per_tile - tb], (warp - rot) & 3, g, fidx, gsrc);
+#endif
+            }
+#endif
+            if (row_ok) {
+                if (bwd) {
+                    ST_ASSERT(meta.x >= 0 && meta.x < N);
+                    out_row = io->z + (int64_t)mat * N * J + (int64_t)meta.x * J + j0;
+                } else {
+                    out_row = FRm + (int64_t)(T.fo + T.r0 + row + T.kp) * ldb;
+                    if (T.flags & 2) st_child_rows<NCT>(meta, FRm, ldb, q, init);
                 }
             }
         }
-        // two accumulator sets (even / odd k-steps, summed at the end): twice the independent
-        // DMMA chains per warp -- the leaf levels are bound by the tensor-core dependency latency
+        // two accumulator sets (even / odd k-steps, summed at the end): a warp alone reaches the fp64
+        // tensor pipe's issue rate with two independent chains (tools/dmma_latency.cu)
         double acc[NCT][2], acc2[NCT][2];
 #pragma unroll
         for (int ct = 0; ct < NCT; ++ct) acc[ct][0] = acc[ct][1] = acc2[ct][0] = acc2[ct][1] = 0.0;
         const int nch = (T.ke - T.kb + KC - 1) / KC;
         for (int c = 0; c < nch; ++c) {
             st_mbar_wait(bbase + 8 * s, ph);
+            if (u == ub && c == 0) ST_MARK(probe_id, 3);
             if (active) {
                 const int kr = min(KC, T.ke - T.kb - c * KC);
                 const int ksteps = (kr + 3) >> 2;
                 const double* stg = reinterpret_cast<const double*>(smem + (size_t)s * stage_bytes);
-                const double* ap = stg + warp * 32 + lane;
+                const double* ap = stg + grp * 32 + lane;
                 const double* bp = stg + A_BYTES / 8 + q * ldb + g;
                 const int astep = T.ng * 32, bstep = 4 * ldb;
                 if (ksteps == KC / 4) {
@@ -767,32 +915,26 @@ __device__ __forceinline__ void st_consume(const STile* sT, int tb, int ub, int 
             s = s + 1 == nst ? 0 : s + 1;
             if (s == 0) ph ^= 1;
         }
-        if (!row_ok) continue;
-        double res[NCT][2];
+        if (u + 1 == ue) ST_MARK(probe_id, 4);
 #pragma unroll
         for (int ct = 0; ct < NCT; ++ct)
 #pragma unroll
-            for (int e = 0; e < 2; ++e) {
-                const int col = 8 * ct + 2 * q + e;
-                const double v = acc[ct][e] + acc2[ct][e];
-                res[ct][e] = bwd ? -v : init[ct][e] - v;
-                if (col < jn) out_row[col] = res[ct][e];
+            for (int e = 0; e < 2; ++e) acc[ct][e] += acc2[ct][e];
+        if constexpr (SPLIT) {   // CTA index = unit * ks + piece
+            if (active) {
+                double* pp = part + ((int64_t)blockIdx.x * 4 + grp) * (2 * NCT * 32) + lane;
+#pragma unroll
+                for (int ct = 0; ct < NCT; ++ct)
+#pragma unroll
+                    for (int e = 0; e < 2; ++e) pp[(2 * ct + e) * 32] = acc[ct][e];
             }
-        for (int t = sc0; t < sc1; ++t) {   // backward: the solution row into every descendant that reads it
-            ST_ASSERT(__ldg(sc_row + t) >= 0 && __ldg(sc_row + t) < nidx);
-            double* dr = FRm + (int64_t)__ldg(sc_row + t) * ldb;
-#pragma unroll
-            for (int ct = 0; ct < NCT; ++ct)
-#pragma unroll
-                for (int e = 0; e < 2; ++e) {
-                    const int col = 8 * ct + 2 * q + e;
-                    if (col < jn) dr[col] = res[ct][e];
-                }
+        } else {
+            st_epilogue<NCT>(T, nsc, grp, lane, acc, init, out_row, row_ok, jn, FRm, ldb, sc_ent, rtbuf, nidx);
         }
     }
 }
 
-// stage ring set-up shared by both streamed kernels
+// stage ring set-up
 __device__ __forceinline__ void st_ring_init(unsigned char* smem, uint32_t bbase, int nst, uint32_t stage_bytes) {
     if (threadIdx.x == 0) {
         for (int s = 0; s < nst; ++s) {
@@ -807,43 +949,133 @@ __device__ __forceinline__ void st_ring_init(unsigned char* smem, uint32_t bbase
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
 
-// One level and direction of the streamed solve; units [cta_off[b], cta_off[b+1]) per CTA,
-// unit u = (tile * 2 + system) * ncb + column block.
-template <int NCT, int KC>
+// One level and direction of the streamed solve.  Units u = (tile * 2 + system) * ncb + column
+// block; CTA b runs units [cta_off[b], cta_off[b+1]).  SPLIT (upper tree levels: few tiles with long
+// inner ranges -- one SM pulls only ~40 GB/s from HBM, so a level has to be spread over all of
+// them): ks CTAs per unit, CTA b streams piece b % ks of unit b / ks and leaves its fragment sums
+// in `part`; k_stream_reduce adds the pieces in order and runs the epilogue.
+template <int NCT, int KC, bool SPLIT>
 __global__ void __launch_bounds__(ST_THREADS, ST_CTAS)
     k_stream_gemm(const STile* __restrict__ tiles, int tile0, const int32_t* __restrict__ cta_off, int ncb, int cw,
                   int ldb, const double* __restrict__ S, int64_t slen, double* __restrict__ FRS,
                   const SolveIO* __restrict__ io, const int32_t* __restrict__ fidx,
-                  const int32_t* __restrict__ gsrc, const int32_t* __restrict__ sc_off,
-                  const int32_t* __restrict__ sc_row, int64_t N, int J, int64_t nidx, int nst,
-                  uint32_t stage_bytes, int probe_id) {
+                  const int32_t* __restrict__ gsrc, const int2* __restrict__ sc_ent, int64_t N, int J,
+                  int64_t nidx, int nst, uint32_t stage_bytes, uint32_t desc_bytes, double* __restrict__ part,
+                  int ks, int probe_id) {
     extern __shared__ __align__(128) unsigned char smem[];
     __shared__ __align__(8) uint64_t bars[2 * ST_MAXST];   // full[0..nst), empty[ST_MAXST..)
     ST_SPAN_BEGIN(probe_id);
+    ST_MARK(probe_id, 0);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t sbase = st_smem_u32(smem);
     const uint32_t bbase = st_smem_u32(bars);
     st_ring_init(smem, bbase, nst, stage_bytes);
     // this CTA's tile descriptors into shared memory (static data: before the dependency wait), so
     // neither the producer nor the consumers pay a global-load latency per unit
-    const int ub = cta_off[blockIdx.x], ue = cta_off[blockIdx.x + 1];
+    const int piece = SPLIT ? (int)(blockIdx.x % (unsigned)ks) : 0;
+    const int ub = SPLIT ? (int)(blockIdx.x / (unsigned)ks) : cta_off[blockIdx.x];
+    const int ue = SPLIT ? ub + 1 : cta_off[blockIdx.x + 1];
     const int per_tile = 2 * ncb;
     STile* sT = reinterpret_cast<STile*>(smem + (size_t)nst * stage_bytes);
     const int tb = ub / per_tile, te = ue > ub ? (ue - 1) / per_tile + 1 : tb;
-    for (int i = threadIdx.x; i < (te - tb) * (int)(sizeof(STile) / 4); i += blockDim.x)
-        reinterpret_cast<int*>(sT)[i] = __ldg(reinterpret_cast<const int*>(tiles + tile0 + tb) + i);
+    for (int i = threadIdx.x; i < (te - tb) * (int)(sizeof(STile) / 4); i += blockDim.x) {
+        int v = __ldg(reinterpret_cast<const int*>(tiles + tile0 + tb) + i);
+        if (SPLIT && (i == 12 || i == 13)) {   // kb / ke: this piece's share of the tile's chunks
+            const int K = __ldg(&tiles[tile0 + tb].K);
+            const int nch = (K + KC - 1) / KC;
+            v = min(K, (int)((unsigned)(piece + (i - 12)) * (unsigned)nch / (unsigned)ks) * KC);
+        }
+        reinterpret_cast<int*>(sT)[i] = v;
+    }
     __syncthreads();
     pdl_trigger();
-    pdl_wait();   // front rows / the iterate come from the previous launch
-    int s = 0;
-    uint32_t ph = 0;
     if (warp == 4) {
-        if (lane == 0) st_produce<KC>(sT, tb, ub, ue, per_tile, ncb, ldb, S, slen, FRS, nidx, nst, stage_bytes, sbase,
-                                      bbase, s, ph);
+        int pre = 0;
+#ifndef ST_NO_EARLYA
+        if (lane == 0)
+            pre = st_produce<KC>(sT, tb, ub, ue, per_tile, ncb, ldb, S, slen, FRS, nidx, nst, stage_bytes, sbase,
+                                 bbase, true, 0);
+#endif
+        pdl_wait();   // front rows / the iterate come from the previous launch (consumers: in st_consume)
+        if (lane == 0)
+            st_produce<KC>(sT, tb, ub, ue, per_tile, ncb, ldb, S, slen, FRS, nidx, nst, stage_bytes, sbase, bbase,
+                           false, pre);
         return;
     }
-    st_consume<NCT, KC>(sT, tb, ub, ue, per_tile, ncb, cw, ldb, FRS, io, fidx, gsrc, sc_off, sc_row, N, J, nidx, nst,
-                        stage_bytes, smem, bbase, s, ph);
+    double* rtbuf = reinterpret_cast<double*>(smem + (size_t)nst * stage_bytes + desc_bytes);
+    st_consume<NCT, KC, SPLIT>(sT, tb, ub, ue, per_tile, ncb, cw, ldb, FRS, io, fidx, gsrc, sc_ent, N, J, nidx, nst,
+                               stage_bytes, smem, rtbuf, bbase, part, probe_id);
+    ST_MARK(probe_id, 5);
+#ifdef ST_PROBE
+    if (lane == 0) ST_SPAN_END(probe_id);
+#endif
+}
+
+// Second half of a SPLIT level: four warps per unit add the unit's ks pieces in order (fixed
+// summation order: deterministic) and run the epilogue; gridDim.y CTAs share a unit's scatter
+// pairs (each sums the pieces itself, CTA y = 0 writes the rows' own output).
+template <int NCT>
+__global__ void __launch_bounds__(128) k_stream_reduce(const STile* __restrict__ tiles, int tile0, int ncb, int cw,
+                                                       int ldb, double* __restrict__ FRS,
+                                                       const SolveIO* __restrict__ io,
+                                                       const int32_t* __restrict__ fidx,
+                                                       const int32_t* __restrict__ gsrc,
+                                                       const int2* __restrict__ sc_ent, int64_t N, int J,
+                                                       int64_t nidx, const double* __restrict__ part, int ks,
+                                                       int probe_id) {
+    __shared__ __align__(16) double rt[ST_ROWS * NCT * 8];
+    ST_SPAN_BEGIN(probe_id);
+    const int u = blockIdx.x, per_tile = 2 * ncb;
+    const int grp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, q = lane & 3;
+    const STile T = tiles[tile0 + u / per_tile];
+    const int mat = (u % per_tile) / ncb, cb = u % ncb;
+    const int j0 = cb * cw, jn = min(cw, J - j0);
+    const bool bwd = T.flags & 1;
+    const int nr = min(ST_ROWS, (bwd ? T.kp : T.m - T.kp) - T.r0);
+    const int row = 8 * grp + g;
+    const bool active = grp < T.ng, row_ok = active && row < nr && blockIdx.y == 0;
+    // CTAs y > 0 only share the scatter: nothing to do if the pairs do not reach their first step
+    const int lpp = jn >> 1, ppw = 32 / lpp, sub = lane / lpp;
+    const int e_first = T.sc_lo + ((int)blockIdx.y * 4 + grp) * ppw + sub, e1 = T.sc_lo + T.sc_n;
+    if (blockIdx.y > 0 && (!bwd || T.sc_lo + (int)blockIdx.y * 4 * ppw >= e1)) return;
+    const int4 meta = st_row_meta(T, grp, g, fidx, gsrc);
+    double* FRm = FRS + (int64_t)(mat * ncb + cb) * nidx * ldb;
+    int2 pre[ST_SCU];
+    if (bwd && sub < ppw) st_scatter_load(pre, sc_ent, e_first, e1, 4 * (int)gridDim.y * ppw);   // (static data)
+    pdl_trigger();
+    pdl_wait();   // the pieces come from the previous launch
+    double sum[NCT][2], init[NCT][2];
+#pragma unroll
+    for (int ct = 0; ct < NCT; ++ct) sum[ct][0] = sum[ct][1] = init[ct][0] = init[ct][1] = 0.0;
+    double* out_row = nullptr;
+    if (row_ok) {
+        if (bwd) {
+            out_row = io->z + (int64_t)mat * N * J + (int64_t)meta.x * J + j0;
+        } else {
+            out_row = FRm + (int64_t)(T.fo + T.r0 + row + T.kp) * ldb;
+            if (T.flags & 2) st_child_rows<NCT>(meta, FRm, ldb, q, init);
+        }
+    }
+    if (active) {
+        const double* pp = part + ((int64_t)u * ks * 4 + grp) * (2 * NCT * 32) + lane;
+        double v[8][NCT][2];
+#pragma unroll
+        for (int p = 0; p < 8; ++p)
+#pragma unroll
+            for (int ct = 0; ct < NCT; ++ct)
+#pragma unroll
+                for (int e = 0; e < 2; ++e)
+                    v[p][ct][e] = p < ks ? pp[(int64_t)p * 4 * (2 * NCT * 32) + (2 * ct + e) * 32] : 0.0;
+#pragma unroll
+        for (int p = 0; p < 8; ++p)
+#pragma unroll
+            for (int ct = 0; ct < NCT; ++ct)
+#pragma unroll
+                for (int e = 0; e < 2; ++e) sum[ct][e] += v[p][ct][e];
+    }
+    int nsc = 0;
+    st_epilogue<NCT>(T, nsc, grp, lane, sum, init, out_row, row_ok, jn, FRm, ldb, sc_ent, rt, nidx, (int)blockIdx.y,
+                     (int)gridDim.y, bwd ? pre : nullptr);
 #ifdef ST_PROBE
     if (lane == 0) ST_SPAN_END(probe_id);
 #endif
@@ -859,21 +1091,31 @@ __global__ void __launch_bounds__(256) k_sfinit(const int32_t* __restrict__ rows
                                                 int J, int64_t nidx, int ncb, int cw, int ldb, int probe_id) {
     const int mat = blockIdx.y;
     ST_SPAN_BEGIN(probe_id);
-    pdl_wait();   // children's contribution rows come from the previous level's GEMM
+    pdl_trigger();   // the level's GEMM may set up (and prefetch its factor entries) meanwhile
     const int hw = cw >> 1, per = ncb * hw;
     const double* b = io->r + (int64_t)mat * N * J;
     const int tot = nrows * per;
-    for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < tot; t += gridDim.x * blockDim.x) {
-        const int rq = t / per, rem = t - rq * per, cb = rem / hw, i = rem - cb * hw;
-        const int col = cb * cw + 2 * i;
-        if (col >= J) continue;
-        const int64_t row = rows[rq];
+    // one element per thread (the grid covers tot): row map, right-hand side and the children's row
+    // map are static during an apply and are fetched before the dependency wait
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    const bool on = t < tot;
+    const int rq = on ? t / per : 0, rem = t - rq * per, cb = rem / hw, i = rem - cb * hw;
+    const int col = cb * cw + 2 * i;
+    const bool live = on && col < J;
+    int64_t row = 0;
+    int4 g = make_int4(-1, -1, -1, -1);
+    double2 v = make_double2(0.0, 0.0);
+    if (live) {
+        row = rows[rq];
         ST_ASSERT(row >= 0 && row < nidx && idx[row] >= 0 && idx[row] < N);
-        const int4 g = *reinterpret_cast<const int4*>(gsrc + 4 * row);
+        g = *reinterpret_cast<const int4*>(gsrc + 4 * row);
         ST_ASSERT(g.x < nidx && g.y < nidx && g.z < nidx && g.w < nidx);
+        v = *reinterpret_cast<const double2*>(b + (int64_t)idx[row] * J + col);
+    }
+    pdl_wait();   // children's contribution rows come from the previous level's GEMM
+    if (live) {
         const double2* F2 = reinterpret_cast<const double2*>(FRS + (int64_t)(mat * ncb + cb) * nidx * ldb);
         const int h = ldb >> 1;
-        double2 v = *reinterpret_cast<const double2*>(b + (int64_t)idx[row] * J + col);
         if (g.x >= 0) {   // rows without children's contributions (all leaf rows) load nothing else
             const int src[4] = {g.x, g.y, g.z, g.w};
 #pragma unroll
@@ -891,7 +1133,6 @@ __global__ void __launch_bounds__(256) k_sfinit(const int32_t* __restrict__ rows
     __syncthreads();
     if (threadIdx.x == 0) ST_SPAN_END(probe_id);
 #endif
-    pdl_trigger();
 }
 
 // ---------------------------------------------------------------------------
@@ -911,7 +1152,27 @@ bool mf_stream_on(ens_ctx* c) {
 
 template <int NCT>
 static cudaError_t stream_attr(size_t smem) {
-    return cudaFuncSetAttribute(k_stream_gemm<NCT, 32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    const cudaError_t e =
+        cudaFuncSetAttribute(k_stream_gemm<NCT, 32, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    return cudaFuncSetAttribute(k_stream_gemm<NCT, 32, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)smem);
+}
+
+// Pieces per unit of a launch with U units whose longest inner range is kmax: as many as keep every
+// CTA resident at once and leave each piece at least two chunks (<= 8).  One CTA per unit cannot
+// pull a sparse upper level's factor entries fast enough (~40 GB/s per SM from HBM).
+// ENS_STREAM_SPLIT caps the piece count (1 = never split).
+static int stream_split(int64_t U, int kmax, int KC, int sms) {
+    static int cmax = -1;
+    if (cmax < 0) {
+        const char* e = std::getenv("ENS_STREAM_SPLIT");
+        cmax = e ? std::max(1, std::min(8, std::atoi(e))) : 8;
+    }
+    const int64_t budget = (int64_t)ST_CTAS * sms;
+    const int nch = (kmax + KC - 1) / KC;
+    const int64_t ks = std::min<int64_t>(std::min<int64_t>(cmax, budget / std::max<int64_t>(U, 1)), nch / 2);
+    return (int)std::max<int64_t>(ks, 1);
 }
 
 // tiles, per-launch CTA partitions and the stream buffer (once per context; J-dependent only in
@@ -935,14 +1196,43 @@ static int stream_setup(ens_ctx* c) {
     const int ldb = cw + (((4 - cw) % 16) + 16) % 16;
     const int KC = 32;
     const size_t stage = ((size_t)KC * ST_ROWS * 8 + ((size_t)KC * ldb + 8) * 8 + 127) & ~(size_t)127;
-    const int nst = (int)std::max<size_t>(2, std::min<size_t>(ST_MAXST, (216 * 1024 / ST_CTAS - 2048) / stage));
+    // backward epilogue: two result tiles (ST_ROWS x 8 * column tiles) + the tile's scatter range
+    const size_t rtb = sizeof(double) * 2 * ST_ROWS * 8 * (size_t)((cw + 7) / 8);
+    const int nst =
+        (int)std::max<size_t>(2, std::min<size_t>(ST_MAXST, (216 * 1024 / ST_CTAS - 2048 - rtb) / stage));
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    // backward scatter pairs: for every pivot position, the contribution rows of descendant fronts
+    // that hold the same dof (the backward epilogue writes the solution row straight into them),
+    // as (destination row, source row within its 32-row tile), ordered by source position -- the
+    // pairs of one backward tile are contiguous
+    const int64_t nidx_h = c->p.n_idx;
+    std::vector<int32_t> fidx_h((size_t)nidx_h);
+    ENS_CK(cudaMemcpy(fidx_h.data(), c->p.f_idx, sizeof(int32_t) * nidx_h, cudaMemcpyDeviceToHost));
+    std::vector<int32_t> piv_of((size_t)c->n_total, -1), piv_t((size_t)c->n_total, 0);
+    for (int f = 0; f < nf; ++f)
+        for (int t = 0; t < fk[f]; ++t) {
+            piv_of[fidx_h[fio[f] + t]] = (int32_t)(fio[f] + t);
+            piv_t[fidx_h[fio[f] + t]] = t % ST_ROWS;
+        }
+    std::vector<int32_t> sc_off((size_t)nidx_h + 1, 0);
+    for (int f = 0; f < nf; ++f)
+        for (int t = fk[f]; t < fm[f]; ++t) ++sc_off[piv_of[fidx_h[fio[f] + t]] + 1];
+    for (int64_t i = 0; i < nidx_h; ++i) sc_off[i + 1] += sc_off[i];
+    std::vector<int2> sc_ent((size_t)sc_off[nidx_h]);
+    {
+        std::vector<int32_t> fill(sc_off.begin(), sc_off.end() - 1);
+        for (int f = 0; f < nf; ++f)
+            for (int t = fk[f]; t < fm[f]; ++t) {
+                const int32_t dof = fidx_h[fio[f] + t];
+                sc_ent[fill[piv_of[dof]]++] = make_int2((int32_t)(fio[f] + t), piv_t[dof]);
+            }
+    }
     std::vector<STile> tiles;
     std::vector<int32_t> cta;
     c->slaunch.clear();
-    int64_t aoff = 0;
+    int64_t aoff = 0, part_units = 0;
     auto add_tile = [&](int f, int r0, int rows, int K, int flags, int row0) {
         STile t;
         const int ng = (std::min(ST_ROWS, rows - r0) + 7) / 8;
@@ -960,6 +1250,12 @@ static int stream_setup(ens_ctx* c) {
         t.row0 = row0;
         t.kb = 0;
         t.ke = K;
+        t.sc_lo = t.sc_n = 0;
+        if (flags & 1) {
+            const int nr = std::min(ST_ROWS, rows - r0);
+            t.sc_lo = sc_off[fio[f] + r0];
+            t.sc_n = sc_off[fio[f] + r0 + nr] - t.sc_lo;
+        }
         aoff += (int64_t)((K + 3) & ~3) * ng * 8;
         tiles.push_back(t);
     };
@@ -995,7 +1291,11 @@ static int stream_setup(ens_ctx* c) {
             const int64_t a = cta[base + i], b = cta[base + i + 1];
             if (b > a) max_cta_tiles = std::max<int>(max_cta_tiles, (int)((b - 1) / (2 * ncb) - a / (2 * ncb) + 1));
         }
-        c->slaunch.insert(c->slaunch.end(), {dir, L, (int64_t)t0, (int64_t)base, G});
+        int kmax = 0;
+        for (int64_t i = 0; i < nt; ++i) kmax = std::max(kmax, tiles[t0 + i].ke - tiles[t0 + i].kb);
+        const int64_t ks = stream_split(U, kmax, KC, sms);
+        if (ks > 1) part_units = std::max(part_units, U * ks);
+        c->slaunch.insert(c->slaunch.end(), {dir, L, (int64_t)t0, (int64_t)base, G, ks, U});
     };
     const int nlev = (int)c->level_front_off.size() - 1;
     for (int L = 0; L < nlev; ++L) {   // forward: contribution rows of every front
@@ -1022,34 +1322,17 @@ static int stream_setup(ens_ctx* c) {
             for (int t = 0; t < fk[f]; ++t) bg.push_back((int32_t)(fio[f] + t));
     }
     c->sbg_off[nlev] = (int64_t)bg.size();
-    // backward scatter lists: for every pivot position, the contribution rows of descendant fronts
-    // that hold the same dof (the backward epilogue writes the solution row straight into them)
-    const int64_t nidx_h = c->p.n_idx;
-    std::vector<int32_t> fidx_h((size_t)nidx_h);
-    ENS_CK(cudaMemcpy(fidx_h.data(), c->p.f_idx, sizeof(int32_t) * nidx_h, cudaMemcpyDeviceToHost));
-    std::vector<int32_t> piv_of((size_t)c->n_total, -1);
-    for (int f = 0; f < nf; ++f)
-        for (int t = 0; t < fk[f]; ++t) piv_of[fidx_h[fio[f] + t]] = (int32_t)(fio[f] + t);
-    std::vector<int32_t> sc_off((size_t)nidx_h + 1, 0), sc_row;
-    for (int f = 0; f < nf; ++f)
-        for (int t = fk[f]; t < fm[f]; ++t) ++sc_off[piv_of[fidx_h[fio[f] + t]] + 1];
-    for (int64_t i = 0; i < nidx_h; ++i) sc_off[i + 1] += sc_off[i];
-    sc_row.resize((size_t)sc_off[nidx_h]);
-    {
-        std::vector<int32_t> fill(sc_off.begin(), sc_off.end() - 1);
-        for (int f = 0; f < nf; ++f)
-            for (int t = fk[f]; t < fm[f]; ++t) sc_row[fill[piv_of[fidx_h[fio[f] + t]]]++] = (int32_t)(fio[f] + t);
-    }
     const size_t sbytes = sizeof(double) * 2 * (size_t)std::max<int64_t>(aoff, 32);
     const size_t frbytes = sizeof(double) * 2 * (size_t)ncb * (size_t)c->p.n_idx * ldb;
+    // fragment sums of the split launches: [unit * pieces + piece][row group][2 * column tiles][lane]
+    const size_t pbytes = sizeof(double) * std::max<size_t>((size_t)part_units * 4 * 2 * ((cw + 7) / 8) * 32, 32);
     if (cudaMalloc(&c->sstream, sbytes) != cudaSuccess || cudaMalloc(&c->stiles, sizeof(STile) * tiles.size()) !=
                                                               cudaSuccess ||
         cudaMalloc(&c->scta, sizeof(int32_t) * cta.size()) != cudaSuccess ||
         cudaMalloc(&c->sfr, frbytes) != cudaSuccess ||
         cudaMalloc(&c->sbg_rows, sizeof(int32_t) * std::max<size_t>(bg.size(), 1)) != cudaSuccess ||
-        cudaMalloc(&c->ssc_off, sizeof(int32_t) * sc_off.size()) != cudaSuccess ||
-
-        cudaMalloc(&c->ssc_row, sizeof(int32_t) * std::max<size_t>(sc_row.size(), 1)) != cudaSuccess) {
+        cudaMalloc(&c->spart, pbytes) != cudaSuccess ||
+        cudaMalloc(&c->ssc_ent, sizeof(int2) * std::max<size_t>(sc_ent.size(), 1)) != cudaSuccess) {
         cudaGetLastError();
         cudaFree(c->sstream);
         cudaFree(c->stiles);
@@ -1068,12 +1351,10 @@ static int stream_setup(ens_ctx* c) {
     ENS_CK(cudaMemcpy(c->scta, cta.data(), sizeof(int32_t) * cta.size(), cudaMemcpyHostToDevice));
     if (!bg.empty())
         ENS_CK(cudaMemcpy(c->sbg_rows, bg.data(), sizeof(int32_t) * bg.size(), cudaMemcpyHostToDevice));
-    ENS_CK(cudaMemcpy(c->ssc_off, sc_off.data(), sizeof(int32_t) * sc_off.size(), cudaMemcpyHostToDevice));
-
-    if (!sc_row.empty())
-        ENS_CK(cudaMemcpy(c->ssc_row, sc_row.data(), sizeof(int32_t) * sc_row.size(), cudaMemcpyHostToDevice));
-    c->ws_bytes += sbytes + frbytes + sizeof(STile) * tiles.size() +
-                   sizeof(int32_t) * (cta.size() + bg.size() + sc_off.size() + sc_row.size());
+    if (!sc_ent.empty())
+        ENS_CK(cudaMemcpy(c->ssc_ent, sc_ent.data(), sizeof(int2) * sc_ent.size(), cudaMemcpyHostToDevice));
+    c->ws_bytes += sbytes + frbytes + pbytes + sizeof(STile) * tiles.size() +
+                   sizeof(int32_t) * (cta.size() + bg.size() + 2 * sc_ent.size());
     // the classic front vectors are not used on this path
     c->ws_bytes -= sizeof(double) * 2 * (size_t)c->p.n_idx * c->J;
     cudaFree(c->frvec);
@@ -1086,8 +1367,9 @@ static int stream_setup(ens_ctx* c) {
     c->snst = nst;
     c->skc = KC;
     c->sstage = stage;
-    c->sdesc = (size_t)max_cta_tiles * sizeof(STile);
-    const size_t smem = stage * nst + c->sdesc;
+    c->sdesc = ((size_t)max_cta_tiles * sizeof(STile) + 15) & ~(size_t)15;
+    c->srt = rtb;
+    const size_t smem = stage * nst + c->sdesc + c->srt;
     if (smem > 220 * 1024) {
         ens_set_error("streamed solve: a CTA's tile descriptors do not fit shared memory", __FILE__, __LINE__);
         return ENS_EINVAL;
@@ -1123,21 +1405,37 @@ static int stream_launches(ens_ctx* c, cudaStream_t s, SolveIO* io, int64_t* cnt
     const int J = c->J;
     const int64_t N = c->n_total, nidx = c->p.n_idx;
     const int nct = (c->scw + 7) / 8;
-    const size_t smem = c->sstage * c->snst + c->sdesc;
     const int nlev = (int)c->level_front_off.size() - 1;
     std::vector<int> fwd_at(nlev, -1), bwd_at(nlev, -1);
-    for (size_t i = 0; i + 5 <= c->slaunch.size(); i += 5)
+    const size_t smem = c->sstage * c->snst + c->sdesc + c->srt;
+    for (size_t i = 0; i + 7 <= c->slaunch.size(); i += 7)
         (c->slaunch[i] == 0 ? fwd_at : bwd_at)[c->slaunch[i + 1]] = (int)i;
     auto gemm = [&](int li) -> int {
         const int64_t* r = &c->slaunch[li];
         const int t0 = (int)r[2], cb = (int)r[3];
-        const unsigned G = (unsigned)r[4];
+        const int ks = (int)r[5];
+        const unsigned U = (unsigned)r[6], G = ks > 1 ? U * (unsigned)ks : (unsigned)r[4];
+#define SGS_(NC, SPL)                                                                                              \
+    ENS_CK(launch_pdl(k_stream_gemm<NC, 32, SPL>, dim3(G), dim3(ST_THREADS), smem, s, (const STile*)c->stiles, t0, \
+                      (const int32_t*)(c->scta + cb), c->sncb, c->scw, c->sldb, (const double*)c->sstream,       \
+                      c->stream_len, c->sfr, (const SolveIO*)io, (const int32_t*)c->p.f_idx,                    \
+                      (const int32_t*)c->p.gsrc, (const int2*)c->ssc_ent, N, J, nidx, c->snst,                   \
+                      (uint32_t)c->sstage, (uint32_t)c->sdesc, c->spart, ks, (int)*cnt))
 #define SGS(NC)                                                                                                    \
-    ENS_CK(launch_pdl(k_stream_gemm<NC, 32>, dim3(G), dim3(ST_THREADS), smem, s, (const STile*)c->stiles, t0,     \
-                      (const int32_t*)(c->scta + cb), c->sncb, c->scw, c->sldb, (const double*)c->sstream,      \
-                      c->stream_len, c->sfr, (const SolveIO*)io, (const int32_t*)c->p.f_idx,                   \
-                      (const int32_t*)c->p.gsrc, (const int32_t*)c->ssc_off, (const int32_t*)c->ssc_row,        \
-                      N, J, nidx, c->snst, (uint32_t)c->sstage, (int)*cnt))
+    do {                                                                                                           \
+        if (ks > 1) {                                                                                              \
+            SGS_(NC, true);                                                                                        \
+            ENS_CKL();                                                                                             \
+            ++*cnt;                                                                                                \
+            ENS_CK(launch_pdl(k_stream_reduce<NC>, dim3(U, r[0] == 1 ? 8 : 1), dim3(128), 0, s,                   \
+                              (const STile*)c->stiles, t0, c->sncb,                                               \
+                              c->scw, c->sldb, c->sfr, (const SolveIO*)io, (const int32_t*)c->p.f_idx,            \
+                              (const int32_t*)c->p.gsrc, (const int2*)c->ssc_ent, N, J, nidx,                     \
+                              (const double*)c->spart, ks, (int)*cnt));                                           \
+        } else {                                                                                                   \
+            SGS_(NC, false);                                                                                       \
+        }                                                                                                          \
+    } while (0)
         switch (nct) {
             case 1: SGS(1); break;
             case 2: SGS(2); break;
@@ -1149,6 +1447,7 @@ static int stream_launches(ens_ctx* c, cudaStream_t s, SolveIO* io, int64_t* cnt
             default: SGS(8); break;
         }
 #undef SGS
+#undef SGS_
         ENS_CKL();
         ++*cnt;
         return ENS_OK;

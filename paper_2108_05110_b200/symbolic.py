@@ -39,7 +39,7 @@ import scipy.sparse as sp
 
 PW = 64          # panel width (max pivots per diagonal block)
 TILE = 64        # GEMM tile edge in the numeric kernels
-LEAF_NODES = int(__import__("os").environ.get("ENS_LEAF", "24"))  # stop dissecting below this many P2 nodes
+LEAF_NODES = int(__import__("os").environ.get("ENS_LEAF", "48"))  # stop dissecting below this many P2 nodes (48: a balanced tree, one level fewer than 24 at the same fill)
 
 
 # ----------------------------------------------------------------------
