@@ -67,7 +67,7 @@ def mesh_key(disc) -> str:
     h = hashlib.sha256()
     h.update(b"ensmhd-b200-hostmesh\0%d\0" % FORMAT)
     h.update(_code_digest())
-    h.update(repr((S.LEAF_NODES, S.PW, S.SPLIT_K, disc.pressure.kind, bool(disc.pin_pressure),
+    h.update(repr((S.LEAF_NODES, S.AMALGAMATE, S.PW, S.SPLIT_K, disc.pressure.kind, bool(disc.pin_pressure),
                    disc.n_scalar, disc.n_pres)).encode())
 
     def arr(a):

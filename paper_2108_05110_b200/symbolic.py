@@ -39,6 +39,8 @@ import scipy.sparse as sp
 
 PW = 64          # panel width (max pivots per diagonal block)
 TILE = 64        # GEMM tile edge in the numeric kernels
+# tree heights (leaves = 0) whose nodes are merged into their parents (ENS_AMALG="1,3")
+AMALGAMATE = tuple(int(x) for x in __import__("os").environ.get("ENS_AMALG", "1").split(",") if x.strip())
 LEAF_NODES = int(__import__("os").environ.get("ENS_LEAF", "48"))  # stop dissecting below this many P2 nodes (48: a balanced tree, one level fewer than 24 at the same fill)
 
 
@@ -186,6 +188,37 @@ def _nested_dissection_py(coords, indptr, indices, leaf=LEAF_NODES):
     return tnodes, kids, 0
 
 
+def _amalgamate(tnodes, kids, root, heights):
+    """Merge every tree node whose height (leaves = 0) is in `heights` into its parent: the parent's
+    front then eliminates both separators (more fill, one tree level -- one launch round of every
+    sweep -- fewer).  Returns (tnodes, kids, root) of the reduced tree."""
+    if not heights:
+        return tnodes, kids, root
+    T = len(tnodes)
+    order = _postorder(kids, root)
+    height = np.zeros(T, dtype=np.int64)
+    parent = np.full(T, -1, dtype=np.int64)
+    for t in order:
+        for c in kids[t]:
+            parent[c] = t
+            height[t] = max(height[t], height[c] + 1)
+    gone = np.zeros(T, dtype=bool)
+    nodes = [np.asarray(x) for x in tnodes]
+    kk = [list(k) for k in kids]
+    for t in order:   # children before parents: a merged node's kids are final when it is merged
+        if t == root or height[t] not in heights:
+            continue
+        p = parent[t]
+        nodes[p] = np.concatenate([nodes[t], nodes[p]])
+        kk[p] = [c for c in kk[p] if c != t] + kk[t]
+        for c in kk[t]:
+            parent[c] = p
+        gone[t] = True
+    new_id = np.cumsum(~gone) - 1
+    keep = [t for t in range(T) if not gone[t]]
+    return ([nodes[t] for t in keep], [[int(new_id[c]) for c in kk[t]] for t in keep], int(new_id[root]))
+
+
 def _postorder(kids, root):
     out, stack = [], [(root, False)]
     while stack:
@@ -242,6 +275,7 @@ def analyse(disc, leaf=LEAF_NODES, pw=PW):
     g.eliminate_zeros()
     g.sort_indices()
     tnodes, kids, root = _nested_dissection(vel.dof_coords, g.indptr, g.indices, leaf)
+    tnodes, kids, root = _amalgamate(tnodes, kids, root, AMALGAMATE)
     post = _postorder(kids, root)
     T = len(tnodes)
     rank = np.empty(T, dtype=np.int64)
