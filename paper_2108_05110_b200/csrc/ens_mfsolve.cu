@@ -828,11 +828,7 @@ __device__ __forceinline__ void st_consume(const STile* sT, int tb, int ub, int 
         const int j0 = cb * cw, jn = min(cw, J - j0);
         const bool bwd = T.flags & 1;
         const int nr = min(ST_ROWS, (bwd ? T.kp : T.m - T.kp) - T.r0);
-#ifdef ST_NO_ROT
-        const int grp = warp;
-#else
         const int grp = (warp - rot) & 3;
-#endif
         const int row = 8 * grp + g;
         const bool active = grp < T.ng;
         const bool row_ok = active && row < nr;
@@ -842,21 +838,9 @@ __device__ __forceinline__ void st_consume(const STile* sT, int tb, int ub, int 
 #pragma unroll
         for (int ct = 0; ct < NCT; ++ct) init[ct][0] = init[ct][1] = 0.0;
         if (!SPLIT) {
-#ifdef ST_NO_METAPF
-            const int4 meta = st_row_meta(T, grp, g, fidx, gsrc);
-#else
             const int4 meta = mnext;
-#endif
             rot = (rot + T.ng) & 3;
-#ifndef ST_NO_METAPF
-            if (u + 1 < ue) {
-#ifdef ST_NO_ROT
-                mnext = st_row_meta(sT[(u + 1) / per_tile - tb], warp, g, fidx, gsrc);
-#else
-                mnext = st_row_meta(sT[(u + 1) / per_tile - tb], (warp - rot) & 3, g, fidx, gsrc);
-#endif
-            }
-#endif
+            if (u + 1 < ue) mnext = st_row_meta(sT[(u + 1) / per_tile - tb], (warp - rot) & 3, g, fidx, gsrc);
             if (row_ok) {
                 if (bwd) {
                     ST_ASSERT(meta.x >= 0 && meta.x < N);
@@ -991,11 +975,9 @@ __global__ void __launch_bounds__(ST_THREADS, ST_CTAS)
     pdl_trigger();
     if (warp == 4) {
         int pre = 0;
-#ifndef ST_NO_EARLYA
         if (lane == 0)
             pre = st_produce<KC>(sT, tb, ub, ue, per_tile, ncb, ldb, S, slen, FRS, nidx, nst, stage_bytes, sbase,
                                  bbase, true, 0);
-#endif
         pdl_wait();   // front rows / the iterate come from the previous launch (consumers: in st_consume)
         if (lane == 0)
             st_produce<KC>(sT, tb, ub, ue, per_tile, ncb, ldb, S, slen, FRS, nidx, nst, stage_bytes, sbase, bbase,
