@@ -145,6 +145,9 @@ int  ens_workspace_bytes(const ens_ctx* ctx, int64_t* bytes);
 /* Panel inverses with in-panel partial pivoting (1) or diagonal pivots (0, default;
  * the symbolic ordering guarantees nonsingular leading blocks in exact arithmetic). */
 int  ens_set_pivoting(ens_ctx* ctx, int on);
+/* Diagnostics: how many tree-level launches of the streamed preconditioner apply run as split-K
+ * pieces + reduction (0 before the first factorisation or on the classic path). */
+int  ens_stream_split_launches(const ens_ctx* ctx);
 
 /* y = a x + b y over one iterate block set (2 x n_total x J); used for the
  * extrapolated FGMRES initial iterate 2 x^n - x^{n-1}. */

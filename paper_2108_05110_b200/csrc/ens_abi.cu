@@ -142,6 +142,13 @@ int ens_set_pivoting(ens_ctx* c, int on) {
     return ENS_OK;
 }
 
+int ens_stream_split_launches(const ens_ctx* c) {
+    if (!c) return -1;
+    int n = 0;
+    for (size_t i = 0; i + 7 <= c->slaunch.size(); i += 7) n += c->slaunch[i + 5] > 1 ? 1 : 0;
+    return n;
+}
+
 int ens_workspace_bytes(const ens_ctx* c, int64_t* bytes) {
     if (!c || !bytes) return ENS_EINVAL;
     *bytes = (int64_t)c->ws_bytes;

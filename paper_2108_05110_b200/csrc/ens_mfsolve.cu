@@ -1020,11 +1020,11 @@ __global__ void __launch_bounds__(128) k_stream_reduce(const STile* __restrict__
     const int lpp = jn >> 1, ppw = 32 / lpp, sub = lane / lpp;
     const int e_first = T.sc_lo + ((int)blockIdx.y * 4 + grp) * ppw + sub, e1 = T.sc_lo + T.sc_n;
     if (blockIdx.y > 0 && (!bwd || T.sc_lo + (int)blockIdx.y * 4 * ppw >= e1)) return;
+    pdl_trigger();
     const int4 meta = st_row_meta(T, grp, g, fidx, gsrc);
     double* FRm = FRS + (int64_t)(mat * ncb + cb) * nidx * ldb;
     int2 pre[ST_SCU];
     if (bwd && sub < ppw) st_scatter_load(pre, sc_ent, e_first, e1, 4 * (int)gridDim.y * ppw);   // (static data)
-    pdl_trigger();
     pdl_wait();   // the pieces come from the previous launch
     double sum[NCT][2], init[NCT][2];
 #pragma unroll
@@ -1146,11 +1146,8 @@ static cudaError_t stream_attr(size_t smem) {
 // pull a sparse upper level's factor entries fast enough (~40 GB/s per SM from HBM).
 // ENS_STREAM_SPLIT caps the piece count (1 = never split).
 static int stream_split(int64_t U, int kmax, int KC, int sms) {
-    static int cmax = -1;
-    if (cmax < 0) {
-        const char* e = std::getenv("ENS_STREAM_SPLIT");
-        cmax = e ? std::max(1, std::min(8, std::atoi(e))) : 8;
-    }
+    const char* e = std::getenv("ENS_STREAM_SPLIT");   // (read per context: tests compare both paths)
+    const int cmax = e ? std::max(1, std::min(8, std::atoi(e))) : 8;
     const int64_t budget = (int64_t)ST_CTAS * sms;
     const int nch = (kmax + KC - 1) / KC;
     const int64_t ks = std::min<int64_t>(std::min<int64_t>(cmax, budget / std::max<int64_t>(U, 1)), nch / 2);

@@ -85,6 +85,41 @@ def test_plan_invariants():
     assert set(np.unique(sched["factor"][:, 0])) <= set(range(7))
 
 
+@pytest.mark.parametrize("heights", [(), (1,), (1, 2), (1, 3), (2, 4)])
+def test_amalgamated_trees_solve(heights, rng, monkeypatch):
+    """Merging tree levels into their parents (symbolic._amalgamate) keeps the plan a valid
+    factorisation: every free dof is still eliminated exactly once, children precede parents, and
+    the emulated factor + solve reproduces the saddle solution; each merged height removes a level."""
+    disc = Discretization.from_mesh(build_structured_square(12), pressure="th")
+    monkeypatch.setattr(S, "AMALGAMATE", ())
+    base = S.analyse(disc, leaf=6)
+    monkeypatch.setattr(S, "AMALGAMATE", heights)
+    plan = S.analyse(disc, leaf=6)
+    assert plan.nlevels == base.nlevels - len(heights)
+    piv = np.concatenate([plan.f_idx[plan.f_idx_off[f]:plan.f_idx_off[f] + plan.f_k[f]] for f in range(plan.nfront)])
+    assert len(np.unique(piv)) == len(piv) == disc.n_total - len(disc.constrained_rows)
+    for f in range(plan.nfront):
+        p = plan.f_parent[f]
+        if p >= 0:
+            assert plan.f_level[p] > plan.f_level[f]
+    cfg = EnsembleConfig((MemberParams(0.01, 0.011), MemberParams(0.009, 0.01)), 1.0, 1.0, 0.01, 0.1)
+    w = rng.standard_normal((2, disc.n_vel))
+    pat = fe.scalar_pattern(disc.velocity)
+    a_s = (O.velocity_block(w.mean(0), w - w.mean(0), cfg, disc) + 0.0 * pat).tocsr()
+    a_s.sort_indices()
+    assert a_s.nnz == pat.nnz
+    K = O.saddle_matrix(a_s, disc)
+    st = E.factor(plan, a_s.data)
+    iid = internal_ids(disc, plan)
+    b = rng.standard_normal((disc.n_total, 2))
+    b[disc.constrained_rows] = 0.0
+    bi = np.zeros_like(b)
+    bi[iid] = b
+    x = E.solve(plan, st, bi)[iid]
+    res = np.linalg.norm(K @ x - b, axis=0) / np.linalg.norm(b, axis=0)
+    assert res.max() < 1e-11, res
+
+
 def test_split_k_schedule(rng, monkeypatch):
     """Force tiny split-K so the partial/reduce path of the solve schedule is exercised."""
     monkeypatch.setattr(S, "SPLIT_K", 16)

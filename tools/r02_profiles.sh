@@ -17,7 +17,7 @@ ncu --profile-from-start off --cache-control none --clock-control none \
     --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum --csv \
     python tools/spmm_once.py > $O/r02_spmm_traffic.csv 2>/dev/null
 # full capture of the largest streamed-GEMM launch (leaf level, backward) for the stall / source pages
-ncu --profile-from-start off --set full --import-source on -k regex:k_stream_gemm --launch-skip 24 -c 1 \
+ncu --profile-from-start off --set full --import-source on -k regex:k_stream_gemm --launch-skip 20 -c 1 \
     -o $O/r02_stream_gemm python tools/precond_once.py > /dev/null 2>&1
 ncu --profile-from-start off --set full --import-source on -k regex:k_spmm -c 1 \
     -o $O/r02_spmm python tools/spmm_once.py > /dev/null 2>&1
