@@ -326,6 +326,148 @@ __global__ void __launch_bounds__(256, 3) k_diag_np(MfDev d, int item0, double* 
         }
 }
 
+// DIAG without pivoting, blocked (default): in-place block Gauss-Jordan with 8 x 8 blocks on the fp64
+// tensor cores.  Warp w keeps row block w (8 x 64) in registers in the DMMA accumulator layout
+// (lane (g, q): row g, columns 8 j + 2 q + {0, 1}) through all 8 block steps.  Block step k:
+//   pivot warp k : P = A[k,k]^-1 by scalar Gauss-Jordan in registers (warp shuffles; pivots below
+//                  1e-14 x max|D| perturbed and counted, as in k_diag_np), then its new row block
+//                  R = P A[k,:] (block k of it: P itself) by DMMA, published in shared memory;
+//   other warps i: A[i,j] -= A[i,k] R[j] (j != k), A[i,k] = -A[i,k] P -- one rank-8 DMMA update of
+//                  the warp's registers (the A[i,k] fragment comes from the accumulator layout by
+//                  shuffles).
+// One CTA barrier per block step (R double-buffered): ~6 us per panel instead of the 64 barrier
+// steps (~33 us) of the scalar k_diag_np, which stays as the reference implementation.
+#define DB_LD 68
+__device__ __forceinline__ void up_mma(double& d0, double& d1, double a, double b) {
+    asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+        : "+d"(d0), "+d"(d1)
+        : "d"(a), "d"(b));
+}
+__device__ __forceinline__ double db_shfl(double v, int src) { return __shfl_sync(0xffffffffu, v, src); }
+// 1 / x for a pivot (|x| >= the perturbation threshold, finite): hardware seed + three Newton steps.
+// The division is on the serial path of every scalar pivot step, IEEE division costs ~10x this.
+__device__ __forceinline__ double db_rcp(double x) {
+    double r;
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+    r = fma(fma(-x, r, 1.0), r, r);
+    r = fma(fma(-x, r, 1.0), r, r);
+    r = fma(fma(-x, r, 1.0), r, r);
+    return r;
+}
+
+__global__ void __launch_bounds__(256) k_diag_blk(MfDev d, int item0, double* __restrict__ F,
+                                                  int32_t* __restrict__ npert) {
+    __shared__ __align__(16) double s_R[2][8 * DB_LD];
+    __shared__ __align__(16) double s_P[8 * 12];   // the pivot block's inverse as the A operand of R = P A[k,:]
+    __shared__ double s_wmax[8];
+    const int* it = d.work + 4LL * (item0 + blockIdx.x);
+    const int f = it[0], a0 = it[1];
+    const int mat = blockIdx.y;
+    const int m = d.m[f];
+    const int pw = min(ENS_PW, d.k[f] - a0);
+    double* Fb = F + (int64_t)mat * d.storage + d.off[f] + (int64_t)a0 * m + a0;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, g = lane >> 2, q = lane & 3;
+    const int row = 8 * warp + g;
+    double acc[8][2];
+    double amax = 0.0;
+#pragma unroll
+    for (int j = 0; j < 8; ++j)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+            const int c = 8 * j + 2 * q + e;
+            double v = (row == c) ? 1.0 : 0.0;
+            if (row < pw && c < pw) {
+                v = Fb[(int64_t)row * m + c];
+                amax = fmax(amax, fabs(v));
+            }
+            acc[j][e] = v;
+        }
+    for (int o = 16; o > 0; o >>= 1) amax = fmax(amax, __shfl_xor_sync(0xffffffffu, amax, o));
+    if (lane == 0) s_wmax[warp] = amax;
+    __syncthreads();
+    double scale = 0.0;
+#pragma unroll
+    for (int w = 0; w < 8; ++w) scale = fmax(scale, s_wmax[w]);
+    const double thr = 1e-14 * (scale > 0.0 ? scale : 1.0);
+    int pert = 0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+        double* R = s_R[k & 1];
+        if (warp == k) {
+            // old row block -> shared memory (the B operand of R = P A[k,:])
+#pragma unroll
+            for (int j = 0; j < 8; ++j)
+                *reinterpret_cast<double2*>(&R[g * DB_LD + 8 * j + 2 * q]) = make_double2(acc[j][0], acc[j][1]);
+            // P = A[k,k]^-1 in registers: b0 = B[g][2q], b1 = B[g][2q+1]
+            double b0 = acc[k][0], b1 = acc[k][1];
+#pragma unroll
+            for (int s2 = 0; s2 < 8; ++s2) {
+                const int hs = s2 >> 1, od = s2 & 1;
+                double piv = db_shfl(od ? b1 : b0, 4 * s2 + hs);
+                if (!(fabs(piv) > thr)) {
+                    piv = piv < 0.0 ? -thr : thr;
+                    pert = 1;
+                }
+                const double inv = db_rcp(piv);
+                const double r0 = db_shfl(b0, 4 * s2 + q) * inv, r1 = db_shfl(b1, 4 * s2 + q) * inv;   // row s2 / piv
+                const double cs = db_shfl(od ? b1 : b0, 4 * g + hs);                                  // B[g][s2]
+                const bool c0 = (2 * q == s2), c1 = (2 * q + 1 == s2);                              // my column s2?
+                if (g == s2) {
+                    b0 = c0 ? inv : r0;
+                    b1 = c1 ? inv : r1;
+                } else {
+                    b0 = c0 ? -cs * inv : b0 - cs * r0;
+                    b1 = c1 ? -cs * inv : b1 - cs * r1;
+                }
+            }
+            __syncwarp();
+            *reinterpret_cast<double2*>(&s_P[g * 12 + 2 * q]) = make_double2(b0, b1);
+            __syncwarp();
+            double nr[8][2];
+#pragma unroll
+            for (int j = 0; j < 8; ++j) nr[j][0] = nr[j][1] = 0.0;
+#pragma unroll
+            for (int u = 0; u < 2; ++u) {
+                const double av = s_P[g * 12 + 4 * u + q];
+#pragma unroll
+                for (int j = 0; j < 8; ++j) up_mma(nr[j][0], nr[j][1], av, R[(4 * u + q) * DB_LD + 8 * j + g]);
+            }
+            __syncwarp();
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                acc[j][0] = j == k ? b0 : nr[j][0];
+                acc[j][1] = j == k ? b1 : nr[j][1];
+                *reinterpret_cast<double2*>(&R[g * DB_LD + 8 * j + 2 * q]) = make_double2(acc[j][0], acc[j][1]);
+            }
+        }
+        __syncthreads();
+        if (warp != k) {
+            // -A[i,k] as the A operand (row g, columns 4 u + q) from the accumulator layout
+            double av[2];
+#pragma unroll
+            for (int u = 0; u < 2; ++u) {
+                const int c = 4 * u + q, src = 4 * g + (c >> 1);
+                const double x0 = db_shfl(acc[k][0], src), x1 = db_shfl(acc[k][1], src);
+                av[u] = -((c & 1) ? x1 : x0);
+            }
+            acc[k][0] = acc[k][1] = 0.0;
+#pragma unroll
+            for (int u = 0; u < 2; ++u)
+#pragma unroll
+                for (int j = 0; j < 8; ++j) up_mma(acc[j][0], acc[j][1], av[u], R[(4 * u + q) * DB_LD + 8 * j + g]);
+        }
+    }
+    pert = __syncthreads_or(pert);
+    if (pert && threadIdx.x == 0) atomicAdd(npert, 1);
+#pragma unroll
+    for (int j = 0; j < 8; ++j)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+            const int c = 8 * j + 2 * q + e;
+            if (row < pw && c < pw) Fb[(int64_t)row * m + c] = -acc[j][e];
+        }
+}
+
 // UPDATE on the fp64 tensor cores with one asynchronous staging round trip:
 // the output tile C (64 x 64, rows/cols outside the panel) is prefetched into the
 // accumulator fragments while A = F[Q-rows, P] and B = F[P, Q-cols] stream into
@@ -337,13 +479,8 @@ __device__ __forceinline__ void up_cp8(double* sdst, const double* g, bool pred)
     const unsigned sa = (unsigned)__cvta_generic_to_shared(sdst);
     asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(sa), "l"(g), "r"(pred ? 8 : 0));
 }
-__device__ __forceinline__ void up_mma(double& d0, double& d1, double a, double b) {
-    asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
-        : "+d"(d0), "+d"(d1)
-        : "d"(a), "d"(b));
-}
 
-__global__ void __launch_bounds__(256, 2) k_update2(MfDev d, int item0, double* __restrict__ F) {
+__global__ void __launch_bounds__(256, 3) k_update2(MfDev d, int item0, double* __restrict__ F) {
     extern __shared__ double sm[];
     double* As = sm;                    // [64 rows][UP_LD]   A[r][k]
     double* Bs = sm + 64 * UP_LD;       // [64 k][UP_LD]      B[k][c]
@@ -484,6 +621,15 @@ int mf_setup(ens_ctx* c) {
     return ENS_OK;
 }
 
+static bool diag_scalar() {   // ENS_DIAG_SCALAR=1: the scalar Gauss-Jordan panel inverse (A/B measurements)
+    static int v = -1;
+    if (v < 0) {
+        const char* e = std::getenv("ENS_DIAG_SCALAR");
+        v = e && e[0] == '1' ? 1 : 0;
+    }
+    return v == 1;
+}
+
 static int mf_factor_launches(ens_ctx* c, cudaStream_t s, const double* as_vals, int64_t* nlaunch) {
     MfDev d = mfdev(c);
     const int64_t st = c->p.front_storage;
@@ -524,8 +670,10 @@ static int mf_factor_launches(ens_ctx* c, cudaStream_t s, const double* as_vals,
             case OP_DIAG:
                 if (c->diag_pivot)
                     k_diag<<<dim3(n, 2), 256, 0, s>>>(d, off, c->fronts, c->d_count);
-                else
+                else if (diag_scalar())
                     k_diag_np<<<dim3(n, 2), 256, 0, s>>>(d, off, c->fronts, c->d_count);
+                else
+                    k_diag_blk<<<dim3(n, 2), 256, 0, s>>>(d, off, c->fronts, c->d_count);
                 break;
             case OP_HPANEL:
                 k_panel2<true><<<dim3(n, 2), 256, SM_UP2, s>>>(d, off, c->fronts);
