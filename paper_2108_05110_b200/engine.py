@@ -41,16 +41,16 @@ RENEW_WINDOW = int(os.environ.get("ENS_RENEW_WINDOW", "6"))   # lifetimes a per-
 RENEW_STALE = int(os.environ.get("ENS_RENEW_STALE", str(4 * RENEW_WINDOW)))
 
 
-# Cost model of the renewal rule, fitted to the round-1 kernels on B200: a
+# Cost model of the renewal rule, fitted to the round-2 kernels on B200: a
 # factorisation costs a fixed latency per tree level plus its flops at an effective DMMA rate; an
 # apply costs a latency per level and direction plus the larger of its bytes and flops terms.  The
 # constants are fixed, so the rule built on them is a deterministic function of the plan, J and the
-# iteration counts (fit: C2 8.4 / 0.71 ms, C3 44 / 5.5 ms, C4 8.9 / 3.0 ms factor / apply).
-FACTOR_LEVEL_S = 0.28e-3       # per tree level (panel, update and extend-add launches)
-RATE_FACTOR_FLOPS = 8.0e12     # sweep factorisation, fp64 DMMA
+# iteration counts (fit: C2 6.84 / 0.47 ms, C3 36.6 / 4.9 ms, C4 7.65 / 2.7 ms factor / apply).
+FACTOR_LEVEL_S = 0.257e-3      # per tree level (panel, update and extend-add launches)
+RATE_FACTOR_FLOPS = 9.87e12    # sweep factorisation, fp64 DMMA
 APPLY_LEVEL_S = 10e-6          # per tree level and sweep direction
-RATE_APPLY_BYTES = 2.2e12      # preconditioner apply, algorithmic bytes
-RATE_APPLY_FLOPS = 11.0e12     # preconditioner apply at large J (fp64 DMMA)
+RATE_APPLY_BYTES = 4.1e12      # preconditioner apply, algorithmic bytes
+RATE_APPLY_FLOPS = 13.7e12     # preconditioner apply at large J (fp64 DMMA)
 RATE_SPMM_BYTES = 1.39e12      # saddle SpMM, algorithmic bytes
 
 
