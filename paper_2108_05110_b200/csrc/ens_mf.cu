@@ -203,140 +203,20 @@ __global__ void __launch_bounds__(256) k_diag(MfDev d, int item0, double* __rest
     }
 }
 
-// DIAG without pivoting (default): the symbolic ordering (velocities before
-// pressures, pressures moved above all their velocity neighbours) makes every
-// leading block of a panel nonsingular, so the in-place Gauss-Jordan can take
-// the diagonal pivot.  One barrier per step: after its update, the owners of
-// column k+1 and row k+1 publish them for the next step.  A pivot below
-// 1e-14 x max|D| is perturbed and counted; the host then refactorises with the
-// pivoting kernel (k_diag).
-__global__ void __launch_bounds__(256, 3) k_diag_np(MfDev d, int item0, double* __restrict__ F,
-                                                  int32_t* __restrict__ npert) {
-    __shared__ double s_col[2][ENS_PW];
-    __shared__ double s_row[2][ENS_PW];
-    __shared__ double s_wmax[8];
-    const int* it = d.work + 4LL * (item0 + blockIdx.x);
-    const int f = it[0], a0 = it[1];
-    const int mat = blockIdx.y;
-    const int m = d.m[f];
-    const int pw = min(ENS_PW, d.k[f] - a0);
-    double* Fb = F + (int64_t)mat * d.storage + d.off[f] + (int64_t)a0 * m + a0;
-    const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    double a[4][4];
-    double amax = 0.0;
-#pragma unroll
-    for (int i = 0; i < 4; ++i)
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-            const int r = ty + 16 * i, c = tx + 16 * j;
-            double v = (r == c) ? 1.0 : 0.0;
-            if (r < pw && c < pw) v = Fb[(int64_t)r * m + c];
-            a[i][j] = v;
-            if (r < pw && c < pw) amax = fmax(amax, fabs(v));
-        }
-    for (int o = 16; o > 0; o >>= 1) amax = fmax(amax, __shfl_xor_sync(0xffffffffu, amax, o));
-    if (lane == 0) s_wmax[warp] = amax;
-    if (tx == 0) {
-#pragma unroll
-        for (int i = 0; i < 4; ++i) s_col[0][ty + 16 * i] = a[i][0];
-    }
-    if (ty == 0) {
-#pragma unroll
-        for (int j = 0; j < 4; ++j) s_row[0][tx + 16 * j] = a[0][j];
-    }
-    __syncthreads();
-    double scale = 0.0;
-#pragma unroll
-    for (int w = 0; w < 8; ++w) scale = fmax(scale, s_wmax[w]);
-    const double thr = 1e-14 * (scale > 0.0 ? scale : 1.0);
-    int pert = 0;
-    for (int k = 0; k < pw; ++k) {
-        const int buf = k & 1;
-        double piv = s_col[buf][k];
-        if (!(fabs(piv) > thr)) {
-            piv = piv < 0.0 ? -thr : thr;
-            pert = 1;
-        }
-        const double inv = 1.0 / piv;
-        // plain rank-1 update of all 16 entries (no per-entry pivot tests: the step was issue-bound
-        // on them), then the pivot column and row of the owning threads are overwritten -- the
-        // same values as before: column k gets 0 - fr * inv, row k gets row * inv (inv on the pivot)
-        const int kk = k & 15, kh = k >> 4;
-        double np[4], fr[4];
-#pragma unroll
-        for (int j = 0; j < 4; ++j) np[j] = s_row[buf][tx + 16 * j] * inv;
-#pragma unroll
-        for (int i = 0; i < 4; ++i) fr[i] = s_col[buf][ty + 16 * i];
-#pragma unroll
-        for (int i = 0; i < 4; ++i)
-#pragma unroll
-            for (int j = 0; j < 4; ++j) a[i][j] -= fr[i] * np[j];
-        if (tx == kk) {   // column k (the thread's column slot kh): -fr * inv
-#pragma unroll
-            for (int j = 0; j < 4; ++j)
-                if (j == kh) {
-#pragma unroll
-                    for (int i = 0; i < 4; ++i) a[i][j] = -(fr[i] * inv);
-                    np[j] = inv;
-                }
-        }
-        if (ty == kk) {   // row k (the thread's row slot kh): row * inv, inv on the pivot
-#pragma unroll
-            for (int i = 0; i < 4; ++i)
-                if (i == kh) {
-#pragma unroll
-                    for (int j = 0; j < 4; ++j) a[i][j] = np[j];
-                }
-        }
-        const int k1 = k + 1;
-        if (k1 < pw) {
-            if (tx == (k1 & 15)) {
-                const int jj = k1 >> 4;
-#pragma unroll
-                for (int i = 0; i < 4; ++i) {
-                    double v = 0.0;
-#pragma unroll
-                    for (int j = 0; j < 4; ++j)
-                        if (j == jj) v = a[i][j];
-                    s_col[buf ^ 1][ty + 16 * i] = v;
-                }
-            }
-            if (ty == (k1 & 15)) {
-                const int ii = k1 >> 4;
-#pragma unroll
-                for (int j = 0; j < 4; ++j) {
-                    double v = 0.0;
-#pragma unroll
-                    for (int i = 0; i < 4; ++i)
-                        if (i == ii) v = a[i][j];
-                    s_row[buf ^ 1][tx + 16 * j] = v;
-                }
-            }
-        }
-        __syncthreads();
-    }
-    if (pert && threadIdx.x == 0) atomicAdd(npert, 1);
-#pragma unroll
-    for (int i = 0; i < 4; ++i)
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-            const int r = ty + 16 * i, c = tx + 16 * j;
-            if (r < pw && c < pw) Fb[(int64_t)r * m + c] = -a[i][j];
-        }
-}
-
-// DIAG without pivoting, blocked (default): in-place block Gauss-Jordan with 8 x 8 blocks on the fp64
-// tensor cores.  Warp w keeps row block w (8 x 64) in registers in the DMMA accumulator layout
+// DIAG without pivoting (default): the symbolic ordering (velocities before pressures, pressures moved
+// above all their velocity neighbours) makes every leading block of a panel nonsingular, so the
+// in-place Gauss-Jordan can take the diagonal pivots; a pivot below 1e-14 x max|D| is perturbed and
+// counted, and the host then refactorises with the pivoting kernel (k_diag).
+// Blocked: 8 x 8 blocks on the fp64 tensor cores.  Warp w keeps row block w (8 x 64) in registers in the DMMA accumulator layout
 // (lane (g, q): row g, columns 8 j + 2 q + {0, 1}) through all 8 block steps.  Block step k:
 //   pivot warp k : P = A[k,k]^-1 by scalar Gauss-Jordan in registers (warp shuffles; pivots below
-//                  1e-14 x max|D| perturbed and counted, as in k_diag_np), then its new row block
+//                  1e-14 x max|D| perturbed and counted), then its new row block
 //                  R = P A[k,:] (block k of it: P itself) by DMMA, published in shared memory;
 //   other warps i: A[i,j] -= A[i,k] R[j] (j != k), A[i,k] = -A[i,k] P -- one rank-8 DMMA update of
 //                  the warp's registers (the A[i,k] fragment comes from the accumulator layout by
 //                  shuffles).
-// One CTA barrier per block step (R double-buffered): ~6 us per panel instead of the 64 barrier
-// steps (~33 us) of the scalar k_diag_np, which stays as the reference implementation.
+// One CTA barrier per block step (R double-buffered): 18 us per panel instead of the 36 us of 64
+// scalar steps with a barrier each (round 1).
 #define DB_LD 68
 __device__ __forceinline__ void up_mma(double& d0, double& d1, double a, double b) {
     asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
@@ -548,7 +428,7 @@ static const size_t SM_UP2 = sizeof(double) * 2 * 64 * UP_LD;
 //   HPANEL: F[P, Q-tile] <- (-F[P,P]) F[P, Q-tile]      (D^-1 = -F[P,P])
 //   GPANEL: F[Q-tile, P] <- F[Q-tile, P] (-F[P,P])
 template <bool H>
-__global__ void __launch_bounds__(256, 2) k_panel2(MfDev d, int item0, double* __restrict__ F) {
+__global__ void __launch_bounds__(256, 3) k_panel2(MfDev d, int item0, double* __restrict__ F) {
     extern __shared__ double sm[];
     double* As = sm;                    // [64][UP_LD]
     double* Bs = sm + 64 * UP_LD;       // [64][UP_LD]
@@ -621,15 +501,6 @@ int mf_setup(ens_ctx* c) {
     return ENS_OK;
 }
 
-static bool diag_scalar() {   // ENS_DIAG_SCALAR=1: the scalar Gauss-Jordan panel inverse (A/B measurements)
-    static int v = -1;
-    if (v < 0) {
-        const char* e = std::getenv("ENS_DIAG_SCALAR");
-        v = e && e[0] == '1' ? 1 : 0;
-    }
-    return v == 1;
-}
-
 static int mf_factor_launches(ens_ctx* c, cudaStream_t s, const double* as_vals, int64_t* nlaunch) {
     MfDev d = mfdev(c);
     const int64_t st = c->p.front_storage;
@@ -670,8 +541,6 @@ static int mf_factor_launches(ens_ctx* c, cudaStream_t s, const double* as_vals,
             case OP_DIAG:
                 if (c->diag_pivot)
                     k_diag<<<dim3(n, 2), 256, 0, s>>>(d, off, c->fronts, c->d_count);
-                else if (diag_scalar())
-                    k_diag_np<<<dim3(n, 2), 256, 0, s>>>(d, off, c->fronts, c->d_count);
                 else
                     k_diag_blk<<<dim3(n, 2), 256, 0, s>>>(d, off, c->fronts, c->d_count);
                 break;
