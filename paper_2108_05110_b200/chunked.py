@@ -70,6 +70,8 @@ def plan_chunk(hm, J, device, restart=2, reserve_frac=0.12):
 class ChunkedEngine(Engine):
     """Engine for J local members processed in chunks of Jc columns (see module docstring)."""
 
+    supports_ahead = False   # (no step(then=...): a chunked step is many passes over the chunks)
+
     def __init__(self, disc, config, j0=0, J=None, chunk=None, device=None, comm=None, **opts):
         J = config.num_members if J is None else J
         if chunk is None or chunk < 1 or J % chunk:

@@ -439,6 +439,7 @@ class Engine:
         self._gdata_cache = {}
         self._lru = OrderedDict()        # problem-data objects with cached device data, least recent first
         self._gspec = {}
+        self._spec = None              # pre-solve graph of the announced next step already enqueued (step(then=))
         self.graph_launch_credit = 0   # kernels replayed by step graphs minus kernels captured
 
     def __del__(self):
@@ -512,6 +513,7 @@ class Engine:
         the reference's step reads only v and w (`stepper.py:360-394`); the
         pressures enter here only as part of the initial iterate.
         """
+        self._spec = None
         g = self._staging()
         s = self.stream
         nv = self.nvel
@@ -672,8 +674,16 @@ class Engine:
         with self.on_stream():
             self._compute_means()
 
-    def step(self, t_next, forcing, boundary):
-        """One time-step of all local members; returns the max relative residual."""
+    supports_ahead = True   # step(then=...): see below
+
+    def step(self, t_next, forcing, boundary, then=None):
+        """One time-step of all local members; returns the max relative residual.
+
+        ``then = (t, forcing, boundary)`` announces the call that follows (a time loop knows it): the
+        pre-solve graph of that step (member sums, right-hand sides, assembly -- it only reads the new
+        state and writes work buffers) is enqueued before this call returns, so the host's
+        bookkeeping between two steps (~80 us of Python at C2) no longer leaves the GPU idle.  A next
+        call that differs from the announcement simply redoes the pre-solve work."""
         with self.on_stream():
             if self._graph_ok(forcing, boundary, t_next):
                 failed = None
@@ -694,7 +704,7 @@ class Engine:
                     self._graphs.clear()
                     torch.cuda.synchronize(self.dev)
                     return self._step(t_next, forcing, boundary)
-                return self._step_graphed(t_next, forcing, boundary)
+                return self._step_graphed(t_next, forcing, boundary, then)
             return self._step(t_next, forcing, boundary)
 
     def _ensure_graphs(self, forcing, boundary):
@@ -803,9 +813,12 @@ class Engine:
         self.graph_launch_credit -= n
         return g, n
 
-    def _step_graphs(self, lo, bc):
-        """Graph segments for the current buffer parity: split at the collectives when members are sharded."""
+    def _step_graphs(self, lo, bc, cached_for=None):
+        """Graph segments for the current buffer parity: split at the collectives when members are sharded.
+        ``cached_for``: only look up the segments of that parity (None when not captured yet)."""
         lib, ctx, s = self.lib, self.ctx, self.sptr
+        if cached_for is not None:
+            return self._graphs.get((cached_for, id(lo), id(bc)))
         cur, nxt = self.cur, 1 - self.cur
         key = (cur, id(lo), id(bc))
         segs = self._graphs.get(key)
@@ -851,21 +864,27 @@ class Engine:
         g.replay()
         self.graph_launch_credit += n
 
-    def _step_graphed(self, t_next, forcing, boundary):
+    def _step_graphed(self, t_next, forcing, boundary, then=None):
         lib, ctx, s = self.lib, self.ctx, self.sptr
         cur, nxt = self.cur, 1 - self.cur
         X, Xn = self.X[cur], self.X[nxt]
+        spec, self._spec = self._spec, None
+        ahead = spec is not None and spec == (t_next, id(forcing), id(boundary), cur, self._nstep)
+        if spec is not None and not ahead:
+            self.stream.synchronize()    # the enqueued graph's H2D copies still read the pinned coefficient blocks
         lo = self._gdata(forcing, "loads") if hasattr(forcing, "separable") else None   # None: no body force
         bc = self._gdata(boundary, "bc")
-        if lo is not None:
-            self._gfill(lo, t_next)
-        self._gfill(bc, t_next)
+        if not ahead:
+            if lo is not None:
+                self._gfill(lo, t_next)
+            self._gfill(bc, t_next)
         segs = self._step_graphs(lo, bc)
         self._retire(nxt)          # (a caller's copy of the state about to be overwritten: not step cost)
         self._cost_begin()
         if self.comm is None:
             need = self._need_factor()
-            self._replay(segs["pre"])
+            if not ahead:
+                self._replay(segs["pre"])
         else:
             self._replay(segs["sums"])
             XC.allreduce_member_sums(self.sums, self.comm)
@@ -897,6 +916,9 @@ class Engine:
         if lo is not None:
             self._gprefetch(lo, t_pred)
         self._gprefetch(bc, t_pred)
+        ahead_segs = None
+        if then is not None and self.comm is None and self.refactor != "timed":
+            ahead_segs = self._prepare_ahead(nxt, *then)
         iters = N.I32(0)
         rel = (N.F64 * 2)()
         code = lib.ens_solve_finish(ctx, s, _dptr(self.as_vals), _dptr(self.rhs), _dptr(Xn), self.rtol,
@@ -917,6 +939,17 @@ class Engine:
         self.cur = nxt
         self.means_valid = False
         self.prev_valid = True
+        if then is not None and self.comm is None and self.refactor != "timed":
+            # first thing after the solve: the GPU has only the pressure epilogue left to run
+            if ahead_segs is not None:
+                nsegs, nlo, nbc = ahead_segs
+                if nlo is not None:
+                    self._gfill(nlo, then[0])
+                self._gfill(nbc, then[0])
+                self._replay(nsegs["pre"])
+                self._spec = (then[0], id(then[1]), id(then[2]), self.cur, self._nstep + 1)
+            else:
+                self._enqueue_ahead(*then)
         renew = self._step_done(iters)
         self._nstep += 1
         if self.comm is None:
@@ -925,6 +958,36 @@ class Engine:
         # sharded: this rank's values travel with the next step's MAX exchange (or flush_global)
         self._prev_local = (max(self.last_relres), float(self.last_iters), float(bool(renew)))
         return max(self.last_relres)
+
+    def _prepare_ahead(self, parity, t, forcing, boundary):
+        """While this step's solve runs: the announced next step's graph segments (buffer parity
+        ``parity``) and data entries; None when its graphs are not captured yet."""
+        if not self._graph_ok(forcing, boundary, t):
+            return None
+        lo = self._gdata(forcing, "loads") if hasattr(forcing, "separable") else None
+        bc = self._gdata(boundary, "bc")
+        segs = self._step_graphs(lo, bc, cached_for=parity)
+        if segs is None:
+            return None
+        # (the pinned coefficient blocks are filled after the solve's host round trip: this step's
+        # own pre-solve graph, enqueued but possibly not executed yet, still reads them)
+        return segs, lo, bc
+
+    def _enqueue_ahead(self, t, forcing, boundary):
+        """Enqueue the announced next step's pre-solve graph now (see ``step``)."""
+        if not self._graph_ok(forcing, boundary, t):
+            return
+        try:
+            lo = self._gdata(forcing, "loads") if hasattr(forcing, "separable") else None
+            bc = self._gdata(boundary, "bc")
+            segs = self._step_graphs(lo, bc)     # (this parity's graphs: captured on its first use)
+        except (RuntimeError, N.NativeError):
+            return
+        if lo is not None:
+            self._gfill(lo, t)
+        self._gfill(bc, t)
+        self._replay(segs["pre"])
+        self._spec = (t, id(forcing), id(boundary), self.cur, self._nstep + 1)   # (the step count once this step is booked)
 
     def flush_global(self):
         """Sharded runs: agree on the last step's (residual, iterations, renewal) now instead of in
@@ -981,6 +1044,7 @@ class Engine:
 
     def _step(self, t_next, forcing, boundary):
         lib, ctx, s = self.lib, self.ctx, self.sptr
+        self._spec = None
         cur, nxt = self.cur, 1 - self.cur
         X = self.X[cur]
         self.flush_global()        # sharded: agree on the previous graphed step's values first
@@ -1272,6 +1336,7 @@ class Engine:
         ``rhs_ref`` (reference order): the same factorisation-preconditioned column-batched Krylov
         as the step, converged to ``rtol`` per column.  Returns (x_ref, relres)."""
         J = self.J
+        self._spec = None
         rhs_int = self.block_to_internal(np.asarray(rhs_ref, dtype=float).reshape(self.ntot, J))
         lib, ctx, s = self.lib, self.ctx, self.sptr
         with self.on_stream():
@@ -1291,6 +1356,7 @@ class Engine:
 
     # raw access for tests
     def spmm(self, x, b=None, mode=0, out=None):
+        self._spec = None
         out = torch.empty_like(x) if out is None else out
         with self.on_stream():
             N.check(self.lib.ens_spmm(self.ctx, self.sptr, _dptr(self.as_vals), _dptr(x),
@@ -1298,11 +1364,13 @@ class Engine:
         return out
 
     def factor(self):
+        self._spec = None
         with self.on_stream():
             self._factor()
         return self.last_pert
 
     def precond(self, r, out=None):
+        self._spec = None
         out = torch.zeros_like(r) if out is None else out
         with self.on_stream():
             N.check(self.lib.ens_precond_apply(self.ctx, self.sptr, _dptr(r), _dptr(out)), "ens_precond_apply")

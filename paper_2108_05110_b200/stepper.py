@@ -177,10 +177,13 @@ def _device_state_of(state, engine):
     return ds if (ds is not None and ds.engine is engine and ds.valid and ds.buf == engine.cur) else None
 
 
-def _step(engine, state, config, forcing, boundary):
+def _step(engine, state, config, forcing, boundary, announce=False):
     t_next = state.time + config.dt
     try:
-        residual = engine.step(t_next, forcing, boundary)
+        if announce:    # a time loop knows its next call: the engine enqueues that step's pre-solve work ahead
+            residual = engine.step(t_next, forcing, boundary, then=(t_next + config.dt, forcing, boundary))
+        else:
+            residual = engine.step(t_next, forcing, boundary)
     except N.NativeError as exc:
         # which sub-step failed: the one whose residual is above tolerance (V first)
         kind = StepKind.W_STEP if engine.last_relres[0] <= engine.rtol else StepKind.V_STEP
@@ -411,7 +414,8 @@ def run(config: EnsembleConfig, problem: Problem, observer=None, snapshot_steps=
     n0 = engine._nstep
     for n in range(m):
         tic = _time.perf_counter()
-        state, res = _step(engine, state, config, problem.forcing, problem.boundary)
+        state, res = _step(engine, state, config, problem.forcing, problem.boundary,
+                           announce=n + 1 < m and getattr(engine, "supports_ahead", False))
         report.wall_clock[n + 1] = _time.perf_counter() - tic
         report.residuals[n + 1] = res
         if exact is not None:

@@ -425,3 +425,29 @@ def test_engine_reuse_with_new_problem_objects(monkeypatch):
     torch.cuda.synchronize()
     v_eager = eng.fields_to_host(eng.cur)["v"]
     assert np.array_equal(s_graph.v, v_eager)
+
+
+def test_announced_steps_bitwise_equal_plain():
+    """step(then=...) enqueues the announced next step's pre-solve graph ahead; a run that announces
+    every step, one that never does and one whose announcements are all wrong (different time: the
+    enqueued work is redone) end in bitwise identical states."""
+    outs = []
+    for mode in ("plain", "announced", "wrong"):
+        disc, cfg, prob = P.build_case("C1", steps=8)
+        eng = Engine(disc, cfg)
+        eng.load_state(prob.initial_v, prob.initial_w, None, None)
+        t = 0.0
+        for i in range(8):
+            t += cfg.dt
+            if mode == "plain":
+                eng.step(t, prob.forcing, prob.boundary)
+            elif mode == "announced":
+                eng.step(t, prob.forcing, prob.boundary, then=(t + cfg.dt, prob.forcing, prob.boundary))
+            else:
+                eng.step(t, prob.forcing, prob.boundary, then=(t + 0.5 * cfg.dt, prob.forcing, prob.boundary))
+            if i == 4:
+                eng.diagnostics()       # (work between two steps must not disturb the enqueued graph)
+        outs.append(eng.X[eng.cur].clone())
+        eng.release()
+    assert torch.equal(outs[0], outs[1])
+    assert torch.equal(outs[0], outs[2])

@@ -31,7 +31,7 @@ torch.cuda.synchronize()
 with profile(activities=[ProfilerActivity.CUDA, ProfilerActivity.CPU]) as prof:
     for _ in range(n):
         t += cfg.dt
-        eng.step(t, prob.forcing, prob.boundary)
+        eng.step(t, prob.forcing, prob.boundary, then=(t + cfg.dt, prob.forcing, prob.boundary))
     torch.cuda.synchronize()
 path = os.environ.get("TRACE", "gpurun_out/step_trace.json")
 prof.export_chrome_trace(path)
