@@ -94,6 +94,8 @@ int ens_create(const ens_mesh_desc* mesh, const ens_plan_desc* plan, int device,
         ens_destroy(c);
         return ENS_ENOMEM;
     }
+    cudaMemset(c->d_count, 0, 16);   // [0] active columns / pivot count, [2] solve round-trip sequence number
+    c->h_count[0] = c->h_count[1] = c->h_count[2] = c->h_count[3] = 0;
     int rc = ens_upload_tables();
     if (rc == ENS_OK) rc = mf_setup(c);
     if (rc != ENS_OK) {

@@ -53,6 +53,7 @@ struct ens_ctx {
     int32_t kry_short = 0;         // cycle shortened for lack of device memory
     int32_t gm_total_it = 0;       // iterations of a begun solve (ens_solve_begin / _finish)
     int32_t gm_predict = 0;
+    int32_t gm_seq = 0;            // last round-trip sequence number seen in h_count[2]
     int32_t krylov_first = -1;     // 1 (default): Richardson first cycle; 0: FGMRES (ENS_KRYLOV_FIRST)
     size_t kry_bytes = 0;
     double* red_part = nullptr;    // reduction partials

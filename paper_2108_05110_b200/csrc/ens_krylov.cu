@@ -95,6 +95,28 @@ __global__ void k_gm_init(GmresCol* cols, const double* bn2, const double* rn2, 
     g.g[0] = beta;
     scale[c] = g.active ? 1.0 / beta : 0.0;
     if (g.active) atomicAdd(count, 1);
+    if (c == 0) count[2] += 1;   // sequence number of the round trip (ens_solve_finish polls it in pinned memory)
+}
+
+// Host side of a begun solve's round trip: spin on the sequence word the D2H copy of the counters
+// carries (pinned memory); the stream is only queried now and then to notice a failed launch.
+static int wait_round_trip(ens_ctx* c, cudaStream_t s) {
+    volatile int32_t* hc = c->h_count;
+    for (unsigned long spins = 1;; ++spins) {
+        if (hc[2] != c->gm_seq) break;
+        if ((spins & 0xfff) == 0) {
+            const cudaError_t q = cudaStreamQuery(s);
+            if (q == cudaSuccess) {
+                if (hc[2] != c->gm_seq) break;
+                ens_set_error("solve finish: no begun solve on this stream", __FILE__, __LINE__);
+                return ENS_EINVAL;
+            }
+            if (q != cudaErrorNotReady) ENS_CK(q);
+        }
+    }
+    __sync_synchronize();
+    c->gm_seq = hc[2];
+    return ENS_OK;
 }
 
 // dst = src * scale[col]
@@ -327,8 +349,10 @@ int gmres_solve(ens_ctx* c, cudaStream_t s, const double* as_vals, const double*
         }
         int active = 1;
         if (resume) {
-            // the begin phase left the count and the norms on their way to pinned memory
-            ENS_CK(cudaStreamSynchronize(s));
+            // the begin phase left the norms and the count on their way to pinned memory: wait for the
+            // count's sequence word, not for the stream -- the caller may already have enqueued the
+            // next step's pre-solve work behind this solve
+            RET(wait_round_trip(c, s));
             active = *c->h_count;
             resume = false;
         } else {
@@ -343,14 +367,16 @@ int gmres_solve(ens_ctx* c, cudaStream_t s, const double* as_vals, const double*
             ENS_CKL();
             if (!blind) {
                 // one round trip: active-column count and the residual norms
-                ENS_CK(cudaMemcpyAsync(c->h_count, c->d_count, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+                // (the norms first: the count's sequence word tells the host that both have landed)
                 ENS_CK(cudaMemcpyAsync(c->h_small, kb.bn2, sizeof(double) * 2 * n, cudaMemcpyDeviceToHost, s));
+                ENS_CK(cudaMemcpyAsync(c->h_count, c->d_count, 3 * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
                 if (phase == 1) {
                     c->gm_total_it = total_it;
                     c->gm_predict = predict;
                     return ENS_OK;
                 }
                 ENS_CK(cudaStreamSynchronize(s));
+                c->gm_seq = c->h_count[2];
                 active = *c->h_count;
             }
         }

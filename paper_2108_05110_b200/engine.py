@@ -406,22 +406,22 @@ class Engine:
         self.gen = [0, 0]
         self.live = [None, None]
         self.cur = 0
-        self.rhs = torch.zeros(2, ntot, J, **f64)
-        self.sums = torch.zeros(2 * nvel, **f64)
-        self.means = torch.zeros(2 * nvel, **f64)
+        # per-step work buffers (right-hand sides, member sums / means, eddy maxima, assembled A_s
+        # values): one set, or -- once a time loop announces its steps (step(then=...)) -- one per
+        # state-buffer parity, so that the next step's pre-solve graph can be enqueued while this
+        # step's solve may still need its own right-hand sides and matrix values (_enable_ahead)
+        self._f64 = f64
+        self._wb = [self._work_set(), None]
         self.means_valid = False
-        # eddy maxima of both families, plus a 3-double tail on which the sharded step sends the
-        # previous step's (residual, iterations, renewal flag) through the same MAX exchange
-        self.maxsq_ext = torch.zeros(2 * self.nt * 7 + 3, **f64)
-        self.maxsq = self.maxsq_ext[:2 * self.nt * 7].view(2, self.nt, 7)
-        self._tail = self.maxsq_ext[2 * self.nt * 7:]
+        # (eddy maxima of both families, plus a 3-double tail on which the sharded step sends the
+        # previous step's (residual, iterations, renewal flag) through the same MAX exchange)
+        self._tail = self._wb[0]["maxsq_ext"][2 * self.nt * 7:]
         self._tail_in = torch.zeros(3, dtype=torch.float64, pin_memory=True)
         self._tail_out = torch.zeros(3, dtype=torch.float64, pin_memory=True)
         self._tail_ev = torch.cuda.Event()
         self._prev_local = None        # (residual, iterations, renew) of the last step, this rank
         self._nstep = 0
         self.global_residuals = {}     # engine step index -> residual max over ranks (sharded runs)
-        self.as_vals = torch.zeros(2, hm.nnz_s, **f64)
         self.diag_out = torch.zeros(2 + 6 * J, **f64)
         # a dedicated (non-default) stream: the factorisation and solve sequences
         # are captured once into CUDA graphs, which needs a capturable stream
@@ -440,7 +440,35 @@ class Engine:
         self._lru = OrderedDict()        # problem-data objects with cached device data, least recent first
         self._gspec = {}
         self._spec = None              # pre-solve graph of the announced next step already enqueued (step(then=))
+        self._ones = 0                 # consecutive steps whose solve converged in its first cycle
         self.graph_launch_credit = 0   # kernels replayed by step graphs minus kernels captured
+
+    def _work_set(self):
+        f64, J = self._f64, self.J
+        return dict(rhs=torch.zeros(2, self.ntot, J, **f64), sums=torch.zeros(2 * self.nvel, **f64),
+                    means=torch.zeros(2 * self.nvel, **f64), maxsq_ext=torch.zeros(2 * self.nt * 7 + 3, **f64),
+                    as_vals=torch.zeros(2, self.hm.nnz_s, **f64))
+
+    def _wset(self):
+        w = self._wb[self.cur]
+        return w if w is not None else self._wb[0]
+
+    rhs = property(lambda self: self._wset()["rhs"])
+    sums = property(lambda self: self._wset()["sums"])
+    means = property(lambda self: self._wset()["means"])
+    maxsq_ext = property(lambda self: self._wset()["maxsq_ext"])
+    as_vals = property(lambda self: self._wset()["as_vals"])
+    maxsq = property(lambda self: self._wset()["maxsq_ext"][:2 * self.nt * 7].view(2, self.nt, 7))
+
+    def _enable_ahead(self):
+        """Second work-buffer set (and per-parity data blocks / step graphs) for announced steps."""
+        torch.cuda.synchronize(self.dev)
+        self._wb[1] = self._work_set()
+        for k, v in self._wb[0].items():
+            self._wb[1][k].copy_(v)
+        self._graphs.clear()
+        self._gdata_cache.clear()
+        self._gspec.clear()
 
     def __del__(self):
         try:
@@ -731,14 +759,15 @@ class Engine:
         lv, lw = forcing.loads(t, self.disc, self.config)
         return lv is None and lw is None
 
-    def _gdata(self, obj, kind):
+    def _gdata(self, obj, kind, parity=None):
         """(coefficient function, pinned host and device coefficient blocks, fixed DataDesc) of one data kind."""
         self._touch(obj)
-        key = (kind, id(obj))
+        par = self.cur if (parity is None and self._wb[1] is not None) else (parity or 0)
+        key = (kind, id(obj), par)       # (pinned / device coefficient blocks per parity once steps run ahead)
         ent = self._gdata_cache.get(key)
         if ent is None:
             self._data(obj, kind, 0.0)                   # builds the device basis once
-            sep, basis_t = self._data_cache[key][:2]
+            sep, basis_t = self._data_cache[(kind, id(obj))][:2]
             K = basis_t.shape[0]
             pin = torch.zeros(2, K, self.J, dtype=torch.float64, pin_memory=True)
             dev = torch.zeros(2, K, self.J, dtype=torch.float64, device=self.dev)
@@ -780,9 +809,10 @@ class Engine:
             torch.cuda.synchronize(self.dev)
             self.lib.ens_destroy(self.ctx)
             self.ctx = None
-        for name in ("X", "Pq", "rhs", "as_vals", "mesh_t", "plan_t", "_stg"):
+        for name in ("X", "Pq", "mesh_t", "plan_t", "_stg"):
             if hasattr(self, name):
                 setattr(self, name, None)
+        self._wb = [None, None]
 
     def _gcoef(self, ent, t):
         sep = ent[0]
@@ -866,6 +896,8 @@ class Engine:
 
     def _step_graphed(self, t_next, forcing, boundary, then=None):
         lib, ctx, s = self.lib, self.ctx, self.sptr
+        if then is not None and self.comm is None and self.refactor != "timed" and self._wb[1] is None:
+            self._enable_ahead()         # first announced step: work buffers and data blocks per parity
         cur, nxt = self.cur, 1 - self.cur
         X, Xn = self.X[cur], self.X[nxt]
         spec, self._spec = self._spec, None
@@ -912,13 +944,24 @@ class Engine:
         else:
             self.since_factor += 1
         self._replay(segs["solve"])
-        t_pred = t_next + self.config.dt                  # host work overlapped with the solve
-        if lo is not None:
-            self._gprefetch(lo, t_pred)
-        self._gprefetch(bc, t_pred)
-        ahead_segs = None
+        if then is None:
+            t_pred = t_next + self.config.dt              # host work overlapped with the solve
+            if lo is not None:
+                self._gprefetch(lo, t_pred)
+            self._gprefetch(bc, t_pred)
+        ahead_segs, early = None, False
         if then is not None and self.comm is None and self.refactor != "timed":
             ahead_segs = self._prepare_ahead(nxt, *then)
+            if ahead_segs is not None and self._ones >= 4 and self._wb[1] is not None:
+                # the last four solves converged in their first cycle: expect the same and enqueue the announced
+                # step's pre-solve graph behind this solve right away (it works on the other parity's
+                # buffers; if this solve does need more cycles, that work is simply redone)
+                nsegs, nlo, nbc = ahead_segs
+                if nlo is not None:
+                    self._gfill(nlo, then[0])
+                self._gfill(nbc, then[0])
+                self._replay(nsegs["pre"])
+                early = True
         iters = N.I32(0)
         rel = (N.F64 * 2)()
         code = lib.ens_solve_finish(ctx, s, _dptr(self.as_vals), _dptr(self.rhs), _dptr(Xn), self.rtol,
@@ -932,6 +975,7 @@ class Engine:
             iters += iters2
             redo = True
         self.last_iters, self.last_relres = iters, rel
+        self._ones = self._ones + 1 if iters == 1 else 0
         N.check(code, "ens_solve_finish")
         if redo:
             N.check(lib.ens_epilogue(ctx, s, _dptr(Xn), _dptr(self.Pq[nxt])), "ens_epilogue")
@@ -939,7 +983,11 @@ class Engine:
         self.cur = nxt
         self.means_valid = False
         self.prev_valid = True
-        if then is not None and self.comm is None and self.refactor != "timed":
+        if early:
+            # (this solve needed more cycles after all: the work enqueued ahead read an unfinished
+            # state and is redone -- after a stream synchronisation, as for any stale announcement)
+            self._spec = (then[0], id(then[1]), id(then[2]), self.cur, self._nstep + 1) if not redo else ("stale",)
+        elif then is not None and self.comm is None and self.refactor != "timed":
             # first thing after the solve: the GPU has only the pressure epilogue left to run
             if ahead_segs is not None:
                 nsegs, nlo, nbc = ahead_segs
@@ -964,8 +1012,8 @@ class Engine:
         ``parity``) and data entries; None when its graphs are not captured yet."""
         if not self._graph_ok(forcing, boundary, t):
             return None
-        lo = self._gdata(forcing, "loads") if hasattr(forcing, "separable") else None
-        bc = self._gdata(boundary, "bc")
+        lo = self._gdata(forcing, "loads", parity) if hasattr(forcing, "separable") else None
+        bc = self._gdata(boundary, "bc", parity)
         segs = self._step_graphs(lo, bc, cached_for=parity)
         if segs is None:
             return None

@@ -18,12 +18,12 @@ eng.load_state(prob.initial_v, prob.initial_w, None, None)
 t = 0.0
 for _ in range(6):
     t += cfg.dt
-    eng.step(t, prob.forcing, prob.boundary)
+    eng.step(t, prob.forcing, prob.boundary, then=(t + cfg.dt, prob.forcing, prob.boundary))
 torch.cuda.synchronize()
 with profile(activities=[ProfilerActivity.CUDA]) as prof:
     for _ in range(n):
         t += cfg.dt
-        eng.step(t, prob.forcing, prob.boundary)
+        eng.step(t, prob.forcing, prob.boundary, then=(t + cfg.dt, prob.forcing, prob.boundary))
     torch.cuda.synchronize()
 agg = defaultdict(lambda: [0, 0.0])
 tot = 0.0
