@@ -115,10 +115,12 @@ void ens_destroy(ens_ctx* c) {
     cudaFree(c->red_out);
     cudaFree(c->cols);
     cudaFree(c->d_count);
+    cudaFree(c->colpanel);
     if (c->h_count) cudaFreeHost(c->h_count);
     if (c->h_small) cudaFreeHost(c->h_small);
     if (c->g_solve) cudaGraphExecDestroy((cudaGraphExec_t)c->g_solve);
     if (c->g_factor) cudaGraphExecDestroy((cudaGraphExec_t)c->g_factor);
+    if (c->g_factor_alt) cudaGraphExecDestroy((cudaGraphExec_t)c->g_factor_alt);
     cudaFree(c->solve_io);
     cudaFree(c->partial);
     cudaFree(c->ticket);

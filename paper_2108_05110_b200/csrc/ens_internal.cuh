@@ -60,6 +60,8 @@ struct ens_ctx {
     double* red_out = nullptr;     // small outputs
     GmresCol* cols = nullptr;      // nmat*J
     int32_t* d_count = nullptr;    // device counters
+    double* colpanel = nullptr;    // factorisation: unscaled column panels of the current panel step (per level)
+    int64_t colpanel_rows = 0;
     int32_t* h_count = nullptr;    // pinned
     double* h_small = nullptr;     // pinned
     size_t ws_bytes = 0;
@@ -98,6 +100,9 @@ struct ens_ctx {
     int64_t g_solve_kernels = 0;
     void* g_factor = nullptr;      // cudaGraphExec_t
     const double* g_factor_key = nullptr;
+    void* g_factor_alt = nullptr;  // the graph of the other value buffer (announced steps: one per parity)
+    const double* g_factor_key_alt = nullptr;
+    int g_factor_pivot_alt = 0;
     int diag_pivot = 0;            // 1: in-panel partial pivoting in DIAG (k_diag), 0: k_diag_np
     int spmm_wide = -1;            // wide-member SpMM variant (ENS_SPMM_WIDE, read on first use)
     int g_factor_pivot = 0;

@@ -15,6 +15,8 @@
 //   forward  fr[C] -= F[C,P] fr[P]             backward  x[P] = -[F[P,P] F[P,C]] [fr[P]; x[C]]
 #include <cmath>
 #include <cstdlib>
+#include <vector>
+#include <algorithm>
 
 #include "ens_internal.cuh"
 
@@ -355,12 +357,17 @@ __global__ void __launch_bounds__(256) k_diag_blk(MfDev d, int item0, double* __
 // C += (-A) B with mma.sync m8n8k4 (warp w: rows 8w..8w+7, all 8 column tiles)
 // and C is stored straight from the fragments.
 #define UP_LD 68   // = 4 (mod 16) doubles: conflict-free m8n8k4 fragment reads
+__device__ __forceinline__ void up_cp16(double* sdst, const double* g, bool pred) {
+    const unsigned sa = (unsigned)__cvta_generic_to_shared(sdst);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(sa), "l"(g), "r"(pred ? 16 : 0));
+}
 __device__ __forceinline__ void up_cp8(double* sdst, const double* g, bool pred) {
     const unsigned sa = (unsigned)__cvta_generic_to_shared(sdst);
     asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(sa), "l"(g), "r"(pred ? 8 : 0));
 }
 
-__global__ void __launch_bounds__(256, 3) k_update2(MfDev d, int item0, double* __restrict__ F) {
+__global__ void __launch_bounds__(256, 3) k_update2(MfDev d, int item0, double* __restrict__ F,
+                                                    const double* __restrict__ colp, int f0, int64_t prow) {
     extern __shared__ double sm[];
     double* As = sm;                    // [64 rows][UP_LD]   A[r][k]
     double* Bs = sm + 64 * UP_LD;       // [64 k][UP_LD]      B[k][c]
@@ -372,13 +379,16 @@ __global__ void __launch_bounds__(256, 3) k_update2(MfDev d, int item0, double* 
     const int t = m - pw;
     const int nr = min(ENS_TILE, t - r0), nc = min(ENS_TILE, t - c0);
     double* base = F + (int64_t)mat * d.storage + d.off[f];
+    // A = the UNSCALED column panel F[Q-rows, P], saved row by row (64 doubles, zero past the panel
+    // width) by the panel kernel before it scaled the panel in place
+    const double* ap0 = colp + ((int64_t)mat * prow + (d.idx_off[f] - d.idx_off[f0]) + r0) * ENS_PW;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, g = lane >> 2, q = lane & 3;
     // (1) operands -> shared memory (one commit group); row r = e >> 6, inner kk = e & 63
 #pragma unroll
-    for (int i = 0; i < 16; ++i) {
-        const int e = tid + 256 * i, r = e >> 6, kk = e & 63;
-        const bool ok = r < nr && kk < pw;
-        up_cp8(&As[r * UP_LD + kk], ok ? base + (int64_t)outside(r0 + r, a, pw) * m + a + kk : base, ok);
+    for (int i = 0; i < 8; ++i) {
+        const int e = tid + 256 * i, r = e >> 5, kk = (e & 31) * 2;
+        const bool ok = r < nr;
+        up_cp16(&As[r * UP_LD + kk], ok ? ap0 + (int64_t)r * ENS_PW + kk : colp, ok);
     }
 #pragma unroll
     for (int i = 0; i < 16; ++i) {
@@ -423,16 +433,19 @@ __global__ void __launch_bounds__(256, 3) k_update2(MfDev d, int item0, double* 
 }
 static const size_t SM_UP2 = sizeof(double) * 2 * 64 * UP_LD;
 
-// HPANEL / GPANEL with the same staging + tensor-core pattern (in place: the
-// operand being overwritten is staged completely before any store).
+// HPANEL and GPANEL in one launch (same staging + tensor-core pattern as the update; in place: the
+// operand being overwritten is staged completely before any store).  Blocks [0, nH) scale a tile of
+// the row panel, the rest a tile of the column panel:
 //   HPANEL: F[P, Q-tile] <- (-F[P,P]) F[P, Q-tile]      (D^-1 = -F[P,P])
-//   GPANEL: F[Q-tile, P] <- F[Q-tile, P] (-F[P,P])
-template <bool H>
-__global__ void __launch_bounds__(256, 3) k_panel2(MfDev d, int item0, double* __restrict__ F) {
+//   GPANEL: F[Q-tile, P] <- F[Q-tile, P] (-F[P,P])      and the UNSCALED tile is saved to colp for
+//           the update, which follows (round 1 ran GPANEL as a fourth launch after the update)
+__global__ void __launch_bounds__(256, 3) k_panel_hg(MfDev d, int offH, int nH, int offG, double* __restrict__ F,
+                                                     double* __restrict__ colp, int f0, int64_t prow) {
     extern __shared__ double sm[];
     double* As = sm;                    // [64][UP_LD]
     double* Bs = sm + 64 * UP_LD;       // [64][UP_LD]
-    const int* it = d.work + 4LL * (item0 + blockIdx.x);
+    const bool H = (int)blockIdx.x < nH;
+    const int* it = d.work + 4LL * (H ? offH + blockIdx.x : offG + (blockIdx.x - nH));
     const int f = it[0], a = it[1], x0 = it[2];
     const int mat = blockIdx.y;
     const int m = d.m[f];
@@ -458,6 +471,16 @@ __global__ void __launch_bounds__(256, 3) k_panel2(MfDev d, int item0, double* _
     asm volatile("cp.async.commit_group;\n" ::);
     asm volatile("cp.async.wait_group 0;\n" ::);
     __syncthreads();
+    if (!H) {   // the unscaled tile, row by row (zero past the panel width), for the update
+        double* cp = colp + ((int64_t)mat * prow + (d.idx_off[f] - d.idx_off[f0]) + x0) * ENS_PW;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            const int e = tid + 256 * i, r = e >> 5, cc = (e & 31) * 2;
+            if (r < nx)
+                *reinterpret_cast<double2*>(cp + (int64_t)r * ENS_PW + cc) =
+                    make_double2(As[r * UP_LD + cc], As[r * UP_LD + cc + 1]);
+        }
+    }
     const int row = 8 * warp + g;
     const double* ap = As + row * UP_LD + q;
     const double* bp = Bs + q * UP_LD + g;
@@ -496,8 +519,7 @@ __global__ void __launch_bounds__(256, 3) k_panel2(MfDev d, int item0, double* _
 int mf_setup(ens_ctx* c) {
     (void)c;
     ENS_CK(cudaFuncSetAttribute(k_update2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SM_UP2));
-    ENS_CK(cudaFuncSetAttribute(k_panel2<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SM_UP2));
-    ENS_CK(cudaFuncSetAttribute(k_panel2<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SM_UP2));
+    ENS_CK(cudaFuncSetAttribute(k_panel_hg, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SM_UP2));
     return ENS_OK;
 }
 
@@ -507,6 +529,7 @@ static int mf_factor_launches(ens_ctx* c, cudaStream_t s, const double* as_vals,
     int64_t cnt = 0;
     ENS_CK(cudaMemsetAsync(c->d_count, 0, sizeof(int32_t), s));
     const int64_t nrow = (int64_t)c->sched_factor.size() / 5;
+    std::vector<char> done((size_t)nrow, 0);
     bool zeroed = false;
     for (int64_t i = 0; i < nrow; ++i) {
         const int64_t* r = &c->sched_factor[5 * i];
@@ -544,15 +567,29 @@ static int mf_factor_launches(ens_ctx* c, cudaStream_t s, const double* as_vals,
                 else
                     k_diag_blk<<<dim3(n, 2), 256, 0, s>>>(d, off, c->fronts, c->d_count);
                 break;
-            case OP_HPANEL:
-                k_panel2<true><<<dim3(n, 2), 256, SM_UP2, s>>>(d, off, c->fronts);
+            case OP_HPANEL: {
+                // the panel step's GPANEL row (scheduled after the update in the plan) runs in the same
+                // launch: the update reads the unscaled column panel from colp instead
+                int64_t j = i + 1;
+                while (j < nrow && !((int)c->sched_factor[5 * j] == OP_GPANEL && (int)c->sched_factor[5 * j + 1] == L)) ++j;
+                if (j >= nrow) {
+                    ens_set_error("factor schedule: HPANEL without its GPANEL", __FILE__, __LINE__);
+                    return ENS_EINVAL;
+                }
+                const int offG = (int)c->sched_factor[5 * j + 2], nG = (int)c->sched_factor[5 * j + 3];
+                done[j] = 1;
+                k_panel_hg<<<dim3(n + nG, 2), 256, SM_UP2, s>>>(d, off, n, offG, c->fronts, c->colpanel,
+                                                              c->level_front_off[L], c->colpanel_rows);
                 break;
+            }
             case OP_UPDATE:
-                k_update2<<<dim3(n, 2), 256, SM_UP2, s>>>(d, off, c->fronts);
+                k_update2<<<dim3(n, 2), 256, SM_UP2, s>>>(d, off, c->fronts, c->colpanel, c->level_front_off[L],
+                                                          c->colpanel_rows);
                 break;
             case OP_GPANEL:
-                k_panel2<false><<<dim3(n, 2), 256, SM_UP2, s>>>(d, off, c->fronts);
-                break;
+                if (done[i]) continue;   // (ran with its HPANEL)
+                ens_set_error("factor schedule: GPANEL without an HPANEL before it", __FILE__, __LINE__);
+                return ENS_EINVAL;
             default:
                 ens_set_error("bad factor op", __FILE__, __LINE__);
                 return ENS_EINVAL;
@@ -576,6 +613,24 @@ int mf_factor(ens_ctx* c, cudaStream_t s, const double* as_vals, int32_t* n_pert
         const int rc = mf_stream_prepare(c);   // allocations happen outside any graph capture
         if (rc != ENS_OK) return rc;
     }
+    if (!c->colpanel) {
+        // unscaled column panels of one panel step of one level: a row of ENS_PW doubles per front row
+        const int nf = (int)c->p.nfront;
+        std::vector<int64_t> io((size_t)nf + 1);
+        ENS_CK(cudaMemcpy(io.data(), c->p.f_idx_off, sizeof(int64_t) * (nf + 1), cudaMemcpyDeviceToHost));
+        int64_t rows = 1;
+        for (size_t L = 0; L + 1 < c->level_front_off.size(); ++L)
+            rows = std::max(rows, io[c->level_front_off[L + 1]] - io[c->level_front_off[L]]);
+        const size_t bytes = sizeof(double) * 2 * (size_t)rows * ENS_PW;
+        if (cudaMalloc(&c->colpanel, bytes) != cudaSuccess) {
+            cudaGetLastError();
+            ens_set_error("out of device memory for the factorisation's column panels", __FILE__, __LINE__);
+            return ENS_ENOMEM;
+        }
+        ENS_CK(cudaMemset(c->colpanel, 0, bytes));
+        c->colpanel_rows = rows;
+        c->ws_bytes += bytes;
+    }
     const char* e = std::getenv("ENS_NO_GRAPH");
     const bool graphs = !(e && e[0] == '1') && s != 0;
     if (!graphs) {
@@ -583,9 +638,16 @@ int mf_factor(ens_ctx* c, cudaStream_t s, const double* as_vals, int32_t* n_pert
         const int rc = mf_factor_launches(c, s, as_vals, &n);
         if (rc != ENS_OK) return rc;
     } else {
+        // two cached graphs: time loops that announce their steps keep two sets of assembled values
+        // (one per state-buffer parity), and the graph is bound to the value buffer it was captured on
         if (c->g_factor && (c->g_factor_key != as_vals || c->g_factor_pivot != c->diag_pivot)) {
-            cudaGraphExecDestroy((cudaGraphExec_t)c->g_factor);
-            c->g_factor = nullptr;
+            std::swap(c->g_factor, c->g_factor_alt);
+            std::swap(c->g_factor_key, c->g_factor_key_alt);
+            std::swap(c->g_factor_pivot, c->g_factor_pivot_alt);
+            if (c->g_factor && (c->g_factor_key != as_vals || c->g_factor_pivot != c->diag_pivot)) {
+                cudaGraphExecDestroy((cudaGraphExec_t)c->g_factor);
+                c->g_factor = nullptr;
+            }
         }
         if (!c->g_factor) {
             cudaGraph_t g;
