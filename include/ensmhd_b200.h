@@ -227,6 +227,18 @@ int  ens_diagnostics(ens_ctx* ctx, void* stream, const double* x, const double* 
  * L2(0,T;H1) error norm of experiments.error_norm_21 (experiments.py:59-73, fem.py:502-505). */
 int  ens_mean_error(ens_ctx* ctx, void* stream, const double* means, const ens_data_desc* exact, double* out);
 
+/* State layout conversion on the device (the EnsembleState arrays of ensemble.py:183-190 cross
+ * PCIe in the reference's own layout; this replaces the reference's host-side array views):
+ *   ref: nsys blocks (stride ref_stride doubles) of J member rows of length ld, reference dof
+ *        order (the (J, n) arrays v, w or q, r), in device memory;
+ *   x:   nsys internal member-minor blocks (stride x_stride doubles), x[row[c] * J + j];
+ *   row[c] (device, int64): internal row of reference dof c, c in [0, n).
+ * import: x[s][row[c]][j] = ref[s][j][c];  export: ref[s][j][c] = x[s][row[c]][j]. */
+int  ens_layout_import(ens_ctx* ctx, void* stream, const double* ref, int64_t ld, int64_t ref_stride, int64_t n,
+                       const int64_t* row, double* x, int64_t x_stride, int32_t nsys);
+int  ens_layout_export(ens_ctx* ctx, void* stream, const double* x, int64_t x_stride, int64_t n, const int64_t* row,
+                       double* ref, int64_t ld, int64_t ref_stride, int32_t nsys);
+
 #ifdef __cplusplus
 }
 #endif

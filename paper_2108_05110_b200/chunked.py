@@ -71,6 +71,7 @@ class ChunkedEngine(Engine):
     """Engine for J local members processed in chunks of Jc columns (see module docstring)."""
 
     supports_ahead = False   # (no step(then=...): a chunked step is many passes over the chunks)
+    step_fetch = False       # (no step(fetch=True): states are downloaded chunk by chunk on demand)
 
     def __init__(self, disc, config, j0=0, J=None, chunk=None, device=None, comm=None, **opts):
         J = config.num_members if J is None else J

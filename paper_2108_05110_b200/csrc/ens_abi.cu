@@ -251,4 +251,18 @@ int ens_diagnostics(ens_ctx* c, void* stream, const double* x, const double* mea
     return launch_diagnostics(c, (cudaStream_t)stream, x, means, out);
 }
 
+int ens_layout_import(ens_ctx* c, void* stream, const double* ref, int64_t ld, int64_t ref_stride, int64_t n,
+                      const int64_t* row, double* x, int64_t x_stride, int32_t nsys) {
+    if (!c || !ref || !row || !x || n < 0 || ld < n || nsys < 1) return ENS_EINVAL;
+    return launch_layout(c, (cudaStream_t)stream, true, const_cast<double*>(ref), ld, ref_stride, n, row, x, x_stride,
+                         nsys);
+}
+
+int ens_layout_export(ens_ctx* c, void* stream, const double* x, int64_t x_stride, int64_t n, const int64_t* row,
+                      double* ref, int64_t ld, int64_t ref_stride, int32_t nsys) {
+    if (!c || !ref || !row || !x || n < 0 || ld < n || nsys < 1) return ENS_EINVAL;
+    return launch_layout(c, (cudaStream_t)stream, false, ref, ld, ref_stride, n, row, const_cast<double*>(x), x_stride,
+                         nsys);
+}
+
 }  // extern "C"

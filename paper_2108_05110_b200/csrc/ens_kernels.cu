@@ -1357,3 +1357,60 @@ int launch_diagnostics(ens_ctx* c, cudaStream_t s, const double* x, const double
     ENS_CKL();
     return ENS_OK;
 }
+
+// ---------------------------------------------------------------------------
+// state layout: reference order (member-major (J, n) blocks, reference dof numbering -- the
+// EnsembleState arrays of ensemble.py:183-190) <-> the internal member-minor blocks in
+// nested-dissection dof order.  One tile of LT_C reference dofs x LT_J members per CTA through
+// shared memory: the reference side is read / written in 512-byte runs along the dofs, the
+// internal side in whole member rows.  row[c] = internal row of reference dof c.
+// ---------------------------------------------------------------------------
+constexpr int LT_C = 64, LT_J = 64;
+
+template <bool IMPORT>
+__global__ void __launch_bounds__(256) k_layout(double* __restrict__ ref, int64_t ld, int64_t ref_ms, int64_t n,
+                                                const int64_t* __restrict__ row, double* __restrict__ x,
+                                                int64_t x_ms, int J) {
+    __shared__ double tile[LT_C][LT_J + 1];
+    __shared__ int64_t srow[LT_C];
+    const int64_t c0 = (int64_t)blockIdx.x * LT_C;
+    const int j0 = blockIdx.y * LT_J;
+    const int nc = (int)min((int64_t)LT_C, n - c0), nj = min(LT_J, J - j0);
+    double* R = ref + (int64_t)blockIdx.z * ref_ms;
+    double* X = x + (int64_t)blockIdx.z * x_ms;
+    if (threadIdx.x < nc) srow[threadIdx.x] = row[c0 + threadIdx.x];
+    if (IMPORT) {
+        for (int e = threadIdx.x; e < LT_C * nj; e += 256) {
+            const int cl = e % LT_C, jj = e / LT_C;
+            if (cl < nc) tile[cl][jj] = R[(int64_t)(j0 + jj) * ld + c0 + cl];
+        }
+        __syncthreads();
+        for (int e = threadIdx.x; e < nc * nj; e += 256) {
+            const int cl = e / nj, jj = e - cl * nj;
+            X[srow[cl] * J + j0 + jj] = tile[cl][jj];
+        }
+    } else {
+        __syncthreads();
+        for (int e = threadIdx.x; e < nc * nj; e += 256) {
+            const int cl = e / nj, jj = e - cl * nj;
+            tile[cl][jj] = X[srow[cl] * J + j0 + jj];
+        }
+        __syncthreads();
+        for (int e = threadIdx.x; e < LT_C * nj; e += 256) {
+            const int cl = e % LT_C, jj = e / LT_C;
+            if (cl < nc) R[(int64_t)(j0 + jj) * ld + c0 + cl] = tile[cl][jj];
+        }
+    }
+}
+
+int launch_layout(ens_ctx* c, cudaStream_t s, bool import, double* ref, int64_t ld, int64_t ref_ms, int64_t n,
+                  const int64_t* row, double* x, int64_t x_ms, int nsys) {
+    if (n <= 0) return ENS_OK;
+    dim3 grid((unsigned)((n + LT_C - 1) / LT_C), (unsigned)((c->J + LT_J - 1) / LT_J), (unsigned)nsys);
+    if (import)
+        k_layout<true><<<grid, 256, 0, s>>>(ref, ld, ref_ms, n, row, x, x_ms, c->J);
+    else
+        k_layout<false><<<grid, 256, 0, s>>>(ref, ld, ref_ms, n, row, x, x_ms, c->J);
+    ENS_CKL();
+    return ENS_OK;
+}

@@ -247,6 +247,7 @@ class DeviceState:
         self.gen = gen
         self.num_members = num_members
         self._host = {}
+        self._pending = None      # (pinned tensors, event): a download enqueued by the step itself
 
     @property
     def valid(self):
@@ -260,9 +261,22 @@ class DeviceState:
     def to_host(self, name):
         if name in self._host:
             return self._host[name]
-        if not self.valid:
+        if self._pending is None and not self.valid:
             raise RuntimeError("device state was overwritten before it was read")
-        fields = self.engine.fields_to_host(self.buf)   # all four fields, one sync
+        if self._pending is None and not getattr(self.engine, "step_fetch", False):
+            fields = self.engine.fields_to_host(self.buf)     # (chunked engine: chunk by chunk)
+        else:
+            if self._pending is not None:
+                # enqueued behind the step that produced this state: it holds the state's values even if
+                # the device buffers have been overwritten since
+                (tens, ev), self._pending = self._pending, None
+            else:
+                tens, ev = self.engine._enqueue_fetch(self.buf)   # all four fields, one wait
+            ev.synchronize()
+            fields = {k: t.numpy() for k, t in tens.items()}
+            if self.engine is not None:
+                # (load_state recognises these arrays if the caller passes them straight back in)
+                self.engine._handed = ((self.buf, self.gen), tens)
         for a in fields.values():
             # an EnsembleState is immutable (`ensemble.py:183-190`): a caller editing a returned field in
             # place would otherwise be silently ignored by a device-resident next step
@@ -273,6 +287,11 @@ class DeviceState:
 
 class Engine:
     """Device-resident ensemble on one GPU (member columns [j0, j0+J) of J_total)."""
+
+    step_fetch = True      # step(fetch=True) is supported (the chunked engine downloads on demand)
+    _fetched = None        # (pinned tensors, event, (buffer, generation)) of the last step(fetch=True)
+    _handed = None         # ((buffer, generation), pinned tensors) last handed out as write-protected arrays
+    n_own_uploads = 0      # load_state calls that recognised their own handed-out arrays (no comparison, no sync)
 
     def __init__(self, disc, config, j0=0, J=None, device=None, comm=None, restart=8, max_restarts=20, rtol=1e-12,
                  refactor="adaptive", lag_max_iters=8, lag_max_steps=500, guess="extrapolate"):
@@ -499,6 +518,9 @@ class Engine:
                 ref_of_int_p=torch.as_tensor(hm.ref_of_int[self.nvel:] - self.nvel).to(d),
                 int_of_ref_v=torch.as_tensor(hm.int_id[:self.nvel]).to(d),
                 int_of_ref_p=torch.as_tensor(hm.int_id[self.nvel:] - self.nvel).to(d))
+            # row maps of the layout kernels (ens_layout_import / _export): internal row of each reference dof
+            self._stg["row_v"] = self._stg["int_of_ref_v"].to(torch.int64).contiguous()
+            self._stg["row_p"] = self._stg["int_of_ref_p"].to(torch.int64).contiguous()
         return self._stg
 
     @staticmethod
@@ -545,13 +567,28 @@ class Engine:
         g = self._staging()
         s = self.stream
         nv = self.nvel
+        own = self._own_arrays(v, w)
+        if own is not None:
+            # the caller passes back, unmodified (write-protected views of our pinned buffers), the very
+            # arrays this buffer set was downloaded into: same values by construction.  They are
+            # uploaded and become the resident velocities like any caller's arrays, but nothing has to
+            # be compared, so no host synchronisation: the step's graphs queue up behind the copies.
+            self.n_own_uploads += 1
+            with self.on_stream():
+                g["d_vel"][0].copy_(own["v"], non_blocking=True)
+                g["d_vel"][1].copy_(own["w"], non_blocking=True)
+                N.check(self.lib.ens_layout_import(self.ctx, self.sptr, _dptr(g["d_vel"]), nv, self.J * nv, nv,
+                                                   _dptr(g["row_v"]), _dptr(self.X[self.cur]), self.ntot * self.J,
+                                                   2), "ens_layout_import")
+            return
         has_p = q is not None and np.asarray(q).size > 0
         with torch.cuda.stream(s):
             hv = self._copy_members(g["d_vel"][0], v)
             hw = self._copy_members(g["d_vel"][1], w)
             Xs = g["x_in"]
-            for m in range(2):
-                torch.index_select(g["d_vel"][m].t(), 0, g["ref_of_int_v"], out=Xs[m, :nv])
+            J, nt = self.J, self.ntot
+            N.check(self.lib.ens_layout_import(self.ctx, self.sptr, _dptr(g["d_vel"]), nv, J * nv, nv,
+                                               _dptr(g["row_v"]), _dptr(Xs), nt * J, 2), "ens_layout_import")
             cur = self.cur
             same = self.gen[cur] > 0 and torch.equal(Xs[:, :nv], self.X[cur][:, :nv])
         keep = (hv, hw)
@@ -568,8 +605,10 @@ class Engine:
                 keep = keep + (hq, hr)
                 g["d_pres"][0].copy_(hq, non_blocking=hq.is_pinned())
                 g["d_pres"][1].copy_(hr, non_blocking=hr.is_pinned())
-                for m in range(2):
-                    torch.index_select(g["d_pres"][m].t(), 0, g["ref_of_int_p"], out=Xs[m, nv:])
+                npr = self.npres
+                N.check(self.lib.ens_layout_import(self.ctx, self.sptr, _dptr(g["d_pres"]), npr, J * npr, npr,
+                                                   _dptr(g["row_p"]), _dptr(Xs[0, nv:]), nt * J, 2),
+                        "ens_layout_import")
             else:
                 Xs[:, nv:] = 0.0
         self._retire(cur)
@@ -582,33 +621,53 @@ class Engine:
         self.means_valid = False
         self.prev_valid = False
 
+    def _enqueue_fetch(self, buf):
+        """Enqueue the download of buffer set ``buf``: two layout kernels (internal member-minor
+        blocks -> reference-order (J, n) staging), then four D2H copies straight into freshly
+        allocated pinned buffers.  Returns ({v, w, q, r} pinned tensors, event after the last copy)."""
+        g = self._staging()
+        J, nv, npr, nt = self.J, self.nvel, self.npres, self.ntot
+        out = {}
+        with torch.cuda.stream(self.stream):
+            N.check(self.lib.ens_layout_export(self.ctx, self.sptr, _dptr(self.X[buf]), nt * J, nv, _dptr(g["row_v"]),
+                                               _dptr(g["d_vel"]), nv, J * nv, 2), "ens_layout_export")
+            N.check(self.lib.ens_layout_export(self.ctx, self.sptr, _dptr(self.Pq[buf]), npr * J, npr,
+                                               _dptr(g["row_p"]), _dptr(g["d_pres"]), npr, J * npr, 2),
+                    "ens_layout_export")
+            for m, name in ((0, "v"), (1, "w")):
+                h = torch.empty(J, nv, dtype=torch.float64, pin_memory=True)
+                h.copy_(g["d_vel"][m], non_blocking=True)
+                out[name] = h
+            for m, name in ((0, "q"), (1, "r")):
+                h = torch.empty(J, npr, dtype=torch.float64, pin_memory=True)
+                h.copy_(g["d_pres"][m], non_blocking=True)
+                out[name] = h
+            ev = torch.cuda.Event()
+            ev.record(self.stream)
+        return out, ev
+
+    def _own_arrays(self, v, w):
+        """The pinned tensors behind (v, w) when these are exactly the write-protected arrays handed out
+        for the current buffer set and generation (``DeviceState.to_host``); else None."""
+        h = self._handed
+        if h is None or h[0] != (self.cur, self.gen[self.cur]):
+            return None
+        tens = h[1]
+        for a, t in ((v, tens["v"]), (w, tens["w"])):
+            if not (isinstance(a, np.ndarray) and not a.flags.writeable and a.dtype == np.float64
+                    and a.shape == tuple(t.shape) and a.flags.c_contiguous and a.ctypes.data == t.data_ptr()):
+                return None
+        return tens
+
     def fields_to_host(self, buf):
         """{v, w, q, r}: (J, n) reference-layout numpy arrays of buffer set ``buf``.
 
-        One device transpose per field, D2H straight into freshly allocated
-        pinned buffers (the returned arrays are views of them -- no host copy,
-        and a later upload of the same arrays is a direct DMA), one sync.
+        One layout kernel per field pair (hand-written transpose + dof permutation), D2H straight
+        into freshly allocated pinned buffers (the returned arrays are views of them -- no host
+        copy, and a later upload of the same arrays is a direct DMA), one wait.
         """
-        g = self._staging()
-        s = self.stream
-        J, nv, npr = self.J, self.nvel, self.npres
-        out = {}
-        with torch.cuda.stream(s):
-            for m, name in ((0, "v"), (1, "w")):
-                dst = g["d_vel"][m]
-                torch.index_select(self.X[buf][m, :nv], 0, g["int_of_ref_v"], out=g["t_vel"])
-                dst.copy_(g["t_vel"].t())
-                h = torch.empty(J, nv, dtype=torch.float64, pin_memory=True)
-                h.copy_(dst, non_blocking=True)
-                out[name] = h
-            for m, name in ((0, "q"), (1, "r")):
-                dst = g["d_pres"][m]
-                torch.index_select(self.Pq[buf][m], 0, g["int_of_ref_p"], out=g["t_pres"])
-                dst.copy_(g["t_pres"].t())
-                h = torch.empty(J, npr, dtype=torch.float64, pin_memory=True)
-                h.copy_(dst, non_blocking=True)
-                out[name] = h
-        s.synchronize()
+        out, ev = self._enqueue_fetch(buf)
+        ev.synchronize()
         return {k: t.numpy() for k, t in out.items()}
 
     def field_to_host(self, buf, name):
@@ -618,6 +677,9 @@ class Engine:
     def state_handle(self):
         h = DeviceState(self, self.cur, self.gen[self.cur], self.J)
         self.live[self.cur] = weakref.ref(h)
+        pre, self._fetched = getattr(self, "_fetched", None), None
+        if pre is not None and pre[2] == (self.cur, self.gen[self.cur]):
+            h._pending = pre[:2]          # this state's download is already on its way (step(fetch=True))
         return h
 
     def _retire(self, buf):
@@ -704,14 +766,19 @@ class Engine:
 
     supports_ahead = True   # step(then=...): see below
 
-    def step(self, t_next, forcing, boundary, then=None):
+    def step(self, t_next, forcing, boundary, then=None, fetch=False):
         """One time-step of all local members; returns the max relative residual.
 
         ``then = (t, forcing, boundary)`` announces the call that follows (a time loop knows it): the
         pre-solve graph of that step (member sums, right-hand sides, assembly -- it only reads the new
         state and writes work buffers) is enqueued before this call returns, so the host's
         bookkeeping between two steps (~80 us of Python at C2) no longer leaves the GPU idle.  A next
-        call that differs from the announcement simply redoes the pre-solve work."""
+        call that differs from the announcement simply redoes the pre-solve work.
+
+        ``fetch=True`` (a caller that reads the new state on the host, `advance()` with host arrays
+        in): the download of the new state -- layout kernels and D2H copies into pinned buffers -- is
+        enqueued by the step itself, right behind the solve when the recent solves converged in their
+        first cycle (redone if this one does not), instead of when the first field is read."""
         with self.on_stream():
             if self._graph_ok(forcing, boundary, t_next):
                 failed = None
@@ -731,9 +798,15 @@ class Engine:
                     self.step_graphs = False
                     self._graphs.clear()
                     torch.cuda.synchronize(self.dev)
-                    return self._step(t_next, forcing, boundary)
-                return self._step_graphed(t_next, forcing, boundary, then)
-            return self._step(t_next, forcing, boundary)
+                    return self._eager(t_next, forcing, boundary, fetch)
+                return self._step_graphed(t_next, forcing, boundary, then, fetch)
+            return self._eager(t_next, forcing, boundary, fetch)
+
+    def _eager(self, t_next, forcing, boundary, fetch):
+        res = self._step(t_next, forcing, boundary)
+        if fetch:      # (right behind the finished step; the graphed path enqueues it behind the solve)
+            self._fetched = self._enqueue_fetch(self.cur) + ((self.cur, self.gen[self.cur]),)
+        return res
 
     def _ensure_graphs(self, forcing, boundary):
         """Capture this parity's step graphs; returns True when they were captured now.  No state
@@ -894,7 +967,7 @@ class Engine:
         g.replay()
         self.graph_launch_credit += n
 
-    def _step_graphed(self, t_next, forcing, boundary, then=None):
+    def _step_graphed(self, t_next, forcing, boundary, then=None, fetch=False):
         lib, ctx, s = self.lib, self.ctx, self.sptr
         if then is not None and self.comm is None and self.refactor != "timed" and self._wb[1] is None:
             self._enable_ahead()         # first announced step: work buffers and data blocks per parity
@@ -962,6 +1035,7 @@ class Engine:
                 self._gfill(nbc, then[0])
                 self._replay(nsegs["pre"])
                 early = True
+        pre = self._enqueue_fetch(nxt) if fetch and self._ones >= 4 else None   # (speculative, as above)
         iters = N.I32(0)
         rel = (N.F64 * 2)()
         code = lib.ens_solve_finish(ctx, s, _dptr(self.as_vals), _dptr(self.rhs), _dptr(Xn), self.rtol,
@@ -983,6 +1057,10 @@ class Engine:
         self.cur = nxt
         self.means_valid = False
         self.prev_valid = True
+        if fetch:
+            if pre is None or redo:
+                pre = self._enqueue_fetch(nxt)
+            self._fetched = pre + ((nxt, self.gen[nxt]),)
         if early:
             # (this solve needed more cycles after all: the work enqueued ahead read an unfinished
             # state and is redone -- after a stream synchronisation, as for any stale announcement)

@@ -177,11 +177,13 @@ def _device_state_of(state, engine):
     return ds if (ds is not None and ds.engine is engine and ds.valid and ds.buf == engine.cur) else None
 
 
-def _step(engine, state, config, forcing, boundary, announce=False):
+def _step(engine, state, config, forcing, boundary, announce=False, fetch=False):
     t_next = state.time + config.dt
     try:
         if announce:    # a time loop knows its next call: the engine enqueues that step's pre-solve work ahead
             residual = engine.step(t_next, forcing, boundary, then=(t_next + config.dt, forcing, boundary))
+        elif fetch and getattr(engine, "step_fetch", False):
+            residual = engine.step(t_next, forcing, boundary, fetch=True)   # new state downloaded by the step itself
         else:
             residual = engine.step(t_next, forcing, boundary)
     except N.NativeError as exc:
@@ -201,9 +203,11 @@ def advance(state: EnsembleState, config: EnsembleConfig, disc: Discretization, 
     sub-steps of the true relative residual (`linalg.py:111-118`).
     """
     engine = get_engine(disc, config)
-    if _device_state_of(state, engine) is None:
+    host_in = _device_state_of(state, engine) is None
+    if host_in:
         engine.load_state(state.v, state.w, state.q, state.r)
-    return _step(engine, state, config, forcing, boundary)
+    # a caller that passes host arrays in reads host arrays out: the step enqueues the download itself
+    return _step(engine, state, config, forcing, boundary, fetch=host_in)
 
 
 def energy(state: EnsembleState, disc: Discretization) -> float:

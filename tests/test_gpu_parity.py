@@ -451,3 +451,60 @@ def test_announced_steps_bitwise_equal_plain():
         eng.release()
     assert torch.equal(outs[0], outs[1])
     assert torch.equal(outs[0], outs[2])
+
+
+def test_layout_kernels_match_numpy_permutation(c1, rng):
+    """ens_layout_import / _export (reference-order (J, n) arrays <-> internal member-minor blocks)
+    against the numpy statement of the same permutation, bit for bit, velocities and pressures."""
+    disc, cfg, prob = c1
+    eng = Engine(disc, cfg)
+    hm = host_mesh(disc)
+    J = cfg.num_members
+    v, w = perturbed_state(disc, cfg, rng)
+    q = rng.standard_normal((J, disc.n_pres))
+    r = rng.standard_normal((J, disc.n_pres))
+    eng.load_state(v, w, q, r)
+    torch.cuda.synchronize()
+    X = eng.X[eng.cur].cpu().numpy()
+    for m, (vel, pr) in enumerate(((v, q), (w, r))):
+        ref_blk = np.concatenate([vel, pr], axis=1).T          # (n_total, J) reference rows
+        assert np.array_equal(X[m], to_internal_block(hm, ref_blk))
+    out = eng.fields_to_host(eng.cur)
+    for name, a in (("v", v), ("w", w), ("q", q), ("r", r)):
+        assert np.array_equal(out[name], a), name
+    eng.release()
+
+
+def test_advance_host_arrays_prefetched_download_bitwise():
+    """advance() with host arrays in enqueues the new state's download inside the step
+    (speculatively behind the solve once the recent solves took one cycle); the arrays it hands
+    out are bitwise those of a device-resident run read at the end, and each intermediate state is
+    the one an on-demand download gives."""
+    disc, cfg, prob = P.build_case("C1", steps=8)
+    host = EnsembleState(v=np.asarray(prob.initial_v), w=np.asarray(prob.initial_w),
+                         q=np.zeros((cfg.num_members, disc.n_pres)), r=np.zeros((cfg.num_members, disc.n_pres)))
+    eng = P.stepper.get_engine(disc, cfg)
+    for i in range(8):
+        new, _ = P.advance(host, cfg, disc, prob.forcing, prob.boundary)
+        pend = new.device_state._pending is not None
+        assert pend                                   # the step enqueued this state's download
+        got = {k: np.array(getattr(new, k)) for k in "vwqr"}
+        ondemand = eng.fields_to_host(eng.cur)
+        for k in "vwqr":
+            assert np.array_equal(got[k], ondemand[k]), (i, k)
+        host = EnsembleState(v=new.v, w=new.w, q=new.q, r=new.r, step=new.step, time=new.time)
+    # every call after the first recognised the arrays it had handed out (uploaded, not compared)
+    assert eng.n_own_uploads == 7
+    # a caller's own copy of the same values takes the general path (upload, compare, keep the trajectory)
+    cp = EnsembleState(v=np.array(host.v), w=np.array(host.w), q=np.array(host.q), r=np.array(host.r),
+                       step=host.step, time=host.time)
+    a, _ = P.advance(cp, cfg, disc, prob.forcing, prob.boundary)
+    b, _ = P.advance(host, cfg, disc, prob.forcing, prob.boundary)
+    assert eng.n_own_uploads == 7                      # (host is no longer the resident level)
+    # (b restarts from the uploaded level: equal at the solver tolerance; w = u - B is ~0 in this case)
+    assert rel(b.v, a.v) < 1e-10 and np.linalg.norm(b.w - a.w) < 1e-10 * np.linalg.norm(a.v)
+    eng.release()
+    disc2, cfg2, prob2 = P.build_case("C1", steps=8)
+    _, dev_state, _ = P.run(cfg2, prob2)
+    for k in "vw":
+        assert np.array_equal(getattr(dev_state, k), got[k]), k

@@ -29,3 +29,22 @@ for _ in range(n):
 pr.disable()
 print(f"wall per step {(time.perf_counter() - t0) / n * 1e3:.3f} ms (under cProfile)")
 pstats.Stats(pr).sort_stats("tottime").print_stats(18)
+
+if os.environ.get("E2E") == "1":     # the public advance() loop with host arrays in / out
+    import numpy as np
+    from paper_2108_05110_b200.ensemble import EnsembleState
+    J = cfg.num_members
+    host = EnsembleState(v=np.asarray(prob.initial_v), w=np.asarray(prob.initial_w),
+                         q=np.zeros((J, disc.n_pres)), r=np.zeros((J, disc.n_pres)))
+    for _ in range(8):
+        new, _ = P.advance(host, cfg, disc, prob.forcing, prob.boundary)
+        host = EnsembleState(v=new.v, w=new.w, q=new.q, r=new.r, step=new.step, time=new.time)
+    pr = cProfile.Profile()
+    t0 = time.perf_counter()
+    pr.enable()
+    for _ in range(n):
+        new, _ = P.advance(host, cfg, disc, prob.forcing, prob.boundary)
+        host = EnsembleState(v=new.v, w=new.w, q=new.q, r=new.r, step=new.step, time=new.time)
+    pr.disable()
+    print(f"advance loop: wall per step {(time.perf_counter() - t0) / n * 1e3:.3f} ms (under cProfile)")
+    pstats.Stats(pr).sort_stats("tottime").print_stats(35)
