@@ -263,8 +263,26 @@ class FactorPlan:
     stats: dict
 
 
+_TRACE = __import__("os").environ.get("ENS_SETUP_TRACE") == "1"
+
+
+class _Tick:
+    """Phase timer of analyse() (ENS_SETUP_TRACE=1 prints one line per phase)."""
+
+    def __init__(self):
+        import time
+        self.clock, self.t = time.perf_counter, time.perf_counter()
+
+    def __call__(self, label):
+        if _TRACE:
+            now = self.clock()
+            print(f"  analyse: {label:28s} {now - self.t:7.3f} s", flush=True)
+            self.t = now
+
+
 def analyse(disc, leaf=LEAF_NODES, pw=PW):
     """Build the FactorPlan for a Discretization (constrained rows per disc)."""
+    tick = _Tick()
     vel = disc.velocity
     ns, nvel, npres = disc.n_scalar, disc.n_vel, disc.n_pres
     n_total = nvel + npres
@@ -274,8 +292,10 @@ def analyse(disc, leaf=LEAF_NODES, pw=PW):
     g.setdiag(0)
     g.eliminate_zeros()
     g.sort_indices()
+    tick("pattern")
     tnodes, kids, root = _nested_dissection(vel.dof_coords, g.indptr, g.indices, leaf)
     tnodes, kids, root = _amalgamate(tnodes, kids, root, AMALGAMATE)
+    tick("dissection + amalgamation")
     post = _postorder(kids, root)
     T = len(tnodes)
     rank = np.empty(T, dtype=np.int64)
@@ -305,6 +325,7 @@ def analyse(disc, leaf=LEAF_NODES, pw=PW):
     tnode_of_node = np.empty(ns, dtype=np.int64)
     tnode_of_node[cat] = post[grp]
 
+    tick("node numbering")
     # free dofs (reference numbering): velocity x = s, y = ns + s ; pressure nvel + p
     cons = np.zeros(n_total, dtype=bool)
     cons[disc.constrained_rows] = True
@@ -337,6 +358,7 @@ def analyse(disc, leaf=LEAF_NODES, pw=PW):
     pres_perm = np.empty(npres, dtype=np.int64)
     pres_perm[porder] = np.arange(npres)
 
+    tick("pressure placement")
     # internal dof id of every reference dof
     int_id = np.empty(n_total, dtype=np.int64)
     int_id[:ns] = 2 * node_perm
@@ -356,6 +378,7 @@ def analyse(disc, leaf=LEAF_NODES, pw=PW):
     elim = np.full(n_total, -1, dtype=np.int64)
     elim[order] = np.arange(nf)
 
+    tick("elimination order")
     # free saddle pattern in elimination order (symmetric structure): the stored entries of
     # [[A_s, 0, Bx^T], [0, A_s, By^T], [Bx, By, 0]] + its transpose (a B entry that is exactly
     # zero cancels out of that sum and is not in the pattern), between free dofs, as CSR with
@@ -374,6 +397,7 @@ def analyse(disc, leaf=LEAF_NODES, pw=PW):
                         np.concatenate([[0], np.cumsum(np.bincount(pkey // nf, minlength=nf))])), shape=(nf, nf))
     del pr_, pc_, keep_, pkey, a_r, a_c, b_r, b_c
 
+    tick("free pattern")
     # tree nodes -> pivot ranges in elimination order; drop empty tree nodes
     t_of_e = rank[dof_t[order]]                      # postorder rank per eliminated dof
     piv_start = np.searchsorted(t_of_e, np.arange(T), side="left")
@@ -402,6 +426,7 @@ def analyse(disc, leaf=LEAF_NODES, pw=PW):
         if fparent[f] >= 0:
             children[fparent[f]].append(f)
 
+    tick("tree bookkeeping")
     # symbolic factorisation: CB(f) = (later neighbours of pivots U children CBs) \ pivots, postorder
     # (children first); csrc/host_symbolic.cpp ens_host_symbolic_cb, the C++ restatement of
     #   cols = fp.indices[fp.indptr[s]:fp.indptr[e]];  cb[f] = unique(cols[cols >= e] U cb[c][cb[c] >= e])
@@ -420,6 +445,7 @@ def analyse(disc, leaf=LEAF_NODES, pw=PW):
     cbn = np.array([len(c) for c in cb], dtype=np.int64)
     m = k + cbn
 
+    tick("symbolic factorisation")
     # levels (height from leaves) -> processing order
     height = np.zeros(F, dtype=np.int64)
     for f in range(F):
@@ -462,6 +488,7 @@ def analyse(disc, leaf=LEAF_NODES, pw=PW):
         assert np.all(out >= 0), "symbolic lookup failed"
         return out
 
+    tick("levels + index lists")
     # child CB -> parent local map (all fronts in one lookup: positions in front order)
     pos_front = np.repeat(np.arange(F, dtype=np.int64), f_m)
     pos_local = np.arange(len(f_idx_elim), dtype=np.int64) - np.repeat(f_idx_off[:-1], f_m)
@@ -470,6 +497,7 @@ def analyse(disc, leaf=LEAF_NODES, pw=PW):
     f_cmap = lookup(f_parent[pos_front[is_cb]], f_idx_elim[is_cb]).astype(np.int32)
     cmap_off = np.concatenate([[0], np.cumsum(f_m - f_k)]).astype(np.int64)
 
+    tick("child maps")
     # original entries: A_s (both components) and B / -B^T, between free dofs
     nnz_s = As.nnz
     a_rows = np.repeat(np.arange(ns), np.diff(As.indptr))
@@ -508,6 +536,7 @@ def analyse(disc, leaf=LEAF_NODES, pw=PW):
     orig_src = src[o].astype(np.int32)
     orig_level_off = np.searchsorted(f_level[fr][o], np.arange(nlevels + 1)).astype(np.int64)
 
+    tick("original-entry scatter")
     plan = FactorPlan(
         node_perm=node_perm, pres_perm=pres_perm, nfront=F,
         f_m=f_m.astype(np.int32), f_k=f_k.astype(np.int32), f_off=f_off,
@@ -518,6 +547,7 @@ def analyse(disc, leaf=LEAF_NODES, pw=PW):
         schedule={}, stats={},
     )
     plan.schedule = build_schedule(plan, pw)
+    tick("schedule")
     # sweep flops: sum_{t<k} 2 (m - 1 - t)^2 = 2 (S(m - 1) - S(m - k - 1)), S(n) = n (n + 1) (2n + 1) / 6
     def sq_sum(n):
         n = n.astype(np.float64)
