@@ -86,16 +86,51 @@ def peaks():
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    """SM clocks + throttle reasons sampled during the timed region.
+
+    In-process NVML (nvidia_ml_py) from a sampling thread every few milliseconds, so that a timed
+    region of ~20 ms holds several samples; `nvidia-smi -lms` in a subprocess when NVML cannot be
+    loaded (its 100 ms period then only brackets the region)."""
 
     Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
          "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    NAMES = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
 
-    def __init__(self, index):
+    def __init__(self, index, period_s=0.004):
         self.index = index
+        self.period = period_s
         self.proc = None
+        self.thread = None
+        self.samples = []          # (sm MHz, reasons bitmask)
+        self.max_mhz = None
+        self._stop = False
+        self.kind = os.environ.get("BENCH_SAMPLER", "nvml")
+
+    def _nvml_loop(self, nv, h):
+        while not self._stop:
+            try:
+                self.samples.append((float(nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)),
+                                     int(nv.nvmlDeviceGetCurrentClocksEventReasons(h))))
+            except Exception:
+                pass
+            time.sleep(self.period)
 
     def start(self):
+        if self.kind == "nvml":
+            try:
+                import threading
+                import pynvml as nv
+                nv.nvmlInit()
+                vis = os.environ.get("CUDA_VISIBLE_DEVICES")
+                idx = int(vis.split(",")[self.index]) if vis and vis.split(",")[self.index].isdigit() else self.index
+                h = nv.nvmlDeviceGetHandleByIndex(idx)
+                self.max_mhz = float(nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM))
+                self._nv = nv
+                self.thread = threading.Thread(target=self._nvml_loop, args=(nv, h), daemon=True)
+                self.thread.start()
+                return
+            except Exception:
+                self.thread = None
         try:
             self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
                                           "--format=csv,noheader,nounits", "-lms", "100"],
@@ -103,14 +138,30 @@ class ClockSampler:
         except Exception:
             self.proc = None
 
+    def ready(self):
+        """True once the sampler has delivered (nvml) or had time to deliver (nvidia-smi) a first sample."""
+        return len(self.samples) > 0 if self.thread is not None else False
+
     def stop(self):
+        if self.thread is not None:
+            time.sleep(3 * self.period)
+            self._stop = True
+            self.thread.join(timeout=2)
+            nv = self._nv
+            bits = {"hw_slowdown": nv.nvmlClocksEventReasonHwSlowdown,
+                    "hw_thermal_slowdown": nv.nvmlClocksEventReasonHwThermalSlowdown,
+                    "sw_thermal_slowdown": nv.nvmlClocksEventReasonSwThermalSlowdown,
+                    "sw_power_cap": nv.nvmlClocksEventReasonSwPowerCap}
+            reasons = sorted(n for n, b in bits.items() if any(r & b for _, r in self.samples))
+            sm = [c for c, _ in self.samples]
+            return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": self.max_mhz,
+                    "reasons": reasons, "samples": len(sm), "sampler": "nvml in-process, every 4 ms"}
         if self.proc is None:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
         time.sleep(0.25)
         self.proc.terminate()
         out, _ = self.proc.communicate(timeout=5)
         sm, mx, reasons = [], [], set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         for line in out.strip().splitlines():
             parts = [p.strip() for p in line.split(",")]
             if len(parts) < 6:
@@ -120,11 +171,11 @@ class ClockSampler:
                 mx.append(float(parts[1]))
             except ValueError:
                 continue
-            for n, v in zip(names, parts[2:6]):
+            for n, v in zip(self.NAMES, parts[2:6]):
                 if v.lower().startswith("active"):
                     reasons.add(n)
         return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": sorted(reasons), "samples": len(sm)}
+                "reasons": sorted(reasons), "samples": len(sm), "sampler": "nvidia-smi -lms 100"}
 
 
 def cpu_baseline(disc, cfg, prob, steps=1):
@@ -216,7 +267,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)
-    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=5)
@@ -311,7 +362,21 @@ def main():
         dist.barrier()
     sampler = ClockSampler(local)
     sampler.start()
-    time.sleep(0.3)
+    # the sampler needs a moment to deliver its first sample: the GPU keeps stepping meanwhile (untimed,
+    # announced like the timed steps), so the timed region starts on a busy GPU, not after an idle gap
+    t_wait = time.perf_counter()
+    busy = os.environ.get("BENCH_IDLE", "busy") == "busy"
+    extra_warm = 0
+    while time.perf_counter() - t_wait < 0.3 and not (busy and sampler.ready() and time.perf_counter() - t_wait > 0.02):
+        if busy:
+            t += cfg.dt
+            extra_warm += 1
+            if ahead:
+                eng.step(t, prob.forcing, prob.boundary, then=(t + cfg.dt, prob.forcing, prob.boundary))
+            else:
+                eng.step(t, prob.forcing, prob.boundary)
+        else:
+            time.sleep(0.01)
     s = eng.stream
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     torch.cuda.synchronize()
@@ -495,7 +560,10 @@ def main():
                        "case": case, "members_total": J_total, "members_per_pass": Jc, "n_total_dofs": int(eng.ntot),
                        "l2": "per-step working set (2 x %.2f GB fronts) exceeds the 126 MB L2" %
                              (plan.front_storage * 8 / 1e9),
-                       "rtol": eng.rtol, "parallelism": f"members sharded dp{world}"},
+                       "rtol": eng.rtol, "parallelism": f"members sharded dp{world}",
+                       "warmup_extra_steps": extra_warm,
+                       "warmup_note": "untimed steps run while the clock sampler delivers its first sample "
+                                      "(the timed region starts on a busy GPU), on top of --warmup"},
             "wall_s": wall, "setup": setup,
             "krylov_iters_per_step": float(np.mean(iters)) if iters else None,
             "preconditioner": {"policy": eng.refactor, "factorizations_in_timed_steps": n_factor,
