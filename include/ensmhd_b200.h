@@ -156,6 +156,10 @@ int  ens_lincomb(ens_ctx* ctx, void* stream, double a, const double* x, double b
 /* Member sums over the J local columns: sum_v[r] = sum_j Xv[r][j] (r < n_vel), same for w. */
 int  ens_member_sums(ens_ctx* ctx, void* stream, const double* x, double* sums);
 
+/* means[2 * n_vel] = sums * inv_members: the ensemble means <v>, <w> (ensemble.py:216-224) from the
+ * member sums -- after the allreduce SUM when members are sharded (inv_members = 1 / J_total). */
+int  ens_means(ens_ctx* ctx, void* stream, const double* sums, double inv_members, double* means);
+
 /* RHS velocity rows (stepper.py:235-247): for both sub-steps
  *   rhs_V = (M/dt - ls_j K) v_j - lc_j K w_j + load_V      (same = v, other = w)
  *   rhs_W = (M/dt - ls_j K) w_j - lc_j K v_j + load_W

@@ -55,7 +55,7 @@ class DataDesc(C.Structure):
 SYMBOLS = [
     "ens_abi_version", "ens_last_error", "ens_kernel_launches", "ens_create", "ens_set_pivoting",
     "ens_destroy", "ens_workspace_bytes", "ens_stream_split_launches",
-    "ens_lincomb", "ens_member_sums", "ens_rhs", "ens_member_pass", "ens_rhs_fused", "ens_apply_bc", "ens_assemble", "ens_factor",
+    "ens_lincomb", "ens_member_sums", "ens_means", "ens_rhs", "ens_member_pass", "ens_rhs_fused", "ens_apply_bc", "ens_assemble", "ens_factor",
     "ens_solve", "ens_solve_begin", "ens_solve_finish", "ens_spmm", "ens_precond_apply", "ens_epilogue", "ens_diagnostics", "ens_mean_error",
     "ens_layout_import", "ens_layout_export",
 ]
@@ -83,6 +83,7 @@ def load(path: str = LIB_PATH):
     lib.ens_stream_split_launches.argtypes = [P]
     lib.ens_stream_split_launches.restype = C.c_int
     lib.ens_member_sums.argtypes = [P, P, P, P]
+    lib.ens_means.argtypes = [P, P, P, F64, P]
     lib.ens_mean_error.argtypes = [P, P, P, C.POINTER(DataDesc), P]
     lib.ens_lincomb.argtypes = [P, P, F64, P, F64, P]
     lib.ens_rhs.argtypes = [P, P, P, P, F64, C.POINTER(DataDesc), P]

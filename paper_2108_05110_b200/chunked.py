@@ -218,7 +218,7 @@ class ChunkedEngine(Engine):
             if c:
                 self.sums.add_(self.sums_part)
         XC.allreduce_member_sums(self.sums, self.comm)
-        torch.mul(self.sums, 1.0 / self.J_total, out=self.means)
+        N.check(lib.ens_means(ctx, s, _dptr(self.sums), 1.0 / self.J_total, _dptr(self.means)), "ens_means")
         self.means_valid = True
 
     def _element_pass(self, X, c, loads):

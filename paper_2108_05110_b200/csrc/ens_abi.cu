@@ -169,6 +169,11 @@ int ens_member_sums(ens_ctx* c, void* stream, const double* x, double* sums) {
     return launch_member_sums(c, (cudaStream_t)stream, x, sums);
 }
 
+int ens_means(ens_ctx* c, void* stream, const double* sums, double inv_members, double* means) {
+    if (!c || !sums || !means || !(inv_members > 0.0)) return ENS_EINVAL;
+    return launch_means(c, (cudaStream_t)stream, sums, inv_members, means);
+}
+
 int ens_rhs(ens_ctx* c, void* stream, const double* x, const double* member_coef, double inv_dt,
             const ens_data_desc* loads, double* rhs) {
     if (!c || !x || !member_coef || !rhs) return ENS_EINVAL;

@@ -129,6 +129,7 @@ int launch_epilogue(ens_ctx* c, cudaStream_t s, const double* x, double* p_out);
 int launch_diagnostics(ens_ctx* c, cudaStream_t s, const double* x, const double* means, double* out);
 int launch_mean_error(ens_ctx* c, cudaStream_t s, const double* means, const ens_data_desc* exact, double* out);
 int launch_copy_cons(ens_ctx* c, cudaStream_t s, const double* src, double* dst);
+int launch_means(ens_ctx* c, cudaStream_t s, const double* sums, double inv_members, double* means);
 // reference-order (J, n) blocks <-> internal member-minor blocks (import: ref -> x)
 int launch_layout(ens_ctx* c, cudaStream_t s, bool import, double* ref, int64_t ld, int64_t ref_ms, int64_t n,
                   const int64_t* row, double* x, int64_t x_ms, int nsys);

@@ -162,6 +162,21 @@ int launch_member_sums(ens_ctx* c, cudaStream_t s, const double* x, double* sums
     return ENS_OK;
 }
 
+// means[r] = sums[r] * inv_members (the ensemble means of ensemble.py:216-224 from the -- in sharded runs
+// all-reduced -- member sums); the same IEEE product as the host expression sums * (1 / J)
+__global__ void __launch_bounds__(256) k_means(const double* __restrict__ sums, double inv_members,
+                                               double* __restrict__ means, int64_t n) {
+    const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (r < n) means[r] = sums[r] * inv_members;
+}
+
+int launch_means(ens_ctx* c, cudaStream_t s, const double* sums, double inv_members, double* means) {
+    const int64_t n = 2LL * c->n_vel;
+    k_means<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(sums, inv_members, means, n);
+    ENS_CKL();
+    return ENS_OK;
+}
+
 // ---------------------------------------------------------------------------
 // right-hand sides, velocity rows (stepper.py:235-247) for both sub-steps
 // ---------------------------------------------------------------------------

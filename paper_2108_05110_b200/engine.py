@@ -933,7 +933,7 @@ class Engine:
             N.check(lib.ens_member_sums(ctx, s, _dptr(X), _dptr(self.sums)), "ens_member_sums")
 
         def rhs():
-            torch.mul(self.sums, 1.0 / self.J_total, out=self.means)
+            N.check(lib.ens_means(ctx, s, _dptr(self.sums), 1.0 / self.J_total, _dptr(self.means)), "ens_means")
             if lo is not None:
                 lo[2].copy_(lo[1], non_blocking=True)
             self._rhs_and_member_pass(X, C.byref(lo[3]) if lo is not None else None)
@@ -1165,7 +1165,7 @@ class Engine:
         X = self.X[self.cur]
         N.check(lib.ens_member_sums(ctx, s, _dptr(X), _dptr(self.sums)), "ens_member_sums")
         XC.allreduce_member_sums(self.sums, self.comm)
-        torch.mul(self.sums, 1.0 / self.J_total, out=self.means)
+        N.check(lib.ens_means(ctx, s, _dptr(self.sums), 1.0 / self.J_total, _dptr(self.means)), "ens_means")
         self.means_valid = True
 
     def _step(self, t_next, forcing, boundary):
