@@ -574,7 +574,7 @@ class Engine:
             # uploaded and become the resident velocities like any caller's arrays, but nothing has to
             # be compared, so no host synchronisation: the step's graphs queue up behind the copies.
             self.n_own_uploads += 1
-            with self.on_stream():
+            with torch.cuda.stream(s):      # (host memory in: nothing of the caller's stream to order against)
                 g["d_vel"][0].copy_(own["v"], non_blocking=True)
                 g["d_vel"][1].copy_(own["w"], non_blocking=True)
                 N.check(self.lib.ens_layout_import(self.ctx, self.sptr, _dptr(g["d_vel"]), nv, self.J * nv, nv,
@@ -655,7 +655,8 @@ class Engine:
         tens = h[1]
         for a, t in ((v, tens["v"]), (w, tens["w"])):
             if not (isinstance(a, np.ndarray) and not a.flags.writeable and a.dtype == np.float64
-                    and a.shape == tuple(t.shape) and a.flags.c_contiguous and a.ctypes.data == t.data_ptr()):
+                    and a.shape == tuple(t.shape) and a.flags.c_contiguous
+                    and a.__array_interface__["data"][0] == t.data_ptr()):
                 return None
         return tens
 
