@@ -367,8 +367,16 @@ def main():
     t_wait = time.perf_counter()
     busy = os.environ.get("BENCH_IDLE", "busy") == "busy"
     extra_warm = 0
-    while time.perf_counter() - t_wait < 0.3 and not (busy and sampler.ready() and time.perf_counter() - t_wait > 0.02):
-        if busy:
+
+    def keep_waiting():
+        if comm is not None:
+            # every rank must run the same number of steps (a step holds collectives): a fixed count
+            return extra_warm < 2
+        return time.perf_counter() - t_wait < 0.3 and not (busy and sampler.ready() and
+                                                           time.perf_counter() - t_wait > 0.02)
+
+    while keep_waiting():
+        if busy or comm is not None:
             t += cfg.dt
             extra_warm += 1
             if ahead:
