@@ -563,12 +563,14 @@ class Engine:
         the reference's step reads only v and w (`stepper.py:360-394`); the
         pressures enter here only as part of the initial iterate.
         """
-        self._spec = None
+        spec, self._spec = self._spec, None
         g = self._staging()
         s = self.stream
         nv = self.nvel
         own = self._own_arrays(v, w)
         if own is not None:
+            if spec is not None:
+                s.synchronize()     # (an announced step's graph is still enqueued: as for any dropped announcement)
             # the caller passes back, unmodified (write-protected views of our pinned buffers), the very
             # arrays this buffer set was downloaded into: same values by construction.  They are
             # uploaded and become the resident velocities like any caller's arrays, but nothing has to

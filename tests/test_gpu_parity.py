@@ -508,3 +508,31 @@ def test_advance_host_arrays_prefetched_download_bitwise():
     _, dev_state, _ = P.run(cfg2, prob2)
     for k in "vw":
         assert np.array_equal(getattr(dev_state, k), got[k]), k
+
+
+def test_advance_host_arrays_after_announced_step_bitwise():
+    """A loop that announced its next step (its pre-solve graph is enqueued) and then hands the state's
+    host arrays to advance(): the dropped announcement is redone; the result is bitwise that of plain
+    steps."""
+    outs = []
+    for mode in ("announced", "plain"):
+        disc, cfg, prob = P.build_case("C1", steps=8)
+        eng = P.stepper.get_engine(disc, cfg)
+        eng.load_state(prob.initial_v, prob.initial_w, None, None)
+        t = 0.0
+        for _ in range(6):
+            t += cfg.dt
+            if mode == "announced":
+                eng.step(t, prob.forcing, prob.boundary, then=(t + cfg.dt, prob.forcing, prob.boundary))
+            else:
+                eng.step(t, prob.forcing, prob.boundary)
+        st = EnsembleState(step=6, time=t, device=eng.state_handle())
+        host = EnsembleState(v=st.v, w=st.w, q=st.q, r=st.r, step=6, time=t)
+        if mode == "announced":
+            assert eng._spec is not None
+        new, _ = P.advance(host, cfg, disc, prob.forcing, prob.boundary)
+        assert eng.n_own_uploads == 1
+        outs.append({k: np.array(getattr(new, k)) for k in "vwqr"})
+        eng.release()
+    for k in "vwqr":
+        assert np.array_equal(outs[0][k], outs[1][k]), k
