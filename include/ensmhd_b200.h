@@ -240,6 +240,10 @@ int  ens_mean_error(ens_ctx* ctx, void* stream, const double* means, const ens_d
  * import: x[s][row[c]][j] = ref[s][j][c];  export: ref[s][j][c] = x[s][row[c]][j]. */
 int  ens_layout_import(ens_ctx* ctx, void* stream, const double* ref, int64_t ld, int64_t ref_stride, int64_t n,
                        const int64_t* row, double* x, int64_t x_stride, int32_t nsys);
+/* The upload half of a host-array step in one call: the (J, n) host arrays v, w (pinned: asynchronous
+ * DMA) -> staging[2][J][n] on the device -> ens_layout_import into x (two systems, stride x_stride). */
+int  ens_state_upload(ens_ctx* ctx, void* stream, const double* host_v, const double* host_w, int64_t n,
+                      double* staging, const int64_t* row, double* x, int64_t x_stride);
 int  ens_layout_export(ens_ctx* ctx, void* stream, const double* x, int64_t x_stride, int64_t n, const int64_t* row,
                        double* ref, int64_t ld, int64_t ref_stride, int32_t nsys);
 

@@ -57,7 +57,7 @@ SYMBOLS = [
     "ens_destroy", "ens_workspace_bytes", "ens_stream_split_launches",
     "ens_lincomb", "ens_member_sums", "ens_means", "ens_rhs", "ens_member_pass", "ens_rhs_fused", "ens_apply_bc", "ens_assemble", "ens_factor",
     "ens_solve", "ens_solve_begin", "ens_solve_finish", "ens_spmm", "ens_precond_apply", "ens_epilogue", "ens_diagnostics", "ens_mean_error",
-    "ens_layout_import", "ens_layout_export",
+    "ens_layout_import", "ens_layout_export", "ens_state_upload",
 ]
 
 _lib = None
@@ -101,6 +101,7 @@ def load(path: str = LIB_PATH):
     lib.ens_diagnostics.argtypes = [P, P, P, P, P]
     lib.ens_layout_import.argtypes = [P, P, P, I64, I64, I64, P, P, I64, I32]
     lib.ens_layout_export.argtypes = [P, P, P, I64, I64, P, P, I64, I64, I32]
+    lib.ens_state_upload.argtypes = [P, P, P, P, I64, P, P, P, I64]
     for name in SYMBOLS:
         if name not in ("ens_abi_version", "ens_last_error", "ens_destroy", "ens_kernel_launches"):
             getattr(lib, name).restype = C.c_int

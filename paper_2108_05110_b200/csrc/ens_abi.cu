@@ -263,6 +263,16 @@ int ens_layout_import(ens_ctx* c, void* stream, const double* ref, int64_t ld, i
                          nsys);
 }
 
+int ens_state_upload(ens_ctx* c, void* stream, const double* host_v, const double* host_w, int64_t n,
+                     double* staging, const int64_t* row, double* x, int64_t x_stride) {
+    if (!c || !host_v || !host_w || !staging || !row || !x || n < 0) return ENS_EINVAL;
+    cudaStream_t s = (cudaStream_t)stream;
+    const size_t bytes = sizeof(double) * (size_t)c->J * (size_t)n;
+    ENS_CK(cudaMemcpyAsync(staging, host_v, bytes, cudaMemcpyHostToDevice, s));
+    ENS_CK(cudaMemcpyAsync(staging + (int64_t)c->J * n, host_w, bytes, cudaMemcpyHostToDevice, s));
+    return launch_layout(c, s, true, staging, n, (int64_t)c->J * n, n, row, x, x_stride, 2);
+}
+
 int ens_layout_export(ens_ctx* c, void* stream, const double* x, int64_t x_stride, int64_t n, const int64_t* row,
                       double* ref, int64_t ld, int64_t ref_stride, int32_t nsys) {
     if (!c || !ref || !row || !x || n < 0 || ld < n || nsys < 1) return ENS_EINVAL;

@@ -272,8 +272,10 @@ class DeviceState:
                 (tens, ev), self._pending = self._pending, None
             else:
                 tens, ev = self.engine._enqueue_fetch(self.buf)   # all four fields, one wait
+            fields = {k: t.numpy() for k, t in tens.items()}      # (views: built while the copies are in flight)
+            for a in fields.values():
+                a.setflags(write=False)
             ev.synchronize()
-            fields = {k: t.numpy() for k, t in tens.items()}
             if self.engine is not None:
                 # (load_state recognises these arrays if the caller passes them straight back in)
                 self.engine._handed = ((self.buf, self.gen), tens)
@@ -576,12 +578,10 @@ class Engine:
             # uploaded and become the resident velocities like any caller's arrays, but nothing has to
             # be compared, so no host synchronisation: the step's graphs queue up behind the copies.
             self.n_own_uploads += 1
-            with torch.cuda.stream(s):      # (host memory in: nothing of the caller's stream to order against)
-                g["d_vel"][0].copy_(own["v"], non_blocking=True)
-                g["d_vel"][1].copy_(own["w"], non_blocking=True)
-                N.check(self.lib.ens_layout_import(self.ctx, self.sptr, _dptr(g["d_vel"]), nv, self.J * nv, nv,
-                                                   _dptr(g["row_v"]), _dptr(self.X[self.cur]), self.ntot * self.J,
-                                                   2), "ens_layout_import")
+            # (one C call: two asynchronous copies from the pinned buffers + the layout kernel, on the engine stream)
+            N.check(self.lib.ens_state_upload(self.ctx, self.sptr, own["v"].data_ptr(), own["w"].data_ptr(), nv,
+                                              _dptr(g["d_vel"]), _dptr(g["row_v"]), _dptr(self.X[self.cur]),
+                                              self.ntot * self.J), "ens_state_upload")
             return
         has_p = q is not None and np.asarray(q).size > 0
         with torch.cuda.stream(s):
