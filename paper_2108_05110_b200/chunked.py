@@ -39,7 +39,7 @@ def per_column_bytes(hm, restart=2):
     n_idx = int(hm.plan.f_idx_off[-1])
     state = 8 * (2 * 2 * ntot + 2 * 2 * npres)
     work = 8 * (2 * ntot * (1 + 2 * restart + 3) + 2 * nt * 12 + 2 * n_idx)
-    staging = 8 * (2 * hm.nvel + 2 * npres + 2 * ntot + hm.nvel + npres)
+    staging = 8 * (2 * hm.nvel + 2 * npres + 2 * ntot)     # reference-layout blocks + the import block
     return state, work + staging
 
 
@@ -120,13 +120,17 @@ class ChunkedEngine(Engine):
             sl = slice(c * Jc, (c + 1) * Jc)
             with torch.cuda.stream(s):
                 Xs = g["x_in"]
+                nt, npr = self.ntot, self.npres
                 for m, a in enumerate((v, w)):
                     self._copy_members(g["d_vel"][m], member_rows(a, c * Jc, Jc))   # lazy stays lazy
-                    torch.index_select(g["d_vel"][m].t(), 0, g["ref_of_int_v"], out=Xs[m, :nv])
+                N.check(self.lib.ens_layout_import(self.ctx, self.sptr, _dptr(g["d_vel"]), nv, Jc * nv, nv,
+                                                   _dptr(g["row_v"]), _dptr(Xs), nt * Jc, 2), "ens_layout_import")
                 if has_p:
                     for m, a in enumerate((q, r)):
                         g["d_pres"][m].copy_(self._host_tensor(np.asarray(a, float)[sl]))
-                        torch.index_select(g["d_pres"][m].t(), 0, g["ref_of_int_p"], out=Xs[m, nv:])
+                    N.check(self.lib.ens_layout_import(self.ctx, self.sptr, _dptr(g["d_pres"]), npr, Jc * npr, npr,
+                                                       _dptr(g["row_p"]), _dptr(Xs[0, nv:]), nt * Jc, 2),
+                            "ens_layout_import")
                 else:
                     Xs[:, nv:] = 0.0
                 self.Xc[cur][c].copy_(Xs)
@@ -144,12 +148,13 @@ class ChunkedEngine(Engine):
         for c in range(self.nchunk):
             sl = slice(c * Jc, (c + 1) * Jc)
             with torch.cuda.stream(s):
-                for m, name in ((0, "v"), (1, "w")):
-                    torch.index_select(self.Xc[buf][c][m, :nv], 0, g["int_of_ref_v"], out=g["t_vel"])
-                    g["d_vel"][m].copy_(g["t_vel"].t())
-                for m, name in ((0, "q"), (1, "r")):
-                    torch.index_select(self.Pqc[buf][c][m], 0, g["int_of_ref_p"], out=g["t_pres"])
-                    g["d_pres"][m].copy_(g["t_pres"].t())
+                nt = self.ntot
+                N.check(self.lib.ens_layout_export(self.ctx, self.sptr, _dptr(self.Xc[buf][c]), nt * Jc, nv,
+                                                   _dptr(g["row_v"]), _dptr(g["d_vel"]), nv, Jc * nv, 2),
+                        "ens_layout_export")
+                N.check(self.lib.ens_layout_export(self.ctx, self.sptr, _dptr(self.Pqc[buf][c]), npr * Jc, npr,
+                                                   _dptr(g["row_p"]), _dptr(g["d_pres"]), npr, Jc * npr, 2),
+                        "ens_layout_export")
             s.synchronize()
             out["v"][sl], out["w"][sl] = g["d_vel"][0].cpu().numpy(), g["d_vel"][1].cpu().numpy()
             out["q"][sl], out["r"][sl] = g["d_pres"][0].cpu().numpy(), g["d_pres"][1].cpu().numpy()

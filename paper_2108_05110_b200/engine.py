@@ -514,15 +514,9 @@ class Engine:
                 d_vel=torch.empty(2, J, self.nvel, dtype=torch.float64, device=d),
                 d_pres=torch.empty(2, J, self.npres, dtype=torch.float64, device=d),
                 x_in=torch.empty(2, self.ntot, J, dtype=torch.float64, device=d),
-                t_vel=torch.empty(self.nvel, J, dtype=torch.float64, device=d),
-                t_pres=torch.empty(self.npres, J, dtype=torch.float64, device=d),
-                ref_of_int_v=torch.as_tensor(hm.ref_of_int[:self.nvel]).to(d),
-                ref_of_int_p=torch.as_tensor(hm.ref_of_int[self.nvel:] - self.nvel).to(d),
-                int_of_ref_v=torch.as_tensor(hm.int_id[:self.nvel]).to(d),
-                int_of_ref_p=torch.as_tensor(hm.int_id[self.nvel:] - self.nvel).to(d))
-            # row maps of the layout kernels (ens_layout_import / _export): internal row of each reference dof
-            self._stg["row_v"] = self._stg["int_of_ref_v"].to(torch.int64).contiguous()
-            self._stg["row_p"] = self._stg["int_of_ref_p"].to(torch.int64).contiguous()
+                # row maps of the layout kernels (ens_layout_import / _export): internal row of each reference dof
+                row_v=torch.as_tensor(hm.int_id[:self.nvel].astype(np.int64)).to(d),
+                row_p=torch.as_tensor((hm.int_id[self.nvel:] - self.nvel).astype(np.int64)).to(d))
         return self._stg
 
     @staticmethod
